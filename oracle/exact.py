@@ -1,0 +1,116 @@
+"""Exact-rational (``fractions.Fraction``) twin of ONE explicit step -- TEST
+INFRASTRUCTURE ONLY (pins the C oracle's sweep; pure-Python loops, tiny
+meshes only).
+
+Written from the face-sum definition rather than the oracle's per-axis
+difference form, so that a dropped term, a wrong sign or a wrong neighbour in
+either is caught:
+
+  Eq. 5 + forward Euler, Eq. 3:
+    I' = I + dt*( (I0 - I)*beta  -  v_b * (1/V) * sum_f A_f (s_d . n_f) I_up(f) )
+  upwind: I_up = value in CELL1 (this cell) if s.n > 0, else the
+    value in CELL2 (neighbour or ghost across f)  -- strict ">".
+  ghosts (Eq. 6; reading #11 for diffuse walls).
+
+Only LINEAR-mode channel tables are supported (I0 is then rational).
+"""
+from __future__ import annotations
+
+from fractions import Fraction as Fr
+
+import numpy as np
+
+
+def _reflect_map(s, axis):
+    nd = s.shape[0]
+    r = []
+    for d in range(nd):
+        t = s[d].copy()
+        t[axis] = -t[axis]
+        hit = [e for e in range(nd) if np.array_equal(s[e], t)]
+        if not hit:
+            raise ValueError("reflection not closed")
+        r.append(hit[0])
+    return r
+
+
+def exact_step_sweep(problem, I, I0c, betac):
+    """One sweep step in exact rationals; returns an object array of Fractions [nc, nd, nb]."""
+    m, dr, bd = problem.mesh, problem.dirs, problem.bands
+    assert bd.mode == 0, "exact twin supports LINEAR channels only"
+    nx, ny, nz = m.nx, m.ny, m.nz
+    nd, nb = dr.nd, bd.nb
+    dims = 3 if m.dim == 3 else 2
+    D = [Fr(m.dx), Fr(m.dy), Fr(m.dz)]
+    n = [nx, ny, nz]
+    vol = D[0] * D[1] * D[2]
+    s = [[Fr(float(x)) for x in row] for row in dr.s]
+    w = [Fr(float(x)) for x in dr.w]
+    v = [Fr(float(x)) for x in bd.v]
+    dt = Fr(problem.dt)
+    If = np.vectorize(Fr, otypes=[object])(np.asarray(I, dtype=np.float64))
+    I0f = np.vectorize(Fr, otypes=[object])(np.asarray(I0c, dtype=np.float64))
+    bf = np.vectorize(Fr, otypes=[object])(np.asarray(betac, dtype=np.float64))
+    refl = {a: _reflect_map(dr.s, a) for a in range(dims)}
+
+    def cidx(x, y, z):
+        return x + nx * (y + ny * z)
+
+    def I0_lin(b, T):
+        return Fr(float(bd.I_ref[b])) + Fr(float(bd.slope[b])) * (Fr(float(T)) - Fr(float(bd.T_ref)))
+
+    def ghost(region, ijk, d, b):
+        a = region // 2
+        bc = problem.bcs[region]
+        c = cidx(*ijk)
+        if bc.kind == 0:  # isothermal: I0_b(T_wall) at the face
+            if bc.T_wall is None:
+                T = bc.T_uniform
+            else:
+                f = [ijk[1] + ny * ijk[2], ijk[0] + nx * ijk[2], ijk[0] + nx * ijk[1]][a]
+                T = bc.T_wall[f]
+            return I0_lin(b, T)
+        if bc.kind == 1:  # specular
+            return If[c, refl[a][d], b]
+        sg = 1 if region & 1 else -1  # diffuse: outgoing re-emitted isotropically
+        num = sum((w[e] * abs(s[e][a]) * If[c, e, b] for e in range(nd) if sg * s[e][a] > 0), Fr(0))
+        den = sum((w[e] * abs(s[e][a]) for e in range(nd) if sg * s[e][a] < 0), Fr(0))
+        return num / den
+
+    out = np.empty((nx * ny * nz, nd, nb), dtype=object)
+    for z in range(nz):
+        for y in range(ny):
+            for x in range(nx):
+                ijk = (x, y, z)
+                c = cidx(x, y, z)
+                for d in range(nd):
+                    for b in range(nb):
+                        face_sum = Fr(0)
+                        for a in range(dims):
+                            area = vol / D[a]
+                            for side in (-1, +1):  # face on the -a / +a side of the cell
+                                sn = s[d][a] * side  # s . n with n = side * e_a
+                                if sn > 0:
+                                    up = If[c, d, b]
+                                else:
+                                    nb_ijk = list(ijk)
+                                    nb_ijk[a] += side
+                                    if 0 <= nb_ijk[a] < n[a]:
+                                        up = If[cidx(*nb_ijk), d, b]
+                                    else:
+                                        up = ghost(2 * a + (1 if side > 0 else 0), ijk, d, b)
+                                face_sum += area * sn * up
+                        out[c, d, b] = If[c, d, b] + dt * ((I0f[c, b] - If[c, d, b]) * bf[c, b]
+                                                            - v[b] * face_sum / vol)
+    return out
+
+
+def ulp_error(approx, exact):
+    """max |approx - exact| in units of ulp(exact) (exact: Fraction array)."""
+    worst = 0.0
+    for a, e in zip(np.asarray(approx).reshape(-1), exact.reshape(-1)):
+        ef = float(e)
+        u = np.spacing(abs(ef)) if ef != 0 else np.finfo(float).tiny
+        err = abs(Fr(float(a)) - e)
+        worst = max(worst, float(err / Fr(u)))
+    return worst

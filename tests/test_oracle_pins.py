@@ -1,0 +1,508 @@
+"""Pins for the CPU oracle (-m "not gpu"): each checks the oracle against
+something other than itself -- the paper's printed numbers, closed forms,
+high-precision references, exact-rational brute force, invariants -- chosen
+so a plausible mistake (dropped term, wrong sign/index/neighbour, transposed
+operand) fails at least one of them.  Citations: P:L = PAPER.md lines,
+S:L = SPEC.md lines, reading #n = DESIGN.md."""
+import json
+import math
+import os
+
+import mpmath
+import numpy as np
+import pytest
+
+import bte_inputs as bi
+import oracle
+from oracle import exact
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_counts.json")))
+HBAR, KB = bi.HBAR, bi.KB
+
+
+# ----------------------------------------------------------------- paper counts
+
+def test_paper_counts():
+    g = GOLD
+    p = bi.config2(n=g["demo_cells"]["nx"])
+    assert p.mesh.ncells == g["demo_cells"]["value"]
+    b55 = bi.silicon_bands(g["channels_from_40_bands"]["n_freq"])
+    assert b55.nb == g["channels_from_40_bands"]["value"]
+    assert b55.polarization.count("LA") == g["channels_from_40_bands"]["longitudinal"]
+    assert b55.polarization.count("TA") == g["channels_from_40_bands"]["transverse"]
+    d20 = bi.directions_inplane(g["demo_dof_per_cell"]["ndirs"])
+    assert d20.nd * b55.nb == g["demo_dof_per_cell"]["value"]
+    tot = p.mesh.ncells * d20.nd * b55.nb
+    assert abs(tot / g["demo_dof_total_approx"]["value"] - 1) < g["demo_dof_total_approx"]["rel_tol"]
+    d400 = bi.directions_control_angle(20, 20)
+    assert d400.nd == g["dirs_3d"]["value"]
+    assert d400.nd * b55.nb == g["pdes_3d"]["value"]
+    # 40 stored channels at n_freq = 29 (reading #5)
+    assert bi.silicon_bands(29).nb == 40
+
+
+def test_grid_face_counts():
+    g = GOLD["grid_4x4_faces"]
+    nx = ny = 4
+    interior = (nx - 1) * ny + nx * (ny - 1)
+    m = bi.Mesh(2, nx, ny, 1, 1.0, 1.0, 1.0)
+    boundary = sum(m.n_faces(r) for r in range(4))
+    assert (interior, boundary) == (g["interior"], g["boundary"])
+
+
+def test_hotspot_profile():
+    g = GOLD["hotspot"]
+    n = 120
+    dx = g["domain"] / n
+    T = bi.hotspot_profile(n, dx, g["T_cold"], g["T_peak"], g["width_1_over_e2"])
+    assert np.array_equal(T, T[::-1])  # exactly mirror-symmetric (reading #13)
+    assert T.max() < g["T_peak"] and T.min() >= g["T_cold"]
+    # 1/e^2 distance: at x = w the excess is exp(-2)
+    x = bi.face_centre_offsets(n, dx)
+    i = np.argmin(np.abs(np.abs(x) - g["width_1_over_e2"]))
+    assert abs((T[i] - 300) / 50 - math.exp(-2 * x[i] ** 2 / g["width_1_over_e2"] ** 2)) < 1e-15
+
+
+# ----------------------------------------------------------------- quadrature
+
+def test_gauss_legendre_vs_numpy():
+    x, w = oracle.gauss_legendre(16)
+    xr, wr = np.polynomial.legendre.leggauss(16)
+    assert np.max(np.abs(x - xr)) < 1e-15 and np.max(np.abs(w - wr)) < 1e-14
+    # exact for polynomials up to degree 31
+    for k in range(0, 32):
+        exact_int = 0.0 if k % 2 else 2.0 / (k + 1)
+        assert abs(np.sum(w * x ** k) - exact_int) < 1e-14
+
+
+def test_direction_sets_closure_and_reflection():
+    for d in (bi.directions_inplane(16), bi.directions_inplane(8), bi.directions_control_angle(20, 20),
+              bi.directions_control_angle(4, 8)):
+        W = d.w.sum()
+        expect = 2 * math.pi if np.all(d.s[:, 2] == 0) else 4 * math.pi
+        assert abs(W - expect) < 1e-13
+        assert np.max(np.abs((d.w[:, None] * d.s).sum(0))) < 1e-14
+        assert np.allclose(np.linalg.norm(d.s, axis=1), 1.0, atol=1e-15)
+        o = oracle.Oracle(bi.small_3d(dirs=d))
+        for ax in range(2 if expect < 7 else 3):
+            r = o.reflection(ax)
+            assert np.array_equal(r[r], np.arange(d.nd))  # involution
+            t = d.s.copy()
+            t[:, ax] *= -1
+            assert np.array_equal(d.s[r], t)  # bit-exact reflected vector
+            assert np.array_equal(d.w[r], d.w)
+
+
+def test_spec_reflection_example():
+    g = GOLD["inplane8_reflection"]
+    d = bi.directions_inplane(g["N"])
+    o = oracle.Oracle(bi.small_3d(dirs=d))
+    assert o.reflection(g["axis"])[g["d"] - 1] + 1 == g["r"]
+
+
+def test_3d_quadrature_discrete_moments():
+    d = bi.directions_control_angle(20, 20)
+    # sum_{s_z>0} w s_z = 3.151307 (not pi); <s_x^2> = 0.332989
+    assert abs((d.w * d.s[:, 2])[d.s[:, 2] > 0].sum() - 3.151307) < 1e-6
+    assert abs((d.w * d.s[:, 0] ** 2).sum() / d.w.sum() - 0.332989) < 1e-6
+
+
+# ----------------------------------------------------------------- I0(T)
+
+def _mp_I0(b: bi.Bands, k: int, T, deriv=False):
+    """Independent high-precision band integral (mpmath adaptive quadrature)."""
+    mpmath.mp.dps = 40
+    vs, c2, g = mpmath.mpf(b.vs[k]), mpmath.mpf(b.c2[k]), mpmath.mpf(b.g[k])
+    hb, kb, T = mpmath.mpf(HBAR), mpmath.mpf(KB), mpmath.mpf(T)
+
+    def kw(w):
+        if c2 == 0:
+            return w / vs
+        return (-vs + mpmath.sqrt(vs * vs + 4 * c2 * w)) / (2 * c2)
+
+    def f(w):
+        x = hb * w / (kb * T)
+        base = w * kw(w) ** 2 / mpmath.expm1(x)
+        if deriv:
+            return base * (x / T) * mpmath.exp(x) / mpmath.expm1(x)
+        return base
+
+    lo, hi = mpmath.mpf(b.w_lo[k]), mpmath.mpf(b.w_hi[k])
+    try:
+        val = mpmath.quad(f, [lo, hi])
+    except ZeroDivisionError:  # mpmath's error estimator when two levels agree exactly
+        val = mpmath.quad(f, [lo, (lo + hi) / 2, hi])
+    return float(g * hb / (8 * mpmath.pi ** 3) * val)
+
+
+@pytest.mark.parametrize("T", [10.0, 100.0, 300.0, 1000.0])
+def test_I0_bose_einstein_vs_mpmath(T):
+    b = bi.silicon_bands(29)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    worst = 0.0
+    for k in range(0, b.nb, 3):
+        v, dv = o.I0(k, T)
+        ref = _mp_I0(b, k, T)
+        worst = max(worst, abs(v / ref - 1))
+        if k % 9 == 0:
+            dref = _mp_I0(b, k, T, deriv=True)
+            assert abs(dv / dref - 1) < 1e-12
+    assert worst < 5e-14, worst
+
+
+@pytest.mark.parametrize("T", [2.0, 5.0, 10.0])
+def test_I0_debye_T4_law(T):
+    # c2 = 0, one polarisation: sum_b I0_b = pi kB^4 T^4 / (120 hbar^3 v^2)
+    v = 6000.0
+    b = bi.debye_bands(v, 2 * math.pi / 5.43e-10, 40)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    tot = sum(o.I0(k, T)[0] for k in range(b.nb))
+    closed = math.pi * KB ** 4 * T ** 4 / (120 * HBAR ** 3 * v ** 2)
+    assert abs(tot / closed - 1) < 1e-13
+
+
+def test_I0_classical_limit_and_monotone():
+    b = bi.silicon_bands(29)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    k = 3
+    T = 1e6
+    v = o.I0(k, T)[0]
+    # classical limit g kB T/(8 pi^3) * int k^2 dw (exact polynomial-root integral via mpmath)
+    mpmath.mp.dps = 30
+    vs, c2 = mpmath.mpf(b.vs[k]), mpmath.mpf(b.c2[k])
+    kk = lambda w: (-vs + mpmath.sqrt(vs * vs + 4 * c2 * w)) / (2 * c2)
+    cl = float(b.g[k] * KB * T / (8 * mpmath.pi ** 3) * mpmath.quad(lambda w: kk(w) ** 2, [b.w_lo[k], b.w_hi[k]]))
+    wbar = 0.5 * (b.w_lo[k] + b.w_hi[k])
+    assert abs((v / cl - 1) + HBAR * wbar / (2 * KB * T)) < 1e-6
+    for kk_ in range(b.nb):
+        assert o.I0(kk_, 310.0)[0] > o.I0(kk_, 300.0)[0]
+        # dI0/dT vs central difference
+        h = 1e-3
+        fd = (o.I0(kk_, 300.0 + h)[0] - o.I0(kk_, 300.0 - h)[0]) / (2 * h)
+        assert abs(fd / o.I0(kk_, 300.0)[1] - 1) < 1e-7
+
+
+def test_I0_linear_mode_example():
+    g = GOLD["linear_mode"]
+    b = bi.linear_bands([1.0], [1.0], [g["a"]], [g["I_ref"]], g["T_ref"])
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    assert o.I0(0, g["T"])[0] == g["I0"]
+    assert o.I0(0, g["T_ref"])[0] == g["I_ref"]
+
+
+def test_beta_scaling_laws():
+    b = bi.silicon_bands(29)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    T = 250.0
+    for k in range(b.nb):
+        p0, p3, p4, pu, th = b.beta_coef[k]
+        e1, e2 = o.beta(k, T) - p0, o.beta(k, 2 * T) - p0
+        if p3:
+            assert abs(e2 / e1 - 8) < 1e-12  # LA: B_L w^2 T^3
+        elif p4:
+            assert abs(e2 / e1 - 16) < 1e-12  # TA normal: B_TN w T^4
+        elif pu:
+            assert abs(e1 * math.sinh(th / T) / pu - 1) < 1e-14  # TA umklapp
+        assert o.beta(k, 350.0) > o.beta(k, 300.0) >= p0 > 0
+    # beta_max(350 K) = 5.42e11 1/s for the 40-channel table
+    assert abs(max(o.beta(k, 350.0) for k in range(b.nb)) / 5.42e11 - 1) < 5e-3
+
+
+# ----------------------------------------------------------------- Newton
+
+def test_newton_linear_closed_form():
+    rng = np.random.default_rng(1)
+    nb = 5
+    b = bi.linear_bands(rng.uniform(1e3, 9e3, nb), rng.uniform(1e-12, 1e-9, nb),
+                        rng.uniform(1e2, 1e4, nb), rng.uniform(1e5, 1e7, nb), 300.0)
+    p = bi.small_3d(bands=b, dirs=bi.directions_control_angle(4, 8))
+    o = oracle.Oracle(p)
+    W = p.dirs.w.sum()
+    for _ in range(300):
+        Tn = rng.uniform(250, 350)
+        I0c = np.array([o.I0(k, Tn)[0] for k in range(nb)])
+        D = rng.normal(0, 1e4, nb) * W
+        bn = 1.0 / rng.uniform(1e-12, 1e-9, nb)
+        T, _ = o.newton(Tn, D, I0c, bn)
+        c = bn / b.v
+        closed = b.T_ref + np.sum(c * (W * (I0c - b.I_ref) - D)) / (W * np.sum(c * b.slope))
+        assert abs(T - closed) <= 1e-12 * closed
+
+
+def test_newton_bose_einstein_vs_mpmath_root():
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 7, 15, 28, 29, 35, 39])
+    p = bi.small_3d(bands=b)
+    o = oracle.Oracle(p)
+    W = p.dirs.w.sum()
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        Tn = rng.uniform(280, 320)
+        I0c = np.array([o.I0(k, Tn)[0] for k in range(b.nb)])
+        D = W * I0c * rng.uniform(-0.02, 0.02, b.nb)
+        bn = np.array([o.beta(k, Tn) for k in range(b.nb)])
+        T, it = o.newton(Tn, D, I0c, bn)
+        assert it <= 6
+        c = bn / b.v
+
+        def F(t):
+            return sum(c[k] * (W * (_mp_I0(b, k, float(t)) - I0c[k]) + D[k]) for k in range(b.nb))
+
+        # exact-integral F changes sign within +-1e-10 K of the oracle's root
+        h = 1e-10 * 300
+        f_lo, f_hi = F(T - h), F(T + h)
+        assert f_lo < 0 < f_hi, (T, f_lo, f_hi)
+
+
+def test_newton_fixed_point_shortcut():
+    b = bi.silicon_bands(29)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    I0c = np.array([o.I0(k, 300.0)[0] for k in range(b.nb)])
+    T, it = o.newton(300.0, np.zeros(b.nb), I0c, np.ones(b.nb))
+    assert T == 300.0 and it == 0
+
+
+# ----------------------------------------------------------------- sweep (exact rationals)
+
+def _lin_problem(mesh, dirs, bcs, nb=2, dt=None, seed=0):
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(2e3, 8e3, nb)
+    tau = rng.uniform(2e-11, 8e-11, nb)
+    bands = bi.linear_bands(v, tau, rng.uniform(1e2, 1e3, nb), rng.uniform(1e4, 1e5, nb), 300.0)
+    if dt is None:
+        dt = 0.3 * min(mesh.dx, mesh.dy) / v.max() / 2
+    return bi.Problem("lin", mesh, dirs, bands, dt, 300.0, bcs)
+
+
+@pytest.mark.parametrize("case", ["3d_all_kinds", "2d_inplane", "2d_3dquad"])
+def test_sweep_exact_rational(case):
+    rng = np.random.default_rng(11)
+    if case == "3d_all_kinds":
+        mesh = bi.Mesh(3, 3, 3, 2, 1e-7, 1.3e-7, 0.9e-7)
+        dirs = bi.directions_control_angle(4, 8)
+        bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, np.array([301.0, 303.0, 305.0, 307.0, 309.0, 311.0])),
+               bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 299.0)]
+    elif case == "2d_inplane":
+        mesh = bi.Mesh(2, 4, 3, 1, 1e-7, 1e-7, 1.0)
+        dirs = bi.directions_inplane(8)
+        bcs = [bi.WallBC(2), bi.WallBC(1), bi.WallBC(0, None, 302.0), bi.WallBC(0, np.arange(4) + 300.5),
+               bi.WallBC(1), bi.WallBC(1)]
+    else:
+        mesh = bi.Mesh(2, 3, 3, 1, 1e-7, 1e-7, 1.0)
+        dirs = bi.directions_control_angle(2, 4)
+        bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 310.0), bi.WallBC(1), bi.WallBC(1)]
+    p = _lin_problem(mesh, dirs, bcs)
+    o = oracle.Oracle(p)
+    nc, nd, nb = mesh.ncells, dirs.nd, p.bands.nb
+    T = rng.uniform(290, 310, nc)
+    I0c, betac = o.refresh(T)
+    I = I0c[:, None, :] * rng.uniform(0.9, 1.1, (nc, nd, nb))
+    got = o.sweep(I, I0c, betac)
+    ex = exact.exact_step_sweep(p, I, I0c, betac)
+    err = exact.ulp_error(got, ex)
+    assert err <= 4.0, err
+
+
+def test_reduce_vs_fsum():
+    p = bi.small_3d()
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    I0c, _ = o.refresh(T)
+    D = o.reduce(I, I0c)
+    w = p.dirs.w
+    for c in (0, 7, p.mesh.ncells - 1):
+        for b in range(p.bands.nb):
+            terms = [w[d] * (I0c[c, b] - I[c, d, b]) for d in range(p.dirs.nd)]
+            ref = math.fsum(terms)
+            bound = p.dirs.nd * 2.0 ** -53 * sum(abs(t) for t in terms) * 2
+            assert abs(D[c, b] - ref) <= bound
+
+
+def test_dense_operator_max_principle():
+    """I' = M I + q: M >= 0 entrywise iff the dt bound holds."""
+    mesh = bi.Mesh(2, 3, 2, 1, 1e-7, 1e-7, 1.0)
+    dirs = bi.directions_inplane(8)
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(1), bi.WallBC(1)]
+    for frac, expect_pos in ((0.9, True), (1.6, False)):
+        p = _lin_problem(mesh, dirs, bcs, nb=2)
+        # dt at `frac` of the positivity limit
+        p.dt = 1.0
+        m1 = 1.0 - oracle.Oracle(p).dt_margin(300.0)  # = max(beta + v sum|s|/D) * 1
+        p.dt = frac / m1
+        o = oracle.Oracle(p)
+        nc, nd, nb = mesh.ncells, dirs.nd, 2
+        T = np.full(nc, 300.0)
+        I0c, betac = o.refresh(T)
+        n = nc * nd * nb
+        q = o.sweep(np.zeros(n), I0c, betac).reshape(-1)
+        M = np.empty((n, n))
+        for k in range(n):
+            e = np.zeros(n)
+            e[k] = 1.0
+            M[:, k] = o.sweep(e, I0c, betac).reshape(-1) - q
+        if expect_pos:
+            assert M.min() >= -1e-15
+            assert abs(o.dt_margin(300.0) - (1 - frac)) < 1e-12
+        else:
+            assert M.min() < -0.1
+
+
+# ----------------------------------------------------------------- invariants
+
+def test_uniform_fixed_point_bitexact():
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 10, 20, 30, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+           bi.WallBC(1)]
+    p = bi.small_3d(bands=b, bcs=bcs)
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    I2, T2, _, _ = o.run(I, T, 100)
+    assert np.array_equal(I2, I) and np.array_equal(T2, T)
+
+
+def test_uniform_fixed_point_diffuse_near_exact():
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 20, 39])
+    p = bi.small_3d(bands=b, bcs=bi.uniform_bcs(bi.BC_DIFFUSE))
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    I2, T2, _, _ = o.run(I, T, 100)
+    assert np.max(np.abs(I2 / I - 1)) < 100 * 2 * 2.0 ** -53
+    assert np.max(np.abs(T2 - 300.0)) < 1e-11
+
+
+@pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE])
+def test_closed_box_energy_conservation(kind):
+    """All walls specular (or diffuse): E = sum V sum_b G_b / v_b constant."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])  # distinct v, tau(T)
+    p = bi.small_3d(6, 5, 4, bands=b, bcs=bi.uniform_bcs(kind), dirs=bi.directions_control_angle(4, 16))
+    o = oracle.Oracle(p)
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)  # consistent start (set_state with I only)
+    E0 = o.energy(I)
+    I2, T2, _, _ = o.run(I, T, 1000, I0c, betac)
+    E1 = o.energy(I2)
+    assert abs(E1 / E0 - 1) < 1e-12, E1 / E0 - 1
+    assert I2.min() > 0
+
+
+def test_mirror_symmetry_2d_hotspot_bitexact():
+    """Centred hot spot, even nx, specular sides: I(x,d,b) = I(nx-1-x, r_x(d), b)."""
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 15, 35])
+    p = bi.config2(n=12)
+    p.bands = b
+    p.mesh = bi.Mesh(2, 12, 12, 1, 2e-6, 2e-6, 1.0)
+    p.dirs = bi.directions_control_angle(4, 8)
+    p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, 2e-6, width=4e-6), 300.0)
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I2, T2, _, _ = o.run(o.equilibrium(T), T, 60)
+    r = o.reflection(0)
+    A = I2.reshape(12, 12, p.dirs.nd, b.nb)
+    assert np.array_equal(A, A[:, ::-1][:, :, r, :])
+    Tm = T2.reshape(12, 12)
+    assert np.array_equal(Tm, Tm[:, ::-1])
+    assert T2.max() > 300.0  # something happened
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_mirror_symmetry_3d_random_bitexact(axis):
+    b = bi.subset_bands(bi.silicon_bands(29), [1, 25, 37])
+    p = bi.small_3d(6, 4, 4, bands=b, bcs=bi.uniform_bcs(bi.BC_SPECULAR))
+    p.bcs[2 * axis] = bi.WallBC(bi.BC_DIFFUSE)
+    p.bcs[2 * axis + 1] = bi.WallBC(bi.BC_DIFFUSE)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    n = (p.mesh.nz, p.mesh.ny, p.mesh.nx)
+    r = o.reflection(axis)
+    flip = 2 - axis  # array axis of the mesh axis in [z][y][x]
+    A = I.reshape(*n, p.dirs.nd, b.nb)
+    A = 0.5 * (A + np.flip(A, flip)[..., r, :])  # symmetrise
+    Tm = T.reshape(n)
+    Tm = 0.5 * (Tm + np.flip(Tm, flip))
+    I = A.reshape(I.shape).copy()
+    T = Tm.reshape(-1).copy()
+    I2, T2, _, _ = o.run(I, T, 30)
+    B = I2.reshape(*n, p.dirs.nd, b.nb)
+    assert np.array_equal(B, np.flip(B, flip)[..., r, :])
+    assert np.array_equal(T2.reshape(n), np.flip(T2.reshape(n), flip))
+
+
+def test_thread_count_invariance():
+    p = bi.small_3d()
+    I, T = oracle.Oracle(p).random_state()
+    a = oracle.Oracle(p, nthreads=1).run(I, T, 5)
+    b = oracle.Oracle(p, nthreads=7).run(I, T, 5)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def _slab(n, kn, beta_scale=1.0, Th=305.0, Tc=295.0):
+    """1-D slab along x: n x 1 cells, in-plane 16 dirs, specular y walls, gray linear."""
+    v = 6400.0
+    C = 1.66e6
+    W = 2 * math.pi
+    a = C * v / W
+    L = 1e-6
+    tau = kn * L / v if beta_scale else 1.0  # Kn = v tau / L
+    bands = bi.linear_bands([v], [tau], [a], [a * 300.0], 300.0)
+    if not beta_scale:
+        bands.beta_coef[:, 0] = 0.0
+    d = L / n
+    mesh = bi.Mesh(2, n, 1, 1, d, d, 1.0)
+    bcs = [bi.WallBC(0, None, Th), bi.WallBC(0, None, Tc), bi.WallBC(1), bi.WallBC(1), bi.WallBC(1),
+           bi.WallBC(1)]
+    dt = 0.45 * d / v
+    if beta_scale:
+        dt = min(dt, 0.2 * tau)
+    return bi.Problem("slab", mesh, bi.directions_inplane(16), bands, dt, 300.0, bcs), a
+
+
+def _flux_x(p, I):
+    """q = sum_d w_d s_x I (one channel) per cell."""
+    return (p.dirs.w[None, :] * p.dirs.s[None, :, 0] * I[:, :, 0]).sum(1)
+
+
+@pytest.mark.slow
+def test_ballistic_slab_closed_form():
+    p, a = _slab(8, 0, beta_scale=0.0)
+    o = oracle.Oracle(p, nthreads=1)
+    T = np.full(8, 300.0)
+    I, T2, _, _ = o.run(o.equilibrium(T), T, 3000)
+    q = _flux_x(p, I)
+    d = p.dirs
+    expect = (a * 305.0 - a * 295.0) * (d.w * d.s[:, 0])[d.s[:, 0] > 0].sum()
+    assert np.max(np.abs(q / expect - 1)) < 1e-9
+
+
+@pytest.mark.slow
+def test_ballistic_slab_temperature():
+    p, a = _slab(8, 1e6)
+    o = oracle.Oracle(p, nthreads=1)
+    T = np.full(8, 300.0)
+    I, T2, _, _ = o.run(o.equilibrium(T), T, 3000)
+    # weak scattering: G = (W/2)(I0h + I0c) -> flat T = (Th + Tc)/2
+    assert np.max(np.abs(T2 - 300.0)) < 1e-4
+
+
+@pytest.mark.slow
+def test_diffusive_slab_fourier():
+    kn = 0.05
+    n = 80
+    p, a = _slab(n, kn, Th=301.0, Tc=299.0)
+    o = oracle.Oracle(p)
+    T = np.full(n, 300.0)
+    tau = 1.0 / p.bands.beta_coef[0, 0]
+    nsteps = int(2500 * tau / p.dt)
+    I, T2, _, _ = o.run(o.equilibrium(T), T, nsteps)
+    x = (np.arange(n) + 0.5) * p.mesh.dx
+    mid = slice(n // 4, 3 * n // 4)
+    fit = np.polyfit(x[mid], T2[mid], 1)
+    resid = T2[mid] - np.polyval(fit, x[mid])
+    assert np.max(np.abs(resid)) < 1e-4 * 2.0
+    q = _flux_x(p, I)
+    assert np.max(np.abs(q[mid] / q[mid].mean() - 1)) < 1e-4
+    d = p.dirs
+    k = a * d.w.sum() * p.bands.v[0] * tau * (d.w * d.s[:, 0] ** 2).sum() / d.w.sum()
+    ratio = q[mid].mean() / (-k * fit[0])
+    assert abs(ratio - 1) < 1e-3, ratio
