@@ -351,28 +351,75 @@ def random_phases(seed: int) -> Tuple[float, float, float]:
     return float(p[0]), float(p[1]), float(p[2])
 
 
-def random_temperature(mesh: Mesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0) -> np.ndarray:
+def random_temperature(mesh: Mesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0,
+                       box=None) -> np.ndarray:
     """T_c = T_mean + T_amp*sin(2pi(x/Lx+p1))*sin(2pi(y/Ly+p2))[*sin(2pi(z/Lz+p3))],
-    x = cell centre (i+1/2)*dx.  Canonical cell order."""
+    x = cell centre (i+1/2)*dx with the GLOBAL index i.  Canonical cell order of
+    the full mesh, or of the sub-box ((x0,x1),(y0,y1),(z0,z1)) when given."""
     p1, p2, p3 = random_phases(seed)
-    x = (np.arange(mesh.nx) + 0.5) * mesh.dx
-    y = (np.arange(mesh.ny) + 0.5) * mesh.dy
-    z = (np.arange(mesh.nz) + 0.5) * mesh.dz
+    (x0, x1), (y0, y1), (z0, z1) = box if box is not None else ((0, mesh.nx), (0, mesh.ny), (0, mesh.nz))
+    x = (np.arange(x0, x1) + 0.5) * mesh.dx
+    y = (np.arange(y0, y1) + 0.5) * mesh.dy
+    z = (np.arange(z0, z1) + 0.5) * mesh.dz
     fx = np.sin(2.0 * math.pi * (x / (mesh.nx * mesh.dx) + p1))
     fy = np.sin(2.0 * math.pi * (y / (mesh.ny * mesh.dy) + p2))
     if mesh.dim == 3:
         fz = np.sin(2.0 * math.pi * (z / (mesh.nz * mesh.dz) + p3))
     else:
-        fz = np.ones(mesh.nz)
+        fz = np.ones(z1 - z0)
     T = T_mean + T_amp * (fz[:, None, None] * fy[None, :, None] * fx[None, None, :])
     return np.ascontiguousarray(T.reshape(-1))
 
 
-def intensity_noise_factor(seed: int, ncells: int, nd: int, nb: int, amp: float = 0.05) -> np.ndarray:
-    """(1 + amp*(2u - 1)) in canonical [cell][d][b] order; the caller multiplies
-    by its own I0_b(T_c)."""
-    u = uniform_noise(seed, ncells * nd * nb)
-    return (1.0 + amp * (2.0 * u - 1.0)).reshape(ncells, nd, nb)
+def intensity_noise_factor(seed: int, ncells: int, nd: int, nb: int, amp: float = 0.05,
+                           mesh: Optional[Mesh] = None, box=None) -> np.ndarray:
+    """(1 + amp*(2u - 1)) in canonical [cell][d][b] order, u from the GLOBAL
+    canonical index (c*nd + d)*nb + b; the caller multiplies by its own
+    I0_b(T_c).  With mesh and box, only the sub-box cells (sub-box order)."""
+    if box is None:
+        u = uniform_noise(seed, ncells * nd * nb)
+        return (1.0 + amp * (2.0 * u - 1.0)).reshape(ncells, nd, nb)
+    (x0, x1), (y0, y1), (z0, z1) = box
+    zz, yy, xx = np.meshgrid(np.arange(z0, z1), np.arange(y0, y1), np.arange(x0, x1), indexing="ij")
+    cg = (xx + mesh.nx * (yy + mesh.ny * zz)).reshape(-1).astype(np.uint64)
+    idx = (cg[:, None] * np.uint64(nd * nb) + np.arange(nd * nb, dtype=np.uint64)[None, :]).reshape(-1)
+    z = splitmix64(np.uint64(seed & MASK64) ^ idx)
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (1.0 + amp * (2.0 * u - 1.0)).reshape(cg.size, nd, nb)
+
+
+def subproblem(problem: "Problem", box, open_kind: int = BC_SPECULAR) -> "Problem":
+    """The problem restricted to a sub-box ((x0,x1),(y0,y1),(z0,z1)).  Sides on
+    the domain boundary keep their wall (T_wall restricted to the box faces);
+    interior ("open") sides get `open_kind` -- cells within k cells of an open
+    side are wrong after k steps, all others are exact."""
+    m = problem.mesh
+    (x0, x1), (y0, y1), (z0, z1) = box
+    sub = Mesh(m.dim, x1 - x0, y1 - y0, z1 - z0, m.dx, m.dy, m.dz)
+    lo = [x0, y0, z0]
+    hi = [x1, y1, z1]
+    n = [m.nx, m.ny, m.nz]
+    bcs = []
+    for r in range(6):
+        a = r // 2
+        on_wall = (lo[a] == 0) if r % 2 == 0 else (hi[a] == n[a])
+        bc = problem.bcs[r]
+        if not on_wall:
+            bcs.append(WallBC(open_kind, None, 300.0))
+            continue
+        Tw = None
+        if bc.T_wall is not None:
+            full = np.asarray(bc.T_wall)
+            if a == 0:
+                Tw = full.reshape(m.nz, m.ny)[z0:z1, y0:y1].reshape(-1)
+            elif a == 1:
+                Tw = full.reshape(m.nz, m.nx)[z0:z1, x0:x1].reshape(-1)
+            else:
+                Tw = full.reshape(m.ny, m.nx)[y0:y1, x0:x1].reshape(-1)
+            Tw = np.ascontiguousarray(Tw)
+        bcs.append(WallBC(bc.kind, Tw, bc.T_uniform))
+    return Problem(problem.name + f"_sub{box}", sub, problem.dirs, problem.bands, problem.dt,
+                   problem.T_init, bcs, problem.nsteps, problem.seed)
 
 
 # --------------------------------------------------------------------------

@@ -1,0 +1,225 @@
+/*
+ * bte.h -- C ABI of the B200-native explicit phonon-BTE time step
+ * (arXiv 2305.19400, "Automating GPU Scalability for Complex Scientific
+ * Models: Phonon Boltzmann Transport Equation").
+ *
+ * One step (all on the GPU, no host callbacks):
+ *   a1  boundary pass: ghost intensities from I^n           (Eq. 6)
+ *   a2  fused upwind-flux + relaxation sweep -> I^{n+1}      (Eq. 5, P:L378-387,
+ *       forward Euler Eqs. 2-3; upwind P:L150-157)
+ *       with the per-(cell, octant, band) partial sum of w_d (I0c - I^{n+1})
+ *   a3  per-cell reduction over directions and bands
+ *   a4  per-cell Newton for T^{n+1} against I0_b(T); refresh I0c, beta
+ *
+ *   a5  (nranks > 1) slab halo exchange of boundary planes
+ * "P:L<a>-<b>" = lines of /root/reference/PAPER.md; readings #n = DESIGN.md.
+ *
+ * Units: SI (m, s, K, rad/s); intensities in W m^-2 sr^-1 per channel.
+ * Precision: IEEE fp64 throughout (fp32 "did not provide adequate
+ * precision").
+ *
+ * Conventions (all functions):
+ *  - Every pointer argument documented "host" is caller-owned and only read
+ *    (or written, for outputs) during the call; the library copies what it
+ *    needs.  Device memory is owned by the context, obtained through
+ *    run->alloc/dealloc when given (PyTorch's caching allocator from Python),
+ *    else cudaMalloc/cudaFree, and released by bte_destroy.
+ *  - Canonical external orders: cell c = x + nx*(y + ny*z); intensity
+ *    arrays are [cell][d][b] (d = index into the caller's direction table,
+ *    b = channel), row-major, fp64.
+ *  - Errors: a bte_status is returned; nothing throws across the ABI.  A
+ *    human-readable message is available from bte_last_error(ctx).  Device-side
+ *    failures (Newton non-convergence, non-finite values) are latched in a
+ *    device word and reported by the bte_step call that observed them, with
+ *    the step and cell index in the message; the state is then undefined.
+ *  - Threading: one context per device per process; calls on one context are
+ *    not thread-safe.  All work is ordered on run->stream (a cudaStream_t, or
+ *    NULL for the legacy default stream).
+ */
+#ifndef BTE_H
+#define BTE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BTE_API __attribute__((visibility("default")))
+#else
+#define BTE_API
+#endif
+
+typedef struct bte_ctx bte_ctx;
+
+typedef enum {
+  BTE_OK = 0,
+  BTE_EINVAL = 1,      /* invalid argument / size / table                         */
+  BTE_ENOMEM = 2,      /* device allocation failed                                */
+  BTE_ECUDA = 3,       /* CUDA runtime error (message has cudaGetErrorString)     */
+  BTE_ENCCL = 4,       /* NCCL error (multi-rank)                                 */
+  BTE_EUNSTABLE = 5,   /* dt violates 1 - dt*beta_max - dt*v_b*sum|s_a|/D_a >= 0  */
+  BTE_ENOTCLOSED = 6,  /* specular wall: reflected direction not in the set      */
+  BTE_ENEWTON = 7,     /* temperature Newton did not converge in 50 iterations   */
+  BTE_ENONFINITE = 8   /* NaN/Inf reached the temperature update                 */
+} bte_status;
+
+typedef enum {
+  BTE_BC_ISOTHERMAL = 0, /* ghost = I0_b(T_wall(face)) for incoming d (Eq. 6 case 1) */
+  BTE_BC_SPECULAR = 1,   /* ghost = I_{r(d),b} of the boundary cell (Eq. 6 case 2;  */
+                         /* "symmetry" walls of the paper)                          */
+  BTE_BC_DIFFUSE = 2     /* adiabatic diffuse wall: ghost_b = sum_out w|s_a| I /     */
+                         /* sum_in w|s_a|, same for every incoming d (reading #11)  */
+} bte_bc_kind;
+
+typedef enum {
+  BTE_I0_LINEAR = 0,        /* I0_b(T) = I_ref[b] + slope[b]*(T - T_ref)   */
+  BTE_I0_BOSE_EINSTEIN = 1  /* g hbar/(8 pi^3) int w k(w)^2/(exp(hbar w/kB T)-1) dw,      */
+                            /* 16-point Gauss-Legendre per channel (reading #1)         */
+} bte_i0_mode;
+
+/* Uniform structured mesh.  dim = 2 or 3; for dim 2,
+ * nz must be 1 and dz is the (unit) depth used for cell volumes only.
+ * Wall regions: 0..5 = -x, +x, -y, +y, -z, +z (4, 5 unused for dim 2). */
+typedef struct {
+  int dim;
+  int64_t nx, ny, nz;
+  double dx, dy, dz;
+} bte_mesh;
+
+/* Discrete directions.  s: host [nd][3] unit vectors,
+ * w: host [nd] weights.  Directions are grouped by octant (sign pattern of s;
+ * a zero component counts as +); every non-empty octant must hold the same
+ * number of directions.  Reflection maps are derived by bit-exact matching. */
+typedef struct {
+  int nd;
+  const double *s;
+  const double *w;
+} bte_dirs;
+
+/* Channels ("bands").  All arrays host, length nb, except
+ * beta_coef [nb][5] = {p0, p3, p4, pu, theta}:
+ *   beta_b(T) = 1/tau_b(T) = p0 + p3*T^3 + p4*T^4 + pu/sinh(theta/T)  (pu = 0 drops
+ *   the term), all coefficients >= 0 (readings #3, #15).
+ * LINEAR mode uses I_ref, slope, T_ref; BOSE_EINSTEIN uses w_lo, w_hi (band
+ * edges, rad/s), vs, c2 (dispersion w = vs*k + c2*k^2), g (degeneracy). */
+typedef struct {
+  int nb;
+  const double *v; /* group speed |v_g|_b, m/s (> 0) */
+  int mode;        /* bte_i0_mode */
+  const double *I_ref, *slope;
+  double T_ref;
+  const double *w_lo, *w_hi, *vs, *c2, *g;
+  const double *beta_coef;
+} bte_bands;
+
+/* Run parameters.  stream: cudaStream_t (NULL = legacy default stream).
+ * alloc/dealloc: optional device allocator (bytes, alloc_ctx) -> 256-B aligned
+ * pointer / (ptr, alloc_ctx); NULL -> cudaMalloc/cudaFree.
+ * rank/nranks/nccl_id: multi-GPU slab decomposition along the slowest axis
+ * (z for dim 3, y for dim 2); nccl_id = 128-byte ncclUniqueId broadcast by the
+ * caller (e.g. through torch.distributed), ignored when nranks == 1. */
+typedef struct {
+  double dt;
+  double T_init;
+  int device;
+  void *stream;
+  int rank, nranks;
+  const void *nccl_id;
+  void *(*alloc)(size_t bytes, void *alloc_ctx);
+  void (*dealloc)(void *ptr, void *alloc_ctx);
+  void *alloc_ctx;
+} bte_run;
+
+/* Create a context: validates tables (positive sizes/speeds, equal octant
+ * populations, W > 0), precomputes geometry and coefficient tables, allocates
+ * the state and initialises it to equilibrium at T_init (I = I0_b(T_init)).
+ * All walls start SPECULAR; call bte_set_bc to change them.
+ * Errors: BTE_EINVAL, BTE_ENOMEM, BTE_ECUDA, BTE_EUNSTABLE, BTE_ENCCL. */
+BTE_API bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                      const bte_run *run, bte_ctx **out);
+
+/* Boundary condition of one wall region (0..5 = -x,+x,-y,+y,-z,+z).
+ * T_wall: host array with one temperature per boundary face of that wall,
+ * row-major over the two in-plane axes in (x,y,z) order ((y,z) for x-walls,
+ * (x,z) for y-walls, (x,y) for z-walls), or NULL to use T_uniform.  Ignored
+ * unless kind == BTE_BC_ISOTHERMAL.  Isothermal ghosts I0_b(T_wall) are
+ * tabulated on the device once here.
+ * Errors: BTE_EINVAL (region/kind), BTE_ENOTCLOSED (specular wall whose
+ * reflections are not in the set), BTE_EUNSTABLE (T_wall raises beta_max past
+ * the dt bound). */
+BTE_API bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, double T_uniform);
+
+/* Replace the state from host arrays (canonical orders, this rank's slab).
+ *  I != NULL, T != NULL : I and T as given; I0c = I0(T), beta = beta(T).
+ *  I == NULL, T != NULL : equilibrium I_{c,d,b} = I0_b(T_c).
+ *  I != NULL, T == NULL : T from one reduction + Newton solve starting at
+ *                         T_init with beta_next = beta(T_init).
+ * Sizes: I has ncells_local*nd*nb doubles, T has ncells_local doubles. */
+BTE_API bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T);
+
+/* Device-generated random start:
+ *   T_c = T_mean + T_amp*sin(2pi(x/Lx+phase[0]))*sin(2pi(y/Ly+phase[1]))[*sin(2pi(z/Lz+phase[2]))]
+ *   I_{c,d,b} = I0_b(T_c) * (1 + I_amp*(2u-1)),
+ *   u = (splitmix64(seed ^ idx) >> 11) * 2^-53, idx = (c_global*nd + d)*nb + b.
+ * x = (i+1/2)*dx is the cell centre (global coordinates under slab decomposition). */
+BTE_API bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], double T_mean,
+                           double T_amp, double I_amp);
+
+/* Advance nsteps explicit steps on the context stream, then synchronise once
+ * and check the device error word.  Errors: BTE_ENEWTON, BTE_ENONFINITE
+ * (with step/cell in bte_last_error), BTE_ECUDA, BTE_ENCCL. */
+BTE_API bte_status bte_step(bte_ctx *ctx, int64_t nsteps);
+
+/* Copy state to caller-allocated host buffers (canonical order, this rank's
+ * slab).  count must equal the exact element count: ncells_local*nd*nb for
+ * the intensity, ncells_local for the temperature; else BTE_EINVAL. */
+BTE_API bte_status bte_get_intensity(bte_ctx *ctx, double *out, size_t count);
+BTE_API bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count);
+
+/* Diagnostic total energy of this rank's slab, E = sum_c V sum_b (1/v_b)
+ * sum_d w_d I_{c,d,b}.  Not on the hot path. */
+BTE_API bte_status bte_get_energy(bte_ctx *ctx, double *E);
+
+/* Sub-step access for kernel unit tests (state unchanged):
+ *   which = 0: I after one boundary pass + sweep from the current state, [cell][d][b]
+ *   which = 1: the reduced deviation D_{c,b} = sum_d w_d (I0c - I^{n+1}), [cell][b]
+ *   which = 2: current I0c [cell][b];  which = 3: current beta [cell][b]. */
+BTE_API bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count);
+
+/* Per-kernel device timing (CUDA events recorded on the context stream around
+ * every launch while enabled; read out after the next bte_step). */
+typedef struct {
+  int64_t steps;           /* steps timed                                    */
+  int64_t launches;        /* kernels launched by the library in those steps */
+  double sweep_ms;         /* summed device time of the a1+a2 sweep launches  */
+  double newton_ms;        /* summed device time of the a3+a4 launches        */
+  double boundary_ms;      /* summed device time of the diffuse-ghost launches */
+  double halo_ms;          /* summed time of the halo exchange (nranks > 1)   */
+  int64_t sweep_launches;
+  int64_t newton_launches;
+  int64_t boundary_launches;
+} bte_timing;
+BTE_API bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps);
+BTE_API bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out);
+
+/* Sizes of this rank's slab and the layout. */
+typedef struct {
+  int64_t ncells_local, ncells_global, z0, nz_local; /* slab along the slowest axis */
+  int nd, nb, n_octants, nj;                         /* nj = directions per octant  */
+  int64_t bytes_state;                               /* device bytes held by ctx    */
+} bte_info;
+BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
+
+BTE_API const char *bte_last_error(const bte_ctx *ctx);
+BTE_API void bte_destroy(bte_ctx *ctx);
+
+/* Library build identification (for the tests' symbol/ABI check). */
+BTE_API const char *bte_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BTE_H */

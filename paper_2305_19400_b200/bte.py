@@ -1,0 +1,291 @@
+"""Thin ctypes binding of libbte.so (include/bte.h).  Argument marshalling only:
+every step of the BTE hot path runs in the library's CUDA kernels.  PyTorch
+supplies device memory (caching allocator), the CUDA stream and, for several
+GPUs, the NCCL unique-id broadcast over torch.distributed.
+
+Names follow include/bte.h.  There is no CPU fallback: if libbte.so is
+missing or no CUDA device is present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbte.so")
+
+BTE_OK = 0
+STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE_ENCCL",
+          5: "BTE_EUNSTABLE", 6: "BTE_ENOTCLOSED", 7: "BTE_ENEWTON", 8: "BTE_ENONFINITE"}
+BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE = 0, 1, 2
+I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
+
+EXPORTS = ("bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
+           "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
+           "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
+           "bte_version")
+
+
+class BteError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Mesh(C.Structure):
+    _fields_ = [("dim", C.c_int), ("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double)]
+
+
+class Dirs(C.Structure):
+    _fields_ = [("nd", C.c_int), ("s", C.c_void_p), ("w", C.c_void_p)]
+
+
+class Bands(C.Structure):
+    _fields_ = [("nb", C.c_int), ("v", C.c_void_p), ("mode", C.c_int), ("I_ref", C.c_void_p),
+                ("slope", C.c_void_p), ("T_ref", C.c_double), ("w_lo", C.c_void_p),
+                ("w_hi", C.c_void_p), ("vs", C.c_void_p), ("c2", C.c_void_p), ("g", C.c_void_p),
+                ("beta_coef", C.c_void_p)]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+DEALLOC_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+class Run(C.Structure):
+    _fields_ = [("dt", C.c_double), ("T_init", C.c_double), ("device", C.c_int),
+                ("stream", C.c_void_p), ("rank", C.c_int), ("nranks", C.c_int),
+                ("nccl_id", C.c_void_p), ("alloc", ALLOC_FN), ("dealloc", DEALLOC_FN),
+                ("alloc_ctx", C.c_void_p)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("launches", C.c_int64), ("sweep_ms", C.c_double),
+                ("newton_ms", C.c_double), ("boundary_ms", C.c_double), ("halo_ms", C.c_double),
+                ("sweep_launches", C.c_int64), ("newton_launches", C.c_int64),
+                ("boundary_launches", C.c_int64)]
+
+
+class Info(C.Structure):
+    _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
+                ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
+                ("nj", C.c_int), ("bytes_state", C.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libbte.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    P = C.c_void_p
+    dp = C.c_void_p
+    lib.bte_create.argtypes = [C.POINTER(Mesh), C.POINTER(Dirs), C.POINTER(Bands), C.POINTER(Run),
+                               C.POINTER(C.c_void_p)]
+    lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
+    lib.bte_set_state.argtypes = [P, dp, dp]
+    lib.bte_init_random.argtypes = [P, C.c_uint64, dp, C.c_double, C.c_double, C.c_double]
+    lib.bte_step.argtypes = [P, C.c_int64]
+    lib.bte_get_intensity.argtypes = [P, dp, C.c_size_t]
+    lib.bte_get_temperature.argtypes = [P, dp, C.c_size_t]
+    lib.bte_get_energy.argtypes = [P, C.POINTER(C.c_double)]
+    lib.bte_debug_substep.argtypes = [P, C.c_int, dp, C.c_size_t]
+    lib.bte_timing_enable.argtypes = [P, C.c_int, C.c_int64]
+    lib.bte_timing_read.argtypes = [P, C.POINTER(Timing)]
+    lib.bte_get_info.argtypes = [P, C.POINTER(Info)]
+    lib.bte_last_error.argtypes = [P]
+    lib.bte_last_error.restype = C.c_char_p
+    lib.bte_destroy.argtypes = [P]
+    lib.bte_destroy.restype = None
+    lib.bte_version.restype = C.c_char_p
+    for name in EXPORTS:
+        if name not in ("bte_last_error", "bte_destroy", "bte_version"):
+            getattr(lib, name).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _f64(a) -> Optional[np.ndarray]:
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+class Solver:
+    """One BTE context on one GPU (one slab of the mesh when nranks > 1)."""
+
+    def __init__(self, mesh, dirs, bands, dt: float, T_init: float, device: int = 0, stream=None,
+                 rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
+                 torch_alloc: bool = True):
+        import torch  # plumbing: device memory and streams
+        if not torch.cuda.is_available():
+            raise RuntimeError("libbte needs a CUDA device (no CPU fallback)")
+        self._lib = load_library()
+        self._torch = torch
+        self.device = device
+        torch.cuda.set_device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        self._keep = []
+        k = self._keep.append
+
+        m = Mesh(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.dx, mesh.dy, mesh.dz)
+        s, w = _f64(dirs.s), _f64(dirs.w)
+        k(s), k(w)
+        d = Dirs(int(w.shape[0]), _p(s), _p(w))
+        arrs = {}
+        for name in ("v", "I_ref", "slope", "w_lo", "w_hi", "vs", "c2", "g", "beta_coef"):
+            a = _f64(getattr(bands, name, None))
+            arrs[name] = a
+            if a is not None:
+                k(a)
+        b = Bands(int(arrs["v"].shape[0]), _p(arrs["v"]), int(bands.mode), _p(arrs["I_ref"]),
+                  _p(arrs["slope"]), float(getattr(bands, "T_ref", 300.0)), _p(arrs["w_lo"]),
+                  _p(arrs["w_hi"]), _p(arrs["vs"]), _p(arrs["c2"]), _p(arrs["g"]), _p(arrs["beta_coef"]))
+        if torch_alloc:
+            def _alloc(nbytes, _ctx):
+                return torch.cuda.caching_allocator_alloc(int(nbytes), device, self.stream)
+
+            def _free(ptr, _ctx):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._alloc_cb, self._free_cb = ALLOC_FN(_alloc), DEALLOC_FN(_free)
+        else:
+            self._alloc_cb, self._free_cb = ALLOC_FN(), DEALLOC_FN()
+        idbuf = None
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nranks > 1 needs the 128-byte ncclUniqueId")
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            k(idbuf)
+        run = Run(float(dt), float(T_init), int(device), C.c_void_p(self.stream.cuda_stream), int(rank),
+                  int(nranks), C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                  self._alloc_cb, self._free_cb, None)
+        h = C.c_void_p()
+        st = self._lib.bte_create(C.byref(m), C.byref(d), C.byref(b), C.byref(run), C.byref(h))
+        self._h = h
+        if st != BTE_OK:
+            msg = self._err()
+            self.close()
+            raise BteError(st, msg)
+        info = Info()
+        self._check(self._lib.bte_get_info(self._h, C.byref(info)))
+        self.ncells = int(info.ncells_local)
+        self.ncells_global = int(info.ncells_global)
+        self.z0 = int(info.z0)
+        self.nz_local = int(info.nz_local)
+        self.nd, self.nb = int(info.nd), int(info.nb)
+        self.n_octants, self.nj = int(info.n_octants), int(info.nj)
+        self.bytes_state = int(info.bytes_state)
+
+    # ---------------------------------------------------------------- helpers
+    @classmethod
+    def from_problem(cls, problem, **kw) -> "Solver":
+        """Build from a problem description (mesh/dirs/bands/dt/T_init/bcs)."""
+        sv = cls(problem.mesh, problem.dirs, problem.bands, problem.dt, problem.T_init, **kw)
+        nreg = 6 if problem.mesh.dim == 3 else 4
+        for r in range(nreg):
+            bc = problem.bcs[r]
+            sv.set_bc(r, bc.kind, bc.T_wall, bc.T_uniform)
+        return sv
+
+    def _err(self) -> str:
+        if not self._h:
+            return "no context"
+        return self._lib.bte_last_error(self._h).decode(errors="replace")
+
+    def _check(self, st: int):
+        if st != BTE_OK:
+            raise BteError(st, self._err())
+
+    # ---------------------------------------------------------------- API
+    def set_bc(self, region: int, kind: int, T_wall=None, T_uniform: float = 300.0):
+        Tw = _f64(T_wall)
+        self._check(self._lib.bte_set_bc(self._h, int(region), int(kind), _p(Tw), float(T_uniform)))
+
+    def set_state(self, I=None, T=None):
+        I, T = _f64(I), _f64(T)
+        if I is not None and I.size != self.ncells * self.nd * self.nb:
+            raise ValueError("I has the wrong size")
+        if T is not None and T.size != self.ncells:
+            raise ValueError("T has the wrong size")
+        self._check(self._lib.bte_set_state(self._h, _p(I), _p(T)))
+
+    def init_random(self, seed: int, phase: Sequence[float], T_mean: float, T_amp: float, I_amp: float):
+        ph = _f64(list(phase) + [0.0] * (3 - len(phase)))
+        self._check(self._lib.bte_init_random(self._h, C.c_uint64(seed & (2 ** 64 - 1)), _p(ph), T_mean,
+                                              T_amp, I_amp))
+
+    def step(self, n: int = 1):
+        self._check(self._lib.bte_step(self._h, int(n)))
+
+    def intensity(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.ncells, self.nd, self.nb))
+        self._check(self._lib.bte_get_intensity(self._h, out.ctypes.data, out.size))
+        return out
+
+    def temperature(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.ncells)
+        self._check(self._lib.bte_get_temperature(self._h, out.ctypes.data, out.size))
+        return out
+
+    def energy(self) -> float:
+        e = C.c_double()
+        self._check(self._lib.bte_get_energy(self._h, C.byref(e)))
+        return e.value
+
+    def debug_substep(self, which: int) -> np.ndarray:
+        shape = {0: (self.ncells, self.nd, self.nb), 1: (self.ncells, self.nb), 2: (self.ncells, self.nb),
+                 3: (self.ncells, self.nb)}[which]
+        out = np.empty(shape)
+        self._check(self._lib.bte_debug_substep(self._h, which, out.ctypes.data, out.size))
+        return out
+
+    def timing_enable(self, enable: bool = True, max_steps: int = 4096):
+        self._check(self._lib.bte_timing_enable(self._h, int(enable), int(max_steps)))
+
+    def timing_read(self) -> dict:
+        t = Timing()
+        self._check(self._lib.bte_timing_read(self._h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in Timing._fields_}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bte_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (rank 0), via the NCCL library PyTorch ships."""
+    import torch  # noqa: F401  (loads libnccl.so.2)
+    nccl = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+    buf = C.create_string_buffer(128)
+    st = nccl.ncclGetUniqueId(buf)
+    if st != 0:
+        raise RuntimeError(f"ncclGetUniqueId failed ({st})")
+    return buf.raw

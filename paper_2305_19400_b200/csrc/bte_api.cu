@@ -1,0 +1,853 @@
+// bte_api.cu -- C ABI (include/bte.h) and host runtime of the B200 BTE step:
+// validation, octant grouping of the direction set, geometry/coefficient
+// precompute (a0), device state, step orchestration, error latching.
+// Every step of the hot path runs in kernels.cu; this file only launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bte.h"
+#include "bte_internal.cuh"
+#include "nccl_shim.h"
+
+using namespace bte;
+
+namespace {
+
+constexpr double kHbar = 1.054571817e-34;  // J s   (CODATA 2018)
+constexpr double kKB = 1.380649e-23;       // J/K   (exact SI)
+
+// 16-point Gauss-Legendre rule on [-1, 1] (nodes ascending; literal table of
+// the standard rule, 17 significant digits).
+const double kGL16[16][2] = {
+    {-0.9894009349916499, 0.027152459411754176}, {-0.9445750230732326, 0.062253523938647456},
+    {-0.8656312023878318, 0.0951585116824926},   {-0.755404408355003, 0.12462897125553407},
+    {-0.6178762444026438, 0.1495959888165767},   {-0.45801677765722737, 0.16915651939500265},
+    {-0.2816035507792589, 0.18260341504492364},  {-0.09501250983763744, 0.18945061045506864},
+    {0.09501250983763744, 0.18945061045506864},  {0.2816035507792589, 0.18260341504492364},
+    {0.45801677765722737, 0.16915651939500265},  {0.6178762444026438, 0.1495959888165767},
+    {0.755404408355003, 0.12462897125553407},    {0.8656312023878318, 0.0951585116824926},
+    {0.9445750230732326, 0.062253523938647456},  {0.9894009349916499, 0.027152459411754176}};
+
+}  // namespace
+
+struct bte_ctx {
+  std::string err;
+  // configuration
+  bte_mesh mesh;
+  int nd = 0, nb = 0;
+  double dt = 0, T_init = 0, W = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, nranks = 1;
+  void *(*alloc)(size_t, void *) = nullptr;
+  void (*dealloc)(void *, void *) = nullptr;
+  void *alloc_ctx = nullptr;
+  std::vector<void *> allocs;
+  int64_t bytes = 0;
+  // host copies of tables
+  std::vector<double> s, w, v, bcoef;
+  int mode = 0;
+  std::vector<int> dmap, canon_d;  // d -> slot*nj+j ; slot*nj+j -> d
+  bool refl_closed[3] = {false, false, false};
+  double Tmax = 0;
+  // device
+  Geometry g{};
+  Material m{};
+  double *I[2] = {nullptr, nullptr};
+  int cur = 0;
+  double *I0c = nullptr, *beta = nullptr, *T = nullptr, *Dpart = nullptr;
+  double *gtab[6] = {nullptr};
+  int *d_dmap = nullptr, *d_canon_d = nullptr;
+  unsigned long long *d_err = nullptr;
+  int *d_step = nullptr;
+  double *staging = nullptr;
+  int64_t staging_cells = 0;
+  int seg_len = 0;
+  int64_t ncells_local = 0, ncells_global = 0;
+  int64_t steps_done = 0;
+  // timing
+  bool timing = false;
+  int64_t timing_max = 0, timing_used = 0;
+  std::vector<cudaEvent_t> ev;  // [max][6]: sweep b/e, newton b/e, bnd b/e
+  std::vector<char> ev_has_bnd;
+  bte_timing tacc{};
+  // NCCL
+  void *nccl_comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+};
+
+static bte_status fail(bte_ctx *c, bte_status st, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, BTE_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+static void *dev_alloc(bte_ctx *ctx, size_t bytes) {
+  if (bytes == 0) bytes = 256;
+  void *p = nullptr;
+  if (ctx->alloc) {
+    p = ctx->alloc(bytes, ctx->alloc_ctx);
+  } else {
+    if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+  }
+  if (p) {
+    ctx->allocs.push_back(p);
+    ctx->bytes += (int64_t)bytes;
+  }
+  return p;
+}
+
+template <typename T>
+static bte_status upload(bte_ctx *ctx, T **dst, const T *src, size_t n) {
+  *dst = (T *)dev_alloc(ctx, n * sizeof(T));
+  if (!*dst) return fail(ctx, BTE_ENOMEM, "device allocation of %zu bytes failed", n * sizeof(T));
+  CU(cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return BTE_OK;
+}
+
+static double host_beta(const bte_ctx *ctx, int b, double T) {
+  const double *q = ctx->bcoef.data() + 5 * b;
+  double r = q[0] + q[1] * T * T * T + q[2] * T * T * T * T;
+  if (q[3] != 0.0) r += q[3] / std::sinh(q[4] / T);
+  return r;
+}
+
+// positivity of the explicit update (reading #9): every coefficient of I^n in
+// I^{n+1} must be >= 0 at the hottest temperature seen.
+static bte_status check_dt(bte_ctx *ctx) {
+  const int na = ctx->mesh.dim == 3 ? 3 : 2;
+  const double D[3] = {ctx->mesh.dx, ctx->mesh.dy, ctx->mesh.dz};
+  double worst = 1e300;
+  for (int b = 0; b < ctx->nb; ++b) {
+    const double be = host_beta(ctx, b, ctx->Tmax);
+    for (int d = 0; d < ctx->nd; ++d) {
+      double k = 0;
+      for (int a = 0; a < na; ++a) k += std::fabs(ctx->s[3 * d + a]) / D[a];
+      worst = std::min(worst, 1.0 - ctx->dt * be - ctx->dt * ctx->v[b] * k);
+    }
+  }
+  if (!(worst >= 0.0))
+    return fail(ctx, BTE_EUNSTABLE,
+                "dt = %g violates the positivity bound at T = %g K (margin %g < 0)", ctx->dt,
+                ctx->Tmax, worst);
+  return BTE_OK;
+}
+
+static int64_t n_faces_global(const bte_ctx *ctx, int region) {
+  const int a = region / 2;
+  const bte_mesh &m = ctx->mesh;
+  if (a == 0) return m.ny * m.nz;
+  if (a == 1) return m.nx * m.nz;
+  return m.nx * m.ny;
+}
+
+static int octant_of(const double *s) {
+  return (s[0] < 0.0 ? 4 : 0) | (s[1] < 0.0 ? 2 : 0) | (s[2] < 0.0 ? 1 : 0);
+}
+
+static bte_status sync_check(bte_ctx *ctx) {
+  CU(cudaStreamSynchronize(ctx->stream));
+  unsigned long long key = ~0ull;
+  CU(cudaMemcpy(&key, ctx->d_err, sizeof key, cudaMemcpyDeviceToHost));
+  if (key != ~0ull) {
+    const unsigned long long step = key >> 40;
+    const int kind = (int)((key >> 36) & 0xF);
+    const unsigned long long cell = key & ((1ull << 36) - 1);
+    const unsigned long long reset = ~0ull;
+    CU(cudaMemcpy(ctx->d_err, &reset, sizeof reset, cudaMemcpyHostToDevice));
+    if (kind == ERR_NEWTON)
+      return fail(ctx, BTE_ENEWTON, "temperature Newton did not converge in %d iterations at step %llu, cell %llu",
+                  kNewtonMaxIt, step, cell);
+    return fail(ctx, BTE_ENONFINITE, "non-finite value in the temperature update at step %llu, cell %llu",
+                step, cell);
+  }
+  return BTE_OK;
+}
+
+extern "C" {
+
+const char *bte_version(void) { return "bte-b200 0.1 (sm_100a, fp64)"; }
+
+const char *bte_last_error(const bte_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands, const bte_run *run,
+                      bte_ctx **out) {
+  if (!out) return BTE_EINVAL;
+  *out = nullptr;
+  bte_ctx *ctx = new bte_ctx();
+  bte_status st = BTE_OK;
+  auto bail = [&](bte_status s) {
+    *out = ctx;  // caller reads bte_last_error, then bte_destroy
+    return s;
+  };
+  if (!mesh || !dirs || !bands || !run) return bail(fail(ctx, BTE_EINVAL, "null argument"));
+  ctx->mesh = *mesh;
+  if (mesh->dim != 2 && mesh->dim != 3) return bail(fail(ctx, BTE_EINVAL, "dim must be 2 or 3"));
+  if (mesh->nx < 1 || mesh->ny < 1 || mesh->nz < 1 || (mesh->dim == 2 && mesh->nz != 1))
+    return bail(fail(ctx, BTE_EINVAL, "bad mesh extents (dim 2 needs nz == 1)"));
+  if (!(mesh->dx > 0 && mesh->dy > 0 && mesh->dz > 0)) return bail(fail(ctx, BTE_EINVAL, "cell sizes must be > 0"));
+  if (mesh->nx > (1 << 30) || mesh->ny > (1 << 30)) return bail(fail(ctx, BTE_EINVAL, "mesh too large"));
+  if (dirs->nd < 1 || !dirs->s || !dirs->w) return bail(fail(ctx, BTE_EINVAL, "empty direction set"));
+  if (bands->nb < 1 || bands->nb > kMaxBands || !bands->v || !bands->beta_coef)
+    return bail(fail(ctx, BTE_EINVAL, "channel count must be in [1, %d]", kMaxBands));
+  if (!(run->dt > 0) || !(run->T_init > 0)) return bail(fail(ctx, BTE_EINVAL, "dt and T_init must be > 0"));
+  if (run->nranks < 1 || run->rank < 0 || run->rank >= run->nranks)
+    return bail(fail(ctx, BTE_EINVAL, "bad rank/nranks"));
+  ctx->nd = dirs->nd;
+  ctx->nb = bands->nb;
+  ctx->dt = run->dt;
+  ctx->T_init = run->T_init;
+  ctx->Tmax = run->T_init;
+  ctx->device = run->device;
+  ctx->stream = (cudaStream_t)run->stream;
+  ctx->rank = run->rank;
+  ctx->nranks = run->nranks;
+  ctx->alloc = run->alloc;
+  ctx->dealloc = run->dealloc;
+  ctx->alloc_ctx = run->alloc_ctx;
+  ctx->s.assign(dirs->s, dirs->s + 3 * dirs->nd);
+  ctx->w.assign(dirs->w, dirs->w + dirs->nd);
+  ctx->v.assign(bands->v, bands->v + bands->nb);
+  ctx->bcoef.assign(bands->beta_coef, bands->beta_coef + 5 * bands->nb);
+  ctx->mode = bands->mode;
+  for (int b = 0; b < ctx->nb; ++b) {
+    if (!(ctx->v[b] > 0)) return bail(fail(ctx, BTE_EINVAL, "group speed of channel %d must be > 0", b));
+    for (int k = 0; k < 5; ++k)
+      if (!(ctx->bcoef[5 * b + k] >= 0)) return bail(fail(ctx, BTE_EINVAL, "beta coefficients must be >= 0"));
+    if (!(host_beta(ctx, b, run->T_init) >= 0)) return bail(fail(ctx, BTE_EINVAL, "beta must be >= 0"));
+  }
+  if (bands->mode == BTE_I0_LINEAR) {
+    if (!bands->I_ref || !bands->slope) return bail(fail(ctx, BTE_EINVAL, "linear mode needs I_ref and slope"));
+  } else if (bands->mode == BTE_I0_BOSE_EINSTEIN) {
+    if (!bands->w_lo || !bands->w_hi || !bands->vs || !bands->c2 || !bands->g)
+      return bail(fail(ctx, BTE_EINVAL, "Bose-Einstein mode needs w_lo, w_hi, vs, c2, g"));
+  } else {
+    return bail(fail(ctx, BTE_EINVAL, "unknown I0 mode"));
+  }
+  double W = 0;
+  for (int d = 0; d < ctx->nd; ++d) {
+    if (!(ctx->w[d] > 0)) return bail(fail(ctx, BTE_EINVAL, "direction weights must be > 0"));
+    W += ctx->w[d];
+  }
+  ctx->W = W;
+
+  // ---- octant grouping: slots = non-empty octants ascending
+  int count[8] = {0};
+  std::vector<int> oct(ctx->nd), jidx(ctx->nd);
+  for (int d = 0; d < ctx->nd; ++d) {
+    oct[d] = octant_of(&ctx->s[3 * d]);
+    jidx[d] = count[oct[d]]++;
+  }
+  int slot_of[8];
+  int nslot = 0, nj = -1;
+  for (int o = 0; o < 8; ++o) {
+    slot_of[o] = -1;
+    if (count[o]) {
+      if (nj < 0) nj = count[o];
+      if (count[o] != nj)
+        return bail(fail(ctx, BTE_EINVAL, "every non-empty octant must hold the same number of directions"));
+      ctx->g.slot_oct[nslot] = o;
+      slot_of[o] = nslot++;
+    }
+  }
+  ctx->dmap.resize(ctx->nd);
+  ctx->canon_d.resize(ctx->nd);
+  for (int d = 0; d < ctx->nd; ++d) {
+    const int sj = slot_of[oct[d]] * nj + jidx[d];
+    ctx->dmap[d] = sj;
+    ctx->canon_d[sj] = d;
+  }
+
+  // ---- geometry / slab decomposition along the slowest axis
+  Geometry &g = ctx->g;
+  g.dim = mesh->dim;
+  g.nx = (int)mesh->nx;
+  g.ny = mesh->dim == 3 ? (int)mesh->ny : 1;
+  g.ncross = mesh->dim == 3 ? (int)(mesh->nx * mesh->ny) : (int)mesh->nx;
+  const int64_t nm = mesh->dim == 3 ? mesh->nz : mesh->ny;
+  g.nplanes_global = nm;
+  {
+    const int64_t P = ctx->nranks, r = ctx->rank;
+    const int64_t base = nm / P, rem = nm % P;
+    const int64_t n_r = base + (r < rem ? 1 : 0);
+    const int64_t m0 = r * base + std::min<int64_t>(r, rem);
+    if (n_r < 1) return bail(fail(ctx, BTE_EINVAL, "more ranks than planes along the slab axis"));
+    g.nplanes = (int)n_r;
+    g.m0 = m0;
+  }
+  g.plane_off = ctx->nranks > 1 ? 1 : 0;
+  g.has_lo_wall = (ctx->rank == 0) ? 1 : 0;
+  g.has_hi_wall = (ctx->rank == ctx->nranks - 1) ? 1 : 0;
+  g.nslot = nslot;
+  g.nj = nj;
+  g.nb = ctx->nb;
+  g.E = nj * ctx->nb;
+  g.plane_stride = (int64_t)g.ncross * g.E;
+  g.slot_stride = (int64_t)(g.nplanes + 2 * g.plane_off) * g.plane_stride;
+  ctx->ncells_local = (int64_t)g.nplanes * g.ncross;
+  ctx->ncells_global = mesh->nx * mesh->ny * mesh->nz;
+
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return bail(fail(ctx, BTE_ECUDA, "cudaSetDevice(%d) failed", ctx->device));
+
+  // ---- per-(slot, j) tables
+  const double Dl[3] = {mesh->dx, mesh->dy, mesh->dz};
+  const int nsj = nslot * nj;
+  std::vector<double> coef(4 * nsj), ws(3 * nsj, 0.0);
+  std::vector<int64_t> roff(3 * nsj, 0);
+  for (int sj = 0; sj < nsj; ++sj) {
+    const int d = ctx->canon_d[sj];
+    for (int a = 0; a < 3; ++a) {
+      coef[4 * sj + a] = ctx->dt * std::fabs(ctx->s[3 * d + a]) / Dl[a];
+      ws[a * nsj + sj] = ctx->w[d] * std::fabs(ctx->s[3 * d + a]);
+    }
+    coef[4 * sj + 3] = ctx->w[d];
+  }
+  for (int a = 0; a < 3; ++a) {
+    bool closed = true;
+    for (int d = 0; d < ctx->nd && closed; ++d) {
+      double t[3] = {ctx->s[3 * d], ctx->s[3 * d + 1], ctx->s[3 * d + 2]};
+      t[a] = -t[a];
+      int hit = -1;
+      for (int e = 0; e < ctx->nd; ++e)
+        if (ctx->s[3 * e] == t[0] && ctx->s[3 * e + 1] == t[1] && ctx->s[3 * e + 2] == t[2] && ctx->w[e] == ctx->w[d]) {
+          hit = e;
+          break;
+        }
+      if (hit < 0) {
+        closed = false;
+        break;
+      }
+      const int sj = ctx->dmap[d], sje = ctx->dmap[hit];
+      roff[a * nsj + sj] = (int64_t)(sje / nj) * g.slot_stride + (int64_t)(sje % nj) * ctx->nb;
+    }
+    ctx->refl_closed[a] = closed;
+  }
+
+  // ---- material tables: A_bj, X_bj (Bose-Einstein, reading #1)
+  std::vector<double> A(ctx->nb * kNGL, 0.0), X(ctx->nb * kNGL, 0.0);
+  std::vector<double> Iref(ctx->nb, 0.0), slope(ctx->nb, 0.0);
+  if (bands->mode == BTE_I0_BOSE_EINSTEIN) {
+    for (int b = 0; b < ctx->nb; ++b) {
+      const double lo = bands->w_lo[b], hi = bands->w_hi[b];
+      if (!(hi > lo && lo >= 0)) return bail(fail(ctx, BTE_EINVAL, "band %d: need 0 <= w_lo < w_hi", b));
+      const double half = 0.5 * (hi - lo), mid = 0.5 * (hi + lo);
+      const double pref = bands->g[b] * kHbar / (8.0 * M_PI * M_PI * M_PI) * half;
+      for (int j = 0; j < kNGL; ++j) {
+        const double w = mid + half * kGL16[j][0];
+        const double vs = bands->vs[b], c2 = bands->c2[b];
+        const double disc = vs * vs + 4.0 * c2 * w;
+        if (!(disc > 0)) return bail(fail(ctx, BTE_EINVAL, "band %d beyond the dispersion maximum", b));
+        const double k = c2 == 0.0 ? w / vs : 2.0 * w / (vs + std::sqrt(disc));
+        A[b * kNGL + j] = pref * kGL16[j][1] * w * k * k;
+        X[b * kNGL + j] = kHbar * w / kKB;
+      }
+    }
+  } else {
+    for (int b = 0; b < ctx->nb; ++b) {
+      Iref[b] = bands->I_ref[b];
+      slope[b] = bands->slope[b];
+    }
+  }
+
+  if ((st = check_dt(ctx)) != BTE_OK) return bail(st);
+
+  // ---- device allocations
+  double *d_coef, *d_ws, *d_v, *d_bc, *d_A, *d_X, *d_Iref, *d_slope;
+  int64_t *d_roff;
+  if ((st = upload(ctx, &d_coef, coef.data(), coef.size()))) return bail(st);
+  if ((st = upload(ctx, &d_ws, ws.data(), ws.size()))) return bail(st);
+  if ((st = upload(ctx, &d_roff, roff.data(), roff.size()))) return bail(st);
+  if ((st = upload(ctx, &d_v, ctx->v.data(), ctx->v.size()))) return bail(st);
+  if ((st = upload(ctx, &d_bc, ctx->bcoef.data(), ctx->bcoef.size()))) return bail(st);
+  if ((st = upload(ctx, &d_A, A.data(), A.size()))) return bail(st);
+  if ((st = upload(ctx, &d_X, X.data(), X.size()))) return bail(st);
+  if ((st = upload(ctx, &d_Iref, Iref.data(), Iref.size()))) return bail(st);
+  if ((st = upload(ctx, &d_slope, slope.data(), slope.size()))) return bail(st);
+  if ((st = upload(ctx, &ctx->d_dmap, ctx->dmap.data(), ctx->dmap.size()))) return bail(st);
+  if ((st = upload(ctx, &ctx->d_canon_d, ctx->canon_d.data(), ctx->canon_d.size()))) return bail(st);
+  g.coef = d_coef;
+  g.ws = d_ws;
+  g.refl_off = d_roff;
+  ctx->m.nb = ctx->nb;
+  ctx->m.mode = bands->mode;
+  ctx->m.v = d_v;
+  ctx->m.bcoef = d_bc;
+  ctx->m.I_ref = d_Iref;
+  ctx->m.slope = d_slope;
+  ctx->m.T_ref = bands->T_ref;
+  ctx->m.A = d_A;
+  ctx->m.X = d_X;
+
+  const size_t ibytes = (size_t)g.slot_stride * nslot * sizeof(double);
+  for (int k = 0; k < 2; ++k) {
+    ctx->I[k] = (double *)dev_alloc(ctx, ibytes);
+    if (!ctx->I[k]) return bail(fail(ctx, BTE_ENOMEM, "cannot allocate the intensity buffer (%zu bytes)", ibytes));
+    CU(cudaMemsetAsync(ctx->I[k], 0, ibytes, ctx->stream));
+  }
+  const int64_t ncl = ctx->ncells_local;
+  ctx->I0c = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+  ctx->beta = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+  ctx->T = (double *)dev_alloc(ctx, ncl * sizeof(double));
+  ctx->Dpart = (double *)dev_alloc(ctx, ncl * nslot * ctx->nb * sizeof(double));
+  ctx->d_err = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
+  ctx->d_step = (int *)dev_alloc(ctx, sizeof(int));
+  if (!ctx->I0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err || !ctx->d_step)
+    return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
+  CU(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), ctx->stream));
+  CU(cudaMemsetAsync(ctx->d_step, 0, sizeof(int), ctx->stream));
+  // staging for host <-> device state transfers (canonical order), <= 256 MB
+  const int64_t per_cell = (int64_t)ctx->nd * ctx->nb * sizeof(double);
+  ctx->staging_cells = std::max<int64_t>(1, std::min<int64_t>(ncl, (256ll << 20) / per_cell));
+  ctx->staging = (double *)dev_alloc(ctx, ctx->staging_cells * per_cell);
+  if (!ctx->staging) return bail(fail(ctx, BTE_ENOMEM, "staging allocation failed"));
+  for (int r = 0; r < 6; ++r) {
+    g.kind[r] = ctx->refl_closed[r / 2] ? BC_SPEC : BC_DIFF;
+    const int64_t nf = n_faces_global(ctx, r);
+    ctx->gtab[r] = (double *)dev_alloc(ctx, nf * ctx->nb * sizeof(double));
+    if (!ctx->gtab[r]) return bail(fail(ctx, BTE_ENOMEM, "ghost table allocation failed"));
+    g.gtab[r] = ctx->gtab[r];
+    // diffuse denominator: sum over incoming directions of w|s_a| (octant tree)
+    const int a = r / 2;
+    const double sg = (r & 1) ? 1.0 : -1.0;
+    double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int d = 0; d < ctx->nd; ++d) {
+      const double sa = ctx->s[3 * d + a];
+      if (sg * sa < 0.0) q[octant_of(&ctx->s[3 * d])] += ctx->w[d] * std::fabs(sa);
+    }
+    g.diff_den[r] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+  }
+  // segment length along the march axis: enough CTAs for >= ~16 per SM
+  {
+    const int64_t cols = (int64_t)g.ncross * nslot;
+    int nseg = (int)std::max<int64_t>(1, (148 * 16 + cols - 1) / cols);
+    nseg = std::min(nseg, std::max(1, g.nplanes / 8));
+    ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
+  }
+
+  // ---- multi-GPU communicator
+  if (ctx->nranks > 1) {
+    if (!run->nccl_id) return bail(fail(ctx, BTE_EINVAL, "nranks > 1 needs an nccl_id"));
+    std::string emsg;
+    if (nccl_shim_init(&ctx->nccl_comm, run->nccl_id, ctx->nranks, ctx->rank, &emsg) != 0)
+      return bail(fail(ctx, BTE_ENCCL, "NCCL init failed: %s", emsg.c_str()));
+    CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  }
+
+  // ---- initial state: equilibrium at T_init
+  std::vector<double> T0(ncl, ctx->T_init);
+  CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->beta, ctx->stream));
+  CU(launch_fill_equilibrium(g, ctx->I0c, ctx->I[0], ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->cur = 0;
+  *out = ctx;
+  return BTE_OK;
+}
+
+bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, double T_uniform) {
+  if (!ctx) return BTE_EINVAL;
+  const int nreg = ctx->mesh.dim == 3 ? 6 : 4;
+  if (region < 0 || region >= nreg) return fail(ctx, BTE_EINVAL, "region %d out of range", region);
+  if (kind == BTE_BC_SPECULAR) {
+    if (!ctx->refl_closed[region / 2])
+      return fail(ctx, BTE_ENOTCLOSED, "specular wall %d: direction set is not closed under the axis-%d reflection",
+                  region, region / 2);
+  } else if (kind == BTE_BC_ISOTHERMAL) {
+    const int64_t nf = n_faces_global(ctx, region);
+    std::vector<double> Tw(nf, T_uniform);
+    if (T_wall) std::copy(T_wall, T_wall + nf, Tw.begin());
+    double tmax = ctx->Tmax;
+    for (double t : Tw) {
+      if (!(t > 0)) return fail(ctx, BTE_EINVAL, "wall temperatures must be > 0");
+      tmax = std::max(tmax, t);
+    }
+    const double old = ctx->Tmax;
+    ctx->Tmax = tmax;
+    bte_status st = check_dt(ctx);
+    if (st) {
+      ctx->Tmax = old;
+      return st;
+    }
+    double *d_Tw = nullptr;
+    CU(cudaMalloc(&d_Tw, nf * sizeof(double)));
+    CU(cudaMemcpyAsync(d_Tw, Tw.data(), nf * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(launch_iso_table(ctx->m, d_Tw, nf, ctx->gtab[region], ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFree(d_Tw));
+  } else if (kind == BTE_BC_DIFFUSE) {
+    if (!(ctx->g.diff_den[region] > 0))
+      return fail(ctx, BTE_EINVAL, "diffuse wall %d: no direction crosses it", region);
+  } else {
+    return fail(ctx, BTE_EINVAL, "unknown boundary kind %d", kind);
+  }
+  ctx->g.kind[region] = kind;
+  return BTE_OK;
+}
+
+static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
+  const Geometry &g = ctx->g;
+  const int64_t per_cell = (int64_t)ctx->nd * ctx->nb;
+  for (int64_t c0 = 0; c0 < ctx->ncells_local; c0 += ctx->staging_cells) {
+    const int64_t n = std::min(ctx->staging_cells, ctx->ncells_local - c0);
+    if (to_device) {
+      CU(cudaMemcpyAsync(ctx->staging, host + c0 * per_cell, n * per_cell * sizeof(double), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CU(launch_permute(g, ctx->d_dmap, ctx->nd, ctx->staging, c0, n, ctx->I[ctx->cur], 1, ctx->stream));
+    } else {
+      CU(launch_permute(g, ctx->d_dmap, ctx->nd, ctx->staging, c0, n, ctx->I[ctx->cur], 0, ctx->stream));
+      CU(cudaMemcpyAsync(host + c0 * per_cell, ctx->staging, n * per_cell * sizeof(double), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    }
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BTE_OK;
+}
+
+static bte_status run_newton(bte_ctx *ctx, const int *step_ctr);
+
+bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
+  if (!ctx) return BTE_EINVAL;
+  if (!I && !T) return fail(ctx, BTE_EINVAL, "set_state needs I or T");
+  const int64_t ncl = ctx->ncells_local;
+  bte_status st;
+  if (T) {
+    double tmax = ctx->Tmax;
+    for (int64_t c = 0; c < ncl; ++c) {
+      if (!(T[c] > 0) || !std::isfinite(T[c])) return fail(ctx, BTE_EINVAL, "T must be finite and > 0");
+      tmax = std::max(tmax, T[c]);
+    }
+    const double old = ctx->Tmax;
+    ctx->Tmax = tmax;
+    if ((st = check_dt(ctx))) {
+      ctx->Tmax = old;
+      return st;
+    }
+    CU(cudaMemcpyAsync(ctx->T, T, ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    std::vector<double> T0(ncl, ctx->T_init);
+    CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->beta, ctx->stream));
+  if (I) {
+    if ((st = transfer_I(ctx, const_cast<double *>(I), 1))) return st;
+  } else {
+    CU(launch_fill_equilibrium(ctx->g, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
+  }
+  if (I && !T) {
+    // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
+    // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
+    CU(launch_dpart_from_I(ctx->g, ctx->I[ctx->cur], ctx->I0c, ctx->Dpart, ctx->stream));
+    if ((st = run_newton(ctx, nullptr))) return st;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return sync_check(ctx);
+}
+
+bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], double T_mean, double T_amp,
+                           double I_amp) {
+  if (!ctx || !phase) return BTE_EINVAL;
+  const double old = ctx->Tmax;
+  ctx->Tmax = std::max(ctx->Tmax, T_mean + std::fabs(T_amp));
+  bte_status st = check_dt(ctx);
+  if (st) {
+    ctx->Tmax = old;
+    return st;
+  }
+  if (!(T_mean - std::fabs(T_amp) > 0)) return fail(ctx, BTE_EINVAL, "random start would give T <= 0");
+  const bte_mesh &m = ctx->mesh;
+  CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
+  CU(launch_refresh(ctx->m, ctx->T, ctx->ncells_local, ctx->I0c, ctx->beta, ctx->stream));
+  CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BTE_OK;
+}
+
+// ---- the step
+
+static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
+  const Geometry &g = ctx->g;
+  const int nreg = g.dim == 3 ? 6 : 4;
+  int n = 0;
+  for (int r = 0; r < nreg; ++r) {
+    if (g.kind[r] != BC_DIFF) continue;
+    const int a = r / 2;
+    if (a == g.dim - 1 && !((r & 1) ? g.has_hi_wall : g.has_lo_wall)) continue;
+    CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
+    ++n;
+  }
+  ctx->tacc.launches += n;
+  ctx->tacc.boundary_launches += n;
+  return BTE_OK;
+}
+
+static int n_diffuse(const bte_ctx *ctx) {
+  int n = 0;
+  for (int r = 0; r < (ctx->g.dim == 3 ? 6 : 4); ++r) n += ctx->g.kind[r] == BC_DIFF;
+  return n;
+}
+
+static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, int *step_ctr) {
+  SweepArgs a;
+  a.g = ctx->g;
+  a.Iin = Iin;
+  a.Iout = Iout;
+  a.I0c = ctx->I0c;
+  a.beta = ctx->beta;
+  a.Dpart = ctx->Dpart;
+  a.v = ctx->m.v;
+  a.dt = ctx->dt;
+  a.seg_len = ctx->seg_len;
+  a.step_ctr = step_ctr;
+  CU(launch_sweep(a, ctx->stream));
+  ctx->tacc.launches++;
+  ctx->tacc.sweep_launches++;
+  return BTE_OK;
+}
+
+static bte_status run_newton(bte_ctx *ctx, const int *step_ctr) {
+  NewtonArgs a;
+  a.m = ctx->m;
+  a.Dpart = ctx->Dpart;
+  a.T = ctx->T;
+  a.I0c = ctx->I0c;
+  a.beta = ctx->beta;
+  a.nslot = ctx->g.nslot;
+  a.nb = ctx->nb;
+  for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
+  a.W = ctx->W;
+  a.ncells = ctx->ncells_local;
+  a.cell0_global = ctx->g.m0 * ctx->g.ncross;
+  a.err = ctx->d_err;
+  a.step_ctr = step_ctr;
+  CU(launch_newton(a, ctx->stream));
+  ctx->tacc.launches++;
+  ctx->tacc.newton_launches++;
+  return BTE_OK;
+}
+
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
+
+bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
+  if (!ctx) return BTE_EINVAL;
+  if (nsteps < 0) return fail(ctx, BTE_EINVAL, "nsteps < 0");
+  const bool has_bnd = n_diffuse(ctx) > 0;
+  for (int64_t s = 0; s < nsteps; ++s) {
+    double *Iin = ctx->I[ctx->cur];
+    double *Iout = ctx->I[1 - ctx->cur];
+    const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
+    cudaEvent_t *ev = t ? &ctx->ev[6 * ctx->timing_used] : nullptr;
+    bte_status st;
+    if (has_bnd) {
+      if (t) CU(cudaEventRecord(ev[4], ctx->stream));
+      if ((st = launch_boundary(ctx, Iin))) return st;
+      if (t) CU(cudaEventRecord(ev[5], ctx->stream));
+    }
+    if (t) CU(cudaEventRecord(ev[0], ctx->stream));
+    if ((st = launch_sweep_step(ctx, Iin, Iout, ctx->d_step))) return st;
+    if (t) CU(cudaEventRecord(ev[1], ctx->stream));
+    if (ctx->nranks > 1 && (st = halo_exchange(ctx, Iout))) return st;
+    if (t) CU(cudaEventRecord(ev[2], ctx->stream));
+    if ((st = run_newton(ctx, ctx->d_step))) return st;
+    if (t) {
+      CU(cudaEventRecord(ev[3], ctx->stream));
+      ctx->ev_has_bnd[ctx->timing_used] = has_bnd;
+      ctx->timing_used++;
+    }
+    ctx->cur = 1 - ctx->cur;
+    ctx->steps_done++;
+  }
+  return sync_check(ctx);
+}
+
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf) {
+  // a5: send the owned boundary planes of the octants whose march-axis upwind
+  // side points at the neighbour, receive into the halo planes.
+  const Geometry &g = ctx->g;
+  const int mbit = g.dim == 3 ? 1 : 2;
+  std::string emsg;
+  if (nccl_shim_group_start(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+  for (int sl = 0; sl < g.nslot; ++sl) {
+    double *base = Ibuf + (int64_t)sl * g.slot_stride;
+    const bool mneg = g.slot_oct[sl] & mbit;
+    const size_t n = (size_t)g.plane_stride;
+    if (!mneg) {
+      // upwind is below: send my last plane up, receive my low halo from below
+      if (ctx->rank + 1 < ctx->nranks &&
+          nccl_shim_send(ctx->nccl_comm, base + (int64_t)(g.nplanes - 1 + g.plane_off) * g.plane_stride, n,
+                         ctx->rank + 1, ctx->stream, &emsg))
+        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+      if (ctx->rank > 0 && nccl_shim_recv(ctx->nccl_comm, base, n, ctx->rank - 1, ctx->stream, &emsg))
+        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+    } else {
+      if (ctx->rank > 0 &&
+          nccl_shim_send(ctx->nccl_comm, base + (int64_t)g.plane_off * g.plane_stride, n, ctx->rank - 1, ctx->stream,
+                         &emsg))
+        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+      if (ctx->rank + 1 < ctx->nranks &&
+          nccl_shim_recv(ctx->nccl_comm, base + (int64_t)(g.nplanes + g.plane_off) * g.plane_stride, n, ctx->rank + 1,
+                         ctx->stream, &emsg))
+        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+    }
+  }
+  if (nccl_shim_group_end(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+  return BTE_OK;
+}
+
+bte_status bte_get_intensity(bte_ctx *ctx, double *out, size_t count) {
+  if (!ctx || !out) return BTE_EINVAL;
+  if (count != (size_t)ctx->ncells_local * ctx->nd * ctx->nb)
+    return fail(ctx, BTE_EINVAL, "intensity count %zu != %lld", count,
+                (long long)(ctx->ncells_local * ctx->nd * ctx->nb));
+  return transfer_I(ctx, out, 0);
+}
+
+bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count) {
+  if (!ctx || !out) return BTE_EINVAL;
+  if (count != (size_t)ctx->ncells_local) return fail(ctx, BTE_EINVAL, "temperature count mismatch");
+  CU(cudaMemcpyAsync(out, ctx->T, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BTE_OK;
+}
+
+bte_status bte_get_energy(bte_ctx *ctx, double *E) {
+  if (!ctx || !E) return BTE_EINVAL;
+  const int64_t ncl = ctx->ncells_local;
+  double *d_E = nullptr;
+  CU(cudaMalloc(&d_E, ncl * sizeof(double)));
+  CU(launch_energy(ctx->g, ctx->I[ctx->cur], ctx->m.v, d_E, ctx->stream));
+  std::vector<double> h(ncl);
+  CU(cudaMemcpyAsync(h.data(), d_E, ncl * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaFree(d_E));
+  const bte_mesh &m = ctx->mesh;
+  const double V = m.dx * m.dy * m.dz;
+  double s = 0, comp = 0;  // Kahan
+  for (double x : h) {
+    const double y = x - comp;
+    const double t = s + y;
+    comp = (t - s) - y;
+    s = t;
+  }
+  *E = V * s;
+  return BTE_OK;
+}
+
+bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count) {
+  if (!ctx || !out) return BTE_EINVAL;
+  const int64_t ncl = ctx->ncells_local;
+  bte_status st;
+  if (which == 2 || which == 3) {
+    if (count != (size_t)(ncl * ctx->nb)) return fail(ctx, BTE_EINVAL, "count mismatch");
+    CU(cudaMemcpy(out, which == 2 ? ctx->I0c : ctx->beta, count * sizeof(double), cudaMemcpyDeviceToHost));
+    return BTE_OK;
+  }
+  if (which != 0 && which != 1) return fail(ctx, BTE_EINVAL, "which must be 0..3");
+  const size_t want = which == 0 ? (size_t)ncl * ctx->nd * ctx->nb : (size_t)ncl * ctx->nb;
+  if (count != want) return fail(ctx, BTE_EINVAL, "count mismatch");
+  double *Iin = ctx->I[ctx->cur];
+  double *Iout = ctx->I[1 - ctx->cur];
+  if (n_diffuse(ctx) && (st = launch_boundary(ctx, Iin))) return st;
+  if ((st = launch_sweep_step(ctx, Iin, Iout, nullptr))) return st;
+  if (which == 0) {
+    ctx->cur = 1 - ctx->cur;  // read the swept buffer, then restore
+    st = transfer_I(ctx, out, 0);
+    ctx->cur = 1 - ctx->cur;
+    return st;
+  }
+  double *d_D = nullptr;
+  CU(cudaMalloc(&d_D, want * sizeof(double)));
+  CU(launch_octant_tree_g(ctx->g, ctx->Dpart, ncl, d_D, ctx->stream));
+  CU(cudaMemcpyAsync(out, d_D, want * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaFree(d_D));
+  return BTE_OK;
+}
+
+bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps) {
+  if (!ctx) return BTE_EINVAL;
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  ctx->ev.clear();
+  ctx->tacc = bte_timing{};
+  ctx->timing = enable != 0;
+  ctx->timing_used = 0;
+  ctx->timing_max = enable ? max_steps : 0;
+  if (enable) {
+    ctx->ev.resize(6 * max_steps);
+    ctx->ev_has_bnd.assign(max_steps, 0);
+    for (auto &e : ctx->ev) CU(cudaEventCreate(&e));
+  }
+  return BTE_OK;
+}
+
+bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out) {
+  if (!ctx || !out) return BTE_EINVAL;
+  CU(cudaStreamSynchronize(ctx->stream));
+  bte_timing t = ctx->tacc;
+  t.steps = ctx->timing_used;
+  t.sweep_ms = t.newton_ms = t.boundary_ms = t.halo_ms = 0;
+  for (int64_t i = 0; i < ctx->timing_used; ++i) {
+    float ms;
+    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i], ctx->ev[6 * i + 1]));
+    t.sweep_ms += ms;
+    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 2], ctx->ev[6 * i + 3]));
+    t.newton_ms += ms;
+    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 1], ctx->ev[6 * i + 2]));
+    t.halo_ms += ms;
+    if (ctx->ev_has_bnd[i]) {
+      CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 4], ctx->ev[6 * i + 5]));
+      t.boundary_ms += ms;
+    }
+  }
+  *out = t;
+  return BTE_OK;
+}
+
+bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
+  if (!ctx || !out) return BTE_EINVAL;
+  out->ncells_local = ctx->ncells_local;
+  out->ncells_global = ctx->ncells_global;
+  out->z0 = ctx->g.m0;
+  out->nz_local = ctx->g.nplanes;
+  out->nd = ctx->nd;
+  out->nb = ctx->nb;
+  out->n_octants = ctx->g.nslot;
+  out->nj = ctx->g.nj;
+  out->bytes_state = ctx->bytes;
+  return BTE_OK;
+}
+
+void bte_destroy(bte_ctx *ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->nccl_comm) nccl_shim_destroy(ctx->nccl_comm);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  for (void *p : ctx->allocs) {
+    if (ctx->dealloc)
+      ctx->dealloc(p, ctx->alloc_ctx);
+    else
+      cudaFree(p);
+  }
+  delete ctx;
+}
+
+}  // extern "C"

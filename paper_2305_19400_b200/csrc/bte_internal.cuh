@@ -1,0 +1,117 @@
+// bte_internal.cuh -- device-side data layout and kernel interfaces of the
+// B200 BTE step.  See DESIGN.md "Data layout in HBM" and include/bte.h.
+//
+// Layout (octant-major, band-innermost):
+//   I[slot][plane][cross cell][j][b]   fp64
+//     slot  = index of a non-empty octant (sign pattern of s_d), 0..nslot-1
+//     plane = position along the slowest ("march") axis: z for dim 3, y for dim 2;
+//             when nranks > 1 each slot holds nplanes+2 planes (one halo plane
+//             on each side), else nplanes
+//     cross = x + nx*y (dim 3) or x (dim 2)
+//     j     = direction index inside the octant, b = channel
+//   E = nj*nb doubles (16 KB at 50 x 40) are contiguous per (slot, cell).
+//   I0c[c][b], beta[c][b], T[c], Dpart[c][slot][b] over the rank's own cells.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bte {
+
+constexpr int kNGL = 16;        // Gauss-Legendre nodes per channel (reading #1)
+constexpr int kMaxBands = 128;  // channels per context
+constexpr int kMaxSlots = 8;
+constexpr double kTlo = 1.0, kThi = 5000.0;  // Newton bracket (reading #18)
+constexpr int kNewtonMaxIt = 50;
+constexpr double kNewtonRtol = 1e-13;
+
+enum { BC_ISO = 0, BC_SPEC = 1, BC_DIFF = 2 };
+enum { ERR_NONE = 0, ERR_NEWTON = 7, ERR_NONFINITE = 8 };
+
+// Channel model tables (device pointers).
+struct Material {
+  int nb;
+  int mode;               // 0 linear, 1 Bose-Einstein
+  const double *v;        // [nb]
+  const double *bcoef;    // [nb][5]
+  const double *I_ref, *slope;
+  double T_ref;
+  const double *A;        // [nb][16] g hbar/(8pi^3) * half * wgl_j * w_j * k_j^2
+  const double *X;        // [nb][16] hbar w_j / kB
+};
+
+struct Geometry {
+  int dim;
+  int nx, ny;             // cross extents (dim 2: ny = 1 in the cross sense)
+  int ncross;             // cells per plane
+  int nplanes;            // owned planes along the march axis
+  int64_t m0;             // global index of the first owned plane
+  int64_t nplanes_global;
+  int plane_off;          // 1 when halo planes are stored, else 0
+  int64_t plane_stride;   // doubles per plane (ncross * E)
+  int64_t slot_stride;    // doubles per slot
+  int nslot, nj, nb, E;
+  int slot_oct[kMaxSlots];
+  int has_lo_wall, has_hi_wall;  // march-axis walls exist on this rank
+  // per-(slot, j) coefficient table [nslot*nj][4]: dt|s_x|/dx, dt|s_y|/dy, dt|s_z|/dz, w
+  const double *coef;
+  // reflected element offset for specular ghosts: [3][nslot*nj] -> slot_r*slot_stride + jr*nb
+  const int64_t *refl_off;
+  // per-(slot, j) weight times |s_a| for the diffuse numerator: [3][nslot*nj]
+  const double *ws;
+  int kind[6];
+  const double *gtab[6];  // iso / diffuse ghost tables [face][nb] (global face index)
+  double diff_den[6];
+};
+
+struct SweepArgs {
+  Geometry g;
+  const double *Iin;
+  double *Iout;
+  const double *I0c, *beta;
+  double *Dpart;
+  const double *v;
+  double dt;
+  int seg_len;            // cells per CTA along the march axis
+  int jpt;                // directions per thread (set by launch_sweep)
+  int *step_ctr;
+};
+
+struct NewtonArgs {
+  Material m;
+  const double *Dpart;
+  double *T, *I0c, *beta;
+  int nslot, nb;
+  int slot_oct[kMaxSlots];
+  double W;
+  int64_t ncells, cell0_global;
+  unsigned long long *err;
+  const int *step_ctr;
+};
+
+// kernels / launchers (kernels.cu)
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s);
+cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
+cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
+                           cudaStream_t s);
+cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,
+                             cudaStream_t s);
+cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c,
+                           double *beta, cudaStream_t s);
+cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I,
+                                    cudaStream_t s);
+cudaError_t launch_permute(const Geometry &g, const int *dmap, int nd, const double *canon,
+                           int64_t c0, int64_t nc_chunk, double *I, int to_layout,
+                           cudaStream_t s);
+cudaError_t launch_random_T(const Geometry &g, int64_t nz_cross_dummy, double dx, double dy,
+                            double dz, const double *phase, double T_mean, double T_amp,
+                            double *T, cudaStream_t s);
+cudaError_t launch_random_I(const Geometry &g, const int *canon_d, int nd, uint64_t seed,
+                            double I_amp, const double *I0c, double *I, cudaStream_t s);
+cudaError_t launch_octant_tree_g(const Geometry &g, const double *Dpart, int64_t nc, double *D,
+                                 cudaStream_t s);
+cudaError_t launch_dpart_from_I(const Geometry &g, const double *I, const double *I0c, double *Dpart,
+                               cudaStream_t s);
+cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, double *Ec,
+                          cudaStream_t s);
+
+}  // namespace bte

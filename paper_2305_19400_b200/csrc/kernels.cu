@@ -1,0 +1,682 @@
+// kernels.cu -- sm_100a kernels of the explicit phonon-BTE step (arXiv 2305.19400).
+//
+//   k_sweep     a1 (specular/isothermal ghosts inline) + a2: fused upwind flux +
+//               relaxation update (Eq. 5 with forward Euler, P:L378-387,
+//               P:L159-184) and the per-(cell, octant, channel) partial
+//               sum_j w_j (I0c - I^{n+1}) of a3.  HBM-bound: 16 B/DOF.
+//   k_diffuse   a1 for diffuse-adiabatic walls (reading #11).
+//   k_newton    a3 (octant tree) + a4: per-cell Newton for T^{n+1} against the
+//               Bose-Einstein band intensity, refresh of I0c and beta
+//               (P:L277-298).  FP64-ALU-bound (expm1).
+//   helpers     layout permutation, equilibrium fill, random start, tables.
+//
+// No tensor cores: nothing on this path is a dense contraction.
+#include <cstdint>
+#include <cstdio>
+#include <algorithm>
+
+#include "bte_internal.cuh"
+
+namespace bte {
+
+// ---------------------------------------------------------------- material
+
+__device__ __forceinline__ double beta_of_T(const double *__restrict__ bc, int b, double T) {
+  const double *q = bc + 5 * b;
+  const double T2 = T * T;
+  double r = q[0] + q[1] * (T2 * T) + q[2] * (T2 * T2);
+  if (q[3] != 0.0) r += q[3] / sinh(q[4] / T);
+  return r;
+}
+
+// I0_b(T) and dI0_b/dT (reading #1).  BE: sum_j A_bj / expm1(X_bj / T),
+// derivative term A/em1 * (X/T)/T * (1 + 1/em1) = integrand * x/T * e^x/(e^x-1).
+__device__ __forceinline__ double I0_of_T(const Material &m, int b, double T, double *dI0) {
+  if (m.mode == 0) {
+    if (dI0) *dI0 = m.slope[b];
+    return m.I_ref[b] + m.slope[b] * (T - m.T_ref);
+  }
+  const double *A = m.A + b * kNGL;
+  const double *X = m.X + b * kNGL;
+  const double rT = 1.0 / T;
+  double s = 0.0, ds = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kNGL; ++j) {
+    const double x = X[j] * rT;
+    const double em1 = expm1(x);
+    const double r = 1.0 / em1;
+    const double f = A[j] * r;
+    s += f;
+    ds += f * x * (1.0 + r);
+  }
+  if (dI0) *dI0 = ds * rT;
+  return s;
+}
+
+// ---------------------------------------------------------------- sweep
+
+__device__ __forceinline__ double ldg(const double *p) { return __ldg(p); }
+
+// Ghost intensity on a wall for element (slot, j, b) of the cell at `cell_base`
+// ((plane + plane_off)*plane_stride + cross*E) -- Eq. 6.
+__device__ __forceinline__ double ghost_value(const Geometry &g, const double *__restrict__ Iin,
+                                              int region, int64_t face, int64_t cell_base, int slot,
+                                              int j, int b) {
+  const int kind = g.kind[region];
+  if (kind == BC_SPEC) {
+    const int axis = region >> 1;
+    const int64_t off = g.refl_off[(int64_t)axis * g.nslot * g.nj + slot * g.nj + j];
+    return ldg(Iin + off + cell_base + b);
+  }
+  return ldg(g.gtab[region] + face * g.nb + b);
+}
+
+// One CTA = one (cross cell, octant slot, segment of the march axis).  The CTA
+// walks its column in the upwind-to-downwind order of that octant, so the
+// march-axis upwind value is the previous iteration's I^n kept in registers.
+// Thread (grp, b) owns channel b and the directions j in [grp*jpt, grp*jpt+jpt)
+// of the octant: consecutive threads touch consecutive channels of one
+// direction (coalesced 8*nb-byte rows), I0c/beta are loaded once per cell per
+// thread, and the octant partial sum over j accumulates in a register before
+// a JG-way fixed-order smem combine.
+template <int DIM, int JMAX>
+__global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
+  extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb]
+  const Geometry &g = A.g;
+  const int nb = g.nb, nj = g.nj, E = g.E;
+  const int tid = threadIdx.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = blockDim.x / nb;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+  double *coef = sm;
+  double *red = sm + 4 * nj;
+
+  const int slot = blockIdx.y;
+  const int oct = g.slot_oct[slot];
+  const int col = blockIdx.x;
+  const int x = (DIM == 3) ? col % g.nx : col;
+  const int y = (DIM == 3) ? col / g.nx : 0;
+  const bool xneg = oct & 4;
+  const bool yneg = oct & 2;
+  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
+
+  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
+  const int xregion = xneg ? 1 : 0;
+  const int64_t xoff = xneg ? (int64_t)E : -(int64_t)E;
+  bool yghost = false;
+  int yregion = 2;
+  int64_t yoff = 0;
+  if (DIM == 3) {
+    yghost = yneg ? (y == g.ny - 1) : (y == 0);
+    yregion = yneg ? 3 : 2;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
+  }
+  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
+  const int max_axis = DIM - 1;  // march axis index (2 for z, 1 for y)
+
+  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
+
+  const int pb = blockIdx.z * A.seg_len;
+  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int np = pe - pb;
+  const int step = mneg ? -1 : 1;
+  int p = mneg ? pe - 1 : pb;
+
+  const double *__restrict__ Iin = A.Iin;
+  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
+  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const int64_t colE = (int64_t)col * E;
+  const double dt = A.dt;
+  const double v = A.v[b];
+  const bool active = grp < JG && tid < JG * nb;
+
+  double prev[JMAX];
+  // march-axis upwind value of the first cell of the segment
+  {
+    const int pm = p - step;
+    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      prev[k] = 0.0;
+      if (active && k < nloc) {
+        const int e = (j0 + k) * nb + b;
+        if (stored)
+          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e);
+        else
+          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
+      }
+    }
+  }
+  __syncthreads();
+
+  int buf = 0;
+  for (int i = 0; i < np; ++i, p += step) {
+    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;  // local canonical cell
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t mg = g.m0 + p;
+    double acc = 0.0;
+    if (active) {
+      const double I0 = ldg(A.I0c + cell * nb + b);
+      const double dtb = dt * ldg(A.beta + cell * nb + b);
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        if (k < nloc) {
+          const int j = j0 + k;
+          const int e = j * nb + b;
+          const double Ic = ldg(Is + base + e);
+          double xu, yu = 0.0;
+          if (!xghost) {
+            xu = ldg(Is + base + xoff + e);
+          } else {
+            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+            xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
+          }
+          if (DIM == 3) {
+            if (!yghost) {
+              yu = ldg(Is + base + yoff + e);
+            } else {
+              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+              yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
+            }
+          }
+          const double *cf = coef + 4 * j;
+          // flux terms in axis order x, y, z (per-axis difference form, reading #19)
+          double fl = (cf[0] * v) * (Ic - xu);
+          if (DIM == 3) fl += (cf[1] * v) * (Ic - yu);
+          fl += (cf[max_axis] * v) * (Ic - prev[k]);
+          const double In = Ic + dtb * (I0 - Ic) - fl;
+          Os[base + e] = In;
+          acc += cf[3] * (I0 - In);
+          prev[k] = Ic;
+        }
+      }
+    }
+    double *rb = red + buf * JG * nb;
+    if (active) rb[tid] = acc;
+    __syncthreads();
+    if (tid < nb) {
+      double s = 0.0;
+      for (int q = 0; q < JG; ++q) s += rb[q * nb + tid];
+      A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
+    }
+    buf ^= 1;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && A.step_ctr)
+    atomicAdd(A.step_ctr, 1);
+}
+
+// thread shape: JG groups of nb threads, jpt directions per thread
+static void sweep_shape(int nb, int nj, int *jpt, int *JG) {
+  int jg = (448 + nb / 2) / nb;
+  jg = std::max(1, std::min(jg, nj));
+  while (jg * nb > 1024) --jg;
+  if (jg < 1) jg = 1;
+  int j = (nj + jg - 1) / jg;
+  jg = (nj + j - 1) / j;
+  *jpt = j;
+  *JG = jg;
+}
+
+template <int DIM>
+static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
+  SweepArgs a = a0;
+  const Geometry &g = a.g;
+  int jpt, JG;
+  sweep_shape(g.nb, g.nj, &jpt, &JG);
+  a.jpt = jpt;
+  const int threads = JG * g.nb;
+  if (threads > 1024 || g.nb > 1024) return cudaErrorInvalidConfiguration;
+  const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
+  dim3 grid(g.ncross, g.nslot, nseg);
+  const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
+  switch (jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 16 ? 16 : 0) {
+#define BTE_CASE(N)                                                                       \
+  case N:                                                                                 \
+    if (smem > 48 * 1024)                                                                 \
+      cudaFuncSetAttribute(k_sweep<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                           (int)smem);                                                    \
+    k_sweep<DIM, N><<<grid, threads, smem, s>>>(a);                                       \
+    break;
+    BTE_CASE(1)
+    BTE_CASE(2)
+    BTE_CASE(4)
+    BTE_CASE(5)
+    BTE_CASE(8)
+    BTE_CASE(16)
+#undef BTE_CASE
+    default:
+      return cudaErrorInvalidConfiguration;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s) {
+  return a.g.dim == 3 ? launch_sweep_dim<3>(a, s) : launch_sweep_dim<2>(a, s);
+}
+
+// ---------------------------------------------------------------- diffuse ghosts
+
+// g_b = [octant tree of sum_{j in outgoing octant} w_j|s_a| I_{j,b}] / den (reading #11).
+// One CTA per boundary face of this rank; threads over channels.
+__global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
+                          double *__restrict__ gtab) {
+  const int axis = region >> 1;
+  const bool hi = region & 1;
+  const int64_t lf = blockIdx.x;
+  int x = 0, y = 0, p = 0;
+  int64_t face;
+  const bool march = (axis == g.dim - 1);
+  if (g.dim == 3) {
+    if (axis == 0) {
+      y = (int)(lf % g.ny);
+      p = (int)(lf / g.ny);
+      x = hi ? g.nx - 1 : 0;
+      face = y + (int64_t)g.ny * (g.m0 + p);
+    } else if (axis == 1) {
+      x = (int)(lf % g.nx);
+      p = (int)(lf / g.nx);
+      y = hi ? g.ny - 1 : 0;
+      face = x + (int64_t)g.nx * (g.m0 + p);
+    } else {
+      x = (int)(lf % g.nx);
+      y = (int)(lf / g.nx);
+      p = hi ? g.nplanes - 1 : 0;
+      face = x + (int64_t)g.nx * y;
+    }
+  } else {
+    if (axis == 0) {
+      p = (int)lf;
+      x = hi ? g.nx - 1 : 0;
+      face = g.m0 + p;
+    } else {
+      x = (int)lf;
+      p = hi ? g.nplanes - 1 : 0;
+      face = x;
+    }
+  }
+  (void)march;
+  const int64_t cross = (g.dim == 3) ? x + (int64_t)g.nx * y : x;
+  const int64_t cell_base = (int64_t)(p + g.plane_off) * g.plane_stride + cross * g.E;
+  // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
+  const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
+  for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
+    double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int sl = 0; sl < g.nslot; ++sl) {
+      const int o = g.slot_oct[sl];
+      const bool out = hi ? !(o & bit) : (o & bit);
+      if (!out) continue;
+      const double *ws = g.ws + (int64_t)axis * g.nslot * g.nj + (int64_t)sl * g.nj;
+      const double *Ip = I + (int64_t)sl * g.slot_stride + cell_base + b;
+      double acc = 0.0;
+      for (int j = 0; j < g.nj; ++j) acc += ws[j] * Ip[(int64_t)j * g.nb];
+      q[o] = acc;
+    }
+    const double num = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    gtab[face * g.nb + b] = num / g.diff_den[region];
+  }
+}
+
+cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
+                           cudaStream_t s) {
+  const int axis = region >> 1;
+  int64_t nf;
+  if (g.dim == 3)
+    nf = axis == 0 ? (int64_t)g.ny * g.nplanes : (axis == 1 ? (int64_t)g.nx * g.nplanes : (int64_t)g.nx * g.ny);
+  else
+    nf = axis == 0 ? g.nplanes : g.nx;
+  if (nf == 0) return cudaSuccess;
+  int threads = ((g.nb + 31) / 32) * 32;
+  if (threads > 256) threads = 256;
+  k_diffuse<<<(unsigned)nf, threads, 0, s>>>(g, I, region, gtab);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Newton
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // bitwise identical in every lane (IEEE addition is commutative)
+}
+
+constexpr int kNewtonWarps = 4;
+constexpr int kMaxBandsPerLane = kMaxBands / 32;
+
+// One warp per cell.  Lane l owns channels b = l, l+32, ...
+__global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * kNewtonWarps + (threadIdx.x >> 5);
+  if (c >= a.ncells) return;
+  const int nb = a.nb;
+  const double Tn = a.T[c];
+  double D[kMaxBandsPerLane], cb[kMaxBandsPerLane], bn[kMaxBandsPerLane], I0c[kMaxBandsPerLane];
+  double F0 = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMaxBandsPerLane; ++k) {
+    const int b = lane + 32 * k;
+    D[k] = 0.0;
+    cb[k] = 0.0;
+    bn[k] = 0.0;
+    I0c[k] = 0.0;
+    if (b < nb) {
+      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = a.Dpart[(c * a.nslot + sl) * nb + b];
+      D[k] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+      bn[k] = beta_of_T(a.m.bcoef, b, Tn);
+      cb[k] = bn[k] / a.m.v[b];
+      I0c[k] = a.I0c[c * nb + b];
+      F0 += cb[k] * D[k];
+    }
+  }
+  F0 = warp_sum(F0);
+  double Tf = Tn;
+  int status = ERR_NONE;
+  if (!isfinite(F0)) {
+    status = ERR_NONFINITE;
+  } else if (F0 != 0.0) {
+    // Newton with bracket [1, 5000] K and bisection fallback (reading #18)
+    double T = Tn, lo = kTlo, hi = kThi;
+    bool conv = false;
+    for (int it = 0; it <= kNewtonMaxIt; ++it) {
+      double F = 0.0, Fp = 0.0;
+#pragma unroll
+      for (int k = 0; k < kMaxBandsPerLane; ++k) {
+        const int b = lane + 32 * k;
+        if (b < nb) {
+          double dI;
+          const double i0 = I0_of_T(a.m, b, T, &dI);
+          F += cb[k] * (a.W * (i0 - I0c[k]) + D[k]);
+          Fp += cb[k] * (a.W * dI);
+        }
+      }
+      F = warp_sum(F);
+      Fp = warp_sum(Fp);
+      if (!isfinite(F) || !isfinite(Fp)) {
+        status = ERR_NONFINITE;
+        break;
+      }
+      if (F == 0.0) {
+        Tf = T;
+        conv = true;
+        break;
+      }
+      if (it == kNewtonMaxIt) break;
+      if (F < 0.0)
+        lo = T;
+      else
+        hi = T;
+      const double stp = F / Fp;
+      double Tn1 = T - stp;
+      if (fabs(stp) <= kNewtonRtol * T) {
+        Tf = Tn1;
+        conv = true;
+        break;
+      }
+      if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
+      T = Tn1;
+    }
+    if (!conv && status == ERR_NONE) status = ERR_NEWTON;
+  }
+  if (status != ERR_NONE) {
+    if (lane == 0) {
+      const unsigned long long stepi = a.step_ctr ? (unsigned long long)(*a.step_ctr - 1) : 0ull;
+      const unsigned long long key = (stepi << 40) | ((unsigned long long)status << 36) |
+                                     (unsigned long long)(a.cell0_global + c);
+      atomicMin(a.err, key);
+    }
+    return;
+  }
+  if (lane == 0) a.T[c] = Tf;
+#pragma unroll
+  for (int k = 0; k < kMaxBandsPerLane; ++k) {
+    const int b = lane + 32 * k;
+    if (b < nb) {
+      if (Tf != Tn) a.I0c[c * nb + b] = I0_of_T(a.m, b, Tf, nullptr);
+      a.beta[c * nb + b] = bn[k];
+    }
+  }
+}
+
+cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
+  if (a.nb > kMaxBands) return cudaErrorInvalidValue;
+  const int64_t nblk = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
+  if (nblk == 0) return cudaSuccess;
+  k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- tables / state helpers
+
+__global__ void k_iso_table(const Material m, const double *__restrict__ Tw, int64_t nf,
+                            double *__restrict__ g) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nf * m.nb) return;
+  const int64_t f = i / m.nb;
+  const int b = (int)(i - f * m.nb);
+  g[i] = I0_of_T(m, b, Tw[f], nullptr);
+}
+
+cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,
+                             cudaStream_t s) {
+  const int64_t n = nf * m.nb;
+  if (n == 0) return cudaSuccess;
+  k_iso_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, Tw, nf, gtab);
+  return cudaGetLastError();
+}
+
+__global__ void k_refresh(const Material m, const double *__restrict__ T, int64_t nc,
+                          double *__restrict__ I0c, double *__restrict__ beta) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc * m.nb) return;
+  const int64_t c = i / m.nb;
+  const int b = (int)(i - c * m.nb);
+  const double t = T[c];
+  I0c[i] = I0_of_T(m, b, t, nullptr);
+  beta[i] = beta_of_T(m.bcoef, b, t);
+}
+
+cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c, double *beta,
+                           cudaStream_t s) {
+  const int64_t n = nc * m.nb;
+  if (n == 0) return cudaSuccess;
+  k_refresh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, T, nc, I0c, beta);
+  return cudaGetLastError();
+}
+
+// I[slot][plane][cross][j][b] = I0c[cell][b] over owned planes
+__global__ void k_fill_eq(const Geometry g, const double *__restrict__ I0c, double *__restrict__ I) {
+  const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_per_slot * g.nslot) return;
+  const int sl = (int)(i / n_per_slot);
+  const int64_t r = i - sl * n_per_slot;
+  const int64_t cell = r / g.E;
+  const int e = (int)(r - cell * g.E);
+  const int b = e % g.nb;
+  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + r] = I0c[cell * g.nb + b];
+}
+
+cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I, cudaStream_t s) {
+  const int64_t n = (int64_t)g.nplanes * g.ncross * g.E * g.nslot;
+  if (n == 0) return cudaSuccess;
+  k_fill_eq<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I0c, I);
+  return cudaGetLastError();
+}
+
+// canonical chunk [c0, c0+nc)[d][b] <-> layout.  dmap[d] = slot*nj + j.
+__global__ void k_permute(const Geometry g, const int *__restrict__ dmap, int nd,
+                          double *__restrict__ canon, int64_t c0, int64_t ncc, double *__restrict__ I,
+                          int to_layout) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_cell = (int64_t)nd * g.nb;
+  if (i >= ncc * per_cell) return;
+  const int64_t cr = i / per_cell;
+  const int rem = (int)(i - cr * per_cell);
+  const int d = rem / g.nb;
+  const int b = rem - d * g.nb;
+  const int sj = dmap[d];
+  const int sl = sj / g.nj;
+  const int j = sj - sl * g.nj;
+  const int64_t c = c0 + cr;
+  const int64_t p = c / g.ncross;
+  const int64_t cross = c - p * g.ncross;
+  const int64_t dst = sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E +
+                      (int64_t)j * g.nb + b;
+  if (to_layout)
+    I[dst] = canon[i];
+  else
+    canon[i] = I[dst];
+}
+
+cudaError_t launch_permute(const Geometry &g, const int *dmap, int nd, const double *canon, int64_t c0,
+                           int64_t ncc, double *I, int to_layout, cudaStream_t s) {
+  const int64_t n = ncc * nd * g.nb;
+  if (n == 0) return cudaSuccess;
+  k_permute<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, dmap, nd, const_cast<double *>(canon), c0,
+                                                          ncc, I, to_layout);
+  return cudaGetLastError();
+}
+
+__global__ void k_random_T(const Geometry g, double dx, double dy, double dz, double p0, double p1,
+                           double p2, double T_mean, double T_amp, double *__restrict__ T) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  if (c >= nc) return;
+  const double twopi = 6.283185307179586;
+  double v;
+  if (g.dim == 3) {
+    const int64_t x = c % g.nx, y = (c / g.nx) % g.ny, z = g.m0 + c / ((int64_t)g.nx * g.ny);
+    const double fx = sin(twopi * (((x + 0.5) * dx) / (g.nx * dx) + p0));
+    const double fy = sin(twopi * (((y + 0.5) * dy) / (g.ny * dy) + p1));
+    const double fz = sin(twopi * (((z + 0.5) * dz) / (g.nplanes_global * dz) + p2));
+    v = T_mean + T_amp * (fz * fy * fx);
+  } else {
+    const int64_t x = c % g.nx, y = g.m0 + c / g.nx;
+    const double fx = sin(twopi * (((x + 0.5) * dx) / (g.nx * dx) + p0));
+    const double fy = sin(twopi * (((y + 0.5) * dy) / (g.nplanes_global * dy) + p1));
+    v = T_mean + T_amp * (1.0 * fy * fx);
+  }
+  T[c] = v;
+}
+
+cudaError_t launch_random_T(const Geometry &g, int64_t, double dx, double dy, double dz,
+                            const double *phase, double T_mean, double T_amp, double *T,
+                            cudaStream_t s) {
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  if (nc == 0) return cudaSuccess;
+  k_random_T<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, dx, dy, dz, phase[0], phase[1], phase[2],
+                                                           T_mean, T_amp, T);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// I = I0c * (1 + amp*(2u - 1)), u from the canonical global index (c_g*nd + d)*nb + b
+__global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, int nd, uint64_t seed,
+                           double amp, const double *__restrict__ I0c, double *__restrict__ I) {
+  const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_per_slot * g.nslot) return;
+  const int sl = (int)(i / n_per_slot);
+  const int64_t r = i - sl * n_per_slot;
+  const int64_t cell = r / g.E;
+  const int e = (int)(r - cell * g.E);
+  const int j = e / g.nb;
+  const int b = e - j * g.nb;
+  const int d = canon_d[sl * g.nj + j];
+  const int64_t cg = g.m0 * g.ncross + cell;
+  const uint64_t idx = ((uint64_t)cg * nd + d) * g.nb + b;
+  const double u = (double)(splitmix64(seed ^ idx) >> 11) * 0x1.0p-53;
+  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + r] =
+      I0c[cell * g.nb + b] * (1.0 + amp * (2.0 * u - 1.0));
+}
+
+cudaError_t launch_random_I(const Geometry &g, const int *canon_d, int nd, uint64_t seed, double amp,
+                            const double *I0c, double *I, cudaStream_t s) {
+  const int64_t n = (int64_t)g.nplanes * g.ncross * g.E * g.nslot;
+  if (n == 0) return cudaSuccess;
+  k_random_I<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, canon_d, nd, seed, amp, I0c, I);
+  return cudaGetLastError();
+}
+
+__global__ void k_octant_tree(const double *__restrict__ Dpart, int nslot, Geometry g, int64_t nc,
+                              double *__restrict__ D) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc * g.nb) return;
+  const int64_t c = i / g.nb;
+  const int b = (int)(i - c * g.nb);
+  double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int sl = 0; sl < nslot; ++sl) q[g.slot_oct[sl]] = Dpart[(c * nslot + sl) * g.nb + b];
+  D[i] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+}
+
+cudaError_t launch_octant_tree_g(const Geometry &g, const double *Dpart, int64_t nc, double *D,
+                                 cudaStream_t s) {
+  const int64_t n = nc * g.nb;
+  if (n == 0) return cudaSuccess;
+  k_octant_tree<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(Dpart, g.nslot, g, nc, D);
+  return cudaGetLastError();
+}
+
+// Dpart[c][slot][b] = sum_j w_j (I0c - I) of the given state (set_state with I only)
+__global__ void k_dpart_from_I(const Geometry g, const double *__restrict__ I, const double *__restrict__ I0c,
+                               double *__restrict__ Dpart) {
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc * g.nslot * g.nb) return;
+  const int b = (int)(i % g.nb);
+  const int sl = (int)((i / g.nb) % g.nslot);
+  const int64_t c = i / ((int64_t)g.nb * g.nslot);
+  const int64_t p = c / g.ncross, cross = c - p * g.ncross;
+  const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E + b;
+  const double i0 = I0c[c * g.nb + b];
+  double s = 0.0;
+  for (int j = 0; j < g.nj; ++j) s += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] * (i0 - Ip[(int64_t)j * g.nb]);
+  Dpart[i] = s;
+}
+
+cudaError_t launch_dpart_from_I(const Geometry &g, const double *I, const double *I0c, double *Dpart,
+                               cudaStream_t s) {
+  const int64_t n = (int64_t)g.nplanes * g.ncross * g.nslot * g.nb;
+  if (n == 0) return cudaSuccess;
+  k_dpart_from_I<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I, I0c, Dpart);
+  return cudaGetLastError();
+}
+
+// per-cell energy density sum_slot sum_j sum_b w_j/v_b I (warp per cell)
+__global__ void k_energy(const Geometry g, const double *__restrict__ I, const double *__restrict__ v,
+                         double *__restrict__ Ec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  if (c >= nc) return;
+  const int64_t p = c / g.ncross, cross = c - p * g.ncross;
+  double acc = 0.0;
+  for (int sl = 0; sl < g.nslot; ++sl) {
+    const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E;
+    for (int e = lane; e < g.E; e += 32) {
+      const int j = e / g.nb, b = e - j * g.nb;
+      acc += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] / v[b] * Ip[e];
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) Ec[c] = acc;
+}
+
+cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, double *Ec, cudaStream_t s) {
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  if (nc == 0) return cudaSuccess;
+  k_energy<<<(unsigned)((nc + 3) / 4), 128, 0, s>>>(g, I, v, Ec);
+  return cudaGetLastError();
+}
+
+}  // namespace bte

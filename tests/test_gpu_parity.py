@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Tolerance (BASELINE.json north_star): max relative error
+1e-10 on intensities and 1e-8 K absolute on temperature after the run.
+
+Sizes: small cases span several CTAs per axis and a ragged tail; the full
+BASELINE.json sizes (config 2 at 120x120x400x40 and config 3 at 64^3x400x40)
+are checked on sampled cells whose k-step domain of dependence the oracle
+recomputes exactly on a sub-box (explicit upwind stencil: a cell after k
+steps depends only on cells within k of it), plus invariants that hold at any
+size (fixed point, energy conservation, mirror symmetry, determinism)."""
+import math
+
+import numpy as np
+import pytest
+
+import bte_inputs as bi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+REL_I = 1e-10
+ABS_T = 1e-8
+
+
+@pytest.fixture(scope="module")
+def Solver():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_19400_b200 import Solver as S, build
+    build.build()
+    return S
+
+
+def _cmp(Ig, Tg, Io, To):
+    rel = float(np.max(np.abs(Ig - Io) / np.abs(Io)))
+    dT = float(np.max(np.abs(Tg - To)))
+    return rel, dT
+
+
+def _run_both(Solver, p, nsteps, start="random", solve_T=False):
+    o = oracle.Oracle(p)
+    if start == "random":
+        I, T = o.random_state()
+    else:
+        T = np.full(p.mesh.ncells, p.T_init)
+        I = o.equilibrium(T)
+    with Solver.from_problem(p) as sv:
+        if solve_T:
+            sv.set_state(I, None)
+            T, I0c, betac = o.solve_T(I, np.full(p.mesh.ncells, p.T_init))
+            Tg0 = sv.temperature()
+            assert np.max(np.abs(Tg0 - T)) <= ABS_T
+            Io, To, _, _ = o.run(I, T, nsteps, I0c, betac)
+        else:
+            sv.set_state(I, T)
+            Io, To, _, _ = o.run(I, T, nsteps)
+        sv.step(nsteps)
+        Ig, Tg = sv.intensity(), sv.temperature()
+    return _cmp(Ig, Tg, Io, To), (Ig, Tg, Io, To)
+
+
+# ----------------------------------------------------------------- small full-field parity
+
+@pytest.mark.parametrize("shape", [(5, 4, 3), (7, 3, 6), (1, 1, 5), (9, 8, 2)])
+def test_parity_small_3d_all_bc_kinds(Solver, shape):
+    p = bi.small_3d(*shape)
+    (rel, dT), _ = _run_both(Solver, p, 10)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_config1_full(Solver):
+    """BASELINE configs[0]: 2-D gray 20x20x16x1, hot/cold walls, diffuse sides, 100 steps."""
+    p = bi.config1()
+    (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, p.nsteps, start="physical")
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    assert To.max() > 300.5  # heat entered from the 310 K wall
+
+
+def test_parity_config2_reduced_physical(Solver):
+    """Config 2 geometry (hot spot, specular sides) on 24x24 with the full 400 x 40 tables."""
+    p = bi.config2(n=24)
+    p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(24, p.mesh.dx, width=40e-6), 300.0)
+    (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, 100, start="physical")
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    assert To.max() > 300.0
+
+
+def test_parity_config2_reduced_random(Solver):
+    p = bi.config2(n=16)
+    (rel, dT), _ = _run_both(Solver, p, 20)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_config3_reduced(Solver):
+    p = bi.config3(n=8)
+    p.mesh = bi.Mesh(3, 9, 7, 6, 1e-6, 1e-6, 1e-6)
+    (rel, dT), _ = _run_both(Solver, p, 5)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_inplane_3d_mesh_55_channels(Solver):
+    """In-plane direction set on a 3-D mesh (4 populated octants), 55 channels (n_freq = 40)."""
+    p = bi.small_3d(6, 5, 3, dirs=bi.directions_inplane(20), bands=bi.silicon_bands(40),
+                    bcs=[bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 303.0), bi.WallBC(1),
+                         bi.WallBC(1), bi.WallBC(1)])
+    (rel, dT), _ = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_set_state_solves_T(Solver):
+    p = bi.small_3d(5, 4, 3)
+    (rel, dT), _ = _run_both(Solver, p, 4, solve_T=True)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_linear_multichannel(Solver):
+    rng = np.random.default_rng(3)
+    nb = 3
+    bands = bi.linear_bands(rng.uniform(2e3, 8e3, nb), rng.uniform(2e-11, 8e-11, nb),
+                            rng.uniform(1e2, 1e3, nb), rng.uniform(1e4, 1e5, nb))
+    p = bi.small_3d(6, 5, 4, bands=bands, dirs=bi.directions_control_angle(4, 8), dt=2e-12, d=1e-7)
+    (rel, dT), _ = _run_both(Solver, p, 30)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+# ----------------------------------------------------------------- kernel units (sub-steps)
+
+def test_substep_sweep_and_reduce(Solver):
+    p = bi.small_3d(7, 5, 4)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    I0c, betac = o.refresh(T)
+    J = o.sweep(I, I0c, betac)
+    D = o.reduce(J, I0c)
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        I0g, bg = sv.debug_substep(2), sv.debug_substep(3)
+        assert np.max(np.abs(I0g / I0c - 1)) < 1e-13
+        assert np.max(np.abs(bg / betac - 1)) < 1e-14
+        Jg = sv.debug_substep(0)
+        Dg = sv.debug_substep(1)
+        # state unchanged by the sub-step calls
+        assert np.array_equal(sv.intensity(), I)
+    assert np.max(np.abs(Jg / J - 1)) < 1e-13
+    scale = np.abs(p.dirs.w[None, :, None] * (I0c[:, None, :] - J)).sum(1)
+    assert np.max(np.abs(Dg - D) / scale) < 1e-13
+
+
+def test_init_random_matches_recipe(Solver):
+    p = bi.small_3d(6, 5, 4)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    with Solver.from_problem(p) as sv:
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        Ig, Tg = sv.intensity(), sv.temperature()
+    assert np.max(np.abs(Tg - T)) < 1e-11
+    assert np.max(np.abs(Ig / I - 1)) < 1e-13
+
+
+# ----------------------------------------------------------------- full BASELINE sizes, sampled
+
+def _sampled_full_size(Solver, p, nsteps, samples):
+    """Run the full problem on the GPU (device-generated random start); for each
+    sample cell recompute its nsteps-step dependence box with the oracle."""
+    m = p.mesh
+    with Solver.from_problem(p) as sv:
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        sv.step(nsteps)
+        Tg = sv.temperature()
+        Ig = None
+        if p.dof * 8 < 4e9:
+            Ig = sv.intensity()
+    worst_rel, worst_T = 0.0, 0.0
+    k = nsteps
+    for (x, y, z) in samples:
+        box = [(max(0, x - k), min(m.nx, x + k + 1)), (max(0, y - k), min(m.ny, y + k + 1)),
+               (max(0, z - k), min(m.nz, z + k + 1))]
+        sp = bi.subproblem(p, box)
+        o = oracle.Oracle(sp)
+        T0 = bi.random_temperature(m, p.seed, p.T_init, 20.0, box=box)
+        I0 = o.equilibrium(T0) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m,
+                                                           box=box)
+        Io, To, _, _ = o.run(I0, T0, nsteps)
+        sm = sp.mesh
+        lc = (x - box[0][0]) + sm.nx * ((y - box[1][0]) + sm.ny * (z - box[2][0]))
+        gc = x + m.nx * (y + m.ny * z)
+        worst_T = max(worst_T, abs(Tg[gc] - To[lc]))
+        if Ig is not None:
+            worst_rel = max(worst_rel, float(np.max(np.abs(Ig[gc] - Io[lc]) / np.abs(Io[lc]))))
+    return worst_rel, worst_T
+
+
+def test_full_size_config2_sampled(Solver):
+    """BASELINE configs[1] at full size (the bench workload), 3 steps, sampled cells incl. walls."""
+    p = bi.config2()
+    n = p.mesh.nx
+    samples = [(0, 0, 0), (n - 1, n - 1, 0), (n // 2, n - 1, 0), (n // 2 - 1, n - 2, 0), (37, 61, 0),
+               (n - 1, 5, 0), (0, n // 2, 0)]
+    rel, dT = _sampled_full_size(Solver, p, 3, samples)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_full_size_config3_sampled(Solver):
+    """BASELINE configs[2] at full size (64^3 x 400 x 40, 33.6 GB/buffer), 2 steps, sampled T."""
+    p = bi.config3()
+    n = p.mesh.nx
+    samples = [(0, 0, 0), (n - 1, n - 1, n - 1), (31, 17, 0), (5, n - 1, 40), (32, 32, 32), (n - 1, 0, n - 2)]
+    rel, dT = _sampled_full_size(Solver, p, 2, samples)
+    assert dT <= ABS_T, dT
+
+
+# ----------------------------------------------------------------- invariants
+
+def test_fixed_point_bitexact(Solver):
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 10, 20, 30, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+           bi.WallBC(1)]
+    p = bi.small_3d(8, 6, 5, bands=b, bcs=bcs)
+    with Solver.from_problem(p) as sv:
+        I0 = sv.intensity()
+        T0 = sv.temperature()
+        sv.step(50)
+        assert np.array_equal(sv.intensity(), I0)
+        assert np.array_equal(sv.temperature(), T0)
+
+
+@pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE])
+def test_energy_conservation_closed_box(Solver, kind):
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    p = bi.small_3d(6, 5, 4, bands=b, bcs=bi.uniform_bcs(kind), dirs=bi.directions_control_angle(4, 16))
+    o = oracle.Oracle(p)
+    I, _ = o.random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, None)  # consistent T from the Newton
+        E0 = sv.energy()
+        sv.step(300)
+        E1 = sv.energy()
+    assert abs(E1 / E0 - 1) < 1e-12, E1 / E0 - 1
+
+
+def test_mirror_symmetry_bitexact(Solver):
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 15, 35])
+    p = bi.config2(n=12)
+    p.bands = b
+    p.mesh = bi.Mesh(2, 12, 12, 1, 2e-6, 2e-6, 1.0)
+    p.dirs = bi.directions_control_angle(4, 8)
+    p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, 2e-6, width=4e-6), 300.0)
+    with Solver.from_problem(p) as sv:
+        sv.step(40)
+        I, T = sv.intensity(), sv.temperature()
+    r = oracle.Oracle(p).reflection(0)
+    A = I.reshape(12, 12, p.dirs.nd, b.nb)
+    assert np.array_equal(A, A[:, ::-1][:, :, r, :])
+    assert np.array_equal(T.reshape(12, 12), T.reshape(12, 12)[:, ::-1])
+    assert T.max() > 300.0
+
+
+def test_determinism(Solver):
+    p = bi.small_3d(8, 7, 6)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    out = []
+    for _ in range(2):
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(7)
+            out.append((sv.intensity(), sv.temperature()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+# ----------------------------------------------------------------- error paths
+
+def test_errors(Solver):
+    from paper_2305_19400_b200 import BteError
+    p = bi.small_3d()
+    p.dt = 1e-10  # violates the positivity bound
+    with pytest.raises(BteError) as e:
+        Solver.from_problem(p)
+    assert e.value.status == 5
+    p = bi.small_3d()
+    with Solver.from_problem(p) as sv:
+        I = sv.intensity()
+        I[3, 2, 1] = np.nan
+        T = sv.temperature()
+        sv.set_state(I, T)
+        with pytest.raises(BteError) as e:
+            sv.step(2)
+        assert e.value.status == 8 and "step 0" in str(e.value)
+        with pytest.raises(ValueError):
+            sv.set_state(I[:-1], T)
+        with pytest.raises(BteError) as e:
+            sv.set_bc(7, 0)
+        assert e.value.status == 1
+    # specular wall with a direction set not closed under the reflection
+    d = bi.directions_control_angle(4, 8)
+    d.s = d.s.copy()
+    d.s[0, 0] += 1e-9
+    p = bi.small_3d(dirs=d, bcs=bi.uniform_bcs(bi.BC_DIFFUSE))
+    with Solver.from_problem(p) as sv:
+        with pytest.raises(BteError) as e:
+            sv.set_bc(0, bi.BC_SPECULAR)
+        assert e.value.status == 6
