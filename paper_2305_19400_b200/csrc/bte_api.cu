@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -70,6 +71,7 @@ struct bte_ctx {
   double *staging = nullptr;
   int64_t staging_cells = 0;
   int seg_len = 0;
+  int use_tma = 1, stages_override = 0, seg_override = 0;  // env BTE_SWEEP / BTE_STAGES / BTE_SEGS (A/B runs)
   int64_t ncells_local = 0, ncells_global = 0;
   int64_t steps_done = 0;
   // timing
@@ -435,11 +437,15 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     }
     g.diff_den[r] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
   }
+  if (const char *e = getenv("BTE_SWEEP")) ctx->use_tma = strcmp(e, "plain") != 0;
+  if (const char *e = getenv("BTE_STAGES")) ctx->stages_override = atoi(e);
+  if (const char *e = getenv("BTE_SEGS")) ctx->seg_override = atoi(e);
   // segment length along the march axis: enough CTAs for >= ~16 per SM
   {
     const int64_t cols = (int64_t)g.ncross * nslot;
     int nseg = (int)std::max<int64_t>(1, (148 * 16 + cols - 1) / cols);
     nseg = std::min(nseg, std::max(1, g.nplanes / 8));
+    if (ctx->seg_override > 0) nseg = std::min(ctx->seg_override, g.nplanes);
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
   }
 
@@ -616,6 +622,8 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.v = ctx->m.v;
   a.dt = ctx->dt;
   a.seg_len = ctx->seg_len;
+  a.use_tma = ctx->use_tma;
+  a.stages_override = ctx->stages_override;
   a.step_ctr = step_ctr;
   CU(launch_sweep(a, ctx->stream));
   ctx->tacc.launches++;

@@ -73,6 +73,10 @@ struct SweepArgs {
   double dt;
   int seg_len;            // cells per CTA along the march axis
   int jpt;                // directions per thread (set by launch_sweep)
+  int use_tma;            // cp.async.bulk pipeline (k_sweep_tma) when the layout allows
+  int stages;             // pipeline depth (set by launch_sweep)
+  int stages_override;    // 0 = automatic
+  int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int *step_ctr;
 };
 

@@ -209,6 +209,208 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
     atomicAdd(A.step_ctr, 1);
 }
 
+// ---------------------------------------------------------------- TMA-pipelined sweep
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Same decomposition and arithmetic as k_sweep, but the (cell, octant) blocks
+// of the cell and of its cross-axis upwind neighbours (16 KB each at 50 x 40),
+// plus the cell's I0c/beta rows, stream into an S-stage shared-memory ring with
+// cp.async.bulk + mbarrier, issued S cells ahead by one thread.  Keeps
+// S x (2 or 3) x 16 KB of HBM/L2 reads in flight per CTA.
+template <int DIM, int JMAX>
+__global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const Geometry &g = A.g;
+  const int nb = g.nb, nj = g.nj, E = g.E;
+  const int S = A.stages;
+  const int tid = threadIdx.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = blockDim.x / nb;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+
+  const int slot = blockIdx.y;
+  const int oct = g.slot_oct[slot];
+  const int col = blockIdx.x;
+  const int x = (DIM == 3) ? col % g.nx : col;
+  const int y = (DIM == 3) ? col / g.nx : 0;
+  const bool xneg = oct & 4;
+  const bool yneg = oct & 2;
+  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
+  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
+  const int xregion = xneg ? 1 : 0;
+  const int64_t xoff = xneg ? (int64_t)E : -(int64_t)E;
+  bool yghost = false;
+  int yregion = 2;
+  int64_t yoff = 0;
+  if (DIM == 3) {
+    yghost = yneg ? (y == g.ny - 1) : (y == 0);
+    yregion = yneg ? 3 : 2;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
+  }
+  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
+  const int max_axis = DIM - 1;
+
+  // shared memory carve-up
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);          // [S] (S <= 16)
+  double *coef = reinterpret_cast<double *>(smraw + 128);        // [nj][4]
+  double *red = coef + 4 * nj;                                   // [2][JG*nb]
+  double *stage0 = red + 2 * JG * nb;                            // [S][stage_doubles]
+  const int64_t sd = A.stage_doubles;                            // own | xup | (yup) | I0 | beta
+  const int nblk = 1 + (xghost ? 0 : 1) + ((DIM == 3 && !yghost) ? 1 : 0);
+  const int o_x = E, o_y = 2 * E, o_i0 = (DIM == 3 ? 3 : 2) * E, o_be = o_i0 + nb;
+
+  const int pb = blockIdx.z * A.seg_len;
+  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int np = pe - pb;
+  const int step = mneg ? -1 : 1;
+  const int pfirst = mneg ? pe - 1 : pb;
+
+  const double *__restrict__ Iin = A.Iin;
+  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
+  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const int64_t colE = (int64_t)col * E;
+  const double dt = A.dt;
+
+  auto issue = [&](int i, int st) {
+    const int pp = pfirst + i * step;
+    const int64_t base = (int64_t)(pp + g.plane_off) * g.plane_stride + colE;
+    const int64_t cell = (int64_t)col + (int64_t)pp * g.ncross;
+    double *sp = stage0 + st * sd;
+    const uint32_t blk = (uint32_t)E * 8u;
+    const uint32_t row = (uint32_t)nb * 8u;
+    mbar_expect_tx(&full[st], blk * nblk + 2u * row);
+    bulk_g2s(sp, Is + base, blk, &full[st]);
+    if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
+    if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
+    bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
+    bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < min(S, np); ++i) issue(i, i);
+
+  const double v = A.v[b];
+  const bool active = grp < JG;
+  double prev[JMAX];
+  {
+    const int p = pfirst;
+    const int pm = p - step;
+    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      prev[k] = 0.0;
+      if (active && k < nloc) {
+        const int e = (j0 + k) * nb + b;
+        if (stored)
+          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e);
+        else
+          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
+      }
+    }
+  }
+
+  int buf = 0;
+  int p = pfirst;
+  for (int i = 0; i < np; ++i, p += step) {
+    const int st = i % S;
+    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t mg = g.m0 + p;
+    const double *sp = stage0 + st * sd;
+    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    double acc = 0.0;
+    if (active) {
+      const double I0 = sp[o_i0 + b];
+      const double dtb = dt * sp[o_be + b];
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        if (k < nloc) {
+          const int j = j0 + k;
+          const int e = j * nb + b;
+          const double Ic = sp[e];
+          double xu, yu = 0.0;
+          if (!xghost) {
+            xu = sp[o_x + e];
+          } else {
+            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+            xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
+          }
+          if (DIM == 3) {
+            if (!yghost) {
+              yu = sp[o_y + e];
+            } else {
+              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+              yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
+            }
+          }
+          const double *cf = coef + 4 * j;
+          double fl = (cf[0] * v) * (Ic - xu);
+          if (DIM == 3) fl += (cf[1] * v) * (Ic - yu);
+          fl += (cf[max_axis] * v) * (Ic - prev[k]);
+          const double In = Ic + dtb * (I0 - Ic) - fl;
+          Os[base + e] = In;
+          acc += cf[3] * (I0 - In);
+          prev[k] = Ic;
+        }
+      }
+    }
+    double *rb = red + buf * JG * nb;
+    if (active) rb[tid] = acc;
+    __syncthreads();  // stage st fully consumed, rb complete
+    if (tid == 0 && i + S < np) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S, st);
+    }
+    if (tid < nb) {
+      double s = 0.0;
+      for (int q = 0; q < JG; ++q) s += rb[q * nb + tid];
+      A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
+    }
+    buf ^= 1;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && A.step_ctr)
+    atomicAdd(A.step_ctr, 1);
+}
+
 // thread shape: JG groups of nb threads, jpt directions per thread
 static void sweep_shape(int nb, int nj, int *jpt, int *JG) {
   int jg = (448 + nb / 2) / nb;
@@ -232,8 +434,41 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
   if (threads > 1024 || g.nb > 1024) return cudaErrorInvalidConfiguration;
   const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
   dim3 grid(g.ncross, g.nslot, nseg);
+  const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 16 ? 16 : 0;
+  const bool tma = a.use_tma && (g.E % 2 == 0) && (g.nb % 2 == 0);
+  if (tma) {
+    // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B
+    const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.E + 2 * g.nb + 15) / 16 * 16;
+    const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
+    const size_t budget = 113 * 1024;  // two CTAs per SM
+    int S = (int)((budget > fixed ? budget - fixed : 0) / (stage_d * sizeof(double)));
+    S = std::max(2, std::min(4, S));
+    if (a.stages_override > 0) S = std::min(16, a.stages_override);
+    a.stages = S;
+    a.stage_doubles = stage_d;
+    const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    switch (jcase) {
+#define BTE_CASE(N)                                                                         \
+  case N:                                                                                   \
+    cudaFuncSetAttribute(k_sweep_tma<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         (int)smem);                                                        \
+    k_sweep_tma<DIM, N><<<grid, threads, smem, s>>>(a);                                     \
+    break;
+      BTE_CASE(1)
+      BTE_CASE(2)
+      BTE_CASE(4)
+      BTE_CASE(5)
+      BTE_CASE(8)
+      BTE_CASE(16)
+#undef BTE_CASE
+      default:
+        return cudaErrorInvalidConfiguration;
+    }
+    return cudaGetLastError();
+  }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
-  switch (jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 16 ? 16 : 0) {
+  switch (jcase) {
 #define BTE_CASE(N)                                                                       \
   case N:                                                                                 \
     if (smem > 48 * 1024)                                                                 \
