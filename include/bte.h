@@ -205,6 +205,33 @@ typedef struct {
 BTE_API bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps);
 BTE_API bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out);
 
+/* Slab decomposition and halo plan for P ranks (P:L552-560 cell
+ * partitioning).  Host-only (no CUDA call): the library's own halo exchange
+ * (a5) executes exactly this list every step, after the sweep.  Planes are
+ * split along the slowest axis (z for dim 3, y for dim 2): rank r owns
+ * [m0, m0 + n_local) with the first (n mod P) ranks taking one extra plane.
+ * For each octant whose slab-axis component points up (s >= 0), rank r sends
+ * its last owned plane to r+1 and receives plane m0-1 from r-1; octants
+ * pointing down do the mirror exchange.  msg[] lists this rank's messages in
+ * execution order; `plane` is the global plane index sent or received. */
+#define BTE_MAX_MSGS 32
+typedef struct {
+  int send;      /* 1 = send an owned plane, 0 = receive into a halo plane */
+  int peer;      /* the other rank                                        */
+  int octant;    /* sign pattern (4*[sx<0] + 2*[sy<0] + [sz<0]) moved     */
+  int slot;      /* index of that octant among the non-empty ones         */
+  int64_t plane; /* global plane index                                    */
+  int64_t count; /* doubles in the message (cells per plane * nj * nb)    */
+} bte_msg;
+typedef struct {
+  int axis;        /* slab axis: 2 (z) for dim 3, 1 (y) for dim 2 */
+  int64_t m0, n_local;
+  int n_msgs;
+  bte_msg msg[BTE_MAX_MSGS];
+} bte_slab_plan;
+BTE_API bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int nb, int nranks, int rank,
+                                 bte_slab_plan *out);
+
 /* Sizes of this rank's slab and the layout. */
 typedef struct {
   int64_t ncells_local, ncells_global, z0, nz_local; /* slab along the slowest axis */

@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE = 0, 1, 2
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_plan_slab", "bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -69,6 +69,16 @@ class Timing(C.Structure):
                 ("boundary_launches", C.c_int64)]
 
 
+class Msg(C.Structure):
+    _fields_ = [("send", C.c_int), ("peer", C.c_int), ("octant", C.c_int), ("slot", C.c_int),
+                ("plane", C.c_int64), ("count", C.c_int64)]
+
+
+class SlabPlan(C.Structure):
+    _fields_ = [("axis", C.c_int), ("m0", C.c_int64), ("n_local", C.c_int64), ("n_msgs", C.c_int),
+                ("msg", Msg * 32)]
+
+
 class Info(C.Structure):
     _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
@@ -101,6 +111,7 @@ def load_library(path: str = LIB_PATH):
     lib.bte_timing_enable.argtypes = [P, C.c_int, C.c_int64]
     lib.bte_timing_read.argtypes = [P, C.POINTER(Timing)]
     lib.bte_get_info.argtypes = [P, C.POINTER(Info)]
+    lib.bte_plan_slab.argtypes = [C.POINTER(Mesh), C.POINTER(Dirs), C.c_int, C.c_int, C.c_int, C.POINTER(SlabPlan)]
     lib.bte_last_error.argtypes = [P]
     lib.bte_last_error.restype = C.c_char_p
     lib.bte_destroy.argtypes = [P]
@@ -278,6 +289,21 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+def plan_slab(mesh, dirs, nb: int, nranks: int, rank: int) -> dict:
+    """The library's slab decomposition + halo plan for one rank (host-only call;
+    the same list bte_step executes with NCCL)."""
+    lib = load_library()
+    m = Mesh(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.dx, mesh.dy, mesh.dz)
+    s, w = _f64(dirs.s), _f64(dirs.w)
+    d = Dirs(int(w.shape[0]), _p(s), _p(w))
+    out = SlabPlan()
+    st = lib.bte_plan_slab(C.byref(m), C.byref(d), int(nb), int(nranks), int(rank), C.byref(out))
+    if st != BTE_OK:
+        raise BteError(st, "bte_plan_slab")
+    msgs = [{f: getattr(out.msg[k], f) for f, _ in Msg._fields_} for k in range(out.n_msgs)]
+    return {"axis": out.axis, "m0": out.m0, "n_local": out.n_local, "msgs": msgs}
 
 
 def nccl_unique_id() -> bytes:

@@ -63,7 +63,7 @@ struct bte_ctx {
   Material m{};
   double *I[2] = {nullptr, nullptr};
   int cur = 0;
-  double *I0c = nullptr, *beta = nullptr, *T = nullptr, *Dpart = nullptr;
+  double *I0c = nullptr, *dI0c = nullptr, *beta = nullptr, *T = nullptr, *Dpart = nullptr;
   double *gtab[6] = {nullptr};
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
@@ -71,7 +71,7 @@ struct bte_ctx {
   double *staging = nullptr;
   int64_t staging_cells = 0;
   int seg_len = 0;
-  int use_tma = 1, stages_override = 0, seg_override = 0;  // env BTE_SWEEP / BTE_STAGES / BTE_SEGS (A/B runs)
+  int use_tma = 1, stages_override = 0, seg_override = 0, target_threads = 0, smem_budget_kb = 0, stcs = 1;  // env BTE_SWEEP / BTE_STAGES / BTE_SEGS (A/B runs)
   int64_t ncells_local = 0, ncells_global = 0;
   int64_t steps_done = 0;
   // timing
@@ -81,6 +81,7 @@ struct bte_ctx {
   std::vector<char> ev_has_bnd;
   bte_timing tacc{};
   // NCCL
+  bte_slab_plan plan{};
   void *nccl_comm = nullptr;
   cudaStream_t comm_stream = nullptr;
 };
@@ -187,9 +188,47 @@ static bte_status sync_check(bte_ctx *ctx) {
 
 extern "C" {
 
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
+
 const char *bte_version(void) { return "bte-b200 0.1 (sm_100a, fp64)"; }
 
 const char *bte_last_error(const bte_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int nb, int nranks, int rank,
+                         bte_slab_plan *out) {
+  if (!mesh || !dirs || !out || nranks < 1 || rank < 0 || rank >= nranks || nb < 1) return BTE_EINVAL;
+  if (mesh->dim != 2 && mesh->dim != 3) return BTE_EINVAL;
+  std::memset(out, 0, sizeof *out);
+  const int axis = mesh->dim == 3 ? 2 : 1;
+  const int64_t nplanes = axis == 2 ? mesh->nz : mesh->ny;
+  const int64_t base = nplanes / nranks, rem = nplanes % nranks;
+  out->axis = axis;
+  out->n_local = base + (rank < rem ? 1 : 0);
+  out->m0 = (int64_t)rank * base + std::min<int64_t>(rank, rem);
+  if (out->n_local < 1) return BTE_EINVAL;
+  int count[8] = {0};
+  for (int d = 0; d < dirs->nd; ++d) count[octant_of(dirs->s + 3 * d)]++;
+  const int bit = axis == 2 ? 1 : 2;
+  const int64_t cross = axis == 2 ? mesh->nx * mesh->ny : mesh->nx;
+  int slot = 0, n = 0;
+  for (int o = 0; o < 8; ++o) {
+    if (!count[o]) continue;
+    const int64_t cnt = cross * count[o] * (int64_t)nb;
+    const bool down = o & bit;  // slab-axis component < 0: upwind side is above
+    const int to = down ? rank - 1 : rank + 1, from = down ? rank + 1 : rank - 1;
+    if (to >= 0 && to < nranks) {
+      if (n >= BTE_MAX_MSGS) return BTE_EINVAL;
+      out->msg[n++] = bte_msg{1, to, o, slot, down ? out->m0 : out->m0 + out->n_local - 1, cnt};
+    }
+    if (from >= 0 && from < nranks) {
+      if (n >= BTE_MAX_MSGS) return BTE_EINVAL;
+      out->msg[n++] = bte_msg{0, from, o, slot, down ? out->m0 + out->n_local : out->m0 - 1, cnt};
+    }
+    ++slot;
+  }
+  out->n_msgs = n;
+  return BTE_OK;
+}
 
 bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands, const bte_run *run,
                       bte_ctx **out) {
@@ -287,15 +326,10 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   g.ncross = mesh->dim == 3 ? (int)(mesh->nx * mesh->ny) : (int)mesh->nx;
   const int64_t nm = mesh->dim == 3 ? mesh->nz : mesh->ny;
   g.nplanes_global = nm;
-  {
-    const int64_t P = ctx->nranks, r = ctx->rank;
-    const int64_t base = nm / P, rem = nm % P;
-    const int64_t n_r = base + (r < rem ? 1 : 0);
-    const int64_t m0 = r * base + std::min<int64_t>(r, rem);
-    if (n_r < 1) return bail(fail(ctx, BTE_EINVAL, "more ranks than planes along the slab axis"));
-    g.nplanes = (int)n_r;
-    g.m0 = m0;
-  }
+  if (bte_plan_slab(mesh, dirs, ctx->nb, ctx->nranks, ctx->rank, &ctx->plan) != BTE_OK)
+    return bail(fail(ctx, BTE_EINVAL, "more ranks than planes along the slab axis"));
+  g.nplanes = (int)ctx->plan.n_local;
+  g.m0 = ctx->plan.m0;
   g.plane_off = ctx->nranks > 1 ? 1 : 0;
   g.has_lo_wall = (ctx->rank == 0) ? 1 : 0;
   g.has_hi_wall = (ctx->rank == ctx->nranks - 1) ? 1 : 0;
@@ -408,11 +442,12 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   const int64_t ncl = ctx->ncells_local;
   ctx->I0c = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
   ctx->beta = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+  ctx->dI0c = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
   ctx->T = (double *)dev_alloc(ctx, ncl * sizeof(double));
   ctx->Dpart = (double *)dev_alloc(ctx, ncl * nslot * ctx->nb * sizeof(double));
   ctx->d_err = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
   ctx->d_step = (int *)dev_alloc(ctx, sizeof(int));
-  if (!ctx->I0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err || !ctx->d_step)
+  if (!ctx->I0c || !ctx->dI0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err || !ctx->d_step)
     return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
   CU(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), ctx->stream));
   CU(cudaMemsetAsync(ctx->d_step, 0, sizeof(int), ctx->stream));
@@ -440,6 +475,9 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   if (const char *e = getenv("BTE_SWEEP")) ctx->use_tma = strcmp(e, "plain") != 0;
   if (const char *e = getenv("BTE_STAGES")) ctx->stages_override = atoi(e);
   if (const char *e = getenv("BTE_SEGS")) ctx->seg_override = atoi(e);
+  if (const char *e = getenv("BTE_THREADS")) ctx->target_threads = atoi(e);
+  if (const char *e = getenv("BTE_SMEM_KB")) ctx->smem_budget_kb = atoi(e);
+  if (const char *e = getenv("BTE_STCS")) ctx->stcs = atoi(e);
   // segment length along the march axis: enough CTAs for >= ~16 per SM
   {
     const int64_t cols = (int64_t)g.ncross * nslot;
@@ -461,10 +499,11 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   // ---- initial state: equilibrium at T_init
   std::vector<double> T0(ncl, ctx->T_init);
   CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->beta, ctx->stream));
+  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
   CU(launch_fill_equilibrium(g, ctx->I0c, ctx->I[0], ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
   ctx->cur = 0;
+  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
+  CU(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
   return BTE_OK;
 }
@@ -529,6 +568,7 @@ static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
 }
 
 static bte_status run_newton(bte_ctx *ctx, const int *step_ctr);
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   if (!ctx) return BTE_EINVAL;
@@ -552,12 +592,13 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
     std::vector<double> T0(ncl, ctx->T_init);
     CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   }
-  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->beta, ctx->stream));
+  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
   if (I) {
     if ((st = transfer_I(ctx, const_cast<double *>(I), 1))) return st;
   } else {
     CU(launch_fill_equilibrium(ctx->g, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
   }
+  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   if (I && !T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
@@ -581,8 +622,9 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
   if (!(T_mean - std::fabs(T_amp) > 0)) return fail(ctx, BTE_EINVAL, "random start would give T <= 0");
   const bte_mesh &m = ctx->mesh;
   CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
-  CU(launch_refresh(ctx->m, ctx->T, ctx->ncells_local, ctx->I0c, ctx->beta, ctx->stream));
+  CU(launch_refresh(ctx->m, ctx->T, ctx->ncells_local, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
   CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
+  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   CU(cudaStreamSynchronize(ctx->stream));
   return BTE_OK;
 }
@@ -624,6 +666,9 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.seg_len = ctx->seg_len;
   a.use_tma = ctx->use_tma;
   a.stages_override = ctx->stages_override;
+  a.target_threads = ctx->target_threads;
+  a.smem_budget_kb = ctx->smem_budget_kb;
+  a.stcs = ctx->stcs;
   a.step_ctr = step_ctr;
   CU(launch_sweep(a, ctx->stream));
   ctx->tacc.launches++;
@@ -637,7 +682,8 @@ static bte_status run_newton(bte_ctx *ctx, const int *step_ctr) {
   a.Dpart = ctx->Dpart;
   a.T = ctx->T;
   a.I0c = ctx->I0c;
-  a.beta = ctx->beta;
+  a.dI0c = ctx->dI0c;
+  a.beta_next = ctx->beta;
   a.nslot = ctx->g.nslot;
   a.nb = ctx->nb;
   for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
@@ -687,34 +733,17 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
 }
 
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf) {
-  // a5: send the owned boundary planes of the octants whose march-axis upwind
-  // side points at the neighbour, receive into the halo planes.
+  // a5: execute this rank's halo plan (bte_plan_slab) as one NCCL group on the
+  // context stream; plane p (global) lives at local index p - m0 + plane_off.
   const Geometry &g = ctx->g;
-  const int mbit = g.dim == 3 ? 1 : 2;
   std::string emsg;
   if (nccl_shim_group_start(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
-  for (int sl = 0; sl < g.nslot; ++sl) {
-    double *base = Ibuf + (int64_t)sl * g.slot_stride;
-    const bool mneg = g.slot_oct[sl] & mbit;
-    const size_t n = (size_t)g.plane_stride;
-    if (!mneg) {
-      // upwind is below: send my last plane up, receive my low halo from below
-      if (ctx->rank + 1 < ctx->nranks &&
-          nccl_shim_send(ctx->nccl_comm, base + (int64_t)(g.nplanes - 1 + g.plane_off) * g.plane_stride, n,
-                         ctx->rank + 1, ctx->stream, &emsg))
-        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
-      if (ctx->rank > 0 && nccl_shim_recv(ctx->nccl_comm, base, n, ctx->rank - 1, ctx->stream, &emsg))
-        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
-    } else {
-      if (ctx->rank > 0 &&
-          nccl_shim_send(ctx->nccl_comm, base + (int64_t)g.plane_off * g.plane_stride, n, ctx->rank - 1, ctx->stream,
-                         &emsg))
-        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
-      if (ctx->rank + 1 < ctx->nranks &&
-          nccl_shim_recv(ctx->nccl_comm, base + (int64_t)(g.nplanes + g.plane_off) * g.plane_stride, n, ctx->rank + 1,
-                         ctx->stream, &emsg))
-        return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
-    }
+  for (int k = 0; k < ctx->plan.n_msgs; ++k) {
+    const bte_msg &m = ctx->plan.msg[k];
+    double *ptr = Ibuf + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+    const int rc = m.send ? nccl_shim_send(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, ctx->stream, &emsg)
+                          : nccl_shim_recv(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, ctx->stream, &emsg);
+    if (rc) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
   }
   if (nccl_shim_group_end(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
   return BTE_OK;

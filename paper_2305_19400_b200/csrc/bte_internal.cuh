@@ -73,9 +73,13 @@ struct SweepArgs {
   double dt;
   int seg_len;            // cells per CTA along the march axis
   int jpt;                // directions per thread (set by launch_sweep)
+  int jg;                 // thread groups (set by launch_sweep)
   int use_tma;            // cp.async.bulk pipeline (k_sweep_tma) when the layout allows
   int stages;             // pipeline depth (set by launch_sweep)
   int stages_override;    // 0 = automatic
+  int target_threads;     // CTA size target (0 = 448)
+  int smem_budget_kb;     // per-CTA shared memory budget for the stage ring (0 = 113 KB)
+  int stcs;               // streaming (evict-first) stores of I^{n+1}
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int *step_ctr;
 };
@@ -83,7 +87,7 @@ struct SweepArgs {
 struct NewtonArgs {
   Material m;
   const double *Dpart;
-  double *T, *I0c, *beta;
+  double *T, *I0c, *dI0c, *beta_next;
   int nslot, nb;
   int slot_oct[kMaxSlots];
   double W;
@@ -100,7 +104,7 @@ cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, doubl
 cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,
                              cudaStream_t s);
 cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c,
-                           double *beta, cudaStream_t s);
+                           double *dI0c, double *beta, cudaStream_t s);
 cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I,
                                     cudaStream_t s);
 cudaError_t launch_permute(const Geometry &g, const int *dmap, int nd, const double *canon,

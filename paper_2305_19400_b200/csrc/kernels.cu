@@ -71,6 +71,18 @@ __device__ __forceinline__ double ghost_value(const Geometry &g, const double *_
   return ldg(g.gtab[region] + face * g.nb + b);
 }
 
+// Element update shared by both sweeps.  Flux in axis order x, y, z (per-axis
+// difference form, reading #19), v_b factored out of the face sum as in Eq. 5:
+//   I^{n+1} = I + dt*beta*(I0c - I) - v_b * sum_a (dt|s_a|/D_a) (I - I_up,a)
+template <int DIM>
+__device__ __forceinline__ double bte_update(double Ic, double xu, double yu, double mu, const double *cf,
+                                             double v, double I0, double dtb) {
+  double fl = cf[0] * (Ic - xu);
+  if (DIM == 3) fl = fma(cf[1], Ic - yu, fl);
+  fl = fma(cf[DIM - 1], Ic - mu, fl);
+  return fma(dtb, I0 - Ic, Ic) - v * fl;
+}
+
 // One CTA = one (cross cell, octant slot, segment of the march axis).  The CTA
 // walks its column in the upwind-to-downwind order of that octant, so the
 // march-axis upwind value is the previous iteration's I^n kept in registers.
@@ -114,7 +126,6 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
     yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
   }
   const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
-  const int max_axis = DIM - 1;  // march axis index (2 for z, 1 for y)
 
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
 
@@ -184,13 +195,9 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
             }
           }
           const double *cf = coef + 4 * j;
-          // flux terms in axis order x, y, z (per-axis difference form, reading #19)
-          double fl = (cf[0] * v) * (Ic - xu);
-          if (DIM == 3) fl += (cf[1] * v) * (Ic - yu);
-          fl += (cf[max_axis] * v) * (Ic - prev[k]);
-          const double In = Ic + dtb * (I0 - Ic) - fl;
+          const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cf, v, I0, dtb);
           Os[base + e] = In;
-          acc += cf[3] * (I0 - In);
+          acc = fma(cf[3], I0 - In, acc);
           prev[k] = Ic;
         }
       }
@@ -241,23 +248,26 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-// Same decomposition and arithmetic as k_sweep, but the (cell, octant) blocks
-// of the cell and of its cross-axis upwind neighbours (16 KB each at 50 x 40),
-// plus the cell's I0c/beta rows, stream into an S-stage shared-memory ring with
-// cp.async.bulk + mbarrier, issued S cells ahead by one thread.  Keeps
-// S x (2 or 3) x 16 KB of HBM/L2 reads in flight per CTA.
-template <int DIM, int JMAX>
+// Same decomposition as k_sweep, but the (cell, octant) blocks of the cell and
+// of its cross-axis upwind neighbours (16 KB each at 50 x 40), plus the cell's
+// I0c/beta rows, stream into an S-stage shared-memory ring with cp.async.bulk
+// + mbarrier, issued S cells ahead by one thread.  Keeps S x (2 or 3) x 16 KB
+// of HBM/L2 reads in flight per CTA.  NBT > 0 fixes the channel count at
+// compile time (immediate smem/global offsets); NBT = 0 is the generic path.
+template <int DIM, int JMAX, int NBT>
 __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
-  const int nb = g.nb, nj = g.nj, E = g.E;
+  const int nb = NBT > 0 ? NBT : g.nb;
+  const int nj = g.nj, E = g.E;
   const int S = A.stages;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
   const int b = tid - grp * nb;
-  const int JG = blockDim.x / nb;
+  const int JG = A.jg;
   const int j0 = grp * A.jpt;
   const int nloc = max(0, min(A.jpt, nj - j0));
+  const bool active = grp < JG;
 
   const int slot = blockIdx.y;
   const int oct = g.slot_oct[slot];
@@ -278,8 +288,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     yregion = yneg ? 3 : 2;
     yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
   }
+  const bool interior = !xghost && !yghost;
   const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
-  const int max_axis = DIM - 1;
 
   // shared memory carve-up
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);          // [S] (S <= 16)
@@ -326,8 +336,9 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   if (tid == 0)
     for (int i = 0; i < min(S, np); ++i) issue(i, i);
 
-  const double v = A.v[b];
-  const bool active = grp < JG;
+  const double v = A.v[active ? b : 0];
+  const int e0 = j0 * nb + b;  // this thread's first element; element k is e0 + k*nb
+  const double *cq = coef + 4 * j0;
   double prev[JMAX];
   {
     const int p = pfirst;
@@ -339,9 +350,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     for (int k = 0; k < JMAX; ++k) {
       prev[k] = 0.0;
       if (active && k < nloc) {
-        const int e = (j0 + k) * nb + b;
         if (stored)
-          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e);
+          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e0 + k * nb);
         else
           prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
       }
@@ -354,42 +364,53 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     const int st = i % S;
     const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
     const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
-    const int64_t mg = g.m0 + p;
     const double *sp = stage0 + st * sd;
     mbar_wait(&full[st], (uint32_t)((i / S) & 1));
     double acc = 0.0;
     if (active) {
       const double I0 = sp[o_i0 + b];
       const double dtb = dt * sp[o_be + b];
+      const double *so = sp + e0;
+      double *op = Os + base + e0;
+      if (interior && nloc == JMAX) {
+        const double *sx = so + o_x;
+        const double *sy = so + o_y;
 #pragma unroll
-      for (int k = 0; k < JMAX; ++k) {
-        if (k < nloc) {
-          const int j = j0 + k;
-          const int e = j * nb + b;
-          const double Ic = sp[e];
-          double xu, yu = 0.0;
-          if (!xghost) {
-            xu = sp[o_x + e];
-          } else {
-            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
-            xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
-          }
-          if (DIM == 3) {
-            if (!yghost) {
-              yu = sp[o_y + e];
-            } else {
-              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
-              yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
-            }
-          }
-          const double *cf = coef + 4 * j;
-          double fl = (cf[0] * v) * (Ic - xu);
-          if (DIM == 3) fl += (cf[1] * v) * (Ic - yu);
-          fl += (cf[max_axis] * v) * (Ic - prev[k]);
-          const double In = Ic + dtb * (I0 - Ic) - fl;
-          Os[base + e] = In;
-          acc += cf[3] * (I0 - In);
+        for (int k = 0; k < JMAX; ++k) {
+          const double Ic = so[k * nb];
+          const double In = bte_update<DIM>(Ic, sx[k * nb], DIM == 3 ? sy[k * nb] : 0.0, prev[k], cq + 4 * k, v,
+                                            I0, dtb);
+          __stcs(op + k * nb, In);  // evict-first: I^{n+1} is not re-read this step
+          acc = fma(cq[4 * k + 3], I0 - In, acc);
           prev[k] = Ic;
+        }
+      } else {
+        const int64_t mg = g.m0 + p;
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+          if (k < nloc) {
+            const int j = j0 + k;
+            const double Ic = so[k * nb];
+            double xu, yu = 0.0;
+            if (!xghost) {
+              xu = so[o_x + k * nb];
+            } else {
+              const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+              xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
+            }
+            if (DIM == 3) {
+              if (!yghost) {
+                yu = so[o_y + k * nb];
+              } else {
+                const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+                yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
+              }
+            }
+            const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cq + 4 * k, v, I0, dtb);
+            __stcs(op + k * nb, In);
+            acc = fma(cq[4 * k + 3], I0 - In, acc);
+            prev[k] = Ic;
+          }
         }
       }
     }
@@ -412,8 +433,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
 }
 
 // thread shape: JG groups of nb threads, jpt directions per thread
-static void sweep_shape(int nb, int nj, int *jpt, int *JG) {
-  int jg = (448 + nb / 2) / nb;
+static void sweep_shape(int nb, int nj, int target, int *jpt, int *JG) {
+  int jg = (target + nb / 2) / nb;
   jg = std::max(1, std::min(jg, nj));
   while (jg * nb > 1024) --jg;
   if (jg < 1) jg = 1;
@@ -428,43 +449,53 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
   SweepArgs a = a0;
   const Geometry &g = a.g;
   int jpt, JG;
-  sweep_shape(g.nb, g.nj, &jpt, &JG);
+  sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 448, &jpt, &JG);
   a.jpt = jpt;
   const int threads = JG * g.nb;
   if (threads > 1024 || g.nb > 1024) return cudaErrorInvalidConfiguration;
   const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
   dim3 grid(g.ncross, g.nslot, nseg);
-  const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 16 ? 16 : 0;
+  const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.E % 2 == 0) && (g.nb % 2 == 0);
   if (tma) {
     // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B
     const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.E + 2 * g.nb + 15) / 16 * 16;
     const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
-    const size_t budget = 113 * 1024;  // two CTAs per SM
+    const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;  // two CTAs/SM
     int S = (int)((budget > fixed ? budget - fixed : 0) / (stage_d * sizeof(double)));
     S = std::max(2, std::min(4, S));
     if (a.stages_override > 0) S = std::min(16, a.stages_override);
     a.stages = S;
     a.stage_doubles = stage_d;
+    a.jg = JG;
     const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    switch (jcase) {
-#define BTE_CASE(N)                                                                         \
-  case N:                                                                                   \
-    cudaFuncSetAttribute(k_sweep_tma<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                         (int)smem);                                                        \
-    k_sweep_tma<DIM, N><<<grid, threads, smem, s>>>(a);                                     \
-    break;
-      BTE_CASE(1)
-      BTE_CASE(2)
-      BTE_CASE(4)
-      BTE_CASE(5)
-      BTE_CASE(8)
-      BTE_CASE(16)
-#undef BTE_CASE
-      default:
-        return cudaErrorInvalidConfiguration;
+    const int tthreads = (threads + 31) / 32 * 32;
+#define BTE_LAUNCH(N, NB)                                                                        \
+  {                                                                                              \
+    cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                         (int)smem);                                                             \
+    k_sweep_tma<DIM, N, NB><<<grid, tthreads, smem, s>>>(a);                                     \
+    break;                                                                                       \
+  }
+    if (g.nb == 40 && jcase == 5) {
+      switch (0) { default: BTE_LAUNCH(5, 40) }
+    } else if (g.nb == 55 && jcase == 8) {
+      switch (0) { default: BTE_LAUNCH(8, 55) }
+    } else {
+      switch (jcase) {
+        case 1: BTE_LAUNCH(1, 0)
+        case 2: BTE_LAUNCH(2, 0)
+        case 4: BTE_LAUNCH(4, 0)
+        case 5: BTE_LAUNCH(5, 0)
+        case 8: BTE_LAUNCH(8, 0)
+        case 10: BTE_LAUNCH(10, 0)
+        case 16: BTE_LAUNCH(16, 0)
+        default:
+          return cudaErrorInvalidConfiguration;
+      }
     }
+#undef BTE_LAUNCH
     return cudaGetLastError();
   }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
@@ -481,6 +512,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
     BTE_CASE(4)
     BTE_CASE(5)
     BTE_CASE(8)
+    BTE_CASE(10)
     BTE_CASE(16)
 #undef BTE_CASE
     default:
@@ -578,109 +610,161 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // bitwise identical in every lane (IEEE addition is commutative)
 }
 
-constexpr int kNewtonWarps = 4;
-constexpr int kMaxBandsPerLane = kMaxBands / 32;
+constexpr int kNewtonWarps = 8;
 
-// One warp per cell.  Lane l owns channels b = l, l+32, ...
+// a3 + a4.  One warp per cell (persistent grid, warps stride over cells).
+// Channel-wise work (octant tree, beta_next, c_b) uses lanes over channels;
+// the band integrals use lanes over (channel, Gauss node) pairs: lane l owns
+// node j = l & 15 of channels b = (l >> 4) + 2m, so every lane evaluates
+// ceil(nb/2) expm1 per F(T) instead of 16 * ceil(nb/32).
+//   F(T)  = W sum_b c_b I0_b(T) + K0,  K0 = sum_b c_b (D_b - W I0c_b)
+//   F'(T) = W sum_b c_b dI0_b/dT
+// F(T^n) = sum_b c_b D_b exactly (I0c = I0(T^n)) and F'(T^n) uses the dI0/dT
+// stored by the previous refresh, so the first Newton step costs no integral.
 __global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * kNewtonWarps + (threadIdx.x >> 5);
-  if (c >= a.ncells) return;
+  extern __shared__ double nsh[];
   const int nb = a.nb;
-  const double Tn = a.T[c];
-  double D[kMaxBandsPerLane], cb[kMaxBandsPerLane], bn[kMaxBandsPerLane], I0c[kMaxBandsPerLane];
-  double F0 = 0.0;
-#pragma unroll
-  for (int k = 0; k < kMaxBandsPerLane; ++k) {
-    const int b = lane + 32 * k;
-    D[k] = 0.0;
-    cb[k] = 0.0;
-    bn[k] = 0.0;
-    I0c[k] = 0.0;
-    if (b < nb) {
+  double *sA = nsh;                      // [nb*16]
+  double *sX = sA + nb * kNGL;           // [nb*16]
+  const int warp = threadIdx.x >> 5;
+  double *cs = sX + nb * kNGL + warp * nb;  // [nb] c_b of this warp's cell
+  const int lane = threadIdx.x & 31;
+  const bool be = a.m.mode != 0;
+  if (be)
+    for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
+      sA[i] = a.m.A[i];
+      sX[i] = a.m.X[i];
+    }
+  __syncthreads();
+  const int jn = lane & 15;
+  const int par = lane >> 4;
+  const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
+  for (int64_t c = (int64_t)blockIdx.x * kNewtonWarps + warp; c < a.ncells; c += nwarps) {
+    const double Tn = a.T[c];
+    double F0 = 0.0, K0 = 0.0, Fp0 = 0.0;
+    for (int b = lane; b < nb; b += 32) {
       double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = a.Dpart[(c * a.nslot + sl) * nb + b];
-      D[k] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-      bn[k] = beta_of_T(a.m.bcoef, b, Tn);
-      cb[k] = bn[k] / a.m.v[b];
-      I0c[k] = a.I0c[c * nb + b];
-      F0 += cb[k] * D[k];
+      const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+      const double bn = beta_of_T(a.m.bcoef, b, Tn);
+      const double cb = bn / a.m.v[b];
+      cs[b] = cb;
+      a.beta_next[c * nb + b] = bn;
+      F0 += cb * D;
+      K0 += cb * (D - a.W * a.I0c[c * nb + b]);
+      Fp0 += cb * (a.W * a.dI0c[c * nb + b]);
     }
-  }
-  F0 = warp_sum(F0);
-  double Tf = Tn;
-  int status = ERR_NONE;
-  if (!isfinite(F0)) {
-    status = ERR_NONFINITE;
-  } else if (F0 != 0.0) {
-    // Newton with bracket [1, 5000] K and bisection fallback (reading #18)
-    double T = Tn, lo = kTlo, hi = kThi;
-    bool conv = false;
-    for (int it = 0; it <= kNewtonMaxIt; ++it) {
-      double F = 0.0, Fp = 0.0;
-#pragma unroll
-      for (int k = 0; k < kMaxBandsPerLane; ++k) {
-        const int b = lane + 32 * k;
-        if (b < nb) {
-          double dI;
-          const double i0 = I0_of_T(a.m, b, T, &dI);
-          F += cb[k] * (a.W * (i0 - I0c[k]) + D[k]);
-          Fp += cb[k] * (a.W * dI);
+    F0 = warp_sum(F0);
+    K0 = warp_sum(K0);
+    Fp0 = warp_sum(Fp0);
+    __syncwarp();
+    double Tf = Tn;
+    int status = ERR_NONE;
+    if (!isfinite(F0) || !isfinite(K0)) {
+      status = ERR_NONFINITE;
+    } else if (F0 != 0.0) {
+      double T = Tn, lo = kTlo, hi = kThi, F = F0, Fp = Fp0;
+      bool conv = false;
+      for (int it = 0; it <= kNewtonMaxIt; ++it) {
+        if (it > 0) {
+          double f = 0.0, fp = 0.0;
+          const double rT = 1.0 / T;
+          if (be) {
+            for (int b = par; b < nb; b += 2) {
+              const double x = sX[b * kNGL + jn] * rT;
+              const double em1 = expm1(x);
+              const double r = 1.0 / em1;
+              const double t = cs[b] * (sA[b * kNGL + jn] * r);
+              f += t;
+              fp += t * x * (1.0 + r);
+            }
+            fp *= rT;
+          } else {
+            for (int b = lane; b < nb; b += 32) {
+              f += cs[b] * (a.m.I_ref[b] + a.m.slope[b] * (T - a.m.T_ref));
+              fp += cs[b] * a.m.slope[b];
+            }
+          }
+          F = a.W * warp_sum(f) + K0;
+          Fp = a.W * warp_sum(fp);
         }
+        if (!isfinite(F) || !isfinite(Fp)) {
+          status = ERR_NONFINITE;
+          break;
+        }
+        if (F == 0.0) {
+          Tf = T;
+          conv = true;
+          break;
+        }
+        if (it == kNewtonMaxIt) break;
+        if (F < 0.0)
+          lo = T;
+        else
+          hi = T;
+        const double stp = F / Fp;
+        double Tn1 = T - stp;
+        if (fabs(stp) <= kNewtonRtol * T) {  // reading R-a: step test before the bracket test
+          Tf = Tn1;
+          conv = true;
+          break;
+        }
+        if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
+        T = Tn1;
       }
-      F = warp_sum(F);
-      Fp = warp_sum(Fp);
-      if (!isfinite(F) || !isfinite(Fp)) {
-        status = ERR_NONFINITE;
-        break;
-      }
-      if (F == 0.0) {
-        Tf = T;
-        conv = true;
-        break;
-      }
-      if (it == kNewtonMaxIt) break;
-      if (F < 0.0)
-        lo = T;
-      else
-        hi = T;
-      const double stp = F / Fp;
-      double Tn1 = T - stp;
-      if (fabs(stp) <= kNewtonRtol * T) {
-        Tf = Tn1;
-        conv = true;
-        break;
-      }
-      if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
-      T = Tn1;
+      if (!conv && status == ERR_NONE) status = ERR_NEWTON;
     }
-    if (!conv && status == ERR_NONE) status = ERR_NEWTON;
-  }
-  if (status != ERR_NONE) {
-    if (lane == 0) {
-      const unsigned long long stepi = a.step_ctr ? (unsigned long long)(*a.step_ctr - 1) : 0ull;
-      const unsigned long long key = (stepi << 40) | ((unsigned long long)status << 36) |
-                                     (unsigned long long)(a.cell0_global + c);
-      atomicMin(a.err, key);
+    if (status != ERR_NONE) {
+      if (lane == 0) {
+        const unsigned long long stepi = a.step_ctr ? (unsigned long long)(*a.step_ctr - 1) : 0ull;
+        const unsigned long long key = (stepi << 40) | ((unsigned long long)status << 36) |
+                                       (unsigned long long)(a.cell0_global + c);
+        atomicMin(a.err, key);
+      }
+      __syncwarp();
+      continue;
     }
-    return;
-  }
-  if (lane == 0) a.T[c] = Tf;
+    if (Tf != Tn) {
+      // refresh I0c = I0(T^{n+1}) and its derivative
+      if (lane == 0) a.T[c] = Tf;
+      if (be) {
+        const double rT = 1.0 / Tf;
+        for (int b0 = 0; b0 < nb; b0 += 2) {
+          const int b = b0 + par;
+          double f = 0.0, fp = 0.0;
+          if (b < nb) {
+            const double x = sX[b * kNGL + jn] * rT;
+            const double em1 = expm1(x);
+            const double r = 1.0 / em1;
+            f = sA[b * kNGL + jn] * r;
+            fp = f * x * (1.0 + r);
+          }
 #pragma unroll
-  for (int k = 0; k < kMaxBandsPerLane; ++k) {
-    const int b = lane + 32 * k;
-    if (b < nb) {
-      if (Tf != Tn) a.I0c[c * nb + b] = I0_of_T(a.m, b, Tf, nullptr);
-      a.beta[c * nb + b] = bn[k];
+          for (int o = 8; o > 0; o >>= 1) {
+            f += __shfl_xor_sync(0xffffffffu, f, o);
+            fp += __shfl_xor_sync(0xffffffffu, fp, o);
+          }
+          if (jn == 0 && b < nb) {
+            a.I0c[c * nb + b] = f;
+            a.dI0c[c * nb + b] = fp * rT;
+          }
+        }
+      } else {
+        for (int b = lane; b < nb; b += 32) a.I0c[c * nb + b] = a.m.I_ref[b] + a.m.slope[b] * (Tf - a.m.T_ref);
+      }
     }
+    __syncwarp();
   }
 }
 
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   if (a.nb > kMaxBands) return cudaErrorInvalidValue;
-  const int64_t nblk = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
-  if (nblk == 0) return cudaSuccess;
-  k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, 0, s>>>(a);
+  if (a.ncells == 0) return cudaSuccess;
+  const int64_t need = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
+  const int64_t nblk = std::min<int64_t>(need, 148 * 8);
+  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * a.nb) * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -704,21 +788,23 @@ cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, do
 }
 
 __global__ void k_refresh(const Material m, const double *__restrict__ T, int64_t nc,
-                          double *__restrict__ I0c, double *__restrict__ beta) {
+                          double *__restrict__ I0c, double *__restrict__ dI0c, double *__restrict__ beta) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nc * m.nb) return;
   const int64_t c = i / m.nb;
   const int b = (int)(i - c * m.nb);
   const double t = T[c];
-  I0c[i] = I0_of_T(m, b, t, nullptr);
+  double d;
+  I0c[i] = I0_of_T(m, b, t, &d);
+  dI0c[i] = d;
   beta[i] = beta_of_T(m.bcoef, b, t);
 }
 
-cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c, double *beta,
-                           cudaStream_t s) {
+cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c, double *dI0c,
+                           double *beta, cudaStream_t s) {
   const int64_t n = nc * m.nb;
   if (n == 0) return cudaSuccess;
-  k_refresh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, T, nc, I0c, beta);
+  k_refresh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(m, T, nc, I0c, dI0c, beta);
   return cudaGetLastError();
 }
 
