@@ -307,7 +307,9 @@ def run_b200(args):
     achieved = BYTES_PER_DOF * dof_local / (sweep_ms * 1e-3) / 1e9
     traffic = _traffic(p.name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_sweep (a1+a2 fused flux+relaxation+octant partial sums)",
+                "traffic": traffic,
+                "kernel": ("k_sweep_tma (a1+a2 fused upwind flux + relaxation + octant partial sums"
+                           + (", a3+a4 Newton fused in the tail)" if tim["newton_launches"] == 0 else ")")),
                 "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_local, "kernel_ms_avg": sweep_ms,
                 "peak_source": peak_src,
                 "step_share": {"sweep": tim["sweep_ms"] / ms, "newton": tim["newton_ms"] / ms,

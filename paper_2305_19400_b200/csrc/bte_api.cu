@@ -67,7 +67,8 @@ struct bte_ctx {
   double *gtab[6] = {nullptr};
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
-  int *d_step = nullptr;
+  int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
+  int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
   int seg_len = 0;
@@ -446,11 +447,9 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   ctx->T = (double *)dev_alloc(ctx, ncl * sizeof(double));
   ctx->Dpart = (double *)dev_alloc(ctx, ncl * nslot * ctx->nb * sizeof(double));
   ctx->d_err = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
-  ctx->d_step = (int *)dev_alloc(ctx, sizeof(int));
-  if (!ctx->I0c || !ctx->dI0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err || !ctx->d_step)
+  if (!ctx->I0c || !ctx->dI0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err)
     return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
   CU(cudaMemsetAsync(ctx->d_err, 0xFF, sizeof(unsigned long long), ctx->stream));
-  CU(cudaMemsetAsync(ctx->d_step, 0, sizeof(int), ctx->stream));
   // staging for host <-> device state transfers (canonical order), <= 256 MB
   const int64_t per_cell = (int64_t)ctx->nd * ctx->nb * sizeof(double);
   ctx->staging_cells = std::max<int64_t>(1, std::min<int64_t>(ncl, (256ll << 20) / per_cell));
@@ -478,13 +477,21 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   if (const char *e = getenv("BTE_THREADS")) ctx->target_threads = atoi(e);
   if (const char *e = getenv("BTE_SMEM_KB")) ctx->smem_budget_kb = atoi(e);
   if (const char *e = getenv("BTE_STCS")) ctx->stcs = atoi(e);
-  // segment length along the march axis: enough CTAs for >= ~16 per SM
+  // segment length along the march axis (measured on B200, configs 2 and 3):
+  // ~16 planes keeps the cross-axis neighbour columns' reads within L2 reach
+  // (short lag between adjacent columns) while the per-segment restart costs
+  // one extra upwind-plane read per 16 cells.
   {
-    const int64_t cols = (int64_t)g.ncross * nslot;
-    int nseg = (int)std::max<int64_t>(1, (148 * 16 + cols - 1) / cols);
-    nseg = std::min(nseg, std::max(1, g.nplanes / 8));
+    int nseg = std::max(1, (int)((g.nplanes + 8) / 16));
     if (ctx->seg_override > 0) nseg = std::min(ctx->seg_override, g.nplanes);
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
+  }
+  if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
+  {
+    const int64_t nseg = (g.nplanes + ctx->seg_len - 1) / ctx->seg_len;
+    ctx->d_done = (int *)dev_alloc(ctx, nseg * g.ncross * sizeof(int));
+    if (!ctx->d_done) return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
+    CU(cudaMemsetAsync(ctx->d_done, 0, nseg * g.ncross * sizeof(int), ctx->stream));
   }
 
   // ---- multi-GPU communicator
@@ -567,7 +574,7 @@ static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, const int *step_ctr);
+static bte_status run_newton(bte_ctx *ctx, int64_t step);
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
@@ -603,7 +610,7 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
     CU(launch_dpart_from_I(ctx->g, ctx->I[ctx->cur], ctx->I0c, ctx->Dpart, ctx->stream));
-    if ((st = run_newton(ctx, nullptr))) return st;
+    if ((st = run_newton(ctx, 0))) return st;
   }
   CU(cudaStreamSynchronize(ctx->stream));
   return sync_check(ctx);
@@ -653,7 +660,28 @@ static int n_diffuse(const bte_ctx *ctx) {
   return n;
 }
 
-static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, int *step_ctr) {
+static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
+  NewtonArgs a;
+  a.m = ctx->m;
+  a.Dpart = ctx->Dpart;
+  a.T = ctx->T;
+  a.I0c = ctx->I0c;
+  a.dI0c = ctx->dI0c;
+  a.beta_next = ctx->beta;
+  a.nslot = ctx->g.nslot;
+  a.nb = ctx->nb;
+  for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
+  a.W = ctx->W;
+  a.ncells = ctx->ncells_local;
+  a.cell0_global = ctx->g.m0 * ctx->g.ncross;
+  a.err = ctx->d_err;
+  a.step = step;
+  return a;
+}
+
+// a1+a2 (+ a3+a4 fused into the sweep tail when *fused is set on return)
+static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
+                                    int *fused) {
   SweepArgs a;
   a.g = ctx->g;
   a.Iin = Iin;
@@ -669,29 +697,17 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.target_threads = ctx->target_threads;
   a.smem_budget_kb = ctx->smem_budget_kb;
   a.stcs = ctx->stcs;
-  a.step_ctr = step_ctr;
-  CU(launch_sweep(a, ctx->stream));
+  a.nw = newton_args(ctx, step);
+  a.fuse_newton = allow_fuse && ctx->fuse_newton;
+  a.done = ctx->d_done;
+  CU(launch_sweep(a, ctx->stream, fused));
   ctx->tacc.launches++;
   ctx->tacc.sweep_launches++;
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, const int *step_ctr) {
-  NewtonArgs a;
-  a.m = ctx->m;
-  a.Dpart = ctx->Dpart;
-  a.T = ctx->T;
-  a.I0c = ctx->I0c;
-  a.dI0c = ctx->dI0c;
-  a.beta_next = ctx->beta;
-  a.nslot = ctx->g.nslot;
-  a.nb = ctx->nb;
-  for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
-  a.W = ctx->W;
-  a.ncells = ctx->ncells_local;
-  a.cell0_global = ctx->g.m0 * ctx->g.ncross;
-  a.err = ctx->d_err;
-  a.step_ctr = step_ctr;
+static bte_status run_newton(bte_ctx *ctx, int64_t step) {
+  NewtonArgs a = newton_args(ctx, step);
   CU(launch_newton(a, ctx->stream));
   ctx->tacc.launches++;
   ctx->tacc.newton_launches++;
@@ -716,11 +732,12 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
       if (t) CU(cudaEventRecord(ev[5], ctx->stream));
     }
     if (t) CU(cudaEventRecord(ev[0], ctx->stream));
-    if ((st = launch_sweep_step(ctx, Iin, Iout, ctx->d_step))) return st;
+    int fused = 0;
+    if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused))) return st;
     if (t) CU(cudaEventRecord(ev[1], ctx->stream));
     if (ctx->nranks > 1 && (st = halo_exchange(ctx, Iout))) return st;
     if (t) CU(cudaEventRecord(ev[2], ctx->stream));
-    if ((st = run_newton(ctx, ctx->d_step))) return st;
+    if (!fused && (st = run_newton(ctx, ctx->steps_done))) return st;
     if (t) {
       CU(cudaEventRecord(ev[3], ctx->stream));
       ctx->ev_has_bnd[ctx->timing_used] = has_bnd;
@@ -803,7 +820,8 @@ bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count)
   double *Iin = ctx->I[ctx->cur];
   double *Iout = ctx->I[1 - ctx->cur];
   if (n_diffuse(ctx) && (st = launch_boundary(ctx, Iin))) return st;
-  if ((st = launch_sweep_step(ctx, Iin, Iout, nullptr))) return st;
+  int fused = 0;
+  if ((st = launch_sweep_step(ctx, Iin, Iout, false, -1, &fused))) return st;
   if (which == 0) {
     ctx->cur = 1 - ctx->cur;  // read the swept buffer, then restore
     st = transfer_I(ctx, out, 0);

@@ -63,6 +63,18 @@ struct Geometry {
   double diff_den[6];
 };
 
+struct NewtonArgs {
+  Material m;
+  const double *Dpart;
+  double *T, *I0c, *dI0c, *beta_next;
+  int nslot, nb;
+  int slot_oct[kMaxSlots];
+  double W;
+  int64_t ncells, cell0_global;
+  unsigned long long *err;
+  int64_t step;           // step index for error reporting
+};
+
 struct SweepArgs {
   Geometry g;
   const double *Iin;
@@ -81,23 +93,14 @@ struct SweepArgs {
   int smem_budget_kb;     // per-CTA shared memory budget for the stage ring (0 = 113 KB)
   int stcs;               // streaming (evict-first) stores of I^{n+1}
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
-  int *step_ctr;
+  NewtonArgs nw;          // fused a3+a4 (k_sweep_tma tail)
+  int fuse_newton;
+  int *done;              // [nseg][ncross] tickets, zero between launches
 };
 
-struct NewtonArgs {
-  Material m;
-  const double *Dpart;
-  double *T, *I0c, *dI0c, *beta_next;
-  int nslot, nb;
-  int slot_oct[kMaxSlots];
-  double W;
-  int64_t ncells, cell0_global;
-  unsigned long long *err;
-  const int *step_ctr;
-};
 
 // kernels / launchers (kernels.cu)
-cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s);
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused);
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
                            cudaStream_t s);

@@ -212,9 +212,10 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
     }
     buf ^= 1;
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && A.step_ctr)
-    atomicAdd(A.step_ctr, 1);
 }
+
+__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, double *cs,
+                            int lane);
 
 // ---------------------------------------------------------------- TMA-pipelined sweep
 
@@ -428,8 +429,37 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     }
     buf ^= 1;
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 && A.step_ctr)
-    atomicAdd(A.step_ctr, 1);
+  if (A.fuse_newton) {
+    // a3 + a4 fused: the last of the nslot CTAs of this (column, segment) runs
+    // the Newton for its cells (threadfence + ticket), overlapping the
+    // FP64-bound solve with other CTAs' HBM streaming.
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      int *ctr = A.done + (int64_t)blockIdx.z * g.ncross + col;
+      const int old = atomicAdd(ctr, 1);
+      s_last = (old == g.nslot - 1);
+      if (s_last) *ctr = 0;  // ready for the next step
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const NewtonArgs &na = A.nw;
+      double *sA = stage0;  // stage ring is free: every stage was consumed
+      double *sX = sA + nb * kNGL;
+      const int nwarp = blockDim.x >> 5;
+      double *cs = sX + nb * kNGL + (tid >> 5) * nb;
+      if (na.m.mode != 0)
+        for (int q = tid; q < nb * kNGL; q += blockDim.x) {
+          sA[q] = na.m.A[q];
+          sX[q] = na.m.X[q];
+        }
+      __syncthreads();
+      for (int pp = pb + (tid >> 5); pp < pe; pp += nwarp)
+        newton_cell(na, (int64_t)col + (int64_t)pp * g.ncross, sA, sX, cs, tid & 31);
+    }
+  }
 }
 
 // thread shape: JG groups of nb threads, jpt directions per thread
@@ -445,8 +475,9 @@ static void sweep_shape(int nb, int nj, int target, int *jpt, int *JG) {
 }
 
 template <int DIM>
-static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
+static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fused) {
   SweepArgs a = a0;
+  *fused = 0;
   const Geometry &g = a.g;
   int jpt, JG;
   sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 448, &jpt, &JG);
@@ -468,7 +499,13 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
     a.stages = S;
     a.stage_doubles = stage_d;
     a.jg = JG;
-    const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
+    size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
+    const int tthreads0 = (threads + 31) / 32 * 32;
+    if (a.fuse_newton) {  // the Newton tail reuses the stage ring for its tables
+      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * g.nb) * sizeof(double);
+      smem = std::max(smem, need);
+      *fused = 1;
+    }
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     const int tthreads = (threads + 31) / 32 * 32;
 #define BTE_LAUNCH(N, NB)                                                                        \
@@ -498,6 +535,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
 #undef BTE_LAUNCH
     return cudaGetLastError();
   }
+  a.fuse_newton = 0;
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
   switch (jcase) {
 #define BTE_CASE(N)                                                                       \
@@ -521,8 +559,8 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s) {
-  return a.g.dim == 3 ? launch_sweep_dim<3>(a, s) : launch_sweep_dim<2>(a, s);
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused) {
+  return a.g.dim == 3 ? launch_sweep_dim<3>(a, s, fused) : launch_sweep_dim<2>(a, s, fused);
 }
 
 // ---------------------------------------------------------------- diffuse ghosts
@@ -621,140 +659,155 @@ constexpr int kNewtonWarps = 8;
 //   F'(T) = W sum_b c_b dI0_b/dT
 // F(T^n) = sum_b c_b D_b exactly (I0c = I0(T^n)) and F'(T^n) uses the dI0/dT
 // stored by the previous refresh, so the first Newton step costs no integral.
+// Newton of one cell by one warp (a3 + a4).  sA/sX: GL tables [nb][16] in
+// shared memory, cs: [nb] scratch of this warp.  Dpart is read with
+// ld.global.cg because, when fused into the sweep, other CTAs wrote it.
+__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, double *cs,
+                            int lane) {
+  const int nb = a.nb;
+  const bool be = a.m.mode != 0;
+  const int jn = lane & 15;
+  const int par = lane >> 4;
+  const double Tn = a.T[c];
+  double F0 = 0.0, K0 = 0.0, Fp0 = 0.0;
+  for (int b = lane; b < nb; b += 32) {
+    double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b);
+    const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    const double bn = beta_of_T(a.m.bcoef, b, Tn);
+    const double cb = bn / a.m.v[b];
+    cs[b] = cb;
+    a.beta_next[c * nb + b] = bn;
+    F0 += cb * D;
+    K0 += cb * (D - a.W * a.I0c[c * nb + b]);
+    Fp0 += cb * (a.W * a.dI0c[c * nb + b]);
+  }
+  F0 = warp_sum(F0);
+  K0 = warp_sum(K0);
+  Fp0 = warp_sum(Fp0);
+  __syncwarp();
+  double Tf = Tn;
+  int status = ERR_NONE;
+  if (!isfinite(F0) || !isfinite(K0)) {
+    status = ERR_NONFINITE;
+  } else if (F0 != 0.0) {
+    double T = Tn, lo = kTlo, hi = kThi, F = F0, Fp = Fp0;
+    bool conv = false;
+    for (int it = 0; it <= kNewtonMaxIt; ++it) {
+      if (it > 0) {
+        double f = 0.0, fp = 0.0;
+        const double rT = 1.0 / T;
+        if (be) {
+          for (int b = par; b < nb; b += 2) {
+            const double x = sX[b * kNGL + jn] * rT;
+            const double em1 = expm1(x);
+            const double r = 1.0 / em1;
+            const double t = cs[b] * (sA[b * kNGL + jn] * r);
+            f += t;
+            fp += t * x * (1.0 + r);
+          }
+          fp *= rT;
+        } else {
+          for (int b = lane; b < nb; b += 32) {
+            f += cs[b] * (a.m.I_ref[b] + a.m.slope[b] * (T - a.m.T_ref));
+            fp += cs[b] * a.m.slope[b];
+          }
+        }
+        F = a.W * warp_sum(f) + K0;
+        Fp = a.W * warp_sum(fp);
+      }
+      if (!isfinite(F) || !isfinite(Fp)) {
+        status = ERR_NONFINITE;
+        break;
+      }
+      if (F == 0.0) {
+        Tf = T;
+        conv = true;
+        break;
+      }
+      if (it == kNewtonMaxIt) break;
+      if (F < 0.0)
+        lo = T;
+      else
+        hi = T;
+      const double stp = F / Fp;
+      double Tn1 = T - stp;
+      if (fabs(stp) <= kNewtonRtol * T) {  // reading R-a: step test before the bracket test
+        Tf = Tn1;
+        conv = true;
+        break;
+      }
+      if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
+      T = Tn1;
+    }
+    if (!conv && status == ERR_NONE) status = ERR_NEWTON;
+  }
+  if (status != ERR_NONE) {
+    if (lane == 0) {
+      const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+                                     (unsigned long long)(a.cell0_global + c);
+      atomicMin(a.err, key);
+    }
+    __syncwarp();
+    return;
+  }
+  if (Tf != Tn) {
+    // refresh I0c = I0(T^{n+1}) and its derivative
+    if (lane == 0) a.T[c] = Tf;
+    if (be) {
+      const double rT = 1.0 / Tf;
+      for (int b0 = 0; b0 < nb; b0 += 2) {
+        const int b = b0 + par;
+        double f = 0.0, fp = 0.0;
+        if (b < nb) {
+          const double x = sX[b * kNGL + jn] * rT;
+          const double em1 = expm1(x);
+          const double r = 1.0 / em1;
+          f = sA[b * kNGL + jn] * r;
+          fp = f * x * (1.0 + r);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          f += __shfl_xor_sync(0xffffffffu, f, o);
+          fp += __shfl_xor_sync(0xffffffffu, fp, o);
+        }
+        if (jn == 0 && b < nb) {
+          a.I0c[c * nb + b] = f;
+          a.dI0c[c * nb + b] = fp * rT;
+        }
+      }
+    } else {
+      for (int b = lane; b < nb; b += 32) a.I0c[c * nb + b] = a.m.I_ref[b] + a.m.slope[b] * (Tf - a.m.T_ref);
+    }
+  }
+  __syncwarp();
+}
+
+// a3 + a4 as a separate kernel: one warp per cell, persistent grid.
+// Channel-wise work (octant tree, beta_next, c_b) uses lanes over channels;
+// the band integrals use lanes over (channel, Gauss node) pairs: lane l owns
+// node j = l & 15 of channels b = (l >> 4) + 2m, so every lane evaluates
+// ceil(nb/2) expm1 per F(T).
+//   F(T)  = W sum_b c_b I0_b(T) + K0,  K0 = sum_b c_b (D_b - W I0c_b)
+//   F'(T) = W sum_b c_b dI0_b/dT
+// F(T^n) = sum_b c_b D_b exactly (I0c = I0(T^n)) and F'(T^n) uses the dI0/dT
+// stored by the previous refresh, so the first Newton step costs no integral.
 __global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a) {
   extern __shared__ double nsh[];
   const int nb = a.nb;
-  double *sA = nsh;                      // [nb*16]
-  double *sX = sA + nb * kNGL;           // [nb*16]
+  double *sA = nsh;
+  double *sX = sA + nb * kNGL;
   const int warp = threadIdx.x >> 5;
-  double *cs = sX + nb * kNGL + warp * nb;  // [nb] c_b of this warp's cell
-  const int lane = threadIdx.x & 31;
-  const bool be = a.m.mode != 0;
-  if (be)
+  double *cs = sX + nb * kNGL + warp * nb;
+  if (a.m.mode != 0)
     for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
       sA[i] = a.m.A[i];
       sX[i] = a.m.X[i];
     }
   __syncthreads();
-  const int jn = lane & 15;
-  const int par = lane >> 4;
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
-  for (int64_t c = (int64_t)blockIdx.x * kNewtonWarps + warp; c < a.ncells; c += nwarps) {
-    const double Tn = a.T[c];
-    double F0 = 0.0, K0 = 0.0, Fp0 = 0.0;
-    for (int b = lane; b < nb; b += 32) {
-      double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = a.Dpart[(c * a.nslot + sl) * nb + b];
-      const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-      const double bn = beta_of_T(a.m.bcoef, b, Tn);
-      const double cb = bn / a.m.v[b];
-      cs[b] = cb;
-      a.beta_next[c * nb + b] = bn;
-      F0 += cb * D;
-      K0 += cb * (D - a.W * a.I0c[c * nb + b]);
-      Fp0 += cb * (a.W * a.dI0c[c * nb + b]);
-    }
-    F0 = warp_sum(F0);
-    K0 = warp_sum(K0);
-    Fp0 = warp_sum(Fp0);
-    __syncwarp();
-    double Tf = Tn;
-    int status = ERR_NONE;
-    if (!isfinite(F0) || !isfinite(K0)) {
-      status = ERR_NONFINITE;
-    } else if (F0 != 0.0) {
-      double T = Tn, lo = kTlo, hi = kThi, F = F0, Fp = Fp0;
-      bool conv = false;
-      for (int it = 0; it <= kNewtonMaxIt; ++it) {
-        if (it > 0) {
-          double f = 0.0, fp = 0.0;
-          const double rT = 1.0 / T;
-          if (be) {
-            for (int b = par; b < nb; b += 2) {
-              const double x = sX[b * kNGL + jn] * rT;
-              const double em1 = expm1(x);
-              const double r = 1.0 / em1;
-              const double t = cs[b] * (sA[b * kNGL + jn] * r);
-              f += t;
-              fp += t * x * (1.0 + r);
-            }
-            fp *= rT;
-          } else {
-            for (int b = lane; b < nb; b += 32) {
-              f += cs[b] * (a.m.I_ref[b] + a.m.slope[b] * (T - a.m.T_ref));
-              fp += cs[b] * a.m.slope[b];
-            }
-          }
-          F = a.W * warp_sum(f) + K0;
-          Fp = a.W * warp_sum(fp);
-        }
-        if (!isfinite(F) || !isfinite(Fp)) {
-          status = ERR_NONFINITE;
-          break;
-        }
-        if (F == 0.0) {
-          Tf = T;
-          conv = true;
-          break;
-        }
-        if (it == kNewtonMaxIt) break;
-        if (F < 0.0)
-          lo = T;
-        else
-          hi = T;
-        const double stp = F / Fp;
-        double Tn1 = T - stp;
-        if (fabs(stp) <= kNewtonRtol * T) {  // reading R-a: step test before the bracket test
-          Tf = Tn1;
-          conv = true;
-          break;
-        }
-        if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
-        T = Tn1;
-      }
-      if (!conv && status == ERR_NONE) status = ERR_NEWTON;
-    }
-    if (status != ERR_NONE) {
-      if (lane == 0) {
-        const unsigned long long stepi = a.step_ctr ? (unsigned long long)(*a.step_ctr - 1) : 0ull;
-        const unsigned long long key = (stepi << 40) | ((unsigned long long)status << 36) |
-                                       (unsigned long long)(a.cell0_global + c);
-        atomicMin(a.err, key);
-      }
-      __syncwarp();
-      continue;
-    }
-    if (Tf != Tn) {
-      // refresh I0c = I0(T^{n+1}) and its derivative
-      if (lane == 0) a.T[c] = Tf;
-      if (be) {
-        const double rT = 1.0 / Tf;
-        for (int b0 = 0; b0 < nb; b0 += 2) {
-          const int b = b0 + par;
-          double f = 0.0, fp = 0.0;
-          if (b < nb) {
-            const double x = sX[b * kNGL + jn] * rT;
-            const double em1 = expm1(x);
-            const double r = 1.0 / em1;
-            f = sA[b * kNGL + jn] * r;
-            fp = f * x * (1.0 + r);
-          }
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) {
-            f += __shfl_xor_sync(0xffffffffu, f, o);
-            fp += __shfl_xor_sync(0xffffffffu, fp, o);
-          }
-          if (jn == 0 && b < nb) {
-            a.I0c[c * nb + b] = f;
-            a.dI0c[c * nb + b] = fp * rT;
-          }
-        }
-      } else {
-        for (int b = lane; b < nb; b += 32) a.I0c[c * nb + b] = a.m.I_ref[b] + a.m.slope[b] * (Tf - a.m.T_ref);
-      }
-    }
-    __syncwarp();
-  }
+  for (int64_t c = (int64_t)blockIdx.x * kNewtonWarps + warp; c < a.ncells; c += nwarps)
+    newton_cell(a, c, sA, sX, cs, threadIdx.x & 31);
 }
 
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
