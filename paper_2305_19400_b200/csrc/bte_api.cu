@@ -405,6 +405,39 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     }
   }
 
+  // uniform band grid detection (exact): channel b spans [i_b dw, (i_b + 1) dw]
+  std::vector<int> ichan;
+  std::vector<double> Ugl(kNGL);
+  int uniform = 0, imax = 0;
+  double Xd = 0;
+  if (bands->mode == BTE_I0_BOSE_EINSTEIN) {
+    const double dw = bands->w_hi[0] - bands->w_lo[0];
+    uniform = dw > 0;
+    std::vector<int> ib(ctx->nb);
+    for (int b = 0; b < ctx->nb && uniform; ++b) {
+      const double q = std::nearbyint(bands->w_lo[b] / dw);
+      if (!(q >= 0 && q < 4096) || bands->w_lo[b] != q * dw || bands->w_hi[b] != (q + 1.0) * dw) uniform = 0;
+      ib[b] = (int)q;
+      imax = std::max(imax, ib[b]);
+    }
+    if (uniform) {
+      ichan.assign(4 * (imax + 1), -1);
+      for (int b = 0; b < ctx->nb && uniform; ++b) {
+        int q = 0;
+        while (q < 4 && ichan[4 * ib[b] + q] >= 0) ++q;
+        if (q == 4) uniform = 0;  // > 4 channels share one band: use the direct path
+        else ichan[4 * ib[b] + q] = b;
+      }
+    }
+    if (const char *e = getenv("BTE_I0_DIRECT")) uniform = uniform && !atoi(e);
+    Xd = kHbar * dw / kKB;
+    for (int j = 0; j < kNGL; ++j) Ugl[j] = 0.5 * (1.0 + kGL16[j][0]);
+  }
+  if (!uniform) {
+    ichan.assign(4, -1);
+    imax = 0;
+  }
+
   if ((st = check_dt(ctx)) != BTE_OK) return bail(st);
 
   // ---- device allocations
@@ -433,6 +466,29 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   ctx->m.T_ref = bands->T_ref;
   ctx->m.A = d_A;
   ctx->m.X = d_X;
+  {
+    double *d_U;
+    int *d_ichan;
+    if ((st = upload(ctx, &d_U, Ugl.data(), Ugl.size()))) return bail(st);
+    if ((st = upload(ctx, &d_ichan, ichan.data(), ichan.size()))) return bail(st);
+    ctx->m.uniform = uniform;
+    ctx->m.imax = imax;
+    ctx->m.Xd = Xd;
+    ctx->m.U = d_U;
+    ctx->m.ichan = d_ichan;
+    int maxcnt = 0;
+    for (int i = 0; i <= imax; ++i) {
+      int c = 0;
+      while (c < 4 && ichan[4 * i + c] >= 0) ++c;
+      maxcnt = std::max(maxcnt, c);
+    }
+    ctx->m.maxcnt = maxcnt;
+    std::vector<double> rv(ctx->nb);
+    for (int b = 0; b < ctx->nb; ++b) rv[b] = 1.0 / ctx->v[b];
+    double *d_rv;
+    if ((st = upload(ctx, &d_rv, rv.data(), rv.size()))) return bail(st);
+    ctx->m.rv = d_rv;
+  }
 
   const size_t ibytes = (size_t)g.slot_stride * nslot * sizeof(double);
   for (int k = 0; k < 2; ++k) {

@@ -37,6 +37,15 @@ struct Material {
   double T_ref;
   const double *A;        // [nb][16] g hbar/(8pi^3) * half * wgl_j * w_j * k_j^2
   const double *X;        // [nb][16] hbar w_j / kB
+  // uniform band grid (every channel spans [i*dw, (i+1)*dw], detected exactly):
+  // exp(hbar w_ij / kB T) = exp(a u_j) r^i, a = Xd/T, r = exp(a), u_j = (1 + x_j)/2
+  int uniform;
+  int imax;
+  double Xd;              // hbar dw / kB
+  const double *U;        // [16] u_j
+  const int *ichan;       // [imax+1][4] channels with band index i (-1 padded)
+  int maxcnt;             // max channels sharing one band index
+  const double *rv;       // [nb] 1 / v_b
 };
 
 struct Geometry {

@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   }
 }
 
-__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, double *cs,
-                            int lane);
+__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
+                            double *cs, int lane);
 
 // ---------------------------------------------------------------- TMA-pipelined sweep
 
@@ -240,6 +240,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 // TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -255,7 +264,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // + mbarrier, issued S cells ahead by one thread.  Keeps S x (2 or 3) x 16 KB
 // of HBM/L2 reads in flight per CTA.  NBT > 0 fixes the channel count at
 // compile time (immediate smem/global offsets); NBT = 0 is the generic path.
-template <int DIM, int JMAX, int NBT>
+template <int DIM, int JMAX, int NBT, bool FUSE>
 __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -429,7 +438,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     }
     buf ^= 1;
   }
-  if (A.fuse_newton) {
+  if (FUSE) {
     // a3 + a4 fused: the last of the nslot CTAs of this (column, segment) runs
     // the Newton for its cells (threadfence + ticket), overlapping the
     // FP64-bound solve with other CTAs' HBM streaming.
@@ -450,14 +459,17 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
       double *sX = sA + nb * kNGL;
       const int nwarp = blockDim.x >> 5;
       double *cs = sX + nb * kNGL + (tid >> 5) * nb;
-      if (na.m.mode != 0)
+      int *sI = reinterpret_cast<int *>(sX + nb * kNGL + nwarp * nb);
+      if (na.m.mode != 0) {
         for (int q = tid; q < nb * kNGL; q += blockDim.x) {
           sA[q] = na.m.A[q];
           sX[q] = na.m.X[q];
         }
+        for (int q = tid; q < 4 * (na.m.imax + 1); q += blockDim.x) sI[q] = na.m.ichan[q];
+      }
       __syncthreads();
       for (int pp = pb + (tid >> 5); pp < pe; pp += nwarp)
-        newton_cell(na, (int64_t)col + (int64_t)pp * g.ncross, sA, sX, cs, tid & 31);
+        newton_cell(na, (int64_t)col + (int64_t)pp * g.ncross, sA, sX, sI, cs, tid & 31);
     }
   }
 }
@@ -502,7 +514,8 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
     const int tthreads0 = (threads + 31) / 32 * 32;
     if (a.fuse_newton) {  // the Newton tail reuses the stage ring for its tables
-      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * g.nb) * sizeof(double);
+      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * g.nb) * sizeof(double) +
+                          4 * (size_t)(a.nw.m.imax + 1) * sizeof(int);
       smem = std::max(smem, need);
       *fused = 1;
     }
@@ -510,9 +523,15 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     const int tthreads = (threads + 31) / 32 * 32;
 #define BTE_LAUNCH(N, NB)                                                                        \
   {                                                                                              \
-    cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                         (int)smem);                                                             \
-    k_sweep_tma<DIM, N, NB><<<grid, tthreads, smem, s>>>(a);                                     \
+    if (a.fuse_newton) {                                                                         \
+      cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB, true>,                                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+      k_sweep_tma<DIM, N, NB, true><<<grid, tthreads, smem, s>>>(a);                             \
+    } else {                                                                                     \
+      cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB, false>,                                       \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+      k_sweep_tma<DIM, N, NB, false><<<grid, tthreads, smem, s>>>(a);                            \
+    }                                                                                            \
     break;                                                                                       \
   }
     if (g.nb == 40 && jcase == 5) {
@@ -662,8 +681,8 @@ constexpr int kNewtonWarps = 8;
 // Newton of one cell by one warp (a3 + a4).  sA/sX: GL tables [nb][16] in
 // shared memory, cs: [nb] scratch of this warp.  Dpart is read with
 // ld.global.cg because, when fused into the sweep, other CTAs wrote it.
-__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, double *cs,
-                            int lane) {
+__device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
+                            double *cs, int lane) {
   const int nb = a.nb;
   const bool be = a.m.mode != 0;
   const int jn = lane & 15;
@@ -675,7 +694,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b);
     const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     const double bn = beta_of_T(a.m.bcoef, b, Tn);
-    const double cb = bn / a.m.v[b];
+    const double cb = bn * a.m.rv[b];
     cs[b] = cb;
     a.beta_next[c * nb + b] = bn;
     F0 += cb * D;
@@ -697,7 +716,30 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
       if (it > 0) {
         double f = 0.0, fp = 0.0;
         const double rT = 1.0 / T;
-        if (be) {
+        if (be && a.m.uniform) {
+          // geometric recurrence over the band index i (17 exp per evaluation)
+          const double aa = a.m.Xd * rT;
+          const double r = exp(aa);
+          const double r2 = r * r;
+          const double x0 = aa * a.m.U[jn];
+          double e = exp(x0);
+          if (par) e *= r;
+          for (int i = par; i <= a.m.imax; i += 2) {
+            const double em1 = (i == 0) ? expm1(x0) : e - 1.0;
+            const double rr = 1.0 / em1;
+            const double xi = fma((double)i, aa, x0);
+            const double dfac = xi * (1.0 + rr);
+            for (int q = 0; q < 4; ++q) {
+              const int b = sI[i * 4 + q];
+              if (b < 0) break;
+              const double t = cs[b] * (sA[b * kNGL + jn] * rr);
+              f += t;
+              fp += t * dfac;
+            }
+            e *= r2;
+          }
+          fp *= rT;
+        } else if (be) {
           for (int b = par; b < nb; b += 2) {
             const double x = sX[b * kNGL + jn] * rT;
             const double em1 = expm1(x);
@@ -754,7 +796,43 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   if (Tf != Tn) {
     // refresh I0c = I0(T^{n+1}) and its derivative
     if (lane == 0) a.T[c] = Tf;
-    if (be) {
+    if (be && a.m.uniform) {
+      const double rT = 1.0 / Tf;
+      const double aa = a.m.Xd * rT;
+      const double r = exp(aa);
+      const double r2 = r * r;
+      const double x0 = aa * a.m.U[jn];
+      double e = exp(x0);
+      if (par) e *= r;
+      const int niter = (a.m.imax + 2) / 2;  // both half-warps run the same trip count
+      for (int m = 0; m < niter; ++m) {
+        const int i = 2 * m + par;
+        double em1 = 1.0, rr = 0.0, dfac = 0.0;
+        if (i <= a.m.imax) {
+          em1 = (i == 0) ? expm1(x0) : e - 1.0;
+          rr = 1.0 / em1;
+          dfac = fma((double)i, aa, x0) * (1.0 + rr);
+        }
+        for (int q = 0; q < a.m.maxcnt; ++q) {  // warp-uniform trip count (shuffles below)
+          const int b = (i <= a.m.imax) ? sI[i * 4 + q] : -1;
+          double f = 0.0, fp = 0.0;
+          if (b >= 0) {
+            f = sA[b * kNGL + jn] * rr;
+            fp = f * dfac;
+          }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            f += __shfl_xor_sync(0xffffffffu, f, o);
+            fp += __shfl_xor_sync(0xffffffffu, fp, o);
+          }
+          if (jn == 0 && b >= 0) {
+            a.I0c[c * nb + b] = f;
+            a.dI0c[c * nb + b] = fp * rT;
+          }
+        }
+        e *= r2;
+      }
+    } else if (be) {
       const double rT = 1.0 / Tf;
       for (int b0 = 0; b0 < nb; b0 += 2) {
         const int b = b0 + par;
@@ -799,15 +877,18 @@ __global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a
   double *sX = sA + nb * kNGL;
   const int warp = threadIdx.x >> 5;
   double *cs = sX + nb * kNGL + warp * nb;
-  if (a.m.mode != 0)
+  int *sI = reinterpret_cast<int *>(sX + nb * kNGL + kNewtonWarps * nb);
+  if (a.m.mode != 0) {
     for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
       sA[i] = a.m.A[i];
       sX[i] = a.m.X[i];
     }
+    for (int i = threadIdx.x; i < 4 * (a.m.imax + 1); i += blockDim.x) sI[i] = a.m.ichan[i];
+  }
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
   for (int64_t c = (int64_t)blockIdx.x * kNewtonWarps + warp; c < a.ncells; c += nwarps)
-    newton_cell(a, c, sA, sX, cs, threadIdx.x & 31);
+    newton_cell(a, c, sA, sX, sI, cs, threadIdx.x & 31);
 }
 
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
@@ -815,7 +896,8 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   if (a.ncells == 0) return cudaSuccess;
   const int64_t need = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
-  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * a.nb) * sizeof(double);
+  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * a.nb) * sizeof(double) +
+                      4 * (size_t)(a.m.imax + 1) * sizeof(int);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
   return cudaGetLastError();

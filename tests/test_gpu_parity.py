@@ -301,3 +301,24 @@ def test_errors(Solver):
         with pytest.raises(BteError) as e:
             sv.set_bc(0, bi.BC_SPECULAR)
         assert e.value.status == 6
+
+
+def test_full_size_config2_physical_100_steps(Solver):
+    """The paper's own scenario at BASELINE.json configs[1] size: equilibrium at
+    300 K, Gaussian hot spot on +y, cold -y wall, specular sides, 100 steps
+    (P:L413-436); full-field comparison against the oracle (~1.5 min on 16 cores)."""
+    p = bi.config2()
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, p.T_init)
+    I = o.equilibrium(T)
+    Io, To, _, _ = o.run(I, T, p.nsteps)
+    with Solver.from_problem(p) as sv:
+        sv.step(p.nsteps)
+        Ig, Tg = sv.intensity(), sv.temperature()
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    assert To.max() > 300.0 and To.min() == 300.0
+    # heat enters only from the hot +y wall: the excess decays away from it
+    dT_rows = np.abs(To.reshape(p.mesh.ny, p.mesh.nx) - 300.0).max(axis=1)
+    assert dT_rows.argmax() == p.mesh.ny - 1
+    assert np.all(np.diff(dT_rows[-20:]) >= 0)
