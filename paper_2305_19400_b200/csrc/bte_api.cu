@@ -406,7 +406,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   }
 
   // uniform band grid detection (exact): channel b spans [i_b dw, (i_b + 1) dw]
-  std::vector<int> ichan;
+  std::vector<int> ichan, ibv(ctx->nb, 0);
   std::vector<double> Ugl(kNGL);
   int uniform = 0, imax = 0;
   double Xd = 0;
@@ -418,6 +418,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
       const double q = std::nearbyint(bands->w_lo[b] / dw);
       if (!(q >= 0 && q < 4096) || bands->w_lo[b] != q * dw || bands->w_hi[b] != (q + 1.0) * dw) uniform = 0;
       ib[b] = (int)q;
+      ibv[b] = ib[b];
       imax = std::max(imax, ib[b]);
     }
     if (uniform) {
@@ -483,6 +484,9 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
       maxcnt = std::max(maxcnt, c);
     }
     ctx->m.maxcnt = maxcnt;
+    int *d_ib;
+    if ((st = upload(ctx, &d_ib, ibv.data(), ibv.size()))) return bail(st);
+    ctx->m.ib = d_ib;
     std::vector<double> rv(ctx->nb);
     for (int b = 0; b < ctx->nb; ++b) rv[b] = 1.0 / ctx->v[b];
     double *d_rv;

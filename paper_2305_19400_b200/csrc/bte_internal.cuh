@@ -45,6 +45,7 @@ struct Material {
   const double *U;        // [16] u_j
   const int *ichan;       // [imax+1][4] channels with band index i (-1 padded)
   int maxcnt;             // max channels sharing one band index
+  const int *ib;          // [nb] band index i of each channel
   const double *rv;       // [nb] 1 / v_b
 };
 

@@ -214,6 +214,12 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   }
 }
 
+// per-warp Newton scratch (doubles): c_b during the solve, node/band factors in the refresh
+__host__ __device__ __forceinline__ int newton_scratch(const Material &m, int nb) {
+  const int r = 2 * kNGL + m.imax + 1;
+  return nb > r ? nb : r;
+}
+
 __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
                             double *cs, int lane);
 
@@ -458,8 +464,9 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
       double *sA = stage0;  // stage ring is free: every stage was consumed
       double *sX = sA + nb * kNGL;
       const int nwarp = blockDim.x >> 5;
-      double *cs = sX + nb * kNGL + (tid >> 5) * nb;
-      int *sI = reinterpret_cast<int *>(sX + nb * kNGL + nwarp * nb);
+      const int wsd = newton_scratch(na.m, nb);
+      double *cs = sX + nb * kNGL + (tid >> 5) * wsd;
+      int *sI = reinterpret_cast<int *>(sX + nb * kNGL + nwarp * wsd);
       if (na.m.mode != 0) {
         for (int q = tid; q < nb * kNGL; q += blockDim.x) {
           sA[q] = na.m.A[q];
@@ -514,7 +521,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
     const int tthreads0 = (threads + 31) / 32 * 32;
     if (a.fuse_newton) {  // the Newton tail reuses the stage ring for its tables
-      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * g.nb) * sizeof(double) +
+      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * newton_scratch(a.nw.m, g.nb)) * sizeof(double) +
                           4 * (size_t)(a.nw.m.imax + 1) * sizeof(int);
       smem = std::max(smem, need);
       *fused = 1;
@@ -669,6 +676,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 constexpr int kNewtonWarps = 8;
 
+// 1/x for x > 0 finite: MUFU seed + two Newton-Raphson steps (<= 1 ulp);
+// +inf -> 0 (a Bose-Einstein term whose exponent overflowed contributes 0).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  return x < 1e300 ? r : 0.0;
+}
+
 // a3 + a4.  One warp per cell (persistent grid, warps stride over cells).
 // Channel-wise work (octant tree, beta_next, c_b) uses lanes over channels;
 // the band integrals use lanes over (channel, Gauss node) pairs: lane l owns
@@ -726,7 +745,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
           if (par) e *= r;
           for (int i = par; i <= a.m.imax; i += 2) {
             const double em1 = (i == 0) ? expm1(x0) : e - 1.0;
-            const double rr = 1.0 / em1;
+            const double rr = rcp_nr(em1);
             const double xi = fma((double)i, aa, x0);
             const double dfac = xi * (1.0 + rr);
             for (int q = 0; q < 4; ++q) {
@@ -797,40 +816,37 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     // refresh I0c = I0(T^{n+1}) and its derivative
     if (lane == 0) a.T[c] = Tf;
     if (be && a.m.uniform) {
+      // per-channel layout: lane = channel, sequential over the 16 nodes, with
+      // the node factors exp(a u_j), expm1(a u_j) and the band factors exp(a i)
+      // computed once per cell by the warp and shared through this warp's
+      // scratch (cs is free again: c_b is no longer needed).
       const double rT = 1.0 / Tf;
       const double aa = a.m.Xd * rT;
-      const double r = exp(aa);
-      const double r2 = r * r;
-      const double x0 = aa * a.m.U[jn];
-      double e = exp(x0);
-      if (par) e *= r;
-      const int niter = (a.m.imax + 2) / 2;  // both half-warps run the same trip count
-      for (int m = 0; m < niter; ++m) {
-        const int i = 2 * m + par;
-        double em1 = 1.0, rr = 0.0, dfac = 0.0;
-        if (i <= a.m.imax) {
-          em1 = (i == 0) ? expm1(x0) : e - 1.0;
-          rr = 1.0 / em1;
-          dfac = fma((double)i, aa, x0) * (1.0 + rr);
+      double *sE = cs;             // [16] exp(a u_j)
+      double *sM = cs + kNGL;      // [16] expm1(a u_j)
+      double *sR = cs + 2 * kNGL;  // [imax+1] exp(a i)
+      __syncwarp();
+      if (lane < kNGL) {
+        const double x0 = aa * a.m.U[lane];
+        sE[lane] = exp(x0);
+        sM[lane] = expm1(x0);
+      }
+      for (int i = lane; i <= a.m.imax; i += 32) sR[i] = exp(aa * (double)i);
+      __syncwarp();
+      for (int b = lane; b < nb; b += 32) {
+        const int ib = a.m.ib[b];
+        const double R = sR[ib];
+        double f = 0.0, fp = 0.0;
+#pragma unroll 4
+        for (int j = 0; j < kNGL; ++j) {
+          const double em1 = (ib == 0) ? sM[j] : fma(sE[j], R, -1.0);
+          const double rr = rcp_nr(em1);
+          const double t = sA[b * kNGL + j] * rr;
+          f += t;
+          fp = fma(t * fma((double)ib, aa, aa * a.m.U[j]), 1.0 + rr, fp);
         }
-        for (int q = 0; q < a.m.maxcnt; ++q) {  // warp-uniform trip count (shuffles below)
-          const int b = (i <= a.m.imax) ? sI[i * 4 + q] : -1;
-          double f = 0.0, fp = 0.0;
-          if (b >= 0) {
-            f = sA[b * kNGL + jn] * rr;
-            fp = f * dfac;
-          }
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) {
-            f += __shfl_xor_sync(0xffffffffu, f, o);
-            fp += __shfl_xor_sync(0xffffffffu, fp, o);
-          }
-          if (jn == 0 && b >= 0) {
-            a.I0c[c * nb + b] = f;
-            a.dI0c[c * nb + b] = fp * rT;
-          }
-        }
-        e *= r2;
+        a.I0c[c * nb + b] = f;
+        a.dI0c[c * nb + b] = fp * rT;
       }
     } else if (be) {
       const double rT = 1.0 / Tf;
@@ -876,8 +892,9 @@ __global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a
   double *sA = nsh;
   double *sX = sA + nb * kNGL;
   const int warp = threadIdx.x >> 5;
-  double *cs = sX + nb * kNGL + warp * nb;
-  int *sI = reinterpret_cast<int *>(sX + nb * kNGL + kNewtonWarps * nb);
+  const int wsd = newton_scratch(a.m, nb);
+  double *cs = sX + nb * kNGL + warp * wsd;
+  int *sI = reinterpret_cast<int *>(sX + nb * kNGL + kNewtonWarps * wsd);
   if (a.m.mode != 0) {
     for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
       sA[i] = a.m.A[i];
@@ -896,7 +913,7 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   if (a.ncells == 0) return cudaSuccess;
   const int64_t need = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
-  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * a.nb) * sizeof(double) +
+  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);

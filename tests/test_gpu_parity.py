@@ -322,3 +322,36 @@ def test_full_size_config2_physical_100_steps(Solver):
     dT_rows = np.abs(To.reshape(p.mesh.ny, p.mesh.nx) - 300.0).max(axis=1)
     assert dT_rows.argmax() == p.mesh.ny - 1
     assert np.all(np.diff(dT_rows[-20:]) >= 0)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_parity_randomized_problems(Solver, seed):
+    """Seeded random small problems: dimension, extents (incl. 1-cell axes),
+    per-wall BC kinds, direction set, channel table and step count."""
+    rng = np.random.default_rng(1000 + seed)
+    dim = int(rng.choice([2, 3]))
+    nx, ny = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+    nz = int(rng.integers(1, 6)) if dim == 3 else 1
+    d = float(rng.choice([1e-6, 2e-6]))
+    dirs = [bi.directions_control_angle(2, 4), bi.directions_control_angle(4, 8), bi.directions_inplane(8),
+            bi.directions_inplane(12)][int(rng.integers(0, 4))]
+    if rng.random() < 0.7:
+        si = bi.silicon_bands(29)
+        bands = bi.subset_bands(si, np.sort(rng.choice(si.nb, int(rng.integers(1, 7)), replace=False)))
+    else:
+        nb = int(rng.integers(1, 4))
+        bands = bi.linear_bands(rng.uniform(2e3, 8e3, nb), rng.uniform(2e-11, 8e-11, nb),
+                                rng.uniform(1e2, 1e3, nb), rng.uniform(1e4, 1e5, nb))
+    bcs = []
+    for r in range(6):
+        k = int(rng.integers(0, 3))
+        if k == 0:
+            bcs.append(bi.WallBC(0, None, float(rng.uniform(295, 310))))
+        else:
+            bcs.append(bi.WallBC(k))
+    p = bi.small_3d(nx, ny, nz, dirs=dirs, bands=bands, bcs=bcs, d=d, dt=1e-12 if d == 1e-6 else 2e-12,
+                    seed=seed)
+    if dim == 2:
+        p.mesh = bi.Mesh(2, nx, ny, 1, d, d, 1.0)
+    (rel, dT), _ = _run_both(Solver, p, int(rng.integers(2, 9)))
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
