@@ -64,16 +64,17 @@ def _peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _traffic(workload: str):
-    """Per-launch DRAM bytes of the sweep from the committed ncu --set full summary."""
+def _traffic_per_dof(workload: str):
+    """DRAM bytes per DOF of the sweep kernel, from the committed ncu --set full
+    summary (dram__bytes_read.sum + dram__bytes_write.sum of one launch / its DOF)."""
     path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
     if not os.path.exists(path):
         return None
     try:
         d = json.load(open(path))
         e = d.get(workload)
-        if e and e.get("dram_bytes_per_launch"):
-            return float(e["dram_bytes_per_launch"])
+        if e and e.get("dram_bytes_per_dof"):
+            return float(e["dram_bytes_per_dof"])
     except Exception:
         return None
     return None
@@ -301,19 +302,24 @@ def run_b200(args):
         ms = float(t.item())
     value = dof_global * args.steps / (ms * 1e-3)
 
-    # roofline of the dominant kernel (the fused sweep): algorithmic 16 B/DOF per launch
+    # roofline of the dominant kernel (the fused sweep): algorithmic 16 B/DOF;
+    # one step launches the sweep once per column chunk
     peak, peak_src = _peaks()
+    launches_per_step = max(1, tim["sweep_launches"] // max(1, tim["steps"]))
     sweep_ms = tim["sweep_ms"] / max(1, tim["sweep_launches"])
-    achieved = BYTES_PER_DOF * dof_local / (sweep_ms * 1e-3) / 1e9
-    traffic = _traffic(p.name)
+    dof_per_launch = dof_local / launches_per_step
+    achieved = BYTES_PER_DOF * dof_per_launch / (sweep_ms * 1e-3) / 1e9
+    tpd = _traffic_per_dof(p.name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic,
+                "traffic": None if tpd is None else tpd * dof_per_launch,
                 "kernel": ("k_sweep_tma (a1+a2 fused upwind flux + relaxation + octant partial sums"
                            + (", a3+a4 Newton fused in the tail)" if tim["newton_launches"] == 0 else ")")),
-                "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_local, "kernel_ms_avg": sweep_ms,
-                "peak_source": peak_src,
-                "step_share": {"sweep": tim["sweep_ms"] / ms, "newton": tim["newton_ms"] / ms,
-                               "boundary": tim["boundary_ms"] / ms, "halo": tim["halo_ms"] / ms}}
+                "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_per_launch, "kernel_ms_avg": sweep_ms,
+                "launches_per_step": launches_per_step, "peak_source": peak_src,
+                "device_ms_per_step": {"sweep": tim["sweep_ms"] / args.steps, "newton": tim["newton_ms"] / args.steps,
+                                       "boundary": tim["boundary_ms"] / args.steps,
+                                       "halo": tim["halo_ms"] / args.steps},
+                "note": "Newton runs on a second stream, overlapped with other chunks' sweeps"}
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None

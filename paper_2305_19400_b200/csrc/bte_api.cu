@@ -75,12 +75,18 @@ struct bte_ctx {
   int use_tma = 1, stages_override = 0, seg_override = 0, target_threads = 0, smem_budget_kb = 0, stcs = 1;  // env BTE_SWEEP / BTE_STAGES / BTE_SEGS (A/B runs)
   int64_t ncells_local = 0, ncells_global = 0;
   int64_t steps_done = 0;
-  // timing
+  // timing: (kind, first event) spans over a preallocated event pool
   bool timing = false;
   int64_t timing_max = 0, timing_used = 0;
-  std::vector<cudaEvent_t> ev;  // [max][6]: sweep b/e, newton b/e, bnd b/e
-  std::vector<char> ev_has_bnd;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> spans;  // kind 0 sweep, 1 newton, 2 boundary, 3 halo
   bte_timing tacc{};
+  // sweep/Newton pipeline over column chunks (second stream for the Newton)
+  int nchunks = 1;
+  cudaStream_t nstream = nullptr;
+  std::vector<cudaEvent_t> ev_sw, ev_nt;
+  std::vector<char> nt_pending;
   // NCCL
   bte_slab_plan plan{};
   void *nccl_comm = nullptr;
@@ -547,6 +553,20 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
   }
   if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
+  // column chunks for the sweep/Newton two-stream pipeline: off by default
+  // (measured slower on B200); BTE_CHUNKS=n enables it.
+  ctx->nchunks = 1;
+  if (const char *e = getenv("BTE_CHUNKS")) ctx->nchunks = std::max(1, std::min(64, atoi(e)));
+  if (ctx->nchunks > 1) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&ctx->nstream, cudaStreamNonBlocking, hi));
+    ctx->ev_sw.resize(ctx->nchunks);
+    ctx->ev_nt.resize(ctx->nchunks);
+    for (auto &e : ctx->ev_sw) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : ctx->ev_nt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ctx->nt_pending.assign(ctx->nchunks, 0);
   {
     const int64_t nseg = (g.nplanes + ctx->seg_len - 1) / ctx->seg_len;
     ctx->d_done = (int *)dev_alloc(ctx, nseg * g.ncross * sizeof(int));
@@ -634,7 +654,8 @@ static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, int64_t step);
+static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0 = 0, int ncols = -1,
+                             cudaStream_t stream = nullptr);
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
@@ -736,13 +757,19 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.cell0_global = ctx->g.m0 * ctx->g.ncross;
   a.err = ctx->d_err;
   a.step = step;
+  a.col0 = 0;
+  a.ncols = ctx->g.ncross;
+  a.ncross = ctx->g.ncross;
+  a.nplanes = ctx->g.nplanes;
   return a;
 }
 
 // a1+a2 (+ a3+a4 fused into the sweep tail when *fused is set on return)
 static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
-                                    int *fused) {
+                                    int *fused, int col0 = 0, int ncols = 0) {
   SweepArgs a;
+  a.col0 = col0;
+  a.ncols = ncols;
   a.g = ctx->g;
   a.Iin = Iin;
   a.Iout = Iout;
@@ -766,9 +793,13 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, int64_t step) {
+static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0, int ncols, cudaStream_t stream) {
   NewtonArgs a = newton_args(ctx, step);
-  CU(launch_newton(a, ctx->stream));
+  if (ncols >= 0) {
+    a.col0 = col0;
+    a.ncols = ncols;
+  }
+  CU(launch_newton(a, stream ? stream : ctx->stream));
   ctx->tacc.launches++;
   ctx->tacc.newton_launches++;
   return BTE_OK;
@@ -776,36 +807,81 @@ static bte_status run_newton(bte_ctx *ctx, int64_t step) {
 
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
+static bte_status span_begin(bte_ctx *ctx, bool t, int kind, cudaStream_t s, size_t *id) {
+  if (!t) return BTE_OK;
+  if (ctx->ev_used + 2 > ctx->ev.size()) return BTE_OK;  // pool exhausted: stop recording
+  *id = ctx->ev_used;
+  ctx->ev_used += 2;
+  ctx->spans.push_back({kind, *id});
+  CU(cudaEventRecord(ctx->ev[*id], s));
+  return BTE_OK;
+}
+static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
+  if (!t || id == (size_t)-1) return BTE_OK;
+  CU(cudaEventRecord(ctx->ev[id + 1], s));
+  return BTE_OK;
+}
+
+// One step = [diffuse ghosts] + for each column chunk k: sweep(k) on the
+// context stream and, on the Newton stream once sweep(k) is done, Newton(k).
+// The next step's sweep(k) waits only for Newton(k), so the FP64-bound Newton
+// of chunk k overlaps the HBM-bound sweeps of the other chunks.
 bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
   if (!ctx) return BTE_EINVAL;
   if (nsteps < 0) return fail(ctx, BTE_EINVAL, "nsteps < 0");
   const bool has_bnd = n_diffuse(ctx) > 0;
+  const int C = ctx->fuse_newton ? 1 : ctx->nchunks;
+  const int ncross = ctx->g.ncross;
+  bte_status st;
   for (int64_t s = 0; s < nsteps; ++s) {
     double *Iin = ctx->I[ctx->cur];
     double *Iout = ctx->I[1 - ctx->cur];
     const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
-    cudaEvent_t *ev = t ? &ctx->ev[6 * ctx->timing_used] : nullptr;
-    bte_status st;
+    size_t id = (size_t)-1;
     if (has_bnd) {
-      if (t) CU(cudaEventRecord(ev[4], ctx->stream));
+      if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
       if ((st = launch_boundary(ctx, Iin))) return st;
-      if (t) CU(cudaEventRecord(ev[5], ctx->stream));
+      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
     }
-    if (t) CU(cudaEventRecord(ev[0], ctx->stream));
-    int fused = 0;
-    if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused))) return st;
-    if (t) CU(cudaEventRecord(ev[1], ctx->stream));
-    if (ctx->nranks > 1 && (st = halo_exchange(ctx, Iout))) return st;
-    if (t) CU(cudaEventRecord(ev[2], ctx->stream));
-    if (!fused && (st = run_newton(ctx, ctx->steps_done))) return st;
-    if (t) {
-      CU(cudaEventRecord(ev[3], ctx->stream));
-      ctx->ev_has_bnd[ctx->timing_used] = has_bnd;
-      ctx->timing_used++;
+    for (int k = 0; k < C; ++k) {
+      const int c0 = (int)((int64_t)k * ncross / C), c1 = (int)((int64_t)(k + 1) * ncross / C);
+      if (c1 <= c0) continue;
+      if (C > 1 && ctx->nt_pending[k]) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
+      id = (size_t)-1;
+      if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
+      int fused = 0;
+      if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused, c0, c1 - c0))) return st;
+      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+      if (fused) continue;
+      cudaStream_t ns = C > 1 ? ctx->nstream : ctx->stream;
+      if (C > 1) {
+        CU(cudaEventRecord(ctx->ev_sw[k], ctx->stream));
+        CU(cudaStreamWaitEvent(ns, ctx->ev_sw[k], 0));
+      }
+      id = (size_t)-1;
+      if ((st = span_begin(ctx, t, 1, ns, &id))) return st;
+      if ((st = run_newton(ctx, ctx->steps_done, c0, c1 - c0, ns))) return st;
+      if ((st = span_end(ctx, t, ns, id))) return st;
+      if (C > 1) {
+        CU(cudaEventRecord(ctx->ev_nt[k], ns));
+        ctx->nt_pending[k] = 1;
+      }
     }
+    if (ctx->nranks > 1) {
+      id = (size_t)-1;
+      if ((st = span_begin(ctx, t, 3, ctx->stream, &id))) return st;
+      if ((st = halo_exchange(ctx, Iout))) return st;
+      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    }
+    if (t) ctx->timing_used++;
     ctx->cur = 1 - ctx->cur;
     ctx->steps_done++;
   }
+  for (int k = 0; k < (int)ctx->nt_pending.size(); ++k)
+    if (ctx->nt_pending[k]) {
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
+      ctx->nt_pending[k] = 0;
+    }
   return sync_check(ctx);
 }
 
@@ -899,15 +975,18 @@ bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count)
 
 bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps) {
   if (!ctx) return BTE_EINVAL;
+  CU(cudaStreamSynchronize(ctx->stream));
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   ctx->ev.clear();
+  ctx->spans.clear();
+  ctx->ev_used = 0;
   ctx->tacc = bte_timing{};
   ctx->timing = enable != 0;
   ctx->timing_used = 0;
   ctx->timing_max = enable ? max_steps : 0;
   if (enable) {
-    ctx->ev.resize(6 * max_steps);
-    ctx->ev_has_bnd.assign(max_steps, 0);
+    const int64_t per_step = 2 * (2 * (int64_t)ctx->nchunks + 2);
+    ctx->ev.resize((size_t)(per_step * max_steps));
     for (auto &e : ctx->ev) CU(cudaEventCreate(&e));
   }
   return BTE_OK;
@@ -916,21 +995,15 @@ bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps) {
 bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out) {
   if (!ctx || !out) return BTE_EINVAL;
   CU(cudaStreamSynchronize(ctx->stream));
+  if (ctx->nstream) CU(cudaStreamSynchronize(ctx->nstream));
   bte_timing t = ctx->tacc;
   t.steps = ctx->timing_used;
   t.sweep_ms = t.newton_ms = t.boundary_ms = t.halo_ms = 0;
-  for (int64_t i = 0; i < ctx->timing_used; ++i) {
+  for (const auto &sp : ctx->spans) {
     float ms;
-    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i], ctx->ev[6 * i + 1]));
-    t.sweep_ms += ms;
-    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 2], ctx->ev[6 * i + 3]));
-    t.newton_ms += ms;
-    CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 1], ctx->ev[6 * i + 2]));
-    t.halo_ms += ms;
-    if (ctx->ev_has_bnd[i]) {
-      CU(cudaEventElapsedTime(&ms, ctx->ev[6 * i + 4], ctx->ev[6 * i + 5]));
-      t.boundary_ms += ms;
-    }
+    CU(cudaEventElapsedTime(&ms, ctx->ev[sp.second], ctx->ev[sp.second + 1]));
+    double *dst = sp.first == 0 ? &t.sweep_ms : sp.first == 1 ? &t.newton_ms : sp.first == 2 ? &t.boundary_ms : &t.halo_ms;
+    *dst += ms;
   }
   *out = t;
   return BTE_OK;
@@ -953,7 +1026,11 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
 void bte_destroy(bte_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->nstream) cudaStreamSynchronize(ctx->nstream);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_sw) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_nt) cudaEventDestroy(e);
+  if (ctx->nstream) cudaStreamDestroy(ctx->nstream);
   if (ctx->nccl_comm) nccl_shim_destroy(ctx->nccl_comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   for (void *p : ctx->allocs) {

@@ -83,6 +83,8 @@ struct NewtonArgs {
   int64_t ncells, cell0_global;
   unsigned long long *err;
   int64_t step;           // step index for error reporting
+  int col0, ncols;        // column (cross-cell) range of this launch
+  int ncross, nplanes;
 };
 
 struct SweepArgs {
@@ -103,6 +105,7 @@ struct SweepArgs {
   int smem_budget_kb;     // per-CTA shared memory budget for the stage ring (0 = 113 KB)
   int stcs;               // streaming (evict-first) stores of I^{n+1}
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
+  int col0, ncols;        // column range of this launch (ncols = 0: all)
   NewtonArgs nw;          // fused a3+a4 (k_sweep_tma tail)
   int fuse_newton;
   int *done;              // [nseg][ncross] tickets, zero between launches

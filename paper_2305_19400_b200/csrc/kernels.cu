@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 
   const int slot = blockIdx.y;
   const int oct = g.slot_oct[slot];
-  const int col = blockIdx.x;
+  const int col = A.col0 + blockIdx.x;
   const int x = (DIM == 3) ? col % g.nx : col;
   const int y = (DIM == 3) ? col / g.nx : 0;
   const bool xneg = oct & 4;
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
 
   const int slot = blockIdx.y;
   const int oct = g.slot_oct[slot];
-  const int col = blockIdx.x;
+  const int col = A.col0 + blockIdx.x;
   const int x = (DIM == 3) ? col % g.nx : col;
   const int y = (DIM == 3) ? col / g.nx : 0;
   const bool xneg = oct & 4;
@@ -504,7 +504,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   const int threads = JG * g.nb;
   if (threads > 1024 || g.nb > 1024) return cudaErrorInvalidConfiguration;
   const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
-  dim3 grid(g.ncross, g.nslot, nseg);
+  dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.E % 2 == 0) && (g.nb % 2 == 0);
   if (tma) {
@@ -904,14 +904,18 @@ __global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a
   }
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
-  for (int64_t c = (int64_t)blockIdx.x * kNewtonWarps + warp; c < a.ncells; c += nwarps)
-    newton_cell(a, c, sA, sX, sI, cs, threadIdx.x & 31);
+  // cells of the column range [col0, col0 + ncols) over all planes
+  const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
+  for (int64_t q = (int64_t)blockIdx.x * kNewtonWarps + warp; q < nq; q += nwarps) {
+    const int64_t p = q / ncol;
+    newton_cell(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, threadIdx.x & 31);
+  }
 }
 
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   if (a.nb > kMaxBands) return cudaErrorInvalidValue;
   if (a.ncells == 0) return cudaSuccess;
-  const int64_t need = (a.ncells + kNewtonWarps - 1) / kNewtonWarps;
+  const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
   const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
