@@ -355,3 +355,40 @@ def test_parity_randomized_problems(Solver, seed):
         p.mesh = bi.Mesh(2, nx, ny, 1, d, d, 1.0)
     (rel, dT), _ = _run_both(Solver, p, int(rng.integers(2, 9)))
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_step_splitting_and_energy(Solver):
+    """bte_step(3)+bte_step(4) == bte_step(7) bit-for-bit; the energy diagnostic
+    matches the oracle's sum_c V sum_b (1/v_b) sum_d w_d I."""
+    p = bi.small_3d(7, 6, 5)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(3)
+        sv.step(4)
+        a = (sv.intensity(), sv.temperature())
+        E = sv.energy()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(7)
+        b = (sv.intensity(), sv.temperature())
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert abs(E / o.energy(a[0]) - 1) < 1e-13
+
+
+def test_newton_failure_is_reported(Solver):
+    """No root in the [1, 5000] K bracket -> BTE_ENEWTON with the step index (the oracle agrees)."""
+    from paper_2305_19400_b200 import BteError
+    p = bi.small_3d(3, 2, 2, bcs=bi.uniform_bcs(bi.BC_SPECULAR))
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I = o.equilibrium(T) * 1e8
+    with pytest.raises(oracle.OracleError) as eo:
+        o.run(I, T, 1)
+    assert eo.value.code == 7
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        with pytest.raises(BteError) as e:
+            sv.step(1)
+        assert e.value.status == 7 and "step 0" in str(e.value)
