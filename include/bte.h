@@ -173,6 +173,14 @@ BTE_API bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double pha
  * (with step/cell in bte_last_error), BTE_ECUDA, BTE_ENCCL. */
 BTE_API bte_status bte_step(bte_ctx *ctx, int64_t nsteps);
 
+/* In-process slab group.  Contexts created in one process with nranks = n,
+ * rank = 0..n-1 and nccl_id == NULL ("local" mode) form one slab-decomposed
+ * problem whose halo planes are moved with device-to-device copies (same GPU,
+ * or peers) instead of NCCL, following exactly the bte_plan_slab list.
+ * bte_group_step advances all n contexts by nsteps (ctxs[r] must be rank r);
+ * bte_step on a local-mode context returns BTE_EINVAL.  Errors as bte_step. */
+BTE_API bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps);
+
 /* Copy state to caller-allocated host buffers (canonical order, this rank's
  * slab).  count must equal the exact element count: ncells_local*nd*nb for
  * the intensity, ncells_local for the temperature; else BTE_EINVAL. */

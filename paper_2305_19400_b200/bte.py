@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE = 0, 1, 2
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_plan_slab", "bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -104,6 +104,7 @@ def load_library(path: str = LIB_PATH):
     lib.bte_set_state.argtypes = [P, dp, dp]
     lib.bte_init_random.argtypes = [P, C.c_uint64, dp, C.c_double, C.c_double, C.c_double]
     lib.bte_step.argtypes = [P, C.c_int64]
+    lib.bte_group_step.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int64]
     lib.bte_get_intensity.argtypes = [P, dp, C.c_size_t]
     lib.bte_get_temperature.argtypes = [P, dp, C.c_size_t]
     lib.bte_get_energy.argtypes = [P, C.POINTER(C.c_double)]
@@ -175,9 +176,9 @@ class Solver:
         else:
             self._alloc_cb, self._free_cb = ALLOC_FN(), DEALLOC_FN()
         idbuf = None
-        if nranks > 1:
-            if nccl_id is None or len(nccl_id) != 128:
-                raise ValueError("nranks > 1 needs the 128-byte ncclUniqueId")
+        if nranks > 1 and nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
             k(idbuf)
         run = Run(float(dt), float(T_init), int(device), C.c_void_p(self.stream.cuda_stream), int(rank),
@@ -240,6 +241,17 @@ class Solver:
 
     def step(self, n: int = 1):
         self._check(self._lib.bte_step(self._h, int(n)))
+
+    @staticmethod
+    def group_step(solvers, n: int = 1):
+        """Advance an in-process slab group (contexts built with nranks = len(solvers),
+        rank = index, no nccl_id) by n steps; halos move by device-to-device copies."""
+        lib = load_library()
+        arr = (C.c_void_p * len(solvers))(*[sv._h.value for sv in solvers])
+        st = lib.bte_group_step(arr, len(solvers), int(n))
+        if st != BTE_OK:
+            msgs = "; ".join(sv._err() for sv in solvers if sv._err())
+            raise BteError(st, msgs)
 
     def intensity(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:

@@ -575,8 +575,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   }
 
   // ---- multi-GPU communicator
-  if (ctx->nranks > 1) {
-    if (!run->nccl_id) return bail(fail(ctx, BTE_EINVAL, "nranks > 1 needs an nccl_id"));
+  if (ctx->nranks > 1 && run->nccl_id) {
     std::string emsg;
     if (nccl_shim_init(&ctx->nccl_comm, run->nccl_id, ctx->nranks, ctx->rank, &emsg) != 0)
       return bail(fail(ctx, BTE_ENCCL, "NCCL init failed: %s", emsg.c_str()));
@@ -589,7 +588,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
   CU(launch_fill_equilibrium(g, ctx->I0c, ctx->I[0], ctx->stream));
   ctx->cur = 0;
-  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
+  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
   CU(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
   return BTE_OK;
@@ -686,7 +685,7 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   } else {
     CU(launch_fill_equilibrium(ctx->g, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
   }
-  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   if (I && !T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
@@ -712,7 +711,7 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
   CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
   CU(launch_refresh(ctx->m, ctx->T, ctx->ncells_local, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
   CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
-  if (ctx->nranks > 1 && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   CU(cudaStreamSynchronize(ctx->stream));
   return BTE_OK;
 }
@@ -826,63 +825,152 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
 // context stream and, on the Newton stream once sweep(k) is done, Newton(k).
 // The next step's sweep(k) waits only for Newton(k), so the FP64-bound Newton
 // of chunk k overlaps the HBM-bound sweeps of the other chunks.
-bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
-  if (!ctx) return BTE_EINVAL;
-  if (nsteps < 0) return fail(ctx, BTE_EINVAL, "nsteps < 0");
+// Launch one step (a1..a4) of ctx on its streams; the caller exchanges halos.
+static bte_status step_launch(bte_ctx *ctx, bool t) {
   const bool has_bnd = n_diffuse(ctx) > 0;
   const int C = ctx->fuse_newton ? 1 : ctx->nchunks;
   const int ncross = ctx->g.ncross;
   bte_status st;
+  double *Iin = ctx->I[ctx->cur];
+  double *Iout = ctx->I[1 - ctx->cur];
+  size_t id = (size_t)-1;
+  if (has_bnd) {
+    if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
+    if ((st = launch_boundary(ctx, Iin))) return st;
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+  }
+  for (int k = 0; k < C; ++k) {
+    const int c0 = (int)((int64_t)k * ncross / C), c1 = (int)((int64_t)(k + 1) * ncross / C);
+    if (c1 <= c0) continue;
+    if (C > 1 && ctx->nt_pending[k]) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
+    int fused = 0;
+    if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused, c0, c1 - c0))) return st;
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    if (fused) continue;
+    cudaStream_t ns = C > 1 ? ctx->nstream : ctx->stream;
+    if (C > 1) {
+      CU(cudaEventRecord(ctx->ev_sw[k], ctx->stream));
+      CU(cudaStreamWaitEvent(ns, ctx->ev_sw[k], 0));
+    }
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 1, ns, &id))) return st;
+    if ((st = run_newton(ctx, ctx->steps_done, c0, c1 - c0, ns))) return st;
+    if ((st = span_end(ctx, t, ns, id))) return st;
+    if (C > 1) {
+      CU(cudaEventRecord(ctx->ev_nt[k], ns));
+      ctx->nt_pending[k] = 1;
+    }
+  }
+  return BTE_OK;
+}
+
+static bte_status join_newton(bte_ctx *ctx) {
+  for (int k = 0; k < (int)ctx->nt_pending.size(); ++k)
+    if (ctx->nt_pending[k]) {
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
+      ctx->nt_pending[k] = 0;
+    }
+  return BTE_OK;
+}
+
+// One step = [diffuse ghosts] + for each column chunk k: sweep(k) on the
+// context stream and, on the Newton stream once sweep(k) is done, Newton(k)
+// (one chunk by default) + [halo exchange (NCCL)].
+bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
+  if (!ctx) return BTE_EINVAL;
+  if (nsteps < 0) return fail(ctx, BTE_EINVAL, "nsteps < 0");
+  if (ctx->nranks > 1 && !ctx->nccl_comm)
+    return fail(ctx, BTE_EINVAL, "local-mode slab context: advance the group with bte_group_step");
+  bte_status st;
   for (int64_t s = 0; s < nsteps; ++s) {
-    double *Iin = ctx->I[ctx->cur];
-    double *Iout = ctx->I[1 - ctx->cur];
     const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
-    size_t id = (size_t)-1;
-    if (has_bnd) {
-      if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
-      if ((st = launch_boundary(ctx, Iin))) return st;
-      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
-    }
-    for (int k = 0; k < C; ++k) {
-      const int c0 = (int)((int64_t)k * ncross / C), c1 = (int)((int64_t)(k + 1) * ncross / C);
-      if (c1 <= c0) continue;
-      if (C > 1 && ctx->nt_pending[k]) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
-      id = (size_t)-1;
-      if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
-      int fused = 0;
-      if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused, c0, c1 - c0))) return st;
-      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
-      if (fused) continue;
-      cudaStream_t ns = C > 1 ? ctx->nstream : ctx->stream;
-      if (C > 1) {
-        CU(cudaEventRecord(ctx->ev_sw[k], ctx->stream));
-        CU(cudaStreamWaitEvent(ns, ctx->ev_sw[k], 0));
-      }
-      id = (size_t)-1;
-      if ((st = span_begin(ctx, t, 1, ns, &id))) return st;
-      if ((st = run_newton(ctx, ctx->steps_done, c0, c1 - c0, ns))) return st;
-      if ((st = span_end(ctx, t, ns, id))) return st;
-      if (C > 1) {
-        CU(cudaEventRecord(ctx->ev_nt[k], ns));
-        ctx->nt_pending[k] = 1;
-      }
-    }
+    if ((st = step_launch(ctx, t))) return st;
     if (ctx->nranks > 1) {
-      id = (size_t)-1;
+      size_t id = (size_t)-1;
       if ((st = span_begin(ctx, t, 3, ctx->stream, &id))) return st;
-      if ((st = halo_exchange(ctx, Iout))) return st;
+      if ((st = halo_exchange(ctx, ctx->I[1 - ctx->cur]))) return st;
       if ((st = span_end(ctx, t, ctx->stream, id))) return st;
     }
     if (t) ctx->timing_used++;
     ctx->cur = 1 - ctx->cur;
     ctx->steps_done++;
   }
-  for (int k = 0; k < (int)ctx->nt_pending.size(); ++k)
-    if (ctx->nt_pending[k]) {
-      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
-      ctx->nt_pending[k] = 0;
-    }
+  if ((st = join_newton(ctx))) return st;
   return sync_check(ctx);
+}
+
+// Local-mode halo exchange of a whole group on buffers I[which] of every
+// context: each sender copies its owned boundary planes straight into the
+// receiver's halo planes (the receives of the plan are implied), after both
+// sides' previous work, and the receivers wait for those copies.
+static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
+  bte_ctx *ctx = ctxs[0];
+  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
+    if (atoi(e)) return BTE_OK;
+  std::vector<cudaEvent_t> done(n), put(n);
+  for (int r = 0; r < n; ++r) {
+    CU(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&put[r], cudaEventDisableTiming));
+    CU(cudaEventRecord(done[r], ctxs[r]->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    const Geometry &g = c->g;
+    double *src = c->I[output_buffers ? 1 - c->cur : c->cur];
+    for (int k = 0; k < c->plan.n_msgs; ++k) {
+      const bte_msg &m = c->plan.msg[k];
+      if (!m.send) continue;
+      bte_ctx *q = ctxs[m.peer];
+      CU(cudaStreamWaitEvent(c->stream, done[m.peer], 0));
+      double *dst = q->I[output_buffers ? 1 - q->cur : q->cur];
+      const double *sp = src + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+      double *dp = dst + (int64_t)m.slot * q->g.slot_stride + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
+      CU(cudaMemcpyAsync(dp, sp, (size_t)m.count * sizeof(double), cudaMemcpyDefault, c->stream));
+    }
+    CU(cudaEventRecord(put[r], c->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    for (int k = 0; k < c->plan.n_msgs; ++k)
+      if (!c->plan.msg[k].send) CU(cudaStreamWaitEvent(c->stream, put[c->plan.msg[k].peer], 0));
+  }
+  for (int r = 0; r < n; ++r) {
+    cudaEventDestroy(done[r]);
+    cudaEventDestroy(put[r]);
+  }
+  return BTE_OK;
+}
+
+bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
+  if (!ctxs || n < 1 || nsteps < 0) return BTE_EINVAL;
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r]) return BTE_EINVAL;
+    if (ctxs[r]->rank != r || ctxs[r]->nranks != n || ctxs[r]->nccl_comm)
+      return fail(ctxs[r], BTE_EINVAL, "bte_group_step: ctxs[%d] must be local-mode rank %d of %d", r, r, n);
+    if (ctxs[r]->steps_done != ctxs[0]->steps_done)
+      return fail(ctxs[r], BTE_EINVAL, "bte_group_step: contexts are at different steps");
+  }
+  bte_status st;
+  if (n > 1 && (st = group_exchange(ctxs, n, false))) return st;  // prime halos from the current state
+  for (int64_t s = 0; s < nsteps; ++s) {
+    for (int r = 0; r < n; ++r) {
+      const bool t = ctxs[r]->timing && ctxs[r]->timing_used < ctxs[r]->timing_max;
+      if ((st = step_launch(ctxs[r], t))) return st;
+      if ((st = join_newton(ctxs[r]))) return st;
+    }
+    if (n > 1 && (st = group_exchange(ctxs, n, true))) return st;
+    for (int r = 0; r < n; ++r) {
+      bte_ctx *c = ctxs[r];
+      if (c->timing && c->timing_used < c->timing_max) c->timing_used++;
+      c->cur = 1 - c->cur;
+      c->steps_done++;
+    }
+  }
+  for (int r = 0; r < n; ++r)
+    if ((st = sync_check(ctxs[r]))) return st;
+  return BTE_OK;
 }
 
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf) {

@@ -392,3 +392,81 @@ def test_newton_failure_is_reported(Solver):
         with pytest.raises(BteError) as e:
             sv.step(1)
         assert e.value.status == 7 and "step 0" in str(e.value)
+
+
+def _group_case(case):
+    if case == "3d":
+        b = bi.subset_bands(bi.silicon_bands(29), [0, 17, 33, 39])
+        bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(1), bi.WallBC(2),
+               bi.WallBC(0, None, 302.0)]
+        return bi.small_3d(6, 5, 9, bands=b, bcs=bcs)
+    p = bi.config2(n=10)
+    p.mesh = bi.Mesh(2, 10, 13, 1, 2e-6, 2e-6, 1.0)
+    p.bands = bi.subset_bands(bi.silicon_bands(29), [3, 22, 30])
+    p.dirs = bi.directions_control_angle(4, 8)
+    p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(10, 2e-6, width=4e-6), 300.0)
+    return p
+
+
+@pytest.mark.parametrize("case", ["3d", "2d"])
+@pytest.mark.parametrize("P", [2, 3])
+def test_local_slab_group_matches_single_domain(Solver, case, P):
+    """Multi-rank data path on one GPU: P slab contexts (halo planes, walls only
+    on the end ranks, bte_plan_slab exchange by device copies) reproduce the
+    single-context run bit-for-bit (per-DOF arithmetic is partition-free)."""
+    p = _group_case(case)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    nsteps = 7
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(nsteps)
+        I1, T1 = sv.intensity(), sv.temperature()
+    group = []
+    try:
+        for r in range(P):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=P)
+            for reg in range(6 if p.mesh.dim == 3 else 4):
+                bc = p.bcs[reg]
+                sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+            group.append(sv)
+        Solver.group_step(group, 3)
+        Solver.group_step(group, nsteps - 3)
+        Ig = np.concatenate([sv.intensity() for sv in group])
+        Tg = np.concatenate([sv.temperature() for sv in group])
+    finally:
+        for sv in group:
+            sv.close()
+    assert np.array_equal(Ig, I1) and np.array_equal(Tg, T1)
+
+
+def test_local_slab_group_mutation_skip_halo(Solver, monkeypatch):
+    """Mutation: without the halo copies the slab group must differ."""
+    p = _group_case("3d")
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(4)
+        I1 = sv.intensity()
+    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")
+    group = []
+    try:
+        for r in range(2):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=2)
+            for reg in range(6):
+                bc = p.bcs[reg]
+                sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+            group.append(sv)
+        Solver.group_step(group, 4)
+        Ig = np.concatenate([sv.intensity() for sv in group])
+    finally:
+        for sv in group:
+            sv.close()
+    assert not np.array_equal(Ig, I1)
