@@ -68,6 +68,7 @@ struct bte_ctx {
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
   int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
+  int newton_predict = 1;  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
@@ -553,6 +554,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
   }
   if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
+  if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   // column chunks for the sweep/Newton two-stream pipeline: off by default
   // (measured slower on B200); BTE_CHUNKS=n enables it.
   ctx->nchunks = 1;
@@ -760,6 +762,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.ncols = ctx->g.ncross;
   a.ncross = ctx->g.ncross;
   a.nplanes = ctx->g.nplanes;
+  a.predict = ctx->newton_predict;
   return a;
 }
 

@@ -85,6 +85,7 @@ struct NewtonArgs {
   int64_t step;           // step index for error reporting
   int col0, ncols;        // column (cross-cell) range of this launch
   int ncross, nplanes;
+  int predict;            // quadratic-convergence acceptance (reading R-f)
 };
 
 struct SweepArgs {

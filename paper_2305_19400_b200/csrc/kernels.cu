@@ -730,6 +730,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     status = ERR_NONFINITE;
   } else if (F0 != 0.0) {
     double T = Tn, lo = kTlo, hi = kThi, F = F0, Fp = Fp0;
+    double Tprev = 0.0, Fpprev = 0.0;
     bool conv = false;
     for (int it = 0; it <= kNewtonMaxIt; ++it) {
       if (it > 0) {
@@ -798,6 +799,20 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
         conv = true;
         break;
       }
+      if (it > 0 && a.predict && Tn1 > lo && Tn1 < hi) {
+        // reading R-f: quadratic convergence -- the next step would be about
+        // |F''/(2F')| stp^2 (F'' from the secant of F'); accept T - stp when that
+        // is 1000x below the tolerance, saving one band-integral evaluation.
+        const double F2 = (Fp - Fpprev) / (T - Tprev);
+        const double pred = fabs(F2 / (2.0 * Fp)) * stp * stp;
+        if (pred <= 1e-3 * kNewtonRtol * T) {
+          Tf = Tn1;
+          conv = true;
+          break;
+        }
+      }
+      Tprev = T;
+      Fpprev = Fp;
       if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
       T = Tn1;
     }
