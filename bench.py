@@ -53,6 +53,8 @@ def _problem(config: int, nranks: int):
         return bi.config3()
     if config == 5:
         return bi.config5(nranks)
+    if config == 6:  # the paper's own demo shape, single GPU
+        return bi.config_demo()
     raise SystemExit(f"unsupported --config {config}")
 
 

@@ -459,6 +459,19 @@ def config2(n: int = 120, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) 
                    dt=1e-12, T_init=300.0, bcs=bcs, nsteps=100, seed=SEED_BASE + 2)
 
 
+def config_demo(n: int = 120, ndirs: int = 20, n_freq: int = 40) -> Problem:
+    """The paper's own demonstration: 2-D 525 um square, 120x120
+    cells, 20 in-plane directions, 40 frequency bands -> 55 channels (40 LA +
+    15 TA), 20 x 55 = 1100 DOF per cell, ~1.6e7 DOF; Gaussian hot
+    spot on +y, 300 K on -y, symmetry (specular) sides; dt = 1e-12 s (reading #9);
+    100 steps."""
+    p = config2(n=n, n_freq=n_freq)
+    p.dirs = directions_inplane(ndirs)
+    p.name = f"demo_2d_si_{n}x{n}x{ndirs}x{p.bands.nb}"
+    p.seed = SEED_BASE + 6
+    return p
+
+
 def config3(n: int = 64, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
     """3-D silicon box n^3, 1 um cells, z=0 isothermal 300 K, z=L 310 K, x/y specular."""
     d = 1e-6
@@ -498,4 +511,4 @@ def small_3d(nx=5, ny=4, nz=3, dirs=None, bands=None, bcs=None, dt=1e-12, d=1e-6
                    bcs=bcs, nsteps=10, seed=seed)
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config_demo}

@@ -229,7 +229,8 @@ typedef struct {
   int octant;    /* sign pattern (4*[sx<0] + 2*[sy<0] + [sz<0]) moved     */
   int slot;      /* index of that octant among the non-empty ones         */
   int64_t plane; /* global plane index                                    */
-  int64_t count; /* doubles in the message (cells per plane * nj * nb)    */
+  int64_t count; /* doubles in the message: cells per plane * Es, where   */
+                 /* Es = nj*nb rounded up to even (device block stride)  */
 } bte_msg;
 typedef struct {
   int axis;        /* slab axis: 2 (z) for dim 3, 1 (y) for dim 2 */

@@ -68,7 +68,8 @@ struct bte_ctx {
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
   int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
-  int newton_predict = 1;  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int newton_predict = 1;
+  int newton_minb = 0;  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
@@ -221,7 +222,8 @@ bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int nb, int
   int slot = 0, n = 0;
   for (int o = 0; o < 8; ++o) {
     if (!count[o]) continue;
-    const int64_t cnt = cross * count[o] * (int64_t)nb;
+    const int64_t Eo = (int64_t)count[o] * nb;
+    const int64_t cnt = cross * (Eo + (Eo & 1));  // device plane incl. the even-stride pad
     const bool down = o & bit;  // slab-axis component < 0: upwind side is above
     const int to = down ? rank - 1 : rank + 1, from = down ? rank + 1 : rank - 1;
     if (to >= 0 && to < nranks) {
@@ -345,7 +347,8 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   g.nj = nj;
   g.nb = ctx->nb;
   g.E = nj * ctx->nb;
-  g.plane_stride = (int64_t)g.ncross * g.E;
+  g.Es = g.E + (g.E & 1);
+  g.plane_stride = (int64_t)g.ncross * g.Es;
   g.slot_stride = (int64_t)(g.nplanes + 2 * g.plane_off) * g.plane_stride;
   ctx->ncells_local = (int64_t)g.nplanes * g.ncross;
   ctx->ncells_global = mesh->nx * mesh->ny * mesh->nz;
@@ -555,6 +558,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   }
   if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
+  if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
   // column chunks for the sweep/Newton two-stream pipeline: off by default
   // (measured slower on B200); BTE_CHUNKS=n enables it.
   ctx->nchunks = 1;
@@ -763,6 +767,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.ncross = ctx->g.ncross;
   a.nplanes = ctx->g.nplanes;
   a.predict = ctx->newton_predict;
+  a.minb = ctx->newton_minb;
   return a;
 }
 

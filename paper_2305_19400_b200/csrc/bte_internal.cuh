@@ -60,6 +60,7 @@ struct Geometry {
   int64_t plane_stride;   // doubles per plane (ncross * E)
   int64_t slot_stride;    // doubles per slot
   int nslot, nj, nb, E;
+  int Es;                 // (cell, octant) block stride in doubles: E rounded up to even (16-B TMA)
   int slot_oct[kMaxSlots];
   int has_lo_wall, has_hi_wall;  // march-axis walls exist on this rank
   // per-(slot, j) coefficient table [nslot*nj][4]: dt|s_x|/dx, dt|s_y|/dy, dt|s_z|/dz, w
@@ -86,6 +87,7 @@ struct NewtonArgs {
   int col0, ncols;        // column (cross-cell) range of this launch
   int ncross, nplanes;
   int predict;            // quadratic-convergence acceptance (reading R-f)
+  int minb;               // k_newton occupancy variant (0 = default)
 };
 
 struct SweepArgs {

@@ -95,7 +95,7 @@ template <int DIM, int JMAX>
 __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb]
   const Geometry &g = A.g;
-  const int nb = g.nb, nj = g.nj, E = g.E;
+  const int nb = g.nb, nj = g.nj, E = g.E, Es = g.Es;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
   const int b = tid - grp * nb;
@@ -116,14 +116,14 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 
   const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
   const int xregion = xneg ? 1 : 0;
-  const int64_t xoff = xneg ? (int64_t)E : -(int64_t)E;
+  const int64_t xoff = xneg ? (int64_t)Es : -(int64_t)Es;
   bool yghost = false;
   int yregion = 2;
   int64_t yoff = 0;
   if (DIM == 3) {
     yghost = yneg ? (y == g.ny - 1) : (y == 0);
     yregion = yneg ? 3 : 2;
-    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
   }
   const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
 
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   const double *__restrict__ Iin = A.Iin;
   const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
   double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
-  const int64_t colE = (int64_t)col * E;
+  const int64_t colE = (int64_t)col * Es;
   const double dt = A.dt;
   const double v = A.v[b];
   const bool active = grp < JG && tid < JG * nb;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const int nb = NBT > 0 ? NBT : g.nb;
-  const int nj = g.nj, E = g.E;
+  const int nj = g.nj, E = g.E, Es = g.Es;
   const int S = A.stages;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
@@ -295,14 +295,14 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
   const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
   const int xregion = xneg ? 1 : 0;
-  const int64_t xoff = xneg ? (int64_t)E : -(int64_t)E;
+  const int64_t xoff = xneg ? (int64_t)Es : -(int64_t)Es;
   bool yghost = false;
   int yregion = 2;
   int64_t yoff = 0;
   if (DIM == 3) {
     yghost = yneg ? (y == g.ny - 1) : (y == 0);
     yregion = yneg ? 3 : 2;
-    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * E;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
   }
   const bool interior = !xghost && !yghost;
   const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   double *stage0 = red + 2 * JG * nb;                            // [S][stage_doubles]
   const int64_t sd = A.stage_doubles;                            // own | xup | (yup) | I0 | beta
   const int nblk = 1 + (xghost ? 0 : 1) + ((DIM == 3 && !yghost) ? 1 : 0);
-  const int o_x = E, o_y = 2 * E, o_i0 = (DIM == 3 ? 3 : 2) * E, o_be = o_i0 + nb;
+  const int o_x = Es, o_y = 2 * Es, o_i0 = (DIM == 3 ? 3 : 2) * Es, o_be = o_i0 + nb;
+  const bool rows_tma = (nb % 2) == 0;  // 16-B bulk-copy granularity; else direct loads
 
   const int pb = blockIdx.z * A.seg_len;
   const int pe = min(g.nplanes, pb + A.seg_len);
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const double *__restrict__ Iin = A.Iin;
   const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
   double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
-  const int64_t colE = (int64_t)col * E;
+  const int64_t colE = (int64_t)col * Es;
   const double dt = A.dt;
 
   auto issue = [&](int i, int st) {
@@ -333,14 +334,16 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     const int64_t base = (int64_t)(pp + g.plane_off) * g.plane_stride + colE;
     const int64_t cell = (int64_t)col + (int64_t)pp * g.ncross;
     double *sp = stage0 + st * sd;
-    const uint32_t blk = (uint32_t)E * 8u;
+    const uint32_t blk = (uint32_t)Es * 8u;
     const uint32_t row = (uint32_t)nb * 8u;
-    mbar_expect_tx(&full[st], blk * nblk + 2u * row);
+    mbar_expect_tx(&full[st], blk * nblk + (rows_tma ? 2u * row : 0u));
     bulk_g2s(sp, Is + base, blk, &full[st]);
     if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
     if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
-    bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
-    bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
+    if (rows_tma) {
+      bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
+      bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
+    }
   };
 
   if (tid == 0) {
@@ -384,8 +387,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     mbar_wait(&full[st], (uint32_t)((i / S) & 1));
     double acc = 0.0;
     if (active) {
-      const double I0 = sp[o_i0 + b];
-      const double dtb = dt * sp[o_be + b];
+      const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + cell * nb + b);
+      const double dtb = dt * (rows_tma ? sp[o_be + b] : ldg(A.beta + cell * nb + b));
       const double *so = sp + e0;
       double *op = Os + base + e0;
       if (interior && nloc == JMAX) {
@@ -506,10 +509,10 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
   dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
-  const bool tma = a.use_tma && (g.E % 2 == 0) && (g.nb % 2 == 0);
+  const bool tma = a.use_tma && (g.Es % 2 == 0);
   if (tma) {
     // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B
-    const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.E + 2 * g.nb + 15) / 16 * 16;
+    const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.Es + 2 * g.nb + 15) / 16 * 16;
     const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
     const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;  // two CTAs/SM
     int S = (int)((budget > fixed ? budget - fixed : 0) / (stage_d * sizeof(double)));
@@ -631,7 +634,7 @@ __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int re
   }
   (void)march;
   const int64_t cross = (g.dim == 3) ? x + (int64_t)g.nx * y : x;
-  const int64_t cell_base = (int64_t)(p + g.plane_off) * g.plane_stride + cross * g.E;
+  const int64_t cell_base = (int64_t)(p + g.plane_off) * g.plane_stride + cross * g.Es;
   // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
   const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
@@ -675,6 +678,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 constexpr int kNewtonWarps = 8;
+#ifndef BTE_NEWTON_MINB
+#define BTE_NEWTON_MINB 4  // resident blocks per SM (caps registers at 64)
+#endif
 
 // 1/x for x > 0 finite: MUFU seed + two Newton-Raphson steps (<= 1 ulp);
 // +inf -> 0 (a Bose-Einstein term whose exponent overflowed contributes 0).
@@ -901,7 +907,8 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
 //   F'(T) = W sum_b c_b dI0_b/dT
 // F(T^n) = sum_b c_b D_b exactly (I0c = I0(T^n)) and F'(T^n) uses the dI0/dT
 // stored by the previous refresh, so the first Newton step costs no integral.
-__global__ void __launch_bounds__(32 * kNewtonWarps) k_newton(const NewtonArgs a) {
+template <int MINB>
+__global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const NewtonArgs a) {
   extern __shared__ double nsh[];
   const int nb = a.nb;
   double *sA = nsh;
@@ -934,8 +941,22 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
   const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_newton<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
+  const int minb = a.minb > 0 ? a.minb : BTE_NEWTON_MINB;
+#define BTE_NL(M)                                                                                   \
+  case M:                                                                                           \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_newton<M><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);                                 \
+    break;
+  switch (minb) {
+    BTE_NL(2)
+    BTE_NL(3)
+    BTE_NL(4)
+    BTE_NL(5)
+    BTE_NL(6)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef BTE_NL
   return cudaGetLastError();
 }
 
@@ -989,7 +1010,7 @@ __global__ void k_fill_eq(const Geometry g, const double *__restrict__ I0c, doub
   const int64_t cell = r / g.E;
   const int e = (int)(r - cell * g.E);
   const int b = e % g.nb;
-  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + r] = I0c[cell * g.nb + b];
+  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] = I0c[cell * g.nb + b];
 }
 
 cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I, cudaStream_t s) {
@@ -1016,7 +1037,7 @@ __global__ void k_permute(const Geometry g, const int *__restrict__ dmap, int nd
   const int64_t c = c0 + cr;
   const int64_t p = c / g.ncross;
   const int64_t cross = c - p * g.ncross;
-  const int64_t dst = sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E +
+  const int64_t dst = sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es +
                       (int64_t)j * g.nb + b;
   if (to_layout)
     I[dst] = canon[i];
@@ -1088,7 +1109,7 @@ __global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, in
   const int64_t cg = g.m0 * g.ncross + cell;
   const uint64_t idx = ((uint64_t)cg * nd + d) * g.nb + b;
   const double u = (double)(splitmix64(seed ^ idx) >> 11) * 0x1.0p-53;
-  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + r] =
+  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] =
       I0c[cell * g.nb + b] * (1.0 + amp * (2.0 * u - 1.0));
 }
 
@@ -1129,7 +1150,7 @@ __global__ void k_dpart_from_I(const Geometry g, const double *__restrict__ I, c
   const int sl = (int)((i / g.nb) % g.nslot);
   const int64_t c = i / ((int64_t)g.nb * g.nslot);
   const int64_t p = c / g.ncross, cross = c - p * g.ncross;
-  const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E + b;
+  const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es + b;
   const double i0 = I0c[c * g.nb + b];
   double s = 0.0;
   for (int j = 0; j < g.nj; ++j) s += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] * (i0 - Ip[(int64_t)j * g.nb]);
@@ -1154,7 +1175,7 @@ __global__ void k_energy(const Geometry g, const double *__restrict__ I, const d
   const int64_t p = c / g.ncross, cross = c - p * g.ncross;
   double acc = 0.0;
   for (int sl = 0; sl < g.nslot; ++sl) {
-    const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.E;
+    const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es;
     for (int e = lane; e < g.E; e += 32) {
       const int j = e / g.nb, b = e - j * g.nb;
       acc += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] / v[b] * Ip[e];

@@ -470,3 +470,13 @@ def test_local_slab_group_mutation_skip_halo(Solver, monkeypatch):
         for sv in group:
             sv.close()
     assert not np.array_equal(Ig, I1)
+
+
+@pytest.mark.parametrize("start,nsteps", [("physical", 100), ("random", 20)])
+def test_demo_workload_full_size(Solver, start, nsteps):
+    """The paper's own demo at full size: 120x120 cells,
+    20 in-plane directions, 55 channels (odd (cell, quadrant) block: 5 x 55
+    doubles -> padded even stride), full-field parity."""
+    p = bi.config_demo()
+    (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, nsteps, start=start)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
