@@ -42,6 +42,8 @@ BYTES_PER_DOF = 16  # read I^n + write I^{n+1}, fp64
 
 
 def _problem(config: int, nranks: int):
+    if config not in (1, 2, 3, 5, 6):
+        raise SystemExit(f"unsupported --config {config}")
     if config == 2:
         p = bi.config2()
         if nranks > 1:  # weak scaling: 120 rows per GPU along the slab axis
@@ -55,6 +57,8 @@ def _problem(config: int, nranks: int):
         return bi.config5(nranks)
     if config == 6:  # the paper's own demo shape, single GPU
         return bi.config_demo()
+    if config == 1:  # BASELINE configs[0]: latency-bound, not roofline-gated
+        return bi.config1()
     raise SystemExit(f"unsupported --config {config}")
 
 

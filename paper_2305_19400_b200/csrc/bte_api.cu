@@ -69,7 +69,8 @@ struct bte_ctx {
   unsigned long long *d_err = nullptr;
   int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
   int newton_predict = 1;
-  int newton_minb = 0;  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int newton_minb = 0;
+  int tx_override = 0;  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
@@ -559,6 +560,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
+  if (const char *e = getenv("BTE_TX")) ctx->tx_override = atoi(e);
   // column chunks for the sweep/Newton two-stream pipeline: off by default
   // (measured slower on B200); BTE_CHUNKS=n enables it.
   ctx->nchunks = 1;
@@ -791,6 +793,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.target_threads = ctx->target_threads;
   a.smem_budget_kb = ctx->smem_budget_kb;
   a.stcs = ctx->stcs;
+  a.tx_override = ctx->tx_override;
   a.nw = newton_args(ctx, step);
   a.fuse_newton = allow_fuse && ctx->fuse_newton;
   a.done = ctx->d_done;

@@ -101,6 +101,8 @@ struct SweepArgs {
   int seg_len;            // cells per CTA along the march axis
   int jpt;                // directions per thread (set by launch_sweep)
   int jg;                 // thread groups (set by launch_sweep)
+  int tx;                 // columns per CTA (k_sweep_tmx; set by launch_sweep)
+  int tx_override;        // 0 auto, 1 force single-column kernel, > 1 force k_sweep_tmx width
   int use_tma;            // cp.async.bulk pipeline (k_sweep_tma) when the layout allows
   int stages;             // pipeline depth (set by launch_sweep)
   int stages_override;    // 0 = automatic

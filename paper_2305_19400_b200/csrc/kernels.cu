@@ -484,6 +484,199 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   }
 }
 
+// Multi-column variant for small (cell, octant) blocks (e.g. the paper's demo:
+// 5 directions x 55 channels = 2.2 KB): one CTA = TX adjacent columns of one
+// x-row (fixed y in 3-D) x one octant slot x one segment.  Per plane one bulk
+// copy brings the TX own blocks plus the upwind halo column (contiguous in
+// memory), so the x-upwind value of every interior column comes from the same
+// stage; 3-D adds one copy of the TX y-upwind blocks.  Thread (t, grp, b)
+// owns column t, channel b and directions [grp*jpt, grp*jpt + jpt).
+template <int DIM, int JMAX>
+__global__ void __launch_bounds__(1024) k_sweep_tmx(const SweepArgs A) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const Geometry &g = A.g;
+  const int nb = g.nb, nj = g.nj, Es = g.Es;
+  const int S = A.stages, TX = A.tx, JG = A.jg;
+  const int tpc = JG * nb;  // threads per column
+  const int tid = threadIdx.x;
+  const int t = tid / tpc;
+  const int rr0 = tid - t * tpc;
+  const int grp = rr0 / nb;
+  const int b = rr0 - grp * nb;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+
+  const int slot = blockIdx.y;
+  const int oct = g.slot_oct[slot];
+  const int ngx = (g.nx + TX - 1) / TX;
+  const int gx = blockIdx.x % ngx;
+  const int y = (DIM == 3) ? blockIdx.x / ngx : 0;
+  const int x0 = gx * TX, x1 = min(g.nx, x0 + TX), tw = x1 - x0;
+  const bool active = t < tw;
+  const int x = x0 + t;
+  const bool xneg = oct & 4;
+  const bool yneg = oct & 2;
+  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
+  const bool halo = xneg ? (x1 < g.nx) : (x0 > 0);
+  const int xa = (xneg || !halo) ? x0 : x0 - 1;
+  const int nxb = tw + (halo ? 1 : 0);
+  const int own_idx = x - xa;
+  const int up_idx = xneg ? own_idx + 1 : own_idx - 1;
+  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
+  const int xregion = xneg ? 1 : 0;
+  bool yghost = false;
+  int yregion = 2;
+  int ycol = 0;
+  if (DIM == 3) {
+    yghost = yneg ? (y == g.ny - 1) : (y == 0);
+    yregion = yneg ? 3 : 2;
+    ycol = yneg ? g.nx : -g.nx;
+  }
+  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
+  const int64_t rowcol0 = (DIM == 3) ? (int64_t)y * g.nx : 0;  // cross index of x = 0 in this row
+  const int64_t colx = rowcol0 + x;
+
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  double *coef = reinterpret_cast<double *>(smraw + 128);
+  double *red = coef + 4 * nj;                // [2][TX*tpc]
+  double *stage0 = red + 2 * TX * tpc;
+  const int64_t sd = A.stage_doubles;
+  const int oY = (TX + 1) * Es;
+  const int oI0 = oY + (DIM == 3 ? TX * Es : 0);
+  const int oBe = oI0 + TX * nb;
+  const bool rows_tma = (nb % 2) == 0;
+
+  const int pb = blockIdx.z * A.seg_len;
+  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int np = pe - pb;
+  const int step = mneg ? -1 : 1;
+  const int pfirst = mneg ? pe - 1 : pb;
+
+  const double *__restrict__ Iin = A.Iin;
+  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
+  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const double dt = A.dt;
+
+  auto issue = [&](int i, int st) {
+    const int pp = pfirst + i * step;
+    const int64_t pbase = (int64_t)(pp + g.plane_off) * g.plane_stride;
+    const int64_t cell0 = rowcol0 + x0 + (int64_t)pp * g.ncross;
+    double *sp = stage0 + st * sd;
+    const uint32_t bx = (uint32_t)nxb * Es * 8u;
+    const uint32_t by = (DIM == 3 && !yghost) ? (uint32_t)tw * Es * 8u : 0u;
+    const uint32_t br = rows_tma ? (uint32_t)tw * nb * 8u : 0u;
+    mbar_expect_tx(&full[st], bx + by + 2u * br);
+    bulk_g2s(sp, Is + pbase + (rowcol0 + xa) * Es, bx, &full[st]);
+    if (by) bulk_g2s(sp + oY, Is + pbase + (rowcol0 + x0 + ycol) * Es, by, &full[st]);
+    if (br) {
+      bulk_g2s(sp + oI0, A.I0c + cell0 * nb, br, &full[st]);
+      bulk_g2s(sp + oBe, A.beta + cell0 * nb, br, &full[st]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < min(S, np); ++i) issue(i, i);
+
+  const double v = A.v[b];
+  const int e0 = j0 * nb + b;
+  const double *cq = coef + 4 * j0;
+  double prev[JMAX];
+  {
+    const int p = pfirst;
+    const int pm = p - step;
+    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colx * Es;
+    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      prev[k] = 0.0;
+      if (active && grp < JG && k < nloc) {
+        if (stored)
+          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colx * Es + e0 + k * nb);
+        else
+          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
+      }
+    }
+  }
+
+  int buf = 0;
+  int p = pfirst;
+  for (int i = 0; i < np; ++i, p += step) {
+    const int st = i % S;
+    const int64_t cell = colx + (int64_t)p * g.ncross;
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colx * Es;
+    const double *sp = stage0 + st * sd;
+    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    double acc = 0.0;
+    if (active && grp < JG) {
+      const double I0 = rows_tma ? sp[oI0 + t * nb + b] : ldg(A.I0c + cell * nb + b);
+      const double dtb = dt * (rows_tma ? sp[oBe + t * nb + b] : ldg(A.beta + cell * nb + b));
+      const double *so = sp + own_idx * Es + e0;
+      const double *sxu = sp + up_idx * Es + e0;
+      const double *syu = sp + oY + t * Es + e0;
+      double *op = Os + base + e0;
+      if (!xghost && !yghost && nloc == JMAX) {
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+          const double Ic = so[k * nb];
+          const double In = bte_update<DIM>(Ic, sxu[k * nb], DIM == 3 ? syu[k * nb] : 0.0, prev[k], cq + 4 * k, v,
+                                            I0, dtb);
+          __stcs(op + k * nb, In);
+          acc = fma(cq[4 * k + 3], I0 - In, acc);
+          prev[k] = Ic;
+        }
+      } else {
+        const int64_t mg = g.m0 + p;
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+          if (k < nloc) {
+            const int j = j0 + k;
+            const double Ic = so[k * nb];
+            double xu, yu = 0.0;
+            if (!xghost) {
+              xu = sxu[k * nb];
+            } else {
+              const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+              xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
+            }
+            if (DIM == 3) {
+              if (!yghost) {
+                yu = syu[k * nb];
+              } else {
+                const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+                yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
+              }
+            }
+            const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cq + 4 * k, v, I0, dtb);
+            __stcs(op + k * nb, In);
+            acc = fma(cq[4 * k + 3], I0 - In, acc);
+            prev[k] = Ic;
+          }
+        }
+      }
+    }
+    double *rb = red + buf * TX * tpc;
+    if (tid < TX * tpc) rb[tid] = acc;
+    __syncthreads();
+    if (tid == 0 && i + S < np) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S, st);
+    }
+    if (active && grp == 0) {
+      double s = 0.0;
+      for (int q = 0; q < JG; ++q) s += rb[t * tpc + q * nb + b];
+      A.Dpart[(cell * g.nslot + slot) * nb + b] = s;
+    }
+    buf ^= 1;
+  }
+}
+
 // thread shape: JG groups of nb threads, jpt directions per thread
 static void sweep_shape(int nb, int nj, int target, int *jpt, int *JG) {
   int jg = (target + nb / 2) / nb;
@@ -510,7 +703,51 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.Es % 2 == 0);
-  if (tma) {
+  // small blocks: several columns per CTA (k_sweep_tmx)
+  const bool full_cols = (a.ncols <= 0 || a.ncols == g.ncross) && a.col0 == 0;
+  if (tma && full_cols && !a.fuse_newton && a.tx_override > 1 && g.nj <= 16) {
+    int jp = g.nj, jgm = 1;                     // all directions of the octant in one thread
+    const int tpc = jgm * g.nb;
+    int TX = std::max(1, std::min(g.nx, 448 / std::max(1, tpc)));
+    if (a.tx_override > 1) TX = std::min(g.nx, a.tx_override);
+    const int thr = ((TX * tpc) + 31) / 32 * 32;
+    if (thr <= 1024) {
+      a.jpt = jp;
+      a.jg = jgm;
+      a.tx = TX;
+      const int64_t sdx = ((int64_t)(TX + 1) * g.Es + (DIM == 3 ? (int64_t)TX * g.Es : 0) + 2 * (int64_t)TX * g.nb + 15) /
+                          16 * 16;
+      const size_t fixedx = 128 + (4 * (size_t)g.nj + 2 * (size_t)TX * tpc) * sizeof(double);
+      const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;
+      int S = (int)((budget > fixedx ? budget - fixedx : 0) / (sdx * sizeof(double)));
+      S = std::max(2, std::min(4, S));
+      if (a.stages_override > 0) S = std::min(16, a.stages_override);
+      a.stages = S;
+      a.stage_doubles = sdx;
+      const size_t smem = fixedx + (size_t)S * sdx * sizeof(double);
+      const int ngx = (g.nx + TX - 1) / TX;
+      dim3 gridx(ngx * (DIM == 3 ? g.ny : 1), g.nslot, nseg);
+      const int jc = jp <= 1 ? 1 : jp <= 2 ? 2 : jp <= 4 ? 4 : jp <= 5 ? 5 : jp <= 8 ? 8 : 16;
+      switch (jc) {
+#define BTE_TMX(N)                                                                                  \
+  case N:                                                                                           \
+    cudaFuncSetAttribute(k_sweep_tmx<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_sweep_tmx<DIM, N><<<gridx, thr, smem, s>>>(a);                                                \
+    break;
+        BTE_TMX(1)
+        BTE_TMX(2)
+        BTE_TMX(4)
+        BTE_TMX(5)
+        BTE_TMX(8)
+        BTE_TMX(16)
+#undef BTE_TMX
+      }
+      return cudaGetLastError();
+    }
+  }
+  // blocks under 384 doubles: the direct-load kernel keeps more cells in
+  // flight than a per-cell TMA ring (measured: demo 0.089 vs 0.110 ms)
+  if (tma && g.E >= 384) {
     // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B
     const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.Es + 2 * g.nb + 15) / 16 * 16;
     const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
