@@ -90,6 +90,8 @@ struct bte_ctx {
   cudaStream_t nstream = nullptr;
   std::vector<cudaEvent_t> ev_sw, ev_nt;
   std::vector<char> nt_pending;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;  // boundary planes swept / halo delivered
+  int overlap = 1;  // env BTE_OVERLAP=0: exchange after the whole sweep
   // NCCL
   bte_slab_plan plan{};
   void *nccl_comm = nullptr;
@@ -198,7 +200,7 @@ static bte_status sync_check(bte_ctx *ctx) {
 
 extern "C" {
 
-static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream = nullptr);
 
 const char *bte_version(void) { return "bte-b200 0.1 (sm_100a, fp64)"; }
 
@@ -575,6 +577,10 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     for (auto &e : ctx->ev_nt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   ctx->nt_pending.assign(ctx->nchunks, 0);
+  if (const char *e = getenv("BTE_OVERLAP")) ctx->overlap = atoi(e);
+  CU(cudaEventCreateWithFlags(&ctx->ev_bnd, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+  if (ctx->nranks > 1 && !ctx->comm_stream) CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   {
     const int64_t nseg = (g.nplanes + ctx->seg_len - 1) / ctx->seg_len;
     ctx->d_done = (int *)dev_alloc(ctx, nseg * g.ncross * sizeof(int));
@@ -587,7 +593,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     std::string emsg;
     if (nccl_shim_init(&ctx->nccl_comm, run->nccl_id, ctx->nranks, ctx->rank, &emsg) != 0)
       return bail(fail(ctx, BTE_ENCCL, "NCCL init failed: %s", emsg.c_str()));
-    CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    if (!ctx->comm_stream) CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   }
 
   // ---- initial state: equilibrium at T_init
@@ -663,7 +669,6 @@ static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
 
 static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0 = 0, int ncols = -1,
                              cudaStream_t stream = nullptr);
-static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   if (!ctx) return BTE_EINVAL;
@@ -775,10 +780,13 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
 
 // a1+a2 (+ a3+a4 fused into the sweep tail when *fused is set on return)
 static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
-                                    int *fused, int col0 = 0, int ncols = 0) {
+                                    int *fused, int col0 = 0, int ncols = 0, int p_lo = 0, int p_hi = 0,
+                                    int seg_len = 0) {
   SweepArgs a;
   a.col0 = col0;
   a.ncols = ncols;
+  a.p_lo = p_lo;
+  a.p_hi = p_hi;
   a.g = ctx->g;
   a.Iin = Iin;
   a.Iout = Iout;
@@ -787,7 +795,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.Dpart = ctx->Dpart;
   a.v = ctx->m.v;
   a.dt = ctx->dt;
-  a.seg_len = ctx->seg_len;
+  a.seg_len = seg_len > 0 ? seg_len : ctx->seg_len;
   a.use_tma = ctx->use_tma;
   a.stages_override = ctx->stages_override;
   a.target_threads = ctx->target_threads;
@@ -815,7 +823,6 @@ static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0, int ncols, cu
   return BTE_OK;
 }
 
-static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf);
 
 static bte_status span_begin(bte_ctx *ctx, bool t, int kind, cudaStream_t s, size_t *id) {
   if (!t) return BTE_OK;
@@ -837,10 +844,14 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
 // The next step's sweep(k) waits only for Newton(k), so the FP64-bound Newton
 // of chunk k overlaps the HBM-bound sweeps of the other chunks.
 // Launch one step (a1..a4) of ctx on its streams; the caller exchanges halos.
-static bte_status step_launch(bte_ctx *ctx, bool t) {
+// split: sweep the two owned boundary planes first and record ctx->ev_bnd, so
+// the halo exchange (a5) can run on the comm stream while the interior planes
+// are swept (SURVEY 8(e) overlap schedule).
+static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   const bool has_bnd = n_diffuse(ctx) > 0;
   const int C = ctx->fuse_newton ? 1 : ctx->nchunks;
   const int ncross = ctx->g.ncross;
+  const int np = ctx->g.nplanes;
   bte_status st;
   double *Iin = ctx->I[ctx->cur];
   double *Iout = ctx->I[1 - ctx->cur];
@@ -849,6 +860,28 @@ static bte_status step_launch(bte_ctx *ctx, bool t) {
     if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
     if ((st = launch_boundary(ctx, Iin))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+  }
+  if (split && (C > 1 || ctx->fuse_newton)) split = false;
+  if (split) {
+    int fused = 0;
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
+    if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, 0, 1, 1))) return st;
+    if (np > 1 && (st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, np - 1, np, 1)))
+      return st;
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
+    if (np > 2) {
+      id = (size_t)-1;
+      if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
+      if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, 1, np - 1))) return st;
+      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    }
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
+    if ((st = run_newton(ctx, ctx->steps_done, 0, -1, ctx->stream))) return st;
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    return BTE_OK;
   }
   for (int k = 0; k < C; ++k) {
     const int c0 = (int)((int64_t)k * ncross / C), c1 = (int)((int64_t)(k + 1) * ncross / C);
@@ -874,6 +907,7 @@ static bte_status step_launch(bte_ctx *ctx, bool t) {
       ctx->nt_pending[k] = 1;
     }
   }
+  CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
   return BTE_OK;
 }
 
@@ -897,12 +931,17 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
   bte_status st;
   for (int64_t s = 0; s < nsteps; ++s) {
     const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
-    if ((st = step_launch(ctx, t))) return st;
+    if ((st = step_launch(ctx, t, ctx->nranks > 1 && ctx->overlap))) return st;
     if (ctx->nranks > 1) {
+      // a5 on the comm stream once the boundary planes are swept; the next
+      // step's sweeps wait for it (the wait sits after this step's Newton)
+      CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
       size_t id = (size_t)-1;
-      if ((st = span_begin(ctx, t, 3, ctx->stream, &id))) return st;
-      if ((st = halo_exchange(ctx, ctx->I[1 - ctx->cur]))) return st;
-      if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+      if ((st = span_begin(ctx, t, 3, ctx->comm_stream, &id))) return st;
+      if ((st = halo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream))) return st;
+      if ((st = span_end(ctx, t, ctx->comm_stream, id))) return st;
+      CU(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
     }
     if (t) ctx->timing_used++;
     ctx->cur = 1 - ctx->cur;
@@ -954,6 +993,39 @@ static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
   return BTE_OK;
 }
 
+// Per-step local exchange, overlapped: on each sender's comm stream, once the
+// sender's boundary planes and the receiver's previous step are done (both
+// ev_bnd), copy the planes into the receiver's halo; each receiver's compute
+// stream waits for its senders' copies after this step's Newton.
+static bte_status group_exchange_overlap(bte_ctx **ctxs, int n) {
+  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
+    if (atoi(e)) return BTE_OK;
+  bte_ctx *ctx = ctxs[0];
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    const Geometry &g = c->g;
+    CU(cudaStreamWaitEvent(c->comm_stream, c->ev_bnd, 0));
+    const double *src = c->I[1 - c->cur];
+    for (int k = 0; k < c->plan.n_msgs; ++k) {
+      const bte_msg &m = c->plan.msg[k];
+      if (!m.send) continue;
+      bte_ctx *q = ctxs[m.peer];
+      CU(cudaStreamWaitEvent(c->comm_stream, q->ev_bnd, 0));
+      double *dst = q->I[1 - q->cur];
+      const double *sp = src + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+      double *dp = dst + (int64_t)m.slot * q->g.slot_stride + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
+      CU(cudaMemcpyAsync(dp, sp, (size_t)m.count * sizeof(double), cudaMemcpyDefault, c->comm_stream));
+    }
+    CU(cudaEventRecord(c->ev_halo, c->comm_stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    for (int k = 0; k < c->plan.n_msgs; ++k)
+      if (!c->plan.msg[k].send) CU(cudaStreamWaitEvent(c->stream, ctxs[c->plan.msg[k].peer]->ev_halo, 0));
+  }
+  return BTE_OK;
+}
+
 bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
   if (!ctxs || n < 1 || nsteps < 0) return BTE_EINVAL;
   for (int r = 0; r < n; ++r) {
@@ -968,10 +1040,10 @@ bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
   for (int64_t s = 0; s < nsteps; ++s) {
     for (int r = 0; r < n; ++r) {
       const bool t = ctxs[r]->timing && ctxs[r]->timing_used < ctxs[r]->timing_max;
-      if ((st = step_launch(ctxs[r], t))) return st;
+      if ((st = step_launch(ctxs[r], t, n > 1 && ctxs[r]->overlap))) return st;
       if ((st = join_newton(ctxs[r]))) return st;
     }
-    if (n > 1 && (st = group_exchange(ctxs, n, true))) return st;
+    if (n > 1 && (st = group_exchange_overlap(ctxs, n))) return st;
     for (int r = 0; r < n; ++r) {
       bte_ctx *c = ctxs[r];
       if (c->timing && c->timing_used < c->timing_max) c->timing_used++;
@@ -984,17 +1056,19 @@ bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
   return BTE_OK;
 }
 
-static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf) {
-  // a5: execute this rank's halo plan (bte_plan_slab) as one NCCL group on the
-  // context stream; plane p (global) lives at local index p - m0 + plane_off.
+static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream) {
+  // a5: execute this rank's halo plan (bte_plan_slab) as one NCCL group on
+  // `stream` (default: the context stream); plane p (global) lives at local
+  // index p - m0 + plane_off.
   const Geometry &g = ctx->g;
+  if (!stream) stream = ctx->stream;
   std::string emsg;
   if (nccl_shim_group_start(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
   for (int k = 0; k < ctx->plan.n_msgs; ++k) {
     const bte_msg &m = ctx->plan.msg[k];
     double *ptr = Ibuf + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
-    const int rc = m.send ? nccl_shim_send(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, ctx->stream, &emsg)
-                          : nccl_shim_recv(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, ctx->stream, &emsg);
+    const int rc = m.send ? nccl_shim_send(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, stream, &emsg)
+                          : nccl_shim_recv(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, stream, &emsg);
     if (rc) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
   }
   if (nccl_shim_group_end(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
@@ -1129,6 +1203,9 @@ void bte_destroy(bte_ctx *ctx) {
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_sw) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_nt) cudaEventDestroy(e);
+  if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
   if (ctx->nstream) cudaStreamDestroy(ctx->nstream);
   if (ctx->nccl_comm) nccl_shim_destroy(ctx->nccl_comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);

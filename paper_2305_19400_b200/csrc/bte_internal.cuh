@@ -111,6 +111,7 @@ struct SweepArgs {
   int stcs;               // streaming (evict-first) stores of I^{n+1}
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int col0, ncols;        // column range of this launch (ncols = 0: all)
+  int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
   NewtonArgs nw;          // fused a3+a4 (k_sweep_tma tail)
   int fuse_newton;
   int *done;              // [nseg][ncross] tickets, zero between launches

@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
 
-  const int pb = blockIdx.z * A.seg_len;
-  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int pb = A.p_lo + blockIdx.z * A.seg_len;
+  const int pe = min(A.p_hi, pb + A.seg_len);
   const int np = pe - pb;
   const int step = mneg ? -1 : 1;
   int p = mneg ? pe - 1 : pb;
@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const int o_x = Es, o_y = 2 * Es, o_i0 = (DIM == 3 ? 3 : 2) * Es, o_be = o_i0 + nb;
   const bool rows_tma = (nb % 2) == 0;  // 16-B bulk-copy granularity; else direct loads
 
-  const int pb = blockIdx.z * A.seg_len;
-  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int pb = A.p_lo + blockIdx.z * A.seg_len;
+  const int pe = min(A.p_hi, pb + A.seg_len);
   const int np = pe - pb;
   const int step = mneg ? -1 : 1;
   const int pfirst = mneg ? pe - 1 : pb;
@@ -546,8 +546,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tmx(const SweepArgs A) {
   const int oBe = oI0 + TX * nb;
   const bool rows_tma = (nb % 2) == 0;
 
-  const int pb = blockIdx.z * A.seg_len;
-  const int pe = min(g.nplanes, pb + A.seg_len);
+  const int pb = A.p_lo + blockIdx.z * A.seg_len;
+  const int pe = min(A.p_hi, pb + A.seg_len);
   const int np = pe - pb;
   const int step = mneg ? -1 : 1;
   const int pfirst = mneg ? pe - 1 : pb;
@@ -699,7 +699,11 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   a.jpt = jpt;
   const int threads = JG * g.nb;
   if (threads > 1024 || g.nb > 1024) return cudaErrorInvalidConfiguration;
-  const int nseg = (g.nplanes + a.seg_len - 1) / a.seg_len;
+  if (a.p_hi <= a.p_lo) {  // default: every owned plane
+    a.p_lo = 0;
+    a.p_hi = g.nplanes;
+  }
+  const int nseg = (a.p_hi - a.p_lo + a.seg_len - 1) / a.seg_len;
   dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.Es % 2 == 0);

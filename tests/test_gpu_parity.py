@@ -410,10 +410,12 @@ def _group_case(case):
 
 @pytest.mark.parametrize("case", ["3d", "2d"])
 @pytest.mark.parametrize("P", [2, 3])
-def test_local_slab_group_matches_single_domain(Solver, case, P):
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_local_slab_group_matches_single_domain(Solver, case, P, overlap, monkeypatch):
     """Multi-rank data path on one GPU: P slab contexts (halo planes, walls only
     on the end ranks, bte_plan_slab exchange by device copies) reproduce the
     single-context run bit-for-bit (per-DOF arithmetic is partition-free)."""
+    monkeypatch.setenv("BTE_OVERLAP", overlap)  # boundary planes first + exchange on the comm stream
     p = _group_case(case)
     o = oracle.Oracle(p)
     I, T = o.random_state()
