@@ -70,7 +70,9 @@ struct bte_ctx {
   int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
   int newton_predict = 1;
   int newton_minb = 0;
-  int tx_override = 0;  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int tx_override = 0;
+  unsigned long long *d_stats = nullptr;  // env BTE_NEWTON_STATS=1: Newton counters printed by bte_step
+  int l2hint = 0;  // env BTE_L2HINT  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
@@ -563,6 +565,12 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
   if (const char *e = getenv("BTE_TX")) ctx->tx_override = atoi(e);
+  if (const char *e = getenv("BTE_L2HINT")) ctx->l2hint = atoi(e);
+  if (const char *e = getenv("BTE_NEWTON_STATS"))
+    if (atoi(e)) {
+      ctx->d_stats = (unsigned long long *)dev_alloc(ctx, 4 * sizeof(unsigned long long));
+      if (ctx->d_stats) CU(cudaMemsetAsync(ctx->d_stats, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    }
   // column chunks for the sweep/Newton two-stream pipeline: off by default
   // (measured slower on B200); BTE_CHUNKS=n enables it.
   ctx->nchunks = 1;
@@ -775,6 +783,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.nplanes = ctx->g.nplanes;
   a.predict = ctx->newton_predict;
   a.minb = ctx->newton_minb;
+  a.stats = ctx->d_stats;
   return a;
 }
 
@@ -802,6 +811,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.smem_budget_kb = ctx->smem_budget_kb;
   a.stcs = ctx->stcs;
   a.tx_override = ctx->tx_override;
+  a.l2hint = ctx->l2hint;
   a.nw = newton_args(ctx, step);
   a.fuse_newton = allow_fuse && ctx->fuse_newton;
   a.done = ctx->d_done;
@@ -948,6 +958,13 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
     ctx->steps_done++;
   }
   if ((st = join_newton(ctx))) return st;
+  if (ctx->d_stats) {
+    unsigned long long h[4];
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(h, ctx->d_stats, sizeof h, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[bte] Newton stats after %lld steps: evaluations %llu, final re-evaluations %llu, cells solved %llu\n",
+            (long long)ctx->steps_done, h[0], h[1], h[2]);
+  }
   return sync_check(ctx);
 }
 

@@ -88,6 +88,7 @@ struct NewtonArgs {
   int ncross, nplanes;
   int predict;            // quadratic-convergence acceptance (reading R-f)
   int minb;               // k_newton occupancy variant (0 = default)
+  unsigned long long *stats;  // debug counters: [evaluations, final re-evaluations, cells solved] or null
 };
 
 struct SweepArgs {
@@ -109,6 +110,7 @@ struct SweepArgs {
   int target_threads;     // CTA size target (0 = 448)
   int smem_budget_kb;     // per-CTA shared memory budget for the stage ring (0 = 113 KB)
   int stcs;               // streaming (evict-first) stores of I^{n+1}
+  int l2hint;             // bulk-copy L2 policies: 0 none, 1 last-use evict-first, 2 + own evict-last
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int col0, ncols;        // column range of this launch (ncols = 0: all)
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)

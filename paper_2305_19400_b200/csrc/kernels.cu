@@ -95,7 +95,7 @@ template <int DIM, int JMAX>
 __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb]
   const Geometry &g = A.g;
-  const int nb = g.nb, nj = g.nj, E = g.E, Es = g.Es;
+  const int nb = g.nb, nj = g.nj, Es = g.Es;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
   const int b = tid - grp * nb;
@@ -216,8 +216,7 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 
 // per-warp Newton scratch (doubles): c_b during the solve, node/band factors in the refresh
 __host__ __device__ __forceinline__ int newton_scratch(const Material &m, int nb) {
-  const int r = 2 * kNGL + m.imax + 1;
-  return nb > r ? nb : r;
+  return 4 * nb + 2 * kNGL + m.imax + 1;  // c | E | M | R | I0 | dI0 | d2I0
 }
 
 __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
@@ -255,6 +254,25 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// L2 eviction-priority policies for bulk copies
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t pol;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 // TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -275,7 +293,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const int nb = NBT > 0 ? NBT : g.nb;
-  const int nj = g.nj, E = g.E, Es = g.Es;
+  const int nj = g.nj, Es = g.Es;
   const int S = A.stages;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
@@ -337,9 +355,17 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     const uint32_t blk = (uint32_t)Es * 8u;
     const uint32_t row = (uint32_t)nb * 8u;
     mbar_expect_tx(&full[st], blk * nblk + (rows_tma ? 2u * row : 0u));
-    bulk_g2s(sp, Is + base, blk, &full[st]);
-    if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
-    if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
+    if (A.l2hint) {
+      // own/x-upwind: keep (read again by the next columns); y-upwind: last use this step
+      const uint64_t keep = l2_policy(A.l2hint == 2 ? 2 : 0), last = l2_policy(1);
+      bulk_g2s_hint(sp, Is + base, blk, &full[st], keep);
+      if (!xghost) bulk_g2s_hint(sp + o_x, Is + base + xoff, blk, &full[st], DIM == 3 ? keep : last);
+      if (DIM == 3 && !yghost) bulk_g2s_hint(sp + o_y, Is + base + yoff, blk, &full[st], last);
+    } else {
+      bulk_g2s(sp, Is + base, blk, &full[st]);
+      if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
+      if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
+    }
     if (rows_tma) {
       bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
       bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
@@ -947,6 +973,72 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // Newton of one cell by one warp (a3 + a4).  sA/sX: GL tables [nb][16] in
 // shared memory, cs: [nb] scratch of this warp.  Dpart is read with
 // ld.global.cg because, when fused into the sweep, other CTAs wrote it.
+// Per-channel band integrals at T on the uniform band grid, balanced over the
+// warp: task k = round*32 + lane -> channel b = k/4, nodes 4(k%4)..4(k%4)+3;
+// the quad of lanes of one channel combine with two xor-shuffles.  Writes
+// I0_b(T), dI0_b/dT and d2I0_b/dT2 to sI0/sD0/sD2; returns W*sum c_b I0_b and
+// W*sum c_b dI0_b/dT in *F (without K0) and *Fp (identical in every lane).
+// Node term g = A/(e^x - 1), x = X/T, r = 1/(e^x - 1):
+//   dg/dT = g (x/T)(1 + r),   d2g/dT2 = g (1 + r)(x/T^2)(x(1 + 2r) - 2).
+__device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, const double *sA, double *scr,
+                                           int lane, double *F, double *Fp) {
+  const int nb = a.nb;
+  const double *cs = scr;
+  double *sE = scr + nb, *sM = sE + kNGL, *sR = sM + kNGL;
+  double *sI0 = sR + a.m.imax + 1, *sD0 = sI0 + nb, *sD2 = sD0 + nb;
+  const double rT = 1.0 / T;
+  const double aa = a.m.Xd * rT;
+  __syncwarp();
+  if (lane < kNGL) {
+    const double x0 = aa * a.m.U[lane];
+    sE[lane] = exp(x0);
+    sM[lane] = expm1(x0);
+  }
+  for (int i = lane; i <= a.m.imax; i += 32) sR[i] = exp(aa * (double)i);
+  __syncwarp();
+  double facc = 0.0, fpacc = 0.0;
+  const int q = lane & 3;
+  const int nrounds = (4 * nb + 31) / 32;
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const int b = (rd * 32 + lane) >> 2;
+    double f = 0.0, fp = 0.0, f2 = 0.0;
+    if (b < nb) {
+      const int ib = a.m.ib[b];
+      const double R = sR[ib];
+      const double bi = (double)ib;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * q + jj;
+        const double em1 = (ib == 0) ? sM[j] : fma(sE[j], R, -1.0);
+        const double rr = rcp_nr(em1);
+        const double t = sA[b * kNGL + j] * rr;
+        const double x = aa * (bi + a.m.U[j]);
+        const double tq = t * (1.0 + rr);
+        f += t;
+        fp = fma(tq, x, fp);
+        f2 = fma(tq * x, fma(x, fma(2.0, rr, 1.0), -2.0), f2);
+      }
+    }
+    f += __shfl_xor_sync(0xffffffffu, f, 1);
+    fp += __shfl_xor_sync(0xffffffffu, fp, 1);
+    f2 += __shfl_xor_sync(0xffffffffu, f2, 1);
+    f += __shfl_xor_sync(0xffffffffu, f, 2);
+    fp += __shfl_xor_sync(0xffffffffu, fp, 2);
+    f2 += __shfl_xor_sync(0xffffffffu, f2, 2);
+    if (q == 0 && b < nb) {
+      const double d = fp * rT;
+      sI0[b] = f;
+      sD0[b] = d;
+      sD2[b] = f2 * rT * rT;
+      facc += cs[b] * f;
+      fpacc += cs[b] * d;
+    }
+  }
+  *F = a.W * warp_sum(facc);
+  *Fp = a.W * warp_sum(fpacc);
+  __syncwarp();
+}
+
 __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
                             double *cs, int lane) {
   const int nb = a.nb;
@@ -972,96 +1064,100 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   Fp0 = warp_sum(Fp0);
   __syncwarp();
   double Tf = Tn;
+  double evaluated_at = -1.0;  // T of the per-channel values held in sI0/sD0
   int status = ERR_NONE;
   if (!isfinite(F0) || !isfinite(K0)) {
     status = ERR_NONFINITE;
   } else if (F0 != 0.0) {
+    if (a.stats && lane == 0) atomicAdd(a.stats + 2, 1ull);
     double T = Tn, lo = kTlo, hi = kThi, F = F0, Fp = Fp0;
     double Tprev = 0.0, Fpprev = 0.0;
-    bool conv = false;
-    for (int it = 0; it <= kNewtonMaxIt; ++it) {
+    bool conv = false, final_eval = false;
+    const bool uni = be && a.m.uniform;
+    // one evaluation call site: the refresh evaluation (when the Taylor step of
+    // reading R-g does not apply) runs as a final pass of this loop
+    for (int it = 0; it <= kNewtonMaxIt + 1; ++it) {
       if (it > 0) {
-        double f = 0.0, fp = 0.0;
-        const double rT = 1.0 / T;
-        if (be && a.m.uniform) {
-          // geometric recurrence over the band index i (17 exp per evaluation)
-          const double aa = a.m.Xd * rT;
-          const double r = exp(aa);
-          const double r2 = r * r;
-          const double x0 = aa * a.m.U[jn];
-          double e = exp(x0);
-          if (par) e *= r;
-          for (int i = par; i <= a.m.imax; i += 2) {
-            const double em1 = (i == 0) ? expm1(x0) : e - 1.0;
-            const double rr = rcp_nr(em1);
-            const double xi = fma((double)i, aa, x0);
-            const double dfac = xi * (1.0 + rr);
-            for (int q = 0; q < 4; ++q) {
-              const int b = sI[i * 4 + q];
-              if (b < 0) break;
-              const double t = cs[b] * (sA[b * kNGL + jn] * rr);
-              f += t;
-              fp += t * dfac;
-            }
-            e *= r2;
-          }
-          fp *= rT;
-        } else if (be) {
-          for (int b = par; b < nb; b += 2) {
-            const double x = sX[b * kNGL + jn] * rT;
-            const double em1 = expm1(x);
-            const double r = 1.0 / em1;
-            const double t = cs[b] * (sA[b * kNGL + jn] * r);
-            f += t;
-            fp += t * x * (1.0 + r);
-          }
-          fp *= rT;
+        if (uni) {
+          double fw, fpw;
+          eval_channels(a, T, sA, cs, lane, &fw, &fpw);
+          F = fw + K0;
+          Fp = fpw;
+          evaluated_at = T;
         } else {
-          for (int b = lane; b < nb; b += 32) {
-            f += cs[b] * (a.m.I_ref[b] + a.m.slope[b] * (T - a.m.T_ref));
-            fp += cs[b] * a.m.slope[b];
+          double f = 0.0, fp = 0.0;
+          const double rT = 1.0 / T;
+          if (be) {
+            for (int b = par; b < nb; b += 2) {
+              const double x = sX[b * kNGL + jn] * rT;
+              const double em1 = expm1(x);
+              const double r = 1.0 / em1;
+              const double t = cs[b] * (sA[b * kNGL + jn] * r);
+              f += t;
+              fp += t * x * (1.0 + r);
+            }
+            fp *= rT;
+          } else {
+            for (int b = lane; b < nb; b += 32) {
+              f += cs[b] * (a.m.I_ref[b] + a.m.slope[b] * (T - a.m.T_ref));
+              fp += cs[b] * a.m.slope[b];
+            }
           }
+          F = a.W * warp_sum(f) + K0;
+          Fp = a.W * warp_sum(fp);
         }
-        F = a.W * warp_sum(f) + K0;
-        Fp = a.W * warp_sum(fp);
       }
+      if (a.stats && lane == 0 && it > 0) atomicAdd(a.stats + (final_eval ? 1 : 0), 1ull);
+      if (final_eval) break;
       if (!isfinite(F) || !isfinite(Fp)) {
         status = ERR_NONFINITE;
         break;
       }
+      bool done = false;
       if (F == 0.0) {
         Tf = T;
-        conv = true;
-        break;
-      }
-      if (it == kNewtonMaxIt) break;
-      if (F < 0.0)
-        lo = T;
-      else
-        hi = T;
-      const double stp = F / Fp;
-      double Tn1 = T - stp;
-      if (fabs(stp) <= kNewtonRtol * T) {  // reading R-a: step test before the bracket test
-        Tf = Tn1;
-        conv = true;
-        break;
-      }
-      if (it > 0 && a.predict && Tn1 > lo && Tn1 < hi) {
-        // reading R-f: quadratic convergence -- the next step would be about
-        // |F''/(2F')| stp^2 (F'' from the secant of F'); accept T - stp when that
-        // is 1000x below the tolerance, saving one band-integral evaluation.
-        const double F2 = (Fp - Fpprev) / (T - Tprev);
-        const double pred = fabs(F2 / (2.0 * Fp)) * stp * stp;
-        if (pred <= 1e-3 * kNewtonRtol * T) {
+        done = true;
+      } else {
+        if (it >= kNewtonMaxIt) break;
+        if (F < 0.0)
+          lo = T;
+        else
+          hi = T;
+        const double stp = F / Fp;
+        double Tn1 = T - stp;
+        if (fabs(stp) <= kNewtonRtol * T) {  // reading R-a: step test before the bracket test
           Tf = Tn1;
-          conv = true;
-          break;
+          done = true;
+        } else if (it > 0 && a.predict && Tn1 > lo && Tn1 < hi) {
+          // reading R-f: quadratic convergence -- the next step would be about
+          // |F''/(2F')| stp^2 (F'' from the secant of F'); accept T - stp when
+          // that is 1000x below the tolerance, saving one evaluation.
+          const double F2 = (Fp - Fpprev) / (T - Tprev);
+          const double pred = fabs(F2 / (2.0 * Fp)) * stp * stp;
+          if (pred <= 1e-3 * kNewtonRtol * T) {
+            Tf = Tn1;
+            done = true;
+          }
+        }
+        if (!done) {
+          Tprev = T;
+          Fpprev = Fp;
+          if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
+          T = Tn1;
         }
       }
-      Tprev = T;
-      Fpprev = Fp;
-      if (!(Tn1 > lo && Tn1 < hi)) Tn1 = 0.5 * (lo + hi);
-      T = Tn1;
+      if (done) {
+        conv = true;
+        if (uni && Tf != Tn) {
+          const double rel = fabs(Tf - evaluated_at) / Tf;
+          if (!(evaluated_at > 0.0 && 10.0 * rel * rel * rel <= 1e-16)) {
+            final_eval = true;  // re-evaluate at T^{n+1} for the refresh
+            T = Tf;
+            continue;
+          }
+        }
+        break;
+      }
     }
     if (!conv && status == ERR_NONE) status = ERR_NEWTON;
   }
@@ -1078,37 +1174,15 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     // refresh I0c = I0(T^{n+1}) and its derivative
     if (lane == 0) a.T[c] = Tf;
     if (be && a.m.uniform) {
-      // per-channel layout: lane = channel, sequential over the 16 nodes, with
-      // the node factors exp(a u_j), expm1(a u_j) and the band factors exp(a i)
-      // computed once per cell by the warp and shared through this warp's
-      // scratch (cs is free again: c_b is no longer needed).
-      const double rT = 1.0 / Tf;
-      const double aa = a.m.Xd * rT;
-      double *sE = cs;             // [16] exp(a u_j)
-      double *sM = cs + kNGL;      // [16] expm1(a u_j)
-      double *sR = cs + 2 * kNGL;  // [imax+1] exp(a i)
-      __syncwarp();
-      if (lane < kNGL) {
-        const double x0 = aa * a.m.U[lane];
-        sE[lane] = exp(x0);
-        sM[lane] = expm1(x0);
-      }
-      for (int i = lane; i <= a.m.imax; i += 32) sR[i] = exp(aa * (double)i);
-      __syncwarp();
+      // refresh from the per-channel values of the last evaluation (at Tf itself
+      // after a final pass, else the second-order Taylor step of reading R-g)
+      double *sI0 = cs + nb + 2 * kNGL + a.m.imax + 1;
+      double *sD0 = sI0 + nb, *sD2 = sD0 + nb;
+      const double dT = Tf - evaluated_at;
       for (int b = lane; b < nb; b += 32) {
-        const int ib = a.m.ib[b];
-        const double R = sR[ib];
-        double f = 0.0, fp = 0.0;
-#pragma unroll 4
-        for (int j = 0; j < kNGL; ++j) {
-          const double em1 = (ib == 0) ? sM[j] : fma(sE[j], R, -1.0);
-          const double rr = rcp_nr(em1);
-          const double t = sA[b * kNGL + j] * rr;
-          f += t;
-          fp = fma(t * fma((double)ib, aa, aa * a.m.U[j]), 1.0 + rr, fp);
-        }
-        a.I0c[c * nb + b] = f;
-        a.dI0c[c * nb + b] = fp * rT;
+        const double i0 = sI0[b], d0 = sD0[b], d2 = sD2[b];
+        a.I0c[c * nb + b] = dT != 0.0 ? fma(fma(0.5 * d2, dT, d0), dT, i0) : i0;
+        a.dI0c[c * nb + b] = dT != 0.0 ? fma(d2, dT, d0) : d0;
       }
     } else if (be) {
       const double rT = 1.0 / Tf;

@@ -482,3 +482,17 @@ def test_demo_workload_full_size(Solver, start, nsteps):
     p = bi.config_demo()
     (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, nsteps, start=start)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_parity_nonuniform_band_grid(Solver):
+    """Channels whose edges are not on one uniform grid take the direct expm1
+    Newton path (reading R-d); also a Debye (c2 = 0) table."""
+    si = bi.subset_bands(bi.silicon_bands(29), [0, 9, 20, 31])
+    si.w_hi = si.w_hi * (1.0 + 1e-3 * np.arange(1, si.nb + 1))  # break the uniform grid
+    p = bi.small_3d(6, 5, 4, bands=si)
+    (rel, dT), _ = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    deb = bi.debye_bands(6000.0, 2 * math.pi / 5.43e-10, 5)
+    p = bi.small_3d(5, 4, 3, bands=deb, dt=1e-12)
+    (rel, dT), _ = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
