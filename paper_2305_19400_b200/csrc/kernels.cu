@@ -215,6 +215,11 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 }
 
 // per-warp Newton scratch (doubles): c_b during the solve, node/band factors in the refresh
+// node-major GL tables in shared memory: entry (b, j) at j*R + b, row stride
+// R = nb rounded up to 2 (mod 4) so that the 4 node groups of a warp load
+// fall on disjoint bank sets
+__host__ __device__ __forceinline__ int gl_stride(int nb) { return nb + ((6 - nb % 4) % 4); }
+
 __host__ __device__ __forceinline__ int newton_scratch(const Material &m, int nb) {
   return 4 * nb + 2 * kNGL + m.imax + 1;  // c | E | M | R | I0 | dI0 | d2I0
 }
@@ -490,16 +495,18 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     if (s_last) {
       __threadfence();
       const NewtonArgs &na = A.nw;
+      const int R = gl_stride(nb);
       double *sA = stage0;  // stage ring is free: every stage was consumed
-      double *sX = sA + nb * kNGL;
+      double *sX = sA + R * kNGL;
       const int nwarp = blockDim.x >> 5;
       const int wsd = newton_scratch(na.m, nb);
-      double *cs = sX + nb * kNGL + (tid >> 5) * wsd;
-      int *sI = reinterpret_cast<int *>(sX + nb * kNGL + nwarp * wsd);
+      double *cs = sX + R * kNGL + (tid >> 5) * wsd;
+      int *sI = reinterpret_cast<int *>(sX + R * kNGL + nwarp * wsd);
       if (na.m.mode != 0) {
         for (int q = tid; q < nb * kNGL; q += blockDim.x) {
-          sA[q] = na.m.A[q];
-          sX[q] = na.m.X[q];
+          const int bq = q / kNGL, jq = q - bq * kNGL;
+          sA[jq * R + bq] = na.m.A[q];
+          sX[jq * R + bq] = na.m.X[q];
         }
         for (int q = tid; q < 4 * (na.m.imax + 1); q += blockDim.x) sI[q] = na.m.ichan[q];
       }
@@ -791,7 +798,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
     const int tthreads0 = (threads + 31) / 32 * 32;
     if (a.fuse_newton) {  // the Newton tail reuses the stage ring for its tables
-      const size_t need = fixed + (2 * (size_t)g.nb * kNGL + (size_t)(tthreads0 / 32) * newton_scratch(a.nw.m, g.nb)) * sizeof(double) +
+      const size_t need = fixed + (2 * (size_t)gl_stride(g.nb) * kNGL + (size_t)(tthreads0 / 32) * newton_scratch(a.nw.m, g.nb)) * sizeof(double) +
                           4 * (size_t)(a.nw.m.imax + 1) * sizeof(int);
       smem = std::max(smem, need);
       *fused = 1;
@@ -997,34 +1004,38 @@ __device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, con
   for (int i = lane; i <= a.m.imax; i += 32) sR[i] = exp(aa * (double)i);
   __syncwarp();
   double facc = 0.0, fpacc = 0.0;
-  const int q = lane & 3;
-  const int nrounds = (4 * nb + 31) / 32;
+  const int q = lane >> 3;            // node group: nodes 4q .. 4q+3
+  const int R = gl_stride(nb);
+  double u[4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) u[jj] = a.m.U[4 * q + jj];
+  const int nrounds = (nb + 7) / 8;
   for (int rd = 0; rd < nrounds; ++rd) {
-    const int b = (rd * 32 + lane) >> 2;
+    const int b = rd * 8 + (lane & 7);
     double f = 0.0, fp = 0.0, f2 = 0.0;
     if (b < nb) {
       const int ib = a.m.ib[b];
-      const double R = sR[ib];
+      const double Rb = sR[ib];
       const double bi = (double)ib;
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int j = 4 * q + jj;
-        const double em1 = (ib == 0) ? sM[j] : fma(sE[j], R, -1.0);
+        const double em1 = (ib == 0) ? sM[j] : fma(sE[j], Rb, -1.0);
         const double rr = rcp_nr(em1);
-        const double t = sA[b * kNGL + j] * rr;
-        const double x = aa * (bi + a.m.U[j]);
+        const double t = sA[j * R + b] * rr;
+        const double x = aa * (bi + u[jj]);
         const double tq = t * (1.0 + rr);
         f += t;
         fp = fma(tq, x, fp);
         f2 = fma(tq * x, fma(x, fma(2.0, rr, 1.0), -2.0), f2);
       }
     }
-    f += __shfl_xor_sync(0xffffffffu, f, 1);
-    fp += __shfl_xor_sync(0xffffffffu, fp, 1);
-    f2 += __shfl_xor_sync(0xffffffffu, f2, 1);
-    f += __shfl_xor_sync(0xffffffffu, f, 2);
-    fp += __shfl_xor_sync(0xffffffffu, fp, 2);
-    f2 += __shfl_xor_sync(0xffffffffu, f2, 2);
+    f += __shfl_xor_sync(0xffffffffu, f, 8);
+    fp += __shfl_xor_sync(0xffffffffu, fp, 8);
+    f2 += __shfl_xor_sync(0xffffffffu, f2, 8);
+    f += __shfl_xor_sync(0xffffffffu, f, 16);
+    fp += __shfl_xor_sync(0xffffffffu, fp, 16);
+    f2 += __shfl_xor_sync(0xffffffffu, f2, 16);
     if (q == 0 && b < nb) {
       const double d = fp * rT;
       sI0[b] = f;
@@ -1089,10 +1100,10 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
           const double rT = 1.0 / T;
           if (be) {
             for (int b = par; b < nb; b += 2) {
-              const double x = sX[b * kNGL + jn] * rT;
+              const double x = sX[jn * gl_stride(nb) + b] * rT;
               const double em1 = expm1(x);
               const double r = 1.0 / em1;
-              const double t = cs[b] * (sA[b * kNGL + jn] * r);
+              const double t = cs[b] * (sA[jn * gl_stride(nb) + b] * r);
               f += t;
               fp += t * x * (1.0 + r);
             }
@@ -1190,10 +1201,10 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
         const int b = b0 + par;
         double f = 0.0, fp = 0.0;
         if (b < nb) {
-          const double x = sX[b * kNGL + jn] * rT;
+          const double x = sX[jn * gl_stride(nb) + b] * rT;
           const double em1 = expm1(x);
           const double r = 1.0 / em1;
-          f = sA[b * kNGL + jn] * r;
+          f = sA[jn * gl_stride(nb) + b] * r;
           fp = f * x * (1.0 + r);
         }
 #pragma unroll
@@ -1226,16 +1237,18 @@ template <int MINB>
 __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const NewtonArgs a) {
   extern __shared__ double nsh[];
   const int nb = a.nb;
+  const int R = gl_stride(nb);
   double *sA = nsh;
-  double *sX = sA + nb * kNGL;
+  double *sX = sA + R * kNGL;
   const int warp = threadIdx.x >> 5;
   const int wsd = newton_scratch(a.m, nb);
-  double *cs = sX + nb * kNGL + warp * wsd;
-  int *sI = reinterpret_cast<int *>(sX + nb * kNGL + kNewtonWarps * wsd);
+  double *cs = sX + R * kNGL + warp * wsd;
+  int *sI = reinterpret_cast<int *>(sX + R * kNGL + kNewtonWarps * wsd);
   if (a.m.mode != 0) {
-    for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
-      sA[i] = a.m.A[i];
-      sX[i] = a.m.X[i];
+    for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {  // node-major transpose
+      const int b = i / kNGL, j = i - b * kNGL;
+      sA[j * R + b] = a.m.A[i];
+      sX[j * R + b] = a.m.X[i];
     }
     for (int i = threadIdx.x; i < 4 * (a.m.imax + 1); i += blockDim.x) sI[i] = a.m.ichan[i];
   }
@@ -1254,7 +1267,7 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   if (a.ncells == 0) return cudaSuccess;
   const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
-  const size_t smem = (2 * (size_t)a.nb * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
+  const size_t smem = (2 * (size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
   const int minb = a.minb > 0 ? a.minb : BTE_NEWTON_MINB;
 #define BTE_NL(M)                                                                                   \
