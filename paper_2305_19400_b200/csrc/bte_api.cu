@@ -972,6 +972,8 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
 // context: each sender copies its owned boundary planes straight into the
 // receiver's halo planes (the receives of the plan are implied), after both
 // sides' previous work, and the receivers wait for those copies.
+// Priming exchange of a local group on the current buffers (before the first
+// step of a bte_group_step call): senders copy owned planes into halos.
 static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
   bte_ctx *ctx = ctxs[0];
   if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch

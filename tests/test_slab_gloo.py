@@ -60,3 +60,18 @@ def test_plan_invariants(P):
             up = not (m["octant"] & 1)
             if m["send"]:
                 assert m["plane"] == (q["m0"] + q["n_local"] - 1 if up else q["m0"])
+
+
+def test_plan_errors_and_odd_blocks():
+    from paper_2305_19400_b200 import BteError
+    p = bi.config3(n=8)
+    p.mesh = bi.Mesh(3, 5, 4, 3, 1e-6, 1e-6, 1e-6)
+    with pytest.raises(BteError):
+        plan_slab(p.mesh, p.dirs, p.bands.nb, 4, 3)  # more ranks than planes: rank 3 owns none
+    with pytest.raises(BteError):
+        plan_slab(p.mesh, p.dirs, p.bands.nb, 2, 2)  # rank out of range
+    # odd (cell, octant) blocks: messages carry the even device stride
+    d = bi.directions_inplane(12)  # 3 directions per quadrant
+    m2 = bi.Mesh(2, 5, 6, 1, 1e-6, 1e-6, 1.0)
+    q = plan_slab(m2, d, 5, 2, 0)  # 3 x 5 = 15 doubles -> stride 16
+    assert q["axis"] == 1 and all(msg["count"] == 5 * 16 for msg in q["msgs"])
