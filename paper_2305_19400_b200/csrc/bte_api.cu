@@ -72,7 +72,8 @@ struct bte_ctx {
   int newton_minb = 0;
   int tx_override = 0;
   unsigned long long *d_stats = nullptr;  // env BTE_NEWTON_STATS=1: Newton counters printed by bte_step
-  int l2hint = 0;  // env BTE_L2HINT  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int l2hint = 0;  // env BTE_L2HINT
+  int persist = 0;  // env BTE_PERSIST  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;

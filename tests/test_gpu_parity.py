@@ -496,3 +496,18 @@ def test_parity_nonuniform_band_grid(Solver):
     p = bi.small_3d(5, 4, 3, bands=deb, dt=1e-12)
     (rel, dT), _ = _run_both(Solver, p, 6)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+@pytest.mark.parametrize("variant", ["BTE_FUSE", "BTE_CHUNKS", "BTE_SWEEP_PLAIN", "BTE_TX"])
+def test_parity_kernel_variants(Solver, variant, monkeypatch):
+    """The A/B kernel variants (sweep-tail Newton, chunked two-stream pipeline,
+    direct-load sweep, multi-column TMA sweep) reach the same results."""
+    if variant == "BTE_SWEEP_PLAIN":
+        monkeypatch.setenv("BTE_SWEEP", "plain")
+    else:
+        monkeypatch.setenv(variant, {"BTE_CHUNKS": "3", "BTE_TX": "4"}.get(variant, "1"))
+    for p, n in ((bi.config2(n=16), 8), (bi.config3(n=8), 4)):
+        if p.mesh.dim == 3:
+            p.mesh = bi.Mesh(3, 9, 7, 6, 1e-6, 1e-6, 1e-6)
+        (rel, dT), _ = _run_both(Solver, p, n)
+        assert rel <= REL_I and dT <= ABS_T, (variant, p.name, rel, dT)
