@@ -325,7 +325,8 @@ def run_b200(args):
                 "device_ms_per_step": {"sweep": tim["sweep_ms"] / args.steps, "newton": tim["newton_ms"] / args.steps,
                                        "boundary": tim["boundary_ms"] / args.steps,
                                        "halo": tim["halo_ms"] / args.steps},
-                "note": "Newton runs on a second stream, overlapped with other chunks' sweeps"}
+                "note": ("sweep and Newton serialised on one stream" if launches_per_step == 1
+                         else "Newton of chunk k on a second stream, overlapped with other chunks' sweeps")}
 
     # e2e through the public API with host buffers (pinned), copies inside the
     # timed region: the job's input state (I, T) goes host->device, K steps run,
