@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbte.so")
+LIB_PATH = os.environ.get("BTE_LIB") or os.path.join(_HERE, "libbte.so")  # BTE_LIB: A/B builds
 
 BTE_OK = 0
 STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE_ENCCL",

@@ -326,6 +326,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
       slot_of[o] = nslot++;
     }
   }
+  for (int o = 0; o < 8; ++o) ctx->g.oct_slot[o] = slot_of[o];
   ctx->dmap.resize(ctx->nd);
   ctx->canon_d.resize(ctx->nd);
   for (int d = 0; d < ctx->nd; ++d) {
@@ -773,6 +774,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.nslot = ctx->g.nslot;
   a.nb = ctx->nb;
   for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
+  for (int o = 0; o < 8; ++o) a.oct_slot[o] = ctx->g.oct_slot[o];
   a.W = ctx->W;
   a.ncells = ctx->ncells_local;
   a.cell0_global = ctx->g.m0 * ctx->g.ncross;

@@ -62,6 +62,7 @@ struct Geometry {
   int nslot, nj, nb, E;
   int Es;                 // (cell, octant) block stride in doubles: E rounded up to even (16-B TMA)
   int slot_oct[kMaxSlots];
+  int oct_slot[8];        // inverse: slot of octant o, or -1
   int has_lo_wall, has_hi_wall;  // march-axis walls exist on this rank
   // per-(slot, j) coefficient table [nslot*nj][4]: dt|s_x|/dx, dt|s_y|/dy, dt|s_z|/dz, w
   const double *coef;
@@ -80,6 +81,7 @@ struct NewtonArgs {
   double *T, *I0c, *dI0c, *beta_next;
   int nslot, nb;
   int slot_oct[kMaxSlots];
+  int oct_slot[8];        // slot of octant o, or -1 (register-indexed octant tree)
   double W;
   int64_t ncells, cell0_global;
   unsigned long long *err;

@@ -903,15 +903,17 @@ __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int re
   // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
   const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
-    double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int sl = 0; sl < g.nslot; ++sl) {
-      const int o = g.slot_oct[sl];
+    double q[8];  // compile-time octant indices: registers, not local memory
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const int sl = g.oct_slot[o];
       const bool out = hi ? !(o & bit) : (o & bit);
-      if (!out) continue;
-      const double *ws = g.ws + (int64_t)axis * g.nslot * g.nj + (int64_t)sl * g.nj;
-      const double *Ip = I + (int64_t)sl * g.slot_stride + cell_base + b;
       double acc = 0.0;
-      for (int j = 0; j < g.nj; ++j) acc += ws[j] * Ip[(int64_t)j * g.nb];
+      if (sl >= 0 && out) {
+        const double *ws = g.ws + (int64_t)axis * g.nslot * g.nj + (int64_t)sl * g.nj;
+        const double *Ip = I + (int64_t)sl * g.slot_stride + cell_base + b;
+        for (int j = 0; j < g.nj; ++j) acc += ws[j] * Ip[(int64_t)j * g.nb];
+      }
       q[o] = acc;
     }
     const double num = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
@@ -1050,8 +1052,12 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   const double Tn = a.T[c];
   double F0 = 0.0, K0 = 0.0, Fp0 = 0.0;
   for (int b = lane; b < nb; b += 32) {
-    double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int sl = 0; sl < a.nslot; ++sl) q[a.slot_oct[sl]] = __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b);
+    double q[8];  // octant-indexed with compile-time indices: stays in registers
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const int sl = a.oct_slot[o];
+      q[o] = sl >= 0 ? __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b) : 0.0;
+    }
     const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     const double bn = beta_of_T(a.m.bcoef, b, Tn);
     const double cb = bn * a.m.rv[b];
@@ -1446,8 +1452,9 @@ __global__ void k_octant_tree(const double *__restrict__ Dpart, int nslot, Geome
   if (i >= nc * g.nb) return;
   const int64_t c = i / g.nb;
   const int b = (int)(i - c * g.nb);
-  double q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int sl = 0; sl < nslot; ++sl) q[g.slot_oct[sl]] = Dpart[(c * nslot + sl) * g.nb + b];
+  double q[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) q[o] = g.oct_slot[o] >= 0 ? Dpart[(c * nslot + g.oct_slot[o]) * g.nb + b] : 0.0;
   D[i] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
 }
 
