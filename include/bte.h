@@ -141,6 +141,23 @@ typedef struct {
 BTE_API bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                       const bte_run *run, bte_ctx **out);
 
+/* Create a band-partitioned context.
+ * Arguments as bte_create with the FULL channel table; run->rank and
+ * run->nranks are this context's band part and the number of parts.  Every
+ * part holds the whole mesh (no halo planes) and sweeps only its channels
+ * [b0, b1) (bte_plan_band).  Per step the parts exchange ONE scalar per cell,
+ * S_r(c) = sum_{b in part r} c_b D_{c,b} (c_b = beta_b(T^n)/v_b, Eq. 8's
+ * weights): ncclAllGather of [nranks][ncells] when run->nccl_id is set, device
+ * copies inside bte_group_step when it is NULL ("local" mode, as for slabs).
+ * Every part then sums the gathered partials in rank order and runs the same
+ * temperature Newton over all channels, so T is bitwise identical on all
+ * parts.  State: I holds this part's channels, canonical [cell][d][b - b0]
+ * (nd*(b1-b0) doubles per cell); T is the whole field; bte_set_state needs
+ * T; bte_get_energy sums this part's channels only; bte_debug_substep
+ * which = 2/3 return all nb_total channels.  Errors as bte_create. */
+BTE_API bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                                   const bte_run *run, bte_ctx **out);
+
 /* Boundary condition of one wall region (0..5 = -x,+x,-y,+y,-z,+z).
  * T_wall: host array with one temperature per boundary face of that wall,
  * row-major over the two in-plane axes in (x,y,z) order ((y,z) for x-walls,
@@ -241,11 +258,21 @@ typedef struct {
 BTE_API bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int nb, int nranks, int rank,
                                  bte_slab_plan *out);
 
-/* Sizes of this rank's slab and the layout. */
+/* Band (channel) partition -- the paper's own multi-process decomposition
+ * ("equation"/band partitioning): part `part` of
+ * `nparts` owns the contiguous channels [*b0, *b1) of every cell,
+ * b0 = floor(part*nb/nparts).  Host-only.  Errors: BTE_EINVAL unless
+ * 1 <= nparts <= nb and 0 <= part < nparts. */
+BTE_API bte_status bte_plan_band(int nb, int nparts, int part, int *b0, int *b1);
+
+/* Sizes of this rank's slab and the layout.  nb is the channel count this
+ * context sweeps (its band [b0, b1) of nb_total for a band context, else
+ * b0 = 0 and nb = nb_total). */
 typedef struct {
   int64_t ncells_local, ncells_global, z0, nz_local; /* slab along the slowest axis */
   int nd, nb, n_octants, nj;                         /* nj = directions per octant  */
   int64_t bytes_state;                               /* device bytes held by ctx    */
+  int b0, b1, nb_total, band;                        /* channel band; band = 1 for bte_create_band */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE = 0, 1, 2
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_create", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -82,7 +82,8 @@ class SlabPlan(C.Structure):
 class Info(C.Structure):
     _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
-                ("nj", C.c_int), ("bytes_state", C.c_int64)]
+                ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
+                ("nb_total", C.c_int), ("band", C.c_int)]
 
 
 _lib = None
@@ -100,6 +101,9 @@ def load_library(path: str = LIB_PATH):
     dp = C.c_void_p
     lib.bte_create.argtypes = [C.POINTER(Mesh), C.POINTER(Dirs), C.POINTER(Bands), C.POINTER(Run),
                                C.POINTER(C.c_void_p)]
+    if hasattr(lib, "bte_create_band"):  # (older A/B builds via BTE_LIB lack the band entry points)
+        lib.bte_create_band.argtypes = lib.bte_create.argtypes
+        lib.bte_plan_band.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
     lib.bte_set_state.argtypes = [P, dp, dp]
     lib.bte_init_random.argtypes = [P, C.c_uint64, dp, C.c_double, C.c_double, C.c_double]
@@ -119,7 +123,7 @@ def load_library(path: str = LIB_PATH):
     lib.bte_destroy.restype = None
     lib.bte_version.restype = C.c_char_p
     for name in EXPORTS:
-        if name not in ("bte_last_error", "bte_destroy", "bte_version"):
+        if name not in ("bte_last_error", "bte_destroy", "bte_version") and hasattr(lib, name):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -134,11 +138,15 @@ def _p(a: Optional[np.ndarray]):
 
 
 class Solver:
-    """One BTE context on one GPU (one slab of the mesh when nranks > 1)."""
+    """One BTE context on one GPU: the whole problem, one slab of the mesh
+    (decomp="slab", nranks > 1) or one band of channels (decomp="band",
+    bte_create_band: rank = band part, nranks = parts)."""
 
     def __init__(self, mesh, dirs, bands, dt: float, T_init: float, device: int = 0, stream=None,
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 torch_alloc: bool = True):
+                 torch_alloc: bool = True, decomp: str = "slab"):
+        if decomp not in ("slab", "band"):
+            raise ValueError("decomp must be 'slab' or 'band'")
         import torch  # plumbing: device memory and streams
         if not torch.cuda.is_available():
             raise RuntimeError("libbte needs a CUDA device (no CPU fallback)")
@@ -185,7 +193,8 @@ class Solver:
                   int(nranks), C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
                   self._alloc_cb, self._free_cb, None)
         h = C.c_void_p()
-        st = self._lib.bte_create(C.byref(m), C.byref(d), C.byref(b), C.byref(run), C.byref(h))
+        create = self._lib.bte_create_band if decomp == "band" else self._lib.bte_create
+        st = create(C.byref(m), C.byref(d), C.byref(b), C.byref(run), C.byref(h))
         self._h = h
         if st != BTE_OK:
             msg = self._err()
@@ -200,6 +209,10 @@ class Solver:
         self.nd, self.nb = int(info.nd), int(info.nb)
         self.n_octants, self.nj = int(info.n_octants), int(info.nj)
         self.bytes_state = int(info.bytes_state)
+        self.b0, self.b1, self.nb_total = int(info.b0), int(info.b1), int(info.nb_total)
+        self.band = bool(info.band)
+        if self.nb_total == 0:  # older A/B build without the band fields
+            self.b0, self.b1, self.nb_total = 0, self.nb, self.nb
 
     # ---------------------------------------------------------------- helpers
     @classmethod
@@ -244,8 +257,9 @@ class Solver:
 
     @staticmethod
     def group_step(solvers, n: int = 1):
-        """Advance an in-process slab group (contexts built with nranks = len(solvers),
-        rank = index, no nccl_id) by n steps; halos move by device-to-device copies."""
+        """Advance an in-process slab or band group (contexts built with nranks =
+        len(solvers), rank = index, no nccl_id) by n steps; halos (slab) or the
+        per-cell band partials (band) move by device-to-device copies."""
         lib = load_library()
         arr = (C.c_void_p * len(solvers))(*[sv._h.value for sv in solvers])
         st = lib.bte_group_step(arr, len(solvers), int(n))
@@ -271,8 +285,8 @@ class Solver:
         return e.value
 
     def debug_substep(self, which: int) -> np.ndarray:
-        shape = {0: (self.ncells, self.nd, self.nb), 1: (self.ncells, self.nb), 2: (self.ncells, self.nb),
-                 3: (self.ncells, self.nb)}[which]
+        shape = {0: (self.ncells, self.nd, self.nb), 1: (self.ncells, self.nb), 2: (self.ncells, self.nb_total),
+                 3: (self.ncells, self.nb_total)}[which]
         out = np.empty(shape)
         self._check(self._lib.bte_debug_substep(self._h, which, out.ctypes.data, out.size))
         return out
@@ -316,6 +330,16 @@ def plan_slab(mesh, dirs, nb: int, nranks: int, rank: int) -> dict:
         raise BteError(st, "bte_plan_slab")
     msgs = [{f: getattr(out.msg[k], f) for f, _ in Msg._fields_} for k in range(out.n_msgs)]
     return {"axis": out.axis, "m0": out.m0, "n_local": out.n_local, "msgs": msgs}
+
+
+def plan_band(nb: int, nparts: int, part: int) -> tuple:
+    """The library's band partition: channels [b0, b1) of part `part` (host-only)."""
+    lib = load_library()
+    b0, b1 = C.c_int(), C.c_int()
+    st = lib.bte_plan_band(int(nb), int(nparts), int(part), C.byref(b0), C.byref(b1))
+    if st != BTE_OK:
+        raise BteError(st, "bte_plan_band")
+    return b0.value, b1.value
 
 
 def nccl_unique_id() -> bytes:

@@ -47,6 +47,13 @@ struct bte_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
+  // band partition (bte_create_band): this context sweeps channels [b0, b0+nb)
+  // of nbT; slab_ranks = nranks for slab contexts, 1 for band contexts
+  int band = 0, b0 = 0, nbT = 0, slab_ranks = 1;
+  double *Sall = nullptr;  // [nranks][ncells] gathered partials (band)
+  // the sweep's I0c / beta rows [cell][nb]: aliases of I0c / beta, or (band)
+  // copies of this part's channel slice kept by the Newton
+  double *I0s = nullptr, *betas = nullptr;
   void *(*alloc)(size_t, void *) = nullptr;
   void (*dealloc)(void *, void *) = nullptr;
   void *alloc_ctx = nullptr;
@@ -60,7 +67,8 @@ struct bte_ctx {
   double Tmax = 0;
   // device
   Geometry g{};
-  Material m{};
+  Material m{};   // the channels this context sweeps (a view into mF for band contexts)
+  Material mF{};  // all channels (Newton, refresh)
   double *I[2] = {nullptr, nullptr};
   int cur = 0;
   double *I0c = nullptr, *dI0c = nullptr, *beta = nullptr, *T = nullptr, *Dpart = nullptr;
@@ -155,7 +163,7 @@ static bte_status check_dt(bte_ctx *ctx) {
   const int na = ctx->mesh.dim == 3 ? 3 : 2;
   const double D[3] = {ctx->mesh.dx, ctx->mesh.dy, ctx->mesh.dz};
   double worst = 1e300;
-  for (int b = 0; b < ctx->nb; ++b) {
+  for (int b = ctx->b0; b < ctx->b0 + ctx->nb; ++b) {  // this context's channels
     const double be = host_beta(ctx, b, ctx->Tmax);
     for (int d = 0; d < ctx->nd; ++d) {
       double k = 0;
@@ -167,6 +175,20 @@ static bte_status check_dt(bte_ctx *ctx) {
     return fail(ctx, BTE_EUNSTABLE,
                 "dt = %g violates the positivity bound at T = %g K (margin %g < 0)", ctx->dt,
                 ctx->Tmax, worst);
+  return BTE_OK;
+}
+
+// I0c, dI0c, beta at the current T (all channels), plus the band slice the sweep reads
+static bte_status refresh(bte_ctx *ctx) {
+  const int64_t ncl = ctx->ncells_local;
+  CU(launch_refresh(ctx->mF, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
+  if (ctx->band && ncl > 0) {
+    const size_t w = (size_t)ctx->nb * sizeof(double), pitch = (size_t)ctx->nbT * sizeof(double);
+    CU(cudaMemcpy2DAsync(ctx->I0s, w, ctx->I0c + ctx->b0, pitch, w, (size_t)ncl, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+    CU(cudaMemcpy2DAsync(ctx->betas, w, ctx->beta + ctx->b0, pitch, w, (size_t)ncl, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  }
   return BTE_OK;
 }
 
@@ -246,8 +268,28 @@ bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int nb, int
   return BTE_OK;
 }
 
+bte_status bte_plan_band(int nb, int nparts, int part, int *b0, int *b1) {
+  if (!b0 || !b1 || nparts < 1 || nparts > nb || part < 0 || part >= nparts) return BTE_EINVAL;
+  *b0 = (int)((int64_t)part * nb / nparts);
+  *b1 = (int)((int64_t)(part + 1) * nb / nparts);
+  return BTE_OK;
+}
+
+static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                              const bte_run *run, bool band, bte_ctx **out);
+
 bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands, const bte_run *run,
                       bte_ctx **out) {
+  return create_impl(mesh, dirs, bands, run, false, out);
+}
+
+bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                           const bte_run *run, bte_ctx **out) {
+  return create_impl(mesh, dirs, bands, run, true, out);
+}
+
+static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                              const bte_run *run, bool band, bte_ctx **out) {
   if (!out) return BTE_EINVAL;
   *out = nullptr;
   bte_ctx *ctx = new bte_ctx();
@@ -270,7 +312,18 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   if (run->nranks < 1 || run->rank < 0 || run->rank >= run->nranks)
     return bail(fail(ctx, BTE_EINVAL, "bad rank/nranks"));
   ctx->nd = dirs->nd;
+  ctx->nbT = bands->nb;
   ctx->nb = bands->nb;
+  ctx->band = band ? 1 : 0;
+  ctx->slab_ranks = band ? 1 : run->nranks;
+  if (band) {
+    int b1 = 0;
+    if (bte_plan_band(bands->nb, run->nranks, run->rank, &ctx->b0, &b1) != BTE_OK)
+      return bail(fail(ctx, BTE_EINVAL, "band partition: need 1 <= nranks (%d) <= channels (%d)", run->nranks,
+                       bands->nb));
+    ctx->nb = b1 - ctx->b0;
+  }
+  const int nbT = ctx->nbT;
   ctx->dt = run->dt;
   ctx->T_init = run->T_init;
   ctx->Tmax = run->T_init;
@@ -286,7 +339,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   ctx->v.assign(bands->v, bands->v + bands->nb);
   ctx->bcoef.assign(bands->beta_coef, bands->beta_coef + 5 * bands->nb);
   ctx->mode = bands->mode;
-  for (int b = 0; b < ctx->nb; ++b) {
+  for (int b = 0; b < nbT; ++b) {
     if (!(ctx->v[b] > 0)) return bail(fail(ctx, BTE_EINVAL, "group speed of channel %d must be > 0", b));
     for (int k = 0; k < 5; ++k)
       if (!(ctx->bcoef[5 * b + k] >= 0)) return bail(fail(ctx, BTE_EINVAL, "beta coefficients must be >= 0"));
@@ -343,16 +396,19 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   g.ncross = mesh->dim == 3 ? (int)(mesh->nx * mesh->ny) : (int)mesh->nx;
   const int64_t nm = mesh->dim == 3 ? mesh->nz : mesh->ny;
   g.nplanes_global = nm;
-  if (bte_plan_slab(mesh, dirs, ctx->nb, ctx->nranks, ctx->rank, &ctx->plan) != BTE_OK)
+  const int srank = ctx->slab_ranks > 1 ? ctx->rank : 0;
+  if (bte_plan_slab(mesh, dirs, ctx->nb, ctx->slab_ranks, srank, &ctx->plan) != BTE_OK)
     return bail(fail(ctx, BTE_EINVAL, "more ranks than planes along the slab axis"));
   g.nplanes = (int)ctx->plan.n_local;
   g.m0 = ctx->plan.m0;
-  g.plane_off = ctx->nranks > 1 ? 1 : 0;
-  g.has_lo_wall = (ctx->rank == 0) ? 1 : 0;
-  g.has_hi_wall = (ctx->rank == ctx->nranks - 1) ? 1 : 0;
+  g.plane_off = ctx->slab_ranks > 1 ? 1 : 0;
+  g.has_lo_wall = (srank == 0) ? 1 : 0;
+  g.has_hi_wall = (srank == ctx->slab_ranks - 1) ? 1 : 0;
   g.nslot = nslot;
   g.nj = nj;
   g.nb = ctx->nb;
+  g.nbT = nbT;
+  g.b0 = ctx->b0;
   g.E = nj * ctx->nb;
   g.Es = g.E + (g.E & 1);
   g.plane_stride = (int64_t)g.ncross * g.Es;
@@ -397,10 +453,10 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   }
 
   // ---- material tables: A_bj, X_bj (Bose-Einstein, reading #1)
-  std::vector<double> A(ctx->nb * kNGL, 0.0), X(ctx->nb * kNGL, 0.0);
-  std::vector<double> Iref(ctx->nb, 0.0), slope(ctx->nb, 0.0);
+  std::vector<double> A(nbT * kNGL, 0.0), X(nbT * kNGL, 0.0);
+  std::vector<double> Iref(nbT, 0.0), slope(nbT, 0.0);
   if (bands->mode == BTE_I0_BOSE_EINSTEIN) {
-    for (int b = 0; b < ctx->nb; ++b) {
+    for (int b = 0; b < nbT; ++b) {
       const double lo = bands->w_lo[b], hi = bands->w_hi[b];
       if (!(hi > lo && lo >= 0)) return bail(fail(ctx, BTE_EINVAL, "band %d: need 0 <= w_lo < w_hi", b));
       const double half = 0.5 * (hi - lo), mid = 0.5 * (hi + lo);
@@ -416,22 +472,22 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
       }
     }
   } else {
-    for (int b = 0; b < ctx->nb; ++b) {
+    for (int b = 0; b < nbT; ++b) {
       Iref[b] = bands->I_ref[b];
       slope[b] = bands->slope[b];
     }
   }
 
   // uniform band grid detection (exact): channel b spans [i_b dw, (i_b + 1) dw]
-  std::vector<int> ichan, ibv(ctx->nb, 0);
+  std::vector<int> ichan, ibv(nbT, 0);
   std::vector<double> Ugl(kNGL);
   int uniform = 0, imax = 0;
   double Xd = 0;
   if (bands->mode == BTE_I0_BOSE_EINSTEIN) {
     const double dw = bands->w_hi[0] - bands->w_lo[0];
     uniform = dw > 0;
-    std::vector<int> ib(ctx->nb);
-    for (int b = 0; b < ctx->nb && uniform; ++b) {
+    std::vector<int> ib(nbT);
+    for (int b = 0; b < nbT && uniform; ++b) {
       const double q = std::nearbyint(bands->w_lo[b] / dw);
       if (!(q >= 0 && q < 4096) || bands->w_lo[b] != q * dw || bands->w_hi[b] != (q + 1.0) * dw) uniform = 0;
       ib[b] = (int)q;
@@ -440,7 +496,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     }
     if (uniform) {
       ichan.assign(4 * (imax + 1), -1);
-      for (int b = 0; b < ctx->nb && uniform; ++b) {
+      for (int b = 0; b < nbT && uniform; ++b) {
         int q = 0;
         while (q < 4 && ichan[4 * ib[b] + q] >= 0) ++q;
         if (q == 4) uniform = 0;  // > 4 channels share one band: use the direct path
@@ -475,7 +531,7 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   g.coef = d_coef;
   g.ws = d_ws;
   g.refl_off = d_roff;
-  ctx->m.nb = ctx->nb;
+  ctx->m.nb = nbT;
   ctx->m.mode = bands->mode;
   ctx->m.v = d_v;
   ctx->m.bcoef = d_bc;
@@ -504,11 +560,27 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     int *d_ib;
     if ((st = upload(ctx, &d_ib, ibv.data(), ibv.size()))) return bail(st);
     ctx->m.ib = d_ib;
-    std::vector<double> rv(ctx->nb);
-    for (int b = 0; b < ctx->nb; ++b) rv[b] = 1.0 / ctx->v[b];
+    std::vector<double> rv(nbT);
+    for (int b = 0; b < nbT; ++b) rv[b] = 1.0 / ctx->v[b];
     double *d_rv;
     if ((st = upload(ctx, &d_rv, rv.data(), rv.size()))) return bail(st);
     ctx->m.rv = d_rv;
+  }
+  // m: the swept channels [b0, b0+nb) as a view of the full tables mF
+  ctx->mF = ctx->m;
+  {
+    Material &m = ctx->m;
+    const int b0 = ctx->b0;
+    m.nb = ctx->nb;
+    m.v += b0;
+    m.bcoef += 5 * b0;
+    m.I_ref += b0;
+    m.slope += b0;
+    m.A += kNGL * b0;
+    m.X += kNGL * b0;
+    m.ib += b0;
+    m.rv += b0;
+    if (ctx->band) m.uniform = 0;  // the band-grid fields index all channels: Newton only (mF)
   }
 
   const size_t ibytes = (size_t)g.slot_stride * nslot * sizeof(double);
@@ -518,9 +590,18 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
     CU(cudaMemsetAsync(ctx->I[k], 0, ibytes, ctx->stream));
   }
   const int64_t ncl = ctx->ncells_local;
-  ctx->I0c = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
-  ctx->beta = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
-  ctx->dI0c = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+  ctx->I0c = (double *)dev_alloc(ctx, ncl * nbT * sizeof(double));
+  ctx->beta = (double *)dev_alloc(ctx, ncl * nbT * sizeof(double));
+  ctx->dI0c = (double *)dev_alloc(ctx, ncl * nbT * sizeof(double));
+  ctx->I0s = ctx->I0c;
+  ctx->betas = ctx->beta;
+  if (ctx->band) {
+    ctx->Sall = (double *)dev_alloc(ctx, (size_t)ctx->nranks * ncl * sizeof(double));
+    ctx->I0s = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+    ctx->betas = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+    if (!ctx->Sall || !ctx->I0s || !ctx->betas) return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
+    CU(cudaMemsetAsync(ctx->Sall, 0, (size_t)ctx->nranks * ncl * sizeof(double), ctx->stream));
+  }
   ctx->T = (double *)dev_alloc(ctx, ncl * sizeof(double));
   ctx->Dpart = (double *)dev_alloc(ctx, ncl * nslot * ctx->nb * sizeof(double));
   ctx->d_err = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
@@ -609,10 +690,10 @@ bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_band
   // ---- initial state: equilibrium at T_init
   std::vector<double> T0(ncl, ctx->T_init);
   CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
-  CU(launch_fill_equilibrium(g, ctx->I0c, ctx->I[0], ctx->stream));
+  if ((st = refresh(ctx))) return bail(st);
+  CU(launch_fill_equilibrium(g, ctx->I0s, ctx->I[0], ctx->stream));
   ctx->cur = 0;
-  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
+  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
   CU(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
   return BTE_OK;
@@ -683,6 +764,7 @@ static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0 = 0, int ncols
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   if (!ctx) return BTE_EINVAL;
   if (!I && !T) return fail(ctx, BTE_EINVAL, "set_state needs I or T");
+  if (ctx->band && !T) return fail(ctx, BTE_EINVAL, "band context: set_state needs T");
   const int64_t ncl = ctx->ncells_local;
   bte_status st;
   if (T) {
@@ -702,13 +784,13 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
     std::vector<double> T0(ncl, ctx->T_init);
     CU(cudaMemcpyAsync(ctx->T, T0.data(), ncl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   }
-  CU(launch_refresh(ctx->m, ctx->T, ncl, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
+  if ((st = refresh(ctx))) return st;
   if (I) {
     if ((st = transfer_I(ctx, const_cast<double *>(I), 1))) return st;
   } else {
-    CU(launch_fill_equilibrium(ctx->g, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
+    CU(launch_fill_equilibrium(ctx->g, ctx->I0s, ctx->I[ctx->cur], ctx->stream));
   }
-  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   if (I && !T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
@@ -732,9 +814,9 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
   if (!(T_mean - std::fabs(T_amp) > 0)) return fail(ctx, BTE_EINVAL, "random start would give T <= 0");
   const bte_mesh &m = ctx->mesh;
   CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
-  CU(launch_refresh(ctx->m, ctx->T, ctx->ncells_local, ctx->I0c, ctx->dI0c, ctx->beta, ctx->stream));
-  CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0c, ctx->I[ctx->cur], ctx->stream));
-  if (ctx->nccl_comm && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if ((st = refresh(ctx))) return st;
+  CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0s, ctx->I[ctx->cur], ctx->stream));
+  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
   CU(cudaStreamSynchronize(ctx->stream));
   return BTE_OK;
 }
@@ -765,14 +847,20 @@ static int n_diffuse(const bte_ctx *ctx) {
 
 static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   NewtonArgs a;
-  a.m = ctx->m;
+  a.m = ctx->mF;
   a.Dpart = ctx->Dpart;
   a.T = ctx->T;
   a.I0c = ctx->I0c;
   a.dI0c = ctx->dI0c;
   a.beta_next = ctx->beta;
   a.nslot = ctx->g.nslot;
-  a.nb = ctx->nb;
+  a.nb = ctx->nbT;
+  a.Sall = ctx->band ? ctx->Sall : nullptr;
+  a.nparts = ctx->nranks;
+  a.I0s = ctx->band ? ctx->I0s : nullptr;
+  a.betas = ctx->band ? ctx->betas : nullptr;
+  a.b0s = ctx->b0;
+  a.nbs = ctx->nb;
   for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
   for (int o = 0; o < 8; ++o) a.oct_slot[o] = ctx->g.oct_slot[o];
   a.W = ctx->W;
@@ -802,8 +890,8 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.g = ctx->g;
   a.Iin = Iin;
   a.Iout = Iout;
-  a.I0c = ctx->I0c;
-  a.beta = ctx->beta;
+  a.I0c = ctx->I0s;
+  a.beta = ctx->betas;
   a.Dpart = ctx->Dpart;
   a.v = ctx->m.v;
   a.dt = ctx->dt;
@@ -924,6 +1012,43 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   return BTE_OK;
 }
 
+// Band partition, first half of a step: boundary + sweep of this part's
+// channels, then its partial S_r = sum_{b in part} c_b D_b into row `rank`
+// of Sall (the bands couple only through this reduction).
+static bte_status band_sweep_launch(bte_ctx *ctx, bool t) {
+  bte_status st;
+  double *Iin = ctx->I[ctx->cur];
+  double *Iout = ctx->I[1 - ctx->cur];
+  size_t id = (size_t)-1;
+  if (n_diffuse(ctx) > 0) {
+    if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
+    if ((st = launch_boundary(ctx, Iin))) return st;
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+  }
+  id = (size_t)-1;
+  if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
+  int fused = 0;
+  if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused))) return st;
+  if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+  id = (size_t)-1;
+  if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
+  CU(launch_band_partial(ctx->g, ctx->mF, ctx->Dpart, ctx->T, ctx->ncells_local,
+                         ctx->Sall + (int64_t)ctx->rank * ctx->ncells_local, ctx->stream));
+  ctx->tacc.launches++;
+  ctx->tacc.newton_launches++;
+  return span_end(ctx, t, ctx->stream, id);
+}
+
+// Band partition, second half: the Newton over all channels from the gathered
+// partials (identical inputs, hence identical T, on every part).
+static bte_status band_newton_launch(bte_ctx *ctx, bool t) {
+  bte_status st;
+  size_t id = (size_t)-1;
+  if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
+  if ((st = run_newton(ctx, ctx->steps_done, 0, -1, ctx->stream))) return st;
+  return span_end(ctx, t, ctx->stream, id);
+}
+
 static bte_status join_newton(bte_ctx *ctx) {
   for (int k = 0; k < (int)ctx->nt_pending.size(); ++k)
     if (ctx->nt_pending[k]) {
@@ -940,8 +1065,29 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
   if (!ctx) return BTE_EINVAL;
   if (nsteps < 0) return fail(ctx, BTE_EINVAL, "nsteps < 0");
   if (ctx->nranks > 1 && !ctx->nccl_comm)
-    return fail(ctx, BTE_EINVAL, "local-mode slab context: advance the group with bte_group_step");
+    return fail(ctx, BTE_EINVAL, "local-mode (slab or band) context: advance the group with bte_group_step");
   bte_status st;
+  if (ctx->band) {
+    const int64_t ncl = ctx->ncells_local;
+    for (int64_t s = 0; s < nsteps; ++s) {
+      const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
+      if ((st = band_sweep_launch(ctx, t))) return st;
+      if (ctx->nranks > 1) {  // AllGather of the per-cell partials, in place
+        size_t id = (size_t)-1;
+        if ((st = span_begin(ctx, t, 3, ctx->stream, &id))) return st;
+        std::string emsg;
+        if (nccl_shim_allgather(ctx->nccl_comm, ctx->Sall + (int64_t)ctx->rank * ncl, ctx->Sall, (size_t)ncl,
+                                ctx->stream, &emsg))
+          return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+        if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+      }
+      if ((st = band_newton_launch(ctx, t))) return st;
+      if (t) ctx->timing_used++;
+      ctx->cur = 1 - ctx->cur;
+      ctx->steps_done++;
+    }
+    return sync_check(ctx);
+  }
   for (int64_t s = 0; s < nsteps; ++s) {
     const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
     if ((st = step_launch(ctx, t, ctx->nranks > 1 && ctx->overlap))) return st;
@@ -1048,6 +1194,40 @@ static bte_status group_exchange_overlap(bte_ctx **ctxs, int n) {
   return BTE_OK;
 }
 
+// Local-mode band exchange: every part's row of Sall is copied into the same
+// row of every other part's Sall, after the receiver's previous Newton (which
+// read its Sall) and the sender's partial.
+static bte_status band_exchange(bte_ctx **ctxs, int n) {
+  bte_ctx *ctx = ctxs[0];
+  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
+    if (atoi(e)) return BTE_OK;
+  const int64_t ncl = ctx->ncells_local;
+  std::vector<cudaEvent_t> done(n), put(n);
+  for (int r = 0; r < n; ++r) {
+    CU(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&put[r], cudaEventDisableTiming));
+    CU(cudaEventRecord(done[r], ctxs[r]->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      CU(cudaStreamWaitEvent(c->stream, done[q], 0));
+      CU(cudaMemcpyAsync(ctxs[q]->Sall + r * ncl, c->Sall + r * ncl, (size_t)ncl * sizeof(double),
+                         cudaMemcpyDefault, c->stream));
+    }
+    CU(cudaEventRecord(put[r], c->stream));
+  }
+  for (int q = 0; q < n; ++q)
+    for (int r = 0; r < n; ++r)
+      if (r != q) CU(cudaStreamWaitEvent(ctxs[q]->stream, put[r], 0));
+  for (int r = 0; r < n; ++r) {
+    cudaEventDestroy(done[r]);
+    cudaEventDestroy(put[r]);
+  }
+  return BTE_OK;
+}
+
 bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
   if (!ctxs || n < 1 || nsteps < 0) return BTE_EINVAL;
   for (int r = 0; r < n; ++r) {
@@ -1056,8 +1236,30 @@ bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
       return fail(ctxs[r], BTE_EINVAL, "bte_group_step: ctxs[%d] must be local-mode rank %d of %d", r, r, n);
     if (ctxs[r]->steps_done != ctxs[0]->steps_done)
       return fail(ctxs[r], BTE_EINVAL, "bte_group_step: contexts are at different steps");
+    if (ctxs[r]->band != ctxs[0]->band || (ctxs[0]->band && ctxs[r]->ncells_local != ctxs[0]->ncells_local))
+      return fail(ctxs[r], BTE_EINVAL, "bte_group_step: mixed band/slab contexts or different meshes");
   }
   bte_status st;
+  if (ctxs[0]->band) {
+    for (int64_t s = 0; s < nsteps; ++s) {
+      for (int r = 0; r < n; ++r) {
+        const bool t = ctxs[r]->timing && ctxs[r]->timing_used < ctxs[r]->timing_max;
+        if ((st = band_sweep_launch(ctxs[r], t))) return st;
+      }
+      if (n > 1 && (st = band_exchange(ctxs, n))) return st;
+      for (int r = 0; r < n; ++r) {
+        bte_ctx *c = ctxs[r];
+        const bool t = c->timing && c->timing_used < c->timing_max;
+        if ((st = band_newton_launch(c, t))) return st;
+        if (t) c->timing_used++;
+        c->cur = 1 - c->cur;
+        c->steps_done++;
+      }
+    }
+    for (int r = 0; r < n; ++r)
+      if ((st = sync_check(ctxs[r]))) return st;
+    return BTE_OK;
+  }
   if (n > 1 && (st = group_exchange(ctxs, n, false))) return st;  // prime halos from the current state
   for (int64_t s = 0; s < nsteps; ++s) {
     for (int r = 0; r < n; ++r) {
@@ -1141,7 +1343,7 @@ bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count)
   const int64_t ncl = ctx->ncells_local;
   bte_status st;
   if (which == 2 || which == 3) {
-    if (count != (size_t)(ncl * ctx->nb)) return fail(ctx, BTE_EINVAL, "count mismatch");
+    if (count != (size_t)(ncl * ctx->nbT)) return fail(ctx, BTE_EINVAL, "count mismatch");
     CU(cudaMemcpy(out, which == 2 ? ctx->I0c : ctx->beta, count * sizeof(double), cudaMemcpyDeviceToHost));
     return BTE_OK;
   }
@@ -1215,6 +1417,10 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
   out->n_octants = ctx->g.nslot;
   out->nj = ctx->g.nj;
   out->bytes_state = ctx->bytes;
+  out->b0 = ctx->b0;
+  out->b1 = ctx->b0 + ctx->nb;
+  out->nb_total = ctx->nbT;
+  out->band = ctx->band;
   return BTE_OK;
 }
 

@@ -59,7 +59,9 @@ struct Geometry {
   int plane_off;          // 1 when halo planes are stored, else 0
   int64_t plane_stride;   // doubles per plane (ncross * E)
   int64_t slot_stride;    // doubles per slot
-  int nslot, nj, nb, E;
+  int nslot, nj, nb, E;   // nb: channels this context sweeps
+  int nbT, b0;            // band partition (bte_create_band): channels [b0, b0+nb) of nbT
+                          // (else nbT = nb, b0 = 0); only the random-start counter uses them
   int Es;                 // (cell, octant) block stride in doubles: E rounded up to even (16-B TMA)
   int slot_oct[kMaxSlots];
   int oct_slot[8];        // inverse: slot of octant o, or -1
@@ -88,6 +90,10 @@ struct NewtonArgs {
   int64_t step;           // step index for error reporting
   int col0, ncols;        // column (cross-cell) range of this launch
   int ncross, nplanes;
+  const double *Sall;     // band partition: [nparts][ncells] gathered partials (else null)
+  int nparts;
+  double *I0s, *betas;    // band partition: the sweep's rows [c][nbs] = channels [b0s, b0s+nbs)
+  int b0s, nbs;
   int predict;            // quadratic-convergence acceptance (reading R-f)
   int minb;               // k_newton occupancy variant (0 = default)
   unsigned long long *stats;  // debug counters: [evaluations, final re-evaluations, cells solved] or null
@@ -147,5 +153,7 @@ cudaError_t launch_dpart_from_I(const Geometry &g, const double *I, const double
                                cudaStream_t s);
 cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, double *Ec,
                           cudaStream_t s);
+cudaError_t launch_band_partial(const Geometry &g, const Material &mF, const double *Dpart, const double *T,
+                                int64_t nc, double *S, cudaStream_t s);
 
 }  // namespace bte

@@ -224,6 +224,7 @@ __host__ __device__ __forceinline__ int newton_scratch(const Material &m, int nb
   return 4 * nb + 2 * kNGL + m.imax + 1;  // c | E | M | R | I0 | dI0 | d2I0
 }
 
+template <bool BAND = false>
 __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
                             double *cs, int lane);
 
@@ -1043,6 +1044,7 @@ __device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, con
   __syncwarp();
 }
 
+template <bool BAND>
 __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, const double *sX, const int *sI,
                             double *cs, int lane) {
   const int nb = a.nb;
@@ -1051,6 +1053,22 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   const int par = lane >> 4;
   const double Tn = a.T[c];
   double F0 = 0.0, K0 = 0.0, Fp0 = 0.0;
+  if (BAND) {
+    // band partition: F(T^n) = sum_b c_b D_b arrives as one partial per part,
+    // summed in part order (identical on every part)
+    for (int r = 0; r < a.nparts; ++r) F0 += __ldcg(a.Sall + (int64_t)r * a.ncells + c);
+    for (int b = lane; b < nb; b += 32) {
+      const double bn = beta_of_T(a.m.bcoef, b, Tn);
+      const double cb = bn * a.m.rv[b];
+      cs[b] = cb;
+      a.beta_next[c * nb + b] = bn;
+      if (b >= a.b0s && b < a.b0s + a.nbs) a.betas[c * a.nbs + b - a.b0s] = bn;  // the sweep's rows
+      K0 -= cb * (a.W * a.I0c[c * nb + b]);
+      Fp0 += cb * (a.W * a.dI0c[c * nb + b]);
+    }
+    K0 = F0 + warp_sum(K0);
+    Fp0 = warp_sum(Fp0);
+  } else {
   for (int b = lane; b < nb; b += 32) {
     double q[8];  // octant-indexed with compile-time indices: stays in registers
 #pragma unroll
@@ -1070,6 +1088,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   F0 = warp_sum(F0);
   K0 = warp_sum(K0);
   Fp0 = warp_sum(Fp0);
+  }
   __syncwarp();
   double Tf = Tn;
   double evaluated_at = -1.0;  // T of the per-channel values held in sI0/sD0
@@ -1217,6 +1236,10 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     } else {
       for (int b = lane; b < nb; b += 32) a.I0c[c * nb + b] = a.m.I_ref[b] + a.m.slope[b] * (Tf - a.m.T_ref);
     }
+    if (BAND) {  // band partition: this part's slice for its sweep (__syncwarp orders the warp's writes)
+      __syncwarp();
+      for (int b = lane; b < a.nbs; b += 32) a.I0s[c * a.nbs + b] = a.I0c[c * nb + a.b0s + b];
+    }
   }
   __syncwarp();
 }
@@ -1230,7 +1253,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
 //   F'(T) = W sum_b c_b dI0_b/dT
 // F(T^n) = sum_b c_b D_b exactly (I0c = I0(T^n)) and F'(T^n) uses the dI0/dT
 // stored by the previous refresh, so the first Newton step costs no integral.
-template <int MINB>
+template <int MINB, bool BAND>
 __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const NewtonArgs a) {
   extern __shared__ double nsh[];
   const int nb = a.nb;
@@ -1255,7 +1278,7 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const Newton
   const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
   for (int64_t q = (int64_t)blockIdx.x * kNewtonWarps + warp; q < nq; q += nwarps) {
     const int64_t p = q / ncol;
-    newton_cell(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, threadIdx.x & 31);
+    newton_cell<BAND>(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, threadIdx.x & 31);
   }
 }
 
@@ -1267,10 +1290,16 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   const size_t smem = (2 * (size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
   const int minb = a.minb > 0 ? a.minb : BTE_NEWTON_MINB;
+  if (a.Sall) {  // band partition (bte_create_band)
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_newton<BTE_NEWTON_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_newton<BTE_NEWTON_MINB, true><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
+    return cudaGetLastError();
+  }
 #define BTE_NL(M)                                                                                   \
   case M:                                                                                           \
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_newton<M><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);                                 \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_newton<M, false><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);                          \
     break;
   switch (minb) {
     BTE_NL(2)
@@ -1418,7 +1447,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-// I = I0c * (1 + amp*(2u - 1)), u from the canonical global index (c_g*nd + d)*nb + b
+// I = I0c * (1 + amp*(2u - 1)), u from the canonical global index (c_g*nd + d)*nbT + b0 + b
 __global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, int nd, uint64_t seed,
                            double amp, const double *__restrict__ I0c, double *__restrict__ I) {
   const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
@@ -1432,7 +1461,7 @@ __global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, in
   const int b = e - j * g.nb;
   const int d = canon_d[sl * g.nj + j];
   const int64_t cg = g.m0 * g.ncross + cell;
-  const uint64_t idx = ((uint64_t)cg * nd + d) * g.nb + b;
+  const uint64_t idx = ((uint64_t)cg * nd + d) * g.nbT + g.b0 + b;
   const double u = (double)(splitmix64(seed ^ idx) >> 11) * 0x1.0p-53;
   I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] =
       I0c[cell * g.nb + b] * (1.0 + amp * (2.0 * u - 1.0));
@@ -1488,6 +1517,36 @@ cudaError_t launch_dpart_from_I(const Geometry &g, const double *I, const double
   const int64_t n = (int64_t)g.nplanes * g.ncross * g.nslot * g.nb;
   if (n == 0) return cudaSuccess;
   k_dpart_from_I<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I, I0c, Dpart);
+  return cudaGetLastError();
+}
+
+// Band partition (bte_create_band): this part's share of F(T^n),
+// S_r(c) = sum_{b in [b0, b0+nb)} c_b D_{c,b}, c_b = beta_b(T^n_c) / v_b, with
+// D_{c,b} the octant tree of the sweep's partials.  One warp per cell.
+__global__ void k_band_partial(const Geometry g, const Material mF, const double *__restrict__ Dpart,
+                               const double *__restrict__ T, int64_t nc, double *__restrict__ S) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  const double Tn = T[c];
+  double part = 0.0;
+  for (int b = lane; b < g.nb; b += 32) {
+    double q[8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) q[o] = g.oct_slot[o] >= 0 ? Dpart[(c * g.nslot + g.oct_slot[o]) * g.nb + b] : 0.0;
+    const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    const int bg = g.b0 + b;
+    const double cb = beta_of_T(mF.bcoef, bg, Tn) * mF.rv[bg];
+    part += cb * D;
+  }
+  part = warp_sum(part);
+  if (lane == 0) S[c] = part;
+}
+
+cudaError_t launch_band_partial(const Geometry &g, const Material &mF, const double *Dpart, const double *T,
+                                int64_t nc, double *S, cudaStream_t s) {
+  if (nc == 0) return cudaSuccess;
+  k_band_partial<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(g, mF, Dpart, T, nc, S);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@ struct Nccl {
   decltype(&ncclCommInitRank) init = nullptr;
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclGroupStart) gstart = nullptr;
   decltype(&ncclGroupEnd) gend = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
@@ -35,12 +36,13 @@ Nccl &lib(std::string *err) {
   n.init = (decltype(n.init))dlsym(n.h, "ncclCommInitRank");
   n.send = (decltype(n.send))dlsym(n.h, "ncclSend");
   n.recv = (decltype(n.recv))dlsym(n.h, "ncclRecv");
+  n.allgather = (decltype(n.allgather))dlsym(n.h, "ncclAllGather");
   n.gstart = (decltype(n.gstart))dlsym(n.h, "ncclGroupStart");
   n.gend = (decltype(n.gend))dlsym(n.h, "ncclGroupEnd");
   n.destroy = (decltype(n.destroy))dlsym(n.h, "ncclCommDestroy");
   n.errstr = (decltype(n.errstr))dlsym(n.h, "ncclGetErrorString");
-  if (!n.init || !n.send || !n.recv || !n.gstart || !n.gend || !n.destroy || !n.errstr) {
-    if (err) *err = "libnccl is missing point-to-point symbols";
+  if (!n.init || !n.send || !n.recv || !n.allgather || !n.gstart || !n.gend || !n.destroy || !n.errstr) {
+    if (err) *err = "libnccl is missing symbols (send/recv/allgather/group)";
     dlclose(n.h);
     n.h = nullptr;
   }
@@ -71,6 +73,11 @@ int nccl_shim_send(void *comm, const double *buf, size_t count, int peer, cudaSt
 
 int nccl_shim_recv(void *comm, double *buf, size_t count, int peer, cudaStream_t s, std::string *err) {
   return check(lib(err).recv(buf, count, ncclFloat64, peer, (ncclComm_t)comm, s), err);
+}
+
+int nccl_shim_allgather(void *comm, const double *send, double *recv, size_t count, cudaStream_t s,
+                        std::string *err) {
+  return check(lib(err).allgather(send, recv, count, ncclFloat64, (ncclComm_t)comm, s), err);
 }
 
 int nccl_shim_group_start(std::string *err) { return check(lib(err).gstart(), err); }

@@ -511,3 +511,102 @@ def test_parity_kernel_variants(Solver, variant, monkeypatch):
             p.mesh = bi.Mesh(3, 9, 7, 6, 1e-6, 1e-6, 1e-6)
         (rel, dT), _ = _run_both(Solver, p, n)
         assert rel <= REL_I and dT <= ABS_T, (variant, p.name, rel, dT)
+
+
+# ----------------------------------------------------------------- band partition
+
+def _band_group(Solver, p, P, I, T):
+    """P band contexts (bte_create_band, local mode) of problem p holding the
+    channel slices of the state (I, T)."""
+    group = []
+    for r in range(P):
+        sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=P, decomp="band")
+        group.append(sv)
+        for reg in range(6 if p.mesh.dim == 3 else 4):
+            bc = p.bcs[reg]
+            sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+        sv.set_state(np.ascontiguousarray(I[:, :, sv.b0:sv.b1]), T)
+    return group
+
+
+def _band_cases():
+    si = bi.config2(n=12)
+    si.mesh = bi.Mesh(2, 12, 11, 1, 2e-6, 2e-6, 1.0)
+    si.dirs = bi.directions_control_angle(4, 8)
+    si.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, 2e-6, width=4e-6), 300.0)
+    return {"3d": _group_case("3d"), "2d": _group_case("2d"), "si40": si}
+
+
+@pytest.mark.parametrize("case,P", [("3d", 2), ("3d", 3), ("2d", 3), ("si40", 3), ("si40", 8), ("si40", 1)])
+def test_band_group_matches_oracle(Solver, case, P):
+    """Band partition on one GPU: P contexts each sweep their channels [b0, b1),
+    exchange one partial per cell, and run the same Newton over all channels.
+    Union of slices and T match the oracle; T is bitwise identical on every
+    part; the result matches the single-context GPU run to rounding."""
+    p = _band_cases()[case]
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    nsteps = 6
+    Io, To, _, _ = o.run(I, T, nsteps)
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(nsteps)
+        I1, T1 = sv.intensity(), sv.temperature()
+    group = _band_group(Solver, p, P, I, T)
+    try:
+        assert [(sv.b0, sv.b1) for sv in group][-1][1] == p.bands.nb
+        Solver.group_step(group, 2)
+        Solver.group_step(group, nsteps - 2)
+        Ig = np.concatenate([sv.intensity() for sv in group], axis=2)
+        Ts = [sv.temperature() for sv in group]
+    finally:
+        for sv in group:
+            sv.close()
+    assert all(np.array_equal(t, Ts[0]) for t in Ts)
+    rel, dT = _cmp(Ig, Ts[0], Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    assert np.max(np.abs(Ts[0] - T1)) <= 1e-10 and np.max(np.abs(Ig / I1 - 1)) <= 1e-12
+
+
+def test_band_group_mutation_skip_exchange(Solver, monkeypatch):
+    """Mutation: without the partial exchange each part's Newton sees
+    only its own channels' reduction, and T leaves the oracle's tolerance."""
+    p = _band_cases()["si40"]
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    Io, To, _, _ = o.run(I, T, 3)
+    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")
+    group = _band_group(Solver, p, 2, I, T)
+    try:
+        Solver.group_step(group, 3)
+        Tg = group[0].temperature()
+    finally:
+        for sv in group:
+            sv.close()
+    assert np.max(np.abs(Tg - To)) > 1e3 * ABS_T
+
+
+def test_band_init_random_and_tables(Solver):
+    """Band contexts draw the single-domain random start (global channel index
+    in the counter) and hold all channels' I0c / beta rows."""
+    p = _band_cases()["si40"]
+    with Solver.from_problem(p) as sv:
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        I1, T1 = sv.intensity(), sv.temperature()
+        I0c1, b1 = sv.debug_substep(2), sv.debug_substep(3)
+    group = []
+    try:
+        for r in range(3):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=3, decomp="band")
+            group.append(sv)
+            sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+            assert np.array_equal(sv.intensity(), I1[:, :, sv.b0:sv.b1])
+            assert np.array_equal(sv.temperature(), T1)
+            assert np.array_equal(sv.debug_substep(2), I0c1) and np.array_equal(sv.debug_substep(3), b1)
+        with pytest.raises(Exception):
+            group[0].set_state(I1[:, :, group[0].b0:group[0].b1], None)  # band contexts need T
+        with pytest.raises(Exception):
+            group[0].step(1)  # local-mode parts advance only through group_step
+    finally:
+        for sv in group:
+            sv.close()
