@@ -2,7 +2,7 @@
 """Benchmark of the B200 explicit phonon-BTE step (arXiv 2305.19400).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config 2|3|5] [--start random|physical]
+                  [--config 2|3|5|6|1] [--start random|physical] [--decomp slab|band]
 
 Prints ONE JSON line (rank 0).  Metric: DOF-updates/s (cell x direction x
 channel per second) of the whole step (boundary pass + fused sweep +
@@ -13,7 +13,10 @@ cells, 400 directions, 40 channels, Gaussian hot spot + cold wall, specular
 sides, dt = 1e-12 s, synthetic seeded inputs (bte_inputs.config2).  Each
 intensity buffer is 1.84 GB >> 126 MB L2, so no L2 flush is needed between
 steps.  For N > 1 the mesh grows along y (120 rows per GPU, weak scaling) and
-is slab-decomposed with NCCL halo exchange.
+is slab-decomposed with NCCL halo exchange; --decomp band instead keeps the
+BASELINE problem fixed and splits its channels over the N GPUs (the paper's
+band partition: one ncclAllGather of a scalar per cell per
+step, strong scaling).
 
 --impl reference times the CPU oracle (oracle/, plain fp64 C, all host cores)
 on a bounded sample of the same workload -- the paper has no runnable code,
@@ -262,16 +265,18 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    p = _problem(args.config, world)
+    band = args.decomp == "band"
+    p = _problem(args.config, 1 if band else world)
     nccl_id = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     stream = torch.cuda.Stream(local)
-    sv = Solver.from_problem(p, device=local, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id)
+    sv = Solver.from_problem(p, device=local, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id,
+                             decomp=args.decomp)
     dof_local = sv.ncells * sv.nd * sv.nb
-    dof_global = sv.ncells_global * sv.nd * sv.nb
+    dof_global = sv.ncells_global * sv.nd * sv.nb_total
 
     def init_state():
         if args.start == "random":
@@ -318,7 +323,8 @@ def run_b200(args):
     tpd = _traffic_per_dof(p.name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None if tpd is None else tpd * dof_per_launch,
-                "kernel": ("k_sweep_tma (a1+a2 fused upwind flux + relaxation + octant partial sums"
+                "kernel": (("k_sweep_tma" if sv.nj * sv.nb >= 384 else "k_sweep")
+                           + " (a1+a2 fused upwind flux + relaxation + octant partial sums"
                            + (", a3+a4 Newton fused in the tail)" if tim["newton_launches"] == 0 else ")")),
                 "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_per_launch, "kernel_ms_avg": sweep_ms,
                 "launches_per_step": launches_per_step, "peak_source": peak_src,
@@ -364,11 +370,11 @@ def run_b200(args):
             "metric": "BTE DOF-updates/s (cell x dir x band / s), whole step",
             "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if band else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
-            "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb,
+            "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb_total,
                        "dof_per_step": dof_global, "start": args.start, "dt": p.dt,
-                       "parallelism": f"slab{world}" if world > 1 else "single",
+                       "parallelism": (f"band{world}" if band else f"slab{world}") if world > 1 else "single",
                        "l2": "inputs > L2 (1.84 GB/buffer vs 126 MB), no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(tim["launches"]),
@@ -391,6 +397,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--decomp", default="slab", choices=["slab", "band"])
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
