@@ -137,6 +137,13 @@ typedef struct {
  * populations, W > 0), precomputes geometry and coefficient tables, allocates
  * the state and initialises it to equilibrium at T_init (I = I0_b(T_init)).
  * All walls start SPECULAR; call bte_set_bc to change them.
+ * Intensity storage: two full buffers (I^n, I^{n+1}) when they fit in free
+ * device memory next to ~2 GB of tables, else octant-slot rotation (SURVEY
+ * 7.3 #1): one buffer of (octants + 1) slot regions, each octant swept from
+ * its region into the spare one, specular ghosts snapshotted first -- e.g.
+ * 144 GB instead of 256 GB for 10^6 cells x 400 directions x 40 channels.
+ * Same results bit for bit; env BTE_ROTATE=0/1 overrides the choice;
+ * bte_info.rotate reports it.  bte_debug_substep 0/1 are unavailable then.
  * Errors: BTE_EINVAL, BTE_ENOMEM, BTE_ECUDA, BTE_EUNSTABLE, BTE_ENCCL. */
 BTE_API bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                       const bte_run *run, bte_ctx **out);
@@ -273,6 +280,7 @@ typedef struct {
   int nd, nb, n_octants, nj;                         /* nj = directions per octant  */
   int64_t bytes_state;                               /* device bytes held by ctx    */
   int b0, b1, nb_total, band;                        /* channel band; band = 1 for bte_create_band */
+  int rotate;                                        /* 1: octant-slot rotation (see bte_create)  */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

@@ -83,7 +83,7 @@ class Info(C.Structure):
     _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
                 ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
-                ("nb_total", C.c_int), ("band", C.c_int)]
+                ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int)]
 
 
 _lib = None
@@ -211,6 +211,7 @@ class Solver:
         self.bytes_state = int(info.bytes_state)
         self.b0, self.b1, self.nb_total = int(info.b0), int(info.b1), int(info.nb_total)
         self.band = bool(info.band)
+        self.rotate = bool(info.rotate)
         if self.nb_total == 0:  # older A/B build without the band fields
             self.b0, self.b1, self.nb_total = 0, self.nb, self.nb
 

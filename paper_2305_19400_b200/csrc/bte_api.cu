@@ -71,6 +71,10 @@ struct bte_ctx {
   Material mF{};  // all channels (Newton, refresh)
   double *I[2] = {nullptr, nullptr};
   int cur = 0;
+  // octant-slot rotation: one buffer of nslot + 1 slot regions;
+  // I[0] == I[1]; g.slot_off maps each slot to its region, `spare` is free
+  int rot = 0, spare = 0;
+  double *gspec[6] = {nullptr};
   double *I0c = nullptr, *dI0c = nullptr, *beta = nullptr, *T = nullptr, *Dpart = nullptr;
   double *gtab[6] = {nullptr};
   int *d_dmap = nullptr, *d_canon_d = nullptr;
@@ -191,6 +195,8 @@ static bte_status refresh(bte_ctx *ctx) {
   }
   return BTE_OK;
 }
+
+static int64_t ncl_of(const bte_ctx *ctx) { return ctx->ncells_local; }
 
 static int64_t n_faces_global(const bte_ctx *ctx, int region) {
   const int a = region / 2;
@@ -584,10 +590,29 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   }
 
   const size_t ibytes = (size_t)g.slot_stride * nslot * sizeof(double);
-  for (int k = 0; k < 2; ++k) {
-    ctx->I[k] = (double *)dev_alloc(ctx, ibytes);
-    if (!ctx->I[k]) return bail(fail(ctx, BTE_ENOMEM, "cannot allocate the intensity buffer (%zu bytes)", ibytes));
-    CU(cudaMemsetAsync(ctx->I[k], 0, ibytes, ctx->stream));
+  // two full buffers, or (when they would not fit next to ~2 GB of tables and
+  // workspace, or BTE_ROTATE=1) octant-slot rotation in (nslot + 1)/nslot of one
+  {
+    size_t freeb = 0, totalb = 0;
+    CU(cudaMemGetInfo(&freeb, &totalb));
+    const size_t other = (size_t)ncl_of(ctx) * (nslot * ctx->nb + 4 * nbT + 2) * sizeof(double) + (2ull << 30);
+    ctx->rot = 2 * ibytes + other > freeb ? 1 : 0;
+    if (const char *e = getenv("BTE_ROTATE")) ctx->rot = atoi(e) ? 1 : 0;
+  }
+  for (int sl = 0; sl < kMaxSlots; ++sl) g.slot_off[sl] = (int64_t)sl * g.slot_stride;
+  g.rot = ctx->rot;
+  if (ctx->rot) {
+    const size_t rbytes = (size_t)g.slot_stride * (nslot + 1) * sizeof(double);
+    ctx->I[0] = ctx->I[1] = (double *)dev_alloc(ctx, rbytes);
+    if (!ctx->I[0]) return bail(fail(ctx, BTE_ENOMEM, "cannot allocate the intensity buffer (%zu bytes)", rbytes));
+    CU(cudaMemsetAsync(ctx->I[0], 0, rbytes, ctx->stream));
+    ctx->spare = nslot;
+  } else {
+    for (int k = 0; k < 2; ++k) {
+      ctx->I[k] = (double *)dev_alloc(ctx, ibytes);
+      if (!ctx->I[k]) return bail(fail(ctx, BTE_ENOMEM, "cannot allocate the intensity buffer (%zu bytes)", ibytes));
+      CU(cudaMemsetAsync(ctx->I[k], 0, ibytes, ctx->stream));
+    }
   }
   const int64_t ncl = ctx->ncells_local;
   ctx->I0c = (double *)dev_alloc(ctx, ncl * nbT * sizeof(double));
@@ -824,24 +849,37 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
 // ---- the step
 
 static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
-  const Geometry &g = ctx->g;
+  Geometry &g = ctx->g;
   const int nreg = g.dim == 3 ? 6 : 4;
   int n = 0;
   for (int r = 0; r < nreg; ++r) {
-    if (g.kind[r] != BC_DIFF) continue;
     const int a = r / 2;
     if (a == g.dim - 1 && !((r & 1) ? g.has_hi_wall : g.has_lo_wall)) continue;
-    CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
-    ++n;
+    if (g.kind[r] == BC_DIFF) {
+      CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
+      ++n;
+    } else if (g.kind[r] == BC_SPEC && ctx->rot) {
+      if (!ctx->gspec[r]) {  // first use: [faces][nslot*nj][nb]
+        const size_t bytes = (size_t)n_faces_global(ctx, r) * g.nslot * g.nj * g.nb * sizeof(double);
+        ctx->gspec[r] = (double *)dev_alloc(ctx, bytes);
+        if (!ctx->gspec[r]) return fail(ctx, BTE_ENOMEM, "specular snapshot allocation (%zu bytes) failed", bytes);
+        g.gspec[r] = ctx->gspec[r];
+      }
+      CU(launch_spec_snapshot(g, Icur, r, ctx->gspec[r], ctx->stream));
+      ++n;
+    }
   }
   ctx->tacc.launches += n;
   ctx->tacc.boundary_launches += n;
   return BTE_OK;
 }
 
+// walls that need a boundary pass before the sweep: diffuse ghosts, and under
+// slot rotation the specular snapshots
 static int n_diffuse(const bte_ctx *ctx) {
   int n = 0;
-  for (int r = 0; r < (ctx->g.dim == 3 ? 6 : 4); ++r) n += ctx->g.kind[r] == BC_DIFF;
+  for (int r = 0; r < (ctx->g.dim == 3 ? 6 : 4); ++r)
+    n += ctx->g.kind[r] == BC_DIFF || (ctx->rot && ctx->g.kind[r] == BC_SPEC);
   return n;
 }
 
@@ -882,7 +920,55 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
 static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
                                     int *fused, int col0 = 0, int ncols = 0, int p_lo = 0, int p_hi = 0,
                                     int seg_len = 0) {
-  SweepArgs a;
+  if (ctx->rot) {
+    // octant-slot rotation: octant k is swept from its region into the spare
+    // region, whose old occupant's region becomes the next spare; the octants
+    // go one launch each, in slot order (each reads only its own I^n; the
+    // specular ghosts come from the boundary pass's snapshot)
+    *fused = 0;
+    for (int k = 0; k < ctx->g.nslot; ++k) {
+      SweepArgs a{};
+      a.col0 = col0;
+      a.ncols = ncols;
+      a.p_lo = p_lo;
+      a.p_hi = p_hi;
+      a.slot0 = k;
+      a.nslots = 1;
+      a.g = ctx->g;
+      for (int sl = 0; sl < kMaxSlots; ++sl) a.out_off[sl] = ctx->g.slot_off[sl];
+      a.out_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
+      a.Iin = Iin;
+      a.Iout = Iout;
+      a.I0c = ctx->I0s;
+      a.beta = ctx->betas;
+      a.Dpart = ctx->Dpart;
+      a.v = ctx->m.v;
+      a.dt = ctx->dt;
+      a.seg_len = seg_len > 0 ? seg_len : ctx->seg_len;
+      a.use_tma = ctx->use_tma;
+      a.stages_override = ctx->stages_override;
+      a.target_threads = ctx->target_threads;
+      a.smem_budget_kb = ctx->smem_budget_kb;
+      a.stcs = ctx->stcs;
+      a.tx_override = ctx->tx_override;
+      a.l2hint = ctx->l2hint;
+      a.nw = newton_args(ctx, step);
+      a.fuse_newton = 0;
+      a.done = ctx->d_done;
+      int f = 0;
+      CU(launch_sweep(a, ctx->stream, &f));
+      const int freed = (int)(ctx->g.slot_off[k] / ctx->g.slot_stride);
+      ctx->g.slot_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
+      ctx->spare = freed;
+      ctx->tacc.launches++;
+      ctx->tacc.sweep_launches++;
+    }
+    return BTE_OK;
+  }
+  SweepArgs a{};
+  a.slot0 = 0;
+  a.nslots = 0;
+  for (int sl = 0; sl < kMaxSlots; ++sl) a.out_off[sl] = ctx->g.slot_off[sl];
   a.col0 = col0;
   a.ncols = ncols;
   a.p_lo = p_lo;
@@ -950,7 +1036,7 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
 // are swept (SURVEY 8(e) overlap schedule).
 static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   const bool has_bnd = n_diffuse(ctx) > 0;
-  const int C = ctx->fuse_newton ? 1 : ctx->nchunks;
+  const int C = (ctx->fuse_newton || ctx->rot) ? 1 : ctx->nchunks;
   const int ncross = ctx->g.ncross;
   const int np = ctx->g.nplanes;
   bte_status st;
@@ -962,7 +1048,7 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
     if ((st = launch_boundary(ctx, Iin))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   }
-  if (split && (C > 1 || ctx->fuse_newton)) split = false;
+  if (split && (C > 1 || ctx->fuse_newton || ctx->rot)) split = false;
   if (split) {
     int fused = 0;
     id = (size_t)-1;
@@ -1143,8 +1229,8 @@ static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
       bte_ctx *q = ctxs[m.peer];
       CU(cudaStreamWaitEvent(c->stream, done[m.peer], 0));
       double *dst = q->I[output_buffers ? 1 - q->cur : q->cur];
-      const double *sp = src + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
-      double *dp = dst + (int64_t)m.slot * q->g.slot_stride + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
+      const double *sp = src + g.slot_off[m.slot] + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+      double *dp = dst + q->g.slot_off[m.slot] + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
       CU(cudaMemcpyAsync(dp, sp, (size_t)m.count * sizeof(double), cudaMemcpyDefault, c->stream));
     }
     CU(cudaEventRecord(put[r], c->stream));
@@ -1180,8 +1266,8 @@ static bte_status group_exchange_overlap(bte_ctx **ctxs, int n) {
       bte_ctx *q = ctxs[m.peer];
       CU(cudaStreamWaitEvent(c->comm_stream, q->ev_bnd, 0));
       double *dst = q->I[1 - q->cur];
-      const double *sp = src + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
-      double *dp = dst + (int64_t)m.slot * q->g.slot_stride + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
+      const double *sp = src + g.slot_off[m.slot] + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+      double *dp = dst + q->g.slot_off[m.slot] + (m.plane - q->g.m0 + q->g.plane_off) * q->g.plane_stride;
       CU(cudaMemcpyAsync(dp, sp, (size_t)m.count * sizeof(double), cudaMemcpyDefault, c->comm_stream));
     }
     CU(cudaEventRecord(c->ev_halo, c->comm_stream));
@@ -1290,7 +1376,7 @@ static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream)
   if (nccl_shim_group_start(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
   for (int k = 0; k < ctx->plan.n_msgs; ++k) {
     const bte_msg &m = ctx->plan.msg[k];
-    double *ptr = Ibuf + (int64_t)m.slot * g.slot_stride + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
+    double *ptr = Ibuf + g.slot_off[m.slot] + (m.plane - g.m0 + g.plane_off) * g.plane_stride;
     const int rc = m.send ? nccl_shim_send(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, stream, &emsg)
                           : nccl_shim_recv(ctx->nccl_comm, ptr, (size_t)m.count, m.peer, stream, &emsg);
     if (rc) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
@@ -1348,6 +1434,7 @@ bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count)
     return BTE_OK;
   }
   if (which != 0 && which != 1) return fail(ctx, BTE_EINVAL, "which must be 0..3");
+  if (ctx->rot) return fail(ctx, BTE_EINVAL, "sub-step 0/1 would overwrite the state under octant-slot rotation");
   const size_t want = which == 0 ? (size_t)ncl * ctx->nd * ctx->nb : (size_t)ncl * ctx->nb;
   if (count != want) return fail(ctx, BTE_EINVAL, "count mismatch");
   double *Iin = ctx->I[ctx->cur];
@@ -1421,6 +1508,7 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
   out->b1 = ctx->b0 + ctx->nb;
   out->nb_total = ctx->nbT;
   out->band = ctx->band;
+  out->rotate = ctx->rot;
   return BTE_OK;
 }
 

@@ -74,6 +74,11 @@ struct Geometry {
   const double *ws;
   int kind[6];
   const double *gtab[6];  // iso / diffuse ghost tables [face][nb] (global face index)
+  // where each octant slot of the CURRENT intensity buffer starts (doubles):
+  // slot * slot_stride, or a rotated region under octant-slot rotation
+  int64_t slot_off[kMaxSlots];
+  int rot;                // octant-slot rotation: specular ghosts come from gspec snapshots
+  const double *gspec[6]; // rot: [face][slot][j][nb] snapshot of the reflected I^n (specular walls)
   double diff_den[6];
 };
 
@@ -121,6 +126,8 @@ struct SweepArgs {
   int l2hint;             // bulk-copy L2 policies: 0 none, 1 last-use evict-first, 2 + own evict-last
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int col0, ncols;        // column range of this launch (ncols = 0: all)
+  int slot0, nslots;      // octant slots of this launch (nslots = 0: all)
+  int64_t out_off[kMaxSlots];  // where slot s of I^{n+1} goes in Iout
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
   NewtonArgs nw;          // fused a3+a4 (k_sweep_tma tail)
   int fuse_newton;
@@ -133,6 +140,7 @@ cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused);
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
                            cudaStream_t s);
+cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s);
 cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,
                              cudaStream_t s);
 cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c,

@@ -63,6 +63,8 @@ __device__ __forceinline__ double ghost_value(const Geometry &g, const double *_
                                               int region, int64_t face, int64_t cell_base, int slot,
                                               int j, int b) {
   const int kind = g.kind[region];
+  if (kind == BC_SPEC && g.rot)  // slot rotation: the reflected octant may be overwritten; snapshot
+    return ldg(g.gspec[region] + ((face * g.nslot + slot) * g.nj + j) * g.nb + b);
   if (kind == BC_SPEC) {
     const int axis = region >> 1;
     const int64_t off = g.refl_off[(int64_t)axis * g.nslot * g.nj + slot * g.nj + j];
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   double *coef = sm;
   double *red = sm + 4 * nj;
 
-  const int slot = blockIdx.y;
+  const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
   const int col = A.col0 + blockIdx.x;
   const int x = (DIM == 3) ? col % g.nx : col;
@@ -136,8 +138,8 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
   int p = mneg ? pe - 1 : pb;
 
   const double *__restrict__ Iin = A.Iin;
-  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
-  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + A.out_off[slot];
   const int64_t colE = (int64_t)col * Es;
   const double dt = A.dt;
   const double v = A.v[b];
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const int nloc = max(0, min(A.jpt, nj - j0));
   const bool active = grp < JG;
 
-  const int slot = blockIdx.y;
+  const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
   const int col = A.col0 + blockIdx.x;
   const int x = (DIM == 3) ? col % g.nx : col;
@@ -339,8 +341,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const int pfirst = mneg ? pe - 1 : pb;
 
   const double *__restrict__ Iin = A.Iin;
-  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
-  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + A.out_off[slot];
   const int64_t colE = (int64_t)col * Es;
   const double dt = A.dt;
 
@@ -531,7 +533,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tmx(const SweepArgs A) {
   const int j0 = grp * A.jpt;
   const int nloc = max(0, min(A.jpt, nj - j0));
 
-  const int slot = blockIdx.y;
+  const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
   const int ngx = (g.nx + TX - 1) / TX;
   const int gx = blockIdx.x % ngx;
@@ -578,8 +580,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tmx(const SweepArgs A) {
   const int pfirst = mneg ? pe - 1 : pb;
 
   const double *__restrict__ Iin = A.Iin;
-  const double *__restrict__ Is = A.Iin + (int64_t)slot * g.slot_stride;
-  double *__restrict__ Os = A.Iout + (int64_t)slot * g.slot_stride;
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + A.out_off[slot];
   const double dt = A.dt;
 
   auto issue = [&](int i, int st) {
@@ -729,7 +731,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     a.p_hi = g.nplanes;
   }
   const int nseg = (a.p_hi - a.p_lo + a.seg_len - 1) / a.seg_len;
-  dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, g.nslot, nseg);
+  dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, a.nslots > 0 ? a.nslots : g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.Es % 2 == 0);
   // small blocks: several columns per CTA (k_sweep_tmx)
@@ -755,7 +757,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
       a.stage_doubles = sdx;
       const size_t smem = fixedx + (size_t)S * sdx * sizeof(double);
       const int ngx = (g.nx + TX - 1) / TX;
-      dim3 gridx(ngx * (DIM == 3 ? g.ny : 1), g.nslot, nseg);
+      dim3 gridx(ngx * (DIM == 3 ? g.ny : 1), a.nslots > 0 ? a.nslots : g.nslot, nseg);
       const int jc = jp <= 1 ? 1 : jp <= 2 ? 2 : jp <= 4 ? 4 : jp <= 5 ? 5 : jp <= 8 ? 8 : 16;
       switch (jc) {
 #define BTE_TMX(N)                                                                                  \
@@ -862,45 +864,58 @@ cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused) {
 
 // g_b = [octant tree of sum_{j in outgoing octant} w_j|s_a| I_{j,b}] / den (reading #11).
 // One CTA per boundary face of this rank; threads over channels.
-__global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
-                          double *__restrict__ gtab) {
+// Boundary face lf (0.. this rank's faces of `region`) -> global face index
+// (the ghost-table row) and the (plane, cross) offset of its boundary cell.
+__device__ __forceinline__ void wall_face(const Geometry &g, int region, int64_t lf, int64_t *face,
+                                          int64_t *cell_base) {
   const int axis = region >> 1;
   const bool hi = region & 1;
-  const int64_t lf = blockIdx.x;
   int x = 0, y = 0, p = 0;
-  int64_t face;
-  const bool march = (axis == g.dim - 1);
   if (g.dim == 3) {
     if (axis == 0) {
       y = (int)(lf % g.ny);
       p = (int)(lf / g.ny);
       x = hi ? g.nx - 1 : 0;
-      face = y + (int64_t)g.ny * (g.m0 + p);
+      *face = y + (int64_t)g.ny * (g.m0 + p);
     } else if (axis == 1) {
       x = (int)(lf % g.nx);
       p = (int)(lf / g.nx);
       y = hi ? g.ny - 1 : 0;
-      face = x + (int64_t)g.nx * (g.m0 + p);
+      *face = x + (int64_t)g.nx * (g.m0 + p);
     } else {
       x = (int)(lf % g.nx);
       y = (int)(lf / g.nx);
       p = hi ? g.nplanes - 1 : 0;
-      face = x + (int64_t)g.nx * y;
+      *face = x + (int64_t)g.nx * y;
     }
   } else {
     if (axis == 0) {
       p = (int)lf;
       x = hi ? g.nx - 1 : 0;
-      face = g.m0 + p;
+      *face = g.m0 + p;
     } else {
       x = (int)lf;
       p = hi ? g.nplanes - 1 : 0;
-      face = x;
+      *face = x;
     }
   }
-  (void)march;
   const int64_t cross = (g.dim == 3) ? x + (int64_t)g.nx * y : x;
-  const int64_t cell_base = (int64_t)(p + g.plane_off) * g.plane_stride + cross * g.Es;
+  *cell_base = (int64_t)(p + g.plane_off) * g.plane_stride + cross * g.Es;
+}
+
+static int64_t wall_faces_local(const Geometry &g, int region) {
+  const int axis = region >> 1;
+  if (g.dim == 3)
+    return axis == 0 ? (int64_t)g.ny * g.nplanes : (axis == 1 ? (int64_t)g.nx * g.nplanes : (int64_t)g.nx * g.ny);
+  return axis == 0 ? g.nplanes : g.nx;
+}
+
+__global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
+                          double *__restrict__ gtab) {
+  const int axis = region >> 1;
+  const bool hi = region & 1;
+  int64_t face, cell_base;
+  wall_face(g, region, blockIdx.x, &face, &cell_base);
   // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
   const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
@@ -912,7 +927,7 @@ __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int re
       double acc = 0.0;
       if (sl >= 0 && out) {
         const double *ws = g.ws + (int64_t)axis * g.nslot * g.nj + (int64_t)sl * g.nj;
-        const double *Ip = I + (int64_t)sl * g.slot_stride + cell_base + b;
+        const double *Ip = I + g.slot_off[sl] + cell_base + b;
         for (int j = 0; j < g.nj; ++j) acc += ws[j] * Ip[(int64_t)j * g.nb];
       }
       q[o] = acc;
@@ -924,16 +939,42 @@ __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int re
 
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
                            cudaStream_t s) {
-  const int axis = region >> 1;
-  int64_t nf;
-  if (g.dim == 3)
-    nf = axis == 0 ? (int64_t)g.ny * g.nplanes : (axis == 1 ? (int64_t)g.nx * g.nplanes : (int64_t)g.nx * g.ny);
-  else
-    nf = axis == 0 ? g.nplanes : g.nx;
+  const int64_t nf = wall_faces_local(g, region);
   if (nf == 0) return cudaSuccess;
   int threads = ((g.nb + 31) / 32) * 32;
   if (threads > 256) threads = 256;
   k_diffuse<<<(unsigned)nf, threads, 0, s>>>(g, I, region, gtab);
+  return cudaGetLastError();
+}
+
+// Octant-slot rotation: specular ghosts read the reflected
+// octant, whose slot may already hold I^{n+1} or another octant when this
+// octant is swept, so the boundary pass snapshots them from I^n first:
+// out[face][slot][j][b] = I^n of the boundary cell at the reflection of (slot, j).
+__global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, int region,
+                                double *__restrict__ out) {
+  const int axis = region >> 1;
+  int64_t face, cell_base;
+  wall_face(g, region, blockIdx.x, &face, &cell_base);
+  const int nsj = g.nslot * g.nj;
+  // only directions entering through this wall read a ghost: s_a >= 0 on the
+  // low wall (octant bit clear), s_a < 0 on the high wall
+  const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
+  const bool hi = region & 1;
+  for (int e = threadIdx.x; e < nsj * g.nb; e += blockDim.x) {
+    const int sj = e / g.nb, b = e - sj * g.nb;
+    const int oct = g.slot_oct[sj / g.nj];
+    if (hi ? !(oct & bit) : (oct & bit)) continue;
+    const int64_t off = g.refl_off[(int64_t)axis * nsj + sj];  // slot_r * slot_stride + jr * nb
+    const int64_t sr = off / g.slot_stride;
+    out[face * nsj * g.nb + e] = I[g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base + b];
+  }
+}
+
+cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s) {
+  const int64_t nf = wall_faces_local(g, region);
+  if (nf == 0) return cudaSuccess;
+  k_spec_snapshot<<<(unsigned)nf, 256, 0, s>>>(g, I, region, out);
   return cudaGetLastError();
 }
 
@@ -1364,7 +1405,7 @@ __global__ void k_fill_eq(const Geometry g, const double *__restrict__ I0c, doub
   const int64_t cell = r / g.E;
   const int e = (int)(r - cell * g.E);
   const int b = e % g.nb;
-  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] = I0c[cell * g.nb + b];
+  I[g.slot_off[sl] + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] = I0c[cell * g.nb + b];
 }
 
 cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I, cudaStream_t s) {
@@ -1391,7 +1432,7 @@ __global__ void k_permute(const Geometry g, const int *__restrict__ dmap, int nd
   const int64_t c = c0 + cr;
   const int64_t p = c / g.ncross;
   const int64_t cross = c - p * g.ncross;
-  const int64_t dst = sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es +
+  const int64_t dst = g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es +
                       (int64_t)j * g.nb + b;
   if (to_layout)
     I[dst] = canon[i];
@@ -1463,7 +1504,7 @@ __global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, in
   const int64_t cg = g.m0 * g.ncross + cell;
   const uint64_t idx = ((uint64_t)cg * nd + d) * g.nbT + g.b0 + b;
   const double u = (double)(splitmix64(seed ^ idx) >> 11) * 0x1.0p-53;
-  I[sl * g.slot_stride + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] =
+  I[g.slot_off[sl] + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] =
       I0c[cell * g.nb + b] * (1.0 + amp * (2.0 * u - 1.0));
 }
 
@@ -1505,7 +1546,7 @@ __global__ void k_dpart_from_I(const Geometry g, const double *__restrict__ I, c
   const int sl = (int)((i / g.nb) % g.nslot);
   const int64_t c = i / ((int64_t)g.nb * g.nslot);
   const int64_t p = c / g.ncross, cross = c - p * g.ncross;
-  const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es + b;
+  const double *Ip = I + g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es + b;
   const double i0 = I0c[c * g.nb + b];
   double s = 0.0;
   for (int j = 0; j < g.nj; ++j) s += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] * (i0 - Ip[(int64_t)j * g.nb]);
@@ -1560,7 +1601,7 @@ __global__ void k_energy(const Geometry g, const double *__restrict__ I, const d
   const int64_t p = c / g.ncross, cross = c - p * g.ncross;
   double acc = 0.0;
   for (int sl = 0; sl < g.nslot; ++sl) {
-    const double *Ip = I + sl * g.slot_stride + (p + g.plane_off) * g.plane_stride + cross * g.Es;
+    const double *Ip = I + g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es;
     for (int e = lane; e < g.E; e += 32) {
       const int j = e / g.nb, b = e - j * g.nb;
       acc += g.coef[(int64_t)(sl * g.nj + j) * 4 + 3] / v[b] * Ip[e];

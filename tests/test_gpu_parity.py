@@ -610,3 +610,73 @@ def test_band_init_random_and_tables(Solver):
     finally:
         for sv in group:
             sv.close()
+
+
+# ----------------------------------------------------------------- octant-slot rotation
+
+@pytest.mark.parametrize("case", ["small3d", "3d", "2d"])
+def test_slot_rotation_bit_exact(Solver, case, monkeypatch):
+    """One buffer of nslot + 1 regions (each octant swept into the spare region,
+    specular ghosts snapshotted first) gives the two-buffer result bit for bit;
+    state I/O, energy and the random start go through the slot map."""
+    p = bi.small_3d(7, 5, 6) if case == "small3d" else _group_case(case)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    res = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("BTE_ROTATE", rot)
+        with Solver.from_problem(p) as sv:
+            assert sv.rotate == (rot == "1")
+            sv.set_state(I, T)
+            sv.step(3)
+            sv.step(4)
+            E = sv.energy()
+            Ig, Tg = sv.intensity(), sv.temperature()
+            sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+            sv.step(2)
+            Ir = sv.intensity()
+        res[rot] = (Ig, Tg, E, Ir)
+    a, b = res["0"], res["1"]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    assert np.array_equal(a[3], b[3])
+    Io, To, _, _ = o.run(I, T, 7)
+    rel, dT = _cmp(b[0], b[1], Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_slot_rotation_groups(Solver, monkeypatch):
+    """Rotation under the slab group (halo planes follow the slot map) and the
+    band group: bit-exact against the same groups without rotation."""
+    p = _group_case("3d")
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    out = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("BTE_ROTATE", rot)
+        group = []
+        try:
+            for r in range(2):
+                sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=2)
+                group.append(sv)
+                for reg in range(6):
+                    bc = p.bcs[reg]
+                    sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+                ncross = sv.ncells // sv.nz_local
+                c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+                sv.set_state(I[c0:c1], T[c0:c1])
+            Solver.group_step(group, 5)
+            slab = (np.concatenate([sv.intensity() for sv in group]),
+                    np.concatenate([sv.temperature() for sv in group]))
+        finally:
+            for sv in group:
+                sv.close()
+        bgroup = _band_group(Solver, p, 2, I, T)
+        try:
+            Solver.group_step(bgroup, 5)
+            band = (np.concatenate([sv.intensity() for sv in bgroup], axis=2), bgroup[0].temperature())
+        finally:
+            for sv in bgroup:
+                sv.close()
+        out[rot] = slab + band
+    for x, y in zip(out["0"], out["1"]):
+        assert np.array_equal(x, y)
