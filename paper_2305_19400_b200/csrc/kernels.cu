@@ -952,29 +952,40 @@ cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, doubl
 // octant is swept, so the boundary pass snapshots them from I^n first:
 // out[face][slot][j][b] = I^n of the boundary cell at the reflection of (slot, j).
 __global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, int region,
-                                double *__restrict__ out) {
+                                double *__restrict__ out, const int4 ins_lo, const int4 ins_hi) {
   const int axis = region >> 1;
   int64_t face, cell_base;
   wall_face(g, region, blockIdx.x, &face, &cell_base);
+  // blockIdx.y: the y-th slot whose directions enter through this wall
+  // (s_a >= 0 on the low wall, s_a < 0 on the high wall; host-built list)
+  const int k = blockIdx.y;
+  const int slot = k < 4 ? (k == 0 ? ins_lo.x : k == 1 ? ins_lo.y : k == 2 ? ins_lo.z : ins_lo.w)
+                         : (k == 4 ? ins_hi.x : k == 5 ? ins_hi.y : k == 6 ? ins_hi.z : ins_hi.w);
   const int nsj = g.nslot * g.nj;
-  // only directions entering through this wall read a ghost: s_a >= 0 on the
-  // low wall (octant bit clear), s_a < 0 on the high wall
-  const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
-  const bool hi = region & 1;
-  for (int e = threadIdx.x; e < nsj * g.nb; e += blockDim.x) {
-    const int sj = e / g.nb, b = e - sj * g.nb;
-    const int oct = g.slot_oct[sj / g.nj];
-    if (hi ? !(oct & bit) : (oct & bit)) continue;
-    const int64_t off = g.refl_off[(int64_t)axis * nsj + sj];  // slot_r * slot_stride + jr * nb
+  const int64_t *ro = g.refl_off + (int64_t)axis * nsj + (int64_t)slot * g.nj;
+  double *o = out + (face * g.nslot + slot) * (int64_t)g.E;
+  for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
+    const int j = e / g.nb, b = e - j * g.nb;
+    const int64_t off = ro[j];  // slot_r * slot_stride + jr * nb
     const int64_t sr = off / g.slot_stride;
-    out[face * nsj * g.nb + e] = I[g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base + b];
+    o[e] = I[g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base + b];
   }
 }
 
 cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s) {
   const int64_t nf = wall_faces_local(g, region);
   if (nf == 0) return cudaSuccess;
-  k_spec_snapshot<<<(unsigned)nf, 256, 0, s>>>(g, I, region, out);
+  const int axis = region >> 1, bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
+  const bool hi = region & 1;
+  int ins[8] = {0, 0, 0, 0, 0, 0, 0, 0}, nin = 0;
+  for (int sl = 0; sl < g.nslot; ++sl) {
+    const int oct = g.slot_oct[sl];
+    if (hi ? (oct & bit) : !(oct & bit)) ins[nin++] = sl;  // entering through this wall
+  }
+  if (nin == 0) return cudaSuccess;
+  const int thr = std::min(256, (g.E + 31) / 32 * 32);
+  k_spec_snapshot<<<dim3((unsigned)nf, (unsigned)nin), thr, 0, s>>>(
+      g, I, region, out, make_int4(ins[0], ins[1], ins[2], ins[3]), make_int4(ins[4], ins[5], ins[6], ins[7]));
   return cudaGetLastError();
 }
 
