@@ -27,6 +27,7 @@ KB = 1.380649e-23  # J / K
 BC_ISOTHERMAL = 0
 BC_SPECULAR = 1
 BC_DIFFUSE = 2
+BC_PARTIAL = 3  # partially specular: specularity*specular + (1 - specularity)*diffuse
 
 I0_LINEAR = 0
 I0_BOSE_EINSTEIN = 1
@@ -110,6 +111,7 @@ class WallBC:
     kind: int
     T_wall: Optional[np.ndarray] = None  # per boundary face (isothermal only)
     T_uniform: float = 300.0
+    specularity: float = 1.0  # BC_PARTIAL only, in [0, 1]
 
 
 @dataclasses.dataclass

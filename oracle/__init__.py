@@ -50,6 +50,7 @@ class _Problem(C.Structure):
         ("dt", C.c_double),
         ("bc_kind", C.c_int * 6), ("T_wall", C.c_void_p * 6), ("T_uniform", C.c_double * 6),
         ("nthreads", C.c_int),
+        ("specularity", C.c_double * 6),
     ]
 
 
@@ -137,6 +138,7 @@ class Oracle:
             st.bc_kind[r] = bc.kind
             st.T_wall[r] = _ptr(keep(bc.T_wall)) if bc.T_wall is not None else None
             st.T_uniform[r] = bc.T_uniform
+            st.specularity[r] = getattr(bc, "specularity", 1.0)
         st.nthreads = nthreads if nthreads else (os.cpu_count() or 1)
         self._st = st
         self.nc, self.nd, self.nb = m.ncells, d.nd, b.nb

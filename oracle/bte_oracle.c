@@ -48,6 +48,7 @@
 #define BC_ISO 0
 #define BC_SPEC 1
 #define BC_DIFF 2
+#define BC_PART 3 /* partially specular (reading R-i) */
 
 #define HBAR 1.054571817e-34
 #define KB 1.380649e-23
@@ -76,6 +77,7 @@ typedef struct {
   const double *T_wall[6]; /* per face or NULL */
   double T_uniform[6];
   int nthreads;
+  double specularity[6]; /* BC_PART: fraction p of specular reflection */
 } ora_problem;
 
 /* ---------------------------------------------------------------- quadrature */
@@ -338,6 +340,13 @@ static int bc_prepare(const ora_problem *p, ora_bcdata *bd) {
       if (!(bd->den[r] > 0.0)) return ORA_EINVAL;
     } else if (p->bc_kind[r] == BC_SPEC) {
       if (ora_reflection(p, r / 2, bd->refl[r / 2]) != ORA_OK) return ORA_ENOTCLOSED;
+    } else if (p->bc_kind[r] == BC_PART) {
+      if (!(p->specularity[r] >= 0.0 && p->specularity[r] <= 1.0)) return ORA_EINVAL;
+      if (ora_reflection(p, r / 2, bd->refl[r / 2]) != ORA_OK) return ORA_ENOTCLOSED;
+      bd->gdiff[r] = (double *)malloc(sizeof(double) * nf * p->nb);
+      if (!bd->gdiff[r]) return ORA_ENOMEM;
+      bd->den[r] = diffuse_den(p, r);
+      if (!(bd->den[r] > 0.0)) return ORA_EINVAL;
     } else {
       return ORA_EINVAL;
     }
@@ -359,7 +368,13 @@ static double ghost(const ora_problem *p, const ora_bcdata *bd, int region, long
   int k = p->bc_kind[region];
   if (k == BC_ISO) return bd->giso[region][f * p->nb + b];
   if (k == BC_DIFF) return bd->gdiff[region][f * p->nb + b];
-  return I[(c * p->nd + bd->refl[region / 2][d]) * p->nb + b];
+  double spec = I[(c * p->nd + bd->refl[region / 2][d]) * p->nb + b];
+  if (k == BC_PART) {
+    /* reading R-i: Ziman/Soffer specularity mixing of the two adiabatic ghosts */
+    double sp = p->specularity[region];
+    return sp * spec + (1.0 - sp) * bd->gdiff[region][f * p->nb + b];
+  }
+  return spec;
 }
 
 /* Sweep (Eq. 5 with forward Euler, Eqs. 2-3):
@@ -517,7 +532,7 @@ int ora_sweep(const ora_problem *p, const double *I, const double *I0c, const do
   }
   int nreg = p->dim == 3 ? 6 : 4;
   for (int r = 0; r < nreg; r++)
-    if (p->bc_kind[r] == BC_DIFF) diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
+    if (p->bc_kind[r] == BC_DIFF || p->bc_kind[r] == BC_PART) diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
   ora_sweep_bd(p, &bd, I, I0c, betac, Iout);
   bc_free(&bd);
   return ORA_OK;
@@ -566,7 +581,7 @@ int ora_run(const ora_problem *p, double *I, double *T, double *I0c, double *bet
   if (err_cell) *err_cell = -1;
   for (long s = 0; s < nsteps && st == ORA_OK; s++) {
     for (int r = 0; r < nreg; r++)
-      if (p->bc_kind[r] == BC_DIFF) diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
+      if (p->bc_kind[r] == BC_DIFF || p->bc_kind[r] == BC_PART) diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
     ora_sweep_bd(p, &bd, I, I0c, betac, J);
     ora_reduce(p, J, I0c, D);
     long bad;

@@ -506,3 +506,58 @@ def test_diffusive_slab_fourier():
     k = a * d.w.sum() * p.bands.v[0] * tau * (d.w * d.s[:, 0] ** 2).sum() / d.w.sum()
     ratio = q[mid].mean() / (-k * fit[0])
     assert abs(ratio - 1) < 1e-3, ratio
+
+
+# ----------------------------------------------------------------- partially specular walls (reading R-i)
+
+def _partial_case(spec, kinds=None):
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    bcs = [bi.WallBC(bi.BC_PARTIAL, specularity=spec), bi.WallBC(bi.BC_PARTIAL, specularity=spec),
+           bi.WallBC(bi.BC_ISOTHERMAL, None, 305.0), bi.WallBC(bi.BC_PARTIAL, specularity=spec),
+           bi.WallBC(bi.BC_PARTIAL, specularity=spec), bi.WallBC(bi.BC_ISOTHERMAL, None, 298.0)]
+    if kinds is not None:
+        bcs = [bi.WallBC(k) if bc.kind == bi.BC_PARTIAL else bc for bc, k in zip(bcs, kinds)]
+    return bi.small_3d(6, 5, 4, bands=b, bcs=bcs)
+
+
+@pytest.mark.parametrize("spec,kind", [(1.0, bi.BC_SPECULAR), (0.0, bi.BC_DIFFUSE)])
+def test_partial_wall_limits_bitexact(spec, kind):
+    """Specularity 1 is the specular wall and 0 the diffuse wall, bit for bit
+    (p*I_r + (1-p)*g reduces exactly), over a multi-step run."""
+    pp = _partial_case(spec)
+    pk = _partial_case(spec, kinds=[kind] * 6)
+    o1, o2 = oracle.Oracle(pp), oracle.Oracle(pk)
+    I, T = o1.random_state()
+    Ia, Ta, _, _ = o1.run(I, T, 5)
+    Ib, Tb, _, _ = o2.run(I, T, 5)
+    assert np.array_equal(Ia, Ib) and np.array_equal(Ta, Tb)
+
+
+def test_partial_wall_sweep_is_affine_in_specularity():
+    """The sweep is affine in the ghost value, so one sweep with specularity p
+    equals p*sweep(specular) + (1-p)*sweep(diffuse) up to rounding -- a check
+    of the mixing formula independent of how it is coded."""
+    p = 0.37
+    cases = [_partial_case(p), _partial_case(1.0), _partial_case(0.0)]
+    oracles = [oracle.Oracle(c) for c in cases]
+    I, T = oracles[0].random_state()
+    I0c, betac = oracles[0].refresh(T)
+    Jp, J1, J0 = (o.sweep(I, I0c, betac) for o in oracles)
+    mix = p * J1 + (1 - p) * J0
+    assert np.max(np.abs(Jp - mix) / np.abs(Jp)) < 1e-14
+    assert np.max(np.abs(J1 - J0) / np.abs(J0)) > 1e-8  # the two limits do differ here
+
+
+def test_partial_wall_closed_box_conservation():
+    """All walls partially specular (p = 0.4): both components are adiabatic,
+    so the energy of a closed box stays constant."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    bcs = [bi.WallBC(bi.BC_PARTIAL, specularity=0.4) for _ in range(6)]
+    p = bi.small_3d(6, 5, 4, bands=b, bcs=bcs, dirs=bi.directions_control_angle(4, 16))
+    o = oracle.Oracle(p)
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)
+    E0 = o.energy(I)
+    I2, _, _, _ = o.run(I, T, 500, I0c, betac)
+    assert abs(o.energy(I2) / E0 - 1) < 1e-12
+    assert I2.min() > 0
