@@ -70,8 +70,11 @@ typedef enum {
   BTE_BC_ISOTHERMAL = 0, /* ghost = I0_b(T_wall(face)) for incoming d (Eq. 6 case 1) */
   BTE_BC_SPECULAR = 1,   /* ghost = I_{r(d),b} of the boundary cell (Eq. 6 case 2;  */
                          /* "symmetry" walls of the paper)                          */
-  BTE_BC_DIFFUSE = 2     /* adiabatic diffuse wall: ghost_b = sum_out w|s_a| I /     */
+  BTE_BC_DIFFUSE = 2,    /* adiabatic diffuse wall: ghost_b = sum_out w|s_a| I /     */
                          /* sum_in w|s_a|, same for every incoming d (reading #11)  */
+  BTE_BC_PARTIAL = 3     /* partially specular adiabatic wall (SURVEY 8(f) f4,      */
+                         /* DESIGN reading R-i): ghost = p*I_{r(d),b} + (1-p)*the   */
+                         /* diffuse ghost; set with bte_set_bc_partial              */
 } bte_bc_kind;
 
 typedef enum {
@@ -175,6 +178,18 @@ BTE_API bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, c
  * reflections are not in the set), BTE_EUNSTABLE (T_wall raises beta_max past
  * the dt bound). */
 BTE_API bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, double T_uniform);
+
+/* Partially specular adiabatic wall on region 0..5 (the
+ * paper has only isothermal and symmetry walls, Eq. 6, so this is
+ * reading R-i of DESIGN.md): for each incoming direction d and channel b
+ *   ghost = p * I^n_{r(d),b} + (1 - p) * [sum_out w|s_a| I^n_b / sum_in w|s_a|]
+ * (products rounded separately, then added: no FMA), i.e. the Ziman/Soffer
+ * specularity-weighted mix of BTE_BC_SPECULAR and BTE_BC_DIFFUSE.  Zero net
+ * energy flux per channel for any p.  p = 1 and p = 0 reproduce the specular
+ * and diffuse walls bit for bit.
+ * Errors: BTE_EINVAL (region, p outside [0, 1] or NaN, no direction crosses
+ * the wall), BTE_ENOTCLOSED (reflections of the set not in the set). */
+BTE_API bte_status bte_set_bc_partial(bte_ctx *ctx, int region, double specularity);
 
 /* Replace the state from host arrays (canonical orders, this rank's slab).
  *  I != NULL, T != NULL : I and T as given; I0c = I0(T), beta = beta(T).

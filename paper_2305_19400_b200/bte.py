@@ -20,10 +20,10 @@ LIB_PATH = os.environ.get("BTE_LIB") or os.path.join(_HERE, "libbte.so")  # BTE_
 BTE_OK = 0
 STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE_ENCCL",
           5: "BTE_EUNSTABLE", 6: "BTE_ENOTCLOSED", 7: "BTE_ENEWTON", 8: "BTE_ENONFINITE"}
-BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE = 0, 1, 2
+BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE, BC_PARTIAL = 0, 1, 2, 3
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_set_bc", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -105,6 +105,8 @@ def load_library(path: str = LIB_PATH):
         lib.bte_create_band.argtypes = lib.bte_create.argtypes
         lib.bte_plan_band.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
+    if hasattr(lib, "bte_set_bc_partial"):
+        lib.bte_set_bc_partial.argtypes = [P, C.c_int, C.c_double]
     lib.bte_set_state.argtypes = [P, dp, dp]
     lib.bte_init_random.argtypes = [P, C.c_uint64, dp, C.c_double, C.c_double, C.c_double]
     lib.bte_step.argtypes = [P, C.c_int64]
@@ -222,8 +224,7 @@ class Solver:
         sv = cls(problem.mesh, problem.dirs, problem.bands, problem.dt, problem.T_init, **kw)
         nreg = 6 if problem.mesh.dim == 3 else 4
         for r in range(nreg):
-            bc = problem.bcs[r]
-            sv.set_bc(r, bc.kind, bc.T_wall, bc.T_uniform)
+            sv.set_wall(r, problem.bcs[r])
         return sv
 
     def _err(self) -> str:
@@ -236,9 +237,16 @@ class Solver:
             raise BteError(st, self._err())
 
     # ---------------------------------------------------------------- API
-    def set_bc(self, region: int, kind: int, T_wall=None, T_uniform: float = 300.0):
+    def set_bc(self, region: int, kind: int, T_wall=None, T_uniform: float = 300.0, specularity: float = 1.0):
+        if int(kind) == BC_PARTIAL:
+            self._check(self._lib.bte_set_bc_partial(self._h, int(region), float(specularity)))
+            return
         Tw = _f64(T_wall)
         self._check(self._lib.bte_set_bc(self._h, int(region), int(kind), _p(Tw), float(T_uniform)))
+
+    def set_wall(self, region: int, bc) -> None:
+        """Apply a wall description (kind, T_wall, T_uniform[, specularity])."""
+        self.set_bc(region, bc.kind, bc.T_wall, bc.T_uniform, getattr(bc, "specularity", 1.0))
 
     def set_state(self, I=None, T=None):
         I, T = _f64(I), _f64(T)

@@ -757,10 +757,29 @@ bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, 
   } else if (kind == BTE_BC_DIFFUSE) {
     if (!(ctx->g.diff_den[region] > 0))
       return fail(ctx, BTE_EINVAL, "diffuse wall %d: no direction crosses it", region);
+  } else if (kind == BTE_BC_PARTIAL) {
+    return fail(ctx, BTE_EINVAL, "partially specular wall %d: use bte_set_bc_partial", region);
   } else {
     return fail(ctx, BTE_EINVAL, "unknown boundary kind %d", kind);
   }
   ctx->g.kind[region] = kind;
+  return BTE_OK;
+}
+
+bte_status bte_set_bc_partial(bte_ctx *ctx, int region, double specularity) {
+  if (!ctx) return BTE_EINVAL;
+  const int nreg = ctx->mesh.dim == 3 ? 6 : 4;
+  if (region < 0 || region >= nreg) return fail(ctx, BTE_EINVAL, "region %d out of range", region);
+  if (!(specularity >= 0.0 && specularity <= 1.0))
+    return fail(ctx, BTE_EINVAL, "specularity must lie in [0, 1] (got %g)", specularity);
+  if (!ctx->refl_closed[region / 2])
+    return fail(ctx, BTE_ENOTCLOSED, "partial wall %d: direction set is not closed under the axis-%d reflection",
+                region, region / 2);
+  if (!(ctx->g.diff_den[region] > 0))
+    return fail(ctx, BTE_EINVAL, "partial wall %d: no direction crosses it", region);
+  ctx->g.spec_p[region] = specularity;
+  ctx->g.spec_q[region] = 1.0 - specularity;
+  ctx->g.kind[region] = BC_PART;
   return BTE_OK;
 }
 
@@ -855,10 +874,11 @@ static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
   for (int r = 0; r < nreg; ++r) {
     const int a = r / 2;
     if (a == g.dim - 1 && !((r & 1) ? g.has_hi_wall : g.has_lo_wall)) continue;
-    if (g.kind[r] == BC_DIFF) {
+    if (g.kind[r] == BC_DIFF || g.kind[r] == BC_PART) {
       CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
       ++n;
-    } else if (g.kind[r] == BC_SPEC && ctx->rot) {
+    }
+    if ((g.kind[r] == BC_SPEC || g.kind[r] == BC_PART) && ctx->rot) {
       if (!ctx->gspec[r]) {  // first use: [faces][nslot*nj][nb]
         const size_t bytes = (size_t)n_faces_global(ctx, r) * g.nslot * g.nj * g.nb * sizeof(double);
         ctx->gspec[r] = (double *)dev_alloc(ctx, bytes);
@@ -879,7 +899,8 @@ static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
 static int n_diffuse(const bte_ctx *ctx) {
   int n = 0;
   for (int r = 0; r < (ctx->g.dim == 3 ? 6 : 4); ++r)
-    n += ctx->g.kind[r] == BC_DIFF || (ctx->rot && ctx->g.kind[r] == BC_SPEC);
+    n += ctx->g.kind[r] == BC_DIFF || ctx->g.kind[r] == BC_PART ||
+         (ctx->rot && ctx->g.kind[r] == BC_SPEC);
   return n;
 }
 

@@ -24,7 +24,7 @@ constexpr double kTlo = 1.0, kThi = 5000.0;  // Newton bracket (reading #18)
 constexpr int kNewtonMaxIt = 50;
 constexpr double kNewtonRtol = 1e-13;
 
-enum { BC_ISO = 0, BC_SPEC = 1, BC_DIFF = 2 };
+enum { BC_ISO = 0, BC_SPEC = 1, BC_DIFF = 2, BC_PART = 3 };
 enum { ERR_NONE = 0, ERR_NEWTON = 7, ERR_NONFINITE = 8 };
 
 // Channel model tables (device pointers).
@@ -80,6 +80,7 @@ struct Geometry {
   int rot;                // octant-slot rotation: specular ghosts come from gspec snapshots
   const double *gspec[6]; // rot: [face][slot][j][nb] snapshot of the reflected I^n (specular walls)
   double diff_den[6];
+  double spec_p[6], spec_q[6];  // BC_PART: specularity p and 1 - p (rounded on the host)
 };
 
 struct NewtonArgs {

@@ -63,14 +63,18 @@ __device__ __forceinline__ double ghost_value(const Geometry &g, const double *_
                                               int region, int64_t face, int64_t cell_base, int slot,
                                               int j, int b) {
   const int kind = g.kind[region];
-  if (kind == BC_SPEC && g.rot)  // slot rotation: the reflected octant may be overwritten; snapshot
-    return ldg(g.gspec[region] + ((face * g.nslot + slot) * g.nj + j) * g.nb + b);
-  if (kind == BC_SPEC) {
+  if (kind == BC_ISO || kind == BC_DIFF) return ldg(g.gtab[region] + face * g.nb + b);
+  double spec;
+  if (g.rot) {  // slot rotation: the reflected octant may be overwritten; snapshot
+    spec = ldg(g.gspec[region] + ((face * g.nslot + slot) * g.nj + j) * g.nb + b);
+  } else {
     const int axis = region >> 1;
     const int64_t off = g.refl_off[(int64_t)axis * g.nslot * g.nj + slot * g.nj + j];
-    return ldg(Iin + off + cell_base + b);
+    spec = ldg(Iin + off + cell_base + b);
   }
-  return ldg(g.gtab[region] + face * g.nb + b);
+  if (kind == BC_SPEC) return spec;
+  // BC_PART (reading R-i): p*I_r + (1-p)*g_diffuse, products rounded separately
+  return __dadd_rn(__dmul_rn(g.spec_p[region], spec), __dmul_rn(g.spec_q[region], ldg(g.gtab[region] + face * g.nb + b)));
 }
 
 // Element update shared by both sweeps.  Flux in axis order x, y, z (per-axis

@@ -430,7 +430,7 @@ def test_local_slab_group_matches_single_domain(Solver, case, P, overlap, monkey
             sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=P)
             for reg in range(6 if p.mesh.dim == 3 else 4):
                 bc = p.bcs[reg]
-                sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+                sv.set_wall(reg, bc)
             ncross = sv.ncells // sv.nz_local
             c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
             sv.set_state(I[c0:c1], T[c0:c1])
@@ -461,7 +461,7 @@ def test_local_slab_group_mutation_skip_halo(Solver, monkeypatch):
             sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=2)
             for reg in range(6):
                 bc = p.bcs[reg]
-                sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+                sv.set_wall(reg, bc)
             ncross = sv.ncells // sv.nz_local
             c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
             sv.set_state(I[c0:c1], T[c0:c1])
@@ -524,7 +524,7 @@ def _band_group(Solver, p, P, I, T):
         group.append(sv)
         for reg in range(6 if p.mesh.dim == 3 else 4):
             bc = p.bcs[reg]
-            sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+            sv.set_wall(reg, bc)
         sv.set_state(np.ascontiguousarray(I[:, :, sv.b0:sv.b1]), T)
     return group
 
@@ -660,7 +660,7 @@ def test_slot_rotation_groups(Solver, monkeypatch):
                 group.append(sv)
                 for reg in range(6):
                     bc = p.bcs[reg]
-                    sv.set_bc(reg, bc.kind, bc.T_wall, bc.T_uniform)
+                    sv.set_wall(reg, bc)
                 ncross = sv.ncells // sv.nz_local
                 c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
                 sv.set_state(I[c0:c1], T[c0:c1])
@@ -680,3 +680,120 @@ def test_slot_rotation_groups(Solver, monkeypatch):
         out[rot] = slab + band
     for x, y in zip(out["0"], out["1"]):
         assert np.array_equal(x, y)
+
+
+# ----------------------------------------------------------------- partially specular walls (reading R-i)
+
+def _partial_problem(case, spec):
+    if case == "3d":
+        b = bi.subset_bands(bi.silicon_bands(29), [1, 18, 34, 39])
+        bcs = [bi.WallBC(bi.BC_PARTIAL, specularity=spec), bi.WallBC(bi.BC_PARTIAL, specularity=1.0 - spec),
+               bi.WallBC(bi.BC_ISOTHERMAL, None, 305.0), bi.WallBC(bi.BC_PARTIAL, specularity=spec),
+               bi.WallBC(bi.BC_PARTIAL, specularity=spec), bi.WallBC(bi.BC_ISOTHERMAL, None, 298.0)]
+        return bi.small_3d(7, 5, 6, bands=b, bcs=bcs)
+    p = _group_case("2d")
+    p.bcs[0] = bi.WallBC(bi.BC_PARTIAL, specularity=spec)
+    p.bcs[1] = bi.WallBC(bi.BC_PARTIAL, specularity=spec)
+    return p
+
+
+@pytest.mark.parametrize("case", ["3d", "2d"])
+@pytest.mark.parametrize("spec", [0.37, 0.9])
+def test_partial_wall_parity(Solver, case, spec):
+    """Partially specular walls (ghost = p I_r + (1-p) g_diffuse) against the oracle."""
+    p = _partial_problem(case, spec)
+    (rel, dT), _ = _run_both(Solver, p, 9)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+@pytest.mark.parametrize("spec,kind", [(1.0, bi.BC_SPECULAR), (0.0, bi.BC_DIFFUSE)])
+def test_partial_wall_limits_bitexact_gpu(Solver, spec, kind):
+    """p = 1 is the specular wall and p = 0 the diffuse wall, bit for bit."""
+    p = _partial_problem("3d", spec)
+    p.bcs[1] = bi.WallBC(bi.BC_PARTIAL, specularity=spec)
+    q = _partial_problem("3d", spec)
+    q.bcs = [bi.WallBC(kind) if bc.kind == bi.BC_PARTIAL else bc for bc in q.bcs]
+    I, T = oracle.Oracle(p).random_state()
+    out = []
+    for prob in (p, q):
+        with Solver.from_problem(prob) as sv:
+            sv.set_state(I, T)
+            sv.step(6)
+            out.append((sv.intensity(), sv.temperature()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_partial_wall_closed_box_energy(Solver):
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    bcs = [bi.WallBC(bi.BC_PARTIAL, specularity=0.4) for _ in range(6)]
+    p = bi.small_3d(6, 5, 4, bands=b, bcs=bcs, dirs=bi.directions_control_angle(4, 16))
+    I, _ = oracle.Oracle(p).random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, None)
+        E0 = sv.energy()
+        sv.step(300)
+        E1 = sv.energy()
+    assert abs(E1 / E0 - 1) < 1e-12, E1 / E0 - 1
+
+
+def test_partial_wall_rotation_and_groups(Solver, monkeypatch):
+    """Partial walls under octant-slot rotation (snapshot + diffuse table), the
+    slab group and the band group: bit-exact against one plain context."""
+    p = _partial_problem("3d", 0.37)
+    I, T = oracle.Oracle(p).random_state()
+    res = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("BTE_ROTATE", rot)
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(5)
+            res[rot] = (sv.intensity(), sv.temperature())
+    assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][1], res["1"][1])
+    monkeypatch.setenv("BTE_ROTATE", "0")
+    group = []
+    try:
+        for r in range(3):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=3)
+            group.append(sv)
+            for reg in range(6):
+                sv.set_wall(reg, p.bcs[reg])
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+        Solver.group_step(group, 5)
+        Ig = np.concatenate([sv.intensity() for sv in group])
+        Tg = np.concatenate([sv.temperature() for sv in group])
+    finally:
+        for sv in group:
+            sv.close()
+    assert np.array_equal(Ig, res["0"][0]) and np.array_equal(Tg, res["0"][1])
+    bgroup = _band_group(Solver, p, 2, I, T)
+    try:
+        Solver.group_step(bgroup, 5)
+        Ib = np.concatenate([sv.intensity() for sv in bgroup], axis=2)
+        Tb = bgroup[0].temperature()
+    finally:
+        for sv in bgroup:
+            sv.close()
+    assert np.max(np.abs(Tb - res["0"][1])) <= 1e-10 and np.max(np.abs(Ib / res["0"][0] - 1)) <= 1e-12
+
+
+def test_partial_wall_errors(Solver):
+    from paper_2305_19400_b200 import BteError
+    p = _partial_problem("3d", 0.5)
+    with Solver.from_problem(p) as sv:
+        for bad in (-0.1, 1.5, float("nan")):
+            with pytest.raises(BteError) as e:
+                sv.set_bc(0, bi.BC_PARTIAL, specularity=bad)
+            assert e.value.status == 1
+        with pytest.raises(BteError) as e:  # the plain entry point refuses kind 3
+            sv._check(sv._lib.bte_set_bc(sv._h, 0, bi.BC_PARTIAL, None, 300.0))
+        assert e.value.status == 1
+    d = bi.directions_control_angle(4, 8)
+    d.s = d.s.copy()
+    d.s[0, 0] += 1e-9
+    q = bi.small_3d(dirs=d, bcs=bi.uniform_bcs(bi.BC_DIFFUSE))
+    with Solver.from_problem(q) as sv:
+        with pytest.raises(BteError) as e:
+            sv.set_bc(0, bi.BC_PARTIAL, specularity=0.5)
+        assert e.value.status == 6
