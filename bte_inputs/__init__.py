@@ -66,6 +66,31 @@ class Mesh:
 
 
 @dataclasses.dataclass
+class UMesh:
+    """Unstructured simplex mesh (Eq. 3 P:L176-184 holds for any
+    polyhedral cell): triangles (dim 2, 3 vertices per cell) or tetrahedra
+    (dim 3, 4 vertices).  DATA only: vertex coordinates [nverts, 3] (z = 0 in
+    2-D) and cell -> vertex lists [ncells, dim+1].  Face k of a cell is the
+    face opposite its local vertex k.  The domain is the axis-aligned box
+    spanned by the vertices; every boundary face must lie on one of its walls
+    (region 0..5 = -x,+x,-y,+y,-z,+z, tested in that order).  depth is the z
+    extent of a 2-D mesh (volumes = area*depth)."""
+
+    dim: int
+    verts: np.ndarray
+    cells: np.ndarray
+    depth: float = 1.0
+
+    @property
+    def ncells(self) -> int:
+        return int(self.cells.shape[0])
+
+    @property
+    def nverts(self) -> int:
+        return int(self.verts.shape[0])
+
+
+@dataclasses.dataclass
 class Directions:
     """Discrete directions s_d (unit vectors, [nd,3]) and weights w_d [nd]."""
 
@@ -358,6 +383,8 @@ def random_temperature(mesh: Mesh, seed: int, T_mean: float = 300.0, T_amp: floa
     """T_c = T_mean + T_amp*sin(2pi(x/Lx+p1))*sin(2pi(y/Ly+p2))[*sin(2pi(z/Lz+p3))],
     x = cell centre (i+1/2)*dx with the GLOBAL index i.  Canonical cell order of
     the full mesh, or of the sub-box ((x0,x1),(y0,y1),(z0,z1)) when given."""
+    if isinstance(mesh, UMesh):
+        return random_temperature_umesh(mesh, seed, T_mean, T_amp)
     p1, p2, p3 = random_phases(seed)
     (x0, x1), (y0, y1), (z0, z1) = box if box is not None else ((0, mesh.nx), (0, mesh.ny), (0, mesh.nz))
     x = (np.arange(x0, x1) + 0.5) * mesh.dx
@@ -388,6 +415,101 @@ def intensity_noise_factor(seed: int, ncells: int, nd: int, nb: int, amp: float 
     z = splitmix64(np.uint64(seed & MASK64) ^ idx)
     u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
     return (1.0 + amp * (2.0 * u - 1.0)).reshape(cg.size, nd, nb)
+
+
+# --------------------------------------------------------------------------
+# unstructured simplex meshes: a lattice of squares / cubes,
+# each split into 2 triangles / 6 tetrahedra, with seeded vertex jitter.  A
+# vertex coordinate along axis a is jittered only when the vertex is not on a
+# wall normal to a, so walls stay planar and axis-aligned.
+
+def _lattice_verts(n, h, jitter: float, seed: int) -> np.ndarray:
+    dim = len(n)
+    grids = np.meshgrid(*[np.arange(k + 1) for k in n[::-1]], indexing="ij")  # slowest axis first
+    idx = [g.reshape(-1) for g in grids[::-1]]  # idx[0] = x index (fastest)
+    nv = idx[0].size
+    X = np.zeros((nv, 3))
+    u = uniform_noise(seed, nv * dim).reshape(nv, dim) if jitter > 0 else np.zeros((nv, dim))
+    for a in range(dim):
+        x = idx[a] * h[a]
+        interior = (idx[a] > 0) & (idx[a] < n[a])
+        X[:, a] = np.where(interior, x + jitter * h[a] * (2.0 * u[:, a] - 1.0), x)
+    return X
+
+
+def umesh_tri(nx: int, ny: int, Lx: float, Ly: float, jitter: float = 0.2, seed: int = 11,
+              shuffle: bool = False, mirror: bool = False, depth: float = 1.0) -> UMesh:
+    """2-D triangulation of an nx x ny lattice of squares (2 triangles each, the
+    diagonal drawn per square from the seeded noise, or mirror-symmetric about
+    x = Lx/2 when mirror=True); square-major cell order unless shuffled."""
+    V = _lattice_verts((nx, ny), (Lx / nx, Ly / ny), jitter, seed)
+    vid = lambda i, j: i + (nx + 1) * j  # noqa: E731
+    flip = uniform_noise(seed + 1, nx * ny) < 0.5
+    cells = []
+    for j in range(ny):
+        for i in range(nx):
+            a, b, c, d = vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)
+            f = (i < nx // 2) if mirror else bool(flip[i + nx * j])
+            if f:
+                cells += [(a, b, c), (a, c, d)]
+            else:
+                cells += [(a, b, d), (b, c, d)]
+    C = np.array(cells, dtype=np.int64)
+    if shuffle:
+        C = C[np.random.Generator(np.random.PCG64(seed + 2)).permutation(len(C))]
+    return UMesh(2, V, np.ascontiguousarray(C), depth)
+
+
+# Kuhn subdivision of a cube into 6 tetrahedra along the main diagonal: for each
+# axis order (p, q, r), the path 000 -> e_p -> e_p + e_q -> 111 (conforming
+# across cubes because every cube uses the same split)
+_KUHN = ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0))
+
+
+def umesh_tet(nx: int, ny: int, nz: int, h: float = 1e-6, jitter: float = 0.1, seed: int = 13,
+              shuffle: bool = False) -> UMesh:
+    """3-D tetrahedral mesh: nx x ny x nz cubes of side h, 6 Kuhn tetrahedra
+    each, jittered vertices; cube-major cell order unless shuffled."""
+    V = _lattice_verts((nx, ny, nz), (h, h, h), jitter, seed)
+    vid = lambda i, j, k: i + (nx + 1) * (j + (ny + 1) * k)  # noqa: E731
+    cells = []
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                for p in _KUHN:
+                    o = [0, 0, 0]
+                    path = [vid(i, j, k)]
+                    for a in p:
+                        o[a] = 1
+                        path.append(vid(i + o[0], j + o[1], k + o[2]))
+                    cells.append(tuple(path))
+    C = np.array(cells, dtype=np.int64)
+    if shuffle:
+        C = C[np.random.Generator(np.random.PCG64(seed + 2)).permutation(len(C))]
+    return UMesh(3, V, np.ascontiguousarray(C), 1.0)
+
+
+def umesh_centroids(m: UMesh) -> np.ndarray:
+    """Cell centroids: vertex coordinates summed in local vertex order, / (dim+1)."""
+    X = m.verts[m.cells]  # [nc, dim+1, 3]
+    acc = X[:, 0, :].copy()
+    for k in range(1, m.dim + 1):
+        acc = acc + X[:, k, :]
+    return acc / (m.dim + 1)
+
+
+def random_temperature_umesh(m: UMesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0) -> np.ndarray:
+    """Random start on an unstructured mesh: the structured recipe with the cell
+    centre replaced by the centroid, measured from the box corner, and L the
+    box extent."""
+    p1, p2, p3 = random_phases(seed)
+    cen = umesh_centroids(m)
+    lo = m.verts.min(axis=0)
+    L = m.verts.max(axis=0) - lo
+    fx = np.sin(2.0 * math.pi * ((cen[:, 0] - lo[0]) / L[0] + p1))
+    fy = np.sin(2.0 * math.pi * ((cen[:, 1] - lo[1]) / L[1] + p2))
+    fz = np.sin(2.0 * math.pi * ((cen[:, 2] - lo[2]) / L[2] + p3)) if m.dim == 3 else np.ones(m.ncells)
+    return np.ascontiguousarray(T_mean + T_amp * (fz * fy * fx))
 
 
 def subproblem(problem: "Problem", box, open_kind: int = BC_SPECULAR) -> "Problem":
@@ -510,6 +632,45 @@ def small_3d(nx=5, ny=4, nz=3, dirs=None, bands=None, bcs=None, dt=1e-12, d=1e-6
         bcs = [WallBC(BC_SPECULAR), WallBC(BC_DIFFUSE), WallBC(BC_ISOTHERMAL, None, 305.0),
                WallBC(BC_SPECULAR), WallBC(BC_ISOTHERMAL, None, 300.0), WallBC(BC_DIFFUSE)]
     return Problem(f"small3d_{nx}x{ny}x{nz}", mesh, dirs, bands, dt=dt, T_init=300.0,
+                   bcs=bcs, nsteps=10, seed=seed)
+
+
+def config_u2(n: int = 120, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
+    """Unstructured analogue of config 2: the 525 um square as 2 n^2
+    jittered triangles, 400 directions, 40 channels, +y 310 K / -y 300 K
+    isothermal walls, specular x-walls, dt = 1e-12 s."""
+    L = 525e-6
+    p = config2(n=n, n_freq=n_freq, n_theta=n_theta, n_phi=n_phi)
+    p.mesh = umesh_tri(n, n, L, L, jitter=0.2, seed=SEED_BASE + 7)
+    p.bcs[3] = WallBC(BC_ISOTHERMAL, None, 310.0)
+    p.name = f"u2_tri_{2*n*n}x{n_theta*n_phi}x{p.bands.nb}"
+    p.seed = SEED_BASE + 7
+    return p
+
+
+def config_u3(n: int = 32, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
+    """Unstructured analogue of config 3: n^3 cubes of 1 um as 6 n^3 jittered
+    tetrahedra, 400 directions, 40 channels, z walls 300/310 K, x/y specular."""
+    p = config3(n=n, n_freq=n_freq, n_theta=n_theta, n_phi=n_phi)
+    p.mesh = umesh_tet(n, n, n, 1e-6, jitter=0.1, seed=SEED_BASE + 8)
+    p.name = f"u3_tet_{6*n**3}x{n_theta*n_phi}x{p.bands.nb}"
+    p.seed = SEED_BASE + 8
+    return p
+
+
+def small_umesh(dim: int = 2, n=(4, 3, 2), dirs=None, bands=None, bcs=None, dt=1e-12, shuffle=False,
+                jitter=None, seed=17) -> Problem:
+    """Small unstructured case for parity tests."""
+    if dim == 2:
+        mesh = umesh_tri(n[0], n[1], n[0] * 1e-6, n[1] * 1e-6, 0.2 if jitter is None else jitter, seed, shuffle)
+    else:
+        mesh = umesh_tet(n[0], n[1], n[2], 1e-6, 0.1 if jitter is None else jitter, seed, shuffle)
+    dirs = dirs if dirs is not None else directions_control_angle(4, 8)
+    bands = bands if bands is not None else subset_bands(silicon_bands(29), [0, 5, 17, 28, 30, 39])
+    if bcs is None:
+        bcs = [WallBC(BC_SPECULAR), WallBC(BC_DIFFUSE), WallBC(BC_ISOTHERMAL, None, 305.0),
+               WallBC(BC_SPECULAR), WallBC(BC_ISOTHERMAL, None, 300.0), WallBC(BC_DIFFUSE)]
+    return Problem(f"small_umesh{dim}d_{mesh.ncells}", mesh, dirs, bands, dt=dt, T_init=300.0,
                    bcs=bcs, nsteps=10, seed=seed)
 
 

@@ -20,6 +20,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bte_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "bte_oracle_umesh.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 ORA_OK = 0
@@ -28,14 +29,20 @@ ORA_ERRORS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 6: "ENOTCLOSED", 7: "ENEWTON", 
 
 def build(force: bool = False) -> str:
     """Compile the oracle (gcc, no fast-math, no FMA contraction)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(f)
+                                                      for f in _SRCS):
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-               "-std=c11", "-D_GNU_SOURCE", "-o", _LIB_PATH, _SRC, "-lm"]
+               "-std=c11", "-D_GNU_SOURCE", "-o", _LIB_PATH, *_SRCS, "-lm"]
         subprocess.check_call(cmd)
     return _LIB_PATH
 
 
 _lib = None
+
+
+class _UMesh(C.Structure):
+    _fields_ = [("dim", C.c_int), ("nverts", C.c_long), ("verts", C.c_void_p), ("ncells", C.c_long),
+                ("cells", C.c_void_p), ("depth", C.c_double)]
 
 
 class _Problem(C.Structure):
@@ -84,6 +91,19 @@ def lib():
         _lib.ora_solve_T.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.ora_n_faces.restype = C.c_long
         _lib.ora_n_faces.argtypes = [P, C.c_int]
+        U = C.POINTER(_UMesh)
+        _lib.ora_ugeom_build.argtypes = [U, C.POINTER(C.c_void_p)]
+        _lib.ora_ugeom_free.argtypes = [C.c_void_p]
+        _lib.ora_ugeom_nfaces.restype = C.c_long
+        _lib.ora_ugeom_nfaces.argtypes = [C.c_void_p, C.c_int]
+        _lib.ora_ugeom_export.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        _lib.ora_usweep.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.ora_urun.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long,
+                                  C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int)]
+        _lib.ora_uenergy.restype = C.c_double
+        _lib.ora_uenergy.argtypes = [P, C.c_void_p, C.c_void_p]
+        _lib.ora_udt_margin.restype = C.c_double
+        _lib.ora_udt_margin.argtypes = [P, C.c_void_p, C.c_double, C.c_int]
         assert _lib.ora_sizeof_problem() == C.sizeof(_Problem)
     return _lib
 
@@ -118,8 +138,13 @@ class Oracle:
             return a
 
         st = _Problem()
-        st.dim, st.nx, st.ny, st.nz = m.dim, m.nx, m.ny, m.nz
-        st.dx, st.dy, st.dz = m.dx, m.dy, m.dz
+        self.umesh = hasattr(m, "cells")
+        if self.umesh:  # unstructured (bte_oracle_umesh.c): per-cell pieces see nx = ncells
+            st.dim, st.nx, st.ny, st.nz = m.dim, m.ncells, 1, 1
+            st.dx = st.dy = st.dz = 1.0
+        else:
+            st.dim, st.nx, st.ny, st.nz = m.dim, m.nx, m.ny, m.nz
+            st.dx, st.dy, st.dz = m.dx, m.dy, m.dz
         st.nd = d.nd
         st.s = _ptr(keep(d.s))
         st.w = _ptr(keep(d.w))
@@ -143,6 +168,43 @@ class Oracle:
         self._st = st
         self.nc, self.nd, self.nb = m.ncells, d.nd, b.nb
         lib()
+        self._ug = None
+        if self.umesh:
+            self._verts = np.ascontiguousarray(m.verts, dtype=np.float64)
+            self._cells = np.ascontiguousarray(m.cells, dtype=np.int64)
+            um = _UMesh(m.dim, self._verts.shape[0], self._verts.ctypes.data, self._cells.shape[0],
+                        self._cells.ctypes.data, float(m.depth))
+            h = C.c_void_p()
+            rc = lib().ora_ugeom_build(C.byref(um), C.byref(h))
+            if rc:
+                raise OracleError(rc, "unstructured geometry")
+            self._ug = h
+
+    def __del__(self):
+        if getattr(self, "_ug", None):
+            lib().ora_ugeom_free(self._ug)
+            self._ug = None
+
+    # -- unstructured geometry (tests)
+    def geometry(self):
+        """(vol[nc], area[nc,K], normal[nc,K,3], nbr[nc,K], region[nc,K]) of an unstructured mesh."""
+        K = self.problem.mesh.dim + 1
+        vol = np.empty(self.nc)
+        area = np.empty((self.nc, K))
+        nrm = np.empty((self.nc, K, 3))
+        nbr = np.empty((self.nc, K), dtype=np.int64)
+        reg = np.empty((self.nc, K), dtype=np.int32)
+        lib().ora_ugeom_export(self._ug, vol.ctypes.data, area.ctypes.data, nrm.ctypes.data, nbr.ctypes.data,
+                               reg.ctypes.data)
+        return vol, area, nrm, nbr, reg
+
+    def n_region_faces(self, region: int) -> int:
+        if self.umesh:
+            return int(lib().ora_ugeom_nfaces(self._ug, region))
+        return int(lib().ora_n_faces(C.byref(self._st), region))
+
+    def udt_margin(self, beta_max: float, b: int) -> float:
+        return lib().ora_udt_margin(C.byref(self._st), self._ug, beta_max, b)
 
     # -- material functions
     def I0(self, b: int, T: float) -> Tuple[float, float]:
@@ -199,7 +261,10 @@ class Oracle:
     def sweep(self, I, I0c, betac) -> np.ndarray:
         I, I0c, betac = _f64(I), _f64(I0c), _f64(betac)
         out = np.empty_like(I)
-        st = lib().ora_sweep(C.byref(self._st), _ptr(I), _ptr(I0c), _ptr(betac), _ptr(out))
+        if self.umesh:
+            st = lib().ora_usweep(C.byref(self._st), self._ug, _ptr(I), _ptr(I0c), _ptr(betac), _ptr(out))
+        else:
+            st = lib().ora_sweep(C.byref(self._st), _ptr(I), _ptr(I0c), _ptr(betac), _ptr(out))
         if st:
             raise OracleError(st, "sweep")
         return out
@@ -249,8 +314,12 @@ class Oracle:
             I0c, betac = _f64(I0c).copy(), _f64(betac).copy()
         es, ec = C.c_long(), C.c_long()
         it = C.c_int()
-        st = lib().ora_run(C.byref(self._st), _ptr(I), _ptr(T), _ptr(I0c), _ptr(betac), nsteps,
-                           C.byref(es), C.byref(ec), C.byref(it))
+        if self.umesh:
+            st = lib().ora_urun(C.byref(self._st), self._ug, _ptr(I), _ptr(T), _ptr(I0c), _ptr(betac), nsteps,
+                                C.byref(es), C.byref(ec), C.byref(it))
+        else:
+            st = lib().ora_run(C.byref(self._st), _ptr(I), _ptr(T), _ptr(I0c), _ptr(betac), nsteps,
+                               C.byref(es), C.byref(ec), C.byref(it))
         if st:
             raise OracleError(st, f"step {es.value} cell {ec.value}")
         self.last_max_iters = it.value
@@ -268,6 +337,8 @@ class Oracle:
 
     def energy(self, I) -> float:
         I = _f64(I)
+        if self.umesh:
+            return lib().ora_uenergy(C.byref(self._st), self._ug, _ptr(I))
         return lib().ora_energy(C.byref(self._st), _ptr(I))
 
 

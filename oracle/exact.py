@@ -114,3 +114,123 @@ def ulp_error(approx, exact):
         err = abs(Fr(float(a)) - e)
         worst = max(worst, float(err / Fr(u)))
     return worst
+
+
+def exact_usweep(problem, I, I0c, betac):
+    """One sweep step on an UNSTRUCTURED simplex mesh in exact rationals
+    (SURVEY 8(f) f3), written from Eq. 3 with rational geometry:
+    for a face f of cell c, A_f n_f / V_c is computed without square roots --
+      triangle: A_f n_f = depth * perp(edge), V = depth * |cross| / 2,
+      tetrahedron: A_f n_f = cross(b - a, c - a) / 2, V = |det| / 6,
+    oriented away from the opposite vertex.  Faces are matched by their vertex
+    sets; a boundary face's wall is the box plane all its vertices lie on.
+    Returns Fractions [nc, nd, nb].  LINEAR channel tables only."""
+    m, dr, bd = problem.mesh, problem.dirs, problem.bands
+    assert bd.mode == 0, "exact twin supports LINEAR channels only"
+    nd, nb = dr.nd, bd.nb
+    K = m.dim + 1
+    P = [[Fr(float(x)) for x in row] for row in m.verts]
+    cells = [[int(v) for v in row] for row in m.cells]
+    nc = len(cells)
+    lo = [min(p[a] for p in P) for a in range(3)]
+    hi = [max(p[a] for p in P) for a in range(3)]
+    s = [[Fr(float(x)) for x in row] for row in dr.s]
+    w = [Fr(float(x)) for x in dr.w]
+    v = [Fr(float(x)) for x in bd.v]
+    dt = Fr(problem.dt)
+    depth = Fr(float(m.depth))
+    If = np.vectorize(Fr, otypes=[object])(np.asarray(I, dtype=np.float64))
+    I0f = np.vectorize(Fr, otypes=[object])(np.asarray(I0c, dtype=np.float64))
+    bf = np.vectorize(Fr, otypes=[object])(np.asarray(betac, dtype=np.float64))
+    refl = {a: _reflect_map(dr.s, a) for a in range(m.dim)}
+    owner = {}
+    for c, cv in enumerate(cells):
+        for k in range(K):
+            owner.setdefault(frozenset(cv[:k] + cv[k + 1:]), []).append((c, k))
+    # wall faces in (cell, local face) order per region
+    wall_index = {}
+    count = [0] * 6
+
+    def sub(p, q):
+        return [p[i] - q[i] for i in range(3)]
+
+    def dot(p, q):
+        return p[0] * q[0] + p[1] * q[1] + p[2] * q[2]
+
+    geo = []  # per cell: volume, [(An vector, neighbour or None, region)]
+    for c, cv in enumerate(cells):
+        X = [P[i] for i in cv]
+        if m.dim == 2:
+            u, vv = sub(X[1], X[0]), sub(X[2], X[0])
+            V = abs(u[0] * vv[1] - u[1] * vv[0]) / 2 * depth
+        else:
+            u, vv, ww = sub(X[1], X[0]), sub(X[2], X[0]), sub(X[3], X[0])
+            det = (u[0] * (vv[1] * ww[2] - vv[2] * ww[1]) - u[1] * (vv[0] * ww[2] - vv[2] * ww[0])
+                   + u[2] * (vv[0] * ww[1] - vv[1] * ww[0]))
+            V = abs(det) / 6
+        faces = []
+        for k in range(K):
+            others = [X[i] for i in range(K) if i != k]
+            if m.dim == 2:
+                e = sub(others[1], others[0])
+                An = [e[1] * depth, -e[0] * depth, Fr(0)]
+            else:
+                e1, e2 = sub(others[1], others[0]), sub(others[2], others[0])
+                An = [(e1[1] * e2[2] - e1[2] * e2[1]) / 2, (e1[2] * e2[0] - e1[0] * e2[2]) / 2,
+                      (e1[0] * e2[1] - e1[1] * e2[0]) / 2]
+            if dot(An, sub(X[k], others[0])) > 0:
+                An = [-x for x in An]
+            key = frozenset(cv[:k] + cv[k + 1:])
+            nbr = [o for o in owner[key] if o[0] != c]
+            region = None
+            if not nbr:
+                for r in range(2 * m.dim):
+                    a = r // 2
+                    wall = hi[a] if r & 1 else lo[a]
+                    if all(p[a] == wall for p in others):
+                        region = r
+                        break
+                assert region is not None, "boundary face off the box walls"
+                wall_index[(c, k)] = count[region]
+                count[region] += 1
+            faces.append((An, nbr[0][0] if nbr else None, region))
+        geo.append((V, faces))
+
+    def I0_lin(b, T):
+        return Fr(float(bd.I_ref[b])) + Fr(float(bd.slope[b])) * (Fr(float(T)) - Fr(float(bd.T_ref)))
+
+    def ghost(region, c, k, d, b):
+        a = region // 2
+        bc = problem.bcs[region]
+        if bc.kind == 0:
+            T = bc.T_uniform if bc.T_wall is None else bc.T_wall[wall_index[(c, k)]]
+            return I0_lin(b, T)
+        spec = If[c, refl[a][d], b] if bc.kind in (1, 3) else None
+        if bc.kind == 1:
+            return spec
+        sg = 1 if region & 1 else -1
+        num = sum((w[e] * abs(s[e][a]) * If[c, e, b] for e in range(nd) if sg * s[e][a] > 0), Fr(0))
+        den = sum((w[e] * abs(s[e][a]) for e in range(nd) if sg * s[e][a] < 0), Fr(0))
+        diff = num / den
+        if bc.kind == 2:
+            return diff
+        p = Fr(float(bc.specularity))
+        return p * spec + (1 - p) * diff
+
+    out = np.empty((nc, nd, nb), dtype=object)
+    for c in range(nc):
+        V, faces = geo[c]
+        for d in range(nd):
+            for b in range(nb):
+                face_sum = Fr(0)
+                for k, (An, nbr, region) in enumerate(faces):
+                    sAn = dot(s[d], An)
+                    if sAn > 0:
+                        up = If[c, d, b]
+                    elif nbr is not None:
+                        up = If[nbr, d, b]
+                    else:
+                        up = ghost(region, c, k, d, b)
+                    face_sum += sAn * up
+                out[c, d, b] = If[c, d, b] + dt * ((I0f[c, b] - If[c, d, b]) * bf[c, b] - v[b] * face_sum / V)
+    return out

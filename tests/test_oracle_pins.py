@@ -561,3 +561,163 @@ def test_partial_wall_closed_box_conservation():
     I2, _, _, _ = o.run(I, T, 500, I0c, betac)
     assert abs(o.energy(I2) / E0 - 1) < 1e-12
     assert I2.min() > 0
+
+
+# ----------------------------------------------------------------- unstructured meshes
+
+def _u_lin_problem(mesh, dirs, bcs, seed=5):
+    rng = np.random.default_rng(seed)
+    nb = 3
+    v = rng.uniform(2e3, 8e3, nb)
+    tau = rng.uniform(2e-11, 8e-11, nb)
+    bands = bi.linear_bands(v, tau, rng.uniform(1e2, 1e3, nb), rng.uniform(1e4, 1e5, nb), 300.0)
+    h = 1e-7
+    dt = 0.08 * h / v.max()
+    return bi.Problem("ulin", mesh, dirs, bands, dt, 300.0, bcs)
+
+
+def _u_meshes():
+    return {
+        "tri": bi.umesh_tri(4, 3, 4e-7, 3e-7, jitter=0.2, seed=3),
+        "tri_shuffled": bi.umesh_tri(3, 3, 3e-7, 3e-7, jitter=0.2, seed=4, shuffle=True),
+        "tet": bi.umesh_tet(2, 2, 2, 1e-7, jitter=0.1, seed=5, shuffle=True),
+    }
+
+
+@pytest.mark.parametrize("case", ["tri", "tri_shuffled", "tet"])
+def test_usweep_exact_rational(case):
+    """The unstructured sweep against the exact-rational twin written from
+    Eq. 3 with square-root-free geometry (A_f n_f / V_c rational), all wall
+    kinds including a non-uniform isothermal wall and a partial wall."""
+    mesh = _u_meshes()[case]
+    dirs = bi.directions_inplane(8) if case == "tri" else bi.directions_control_angle(2, 4)
+    o0 = oracle.Oracle(_u_lin_problem(mesh, dirs, bi.uniform_bcs(bi.BC_SPECULAR)))
+    nf2 = o0.n_region_faces(2)
+    bcs = [bi.WallBC(bi.BC_SPECULAR), bi.WallBC(bi.BC_DIFFUSE), bi.WallBC(0, np.arange(nf2) * 1.5 + 300.5),
+           bi.WallBC(bi.BC_PARTIAL, specularity=0.3), bi.WallBC(0, None, 299.0), bi.WallBC(bi.BC_DIFFUSE)]
+    p = _u_lin_problem(mesh, dirs, bcs)
+    o = oracle.Oracle(p)
+    rng = np.random.default_rng(12)
+    nc, nd, nb = mesh.ncells, dirs.nd, p.bands.nb
+    T = rng.uniform(290, 310, nc)
+    I0c, betac = o.refresh(T)
+    I = I0c[:, None, :] * rng.uniform(0.9, 1.1, (nc, nd, nb))
+    got = o.sweep(I, I0c, betac)
+    ex = exact.exact_usweep(p, I, I0c, betac)
+    assert exact.ulp_error(got, ex) <= 4.0
+    # the flux term is not negligible here (the pin would be vacuous otherwise)
+    assert np.max(np.abs(got - I) / I) > 1e-3
+
+
+def test_ugeometry_closure_and_volume():
+    """Each simplex is closed (sum_f A_f n_f = 0), the volumes tile the box,
+    shared faces have equal areas and opposite normals, and the wall faces
+    partition the box surface."""
+    for mesh in _u_meshes().values():
+        p = _u_lin_problem(mesh, bi.directions_inplane(8), bi.uniform_bcs(bi.BC_SPECULAR))
+        o = oracle.Oracle(p)
+        vol, area, nrm, nbr, reg = o.geometry()
+        An = area[:, :, None] * nrm
+        scale = area.max()
+        assert np.max(np.abs(An.sum(axis=1))) < 1e-14 * scale
+        L = mesh.verts.max(axis=0) - mesh.verts.min(axis=0)
+        box = L[0] * L[1] * (L[2] if mesh.dim == 3 else mesh.depth)
+        assert abs(vol.sum() / box - 1) < 1e-13
+        for c in range(mesh.ncells):
+            for k in range(mesh.dim + 1):
+                e = nbr[c, k]
+                if e < 0:
+                    assert reg[c, k] >= 0
+                    continue
+                kk = int(np.where(nbr[e] == c)[0][0])
+                assert abs(area[e, kk] / area[c, k] - 1) < 1e-14
+                assert np.max(np.abs(nrm[e, kk] + nrm[c, k])) < 1e-14
+        for r in range(2 * mesh.dim):
+            a = r // 2
+            other = [L[i] for i in range(3) if i != a][: mesh.dim - 1]
+            wall = np.prod(other) * (1.0 if mesh.dim == 3 else mesh.depth)
+            assert abs(area[reg == r].sum() / wall - 1) < 1e-13
+
+
+@pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE, bi.BC_PARTIAL])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_ustep_closed_box_conservation(kind, dim):
+    """Closed box of adiabatic walls: interior face fluxes cancel pairwise and
+    the walls carry no net flux, so the energy is conserved."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    bcs = [bi.WallBC(kind, specularity=0.6) for _ in range(6)]
+    p = bi.small_umesh(dim, (4, 3, 2), bands=b, bcs=bcs, dirs=bi.directions_control_angle(2, 8))
+    o = oracle.Oracle(p)
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)
+    E0 = o.energy(I)
+    I2, _, _, _ = o.run(I, T, 200, I0c, betac)
+    assert abs(o.energy(I2) / E0 - 1) < 1e-12
+    assert I2.min() > 0 and np.max(np.abs(I2 / I - 1)) > 1e-4
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_ustep_uniform_fixed_point(dim):
+    """Uniform equilibrium with specular/diffuse walls and isothermal walls at
+    the same temperature stays fixed (Eq. 3 with sum_f A_f n_f = 0)."""
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 20, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 300.0), bi.WallBC(3, specularity=0.5),
+           bi.WallBC(1), bi.WallBC(0, None, 300.0)]
+    p = bi.small_umesh(dim, (4, 3, 2), bands=b, bcs=bcs)
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    I2, T2, _, _ = o.run(I, T, 30)
+    assert np.max(np.abs(I2 / I - 1)) < 1e-14 and np.max(np.abs(T2 - 300.0)) < 1e-10
+
+
+def test_ustep_ballistic_slab():
+    """Ballistic limit (beta = 0) between isothermal walls at x = 0 (T_h) and
+    x = L (T_c) with specular y walls: the upwind steady state carries
+    I0(T_h) in every direction with s_x > 0 and I0(T_c) in every direction with
+    s_x < 0, in every cell, whatever the cell shapes (transport of a constant)."""
+    mesh = bi.umesh_tri(3, 2, 3e-7, 2e-7, jitter=0.2, seed=9)
+    dirs = bi.directions_inplane(8)
+    v = np.array([5e3])
+    bands = bi.linear_bands(v, np.array([1.0]), np.array([800.0]), np.array([4e4]), 300.0)
+    bands.beta_coef[:] = 0.0
+    bcs = [bi.WallBC(0, None, 310.0), bi.WallBC(0, None, 290.0), bi.WallBC(1), bi.WallBC(1),
+           bi.WallBC(1), bi.WallBC(1)]
+    p = bi.Problem("ball", mesh, dirs, bands, 0.15 * 1e-7 / v[0], 300.0, bcs)
+    o = oracle.Oracle(p)
+    T = np.full(mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    I2, _, _, _ = o.run(I, T, 3000)
+    hot, cold = 4e4 + 800.0 * 10.0, 4e4 - 800.0 * 10.0
+    want = np.where(dirs.s[:, 0] > 0, hot, cold)
+    assert np.max(np.abs(I2[:, :, 0] / want[None, :] - 1)) < 1e-9
+
+
+def test_ustep_mirror_symmetry():
+    """A mesh mirror-symmetric about x = L/2 (power-of-two coordinates, no
+    jitter) with symmetric walls gives a mirror-symmetric temperature field
+    (to rounding: mirrored cells list their faces in another order)."""
+    h = 2.0 ** -20
+    mesh = bi.umesh_tri(6, 4, 6 * h, 4 * h, jitter=0.0, mirror=True)
+    b = bi.subset_bands(bi.silicon_bands(29), [3, 25])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(0, None, 320.0),
+           bi.WallBC(1), bi.WallBC(1)]
+    p = bi.Problem("umirror", mesh, bi.directions_control_angle(2, 8), b, 1e-12, 300.0, bcs)
+    o = oracle.Oracle(p)
+    T = np.full(mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    _, T2, _, _ = o.run(I, T, 40)
+    cen = bi.umesh_centroids(mesh)
+    L = 6 * h
+    order = np.lexsort((cen[:, 1], cen[:, 0]))
+    mirror = np.lexsort((cen[:, 1], L - cen[:, 0]))
+    # cells paired with their mirror images by centroid
+    pairs = {}
+    key = lambda x, y: (round(x / h * 3), round(y / h * 3))  # noqa: E731
+    for c in range(mesh.ncells):
+        pairs[key(cen[c, 0], cen[c, 1])] = c
+    for c in range(mesh.ncells):
+        m = pairs[key(L - cen[c, 0], cen[c, 1])]
+        assert abs(T2[c] - T2[m]) < 1e-9
+    assert T2.max() > 300.0 + 1e-6
+    assert order.size == mirror.size
