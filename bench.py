@@ -45,8 +45,14 @@ BYTES_PER_DOF = 16  # read I^n + write I^{n+1}, fp64
 
 
 def _problem(config: int, nranks: int):
-    if config not in (1, 2, 3, 4, 5, 6):
+    if config not in (1, 2, 3, 4, 5, 6, 7, 8):
         raise SystemExit(f"unsupported --config {config}")
+    if config in (7, 8) and nranks > 1:
+        raise SystemExit("unstructured workloads (--config 7/8) run on one GPU")
+    if config == 7:  # unstructured analogue of config 2: 28,800 triangles
+        return bi.config_u2()
+    if config == 8:  # unstructured analogue of config 3: 196,608 tetrahedra
+        return bi.config_u3()
     if config == 2:
         p = bi.config2()
         if nranks > 1:  # weak scaling: 120 rows per GPU along the slab axis
@@ -173,6 +179,8 @@ def _oracle_sample(p, target_s: float, max_steps: int = 1000):
         T = bi.random_temperature(m, p.seed, p.T_init, 20.0, box=box)
         I = o.equilibrium(T) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m, box=box)
         return sp, o, I, T
+    if hasattr(m, "cells"):  # unstructured: a smaller mesh of the same generator
+        return _oracle_sample_umesh(p, target_s, max_steps, nthreads)
     nr = max(1, min(rows, 4))
     sp, o, I, T = make(nr)
     t = time.perf_counter()
@@ -192,6 +200,39 @@ def _oracle_sample(p, target_s: float, max_steps: int = 1000):
     dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
     desc = (f"oracle C fp64 (gcc -O2 -ffp-contract=off, OpenMP), {steps} step(s) of a "
             f"{sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of {p.name} (random start), {el:.1f} s")
+    return dof * steps / el, desc, nthreads
+
+
+def _umesh_problem(p, n):
+    return bi.config_u2(n=n) if p.mesh.dim == 2 else bi.config_u3(n=n)
+
+
+def _oracle_sample_umesh(p, target_s, max_steps, nthreads):
+    import oracle
+    n_full = 120 if p.mesh.dim == 2 else 32
+    sp = _umesh_problem(p, 4)
+    o = oracle.Oracle(sp, nthreads=nthreads)
+    I, T = o.random_state()
+    t = time.perf_counter()
+    o.run(I, T, 1)
+    per_cell = (time.perf_counter() - t) / sp.mesh.ncells
+    cells = (target_s / 3) / max(per_cell, 1e-12)
+    per_unit = 2 if p.mesh.dim == 2 else 6
+    n = int(max(2, min(n_full, (cells / per_unit) ** (1.0 / p.mesh.dim))))
+    sp = _umesh_problem(p, n)
+    o = oracle.Oracle(sp, nthreads=nthreads)
+    I, T = o.random_state()
+    steps = 0
+    t = time.perf_counter()
+    while True:
+        I, T, _, _ = o.run(I, T, 1)[:4]
+        steps += 1
+        if time.perf_counter() - t >= target_s or steps >= max_steps:
+            break
+    el = time.perf_counter() - t
+    dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
+    desc = (f"oracle C fp64 (gcc -O2 -ffp-contract=off, OpenMP), {steps} step(s) of {sp.name} "
+            f"(the same generator at n = {n} instead of {n_full}, random start), {el:.1f} s")
     return dof * steps / el, desc, nthreads
 
 
@@ -222,12 +263,25 @@ def run_reference(args):
         I = o.equilibrium(T) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m, box=box)
         return sp, o, I, T
 
-    sp, o, I, T = make(1)
-    t = time.perf_counter()
-    o.run(I, T, 1)
-    per_row = time.perf_counter() - t
-    nr = int(max(1, min(rows_total, per_step / max(per_row, 1e-9))))
-    sp, o, I, T = make(nr)
+    if hasattr(m, "cells"):  # unstructured: each step on a smaller mesh of the same generator
+        sp = _umesh_problem(p, 4)
+        o = oracle.Oracle(sp, nthreads=nthreads)
+        I, T = o.random_state()
+        t = time.perf_counter()
+        o.run(I, T, 1)
+        per_cell = (time.perf_counter() - t) / sp.mesh.ncells
+        per_unit = 2 if m.dim == 2 else 6
+        n = int(max(2, ((per_step / max(per_cell, 1e-12)) / per_unit) ** (1.0 / m.dim)))
+        sp = _umesh_problem(p, n)
+        o = oracle.Oracle(sp, nthreads=nthreads)
+        I, T = o.random_state()
+    else:
+        sp, o, I, T = make(1)
+        t = time.perf_counter()
+        o.run(I, T, 1)
+        per_row = time.perf_counter() - t
+        nr = int(max(1, min(rows_total, per_step / max(per_row, 1e-9))))
+        sp, o, I, T = make(nr)
     I0c, betac = o.refresh(T)
     for _ in range(args.warmup):
         I, T, I0c, betac = o.run(I, T, 1, I0c, betac)
@@ -237,8 +291,11 @@ def run_reference(args):
     el = time.perf_counter() - t
     dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
     value = dof * args.steps / el
-    sample = (f"each step = one oracle step of a {sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of "
-              f"{p.name} (random start)")
+    if hasattr(m, "cells"):
+        sample = f"each step = one oracle step of {sp.name} (same generator, smaller mesh; random start)"
+    else:
+        sample = (f"each step = one oracle step of a {sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of "
+                  f"{p.name} (random start)")
     line = {
         "impl": "reference", "metric": "BTE DOF-updates/s (cell x dir x band / s), whole step",
         "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -325,7 +382,8 @@ def run_b200(args):
     tpd = _traffic_per_dof(p.name)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None if tpd is None else tpd * dof_per_launch,
-                "kernel": (("k_sweep_tma" if sv.nj * sv.nb >= 384 else "k_sweep")
+                "kernel": ("k_usweep (a1+a2 face-list upwind flux + relaxation on simplices + octant partial sums)"
+                           if sv.umesh else ("k_sweep_tma" if sv.nj * sv.nb >= 384 else "k_sweep")
                            + " (a1+a2 fused upwind flux + relaxation + octant partial sums"
                            + (", a3+a4 Newton fused in the tail)" if tim["newton_launches"] == 0 else ")")),
                 "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_per_launch, "kernel_ms_avg": sweep_ms,

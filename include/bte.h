@@ -168,6 +168,46 @@ BTE_API bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const 
 BTE_API bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                                    const bte_run *run, bte_ctx **out);
 
+/* Unstructured simplex mesh.  The finite-volume step is
+ * Eq. 3 for m-sided cells with the upwind face value of
+ * I' = I + dt*(beta (I0c - I) - v_b sum_f (A_f/V_c)(s_d.n_f) I_up).
+ *   dim 2: triangles, cells[c][0..2]; verts z ignored; depth = z extent.
+ *   dim 3: tetrahedra, cells[c][0..3].
+ * Face k of cell c is the face opposite its local vertex k.  The domain is
+ * the axis-aligned bounding box of the vertices; every face without a
+ * neighbour must lie on one of its walls (all face vertices at x = xmin ->
+ * region 0, x = xmax -> 1, y -> 2/3, z -> 4/5, tested in that order).  Wall
+ * faces are numbered per region in (cell, local face) ascending order: that
+ * is the order of bte_set_bc's T_wall array (bte_get_region_faces gives the
+ * count).  Arrays are host memory, read during the call only. */
+typedef struct {
+  int dim;               /* 2 or 3 */
+  int64_t nverts;
+  const double *verts;   /* [nverts][3], metres */
+  int64_t ncells;
+  const int64_t *cells;  /* [ncells][dim+1] vertex indices */
+  double depth;          /* dim 2: z extent (volumes and face areas scale with it) */
+} bte_umesh;
+
+/* Create a single-GPU context on an unstructured mesh.  Geometry precompute
+ * (a0) on the host: A_f n_f / V_c per (cell, face) without square roots
+ * (triangle: 2 perp(edge)/|cross|; tetrahedron: 3 cross/|det|, oriented away
+ * from the opposite vertex), face matching by vertex sets, wall regions.
+ * State layout, set_state/get_* orders, the temperature update and the wall
+ * kinds are as for bte_create (canonical cell index = position in cells).
+ * run->nranks must be 1 (no slab/band decomposition of unstructured meshes);
+ * octant-slot rotation is not used.  The dt check is the general positivity
+ * bound 1 - dt beta_b - dt v_b max_c sum_{f: s.n>0} (A_f/V_c) s.n >= 0.
+ * Errors: BTE_EINVAL (degenerate cell, bad vertex index, a face shared by more
+ * than two cells, a boundary face off the box walls, nranks != 1, or as
+ * bte_create), BTE_EUNSTABLE, BTE_ENOMEM, BTE_ECUDA. */
+BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
+                                    const bte_run *run, bte_ctx **out);
+
+/* Number of boundary faces of wall region 0..5 (the T_wall length of
+ * bte_set_bc) for structured and unstructured contexts.  Errors: BTE_EINVAL. */
+BTE_API bte_status bte_get_region_faces(const bte_ctx *ctx, int region, int64_t *nfaces);
+
 /* Boundary condition of one wall region (0..5 = -x,+x,-y,+y,-z,+z).
  * T_wall: host array with one temperature per boundary face of that wall,
  * row-major over the two in-plane axes in (x,y,z) order ((y,z) for x-walls,

@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE, BC_PARTIAL = 0, 1, 2, 3
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -38,6 +38,11 @@ class BteError(RuntimeError):
 class Mesh(C.Structure):
     _fields_ = [("dim", C.c_int), ("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
                 ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double)]
+
+
+class UMeshC(C.Structure):
+    _fields_ = [("dim", C.c_int), ("nverts", C.c_int64), ("verts", C.c_void_p), ("ncells", C.c_int64),
+                ("cells", C.c_void_p), ("depth", C.c_double)]
 
 
 class Dirs(C.Structure):
@@ -104,6 +109,10 @@ def load_library(path: str = LIB_PATH):
     if hasattr(lib, "bte_create_band"):  # (older A/B builds via BTE_LIB lack the band entry points)
         lib.bte_create_band.argtypes = lib.bte_create.argtypes
         lib.bte_plan_band.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    if hasattr(lib, "bte_create_umesh"):
+        lib.bte_create_umesh.argtypes = [C.POINTER(UMeshC), C.POINTER(Dirs), C.POINTER(Bands), C.POINTER(Run),
+                                         C.POINTER(C.c_void_p)]
+        lib.bte_get_region_faces.argtypes = [P, C.c_int, C.POINTER(C.c_int64)]
     lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
     if hasattr(lib, "bte_set_bc_partial"):
         lib.bte_set_bc_partial.argtypes = [P, C.c_int, C.c_double]
@@ -162,7 +171,16 @@ class Solver:
         self._keep = []
         k = self._keep.append
 
-        m = Mesh(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.dx, mesh.dy, mesh.dz)
+        self.umesh = hasattr(mesh, "cells")
+        if self.umesh:  # unstructured simplex mesh (bte_create_umesh)
+            if decomp != "slab" or nranks != 1:
+                raise ValueError("unstructured meshes run on one context (nranks = 1)")
+            verts = np.ascontiguousarray(mesh.verts, dtype=np.float64)
+            cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
+            k(verts), k(cells)
+            m = UMeshC(int(mesh.dim), verts.shape[0], _p(verts), cells.shape[0], _p(cells), float(mesh.depth))
+        else:
+            m = Mesh(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.dx, mesh.dy, mesh.dz)
         s, w = _f64(dirs.s), _f64(dirs.w)
         k(s), k(w)
         d = Dirs(int(w.shape[0]), _p(s), _p(w))
@@ -196,6 +214,8 @@ class Solver:
                   self._alloc_cb, self._free_cb, None)
         h = C.c_void_p()
         create = self._lib.bte_create_band if decomp == "band" else self._lib.bte_create
+        if self.umesh:
+            create = self._lib.bte_create_umesh
         st = create(C.byref(m), C.byref(d), C.byref(b), C.byref(run), C.byref(h))
         self._h = h
         if st != BTE_OK:
@@ -243,6 +263,12 @@ class Solver:
             return
         Tw = _f64(T_wall)
         self._check(self._lib.bte_set_bc(self._h, int(region), int(kind), _p(Tw), float(T_uniform)))
+
+    def region_faces(self, region: int) -> int:
+        """Boundary faces of wall region 0..5 (the T_wall length of set_bc)."""
+        n = C.c_int64()
+        self._check(self._lib.bte_get_region_faces(self._h, int(region), C.byref(n)))
+        return int(n.value)
 
     def set_wall(self, region: int, bc) -> None:
         """Apply a wall description (kind, T_wall, T_uniform[, specularity])."""

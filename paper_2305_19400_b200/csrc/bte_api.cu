@@ -107,6 +107,13 @@ struct bte_ctx {
   std::vector<char> nt_pending;
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;  // boundary planes swept / halo delivered
   int overlap = 1;  // env BTE_OVERLAP=0: exchange after the whole sweep
+  // unstructured mesh (bte_create_umesh): the layout sees one plane of ncells
+  int umesh = 0;
+  UMeshDev u{};
+  std::vector<double> uvol;  // V_c
+  std::vector<double> uKd;   // per direction: max_c sum_{f: s.an > 0} s.an (dt check)
+  double *d_ucen = nullptr;  // [nc][3] centroids (random start)
+  double ulo[3] = {0, 0, 0}, uL[3] = {0, 0, 0};
   // NCCL
   bte_slab_plan plan{};
   void *nccl_comm = nullptr;
@@ -171,7 +178,10 @@ static bte_status check_dt(bte_ctx *ctx) {
     const double be = host_beta(ctx, b, ctx->Tmax);
     for (int d = 0; d < ctx->nd; ++d) {
       double k = 0;
-      for (int a = 0; a < na; ++a) k += std::fabs(ctx->s[3 * d + a]) / D[a];
+      if (ctx->umesh)
+        k = ctx->uKd[d];  // general mesh: the largest outflow factor of direction d
+      else
+        for (int a = 0; a < na; ++a) k += std::fabs(ctx->s[3 * d + a]) / D[a];
       worst = std::min(worst, 1.0 - ctx->dt * be - ctx->dt * ctx->v[b] * k);
     }
   }
@@ -199,6 +209,7 @@ static bte_status refresh(bte_ctx *ctx) {
 static int64_t ncl_of(const bte_ctx *ctx) { return ctx->ncells_local; }
 
 static int64_t n_faces_global(const bte_ctx *ctx, int region) {
+  if (ctx->umesh) return ctx->u.rn[region];
   const int a = region / 2;
   const bte_mesh &m = ctx->mesh;
   if (a == 0) return m.ny * m.nz;
@@ -281,8 +292,191 @@ bte_status bte_plan_band(int nb, int nparts, int part, int *b0, int *b1) {
   return BTE_OK;
 }
 
+struct UHost;
 static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
-                              const bte_run *run, bool band, bte_ctx **out);
+                              const bte_run *run, bool band, bte_ctx **out, const UHost *uh = nullptr);
+
+// ---- unstructured simplex meshes: host geometry precompute (a0)
+struct UHost {
+  int dim = 0, K = 0;
+  int64_t nc = 0;
+  std::vector<int64_t> nbr;   // [nc][K]
+  std::vector<double> an;     // [nc][K][3] A_f n_f / V_c
+  std::vector<double> vol;    // [nc]
+  std::vector<double> cen;    // [nc][3]
+  std::vector<int64_t> rcell[6];
+  double lo[3], L[3];
+};
+
+// Eq. 3 geometry without square roots: triangle A_f n_f / V_c = 2 perp(edge) /
+// |cross| (depth cancels), tetrahedron = 3 cross(b - a, c - a) / |det|, each
+// oriented away from the opposite vertex.  Faces matched by their vertex sets;
+// unmatched faces classified onto the box walls (region order -x,+x,-y,+y,-z,+z).
+static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
+  const int dim = um->dim, K = dim + 1;
+  const int64_t nc = um->ncells, nv = um->nverts;
+  h->dim = dim;
+  h->K = K;
+  h->nc = nc;
+  h->nbr.assign(nc * K, -1);
+  h->an.assign(nc * K * 3, 0.0);
+  h->vol.assign(nc, 0.0);
+  h->cen.assign(nc * 3, 0.0);
+  double hi[3];
+  for (int a = 0; a < 3; ++a) {
+    h->lo[a] = INFINITY;
+    hi[a] = -INFINITY;
+  }
+  for (int64_t i = 0; i < nv; ++i)
+    for (int a = 0; a < 3; ++a) {
+      h->lo[a] = std::min(h->lo[a], um->verts[3 * i + a]);
+      hi[a] = std::max(hi[a], um->verts[3 * i + a]);
+    }
+  for (int a = 0; a < 3; ++a) h->L[a] = hi[a] - h->lo[a];
+  struct FaceKey {
+    int64_t v[3];
+    int64_t slot;  // c*K + k
+  };
+  std::vector<FaceKey> keys(nc * K);
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t *cv = um->cells + c * K;
+    const double *X[4];
+    for (int k = 0; k < K; ++k) {
+      if (cv[k] < 0 || cv[k] >= nv) {
+        *err = "cell " + std::to_string(c) + ": vertex index out of range";
+        return false;
+      }
+      X[k] = um->verts + 3 * cv[k];
+    }
+    double cen[3] = {X[0][0], X[0][1], X[0][2]};
+    for (int k = 1; k < K; ++k)
+      for (int a = 0; a < 3; ++a) cen[a] = cen[a] + X[k][a];
+    for (int a = 0; a < 3; ++a) h->cen[3 * c + a] = cen[a] / K;
+    double scale = 0.0;  // 2/|cross| or 3/|det|
+    if (dim == 2) {
+      const double cr = (X[1][0] - X[0][0]) * (X[2][1] - X[0][1]) - (X[1][1] - X[0][1]) * (X[2][0] - X[0][0]);
+      h->vol[c] = std::fabs(cr) * 0.5 * um->depth;
+      scale = 2.0 / std::fabs(cr);
+    } else {
+      double e[3][3];
+      for (int r = 0; r < 3; ++r)
+        for (int a = 0; a < 3; ++a) e[r][a] = X[r + 1][a] - X[0][a];
+      const double det = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                         e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                         e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+      h->vol[c] = std::fabs(det) / 6.0;
+      scale = 3.0 / std::fabs(det);
+    }
+    if (!(h->vol[c] > 0.0) || !std::isfinite(scale)) {
+      *err = "cell " + std::to_string(c) + " is degenerate (zero volume)";
+      return false;
+    }
+    for (int k = 0; k < K; ++k) {
+      int q[3], n = 0;
+      for (int i = 0; i < K; ++i)
+        if (i != k) q[n++] = i;
+      double An[3];
+      if (dim == 2) {
+        const double ex = X[q[1]][0] - X[q[0]][0], ey = X[q[1]][1] - X[q[0]][1];
+        An[0] = ey;
+        An[1] = -ex;
+        An[2] = 0.0;
+      } else {
+        double u[3], w[3];
+        for (int a = 0; a < 3; ++a) {
+          u[a] = X[q[1]][a] - X[q[0]][a];
+          w[a] = X[q[2]][a] - X[q[0]][a];
+        }
+        An[0] = u[1] * w[2] - u[2] * w[1];
+        An[1] = u[2] * w[0] - u[0] * w[2];
+        An[2] = u[0] * w[1] - u[1] * w[0];
+      }
+      double o = 0.0;
+      for (int a = 0; a < 3; ++a) o += An[a] * (X[k][a] - X[q[0]][a]);
+      const double sg = o > 0.0 ? -scale : scale;
+      for (int a = 0; a < 3; ++a) h->an[(c * K + k) * 3 + a] = sg * An[a];
+      FaceKey &fk = keys[c * K + k];
+      int64_t vv[3] = {cv[q[0]], cv[q[1]], dim == 3 ? cv[q[2]] : -1};
+      std::sort(vv, vv + (dim == 3 ? 3 : 2));
+      for (int a = 0; a < 3; ++a) fk.v[a] = vv[a];
+      fk.slot = c * K + k;
+    }
+  }
+  std::sort(keys.begin(), keys.end(), [](const FaceKey &x, const FaceKey &y) {
+    if (x.v[0] != y.v[0]) return x.v[0] < y.v[0];
+    if (x.v[1] != y.v[1]) return x.v[1] < y.v[1];
+    if (x.v[2] != y.v[2]) return x.v[2] < y.v[2];
+    return x.slot < y.slot;
+  });
+  for (size_t i = 0; i < keys.size();) {
+    size_t j = i + 1;
+    while (j < keys.size() && keys[j].v[0] == keys[i].v[0] && keys[j].v[1] == keys[i].v[1] &&
+           keys[j].v[2] == keys[i].v[2])
+      ++j;
+    if (j - i > 2) {
+      *err = "a face is shared by more than two cells";
+      return false;
+    }
+    if (j - i == 2) {
+      h->nbr[keys[i].slot] = keys[i + 1].slot / K;
+      h->nbr[keys[i + 1].slot] = keys[i].slot / K;
+    }
+    i = j;
+  }
+  int64_t count[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t c = 0; c < nc; ++c)
+    for (int k = 0; k < K; ++k) {
+      if (h->nbr[c * K + k] >= 0) continue;
+      const int64_t *cv = um->cells + c * K;
+      int reg = -1;
+      for (int r = 0; r < 2 * dim && reg < 0; ++r) {
+        const int a = r / 2;
+        const double wall = (r & 1) ? hi[a] : h->lo[a];
+        bool on = true;
+        for (int i = 0; i < K; ++i)
+          if (i != k && um->verts[3 * cv[i] + a] != wall) on = false;
+        if (on) reg = r;
+      }
+      if (reg < 0) {
+        *err = "cell " + std::to_string(c) + " face " + std::to_string(k) + ": boundary face off the box walls";
+        return false;
+      }
+      h->nbr[c * K + k] = -1 - (count[reg] * 8 + reg);
+      h->rcell[reg].push_back(c);
+      ++count[reg];
+    }
+  return true;
+}
+
+bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte_bands *bands, const bte_run *run,
+                            bte_ctx **out) {
+  if (!out) return BTE_EINVAL;
+  *out = nullptr;
+  auto early = [&](const char *msg) {
+    bte_ctx *c = new bte_ctx();
+    c->err = msg;
+    *out = c;
+    return BTE_EINVAL;
+  };
+  if (!um || !um->verts || !um->cells) return early("null unstructured mesh");
+  if (um->dim != 2 && um->dim != 3) return early("unstructured dim must be 2 (triangles) or 3 (tetrahedra)");
+  if (um->ncells < 1 || um->nverts < um->dim + 1) return early("empty unstructured mesh");
+  if (um->ncells > (1ll << 30)) return early("unstructured mesh too large");
+  if (um->dim == 2 && !(um->depth > 0)) return early("depth must be > 0");
+  if (run && run->nranks != 1) return early("unstructured contexts are single-rank (nranks must be 1)");
+  UHost uh;
+  std::string err;
+  if (!build_uhost(um, &uh, &err)) return early(err.c_str());
+  // the state layout sees one plane of ncells cross cells
+  bte_mesh fm{um->dim, um->ncells, 1, 1, 1.0, 1.0, 1.0};
+  return create_impl(&fm, dirs, bands, run, false, out, &uh);
+}
+
+bte_status bte_get_region_faces(const bte_ctx *ctx, int region, int64_t *nfaces) {
+  if (!ctx || !nfaces || region < 0 || region >= 6) return BTE_EINVAL;
+  *nfaces = n_faces_global(ctx, region);
+  return BTE_OK;
+}
 
 bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands, const bte_run *run,
                       bte_ctx **out) {
@@ -295,7 +489,7 @@ bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, const bte
 }
 
 static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
-                              const bte_run *run, bool band, bte_ctx **out) {
+                              const bte_run *run, bool band, bte_ctx **out, const UHost *uh) {
   if (!out) return BTE_EINVAL;
   *out = nullptr;
   bte_ctx *ctx = new bte_ctx();
@@ -518,6 +712,32 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     imax = 0;
   }
 
+  if (uh) {
+    ctx->umesh = 1;
+    ctx->uvol = uh->vol;
+    ctx->uKd.assign(ctx->nd, 0.0);
+    for (int d = 0; d < ctx->nd; ++d) {
+      const double *sd = &ctx->s[3 * d];
+      double kmax = 0.0;
+      for (int64_t c = 0; c < uh->nc; ++c) {
+        double k = 0.0;
+        for (int f = 0; f < uh->K; ++f) {
+          const double *an = &uh->an[(c * uh->K + f) * 3];
+          const double sa = fma(sd[2], an[2], fma(sd[1], an[1], sd[0] * an[0]));
+          if (sa > 0.0) k += sa;
+        }
+        kmax = std::max(kmax, k);
+      }
+      ctx->uKd[d] = kmax;
+    }
+    for (int a = 0; a < 3; ++a) {
+      ctx->ulo[a] = uh->lo[a];
+      ctx->uL[a] = uh->L[a];
+    }
+    ctx->u.K = uh->K;
+    ctx->u.ncells = uh->nc;
+    for (int r = 0; r < 6; ++r) ctx->u.rn[r] = (int64_t)uh->rcell[r].size();
+  }
   if ((st = check_dt(ctx)) != BTE_OK) return bail(st);
 
   // ---- device allocations
@@ -598,6 +818,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     const size_t other = (size_t)ncl_of(ctx) * (nslot * ctx->nb + 4 * nbT + 2) * sizeof(double) + (2ull << 30);
     ctx->rot = 2 * ibytes + other > freeb ? 1 : 0;
     if (const char *e = getenv("BTE_ROTATE")) ctx->rot = atoi(e) ? 1 : 0;
+    if (ctx->umesh) ctx->rot = 0;  // unstructured: two buffers
   }
   for (int sl = 0; sl < kMaxSlots; ++sl) g.slot_off[sl] = (int64_t)sl * g.slot_stride;
   g.rot = ctx->rot;
@@ -653,6 +874,28 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
       if (sg * sa < 0.0) q[octant_of(&ctx->s[3 * d])] += ctx->w[d] * std::fabs(sa);
     }
     g.diff_den[r] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+  }
+  if (uh) {  // unstructured tables (a0)
+    int64_t *d_nbr = nullptr;
+    double *d_an = nullptr, *d_sw = nullptr;
+    if ((st = upload(ctx, &d_nbr, uh->nbr.data(), uh->nbr.size()))) return bail(st);
+    if ((st = upload(ctx, &d_an, uh->an.data(), uh->an.size()))) return bail(st);
+    if ((st = upload(ctx, &ctx->d_ucen, uh->cen.data(), uh->cen.size()))) return bail(st);
+    std::vector<double> sw(4 * (size_t)ctx->nd);
+    for (int sj = 0; sj < ctx->nd; ++sj) {
+      const int d = ctx->canon_d[sj];
+      for (int a = 0; a < 3; ++a) sw[4 * sj + a] = ctx->s[3 * d + a];
+      sw[4 * sj + 3] = ctx->w[d];
+    }
+    if ((st = upload(ctx, &d_sw, sw.data(), sw.size()))) return bail(st);
+    ctx->u.nbr = d_nbr;
+    ctx->u.an = d_an;
+    ctx->u.sw = d_sw;
+    for (int r = 0; r < 6; ++r) {
+      int64_t *d_rc = nullptr;
+      if ((st = upload(ctx, &d_rc, uh->rcell[r].data(), uh->rcell[r].size()))) return bail(st);
+      ctx->u.rcell[r] = d_rc;
+    }
   }
   if (const char *e = getenv("BTE_SWEEP")) ctx->use_tma = strcmp(e, "plain") != 0;
   if (const char *e = getenv("BTE_STAGES")) ctx->stages_override = atoi(e);
@@ -857,7 +1100,11 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
   }
   if (!(T_mean - std::fabs(T_amp) > 0)) return fail(ctx, BTE_EINVAL, "random start would give T <= 0");
   const bte_mesh &m = ctx->mesh;
-  CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
+  if (ctx->umesh)
+    CU(launch_random_T_u(ctx->ncells_local, m.dim, ctx->d_ucen, ctx->ulo, ctx->uL, phase, T_mean, T_amp, ctx->T,
+                         ctx->stream));
+  else
+    CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
   if ((st = refresh(ctx))) return st;
   CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0s, ctx->I[ctx->cur], ctx->stream));
   if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
@@ -875,7 +1122,10 @@ static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
     const int a = r / 2;
     if (a == g.dim - 1 && !((r & 1) ? g.has_hi_wall : g.has_lo_wall)) continue;
     if (g.kind[r] == BC_DIFF || g.kind[r] == BC_PART) {
-      CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
+      if (ctx->umesh)
+        CU(launch_udiffuse(g, ctx->u, Icur, r, ctx->gtab[r], ctx->stream));
+      else
+        CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
       ++n;
     }
     if ((g.kind[r] == BC_SPEC || g.kind[r] == BC_PART) && ctx->rot) {
@@ -941,6 +1191,27 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
 static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
                                     int *fused, int col0 = 0, int ncols = 0, int p_lo = 0, int p_hi = 0,
                                     int seg_len = 0) {
+  if (ctx->umesh) {
+    *fused = 0;
+    USweepArgs a{};
+    a.g = ctx->g;
+    a.u = ctx->u;
+    a.Iin = Iin;
+    a.Iout = Iout;
+    a.I0c = ctx->I0s;
+    a.beta = ctx->betas;
+    a.Dpart = ctx->Dpart;
+    a.v = ctx->m.v;
+    a.dt = ctx->dt;
+    a.target_threads = ctx->target_threads;
+    a.pipelined = ctx->use_tma;
+    a.stages = ctx->stages_override;
+    a.chunk = ctx->seg_override;
+    CU(launch_usweep(a, ctx->stream));
+    ctx->tacc.launches++;
+    ctx->tacc.sweep_launches++;
+    return BTE_OK;
+  }
   if (ctx->rot) {
     // octant-slot rotation: octant k is swept from its region into the spare
     // region, whose old occupant's region becomes the next spare; the octants
@@ -1057,7 +1328,7 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
 // are swept (SURVEY 8(e) overlap schedule).
 static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   const bool has_bnd = n_diffuse(ctx) > 0;
-  const int C = (ctx->fuse_newton || ctx->rot) ? 1 : ctx->nchunks;
+  const int C = (ctx->fuse_newton || ctx->rot || ctx->umesh) ? 1 : ctx->nchunks;
   const int ncross = ctx->g.ncross;
   const int np = ctx->g.nplanes;
   bte_status st;
@@ -1433,7 +1704,9 @@ bte_status bte_get_energy(bte_ctx *ctx, double *E) {
   CU(cudaStreamSynchronize(ctx->stream));
   CU(cudaFree(d_E));
   const bte_mesh &m = ctx->mesh;
-  const double V = m.dx * m.dy * m.dz;
+  const double V = ctx->umesh ? 1.0 : m.dx * m.dy * m.dz;
+  if (ctx->umesh)
+    for (int64_t c = 0; c < ncl; ++c) h[c] *= ctx->uvol[c];
   double s = 0, comp = 0;  // Kahan
   for (double x : h) {
     const double y = x - comp;

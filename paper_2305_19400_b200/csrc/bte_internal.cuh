@@ -135,6 +135,33 @@ struct SweepArgs {
   int *done;              // [nseg][ncross] tickets, zero between launches
 };
 
+// Unstructured simplex mesh, device view.  The state layout
+// is the structured one with one "plane" of ncells cross cells:
+// I[slot][cell][j][b], (cell, slot) blocks of Es doubles.
+struct UMeshDev {
+  int K;                  // faces per cell (dim + 1)
+  int64_t ncells;
+  const int64_t *nbr;     // [nc][K]: neighbour >= 0, or -1 - (face_in_region * 8 + region)
+  const double *an;       // [nc][K][3]: (A_f / V_c) n_f
+  const double *sw;       // [nslot * nj][4]: s_x, s_y, s_z, w of direction (slot, j)
+  const int64_t *rcell[6];  // wall face -> cell
+  int64_t rn[6];          // wall faces per region
+};
+
+struct USweepArgs {
+  Geometry g;
+  UMeshDev u;
+  const double *Iin;
+  double *Iout;
+  const double *I0c, *beta;
+  double *Dpart;
+  const double *v;
+  double dt;
+  int jpt, jg;
+  int target_threads;
+  int pipelined;          // k_usweep_tma (default) vs the one-CTA-per-cell k_usweep
+  int stages, chunk;      // pipeline depth and cells per CTA (0 = automatic)
+};
 
 // kernels / launchers (kernels.cu)
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused);
@@ -162,6 +189,11 @@ cudaError_t launch_dpart_from_I(const Geometry &g, const double *I, const double
                                cudaStream_t s);
 cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, double *Ec,
                           cudaStream_t s);
+cudaError_t launch_usweep(const USweepArgs &a, cudaStream_t s);
+cudaError_t launch_udiffuse(const Geometry &g, const UMeshDev &u, const double *I, int region, double *gtab,
+                            cudaStream_t s);
+cudaError_t launch_random_T_u(int64_t nc, int dim, const double *cen, const double *lo, const double *L,
+                              const double *phase, double T_mean, double T_amp, double *T, cudaStream_t s);
 cudaError_t launch_band_partial(const Geometry &g, const Material &mF, const double *Dpart, const double *T,
                                 int64_t nc, double *S, cudaStream_t s);
 

@@ -914,12 +914,10 @@ static int64_t wall_faces_local(const Geometry &g, int region) {
   return axis == 0 ? g.nplanes : g.nx;
 }
 
-__global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
-                          double *__restrict__ gtab) {
+__device__ __forceinline__ void diffuse_face(const Geometry &g, const double *__restrict__ I, int region,
+                                             int64_t face, int64_t cell_base, double *__restrict__ gtab) {
   const int axis = region >> 1;
   const bool hi = region & 1;
-  int64_t face, cell_base;
-  wall_face(g, region, blockIdx.x, &face, &cell_base);
   // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
   const int bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
@@ -939,6 +937,13 @@ __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int re
     const double num = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     gtab[face * g.nb + b] = num / g.diff_den[region];
   }
+}
+
+__global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
+                          double *__restrict__ gtab) {
+  int64_t face, cell_base;
+  wall_face(g, region, blockIdx.x, &face, &cell_base);
+  diffuse_face(g, I, region, face, cell_base, gtab);
 }
 
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
@@ -1630,6 +1635,365 @@ cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, d
   const int64_t nc = (int64_t)g.nplanes * g.ncross;
   if (nc == 0) return cudaSuccess;
   k_energy<<<(unsigned)((nc + 3) / 4), 128, 0, s>>>(g, I, v, Ec);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- unstructured meshes
+
+// Eq. 3 on a simplex: one CTA per (cell, octant slot).  The CTA
+// first forms a_{f,j} = dt * s_j . (A_f n_f / V_c) for its K faces and nj
+// directions in shared memory; thread (grp, b) then updates channel b of
+// directions [grp*jpt, grp*jpt + jpt):
+//   I' = I + dt beta (I0c - I) - v_b sum_f a_{f,j} I_up,
+//   I_up = I (own) if a > 0, else the neighbour's value (same slot, j, b) or
+//   the wall ghost (P:L150-157 strict ">").
+// Neighbour reads are 8*nb-byte coalesced rows of the neighbour's block; the
+// octant partial sum over j feeds the same Dpart[c][slot][b] as the
+// structured sweep (fixed order: within a thread ascending j, then groups).
+template <int JMAX>
+__global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
+  extern __shared__ double sm[];  // a[K][nj] | red[JG*nb]
+  __shared__ int64_t snbr[4];
+  const Geometry &g = A.g;
+  const UMeshDev &u = A.u;
+  const int nb = g.nb, nj = g.nj, Es = g.Es, K = u.K;
+  const int tid = threadIdx.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = A.jg;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+  const int64_t cell = blockIdx.x;
+  const int slot = blockIdx.y;
+  double *a = sm;
+  double *red = sm + 4 * nj;
+  if (tid < K) snbr[tid] = u.nbr[cell * K + tid];
+  for (int i = tid; i < K * nj; i += blockDim.x) {
+    const int f = i / nj, j = i - f * nj;
+    const double *sv = u.sw + (int64_t)(slot * nj + j) * 4;
+    const double *an = u.an + (cell * K + f) * 3;
+    a[f * nj + j] = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
+  }
+  __syncthreads();
+  const bool active = grp < JG;
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + g.slot_off[slot];
+  const int64_t base = cell * Es;
+  double acc = 0.0;
+  if (active) {
+    const double I0 = __ldg(A.I0c + cell * nb + b);
+    const double dtb = A.dt * __ldg(A.beta + cell * nb + b);
+    const double v = A.v[b];
+    double Ic[JMAX], up[JMAX][4];
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {  // issue every load of the cell first
+      if (k < nloc) {
+        const int j = j0 + k;
+        const int e = j * nb + b;
+        Ic[k] = __ldg(Is + base + e);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          up[k][f] = 0.0;
+          if (f < K && !(a[f * nj + j] > 0.0)) {
+            const int64_t n = snbr[f];
+            if (n >= 0) up[k][f] = __ldg(Is + n * Es + e);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      if (k < nloc) {
+        const int j = j0 + k;
+        const int e = j * nb + b;
+        double flux = 0.0;
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          if (f < K) {
+            const double af = a[f * nj + j];
+            double w;
+            if (af > 0.0) {
+              w = Ic[k];
+            } else {
+              const int64_t n = snbr[f];
+              if (n >= 0) {
+                w = up[k][f];
+              } else {
+                const int64_t code = -1 - n;
+                w = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, b);
+              }
+            }
+            flux = fma(af, w, flux);
+          }
+        }
+        const double In = fma(dtb, I0 - Ic[k], Ic[k]) - v * flux;
+        Os[base + e] = In;
+        acc = fma(u.sw[(int64_t)(slot * nj + j) * 4 + 3], I0 - In, acc);
+      }
+    }
+    red[tid] = acc;
+  }
+  __syncthreads();
+  if (tid < nb) {
+    double s = 0.0;
+    for (int q = 0; q < JG; ++q) s += red[q * nb + tid];
+    A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
+  }
+}
+
+// Pipelined unstructured sweep: one CTA per (chunk of Q consecutive cells,
+// octant slot), ~1000 threads (jpt = 2), walking its cells in order.
+//  - the cell's own (cell, slot) block (the DRAM stream) arrives by
+//    cp.async.bulk into an S-stage ring issued S cells ahead (one thread);
+//  - the neighbour values (L2: adjacent cells in the order are read by this
+//    or a concurrently running CTA) are loaded into registers one cell ahead;
+//  - the face coefficients a_{f,j} = dt s_j.(A_f n_f / V_c) and neighbour
+//    indices of cell i+2 are formed in shared memory while cell i computes.
+// Same arithmetic and summation order as k_usweep (bitwise identical results).
+template <int JMAX, int KF>
+__global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const Geometry &g = A.g;
+  const UMeshDev &u = A.u;
+  const int nb = g.nb, nj = g.nj, Es = g.Es, E = g.E;
+  const int S = A.stages, Q = A.chunk;
+  const int tid = threadIdx.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = A.jg;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+  const bool active = grp < JG;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);                  // [S]
+  double *stg = reinterpret_cast<double *>(smraw + 128);                // [S][Es]
+  double *ring_a = stg + (size_t)S * Es;                                // [4][KF][nj]
+  double *red = ring_a + 4 * KF * nj;                                   // [2][JG*nb]
+  int64_t *ring_n = reinterpret_cast<int64_t *>(red + 2 * JG * nb);     // [4][KF]
+  double *sws = reinterpret_cast<double *>(ring_n + 4 * KF);            // [nj][4]
+  const int slot = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * Q;
+  const int n = (int)min((int64_t)Q, u.ncells - c0);
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + g.slot_off[slot];
+
+  auto issue = [&](int i) {
+    const int st = i % S;
+    mbar_expect_tx(&full[st], (uint32_t)E * 8u);
+    bulk_g2s(stg + (size_t)st * Es, Is + (c0 + i) * Es, (uint32_t)E * 8u, &full[st]);
+  };
+  // a / nbr of cell i into ring entry i & 3 (threads tid < KF*nj, tid < KF)
+  auto faces = [&](int i) {
+    if (i >= n) return;
+    const int64_t cell = c0 + i;
+    double *ra = ring_a + (i & 3) * KF * nj;
+    for (int t = tid; t < KF * nj; t += blockDim.x) {
+      const int f = t / nj, j = t - f * nj;
+      const double *an = u.an + (cell * KF + f) * 3;
+      const double *sv = sws + 4 * j;
+      ra[t] = A.dt * fma(sv[2], __ldg(an + 2), fma(sv[1], __ldg(an + 1), sv[0] * __ldg(an)));
+    }
+    if (tid < KF) ring_n[(i & 3) * KF + tid] = __ldg(u.nbr + cell * KF + tid);
+  };
+
+  for (int t = tid; t < 4 * nj; t += blockDim.x) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  faces(0);
+  faces(1);
+  if (tid == 0)
+    for (int i = 0; i < min(S, n); ++i) issue(i);
+  __syncthreads();
+
+  const double v = A.v[active ? b : 0];
+  const int e0 = j0 * nb + b;
+  double upC[JMAX][KF], upN[JMAX][KF];
+  double I0C = 0.0, btC = 0.0, I0N = 0.0, btN = 0.0;
+  auto prefetch = [&](int i, double (&up)[JMAX][KF], double &I0, double &bt) {
+    if (!active || i >= n) return;
+    const int64_t cell = c0 + i;
+    const double *ra = ring_a + (i & 3) * KF * nj;
+    const int64_t *rn = ring_n + (i & 3) * KF;
+    I0 = __ldg(A.I0c + cell * nb + b);
+    bt = __ldg(A.beta + cell * nb + b);
+#pragma unroll
+    for (int f = 0; f < KF; ++f) {
+      const int64_t nbf = rn[f];
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        up[k][f] = 0.0;
+        if (k < nloc && nbf >= 0 && !(ra[f * nj + j0 + k] > 0.0)) up[k][f] = __ldg(Is + nbf * Es + e0 + k * nb);
+      }
+    }
+  };
+  prefetch(0, upC, I0C, btC);
+
+  for (int i = 0; i < n; ++i) {
+    const int64_t cell = c0 + i;
+    const int st = i % S;
+    prefetch(i + 1, upN, I0N, btN);
+    double acc = 0.0;
+    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    if (active) {
+      const double *ra = ring_a + (i & 3) * KF * nj;
+      const int64_t *rn = ring_n + (i & 3) * KF;
+      const double *own = stg + (size_t)st * Es;
+      const double dtb = A.dt * btC;
+      const int64_t base = cell * Es;
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        if (k < nloc) {
+          const int j = j0 + k;
+          const int e = e0 + k * nb;
+          const double Ic = own[e];
+          double flux = 0.0;
+#pragma unroll
+          for (int f = 0; f < KF; ++f) {
+            const double af = ra[f * nj + j];
+            double w;
+            if (af > 0.0) {
+              w = Ic;
+            } else if (rn[f] >= 0) {
+              w = upC[k][f];
+            } else {
+              const int64_t code = -1 - rn[f];
+              w = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, b);
+            }
+            flux = fma(af, w, flux);
+          }
+          const double In = fma(dtb, I0C - Ic, Ic) - v * flux;
+          __stcs(Os + base + e, In);
+          acc = fma(sws[4 * j + 3], I0C - In, acc);
+        }
+      }
+      red[(i & 1) * JG * nb + tid] = acc;
+    }
+    faces(i + 2);
+    __syncthreads();  // stage st consumed, red complete, ring entry (i+2)&3 written
+    if (tid == 0 && i + S < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S);
+    }
+    if (tid < nb) {
+      const double *rb = red + (i & 1) * JG * nb;
+      double sum = 0.0;
+      for (int q = 0; q < JG; ++q) sum += rb[q * nb + tid];
+      A.Dpart[(cell * g.nslot + slot) * nb + tid] = sum;
+    }
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k)
+#pragma unroll
+      for (int f = 0; f < KF; ++f) upC[k][f] = upN[k][f];
+    I0C = I0N;
+    btC = btN;
+  }
+}
+
+cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
+  USweepArgs a = a0;
+  const Geometry &g = a.g;
+  if (a.u.ncells == 0) return cudaSuccess;
+  if (a.pipelined && g.Es % 2 == 0) {
+    int jpt, JG;
+    sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 1000, &jpt, &JG);
+    const int threads = JG * g.nb;
+    const int jc = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : 0;
+    if (threads <= 1024 && jc > 0) {
+      a.jpt = jpt;
+      a.jg = JG;
+      a.chunk = a.chunk > 0 ? a.chunk : 128;
+      const size_t fixed = 128 + (4 * (size_t)a.u.K * g.nj + 2 * (size_t)threads + 4 * (size_t)g.nj) * sizeof(double) +
+                           4 * (size_t)a.u.K * sizeof(int64_t);
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)200 * 1024 - fixed) / ((size_t)g.Es * 8));
+      S = std::max(2, std::min(12, S));
+      a.stages = S;
+      const size_t smem = fixed + (size_t)S * g.Es * 8;
+      if (smem <= 227 * 1024) {
+        dim3 grid((unsigned)((a.u.ncells + a.chunk - 1) / a.chunk), g.nslot);
+#define BTE_UTMA(N, KK)                                                                              \
+  if (jc == N && a.u.K == KK) {                                                                      \
+    cudaFuncSetAttribute(k_usweep_tma<N, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_usweep_tma<N, KK><<<grid, threads, smem, s>>>(a);                                              \
+    return cudaGetLastError();                                                                       \
+  }
+        BTE_UTMA(1, 3)
+        BTE_UTMA(2, 3)
+        BTE_UTMA(4, 3)
+        BTE_UTMA(1, 4)
+        BTE_UTMA(2, 4)
+        BTE_UTMA(4, 4)
+#undef BTE_UTMA
+      }
+    }
+  }
+  int jpt, JG;
+  sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 448, &jpt, &JG);
+  a.jpt = jpt;
+  a.jg = JG;
+  const int threads = JG * g.nb;
+  if (threads > 1024) return cudaErrorInvalidConfiguration;
+  const size_t smem = (4 * (size_t)g.nj + (size_t)threads) * sizeof(double);
+  dim3 grid((unsigned)a.u.ncells, g.nslot);
+  const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
+  switch (jcase) {
+#define BTE_UCASE(N)                                                                    \
+  case N:                                                                               \
+    if (smem > 48 * 1024)                                                               \
+      cudaFuncSetAttribute(k_usweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           (int)smem);                                                  \
+    k_usweep<N><<<grid, threads, smem, s>>>(a);                                         \
+    break;
+    BTE_UCASE(1)
+    BTE_UCASE(2)
+    BTE_UCASE(4)
+    BTE_UCASE(5)
+    BTE_UCASE(8)
+    BTE_UCASE(10)
+    BTE_UCASE(16)
+#undef BTE_UCASE
+    default:
+      return cudaErrorInvalidConfiguration;
+  }
+  return cudaGetLastError();
+}
+
+__global__ void k_udiffuse(const Geometry g, const UMeshDev u, const double *__restrict__ I, int region,
+                           double *__restrict__ gtab) {
+  const int64_t f = blockIdx.x;
+  diffuse_face(g, I, region, f, u.rcell[region][f] * g.Es, gtab);
+}
+
+cudaError_t launch_udiffuse(const Geometry &g, const UMeshDev &u, const double *I, int region, double *gtab,
+                            cudaStream_t s) {
+  const int64_t nf = u.rn[region];
+  if (nf == 0) return cudaSuccess;
+  int threads = ((g.nb + 31) / 32) * 32;
+  if (threads > 256) threads = 256;
+  k_udiffuse<<<(unsigned)nf, threads, 0, s>>>(g, u, I, region, gtab);
+  return cudaGetLastError();
+}
+
+// random start on an unstructured mesh: the structured recipe with the
+// centroid (measured from the box corner lo) in place of the cell centre
+__global__ void k_random_T_u(int64_t nc, int dim, const double *__restrict__ cen, double lo0, double lo1,
+                             double lo2, double L0, double L1, double L2, double p0, double p1, double p2,
+                             double T_mean, double T_amp, double *__restrict__ T) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const double twopi = 6.283185307179586;
+  const double fx = sin(twopi * ((cen[3 * c] - lo0) / L0 + p0));
+  const double fy = sin(twopi * ((cen[3 * c + 1] - lo1) / L1 + p1));
+  const double fz = dim == 3 ? sin(twopi * ((cen[3 * c + 2] - lo2) / L2 + p2)) : 1.0;
+  T[c] = T_mean + T_amp * (fz * fy * fx);
+}
+
+cudaError_t launch_random_T_u(int64_t nc, int dim, const double *cen, const double *lo, const double *L,
+                              const double *phase, double T_mean, double T_amp, double *T, cudaStream_t s) {
+  if (nc == 0) return cudaSuccess;
+  k_random_T_u<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, dim, cen, lo[0], lo[1], lo[2], L[0], L[1], L[2],
+                                                            phase[0], phase[1], phase[2], T_mean, T_amp, T);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,182 @@
+"""GPU parity on unstructured simplex meshes: the CUDA path
+(bte_create_umesh through the C ABI) against the CPU oracle
+(oracle/bte_oracle_umesh.c) on the same seeded inputs.  Tolerances as for the
+structured path (BASELINE.json north_star): max relative error 1e-10 on
+intensities, 1e-8 K absolute on temperature."""
+import numpy as np
+import pytest
+
+import bte_inputs as bi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+REL_I = 1e-10
+ABS_T = 1e-8
+
+
+@pytest.fixture(scope="module")
+def Solver():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_19400_b200 import Solver as S, build
+    build.build()
+    return S
+
+
+def _cmp(Ig, Tg, Io, To):
+    return float(np.max(np.abs(Ig - Io) / np.abs(Io))), float(np.max(np.abs(Tg - To)))
+
+
+def _run_both(Solver, p, nsteps, solve_T=False):
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    with Solver.from_problem(p) as sv:
+        for r in range(2 * p.mesh.dim):
+            assert sv.region_faces(r) == o.n_region_faces(r)
+        if solve_T:
+            sv.set_state(I, None)
+            T, I0c, betac = o.solve_T(I, np.full(p.mesh.ncells, p.T_init))
+            assert np.max(np.abs(sv.temperature() - T)) <= ABS_T
+            Io, To, _, _ = o.run(I, T, nsteps, I0c, betac)
+        else:
+            sv.set_state(I, T)
+            Io, To, _, _ = o.run(I, T, nsteps)
+        sv.step(nsteps)
+        Ig, Tg = sv.intensity(), sv.temperature()
+    return _cmp(Ig, Tg, Io, To)
+
+
+def _walls(p):
+    o = oracle.Oracle(p)
+    nf = o.n_region_faces(2)
+    return [bi.WallBC(bi.BC_SPECULAR), bi.WallBC(bi.BC_DIFFUSE),
+            bi.WallBC(bi.BC_ISOTHERMAL, 300.0 + 10.0 * np.linspace(0, 1, nf)),
+            bi.WallBC(bi.BC_PARTIAL, specularity=0.35), bi.WallBC(bi.BC_ISOTHERMAL, None, 298.0),
+            bi.WallBC(bi.BC_DIFFUSE)]
+
+
+@pytest.mark.parametrize("dim,n,shuffle", [(2, (5, 4, 1), False), (2, (7, 3, 1), True), (3, (3, 2, 2), False),
+                                           (3, (2, 3, 3), True)])
+def test_umesh_parity_all_wall_kinds(Solver, dim, n, shuffle):
+    p = bi.small_umesh(dim, n, shuffle=shuffle)
+    p.bcs = _walls(p)
+    rel, dT = _run_both(Solver, p, 8)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_umesh_parity_set_state_solves_T(Solver):
+    p = bi.small_umesh(3, (3, 3, 2))
+    rel, dT = _run_both(Solver, p, 4, solve_T=True)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+@pytest.mark.parametrize("case", ["u2", "u3"])
+def test_umesh_parity_silicon_400x40_reduced(Solver, case):
+    """The bench workloads' directions (400) and channels (40) on reduced meshes."""
+    p = bi.config_u2(n=10) if case == "u2" else bi.config_u3(n=3)
+    rel, dT = _run_both(Solver, p, 3)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_umesh_full_size_u2(Solver):
+    """bench workload u2 at full size (28,800 triangles x 400 x 40), 2 steps, full field."""
+    p = bi.config_u2()
+    rel, dT = _run_both(Solver, p, 2)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_umesh_init_random_matches_recipe(Solver):
+    p = bi.small_umesh(3, (3, 2, 2))
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    with Solver.from_problem(p) as sv:
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        Tg, Ig = sv.temperature(), sv.intensity()
+    assert np.max(np.abs(Tg - T)) < 1e-10
+    assert np.max(np.abs(Ig / I - 1)) < 1e-12
+
+
+@pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE, bi.BC_PARTIAL])
+def test_umesh_closed_box_energy(Solver, kind):
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    p = bi.small_umesh(3, (3, 3, 2), bands=b, bcs=[bi.WallBC(kind, specularity=0.6) for _ in range(6)],
+                       dirs=bi.directions_control_angle(2, 8))
+    I, _ = oracle.Oracle(p).random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, None)
+        E0 = sv.energy()
+        sv.step(200)
+        E1 = sv.energy()
+    assert abs(E1 / E0 - 1) < 1e-12, E1 / E0 - 1
+    assert abs(E0 / oracle.Oracle(p).energy(I) - 1) < 1e-13
+
+
+def test_umesh_full_size_u3_properties(Solver):
+    """bench workload u3 at full size (196,608 tetrahedra x 400 x 40): closed
+    specular box conserves energy; a uniform equilibrium stays fixed."""
+    p = bi.config_u3()
+    p.bcs = bi.uniform_bcs(bi.BC_SPECULAR)
+    with Solver.from_problem(p) as sv:
+        T0 = sv.temperature()
+        sv.step(2)
+        assert np.max(np.abs(sv.temperature() - T0)) < 1e-10
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        sv.step(1)  # afterwards (I, T) satisfy the Newton balance (conservation holds from here)
+        E0 = sv.energy()
+        sv.step(3)
+        E1 = sv.energy()
+    assert abs(E1 / E0 - 1) < 1e-12
+
+
+def test_umesh_fixed_point_and_errors(Solver):
+    from paper_2305_19400_b200 import BteError
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 20, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 300.0), bi.WallBC(3, specularity=0.5),
+           bi.WallBC(1), bi.WallBC(0, None, 300.0)]
+    p = bi.small_umesh(3, (3, 2, 2), bands=b, bcs=bcs)
+    with Solver.from_problem(p) as sv:
+        I0, T0 = sv.intensity(), sv.temperature()
+        sv.step(20)
+        assert np.max(np.abs(sv.intensity() / I0 - 1)) < 1e-14
+        assert np.max(np.abs(sv.temperature() - T0)) < 1e-10
+    q = bi.small_umesh(2, (3, 2, 1))
+    q.dt = 1e-9  # violates the positivity bound
+    with pytest.raises(BteError) as e:
+        Solver.from_problem(q)
+    assert e.value.status == 5
+    q = bi.small_umesh(2, (3, 2, 1))
+    q.mesh.cells = q.mesh.cells.copy()
+    q.mesh.cells[0, 1] = q.mesh.cells[0, 0]  # degenerate triangle
+    with pytest.raises(BteError) as e:
+        Solver.from_problem(q)
+    assert e.value.status == 1
+    q = bi.small_umesh(2, (3, 2, 1))
+    q.mesh.cells = q.mesh.cells[1:].copy()  # a hole: interior faces become boundary faces off the walls
+    with pytest.raises(BteError) as e:
+        Solver.from_problem(q)
+    assert e.value.status == 1
+    with pytest.raises(ValueError):
+        Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=0, nranks=2)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
+    """The pipelined sweep (k_usweep_tma: TMA ring + register prefetch, several
+    chunk sizes and pipeline depths) and the one-CTA-per-cell sweep give
+    bitwise identical results."""
+    p = bi.config_u2(n=9) if dim == 2 else bi.config_u3(n=3)
+    I, T = oracle.Oracle(p).random_state()
+    out = []
+    for env in ({"BTE_SWEEP": "plain"}, {}, {"BTE_SEGS": "5", "BTE_STAGES": "2"}, {"BTE_SEGS": "1000"}):
+        for k in ("BTE_SWEEP", "BTE_SEGS", "BTE_STAGES"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(3)
+            out.append((sv.intensity(), sv.temperature()))
+    for Ix, Tx in out[1:]:
+        assert np.array_equal(Ix, out[0][0]) and np.array_equal(Tx, out[0][1])
