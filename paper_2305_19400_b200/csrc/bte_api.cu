@@ -878,8 +878,17 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   if (uh) {  // unstructured tables (a0)
     int64_t *d_nbr = nullptr;
     double *d_an = nullptr, *d_sw = nullptr;
-    if ((st = upload(ctx, &d_nbr, uh->nbr.data(), uh->nbr.size()))) return bail(st);
-    if ((st = upload(ctx, &d_an, uh->an.data(), uh->an.size()))) return bail(st);
+    // device rows padded to 4 faces: nbr [nc][4] (32 B), an [nc][4][3] (96 B), so
+    // that the pipelined sweep moves them with 16-B bulk copies
+    std::vector<int64_t> nbr4(4 * (size_t)uh->nc, -1);
+    std::vector<double> an4(12 * (size_t)uh->nc, 0.0);
+    for (int64_t c = 0; c < uh->nc; ++c)
+      for (int f = 0; f < uh->K; ++f) {
+        nbr4[4 * c + f] = uh->nbr[c * uh->K + f];
+        for (int a = 0; a < 3; ++a) an4[12 * c + 3 * f + a] = uh->an[(c * uh->K + f) * 3 + a];
+      }
+    if ((st = upload(ctx, &d_nbr, nbr4.data(), nbr4.size()))) return bail(st);
+    if ((st = upload(ctx, &d_an, an4.data(), an4.size()))) return bail(st);
     if ((st = upload(ctx, &ctx->d_ucen, uh->cen.data(), uh->cen.size()))) return bail(st);
     std::vector<double> sw(4 * (size_t)ctx->nd);
     for (int sj = 0; sj < ctx->nd; ++sj) {

@@ -141,8 +141,8 @@ struct SweepArgs {
 struct UMeshDev {
   int K;                  // faces per cell (dim + 1)
   int64_t ncells;
-  const int64_t *nbr;     // [nc][K]: neighbour >= 0, or -1 - (face_in_region * 8 + region)
-  const double *an;       // [nc][K][3]: (A_f / V_c) n_f
+  const int64_t *nbr;     // [nc][4] (faces >= K unused): neighbour >= 0, or -1 - (face_in_region * 8 + region)
+  const double *an;       // [nc][4][3] (faces >= K unused): (A_f / V_c) n_f
   const double *sw;       // [nslot * nj][4]: s_x, s_y, s_z, w of direction (slot, j)
   const int64_t *rcell[6];  // wall face -> cell
   int64_t rn[6];          // wall faces per region

@@ -1667,11 +1667,11 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
   const int slot = blockIdx.y;
   double *a = sm;
   double *red = sm + 4 * nj;
-  if (tid < K) snbr[tid] = u.nbr[cell * K + tid];
+  if (tid < K) snbr[tid] = u.nbr[cell * 4 + tid];
   for (int i = tid; i < K * nj; i += blockDim.x) {
     const int f = i / nj, j = i - f * nj;
     const double *sv = u.sw + (int64_t)(slot * nj + j) * 4;
-    const double *an = u.an + (cell * K + f) * 3;
+    const double *an = u.an + cell * 12 + f * 3;
     a[f * nj + j] = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
   }
   __syncthreads();
@@ -1742,34 +1742,46 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 }
 
 // Pipelined unstructured sweep: one CTA per (chunk of Q consecutive cells,
-// octant slot), ~1000 threads (jpt = 2), walking its cells in order.
-//  - the cell's own (cell, slot) block (the DRAM stream) arrives by
-//    cp.async.bulk into an S-stage ring issued S cells ahead (one thread);
-//  - the neighbour values (L2: adjacent cells in the order are read by this
-//    or a concurrently running CTA) are loaded into registers one cell ahead;
-//  - the face coefficients a_{f,j} = dt s_j.(A_f n_f / V_c) and neighbour
-//    indices of cell i+2 are formed in shared memory while cell i computes.
-// Same arithmetic and summation order as k_usweep (bitwise identical results).
-template <int JMAX, int KF>
+// octant slot) walking its cells in order; thread (jg, q) owns the channel
+// pair (2q, 2q+1) of directions j = jg + r*JG (16-B loads and stores).
+//  - stage i (S-deep ring, cp.async.bulk issued S cells ahead by one thread):
+//    the cell's own (cell, slot) block (the DRAM stream), its I0c and beta
+//    rows, its face rows A_f n_f / V_c and neighbour indices;
+//  - per-direction face lists of cell i+2 (threads j < nj): a_f = dt s_j.(A_f
+//    n_f / V_c), the outflow sum aout = sum_{a_f > 0} a_f and the inflow faces
+//    (coefficient, source offset or wall code), in a 4-entry ring;
+//  - the inflow neighbour values of cell i+1 are loaded into registers while
+//    cell i computes (L2: adjacent cells are read by this or a concurrently
+//    running CTA);
+//  - I' = I + dt beta (I0c - I) - v (aout I + sum_in a_f I_up): the face sum of
+//    Eq. 3 regrouped (outflow faces first), within the parity tolerance;
+//  - octant partials: per-thread, then 8 contiguous group ranges ascending,
+//    then the fixed tree ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)); cell i's
+//    partial is finalised after the next barrier.
+constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
+
+template <int JPT, int KF>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const UMeshDev &u = A.u;
   const int nb = g.nb, nj = g.nj, Es = g.Es, E = g.E;
+  const int NBP = nb >> 1;
   const int S = A.stages, Q = A.chunk;
   const int tid = threadIdx.x;
-  const int grp = tid / nb;
-  const int b = tid - grp * nb;
+  const int q = tid % NBP;
+  const int jg = tid / NBP;
   const int JG = A.jg;
-  const int j0 = grp * A.jpt;
-  const int nloc = max(0, min(A.jpt, nj - j0));
-  const bool active = grp < JG;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);                  // [S]
-  double *stg = reinterpret_cast<double *>(smraw + 128);                // [S][Es]
-  double *ring_a = stg + (size_t)S * Es;                                // [4][KF][nj]
-  double *red = ring_a + 4 * KF * nj;                                   // [2][JG*nb]
-  int64_t *ring_n = reinterpret_cast<int64_t *>(red + 2 * JG * nb);     // [4][KF]
-  double *sws = reinterpret_cast<double *>(ring_n + 4 * KF);            // [nj][4]
+  const bool active = jg < JG;
+  // stage layout (doubles): own[Es] | I0[nb] | beta[nb] | an[12] | nbr[4] (int64)
+  const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 12;
+  const int sd = o_nb + 4;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);        // [S]
+  double *stg = reinterpret_cast<double *>(smraw + 128);      // [S][sd]
+  double *red = stg + (size_t)S * sd;                         // [2][JG][nb]
+  double *red2 = red + 2 * JG * nb;                           // [2][8][nb]
+  double *sws = red2 + 2 * 8 * nb;                            // [nj][4]
+  double *fl = sws + 4 * nj;                                  // [4][nj][kUW]
   const int slot = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * Q;
   const int n = (int)min((int64_t)Q, u.ncells - c0);
@@ -1778,116 +1790,154 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
 
   auto issue = [&](int i) {
     const int st = i % S;
-    mbar_expect_tx(&full[st], (uint32_t)E * 8u);
-    bulk_g2s(stg + (size_t)st * Es, Is + (c0 + i) * Es, (uint32_t)E * 8u, &full[st]);
-  };
-  // a / nbr of cell i into ring entry i & 3 (threads tid < KF*nj, tid < KF)
-  auto faces = [&](int i) {
-    if (i >= n) return;
     const int64_t cell = c0 + i;
-    double *ra = ring_a + (i & 3) * KF * nj;
-    for (int t = tid; t < KF * nj; t += blockDim.x) {
-      const int f = t / nj, j = t - f * nj;
-      const double *an = u.an + (cell * KF + f) * 3;
-      const double *sv = sws + 4 * j;
-      ra[t] = A.dt * fma(sv[2], __ldg(an + 2), fma(sv[1], __ldg(an + 1), sv[0] * __ldg(an)));
+    double *sp = stg + (size_t)st * sd;
+    mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + 16) * 8u);
+    bulk_g2s(sp, Is + cell * Es, (uint32_t)E * 8u, &full[st]);
+    bulk_g2s(sp + o_i0, A.I0c + cell * nb, (uint32_t)nb * 8u, &full[st]);
+    bulk_g2s(sp + o_be, A.beta + cell * nb, (uint32_t)nb * 8u, &full[st]);
+    bulk_g2s(sp + o_an, u.an + cell * 12, 96u, &full[st]);
+    bulk_g2s(sp + o_nb, u.nbr + cell * 4, 32u, &full[st]);
+  };
+  // face lists of cell i (threads tid < nj), from its stage
+  auto prep = [&](int i) {
+    if (i >= n || tid >= nj) return;
+    const int st = i % S;
+    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    const double *sp = stg + (size_t)st * sd;
+    const int64_t *rn = reinterpret_cast<const int64_t *>(sp + o_nb);
+    const double *sv = sws + 4 * tid;
+    double *w = fl + ((size_t)(i & 3) * nj + tid) * kUW;
+    int64_t *wi = reinterpret_cast<int64_t *>(w);
+    double aout = 0.0;
+    int nin = 0;
+#pragma unroll
+    for (int f = 0; f < KF; ++f) {
+      const double *an = sp + o_an + 3 * f;
+      const double a = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
+      if (a > 0.0) {
+        aout += a;
+      } else {
+        w[2 + nin] = a;
+        wi[6 + nin] = rn[f] >= 0 ? rn[f] * Es : rn[f];  // source block offset, or the wall code (< 0)
+        ++nin;
+      }
     }
-    if (tid < KF) ring_n[(i & 3) * KF + tid] = __ldg(u.nbr + cell * KF + tid);
+    w[0] = aout;
+    wi[1] = nin;
   };
 
   for (int t = tid; t < 4 * nj; t += blockDim.x) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < min(S, n); ++i) issue(i);
   }
   __syncthreads();
-  faces(0);
-  faces(1);
-  if (tid == 0)
-    for (int i = 0; i < min(S, n); ++i) issue(i);
+  prep(0);
+  prep(1);
   __syncthreads();
 
-  const double v = A.v[active ? b : 0];
-  const int e0 = j0 * nb + b;
-  double upC[JMAX][KF], upN[JMAX][KF];
-  double I0C = 0.0, btC = 0.0, I0N = 0.0, btN = 0.0;
-  auto prefetch = [&](int i, double (&up)[JMAX][KF], double &I0, double &bt) {
+  const double2 v2 = make_double2(A.v[2 * q], A.v[2 * q + 1]);
+  double2 upC[JPT][KF], upN[JPT][KF];
+  auto prefetch = [&](int i, double2 (&up)[JPT][KF]) {
     if (!active || i >= n) return;
-    const int64_t cell = c0 + i;
-    const double *ra = ring_a + (i & 3) * KF * nj;
-    const int64_t *rn = ring_n + (i & 3) * KF;
-    I0 = __ldg(A.I0c + cell * nb + b);
-    bt = __ldg(A.beta + cell * nb + b);
 #pragma unroll
-    for (int f = 0; f < KF; ++f) {
-      const int64_t nbf = rn[f];
+    for (int r = 0; r < JPT; ++r) {
+      const int j = jg + r * JG;
+      if (j < nj) {
+        const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
+        const int64_t *wi = reinterpret_cast<const int64_t *>(w);
+        const int nin = (int)wi[1];
 #pragma unroll
-      for (int k = 0; k < JMAX; ++k) {
-        up[k][f] = 0.0;
-        if (k < nloc && nbf >= 0 && !(ra[f * nj + j0 + k] > 0.0)) up[k][f] = __ldg(Is + nbf * Es + e0 + k * nb);
+        for (int f = 0; f < KF; ++f)
+          if (f < nin && wi[6 + f] >= 0)
+            up[r][f] = __ldg(reinterpret_cast<const double2 *>(Is + wi[6 + f] + j * nb) + q);
       }
     }
   };
-  prefetch(0, upC, I0C, btC);
+  prefetch(0, upC);
 
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
     const int st = i % S;
-    prefetch(i + 1, upN, I0N, btN);
-    double acc = 0.0;
+    prefetch(i + 1, upN);
+    double2 acc = make_double2(0.0, 0.0);
     mbar_wait(&full[st], (uint32_t)((i / S) & 1));
     if (active) {
-      const double *ra = ring_a + (i & 3) * KF * nj;
-      const int64_t *rn = ring_n + (i & 3) * KF;
-      const double *own = stg + (size_t)st * Es;
-      const double dtb = A.dt * btC;
+      const double *sp = stg + (size_t)st * sd;
+      const double2 I0 = reinterpret_cast<const double2 *>(sp + o_i0)[q];
+      const double2 be = reinterpret_cast<const double2 *>(sp + o_be)[q];
+      const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
 #pragma unroll
-      for (int k = 0; k < JMAX; ++k) {
-        if (k < nloc) {
-          const int j = j0 + k;
-          const int e = e0 + k * nb;
-          const double Ic = own[e];
-          double flux = 0.0;
+      for (int r = 0; r < JPT; ++r) {
+        const int j = jg + r * JG;
+        if (j < nj) {
+          const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
+          const int64_t *wi = reinterpret_cast<const int64_t *>(w);
+          const int nin = (int)wi[1];
+          const double2 Ic = reinterpret_cast<const double2 *>(sp + j * nb)[q];
+          double f0 = w[0] * Ic.x, f1 = w[0] * Ic.y;
 #pragma unroll
           for (int f = 0; f < KF; ++f) {
-            const double af = ra[f * nj + j];
-            double w;
-            if (af > 0.0) {
-              w = Ic;
-            } else if (rn[f] >= 0) {
-              w = upC[k][f];
-            } else {
-              const int64_t code = -1 - rn[f];
-              w = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, b);
+            if (f < nin) {
+              const double a = w[2 + f];
+              const int64_t src = wi[6 + f];
+              double2 up;
+              if (src >= 0) {
+                up = upC[r][f];
+              } else {
+                const int64_t code = -1 - src;
+                up.x = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, 2 * q);
+                up.y = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, 2 * q + 1);
+              }
+              f0 = fma(a, up.x, f0);
+              f1 = fma(a, up.y, f1);
             }
-            flux = fma(af, w, flux);
           }
-          const double In = fma(dtb, I0C - Ic, Ic) - v * flux;
-          __stcs(Os + base + e, In);
-          acc = fma(sws[4 * j + 3], I0C - In, acc);
+          double2 In;
+          In.x = fma(dtb0, I0.x - Ic.x, Ic.x) - v2.x * f0;
+          In.y = fma(dtb1, I0.y - Ic.y, Ic.y) - v2.y * f1;
+          __stcs(reinterpret_cast<double2 *>(Os + base + j * nb) + q, In);
+          const double wj = sws[4 * j + 3];
+          acc.x = fma(wj, I0.x - In.x, acc.x);
+          acc.y = fma(wj, I0.y - In.y, acc.y);
         }
       }
-      red[(i & 1) * JG * nb + tid] = acc;
+      reinterpret_cast<double2 *>(red + (size_t)(i & 1) * JG * nb + jg * nb)[q] = acc;
     }
-    faces(i + 2);
-    __syncthreads();  // stage st consumed, red complete, ring entry (i+2)&3 written
+    prep(i + 2);
+    __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
     if (tid == 0 && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
     }
-    if (tid < nb) {
-      const double *rb = red + (i & 1) * JG * nb;
+    // octant partials: 8 contiguous group ranges of cell i; finalise cell i-1
+    if (tid < 8 * nb) {
+      const int b = tid % nb, p = tid / nb;
+      const int ga = (p * JG) >> 3, gb = ((p + 1) * JG) >> 3;
+      const double *rb = red + (size_t)(i & 1) * JG * nb;
       double sum = 0.0;
-      for (int q = 0; q < JG; ++q) sum += rb[q * nb + tid];
-      A.Dpart[(cell * g.nslot + slot) * nb + tid] = sum;
+      for (int gq = ga; gq < gb; ++gq) sum += rb[gq * nb + b];
+      red2[((i & 1) * 8 + p) * nb + b] = sum;
+    }
+    if (i > 0 && tid >= 8 * nb && tid < 9 * nb) {
+      const int b = tid - 8 * nb;
+      const double *r2 = red2 + ((i - 1) & 1) * 8 * nb + b;
+      A.Dpart[((cell - 1) * g.nslot + slot) * nb + b] =
+          ((r2[0] + r2[nb]) + (r2[2 * nb] + r2[3 * nb])) + ((r2[4 * nb] + r2[5 * nb]) + (r2[6 * nb] + r2[7 * nb]));
     }
 #pragma unroll
-    for (int k = 0; k < JMAX; ++k)
+    for (int r = 0; r < JPT; ++r)
 #pragma unroll
-      for (int f = 0; f < KF; ++f) upC[k][f] = upN[k][f];
-    I0C = I0N;
-    btC = btN;
+      for (int f = 0; f < KF; ++f) upC[r][f] = upN[r][f];
+  }
+  __syncthreads();
+  if (n > 0 && tid < nb) {
+    const double *r2 = red2 + ((n - 1) & 1) * 8 * nb + tid;
+    A.Dpart[((c0 + n - 1) * g.nslot + slot) * nb + tid] =
+        ((r2[0] + r2[nb]) + (r2[2 * nb] + r2[3 * nb])) + ((r2[4 * nb] + r2[5 * nb]) + (r2[6 * nb] + r2[7 * nb]));
   }
 }
 
@@ -1895,35 +1945,36 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   USweepArgs a = a0;
   const Geometry &g = a.g;
   if (a.u.ncells == 0) return cudaSuccess;
-  if (a.pipelined && g.Es % 2 == 0) {
-    int jpt, JG;
-    sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 1000, &jpt, &JG);
-    const int threads = JG * g.nb;
-    const int jc = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : 0;
-    if (threads <= 1024 && jc > 0) {
+  if (a.pipelined && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
+    const int NBP = g.nb / 2;
+    const int tgt = a.target_threads > 0 ? a.target_threads : 1024;
+    int JG = std::max(1, std::min(g.nj, tgt / NBP));
+    const int jpt = (g.nj + JG - 1) / JG;
+    JG = (g.nj + jpt - 1) / jpt;
+    const int threads = std::max(JG * NBP, 9 * g.nb);
+    if (jpt <= 2 && threads <= 1024 && JG >= 8) {
       a.jpt = jpt;
       a.jg = JG;
-      a.chunk = a.chunk > 0 ? a.chunk : 128;
-      const size_t fixed = 128 + (4 * (size_t)a.u.K * g.nj + 2 * (size_t)threads + 4 * (size_t)g.nj) * sizeof(double) +
-                           4 * (size_t)a.u.K * sizeof(int64_t);
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)200 * 1024 - fixed) / ((size_t)g.Es * 8));
-      S = std::max(2, std::min(12, S));
+      a.chunk = a.chunk > 0 ? a.chunk : 32;
+      const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
+                                  4 * (size_t)g.nj * kUW) * sizeof(double);
+      const size_t sd = (size_t)g.Es + 2 * g.nb + 16;
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)200 * 1024 - fixed) / (sd * 8));
+      S = std::max(3, std::min(12, S));
       a.stages = S;
-      const size_t smem = fixed + (size_t)S * g.Es * 8;
+      const size_t smem = fixed + (size_t)S * sd * 8;
       if (smem <= 227 * 1024) {
         dim3 grid((unsigned)((a.u.ncells + a.chunk - 1) / a.chunk), g.nslot);
 #define BTE_UTMA(N, KK)                                                                              \
-  if (jc == N && a.u.K == KK) {                                                                      \
+  if (jpt == N && a.u.K == KK) {                                                                     \
     cudaFuncSetAttribute(k_usweep_tma<N, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k_usweep_tma<N, KK><<<grid, threads, smem, s>>>(a);                                              \
     return cudaGetLastError();                                                                       \
   }
         BTE_UTMA(1, 3)
         BTE_UTMA(2, 3)
-        BTE_UTMA(4, 3)
         BTE_UTMA(1, 4)
         BTE_UTMA(2, 4)
-        BTE_UTMA(4, 4)
 #undef BTE_UTMA
       }
     }

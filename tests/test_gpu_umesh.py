@@ -163,9 +163,10 @@ def test_umesh_fixed_point_and_errors(Solver):
 
 @pytest.mark.parametrize("dim", [2, 3])
 def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
-    """The pipelined sweep (k_usweep_tma: TMA ring + register prefetch, several
-    chunk sizes and pipeline depths) and the one-CTA-per-cell sweep give
-    bitwise identical results."""
+    """The pipelined sweep (k_usweep_tma: TMA ring + register prefetch) is
+    bitwise identical across chunk sizes and pipeline depths, and agrees with
+    the one-CTA-per-cell k_usweep to rounding (the two group the face and
+    direction sums differently)."""
     p = bi.config_u2(n=9) if dim == 2 else bi.config_u3(n=3)
     I, T = oracle.Oracle(p).random_state()
     out = []
@@ -178,5 +179,7 @@ def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
             sv.set_state(I, T)
             sv.step(3)
             out.append((sv.intensity(), sv.temperature()))
-    for Ix, Tx in out[1:]:
-        assert np.array_equal(Ix, out[0][0]) and np.array_equal(Tx, out[0][1])
+    for Ix, Tx in out[2:]:
+        assert np.array_equal(Ix, out[1][0]) and np.array_equal(Tx, out[1][1])
+    assert np.max(np.abs(out[1][0] / out[0][0] - 1)) < 1e-13
+    assert np.max(np.abs(out[1][1] - out[0][1])) < 1e-10
