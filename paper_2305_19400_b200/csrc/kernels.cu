@@ -1767,7 +1767,8 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   const UMeshDev &u = A.u;
   const int nb = g.nb, nj = g.nj, Es = g.Es, E = g.E;
   const int NBP = nb >> 1;
-  const int S = A.stages, Q = A.chunk;
+  const int S = A.stages, Q = A.chunk;  // S: power of two
+  const int Sm = S - 1, Sl = __ffs(S) - 1;
   const int tid = threadIdx.x;
   const int q = tid % NBP;
   const int jg = tid / NBP;
@@ -1789,7 +1790,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   double *__restrict__ Os = A.Iout + g.slot_off[slot];
 
   auto issue = [&](int i) {
-    const int st = i % S;
+    const int st = i & Sm;
     const int64_t cell = c0 + i;
     double *sp = stg + (size_t)st * sd;
     mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + 16) * 8u);
@@ -1802,8 +1803,8 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   // face lists of cell i (threads tid < nj), from its stage
   auto prep = [&](int i) {
     if (i >= n || tid >= nj) return;
-    const int st = i % S;
-    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    const int st = i & Sm;
+    mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     const double *sp = stg + (size_t)st * sd;
     const int64_t *rn = reinterpret_cast<const int64_t *>(sp + o_nb);
     const double *sv = sws + 4 * tid;
@@ -1860,10 +1861,10 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
 
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
-    const int st = i % S;
+    const int st = i & Sm;
     prefetch(i + 1, upN);
     double2 acc = make_double2(0.0, 0.0);
-    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
       const double2 I0 = reinterpret_cast<const double2 *>(sp + o_i0)[q];
@@ -1960,7 +1961,8 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
                                   4 * (size_t)g.nj * kUW) * sizeof(double);
       const size_t sd = (size_t)g.Es + 2 * g.nb + 16;
       int S = a.stages > 0 ? a.stages : (int)(((size_t)200 * 1024 - fixed) / (sd * 8));
-      S = std::max(3, std::min(12, S));
+      S = std::max(4, std::min(8, S));
+      while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;
       const size_t smem = fixed + (size_t)S * sd * 8;
       if (smem <= 227 * 1024) {

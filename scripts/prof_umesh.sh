@@ -4,7 +4,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 TAG=${TAG:-r03}
 for CFG in ${CFGS:-7 8}; do
-  for V in tma plain; do
+  for V in ${VARS:-tma plain}; do
     R=gpurun_out/prof_usweep_${V}_${TAG}_c${CFG}
     if [ $V = plain ]; then export BTE_SWEEP=plain; else unset BTE_SWEEP; fi
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_usweep -s 2 -c 1 \
