@@ -150,6 +150,7 @@ class Problem:
     bcs: List[WallBC]  # 6 entries (-x,+x,-y,+y,-z,+z); z entries ignored for dim 2
     nsteps: int = 100
     seed: int = 0
+    tau_mode: int = 0  # 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k)
 
     @property
     def dof(self) -> int:

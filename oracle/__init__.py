@@ -58,6 +58,7 @@ class _Problem(C.Structure):
         ("bc_kind", C.c_int * 6), ("T_wall", C.c_void_p * 6), ("T_uniform", C.c_double * 6),
         ("nthreads", C.c_int),
         ("specularity", C.c_double * 6),
+        ("tau_mode", C.c_int),
     ]
 
 
@@ -71,6 +72,9 @@ def lib():
         _lib.ora_I0.argtypes = [P, C.c_int, C.c_double, dp]
         _lib.ora_beta.restype = C.c_double
         _lib.ora_beta.argtypes = [P, C.c_int, C.c_double]
+        _lib.ora_dbeta.restype = C.c_double
+        _lib.ora_dbeta.argtypes = [P, C.c_int, C.c_double]
+        _lib.ora_newton_sc.argtypes = [P, C.c_double, C.c_void_p, C.c_void_p, dp, C.POINTER(C.c_int)]
         _lib.ora_energy.restype = C.c_double
         _lib.ora_energy.argtypes = [P, C.c_void_p]
         _lib.ora_dt_margin.restype = C.c_double
@@ -165,6 +169,7 @@ class Oracle:
             st.T_uniform[r] = bc.T_uniform
             st.specularity[r] = getattr(bc, "specularity", 1.0)
         st.nthreads = nthreads if nthreads else (os.cpu_count() or 1)
+        st.tau_mode = int(getattr(problem, "tau_mode", 0))
         self._st = st
         self.nc, self.nd, self.nb = m.ncells, d.nd, b.nb
         lib()
@@ -214,6 +219,19 @@ class Oracle:
 
     def beta(self, b: int, T: float) -> float:
         return lib().ora_beta(C.byref(self._st), b, T)
+
+    def dbeta(self, b: int, T: float) -> float:
+        return lib().ora_dbeta(C.byref(self._st), b, T)
+
+    def newton_sc(self, Tn: float, D, I0c):
+        """Self-consistent-tau Newton of one cell (reading R-k)."""
+        D, I0c = _f64(D), _f64(I0c)
+        T = C.c_double()
+        it = C.c_int()
+        st = lib().ora_newton_sc(C.byref(self._st), Tn, _ptr(D), _ptr(I0c), C.byref(T), C.byref(it))
+        if st:
+            raise OracleError(st, "newton_sc")
+        return T.value, it.value
 
     def I0_vec(self, T: np.ndarray) -> np.ndarray:
         T = np.asarray(T, dtype=np.float64).reshape(-1)

@@ -78,6 +78,7 @@ typedef struct {
   double T_uniform[6];
   int nthreads;
   double specularity[6]; /* BC_PART: fraction p of specular reflection */
+  int tau_mode;          /* 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k) */
 } ora_problem;
 
 /* ---------------------------------------------------------------- quadrature */
@@ -167,6 +168,18 @@ double ora_beta(const ora_problem *p, int b, double T) {
   const double *q = p->beta_coef + 5 * b;
   double r = q[0] + q[1] * T * T * T + q[2] * T * T * T * T;
   if (q[3] != 0.0) r += q[3] / sinh(q[4] / T);
+  return r;
+}
+
+/* d beta_b / dT of the expression above, term by term:
+ * 3 p3 T^2 + 4 p4 T^3 + pu theta cosh(theta/T) / (T^2 sinh^2(theta/T)) */
+double ora_dbeta(const ora_problem *p, int b, double T) {
+  const double *q = p->beta_coef + 5 * b;
+  double r = 3.0 * q[1] * T * T + 4.0 * q[2] * T * T * T;
+  if (q[3] != 0.0) {
+    double x = q[4] / T, sh = sinh(x);
+    r += q[3] * q[4] * cosh(x) / (T * T * sh * sh);
+  }
   return r;
 }
 
@@ -483,6 +496,50 @@ int ora_newton(const ora_problem *p, double Tn, const double *D, const double *I
   return ORA_ENEWTON;
 }
 
+/* Self-consistent tau (reading R-k, SURVEY f4 "non-lagged tau(T) inside the
+ * Newton"): solve
+ *   F(T) = sum_b (beta_b(T)/v_b) [ W (I0_b(T) - I0c_b) + D_b ] = 0
+ * with F'(T) = sum_b [ (beta_b'(T)/v_b)(W (I0_b - I0c_b) + D_b) + (beta_b/v_b) W dI0_b/dT ],
+ * the same bracket / step rules as ora_newton (F(Tn) == 0.0 keeps Tn). */
+int ora_newton_sc(const ora_problem *p, double Tn, const double *D, const double *I0c, double *Tout, int *iters) {
+  double W = 0.0;
+  for (int d = 0; d < p->nd; d++) W += p->w[d];
+  int nb = p->nb;
+  double T = Tn, lo = T_LO, hi = T_HI;
+  *iters = 0;
+  for (int it = 0; it <= NEWTON_MAXIT; it++) {
+    double F = 0.0, Fp = 0.0;
+    for (int b = 0; b < nb; b++) {
+      double dI0;
+      double i0 = ora_I0(p, b, T, &dI0);
+      double h = W * (i0 - I0c[b]) + D[b];
+      F += ora_beta(p, b, T) / p->v[b] * h;
+      Fp += ora_dbeta(p, b, T) / p->v[b] * h + ora_beta(p, b, T) / p->v[b] * W * dI0;
+    }
+    if (!isfinite(F) || !isfinite(Fp)) return ORA_ENONFINITE;
+    if (F == 0.0) {
+      *Tout = T;
+      return ORA_OK;
+    }
+    if (it == NEWTON_MAXIT) break;
+    if (F < 0.0)
+      lo = T;
+    else
+      hi = T;
+    double step = F / Fp;
+    double Tn1 = T - step;
+    *iters = it + 1;
+    if (fabs(step) <= NEWTON_RTOL * T) {
+      *Tout = Tn1;
+      return ORA_OK;
+    }
+    if (!(Tn1 > lo && Tn1 < hi) || !(Fp > 0.0)) Tn1 = 0.5 * (lo + hi);
+    T = Tn1;
+  }
+  *Tout = T;
+  return ORA_ENEWTON;
+}
+
 /* Temperature update over all cells: beta_next = beta(Tn) (lagged tau, reading
  * #15), Newton, then refresh I0c <- I0(T^{n+1}), betac <- beta_next (P:L277-281,
  * P:L498-500).  Returns first failing cell in *bad (or -1). */
@@ -498,7 +555,8 @@ int ora_temperature_update(const ora_problem *p, const double *D, double *T, dou
     for (int b = 0; b < nb; b++) bn[b] = ora_beta(p, b, T[c]);
     double Tnew;
     int it;
-    int st = ora_newton(p, T[c], D + c * nb, I0c + c * nb, bn, &Tnew, &it);
+    int st = p->tau_mode == 1 ? ora_newton_sc(p, T[c], D + c * nb, I0c + c * nb, &Tnew, &it)
+                              : ora_newton(p, T[c], D + c * nb, I0c + c * nb, bn, &Tnew, &it);
     if (it > mit) mit = it;
     if (st != ORA_OK) {
 #pragma omp critical
@@ -513,7 +571,7 @@ int ora_temperature_update(const ora_problem *p, const double *D, double *T, dou
     T[c] = Tnew;
     for (int b = 0; b < nb; b++) {
       I0c[c * nb + b] = ora_I0(p, b, Tnew, NULL);
-      betac[c * nb + b] = bn[b];
+      betac[c * nb + b] = p->tau_mode == 1 ? ora_beta(p, b, Tnew) : bn[b];
     }
   }
   if (bad) *bad = first_bad;

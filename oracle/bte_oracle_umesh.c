@@ -70,6 +70,7 @@ typedef struct {
   double T_uniform[6];
   int nthreads;
   double specularity[6];
+  int tau_mode;
 } ora_problem;
 
 double ora_I0(const ora_problem *p, int b, double T, double *dI0dT);

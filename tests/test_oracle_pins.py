@@ -721,3 +721,94 @@ def test_ustep_mirror_symmetry():
         assert abs(T2[c] - T2[m]) < 1e-9
     assert T2.max() > 300.0 + 1e-6
     assert order.size == mirror.size
+
+
+# ----------------------------------------------------------------- self-consistent tau (reading R-k)
+
+def test_dbeta_against_mpmath_derivative():
+    """d beta_b / dT against mpmath's numerical derivative of the closed form."""
+    b = bi.silicon_bands(29)
+    o = oracle.Oracle(bi.small_3d(bands=b))
+    mpmath.mp.dps = 40
+    for k in range(b.nb):
+        p0, p3, p4, pu, th = [mpmath.mpf(float(x)) for x in b.beta_coef[k]]
+
+        def beta(t):
+            r = p0 + p3 * t ** 3 + p4 * t ** 4
+            return r + (pu / mpmath.sinh(th / t) if pu != 0 else 0)
+
+        for T in (120.0, 300.0, 420.0):
+            ref = float(mpmath.diff(beta, mpmath.mpf(T)))
+            assert abs(o.dbeta(k, T) - ref) <= 1e-12 * abs(ref) + 1e-30, (k, T)
+
+
+def test_newton_sc_root_and_lagged_limit():
+    """The self-consistent Newton's T solves sum_b beta_b(T)/v_b [W(I0_b(T) - I0c_b) + D_b] = 0
+    (sign change of the mpmath-integral F within +-3e-8 K); with beta independent of
+    T it reduces to the lagged Newton bit for bit."""
+    b = bi.subset_bands(bi.silicon_bands(29), [1, 12, 27, 33, 38])
+    p = bi.small_3d(bands=b)
+    o = oracle.Oracle(p)
+    W = p.dirs.w.sum()
+    rng = np.random.default_rng(9)
+    for _ in range(3):
+        Tn = rng.uniform(280, 320)
+        I0c = np.array([o.I0(k, Tn)[0] for k in range(b.nb)])
+        D = W * I0c * rng.uniform(-0.03, 0.03, b.nb)
+        T, it = o.newton_sc(Tn, D, I0c)
+        assert it <= 8
+
+        def F(t):
+            return sum(o.beta(k, float(t)) / b.v[k] * (W * (_mp_I0(b, k, float(t)) - I0c[k]) + D[k])
+                       for k in range(b.nb))
+
+        h = 1e-10 * 300
+        assert F(T - h) < 0 < F(T + h), T
+        Tl, _ = o.newton(Tn, D, I0c, np.array([o.beta(k, Tn) for k in range(b.nb)]))
+        assert abs(Tl - T) > 1e-9  # the lag matters here
+    bc = b.beta_coef.copy()
+    bc[:, 1:] = 0.0  # tau independent of T
+    b2 = bi.Bands(b.v, b.mode, bc, w_lo=b.w_lo, w_hi=b.w_hi, vs=b.vs, c2=b.c2, g=b.g)
+    pl = bi.small_3d(bands=b2)
+    ps = bi.small_3d(bands=b2)
+    ps.tau_mode = 1
+    ol, osc = oracle.Oracle(pl), oracle.Oracle(ps)
+    I, T0 = ol.random_state()
+    Ia, Ta, _, ba = ol.run(I, T0, 4)
+    Ib, Tb, _, bb = osc.run(I, T0, 4)
+    assert np.array_equal(Ia, Ib) and np.array_equal(Ta, Tb) and np.array_equal(ba, bb)
+
+
+def test_sc_step_balances_at_new_temperature():
+    """After a self-consistent step, beta_c = beta(T^{n+1}) and the scattering
+    balance sum_b beta_b(T^{n+1})/v_b (W I0_b(T^{n+1}) - G_b) vanishes (G summed
+    here from the new intensities); under the lagged rule it does not."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 15, 30, 36])
+    res = {}
+    for mode in (0, 1):
+        p = bi.small_3d(4, 3, 3, bands=b)
+        p.tau_mode = mode
+        o = oracle.Oracle(p)
+        I, T = o.random_state()
+        I1, T1, I0c, betac = o.run(I, T, 1)
+        W = p.dirs.w.sum()
+        G = np.einsum("d,cdb->cb", p.dirs.w, I1)
+        bT = np.array([[o.beta(k, t) for k in range(b.nb)] for t in T1])
+        I0T = o.I0_vec(T1)
+        terms = bT / b.v * (W * I0T - G)
+        res[mode] = np.max(np.abs(terms.sum(axis=1)) / np.abs(terms).sum(axis=1))
+        if mode == 1:
+            assert np.array_equal(betac, bT)
+    assert res[1] < 1e-10 and res[0] > 1e-6, res
+
+
+def test_sc_closed_box_conservation():
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    p = bi.small_3d(5, 4, 3, bands=b, bcs=bi.uniform_bcs(bi.BC_DIFFUSE), dirs=bi.directions_control_angle(4, 16))
+    p.tau_mode = 1
+    o = oracle.Oracle(p)
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)
+    E0 = o.energy(I)
+    I2, _, _, _ = o.run(I, T, 300, I0c, betac)
+    assert abs(o.energy(I2) / E0 - 1) < 1e-12
