@@ -334,6 +334,8 @@ def run_b200(args):
     stream = torch.cuda.Stream(local)
     sv = Solver.from_problem(p, device=local, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id,
                              decomp=args.decomp)
+    if args.tau == "sc":
+        sv.set_tau_mode(1)
     dof_local = sv.ncells * sv.nd * sv.nb
     dof_global = sv.ncells_global * sv.nd * sv.nb_total
 
@@ -437,7 +439,7 @@ def run_b200(args):
             "scaling": "strong" if (band or args.config == 4) else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
             "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb_total,
-                       "dof_per_step": dof_global, "start": args.start, "dt": p.dt,
+                       "dof_per_step": dof_global, "start": args.start, "dt": p.dt, "tau": args.tau,
                        "parallelism": (f"band{world}" if band else f"slab{world}") if world > 1 else "single",
                        "storage": "octant-slot rotation" if sv.rotate else "two buffers",
                        "l2": f"inputs > L2 ({state_gb:.2f} GB/buffer vs 126 MB), no flush"},
@@ -463,6 +465,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--decomp", default="slab", choices=["slab", "band"])
+    ap.add_argument("--tau", default="lagged", choices=["lagged", "sc"],
+                    help="temperature update: lagged tau (reading #15) or self-consistent tau (R-k)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

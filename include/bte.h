@@ -204,6 +204,17 @@ typedef struct {
 BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                                     const bte_run *run, bte_ctx **out);
 
+/* Temperature-update rule for tau(T).
+ *   mode 0 (default, reading #15): lagged, beta_next = beta_b(T^n) weights the
+ *          Newton for T^{n+1} and the next sweep;
+ *   mode 1 (reading R-k): self-consistent, the Newton solves
+ *          sum_b (beta_b(T)/v_b) [W (I0_b(T) - I0c_b) + D_b] = 0 (beta' in F')
+ *          and the next sweep uses beta_b(T^{n+1}).
+ * Switching to mode 1 refreshes I0c and beta from the current T.  Identical
+ * results in both modes when beta does not depend on T.
+ * Errors: BTE_EINVAL (mode, band contexts, the fused-Newton variant). */
+BTE_API bte_status bte_set_tau_mode(bte_ctx *ctx, int mode);
+
 /* Number of boundary faces of wall region 0..5 (the T_wall length of
  * bte_set_bc) for structured and unstructured contexts.  Errors: BTE_EINVAL. */
 BTE_API bte_status bte_get_region_faces(const bte_ctx *ctx, int region, int64_t *nfaces);

@@ -108,6 +108,7 @@ struct bte_ctx {
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;  // boundary planes swept / halo delivered
   int overlap = 1;  // env BTE_OVERLAP=0: exchange after the whole sweep
   // unstructured mesh (bte_create_umesh): the layout sees one plane of ncells
+  int tau_mode = 0;  // 0 lagged tau (reading #15), 1 self-consistent (reading R-k)
   int umesh = 0;
   UMeshDev u{};
   std::vector<double> uvol;  // V_c
@@ -470,6 +471,21 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
   // the state layout sees one plane of ncells cross cells
   bte_mesh fm{um->dim, um->ncells, 1, 1, 1.0, 1.0, 1.0};
   return create_impl(&fm, dirs, bands, run, false, out, &uh);
+}
+
+bte_status bte_set_tau_mode(bte_ctx *ctx, int mode) {
+  if (!ctx) return BTE_EINVAL;
+  if (mode != 0 && mode != 1) return fail(ctx, BTE_EINVAL, "tau mode must be 0 (lagged) or 1 (self-consistent)");
+  if (mode == 1 && ctx->band)
+    return fail(ctx, BTE_EINVAL, "self-consistent tau needs every channel's reduction in the Newton (not band contexts)");
+  if (mode == 1 && ctx->fuse_newton) return fail(ctx, BTE_EINVAL, "self-consistent tau: unfused Newton only");
+  ctx->tau_mode = mode;
+  if (mode == 1) {  // I0c, dI0c, beta at the current T (the next sweep's beta is beta(T^n))
+    bte_status st = refresh(ctx);
+    if (st) return st;
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return BTE_OK;
 }
 
 bte_status bte_get_region_faces(const bte_ctx *ctx, int region, int64_t *nfaces) {
@@ -1305,7 +1321,10 @@ static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0, int ncols, cu
     a.col0 = col0;
     a.ncols = ncols;
   }
-  CU(launch_newton(a, stream ? stream : ctx->stream));
+  if (ctx->tau_mode == 1)
+    CU(launch_newton_sc(a, stream ? stream : ctx->stream));
+  else
+    CU(launch_newton(a, stream ? stream : ctx->stream));
   ctx->tacc.launches++;
   ctx->tacc.newton_launches++;
   return BTE_OK;

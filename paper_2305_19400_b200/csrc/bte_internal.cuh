@@ -166,6 +166,7 @@ struct USweepArgs {
 // kernels / launchers (kernels.cu)
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused);
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
+cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
                            cudaStream_t s);
 cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s);

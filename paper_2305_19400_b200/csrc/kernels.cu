@@ -29,6 +29,18 @@ __device__ __forceinline__ double beta_of_T(const double *__restrict__ bc, int b
   return r;
 }
 
+// d beta_b / dT: 3 p3 T^2 + 4 p4 T^3 + pu theta cosh(theta/T) / (T^2 sinh^2(theta/T))
+__device__ __forceinline__ double dbeta_of_T(const double *__restrict__ bc, int b, double T) {
+  const double *q = bc + 5 * b;
+  const double T2 = T * T;
+  double r = 3.0 * q[1] * T2 + 4.0 * q[2] * (T2 * T);
+  if (q[3] != 0.0) {
+    const double x = q[4] / T, sh = sinh(x);
+    r += q[3] * q[4] * cosh(x) / (T2 * (sh * sh));
+  }
+  return r;
+}
+
 // I0_b(T) and dI0_b/dT (reading #1).  BE: sum_j A_bj / expm1(X_bj / T),
 // derivative term A/em1 * (X/T)/T * (1 + 1/em1) = integrand * x/T * e^x/(e^x-1).
 __device__ __forceinline__ double I0_of_T(const Material &m, int b, double T, double *dI0) {
@@ -1341,6 +1353,116 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const Newton
     const int64_t p = q / ncol;
     newton_cell<BAND>(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, threadIdx.x & 31);
   }
+}
+
+// Self-consistent tau (reading R-k): one warp per cell, lanes
+// over channels (up to kScCh per lane), direct band integrals.  Solves
+//   F(T) = sum_b (beta_b(T)/v_b) [W (I0_b(T) - I0c_b) + D_b] = 0,
+//   F'(T) = sum_b [(beta_b'(T)/v_b)(W (I0_b - I0c_b) + D_b) + (beta_b/v_b) W dI0_b/dT],
+// with the bracket and step rules of the lagged Newton (reading #18, R-a; a
+// bisection also when F' <= 0), then refreshes I0c, dI0c and beta at T^{n+1}.
+constexpr int kScCh = kMaxBands / 32;
+
+__global__ void __launch_bounds__(256) k_newton_sc(const NewtonArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int nb = a.nb;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
+  for (int64_t qq = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); qq < nq; qq += nwarps) {
+    const int64_t pl = qq / ncol;
+    const int64_t c = a.col0 + (qq - pl * ncol) + pl * a.ncross;
+    const double Tn = a.T[c];
+    double D[kScCh], I0c[kScCh], i0v[kScCh], di0v[kScCh];
+#pragma unroll
+    for (int r = 0; r < kScCh; ++r) {
+      const int b = lane + 32 * r;
+      D[r] = 0.0;
+      I0c[r] = 0.0;
+      if (b < nb) {
+        double q[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+          const int sl = a.oct_slot[o];
+          q[o] = sl >= 0 ? __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b) : 0.0;
+        }
+        D[r] = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+        I0c[r] = a.I0c[c * nb + b];
+      }
+    }
+    double T = Tn, lo = kTlo, hi = kThi, Tf = Tn, evaluated_at = -1.0;
+    int status = ERR_NEWTON;
+    for (int it = 0; it <= kNewtonMaxIt; ++it) {
+      double f = 0.0, fp = 0.0;
+#pragma unroll
+      for (int r = 0; r < kScCh; ++r) {
+        const int b = lane + 32 * r;
+        if (b < nb) {
+          double d;
+          const double i0 = I0_of_T(a.m, b, T, &d);
+          i0v[r] = i0;
+          di0v[r] = d;
+          const double h = a.W * (i0 - I0c[r]) + D[r];
+          const double rv = a.m.rv[b];
+          f += beta_of_T(a.m.bcoef, b, T) * rv * h;
+          fp += dbeta_of_T(a.m.bcoef, b, T) * rv * h + beta_of_T(a.m.bcoef, b, T) * rv * (a.W * d);
+        }
+      }
+      const double F = warp_sum(f), Fp = warp_sum(fp);
+      evaluated_at = T;
+      if (!isfinite(F) || !isfinite(Fp)) {
+        status = ERR_NONFINITE;
+        break;
+      }
+      if (F == 0.0) {
+        Tf = T;
+        status = ERR_NONE;
+        break;
+      }
+      if (it == kNewtonMaxIt) break;
+      if (F < 0.0)
+        lo = T;
+      else
+        hi = T;
+      const double stp = F / Fp;
+      double Tn1 = T - stp;
+      if (fabs(stp) <= kNewtonRtol * T) {
+        Tf = Tn1;
+        status = ERR_NONE;
+        break;
+      }
+      if (!(Tn1 > lo && Tn1 < hi) || !(Fp > 0.0)) Tn1 = 0.5 * (lo + hi);
+      T = Tn1;
+    }
+    if (status != ERR_NONE) {
+      if (lane == 0) {
+        const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+                                       (unsigned long long)(a.cell0_global + c);
+        atomicMin(a.err, key);
+      }
+      continue;
+    }
+    if (lane == 0) a.T[c] = Tf;
+#pragma unroll
+    for (int r = 0; r < kScCh; ++r) {
+      const int b = lane + 32 * r;
+      if (b < nb) {
+        double i0 = i0v[r], d = di0v[r];
+        if (evaluated_at != Tf) i0 = I0_of_T(a.m, b, Tf, &d);
+        a.I0c[c * nb + b] = i0;
+        a.dI0c[c * nb + b] = d;
+        a.beta_next[c * nb + b] = beta_of_T(a.m.bcoef, b, Tf);
+      }
+    }
+  }
+}
+
+cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s) {
+  if (a.nb > kMaxBands) return cudaErrorInvalidValue;
+  if (a.ncells == 0) return cudaSuccess;
+  const int64_t need = ((int64_t)a.ncols * a.nplanes + 7) / 8;
+  const int64_t nblk = std::min<int64_t>(need, 148 * 8);
+  k_newton_sc<<<(unsigned)nblk, 256, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {

@@ -797,3 +797,62 @@ def test_partial_wall_errors(Solver):
         with pytest.raises(BteError) as e:
             sv.set_bc(0, bi.BC_PARTIAL, specularity=0.5)
         assert e.value.status == 6
+
+
+# ----------------------------------------------------------------- self-consistent tau (reading R-k)
+
+@pytest.mark.parametrize("case", ["small3d", "config2_reduced", "umesh3d"])
+def test_sc_tau_parity(Solver, case):
+    if case == "small3d":
+        p = bi.small_3d(7, 5, 4)
+    elif case == "config2_reduced":
+        p = bi.config2(n=12)
+        p.mesh = bi.Mesh(2, 12, 12, 1, p.mesh.dx, p.mesh.dy, 1.0)
+        p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, p.mesh.dx), 300.0)
+    else:
+        p = bi.small_umesh(3, (3, 2, 2))
+    p.tau_mode = 1
+    (rel, dT), _ = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    (rel, dT), _ = _run_both(Solver, p, 3, solve_T=True)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_sc_tau_slab_group_and_errors(Solver):
+    from paper_2305_19400_b200 import BteError
+    p = _group_case("3d")
+    p.tau_mode = 1
+    I, T = oracle.Oracle(p).random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(5)
+        I1, T1 = sv.intensity(), sv.temperature()
+    group = []
+    try:
+        for r in range(2):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=2)
+            group.append(sv)
+            for reg in range(6):
+                sv.set_wall(reg, p.bcs[reg])
+            sv.set_tau_mode(1)
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+        Solver.group_step(group, 5)
+        Ig = np.concatenate([s.intensity() for s in group])
+        Tg = np.concatenate([s.temperature() for s in group])
+    finally:
+        for sv in group:
+            sv.close()
+    assert np.array_equal(Ig, I1) and np.array_equal(Tg, T1)
+    bg = _band_group(Solver, p, 2, I, T)
+    try:
+        with pytest.raises(BteError) as e:
+            bg[0].set_tau_mode(1)
+        assert e.value.status == 1
+    finally:
+        for sv in bg:
+            sv.close()
+    with Solver.from_problem(p) as sv:
+        with pytest.raises(BteError):
+            sv.set_tau_mode(2)
