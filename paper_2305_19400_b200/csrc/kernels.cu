@@ -1922,15 +1922,18 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     bulk_g2s(sp + o_an, u.an + cell * 12, 96u, &full[st]);
     bulk_g2s(sp + o_nb, u.nbr + cell * 4, 32u, &full[st]);
   };
-  // face lists of cell i (threads tid < nj), from its stage
+  // face lists of cell i (the last nj threads: the reducers and the issuing
+  // thread sit in other warps, so no warp carries two extra jobs), from its stage
+  const int pj = tid - ((int)blockDim.x - nj);
+  const int tis = 9 * nb < (int)blockDim.x - nj ? 9 * nb : 0;  // the issuing thread
   auto prep = [&](int i) {
-    if (i >= n || tid >= nj) return;
+    if (i >= n || pj < 0) return;
     const int st = i & Sm;
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     const double *sp = stg + (size_t)st * sd;
     const int64_t *rn = reinterpret_cast<const int64_t *>(sp + o_nb);
-    const double *sv = sws + 4 * tid;
-    double *w = fl + ((size_t)(i & 3) * nj + tid) * kUW;
+    const double *sv = sws + 4 * pj;
+    double *w = fl + ((size_t)(i & 3) * nj + pj) * kUW;
     int64_t *wi = reinterpret_cast<int64_t *>(w);
     double aout = 0.0;
     int nin = 0;
@@ -1954,9 +1957,10 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < min(S, n); ++i) issue(i);
   }
   __syncthreads();
+  if (tid == tis)
+    for (int i = 0; i < min(S, n); ++i) issue(i);
   prep(0);
   prep(1);
   __syncthreads();
@@ -2032,7 +2036,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     }
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
-    if (tid == 0 && i + S < n) {
+    if (tid == tis && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
     }

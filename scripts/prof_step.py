@@ -13,10 +13,13 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--start", default="random")
+ap.add_argument("--tau", type=int, default=0)
 a = ap.parse_args()
 p = {2: bi.config2, 3: bi.config3, 1: bi.config1, 5: bi.config5, 6: bi.config_demo, 7: bi.config_u2,
      8: bi.config_u3}[a.config]()
 with Solver.from_problem(p) as sv:
+    if a.tau:
+        sv.set_tau_mode(a.tau)
     if a.start == "random":
         sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
     sv.step(a.warmup)
