@@ -1882,7 +1882,7 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 //    partial is finalised after the next barrier.
 constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
 
-template <int JPT, int KF>
+template <int JPT, int KF, bool ASYNC>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -1905,6 +1905,9 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   double *red2 = red + 2 * JG * nb;                           // [2][8][nb]
   double *sws = red2 + 2 * 8 * nb;                            // [nj][4]
   double *fl = sws + 4 * nj;                                  // [4][nj][kUW]
+  // ASYNC: inflow neighbour values staged by per-thread cp.async (16 B):
+  // [2 cells][KF-1 inflow faces (a simplex has an outflow face)][JPT][blockDim]
+  double2 *nbuf = reinterpret_cast<double2 *>(fl + ((4 * nj * kUW + 1) & ~1));
   const int slot = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * Q;
   const int n = (int)min((int64_t)Q, u.ncells - c0);
@@ -1966,8 +1969,31 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   __syncthreads();
 
   const double2 v2 = make_double2(A.v[2 * q], A.v[2 * q + 1]);
-  double2 upC[JPT][KF], upN[JPT][KF];
-  auto prefetch = [&](int i, double2 (&up)[JPT][KF]) {
+  double2 upC[ASYNC ? 1 : JPT][ASYNC ? 1 : KF], upN[ASYNC ? 1 : JPT][ASYNC ? 1 : KF];
+  const int nt = blockDim.x;
+  auto prefetch = [&](int i, double2 (&up)[ASYNC ? 1 : JPT][ASYNC ? 1 : KF]) {
+    if (ASYNC) {
+      if (active && i < n) {
+#pragma unroll
+        for (int r = 0; r < JPT; ++r) {
+          const int j = jg + r * JG;
+          if (j < nj) {
+            const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
+            const int64_t *wi = reinterpret_cast<const int64_t *>(w);
+            const int nin = (int)wi[1];
+#pragma unroll
+            for (int f = 0; f < KF - 1; ++f)
+              if (f < nin && wi[6 + f] >= 0) {
+                const double *src = Is + wi[6 + f] + j * nb + 2 * q;
+                const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * (KF - 1) + f) * JPT + r) * nt + tid));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+              }
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
     if (!active || i >= n) return;
 #pragma unroll
     for (int r = 0; r < JPT; ++r) {
@@ -1990,6 +2016,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     const int st = i & Sm;
     prefetch(i + 1, upN);
     double2 acc = make_double2(0.0, 0.0);
+    if (ASYNC) asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
@@ -2013,7 +2040,10 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
               const int64_t src = wi[6 + f];
               double2 up;
               if (src >= 0) {
-                up = upC[r][f];
+                if (ASYNC)
+                  up = nbuf[((size_t)(((i & 1) * (KF - 1) + f) * JPT + r)) * nt + tid];
+                else
+                  up = upC[ASYNC ? 0 : r][ASYNC ? 0 : f];
               } else {
                 const int64_t code = -1 - src;
                 up.x = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, 2 * q);
@@ -2055,10 +2085,12 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       A.Dpart[((cell - 1) * g.nslot + slot) * nb + b] =
           ((r2[0] + r2[nb]) + (r2[2 * nb] + r2[3 * nb])) + ((r2[4 * nb] + r2[5 * nb]) + (r2[6 * nb] + r2[7 * nb]));
     }
+    if (!ASYNC) {
 #pragma unroll
-    for (int r = 0; r < JPT; ++r)
+      for (int r = 0; r < (ASYNC ? 1 : JPT); ++r)
 #pragma unroll
-      for (int f = 0; f < KF; ++f) upC[r][f] = upN[r][f];
+        for (int f = 0; f < (ASYNC ? 1 : KF); ++f) upC[r][f] = upN[r][f];
+    }
   }
   __syncthreads();
   if (n > 0 && tid < nb) {
@@ -2083,21 +2115,28 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.jpt = jpt;
       a.jg = JG;
       a.chunk = a.chunk > 0 ? a.chunk : 32;
+      const bool async = a.async_nbr;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
-                                  4 * (size_t)g.nj * kUW) * sizeof(double);
+                                  4 * (size_t)g.nj * kUW + 2) * sizeof(double) +
+                           (async ? 2 * (size_t)(a.u.K - 1) * jpt * threads * 16 : 0);
       const size_t sd = (size_t)g.Es + 2 * g.nb + 16;
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)200 * 1024 - fixed) / (sd * 8));
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)(async ? 226 : 200) * 1024 - fixed) / (sd * 8));
       S = std::max(4, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;
       const size_t smem = fixed + (size_t)S * sd * 8;
       if (smem <= 227 * 1024) {
         dim3 grid((unsigned)((a.u.ncells + a.chunk - 1) / a.chunk), g.nslot);
-#define BTE_UTMA(N, KK)                                                                              \
-  if (jpt == N && a.u.K == KK) {                                                                     \
-    cudaFuncSetAttribute(k_usweep_tma<N, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_usweep_tma<N, KK><<<grid, threads, smem, s>>>(a);                                              \
-    return cudaGetLastError();                                                                       \
+#define BTE_UTMA(N, KK)                                                                                     \
+  if (jpt == N && a.u.K == KK) {                                                                            \
+    if (async) {                                                                                            \
+      cudaFuncSetAttribute(k_usweep_tma<N, KK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      k_usweep_tma<N, KK, true><<<grid, threads, smem, s>>>(a);                                             \
+    } else {                                                                                                \
+      cudaFuncSetAttribute(k_usweep_tma<N, KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      k_usweep_tma<N, KK, false><<<grid, threads, smem, s>>>(a);                                            \
+    }                                                                                                       \
+    return cudaGetLastError();                                                                              \
   }
         BTE_UTMA(1, 3)
         BTE_UTMA(2, 3)

@@ -170,8 +170,9 @@ def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
     p = bi.config_u2(n=9) if dim == 2 else bi.config_u3(n=3)
     I, T = oracle.Oracle(p).random_state()
     out = []
-    for env in ({"BTE_SWEEP": "plain"}, {}, {"BTE_SEGS": "5", "BTE_STAGES": "2"}, {"BTE_SEGS": "1000"}):
-        for k in ("BTE_SWEEP", "BTE_SEGS", "BTE_STAGES"):
+    for env in ({"BTE_SWEEP": "plain"}, {}, {"BTE_SEGS": "5", "BTE_STAGES": "2"}, {"BTE_SEGS": "1000"},
+                {"BTE_UASYNC": "0"}):
+        for k in ("BTE_SWEEP", "BTE_SEGS", "BTE_STAGES", "BTE_UASYNC"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
