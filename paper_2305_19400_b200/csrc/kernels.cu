@@ -13,6 +13,7 @@
 // No tensor cores: nothing on this path is a dense contraction.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 
 #include "bte_internal.cuh"
@@ -1869,44 +1870,50 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 //  - stage i (S-deep ring, cp.async.bulk issued S cells ahead by one thread):
 //    the cell's own (cell, slot) block (the DRAM stream), its I0c and beta
 //    rows, its face rows A_f n_f / V_c and neighbour indices;
-//  - per-direction face lists of cell i+2 (threads j < nj): a_f = dt s_j.(A_f
-//    n_f / V_c), the outflow sum aout = sum_{a_f > 0} a_f and the inflow faces
-//    (coefficient, source offset or wall code), in a 4-entry ring;
-//  - the inflow neighbour values of cell i+1 are loaded into registers while
-//    cell i computes (L2: adjacent cells are read by this or a concurrently
-//    running CTA);
-//  - I' = I + dt beta (I0c - I) - v (aout I + sum_in a_f I_up): the face sum of
-//    Eq. 3 regrouped (outflow faces first), within the parity tolerance;
+//  - per-direction face lists of cell i+2 (the last nj threads): a_f = dt
+//    s_j.(A_f n_f / V_c), the outflow sum aout = sum_{a_f > 0} a_f and KF-1
+//    inflow slots (coefficient, source block offset; unused slots have a = 0);
+//    a cell with a wall face or a direction with KF inflow faces is flagged
+//    for the generic path;
+//  - the inflow neighbour values of cell i+1 are staged in shared memory by
+//    per-thread cp.async while cell i computes (L2: adjacent cells are read by
+//    this or a concurrently running CTA);
+//  - interior cells: I' = I + dt beta (I0c - I) - v (aout I + sum_slots a I_up),
+//    branch-free (the face sum of Eq. 3 regrouped, outflow faces first);
 //  - octant partials: per-thread, then 8 contiguous group ranges ascending,
 //    then the fixed tree ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)); cell i's
 //    partial is finalised after the next barrier.
 constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
 
-template <int JPT, int KF, bool ASYNC>
+// NBT/NJT > 0 fix the channel and direction counts at compile time (with JPT = 1).
+template <int JPT, int KF, int NBT, int NJT>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const UMeshDev &u = A.u;
-  const int nb = g.nb, nj = g.nj, Es = g.Es, E = g.E;
+  constexpr bool FIX = NBT > 0 && NJT > 0 && JPT == 1;
+  const int nb = FIX ? NBT : g.nb, nj = FIX ? NJT : g.nj;
+  const int E = FIX ? NBT * NJT : g.E, Es = FIX ? (NBT * NJT + ((NBT * NJT) & 1)) : g.Es;
   const int NBP = nb >> 1;
-  const int S = A.stages, Q = A.chunk;  // S: power of two
+  const int S = A.stages, Q = A.chunk;  // S is a power of two
   const int Sm = S - 1, Sl = __ffs(S) - 1;
   const int tid = threadIdx.x;
+  const int nt = FIX ? (NJT * (NBT / 2) > 9 * NBT ? NJT * (NBT / 2) : 9 * NBT) : (int)blockDim.x;
   const int q = tid % NBP;
   const int jg = tid / NBP;
-  const int JG = A.jg;
+  const int JG = FIX ? NJT : A.jg;
   const bool active = jg < JG;
   // stage layout (doubles): own[Es] | I0[nb] | beta[nb] | an[12] | nbr[4] (int64)
   const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 12;
   const int sd = o_nb + 4;
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);        // [S]
+  int *slow = reinterpret_cast<int *>(smraw + 64);            // [4] cell needs the generic path
   double *stg = reinterpret_cast<double *>(smraw + 128);      // [S][sd]
   double *red = stg + (size_t)S * sd;                         // [2][JG][nb]
   double *red2 = red + 2 * JG * nb;                           // [2][8][nb]
   double *sws = red2 + 2 * 8 * nb;                            // [nj][4]
   double *fl = sws + 4 * nj;                                  // [4][nj][kUW]
-  // ASYNC: inflow neighbour values staged by per-thread cp.async (16 B):
-  // [2 cells][KF-1 inflow faces (a simplex has an outflow face)][JPT][blockDim]
+  // inflow neighbour values: [2 cells][KF-1 slots][JPT][nt] (16 B each)
   double2 *nbuf = reinterpret_cast<double2 *>(fl + ((4 * nj * kUW + 1) & ~1));
   const int slot = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * Q;
@@ -1927,8 +1934,8 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   };
   // face lists of cell i (the last nj threads: the reducers and the issuing
   // thread sit in other warps, so no warp carries two extra jobs), from its stage
-  const int pj = tid - ((int)blockDim.x - nj);
-  const int tis = 9 * nb < (int)blockDim.x - nj ? 9 * nb : 0;  // the issuing thread
+  const int pj = tid - (nt - nj);
+  const int tis = 9 * nb < nt - nj ? 9 * nb : 0;  // the issuing thread
   auto prep = [&](int i) {
     if (i >= n || pj < 0) return;
     const int st = i & Sm;
@@ -1940,10 +1947,12 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     int64_t *wi = reinterpret_cast<int64_t *>(w);
     double aout = 0.0;
     int nin = 0;
+    bool generic = false;
 #pragma unroll
     for (int f = 0; f < KF; ++f) {
       const double *an = sp + o_an + 3 * f;
       const double a = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
+      if (rn[f] < 0) generic = true;
       if (a > 0.0) {
         aout += a;
       } else {
@@ -1952,11 +1961,19 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
         ++nin;
       }
     }
+    if (nin == KF) generic = true;
+    for (int f = nin; f < KF; ++f) {
+      w[2 + f] = 0.0;
+      wi[6 + f] = -1;
+    }
     w[0] = aout;
     wi[1] = nin;
+    if (generic) slow[i & 3] = 1;  // every writer stores the same value
   };
 
-  for (int t = tid; t < 4 * nj; t += blockDim.x) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
+  for (int t = tid; t < 4 * nj; t += nt) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
+  for (int t = tid; t < 2 * (KF - 1) * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
+  if (tid < 4) slow[tid] = 0;
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1969,54 +1986,38 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   __syncthreads();
 
   const double2 v2 = make_double2(A.v[2 * q], A.v[2 * q + 1]);
-  double2 upC[ASYNC ? 1 : JPT][ASYNC ? 1 : KF], upN[ASYNC ? 1 : JPT][ASYNC ? 1 : KF];
-  const int nt = blockDim.x;
-  auto prefetch = [&](int i, double2 (&up)[ASYNC ? 1 : JPT][ASYNC ? 1 : KF]) {
-    if (ASYNC) {
-      if (active && i < n) {
+  const int e0 = jg * nb + 2 * q;  // this thread's element offset for r = 0; + r*JG*nb
+  // stage the inflow values of cell i (slot f of direction r at nbuf[((i&1)(KF-1) + f) JPT + r][tid])
+  auto prefetch = [&](int i) {
+    if (active && i < n) {
+      const double *w = fl + ((size_t)(i & 3) * nj + jg) * kUW;
 #pragma unroll
-        for (int r = 0; r < JPT; ++r) {
-          const int j = jg + r * JG;
-          if (j < nj) {
-            const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
-            const int64_t *wi = reinterpret_cast<const int64_t *>(w);
-            const int nin = (int)wi[1];
+      for (int r = 0; r < JPT; ++r) {
+        if (jg + r * JG < nj) {
+          const int64_t *wi = reinterpret_cast<const int64_t *>(w + (size_t)r * JG * kUW);
 #pragma unroll
-            for (int f = 0; f < KF - 1; ++f)
-              if (f < nin && wi[6 + f] >= 0) {
-                const double *src = Is + wi[6 + f] + j * nb + 2 * q;
-                const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * (KF - 1) + f) * JPT + r) * nt + tid));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-              }
+          for (int f = 0; f < KF - 1; ++f) {
+            const int64_t src = wi[6 + f];
+            if (src >= 0) {
+              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * (KF - 1) + f) * JPT + r)) * nt + tid);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                           "l"(Is + src + e0 + r * JG * nb)
+                           : "memory");
+            }
           }
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      return;
     }
-    if (!active || i >= n) return;
-#pragma unroll
-    for (int r = 0; r < JPT; ++r) {
-      const int j = jg + r * JG;
-      if (j < nj) {
-        const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
-        const int64_t *wi = reinterpret_cast<const int64_t *>(w);
-        const int nin = (int)wi[1];
-#pragma unroll
-        for (int f = 0; f < KF; ++f)
-          if (f < nin && wi[6 + f] >= 0)
-            up[r][f] = __ldg(reinterpret_cast<const double2 *>(Is + wi[6 + f] + j * nb) + q);
-      }
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  prefetch(0, upC);
+  prefetch(0);
 
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
     const int st = i & Sm;
-    prefetch(i + 1, upN);
+    prefetch(i + 1);
     double2 acc = make_double2(0.0, 0.0);
-    if (ASYNC) asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
@@ -2024,26 +2025,35 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double2 be = reinterpret_cast<const double2 *>(sp + o_be)[q];
       const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
+      const bool generic = slow[i & 3] != 0;  // CTA-uniform
+      const double2 *nb2 = nbuf + (size_t)((i & 1) * (KF - 1) * JPT) * nt + tid;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
         if (j < nj) {
           const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
-          const int64_t *wi = reinterpret_cast<const int64_t *>(w);
-          const int nin = (int)wi[1];
-          const double2 Ic = reinterpret_cast<const double2 *>(sp + j * nb)[q];
+          const int e = e0 + r * JG * nb;
+          const double2 Ic = *reinterpret_cast<const double2 *>(sp + e);
           double f0 = w[0] * Ic.x, f1 = w[0] * Ic.y;
+          if (!generic) {
 #pragma unroll
-          for (int f = 0; f < KF; ++f) {
-            if (f < nin) {
+            for (int f = 0; f < KF - 1; ++f) {  // unused slots: a = 0 times a finite stale value
+              const double a = w[2 + f];
+              const double2 up = nb2[(size_t)(f * JPT + r) * nt];
+              f0 = fma(a, up.x, f0);
+              f1 = fma(a, up.y, f1);
+            }
+          } else {
+            const int64_t *wi = reinterpret_cast<const int64_t *>(w);
+            const int nin = (int)wi[1];
+            for (int f = 0; f < nin; ++f) {
               const double a = w[2 + f];
               const int64_t src = wi[6 + f];
               double2 up;
-              if (src >= 0) {
-                if (ASYNC)
-                  up = nbuf[((size_t)(((i & 1) * (KF - 1) + f) * JPT + r)) * nt + tid];
-                else
-                  up = upC[ASYNC ? 0 : r][ASYNC ? 0 : f];
+              if (src >= 0 && f < KF - 1) {
+                up = nb2[(size_t)(f * JPT + r) * nt];
+              } else if (src >= 0) {
+                up = __ldg(reinterpret_cast<const double2 *>(Is + src + e));
               } else {
                 const int64_t code = -1 - src;
                 up.x = ghost_value(g, A.Iin, (int)(code & 7), code >> 3, base, slot, j, 2 * q);
@@ -2056,7 +2066,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
           double2 In;
           In.x = fma(dtb0, I0.x - Ic.x, Ic.x) - v2.x * f0;
           In.y = fma(dtb1, I0.y - Ic.y, Ic.y) - v2.y * f1;
-          __stcs(reinterpret_cast<double2 *>(Os + base + j * nb) + q, In);
+          __stcs(reinterpret_cast<double2 *>(Os + base + e), In);
           const double wj = sws[4 * j + 3];
           acc.x = fma(wj, I0.x - In.x, acc.x);
           acc.y = fma(wj, I0.y - In.y, acc.y);
@@ -2064,6 +2074,9 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       }
       reinterpret_cast<double2 *>(red + (size_t)(i & 1) * JG * nb + jg * nb)[q] = acc;
     }
+    // flag of ring entry (i+3)&3: last read at iteration i-1, next written by
+    // prep(i+3) in iteration i+1 (after this iteration's barrier)
+    if (tid == 0) slow[(i + 3) & 3] = 0;
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
     if (tid == tis && i + S < n) {
@@ -2084,12 +2097,6 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double *r2 = red2 + ((i - 1) & 1) * 8 * nb + b;
       A.Dpart[((cell - 1) * g.nslot + slot) * nb + b] =
           ((r2[0] + r2[nb]) + (r2[2 * nb] + r2[3 * nb])) + ((r2[4 * nb] + r2[5 * nb]) + (r2[6 * nb] + r2[7 * nb]));
-    }
-    if (!ASYNC) {
-#pragma unroll
-      for (int r = 0; r < (ASYNC ? 1 : JPT); ++r)
-#pragma unroll
-        for (int f = 0; f < (ASYNC ? 1 : KF); ++f) upC[r][f] = upN[r][f];
     }
   }
   __syncthreads();
@@ -2114,8 +2121,8 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
     if (jpt <= 2 && threads <= 1024 && JG >= 8) {
       a.jpt = jpt;
       a.jg = JG;
-      a.chunk = a.chunk > 0 ? a.chunk : 32;
-      const bool async = a.async_nbr;
+      a.chunk = a.chunk > 0 ? a.chunk : 64;
+      const bool async = true;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
                                   4 * (size_t)g.nj * kUW + 2) * sizeof(double) +
                            (async ? 2 * (size_t)(a.u.K - 1) * jpt * threads * 16 : 0);
@@ -2127,22 +2134,24 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       const size_t smem = fixed + (size_t)S * sd * 8;
       if (smem <= 227 * 1024) {
         dim3 grid((unsigned)((a.u.ncells + a.chunk - 1) / a.chunk), g.nslot);
-#define BTE_UTMA(N, KK)                                                                                     \
-  if (jpt == N && a.u.K == KK) {                                                                            \
-    if (async) {                                                                                            \
-      cudaFuncSetAttribute(k_usweep_tma<N, KK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      k_usweep_tma<N, KK, true><<<grid, threads, smem, s>>>(a);                                             \
-    } else {                                                                                                \
-      cudaFuncSetAttribute(k_usweep_tma<N, KK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      k_usweep_tma<N, KK, false><<<grid, threads, smem, s>>>(a);                                            \
-    }                                                                                                       \
-    return cudaGetLastError();                                                                              \
+#define BTE_UTMA_(N, KK, B, J)                                                                          \
+  {                                                                                                     \
+    cudaFuncSetAttribute(k_usweep_tma<N, KK, B, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_usweep_tma<N, KK, B, J><<<grid, threads, smem, s>>>(a);                                           \
+    return cudaGetLastError();                                                                          \
   }
+#define BTE_UTMA(N, KK) \
+  if (jpt == N && a.u.K == KK) BTE_UTMA_(N, KK, 0, 0)
+        if (jpt == 1 && g.nb == 40 && g.nj == 50 && JG == 50 && threads == 1000 && !getenv("BTE_UGENERIC")) {
+          if (a.u.K == 3) BTE_UTMA_(1, 3, 40, 50)
+          if (a.u.K == 4) BTE_UTMA_(1, 4, 40, 50)
+        }
         BTE_UTMA(1, 3)
         BTE_UTMA(2, 3)
         BTE_UTMA(1, 4)
         BTE_UTMA(2, 4)
 #undef BTE_UTMA
+#undef BTE_UTMA_
       }
     }
   }

@@ -171,8 +171,8 @@ def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
     I, T = oracle.Oracle(p).random_state()
     out = []
     for env in ({"BTE_SWEEP": "plain"}, {}, {"BTE_SEGS": "5", "BTE_STAGES": "2"}, {"BTE_SEGS": "1000"},
-                {"BTE_UASYNC": "0"}):
-        for k in ("BTE_SWEEP", "BTE_SEGS", "BTE_STAGES", "BTE_UASYNC"):
+                {"BTE_UGENERIC": "1"}):
+        for k in ("BTE_SWEEP", "BTE_SEGS", "BTE_STAGES", "BTE_UGENERIC"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
