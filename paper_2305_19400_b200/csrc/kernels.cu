@@ -1891,17 +1891,17 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const UMeshDev &u = A.u;
-  constexpr bool FIX = NBT > 0 && NJT > 0 && JPT == 1;
+  constexpr bool FIX = NBT > 0 && NJT > 0 && NJT % JPT == 0;
   const int nb = FIX ? NBT : g.nb, nj = FIX ? NJT : g.nj;
   const int E = FIX ? NBT * NJT : g.E, Es = FIX ? (NBT * NJT + ((NBT * NJT) & 1)) : g.Es;
   const int NBP = nb >> 1;
   const int S = A.stages, Q = A.chunk;  // S is a power of two
   const int Sm = S - 1, Sl = __ffs(S) - 1;
   const int tid = threadIdx.x;
-  const int nt = FIX ? (NJT * (NBT / 2) > 9 * NBT ? NJT * (NBT / 2) : 9 * NBT) : (int)blockDim.x;
+  const int nt = FIX ? ((NJT / JPT) * (NBT / 2) > 9 * NBT ? (NJT / JPT) * (NBT / 2) : 9 * NBT) : (int)blockDim.x;
   const int q = tid % NBP;
   const int jg = tid / NBP;
-  const int JG = FIX ? NJT : A.jg;
+  const int JG = FIX ? NJT / JPT : A.jg;
   const bool active = jg < JG;
   // stage layout (doubles): own[Es] | I0[nb] | beta[nb] | an[12] | nbr[4] (int64)
   const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 12;
@@ -2142,9 +2142,15 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   }
 #define BTE_UTMA(N, KK) \
   if (jpt == N && a.u.K == KK) BTE_UTMA_(N, KK, 0, 0)
-        if (jpt == 1 && g.nb == 40 && g.nj == 50 && JG == 50 && threads == 1000 && !getenv("BTE_UGENERIC")) {
-          if (a.u.K == 3) BTE_UTMA_(1, 3, 40, 50)
-          if (a.u.K == 4) BTE_UTMA_(1, 4, 40, 50)
+        if (g.nb == 40 && g.nj == 50 && !getenv("BTE_UGENERIC")) {
+          if (jpt == 1 && JG == 50 && threads == 1000) {
+            if (a.u.K == 3) BTE_UTMA_(1, 3, 40, 50)
+            if (a.u.K == 4) BTE_UTMA_(1, 4, 40, 50)
+          }
+          if (jpt == 2 && JG == 25 && threads == 500) {
+            if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
+            if (a.u.K == 4) BTE_UTMA_(2, 4, 40, 50)
+          }
         }
         BTE_UTMA(1, 3)
         BTE_UTMA(2, 3)
