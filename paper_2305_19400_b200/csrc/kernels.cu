@@ -318,6 +318,13 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const int j0 = grp * A.jpt;
   const int nloc = max(0, min(A.jpt, nj - j0));
   const bool active = grp < JG;
+  // side jobs on the spare threads past the JG*nb compute threads when the
+  // launch provides them (reducers [JG*nb, JG*nb + nb), issuer JG*nb + nb),
+  // else on threads 0..nb-1 / 0
+  const int spare0 = JG * nb;
+  const bool spare = (int)blockDim.x >= spare0 + nb + 1;
+  const int rtid = spare ? tid - spare0 : tid;  // reducer index (channel) when in [0, nb)
+  const int tis = spare ? spare0 + nb : 0;
 
   const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   }
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
   __syncthreads();
-  if (tid == 0)
+  if (tid == tis)
     for (int i = 0; i < min(S, np); ++i) issue(i, i);
 
   const double v = A.v[active ? b : 0];
@@ -478,14 +485,14 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     double *rb = red + buf * JG * nb;
     if (active) rb[tid] = acc;
     __syncthreads();  // stage st fully consumed, rb complete
-    if (tid == 0 && i + S < np) {
+    if (tid == tis && i + S < np) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S, st);
     }
-    if (tid < nb) {
+    if (rtid >= 0 && rtid < nb) {
       double s = 0.0;
-      for (int q = 0; q < JG; ++q) s += rb[q * nb + tid];
-      A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
+      for (int q = 0; q < JG; ++q) s += rb[q * nb + rtid];
+      A.Dpart[(cell * g.nslot + slot) * nb + rtid] = s;
     }
     buf ^= 1;
   }
@@ -815,7 +822,9 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
       *fused = 1;
     }
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    const int tthreads = (threads + 31) / 32 * 32;
+    // spare threads for the side jobs (reducers + issuer) unless BTE_SPARE=0
+    const bool spare = !(getenv("BTE_SPARE") && atoi(getenv("BTE_SPARE")) == 0) && !a.fuse_newton;
+    const int tthreads = ((spare ? threads + g.nb + 1 : threads) + 31) / 32 * 32;
 #define BTE_LAUNCH(N, NB)                                                                        \
   {                                                                                              \
     if (a.fuse_newton) {                                                                         \
