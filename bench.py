@@ -167,7 +167,7 @@ def _oracle_sample(p, target_s: float, max_steps: int = 1000):
     import oracle
     m = p.mesh
     nthreads = os.cpu_count() or 1
-    rows = m.ny if m.dim == 2 else m.nz
+    rows = (m.ny if m.dim == 2 else m.nz) if not hasattr(m, "cells") else 0
     # one-step probe on a thin slab to size the sample
     def make(nrows):
         if m.dim == 2:
@@ -250,7 +250,7 @@ def run_reference(args):
     # whole --warmup W --steps K run stays within a few minutes
     budget = 150.0
     per_step = budget / max(1, args.steps + args.warmup)
-    rows_total = m.ny if m.dim == 2 else m.nz
+    rows_total = (m.ny if m.dim == 2 else m.nz) if not hasattr(m, "cells") else 0
 
     def make(nrows):
         if m.dim == 2:
