@@ -275,6 +275,10 @@ BTE_API bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps);
  * slab).  count must equal the exact element count: ncells_local*nd*nb for
  * the intensity, ncells_local for the temperature; else BTE_EINVAL. */
 BTE_API bte_status bte_get_intensity(bte_ctx *ctx, double *out, size_t count);
+/* Intensities of selected cells (this rank's local canonical indices, host
+ * array of n), in canonical [i][d][b] order into host out (n*nd*nb doubles).
+ * For sampled checks of states too large to copy whole.  Errors: BTE_EINVAL. */
+BTE_API bte_status bte_get_intensity_cells(bte_ctx *ctx, const int64_t *cells, int64_t n, double *out);
 BTE_API bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count);
 
 /* Diagnostic total energy of this rank's slab, E = sum_c V sum_b (1/v_b)

@@ -24,7 +24,7 @@ BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE, BC_PARTIAL = 0, 1, 2, 3
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
 EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_set_tau_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
-           "bte_get_intensity", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
+           "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
 
@@ -113,6 +113,8 @@ def load_library(path: str = LIB_PATH):
         lib.bte_create_umesh.argtypes = [C.POINTER(UMeshC), C.POINTER(Dirs), C.POINTER(Bands), C.POINTER(Run),
                                          C.POINTER(C.c_void_p)]
         lib.bte_get_region_faces.argtypes = [P, C.c_int, C.POINTER(C.c_int64)]
+    if hasattr(lib, "bte_get_intensity_cells"):
+        lib.bte_get_intensity_cells.argtypes = [P, dp, C.c_int64, dp]
     if hasattr(lib, "bte_set_tau_mode"):
         lib.bte_set_tau_mode.argtypes = [P, C.c_int]
     lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
@@ -271,6 +273,13 @@ class Solver:
     def set_tau_mode(self, mode: int) -> None:
         """0: lagged tau (default); 1: self-consistent tau(T^{n+1}) (reading R-k)."""
         self._check(self._lib.bte_set_tau_mode(self._h, int(mode)))
+
+    def intensity_cells(self, cells) -> np.ndarray:
+        """Intensities [len(cells), nd, nb] of selected local cells (canonical order)."""
+        idx = np.ascontiguousarray(cells, dtype=np.int64)
+        out = np.empty((idx.size, self.nd, self.nb))
+        self._check(self._lib.bte_get_intensity_cells(self._h, _p(idx), idx.size, _p(out)))
+        return out
 
     def region_faces(self, region: int) -> int:
         """Boundary faces of wall region 0..5 (the T_wall length of set_bc)."""

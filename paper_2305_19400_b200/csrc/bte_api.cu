@@ -1715,6 +1715,27 @@ bte_status bte_get_intensity(bte_ctx *ctx, double *out, size_t count) {
   return transfer_I(ctx, out, 0);
 }
 
+bte_status bte_get_intensity_cells(bte_ctx *ctx, const int64_t *cells, int64_t n, double *out) {
+  if (!ctx || (n > 0 && (!cells || !out)) || n < 0) return BTE_EINVAL;
+  for (int64_t k = 0; k < n; ++k)
+    if (cells[k] < 0 || cells[k] >= ctx->ncells_local)
+      return fail(ctx, BTE_EINVAL, "cell index %lld out of range", (long long)cells[k]);
+  const int64_t per_cell = (int64_t)ctx->nd * ctx->nb;
+  // staging holds staging_cells * per_cell doubles: the index list goes at its
+  // end (8 B per cell), the gathered rows at its start
+  const int64_t chunk = std::max<int64_t>(1, (ctx->staging_cells * per_cell) / (per_cell + 1));
+  for (int64_t k0 = 0; k0 < n; k0 += chunk) {
+    const int64_t m = std::min(chunk, n - k0);
+    int64_t *d_idx = reinterpret_cast<int64_t *>(ctx->staging + ctx->staging_cells * per_cell) - m;
+    CU(cudaMemcpyAsync(d_idx, cells + k0, m * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    CU(launch_gather_cells(ctx->g, ctx->d_dmap, ctx->nd, d_idx, m, ctx->I[ctx->cur], ctx->staging, ctx->stream));
+    CU(cudaMemcpyAsync(out + k0 * per_cell, ctx->staging, m * per_cell * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return BTE_OK;
+}
+
 bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count) {
   if (!ctx || !out) return BTE_EINVAL;
   if (count != (size_t)ctx->ncells_local) return fail(ctx, BTE_EINVAL, "temperature count mismatch");

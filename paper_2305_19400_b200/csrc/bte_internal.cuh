@@ -183,6 +183,8 @@ cudaError_t launch_permute(const Geometry &g, const int *dmap, int nd, const dou
 cudaError_t launch_random_T(const Geometry &g, int64_t nz_cross_dummy, double dx, double dy,
                             double dz, const double *phase, double T_mean, double T_amp,
                             double *T, cudaStream_t s);
+cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, const int64_t *cells, int64_t n,
+                                const double *I, double *out, cudaStream_t s);
 cudaError_t launch_random_I(const Geometry &g, const int *canon_d, int nd, uint64_t seed,
                             double I_amp, const double *I0c, double *I, cudaStream_t s);
 cudaError_t launch_octant_tree_g(const Geometry &g, const double *Dpart, int64_t nc, double *D,

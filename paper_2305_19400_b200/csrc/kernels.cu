@@ -1601,6 +1601,35 @@ cudaError_t launch_permute(const Geometry &g, const int *dmap, int nd, const dou
   return cudaGetLastError();
 }
 
+// gather selected cells (local canonical indices) of the layout into canonical
+// [i][d][b] rows (bte_get_intensity_cells)
+__global__ void k_gather_cells(const Geometry g, const int *__restrict__ dmap, int nd,
+                               const int64_t *__restrict__ cells, int64_t n, const double *__restrict__ I,
+                               double *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_cell = (int64_t)nd * g.nb;
+  if (i >= n * per_cell) return;
+  const int64_t k = i / per_cell;
+  const int rem = (int)(i - k * per_cell);
+  const int d = rem / g.nb;
+  const int b = rem - d * g.nb;
+  const int sj = dmap[d];
+  const int sl = sj / g.nj;
+  const int j = sj - sl * g.nj;
+  const int64_t c = cells[k];
+  const int64_t p = c / g.ncross;
+  const int64_t cross = c - p * g.ncross;
+  out[i] = I[g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es + (int64_t)j * g.nb + b];
+}
+
+cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, const int64_t *cells, int64_t n,
+                                const double *I, double *out, cudaStream_t s) {
+  const int64_t m = n * nd * g.nb;
+  if (m == 0) return cudaSuccess;
+  k_gather_cells<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(g, dmap, nd, cells, n, I, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_random_T(const Geometry g, double dx, double dy, double dz, double p0, double p1,
                            double p2, double T_mean, double T_amp, double *__restrict__ T) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
