@@ -151,6 +151,7 @@ class Problem:
     nsteps: int = 100
     seed: int = 0
     tau_mode: int = 0  # 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k)
+    semi: int = 0  # 1: semi-implicit step (explicit advection, implicit relaxation; reading R-l)
 
     @property
     def dof(self) -> int:

@@ -59,6 +59,7 @@ class _Problem(C.Structure):
         ("nthreads", C.c_int),
         ("specularity", C.c_double * 6),
         ("tau_mode", C.c_int),
+        ("semi", C.c_int),
     ]
 
 
@@ -170,6 +171,7 @@ class Oracle:
             st.specularity[r] = getattr(bc, "specularity", 1.0)
         st.nthreads = nthreads if nthreads else (os.cpu_count() or 1)
         st.tau_mode = int(getattr(problem, "tau_mode", 0))
+        st.semi = int(getattr(problem, "semi", 0))
         self._st = st
         self.nc, self.nd, self.nb = m.ncells, d.nd, b.nb
         lib()

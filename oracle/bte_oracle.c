@@ -79,6 +79,7 @@ typedef struct {
   int nthreads;
   double specularity[6]; /* BC_PART: fraction p of specular reflection */
   int tau_mode;          /* 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k) */
+  int semi;              /* 1: semi-implicit step, implicit relaxation (reading R-l) */
 } ora_problem;
 
 /* ---------------------------------------------------------------- quadrature */
@@ -241,7 +242,7 @@ double ora_dt_margin(const ora_problem *p, double Tmax) {
     for (int d = 0; d < p->nd; d++) {
       double k = 0.0;
       for (int a = 0; a < na; a++) k += fabs(p->s[3 * d + a]) / d_axis(p, a);
-      double mm = 1.0 - p->dt * be - p->dt * p->v[b] * k;
+      double mm = 1.0 - (p->semi ? 0.0 : p->dt * be) - p->dt * p->v[b] * k;
       if (mm < m) m = mm;
     }
   }
@@ -555,8 +556,10 @@ int ora_temperature_update(const ora_problem *p, const double *D, double *T, dou
     for (int b = 0; b < nb; b++) bn[b] = ora_beta(p, b, T[c]);
     double Tnew;
     int it;
+    double bw[512]; /* Newton weights times v_b: beta_b, or beta_b/(1 + dt beta_b) in the semi-implicit step (R-l) */
+    for (int b = 0; b < nb; b++) bw[b] = p->semi ? bn[b] / (1.0 + p->dt * bn[b]) : bn[b];
     int st = p->tau_mode == 1 ? ora_newton_sc(p, T[c], D + c * nb, I0c + c * nb, &Tnew, &it)
-                              : ora_newton(p, T[c], D + c * nb, I0c + c * nb, bn, &Tnew, &it);
+                              : ora_newton(p, T[c], D + c * nb, I0c + c * nb, bw, &Tnew, &it);
     if (it > mit) mit = it;
     if (st != ORA_OK) {
 #pragma omp critical
@@ -612,6 +615,19 @@ int ora_ghost_table(const ora_problem *p, int region, const double *I, double *g
   return st;
 }
 
+/* Semi-implicit step (reading R-l), last part: with J the advected field and
+ * (I0c, betac) refreshed at T^{n+1} (betac = beta(T^n), lagged),
+ *   I^{n+1}_{c,d,b} = (J + dt beta_b I0_b(T^{n+1})) / (1 + dt beta_b). */
+void ora_relax(const ora_problem *p, long nc, const double *J, const double *I0c, const double *betac, double *I) {
+  int nd = p->nd, nb = p->nb;
+  for (long c = 0; c < nc; c++)
+    for (int d = 0; d < nd; d++)
+      for (int b = 0; b < nb; b++) {
+        double db = p->dt * betac[c * nb + b];
+        I[(c * nd + d) * nb + b] = (J[(c * nd + d) * nb + b] + db * I0c[c * nb + b]) / (1.0 + db);
+      }
+}
+
 /* Run nsteps explicit steps in place on (I, T, I0c, betac).
  * Order within a step (reading #14): ghosts from I^n -> sweep -> reduce ->
  * Newton -> refresh.  On error: *err_step = failing step, *err_cell = cell. */
@@ -627,11 +643,20 @@ int ora_run(const ora_problem *p, double *I, double *T, double *I0c, double *bet
   }
   double *J = (double *)malloc(sizeof(double) * n);
   double *D = (double *)malloc(sizeof(double) * nc * p->nb);
-  if (!J || !D) {
+  double *Z = (double *)calloc((size_t)nc * p->nb, sizeof(double));
+  if (!J || !D || !Z) {
     free(J);
     free(D);
+    free(Z);
     bc_free(&bd);
     return ORA_ENOMEM;
+  }
+  if (p->semi && p->tau_mode == 1) {
+    free(J);
+    free(D);
+    free(Z);
+    bc_free(&bd);
+    return ORA_EINVAL;
   }
   int nreg = p->dim == 3 ? 6 : 4;
   int mit = 0;
@@ -640,13 +665,18 @@ int ora_run(const ora_problem *p, double *I, double *T, double *I0c, double *bet
   for (long s = 0; s < nsteps && st == ORA_OK; s++) {
     for (int r = 0; r < nreg; r++)
       if (p->bc_kind[r] == BC_DIFF || p->bc_kind[r] == BC_PART) diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
-    ora_sweep_bd(p, &bd, I, I0c, betac, J);
+    /* semi-implicit (R-l): advection only (beta = 0 in the sweep), then the
+     * temperature with weights beta/(1 + dt beta), then the implicit relaxation */
+    ora_sweep_bd(p, &bd, I, I0c, p->semi ? Z : betac, J);
     ora_reduce(p, J, I0c, D);
     long bad;
     int it;
     st = ora_temperature_update(p, D, T, I0c, betac, &bad, &it);
     if (it > mit) mit = it;
-    memcpy(I, J, sizeof(double) * n);
+    if (p->semi)
+      ora_relax(p, nc, J, I0c, betac, I);
+    else
+      memcpy(I, J, sizeof(double) * n);
     if (st != ORA_OK) {
       if (err_step) *err_step = s;
       if (err_cell) *err_cell = bad;
@@ -655,6 +685,7 @@ int ora_run(const ora_problem *p, double *I, double *T, double *I0c, double *bet
   if (max_iters) *max_iters = mit;
   free(J);
   free(D);
+  free(Z);
   bc_free(&bd);
   return st;
 }

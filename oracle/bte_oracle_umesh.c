@@ -71,6 +71,7 @@ typedef struct {
   int nthreads;
   double specularity[6];
   int tau_mode;
+  int semi;
 } ora_problem;
 
 double ora_I0(const ora_problem *p, int b, double T, double *dI0dT);
@@ -79,6 +80,7 @@ int ora_reflection(const ora_problem *p, int axis, int *r);
 void ora_reduce(const ora_problem *p, const double *I, const double *I0c, double *D);
 int ora_temperature_update(const ora_problem *p, const double *D, double *T, double *I0c, double *betac,
                            long *bad, int *max_iters);
+void ora_relax(const ora_problem *p, long nc, const double *J, const double *I0c, const double *betac, double *I);
 
 typedef struct {
   int dim;
@@ -477,24 +479,29 @@ int ora_urun(const ora_problem *p, const ora_ugeom *g, double *I, double *T, dou
   }
   double *J = (double *)malloc(sizeof(double) * n);
   double *D = (double *)malloc(sizeof(double) * g->nc * p->nb);
-  if (!J || !D) {
+  double *Z = (double *)calloc((size_t)g->nc * p->nb, sizeof(double));
+  if (!J || !D || !Z || (p->semi && p->tau_mode == 1)) {
     free(J);
     free(D);
+    free(Z);
     ubc_free(&bd);
-    return ORA_ENOMEM;
+    return (J && D && Z) ? ORA_EINVAL : ORA_ENOMEM;
   }
   int mit = 0;
   if (err_step) *err_step = -1;
   if (err_cell) *err_cell = -1;
   for (long s = 0; s < nsteps && st == ORA_OK; s++) {
     ubc_update(p, g, &bd, I);
-    usweep_bd(p, g, &bd, I, I0c, betac, J);
+    usweep_bd(p, g, &bd, I, I0c, p->semi ? Z : betac, J);  /* semi-implicit (R-l): advection only */
     ora_reduce(p, J, I0c, D);
     long bad;
     int it;
     st = ora_temperature_update(p, D, T, I0c, betac, &bad, &it);
     if (it > mit) mit = it;
-    memcpy(I, J, sizeof(double) * n);
+    if (p->semi)
+      ora_relax(p, g->nc, J, I0c, betac, I);
+    else
+      memcpy(I, J, sizeof(double) * n);
     if (st != ORA_OK) {
       if (err_step) *err_step = s;
       if (err_cell) *err_cell = bad;
@@ -503,6 +510,7 @@ int ora_urun(const ora_problem *p, const ora_ugeom *g, double *I, double *T, dou
   if (max_iters) *max_iters = mit;
   free(J);
   free(D);
+  free(Z);
   ubc_free(&bd);
   return st;
 }

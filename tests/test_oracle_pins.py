@@ -812,3 +812,87 @@ def test_sc_closed_box_conservation():
     E0 = o.energy(I)
     I2, _, _, _ = o.run(I, T, 300, I0c, betac)
     assert abs(o.energy(I2) / E0 - 1) < 1e-12
+
+
+# ----------------------------------------------------------------- semi-implicit step (reading R-l)
+
+def _semi_case(dt_factor=20.0, bcs=None, n=(5, 4, 3)):
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 12, 27, 33, 39])
+    p = bi.small_3d(*n, bands=b, bcs=bcs)
+    o = oracle.Oracle(p)
+    p.dt = dt_factor * p.dt  # beyond the explicit bound (relaxation-limited) ...
+    p.semi = 1
+    return p
+
+
+def test_semi_step_relaxation_identity_and_balance():
+    """One semi-implicit step: I' (1 + dt beta) = J + dt beta I0(T') with J the
+    pure advection of I (the beta = 0 sweep, pinned by the exact-rational
+    tests) and beta = beta(T^n); the scattering balance
+    sum_b beta_b/v_b sum_d w_d (I0_b(T') - I'_{d,b}) vanishes at T'."""
+    p = _semi_case()
+    o = oracle.Oracle(p)
+    assert o.dt_margin(350.0) >= 0.0  # advection alone is stable at this dt ...
+    pe = bi.small_3d(5, 4, 3, bands=p.bands)
+    pe.dt = p.dt
+    assert oracle.Oracle(pe).dt_margin(350.0) < 0.0  # ... the explicit step is not
+    I, T = o.random_state()
+    I0c, betac = o.refresh(T)
+    J = o.sweep(I, I0c, np.zeros_like(betac))
+    I1, T1, I0n, bn = o.run(I, T, 1)
+    assert np.array_equal(bn, betac)  # lagged beta
+    I0T = o.I0_vec(T1)
+    dtb = p.dt * betac[:, None, :]
+    lhs = I1 * (1 + dtb)
+    rhs = J + dtb * I0T[:, None, :]
+    assert np.max(np.abs(lhs / rhs - 1)) < 1e-14
+    W = p.dirs.w
+    terms = betac / p.bands.v * (W.sum() * I0T - np.einsum("d,cdb->cb", W, I1))
+    assert np.max(np.abs(terms.sum(axis=1)) / np.abs(terms).sum(axis=1)) < 1e-11
+    assert np.max(np.abs(dtb)) > 5.0  # stiff: dt beta well above 1
+
+
+def test_semi_closed_box_large_dt():
+    p = _semi_case(40.0, bcs=bi.uniform_bcs(bi.BC_SPECULAR))
+    o = oracle.Oracle(p)
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)
+    E0 = o.energy(I)
+    I2, T2, _, _ = o.run(I, T, 100, I0c, betac)
+    assert abs(o.energy(I2) / E0 - 1) < 1e-12
+    assert I2.min() > 0 and np.all(np.isfinite(T2))
+
+
+def test_semi_first_order_consistency():
+    """At dt within the explicit bound both steps approximate the same ODE:
+    their difference after a fixed physical time halves with dt (first order)."""
+    b = bi.subset_bands(bi.silicon_bands(29), [5, 30])
+    p = bi.small_3d(4, 3, 3, bands=b)
+    base = 0.4 * p.dt
+    err = []
+    for k in (1, 2, 4):
+        runs = []
+        for semi in (0, 1):
+            q = bi.small_3d(4, 3, 3, bands=b)
+            q.dt = base / k
+            q.semi = semi
+            o = oracle.Oracle(q)
+            I, T = o.random_state()
+            runs.append(o.run(I, T, 8 * k)[0])
+        err.append(np.max(np.abs(runs[1] - runs[0]) / runs[0]))
+    r1, r2 = err[0] / err[1], err[1] / err[2]
+    assert 1.7 < r1 < 2.3 and 1.7 < r2 < 2.3, (err, r1, r2)
+
+
+def test_semi_stiff_limit_isotropic():
+    """dt beta >> 1: the step relaxes every direction to I0(T') (isotropic)."""
+    p = _semi_case(1.0)
+    bc = p.bands.beta_coef.copy()
+    bc[:, :4] *= 1e9  # every rate term (theta unchanged): dt beta >= 1e5
+    p.bands = bi.Bands(p.bands.v, p.bands.mode, bc, w_lo=p.bands.w_lo, w_hi=p.bands.w_hi, vs=p.bands.vs,
+                       c2=p.bands.c2, g=p.bands.g)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    I1, T1, _, _ = o.run(I, T, 1)
+    I0T = o.I0_vec(T1)
+    assert np.max(np.abs(I1 / I0T[:, None, :] - 1)) < 1e-5
