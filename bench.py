@@ -326,6 +326,9 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     band = args.decomp == "band"
     p = _problem(args.config, 1 if band else world)
+    if args.semi > 0:
+        p.dt = args.semi * p.dt
+        p.semi = 1
     nccl_id = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -440,6 +443,8 @@ def run_b200(args):
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
             "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb_total,
                        "dof_per_step": dof_global, "start": args.start, "dt": p.dt, "tau": args.tau,
+                       "integrator": "semi-implicit" if args.semi > 0 else "explicit",
+                       "simulated_s_per_s": p.dt * args.steps / (ms * 1e-3),
                        "parallelism": (f"band{world}" if band else f"slab{world}") if world > 1 else "single",
                        "storage": "octant-slot rotation" if sv.rotate else "two buffers",
                        "l2": f"inputs > L2 ({state_gb:.2f} GB/buffer vs 126 MB), no flush"},
@@ -465,6 +470,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--decomp", default="slab", choices=["slab", "band"])
+    ap.add_argument("--semi", type=float, default=0.0,
+                    help="semi-implicit step (reading R-l) at this multiple of the workload's dt (0: explicit)")
     ap.add_argument("--tau", default="lagged", choices=["lagged", "sc"],
                     help="temperature update: lagged tau (reading #15) or self-consistent tau (R-k)")
     args = ap.parse_args()

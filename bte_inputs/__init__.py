@@ -545,7 +545,7 @@ def subproblem(problem: "Problem", box, open_kind: int = BC_SPECULAR) -> "Proble
             Tw = np.ascontiguousarray(Tw)
         bcs.append(WallBC(bc.kind, Tw, bc.T_uniform))
     return Problem(problem.name + f"_sub{box}", sub, problem.dirs, problem.bands, problem.dt,
-                   problem.T_init, bcs, problem.nsteps, problem.seed)
+                   problem.T_init, bcs, problem.nsteps, problem.seed, problem.tau_mode, problem.semi)
 
 
 # --------------------------------------------------------------------------

@@ -134,6 +134,8 @@ typedef struct {
   void *(*alloc)(size_t bytes, void *alloc_ctx);
   void (*dealloc)(void *ptr, void *alloc_ctx);
   void *alloc_ctx;
+  int step_mode;  /* 0: explicit step (Eq. 5 + forward Euler); 1: semi-implicit (reading
+                     R-l: explicit advection, implicit relaxation, bte_set_step_mode) */
 } bte_run;
 
 /* Create a context: validates tables (positive sizes/speeds, equal octant
@@ -214,6 +216,20 @@ BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs,
  * results in both modes when beta does not depend on T.
  * Errors: BTE_EINVAL (mode, band contexts, the fused-Newton variant). */
 BTE_API bte_status bte_set_tau_mode(bte_ctx *ctx, int mode);
+
+/* Time integrator (SURVEY 8(f) f4 "implicit per-step solvers", reading R-l).
+ *   mode 0 (default): explicit forward-Euler step of Eq. 5;
+ *   mode 1: semi-implicit step -- J = I^n - dt v_b sum_f (A_f/V)(s.n) I_up
+ *           (explicit upwind advection), T^{n+1} from the energy balance with
+ *           weights beta_b/(v_b (1 + dt beta_b)) on the reduction of J, then
+ *           I^{n+1} = (J + dt beta_b I0_b(T^{n+1})) / (1 + dt beta_b).
+ *           The dt bound keeps only the advection term (1 - dt v_b
+ *           sum_a |s_a|/D_a >= 0), so stiff scattering no longer limits dt.
+ * Also settable at creation through bte_run.step_mode (needed when dt
+ * exceeds the explicit bound).  Errors: BTE_EINVAL (mode, band contexts,
+ * self-consistent tau, fused Newton), BTE_EUNSTABLE (switching to the explicit
+ * step at a dt beyond its bound). */
+BTE_API bte_status bte_set_step_mode(bte_ctx *ctx, int mode);
 
 /* Number of boundary faces of wall region 0..5 (the T_wall length of
  * bte_set_bc) for structured and unstructured contexts.  Errors: BTE_EINVAL. */

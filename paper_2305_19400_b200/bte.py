@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE, BC_PARTIAL = 0, 1, 2, 3
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_set_tau_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -64,7 +64,7 @@ class Run(C.Structure):
     _fields_ = [("dt", C.c_double), ("T_init", C.c_double), ("device", C.c_int),
                 ("stream", C.c_void_p), ("rank", C.c_int), ("nranks", C.c_int),
                 ("nccl_id", C.c_void_p), ("alloc", ALLOC_FN), ("dealloc", DEALLOC_FN),
-                ("alloc_ctx", C.c_void_p)]
+                ("alloc_ctx", C.c_void_p), ("step_mode", C.c_int)]
 
 
 class Timing(C.Structure):
@@ -117,6 +117,8 @@ def load_library(path: str = LIB_PATH):
         lib.bte_get_intensity_cells.argtypes = [P, dp, C.c_int64, dp]
     if hasattr(lib, "bte_set_tau_mode"):
         lib.bte_set_tau_mode.argtypes = [P, C.c_int]
+    if hasattr(lib, "bte_set_step_mode"):
+        lib.bte_set_step_mode.argtypes = [P, C.c_int]
     lib.bte_set_bc.argtypes = [P, C.c_int, C.c_int, dp, C.c_double]
     if hasattr(lib, "bte_set_bc_partial"):
         lib.bte_set_bc_partial.argtypes = [P, C.c_int, C.c_double]
@@ -159,7 +161,7 @@ class Solver:
 
     def __init__(self, mesh, dirs, bands, dt: float, T_init: float, device: int = 0, stream=None,
                  rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 torch_alloc: bool = True, decomp: str = "slab"):
+                 torch_alloc: bool = True, decomp: str = "slab", step_mode: int = 0):
         if decomp not in ("slab", "band"):
             raise ValueError("decomp must be 'slab' or 'band'")
         import torch  # plumbing: device memory and streams
@@ -215,7 +217,7 @@ class Solver:
             k(idbuf)
         run = Run(float(dt), float(T_init), int(device), C.c_void_p(self.stream.cuda_stream), int(rank),
                   int(nranks), C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
-                  self._alloc_cb, self._free_cb, None)
+                  self._alloc_cb, self._free_cb, None, int(step_mode))
         h = C.c_void_p()
         create = self._lib.bte_create_band if decomp == "band" else self._lib.bte_create
         if self.umesh:
@@ -245,6 +247,7 @@ class Solver:
     @classmethod
     def from_problem(cls, problem, **kw) -> "Solver":
         """Build from a problem description (mesh/dirs/bands/dt/T_init/bcs)."""
+        kw.setdefault("step_mode", int(getattr(problem, "semi", 0)))
         sv = cls(problem.mesh, problem.dirs, problem.bands, problem.dt, problem.T_init, **kw)
         nreg = 6 if problem.mesh.dim == 3 else 4
         for r in range(nreg):
@@ -269,6 +272,10 @@ class Solver:
             return
         Tw = _f64(T_wall)
         self._check(self._lib.bte_set_bc(self._h, int(region), int(kind), _p(Tw), float(T_uniform)))
+
+    def set_step_mode(self, mode: int) -> None:
+        """0: explicit step; 1: semi-implicit (explicit advection, implicit relaxation; reading R-l)."""
+        self._check(self._lib.bte_set_step_mode(self._h, int(mode)))
 
     def set_tau_mode(self, mode: int) -> None:
         """0: lagged tau (default); 1: self-consistent tau(T^{n+1}) (reading R-k)."""

@@ -109,6 +109,8 @@ struct bte_ctx {
   int overlap = 1;  // env BTE_OVERLAP=0: exchange after the whole sweep
   // unstructured mesh (bte_create_umesh): the layout sees one plane of ncells
   int tau_mode = 0;  // 0 lagged tau (reading #15), 1 self-consistent (reading R-k)
+  int semi = 0;      // 1: semi-implicit step (reading R-l)
+  double *zbeta = nullptr;  // zeros [ncells][nb]: the semi-implicit sweep advects only
   int umesh = 0;
   UMeshDev u{};
   std::vector<double> uvol;  // V_c
@@ -176,7 +178,7 @@ static bte_status check_dt(bte_ctx *ctx) {
   const double D[3] = {ctx->mesh.dx, ctx->mesh.dy, ctx->mesh.dz};
   double worst = 1e300;
   for (int b = ctx->b0; b < ctx->b0 + ctx->nb; ++b) {  // this context's channels
-    const double be = host_beta(ctx, b, ctx->Tmax);
+    const double be = ctx->semi ? 0.0 : host_beta(ctx, b, ctx->Tmax);  // semi-implicit: advection bound only
     for (int d = 0; d < ctx->nd; ++d) {
       double k = 0;
       if (ctx->umesh)
@@ -473,9 +475,23 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
   return create_impl(&fm, dirs, bands, run, false, out, &uh);
 }
 
+bte_status bte_set_step_mode(bte_ctx *ctx, int mode) {
+  if (!ctx) return BTE_EINVAL;
+  if (mode != 0 && mode != 1) return fail(ctx, BTE_EINVAL, "step mode must be 0 (explicit) or 1 (semi-implicit)");
+  if (mode == 1 && ctx->band) return fail(ctx, BTE_EINVAL, "semi-implicit step: not for band contexts");
+  if (mode == 1 && ctx->tau_mode == 1)
+    return fail(ctx, BTE_EINVAL, "semi-implicit step: lagged tau only (bte_set_tau_mode 0)");
+  const int old = ctx->semi;
+  ctx->semi = mode;
+  bte_status st = check_dt(ctx);
+  if (st) ctx->semi = old;
+  return st;
+}
+
 bte_status bte_set_tau_mode(bte_ctx *ctx, int mode) {
   if (!ctx) return BTE_EINVAL;
   if (mode != 0 && mode != 1) return fail(ctx, BTE_EINVAL, "tau mode must be 0 (lagged) or 1 (self-consistent)");
+  if (mode == 1 && ctx->semi) return fail(ctx, BTE_EINVAL, "self-consistent tau: explicit step only");
   if (mode == 1 && ctx->band)
     return fail(ctx, BTE_EINVAL, "self-consistent tau needs every channel's reduction in the Newton (not band contexts)");
   if (mode == 1 && ctx->fuse_newton) return fail(ctx, BTE_EINVAL, "self-consistent tau: unfused Newton only");
@@ -754,6 +770,9 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     ctx->u.ncells = uh->nc;
     for (int r = 0; r < 6; ++r) ctx->u.rn[r] = (int64_t)uh->rcell[r].size();
   }
+  if (run->step_mode != 0 && run->step_mode != 1) return bail(fail(ctx, BTE_EINVAL, "step_mode must be 0 or 1"));
+  if (run->step_mode == 1 && band) return bail(fail(ctx, BTE_EINVAL, "semi-implicit step: not for band contexts"));
+  ctx->semi = run->step_mode;
   if ((st = check_dt(ctx)) != BTE_OK) return bail(st);
 
   // ---- device allocations
@@ -865,6 +884,9 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     CU(cudaMemsetAsync(ctx->Sall, 0, (size_t)ctx->nranks * ncl * sizeof(double), ctx->stream));
   }
   ctx->T = (double *)dev_alloc(ctx, ncl * sizeof(double));
+  ctx->zbeta = (double *)dev_alloc(ctx, ncl * ctx->nb * sizeof(double));
+  if (!ctx->zbeta) return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
+  CU(cudaMemsetAsync(ctx->zbeta, 0, ncl * ctx->nb * sizeof(double), ctx->stream));
   ctx->Dpart = (double *)dev_alloc(ctx, ncl * nslot * ctx->nb * sizeof(double));
   ctx->d_err = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
   if (!ctx->I0c || !ctx->dI0c || !ctx->beta || !ctx->T || !ctx->Dpart || !ctx->d_err)
@@ -1194,6 +1216,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.I0s = ctx->band ? ctx->I0s : nullptr;
   a.betas = ctx->band ? ctx->betas : nullptr;
   a.b0s = ctx->b0;
+  a.semi_dt = ctx->semi ? ctx->dt : 0.0;
   a.nbs = ctx->nb;
   for (int k = 0; k < kMaxSlots; ++k) a.slot_oct[k] = ctx->g.slot_oct[k];
   for (int o = 0; o < 8; ++o) a.oct_slot[o] = ctx->g.oct_slot[o];
@@ -1224,7 +1247,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
     a.Iin = Iin;
     a.Iout = Iout;
     a.I0c = ctx->I0s;
-    a.beta = ctx->betas;
+    a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
     a.Dpart = ctx->Dpart;
     a.v = ctx->m.v;
     a.dt = ctx->dt;
@@ -1259,7 +1282,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
       a.Iin = Iin;
       a.Iout = Iout;
       a.I0c = ctx->I0s;
-      a.beta = ctx->betas;
+      a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
       a.Dpart = ctx->Dpart;
       a.v = ctx->m.v;
       a.dt = ctx->dt;
@@ -1296,7 +1319,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.Iin = Iin;
   a.Iout = Iout;
   a.I0c = ctx->I0s;
-  a.beta = ctx->betas;
+  a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
   a.Dpart = ctx->Dpart;
   a.v = ctx->m.v;
   a.dt = ctx->dt;
@@ -1358,7 +1381,7 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
 // are swept (SURVEY 8(e) overlap schedule).
 static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   const bool has_bnd = n_diffuse(ctx) > 0;
-  const int C = (ctx->fuse_newton || ctx->rot || ctx->umesh) ? 1 : ctx->nchunks;
+  const int C = (ctx->fuse_newton || ctx->rot || ctx->umesh || ctx->semi) ? 1 : ctx->nchunks;
   const int ncross = ctx->g.ncross;
   const int np = ctx->g.nplanes;
   bte_status st;
@@ -1370,7 +1393,8 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
     if ((st = launch_boundary(ctx, Iin))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   }
-  if (split && (C > 1 || ctx->fuse_newton || ctx->rot)) split = false;
+  // the semi-implicit step exchanges halos after its relaxation pass
+  if (split && (C > 1 || ctx->fuse_newton || ctx->rot || ctx->semi)) split = false;
   if (split) {
     int fused = 0;
     id = (size_t)-1;
@@ -1415,6 +1439,13 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
       CU(cudaEventRecord(ctx->ev_nt[k], ns));
       ctx->nt_pending[k] = 1;
     }
+  }
+  if (ctx->semi) {  // reading R-l: I^{n+1} = (J + dt beta I0(T^{n+1})) / (1 + dt beta)
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
+    CU(launch_relax(ctx->g, Iout, ctx->I0c, ctx->beta, ctx->dt, ctx->stream));
+    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    ctx->tacc.launches++;
   }
   CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
   return BTE_OK;

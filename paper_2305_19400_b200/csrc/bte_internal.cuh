@@ -102,6 +102,7 @@ struct NewtonArgs {
   int b0s, nbs;
   int predict;            // quadratic-convergence acceptance (reading R-f)
   int minb;               // k_newton occupancy variant (0 = default)
+  double semi_dt;         // > 0: semi-implicit step weights beta/(v(1 + semi_dt beta)) (reading R-l)
   unsigned long long *stats;  // debug counters: [evaluations, final re-evaluations, cells solved] or null
 };
 
@@ -185,6 +186,8 @@ cudaError_t launch_random_T(const Geometry &g, int64_t nz_cross_dummy, double dx
                             double *T, cudaStream_t s);
 cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, const int64_t *cells, int64_t n,
                                 const double *I, double *out, cudaStream_t s);
+cudaError_t launch_relax(const Geometry &g, double *I, const double *I0c, const double *beta, double dt,
+                         cudaStream_t s);
 cudaError_t launch_random_I(const Geometry &g, const int *canon_d, int nd, uint64_t seed,
                             double I_amp, const double *I0c, double *I, cudaStream_t s);
 cudaError_t launch_octant_tree_g(const Geometry &g, const double *Dpart, int64_t nc, double *D,

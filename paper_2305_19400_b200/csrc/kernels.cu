@@ -1161,7 +1161,8 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
     }
     const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     const double bn = beta_of_T(a.m.bcoef, b, Tn);
-    const double cb = bn * a.m.rv[b];
+    // semi-implicit step (reading R-l): weights beta / (v (1 + dt beta))
+    const double cb = a.semi_dt > 0.0 ? bn * a.m.rv[b] / (1.0 + a.semi_dt * bn) : bn * a.m.rv[b];
     cs[b] = cb;
     a.beta_next[c * nb + b] = bn;
     F0 += cb * D;
@@ -1627,6 +1628,32 @@ cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, cons
   const int64_t m = n * nd * g.nb;
   if (m == 0) return cudaSuccess;
   k_gather_cells<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(g, dmap, nd, cells, n, I, out);
+  return cudaGetLastError();
+}
+
+// Semi-implicit step (reading R-l), last part: I = (J + dt beta I0c) / (1 + dt beta)
+// over the owned cells of the output buffer (beta lagged, I0c refreshed at T^{n+1}).
+__global__ void k_relax(const Geometry g, double *__restrict__ I, const double *__restrict__ I0c,
+                        const double *__restrict__ beta, double dt) {
+  const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_per_slot * g.nslot) return;
+  const int sl = (int)(i / n_per_slot);
+  const int64_t r = i - sl * n_per_slot;
+  const int64_t cell = r / g.E;
+  const int e = (int)(r - cell * g.E);
+  const int b = e % g.nb;
+  const int64_t p = cell / g.ncross, cross = cell - p * g.ncross;
+  double *x = I + g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es + e;
+  const double db = dt * beta[cell * g.nb + b];
+  *x = (*x + db * I0c[cell * g.nb + b]) / (1.0 + db);
+}
+
+cudaError_t launch_relax(const Geometry &g, double *I, const double *I0c, const double *beta, double dt,
+                         cudaStream_t s) {
+  const int64_t n = (int64_t)g.nplanes * g.ncross * g.E * g.nslot;
+  if (n == 0) return cudaSuccess;
+  k_relax<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I, I0c, beta, dt);
   return cudaGetLastError();
 }
 

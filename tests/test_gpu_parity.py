@@ -881,3 +881,82 @@ def test_sc_tau_slab_group_and_errors(Solver):
     with Solver.from_problem(p) as sv:
         with pytest.raises(BteError):
             sv.set_tau_mode(2)
+
+
+# ----------------------------------------------------------------- semi-implicit step (reading R-l)
+
+def _semi(p, factor=20.0):
+    p.dt = factor * p.dt  # beyond the explicit bound: only the semi-implicit step is stable
+    p.semi = 1
+    return p
+
+
+@pytest.mark.parametrize("case", ["small3d", "config2_reduced", "umesh3d"])
+def test_semi_parity(Solver, case):
+    if case == "small3d":
+        p = bi.small_3d(7, 5, 4)
+    elif case == "config2_reduced":
+        p = bi.config2(n=12)
+        p.mesh = bi.Mesh(2, 12, 12, 1, p.mesh.dx, p.mesh.dy, 1.0)
+        p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, p.mesh.dx), 300.0)
+    else:
+        p = bi.small_umesh(3, (3, 2, 2))
+        p.bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(3, specularity=0.4),
+                 bi.WallBC(0, None, 298.0), bi.WallBC(1)]
+    p = _semi(p, 10.0 if case == "umesh3d" else 20.0)  # (the simplices' advection bound is tighter)
+    (rel, dT), _ = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_semi_groups_rotation_energy_errors(Solver, monkeypatch):
+    from paper_2305_19400_b200 import BteError
+    p = _semi(_group_case("3d"))
+    I, T = oracle.Oracle(p).random_state()
+    res = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("BTE_ROTATE", rot)
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(5)
+            res[rot] = (sv.intensity(), sv.temperature())
+    assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][1], res["1"][1])
+    monkeypatch.setenv("BTE_ROTATE", "0")
+    group = []
+    try:
+        for r in range(3):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=3, step_mode=1)
+            group.append(sv)
+            for reg in range(6):
+                sv.set_wall(reg, p.bcs[reg])
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+        Solver.group_step(group, 5)
+        Ig = np.concatenate([s.intensity() for s in group])
+        Tg = np.concatenate([s.temperature() for s in group])
+    finally:
+        for sv in group:
+            sv.close()
+    assert np.array_equal(Ig, res["0"][0]) and np.array_equal(Tg, res["0"][1])
+    # closed box at 40x the explicit bound: conservative and positive
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    q = _semi(bi.small_3d(6, 5, 4, bands=b, bcs=bi.uniform_bcs(bi.BC_SPECULAR)), 40.0)
+    Iq, _ = oracle.Oracle(q).random_state()
+    with Solver.from_problem(q) as sv:
+        sv.set_state(Iq, None)
+        E0 = sv.energy()
+        sv.step(100)
+        E1 = sv.energy()
+        assert sv.intensity().min() > 0
+        with pytest.raises(BteError) as e:
+            sv.set_step_mode(0)  # explicit at this dt: unstable
+        assert e.value.status == 5
+        with pytest.raises(BteError):
+            sv.set_tau_mode(1)
+    assert abs(E1 / E0 - 1) < 1e-12
+    with pytest.raises(BteError) as e:
+        Solver(q.mesh, q.dirs, q.bands, q.dt, q.T_init)  # explicit creation at this dt
+    assert e.value.status == 5
+    with pytest.raises(BteError) as e:
+        Solver(q.mesh, q.dirs, q.bands, q.dt, q.T_init, rank=0, nranks=2, decomp="band", step_mode=1)
+    assert e.value.status == 1
