@@ -1255,8 +1255,6 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
     a.pipelined = ctx->use_tma;
     a.stages = ctx->stages_override;
     a.chunk = ctx->seg_override;
-    a.async_nbr = 1;
-    if (const char *e = getenv("BTE_UASYNC")) a.async_nbr = atoi(e);
     CU(launch_usweep(a, ctx->stream));
     ctx->tacc.launches++;
     ctx->tacc.sweep_launches++;

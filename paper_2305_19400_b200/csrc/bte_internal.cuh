@@ -162,7 +162,6 @@ struct USweepArgs {
   int target_threads;
   int pipelined;          // k_usweep_tma (default) vs the one-CTA-per-cell k_usweep
   int stages, chunk;      // pipeline depth and cells per CTA (0 = automatic)
-  int async_nbr;          // stage neighbour values with cp.async instead of registers
 };
 
 // kernels / launchers (kernels.cu)

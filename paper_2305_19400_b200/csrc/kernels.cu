@@ -298,6 +298,164 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Small-block sweep with per-thread cp.async prefetch (the demo's 5 x 55
+// blocks): as k_sweep, but the values cell i+1 needs (own, cross-upwind, I0c,
+// beta) are copied into a per-thread shared-memory slot pair while cell i
+// computes, so a DRAM latency is paid once per column segment instead of once
+// per cell, without the registers a register prefetch costs (occupancy).
+// Identical arithmetic to k_sweep (bitwise equal results).
+template <int DIM, int JMAX>
+__global__ void __launch_bounds__(1024) k_sweep_ca(const SweepArgs A) {
+  extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb] | pf[2][W][blockDim]
+  const Geometry &g = A.g;
+  const int nb = g.nb, nj = g.nj, Es = g.Es;
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = blockDim.x / nb;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+  constexpr int W = (DIM == 3 ? 3 : 2) * JMAX + 2;  // own | xu | (yu) | I0 | beta
+  double *coef = sm;
+  double *red = sm + 4 * nj;
+  double *pf = red + 2 * JG * nb;
+
+  const int slot = A.slot0 + blockIdx.y;
+  const int oct = g.slot_oct[slot];
+  const int col = A.col0 + blockIdx.x;
+  const int x = (DIM == 3) ? col % g.nx : col;
+  const int y = (DIM == 3) ? col / g.nx : 0;
+  const bool xneg = oct & 4;
+  const bool yneg = oct & 2;
+  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
+  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
+  const int xregion = xneg ? 1 : 0;
+  const int64_t xoff = xneg ? (int64_t)Es : -(int64_t)Es;
+  bool yghost = false;
+  int yregion = 2;
+  int64_t yoff = 0;
+  if (DIM == 3) {
+    yghost = yneg ? (y == g.ny - 1) : (y == 0);
+    yregion = yneg ? 3 : 2;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
+  }
+  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
+  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
+
+  const int pb = A.p_lo + blockIdx.z * A.seg_len;
+  const int pe = min(A.p_hi, pb + A.seg_len);
+  const int np = pe - pb;
+  const int step = mneg ? -1 : 1;
+  const int pfirst = mneg ? pe - 1 : pb;
+  const double *__restrict__ Iin = A.Iin;
+  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + A.out_off[slot];
+  const int64_t colE = (int64_t)col * Es;
+  const double dt = A.dt;
+  const double v = A.v[b < nb ? b : 0];
+  const bool active = grp < JG && tid < JG * nb;
+
+  auto cp8 = [&](double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  };
+  // values of the i-th cell of the segment into slot pair buf
+  auto prefetch = [&](int i, int buf) {
+    if (active && i < np) {
+      const int p = pfirst + i * step;
+      const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
+      const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+      double *q = pf + ((size_t)buf * W) * nt + tid;
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k)
+        if (k < nloc) {
+          const int e = (j0 + k) * nb + b;
+          cp8(q + (size_t)k * nt, Is + base + e);
+          if (!xghost) cp8(q + (size_t)(JMAX + k) * nt, Is + base + xoff + e);
+          if (DIM == 3 && !yghost) cp8(q + (size_t)(2 * JMAX + k) * nt, Is + base + yoff + e);
+        }
+      cp8(q + (size_t)(W - 2) * nt, A.I0c + cell * nb + b);
+      cp8(q + (size_t)(W - 1) * nt, A.beta + cell * nb + b);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  double prev[JMAX];
+  {
+    const int p = pfirst;
+    const int pm = p - step;
+    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      prev[k] = 0.0;
+      if (active && k < nloc) {
+        const int e = (j0 + k) * nb + b;
+        if (stored)
+          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e);
+        else
+          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
+      }
+    }
+  }
+  prefetch(0, 0);
+  __syncthreads();
+
+  int buf = 0;
+  int p = pfirst;
+  for (int i = 0; i < np; ++i, p += step) {
+    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
+    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
+    const int64_t mg = g.m0 + p;
+    prefetch(i + 1, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    double acc = 0.0;
+    if (active) {
+      const double *q = pf + ((size_t)buf * W) * nt + tid;
+      const double I0 = q[(size_t)(W - 2) * nt];
+      const double dtb = dt * q[(size_t)(W - 1) * nt];
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        if (k < nloc) {
+          const int j = j0 + k;
+          const int e = j * nb + b;
+          const double Ic = q[(size_t)k * nt];
+          double xu, yu = 0.0;
+          if (!xghost) {
+            xu = q[(size_t)(JMAX + k) * nt];
+          } else {
+            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+            xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
+          }
+          if (DIM == 3) {
+            if (!yghost) {
+              yu = q[(size_t)(2 * JMAX + k) * nt];
+            } else {
+              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+              yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
+            }
+          }
+          const double *cf = coef + 4 * j;
+          const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cf, v, I0, dtb);
+          Os[base + e] = In;
+          acc = fma(cf[3], I0 - In, acc);
+          prev[k] = Ic;
+        }
+      }
+    }
+    double *rb = red + (i & 1) * JG * nb;
+    if (active) rb[tid] = acc;
+    __syncthreads();
+    if (tid < nb) {
+      double s = 0.0;
+      for (int qq = 0; qq < JG; ++qq) s += rb[qq * nb + tid];
+      A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
+    }
+    buf ^= 1;
+  }
+}
+
 // Same decomposition as k_sweep, but the (cell, octant) blocks of the cell and
 // of its cross-axis upwind neighbours (16 KB each at 50 x 40), plus the cell's
 // I0c/beta rows, stream into an S-stage shared-memory ring with cp.async.bulk
@@ -859,6 +1017,33 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     return cudaGetLastError();
   }
   a.fuse_newton = 0;
+  // k_sweep_ca (cp.async prefetch of cell i+1) only on request (BTE_CA=1):
+  // measured slower on the demo shape (0.118 vs 0.095 ms), DESIGN.md section 7
+  if (getenv("BTE_CA") && atoi(getenv("BTE_CA")) == 1) {
+    const int W = (DIM == 3 ? 3 : 2) * jcase + 2;
+    const size_t smemc = (4 * (size_t)g.nj + 2 * (size_t)threads + 2 * (size_t)W * threads) * sizeof(double);
+    if (smemc <= 227 * 1024) {
+      switch (jcase) {
+#define BTE_CCASE(N)                                                                      \
+  case N:                                                                                 \
+    if (smemc > 48 * 1024)                                                                \
+      cudaFuncSetAttribute(k_sweep_ca<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smemc);                                                   \
+    k_sweep_ca<DIM, N><<<grid, threads, smemc, s>>>(a);                                   \
+    return cudaGetLastError();
+        BTE_CCASE(1)
+        BTE_CCASE(2)
+        BTE_CCASE(4)
+        BTE_CCASE(5)
+        BTE_CCASE(8)
+        BTE_CCASE(10)
+        BTE_CCASE(16)
+#undef BTE_CCASE
+        default:
+          break;
+      }
+    }
+  }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
   switch (jcase) {
 #define BTE_CASE(N)                                                                       \
@@ -1635,25 +1820,27 @@ cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, cons
 // over the owned cells of the output buffer (beta lagged, I0c refreshed at T^{n+1}).
 __global__ void k_relax(const Geometry g, double *__restrict__ I, const double *__restrict__ I0c,
                         const double *__restrict__ beta, double dt) {
-  const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_per_slot * g.nslot) return;
-  const int sl = (int)(i / n_per_slot);
-  const int64_t r = i - sl * n_per_slot;
-  const int64_t cell = r / g.E;
-  const int e = (int)(r - cell * g.E);
-  const int b = e % g.nb;
+  // block (cell, slot); threads (b, j-lane): no integer division per element
+  const int64_t cell = blockIdx.x;
+  const int sl = blockIdx.y;
+  const int b = threadIdx.x;
   const int64_t p = cell / g.ncross, cross = cell - p * g.ncross;
-  double *x = I + g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es + e;
+  double *blk = I + g.slot_off[sl] + (p + g.plane_off) * g.plane_stride + cross * g.Es;
   const double db = dt * beta[cell * g.nb + b];
-  *x = (*x + db * I0c[cell * g.nb + b]) / (1.0 + db);
+  const double i0 = I0c[cell * g.nb + b];
+  const double inv = 1.0 / (1.0 + db);
+  for (int j = threadIdx.y; j < g.nj; j += blockDim.y) {
+    double *x = blk + (int64_t)j * g.nb + b;
+    *x = (*x + db * i0) * inv;
+  }
 }
 
 cudaError_t launch_relax(const Geometry &g, double *I, const double *I0c, const double *beta, double dt,
                          cudaStream_t s) {
-  const int64_t n = (int64_t)g.nplanes * g.ncross * g.E * g.nslot;
-  if (n == 0) return cudaSuccess;
-  k_relax<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I, I0c, beta, dt);
+  const int64_t nc = (int64_t)g.nplanes * g.ncross;
+  if (nc == 0 || g.nb > 1024) return nc == 0 ? cudaSuccess : cudaErrorInvalidValue;
+  const int ty = std::max(1, std::min(g.nj, 256 / g.nb));
+  k_relax<<<dim3((unsigned)nc, g.nslot), dim3(g.nb, ty), 0, s>>>(g, I, I0c, beta, dt);
   return cudaGetLastError();
 }
 
@@ -2187,12 +2374,12 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.jpt = jpt;
       a.jg = JG;
       a.chunk = a.chunk > 0 ? a.chunk : 64;
-      const bool async = true;
+      // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
                                   4 * (size_t)g.nj * kUW + 2) * sizeof(double) +
-                           (async ? 2 * (size_t)(a.u.K - 1) * jpt * threads * 16 : 0);
+                           2 * (size_t)(a.u.K - 1) * jpt * threads * 16;
       const size_t sd = (size_t)g.Es + 2 * g.nb + 16;
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)(async ? 226 : 200) * 1024 - fixed) / (sd * 8));
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)226 * 1024 - fixed) / (sd * 8));
       S = std::max(4, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;

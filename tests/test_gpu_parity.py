@@ -523,14 +523,14 @@ def test_parity_nonuniform_band_grid(Solver):
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
 
 
-@pytest.mark.parametrize("variant", ["BTE_FUSE", "BTE_CHUNKS", "BTE_SWEEP_PLAIN", "BTE_TX"])
+@pytest.mark.parametrize("variant", ["BTE_FUSE", "BTE_CHUNKS", "BTE_SWEEP_PLAIN", "BTE_TX", "BTE_CA"])
 def test_parity_kernel_variants(Solver, variant, monkeypatch):
     """The A/B kernel variants (sweep-tail Newton, chunked two-stream pipeline,
     direct-load sweep, multi-column TMA sweep) reach the same results."""
     if variant == "BTE_SWEEP_PLAIN":
         monkeypatch.setenv("BTE_SWEEP", "plain")
     else:
-        monkeypatch.setenv(variant, {"BTE_CHUNKS": "3", "BTE_TX": "4"}.get(variant, "1"))
+        monkeypatch.setenv(variant, {"BTE_CHUNKS": "3", "BTE_TX": "4", "BTE_CA": "1"}.get(variant, "1"))
     for p, n in ((bi.config2(n=16), 8), (bi.config3(n=8), 4)):
         if p.mesh.dim == 3:
             p.mesh = bi.Mesh(3, 9, 7, 6, 1e-6, 1e-6, 1e-6)
