@@ -80,12 +80,11 @@ struct bte_ctx {
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
   int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
-  int newton_predict = 1;
-  int newton_minb = 0;
-  int tx_override = 0;
+  int newton_predict = 1;  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int newton_minb = 0;     // env BTE_NEWTON_MINB (k_newton occupancy variant)
+  int tx_override = 0;     // env BTE_TX (columns per CTA of the small-block sweep)
   unsigned long long *d_stats = nullptr;  // env BTE_NEWTON_STATS=1: Newton counters printed by bte_step
-  int l2hint = 0;  // env BTE_L2HINT
-  int persist = 0;  // env BTE_PERSIST  // env BTE_TX (columns per CTA of the small-block sweep)  // env BTE_NEWTON_MINB (k_newton occupancy variant)  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
+  int l2hint = 0;          // env BTE_L2HINT
   int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
   double *staging = nullptr;
   int64_t staging_cells = 0;
