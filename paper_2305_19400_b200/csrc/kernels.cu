@@ -1163,6 +1163,8 @@ cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, doubl
   return cudaGetLastError();
 }
 
+constexpr int kMaxSnapJ = 1024;  // directions per octant handled by k_spec_snapshot
+
 // Octant-slot rotation: specular ghosts read the reflected
 // octant, whose slot may already hold I^{n+1} or another octant when this
 // octant is swept, so the boundary pass snapshots them from I^n first:
@@ -1180,17 +1182,32 @@ __global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, 
   const int nsj = g.nslot * g.nj;
   const int64_t *ro = g.refl_off + (int64_t)axis * nsj + (int64_t)slot * g.nj;
   double *o = out + (face * g.nslot + slot) * (int64_t)g.E;
-  for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
-    const int j = e / g.nb, b = e - j * g.nb;
+  // per direction j the source row (reflected slot region, reflected j) of this cell
+  __shared__ const double *srow[kMaxSnapJ];
+  for (int j = threadIdx.x; j < g.nj; j += blockDim.x) {
     const int64_t off = ro[j];  // slot_r * slot_stride + jr * nb
     const int64_t sr = off / g.slot_stride;
-    o[e] = I[g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base + b];
+    srow[j] = I + g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base;
+  }
+  __syncthreads();
+  if ((g.nb & 1) == 0) {  // 16-B rows: double2 copies
+    const int hp = g.nb >> 1;
+    for (int e = threadIdx.x; e < g.nj * hp; e += blockDim.x) {
+      const int j = e / hp, q = e - j * hp;
+      reinterpret_cast<double2 *>(o + (int64_t)j * g.nb)[q] = __ldg(reinterpret_cast<const double2 *>(srow[j]) + q);
+    }
+  } else {
+    for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
+      const int j = e / g.nb, b = e - j * g.nb;
+      o[e] = srow[j][b];
+    }
   }
 }
 
 cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s) {
   const int64_t nf = wall_faces_local(g, region);
   if (nf == 0) return cudaSuccess;
+  if (g.nj > kMaxSnapJ) return cudaErrorInvalidValue;
   const int axis = region >> 1, bit = axis == 0 ? 4 : (axis == 1 ? 2 : 1);
   const bool hi = region & 1;
   int ins[8] = {0, 0, 0, 0, 0, 0, 0, 0}, nin = 0;
@@ -2365,7 +2382,9 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   if (a.u.ncells == 0) return cudaSuccess;
   if (a.pipelined && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
     const int NBP = g.nb / 2;
-    const int tgt = a.target_threads > 0 ? a.target_threads : 1024;
+    // 2 directions x 2 channels per thread on triangles (measured 3 % faster on u2),
+    // 1 x 2 on tetrahedra (their 4-face lists fill the registers)
+    const int tgt = a.target_threads > 0 ? a.target_threads : (a.u.K == 3 ? 500 : 1024);
     int JG = std::max(1, std::min(g.nj, tgt / NBP));
     const int jpt = (g.nj + JG - 1) / JG;
     JG = (g.nj + jpt - 1) / jpt;
