@@ -702,7 +702,11 @@ int ora_solve_T(const ora_problem *p, const double *I, const double *T_guess, do
   ora_reduce(p, I, I0c, D);
   long bad;
   int it;
-  int st = ora_temperature_update(p, D, T, I0c, betac, &bad, &it);
+  /* the temperature of a given state is the plain scattering balance (#2),
+   * whatever the integrator (the semi-implicit weights belong to its step) */
+  ora_problem q = *p;
+  q.semi = 0;
+  int st = ora_temperature_update(&q, D, T, I0c, betac, &bad, &it);
   free(D);
   return st;
 }

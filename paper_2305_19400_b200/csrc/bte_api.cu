@@ -1128,7 +1128,13 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
     CU(launch_dpart_from_I(ctx->g, ctx->I[ctx->cur], ctx->I0c, ctx->Dpart, ctx->stream));
-    if ((st = run_newton(ctx, 0))) return st;
+    // the temperature of a state is the plain balance (#2), also under the
+    // semi-implicit integrator (its weights belong to its step)
+    const int semi = ctx->semi;
+    ctx->semi = 0;
+    st = run_newton(ctx, 0);
+    ctx->semi = semi;
+    if (st) return st;
   }
   CU(cudaStreamSynchronize(ctx->stream));
   return sync_check(ctx);
