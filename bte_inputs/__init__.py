@@ -67,11 +67,13 @@ class Mesh:
 
 @dataclasses.dataclass
 class UMesh:
-    """Unstructured simplex mesh (Eq. 3 P:L176-184 holds for any
-    polyhedral cell): triangles (dim 2, 3 vertices per cell) or tetrahedra
+    """Unstructured mesh (Eq. 3 P:L176-184 holds for "a
+    polygonal/polyhedral cell with m sides"): convex polygons in 2-D (3
+    vertices: triangles, 4: quadrilaterals, in boundary order) or tetrahedra
     (dim 3, 4 vertices).  DATA only: vertex coordinates [nverts, 3] (z = 0 in
-    2-D) and cell -> vertex lists [ncells, dim+1].  Face k of a cell is the
-    face opposite its local vertex k.  The domain is the axis-aligned box
+    2-D) and cell -> vertex lists [ncells, m].  Face k of a cell is the edge
+    (v_{k+1}, v_{k+2}) in 2-D (for a triangle: the edge opposite v_k) and the
+    face opposite v_k of a tetrahedron.  The domain is the axis-aligned box
     spanned by the vertices; every boundary face must lie on one of its walls
     (region 0..5 = -x,+x,-y,+y,-z,+z, tested in that order).  depth is the z
     extent of a 2-D mesh (volumes = area*depth)."""
@@ -462,6 +464,21 @@ def umesh_tri(nx: int, ny: int, Lx: float, Ly: float, jitter: float = 0.2, seed:
     return UMesh(2, V, np.ascontiguousarray(C), depth)
 
 
+def umesh_quad(nx: int, ny: int, Lx: float, Ly: float, jitter: float = 0.2, seed: int = 19,
+               shuffle: bool = False, depth: float = 1.0) -> UMesh:
+    """2-D quadrilaterals: the nx x ny lattice of squares with jittered
+    interior vertices (convex for jitter < 0.25), vertices counter-clockwise
+    from the lower-left corner, row-major cell order (the structured grid's
+    canonical order when jitter = 0) unless shuffled."""
+    V = _lattice_verts((nx, ny), (Lx / nx, Ly / ny), jitter, seed)
+    vid = lambda i, j: i + (nx + 1) * j  # noqa: E731
+    C = np.array([(vid(i, j), vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1))
+                  for j in range(ny) for i in range(nx)], dtype=np.int64)
+    if shuffle:
+        C = C[np.random.Generator(np.random.PCG64(seed + 2)).permutation(len(C))]
+    return UMesh(2, V, np.ascontiguousarray(C), depth)
+
+
 # Kuhn subdivision of a cube into 6 tetrahedra along the main diagonal: for each
 # axis order (p, q, r), the path 000 -> e_p -> e_p + e_q -> 111 (conforming
 # across cubes because every cube uses the same split)
@@ -493,11 +510,11 @@ def umesh_tet(nx: int, ny: int, nz: int, h: float = 1e-6, jitter: float = 0.1, s
 
 def umesh_centroids(m: UMesh) -> np.ndarray:
     """Cell centroids: vertex coordinates summed in local vertex order, / (dim+1)."""
-    X = m.verts[m.cells]  # [nc, dim+1, 3]
+    X = m.verts[m.cells]  # [nc, m, 3]
     acc = X[:, 0, :].copy()
-    for k in range(1, m.dim + 1):
+    for k in range(1, X.shape[1]):
         acc = acc + X[:, k, :]
-    return acc / (m.dim + 1)
+    return acc / X.shape[1]
 
 
 def random_temperature_umesh(m: UMesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0) -> np.ndarray:
@@ -647,6 +664,16 @@ def config_u2(n: int = 120, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20
     p.bcs[3] = WallBC(BC_ISOTHERMAL, None, 310.0)
     p.name = f"u2_tri_{2*n*n}x{n_theta*n_phi}x{p.bands.nb}"
     p.seed = SEED_BASE + 7
+    return p
+
+
+def config_uq(n: int = 120, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
+    """config_u2 on jittered quadrilaterals (n^2 cells)."""
+    p = config_u2(n=n, n_freq=n_freq, n_theta=n_theta, n_phi=n_phi)
+    L = 525e-6
+    p.mesh = umesh_quad(n, n, L, L, jitter=0.2, seed=SEED_BASE + 9)
+    p.name = f"uq_quad_{n*n}x{n_theta*n_phi}x{p.bands.nb}"
+    p.seed = SEED_BASE + 9
     return p
 
 

@@ -42,7 +42,7 @@ _lib = None
 
 class _UMesh(C.Structure):
     _fields_ = [("dim", C.c_int), ("nverts", C.c_long), ("verts", C.c_void_p), ("ncells", C.c_long),
-                ("cells", C.c_void_p), ("depth", C.c_double)]
+                ("cells", C.c_void_p), ("depth", C.c_double), ("nvc", C.c_int)]
 
 
 class _Problem(C.Structure):
@@ -180,7 +180,7 @@ class Oracle:
             self._verts = np.ascontiguousarray(m.verts, dtype=np.float64)
             self._cells = np.ascontiguousarray(m.cells, dtype=np.int64)
             um = _UMesh(m.dim, self._verts.shape[0], self._verts.ctypes.data, self._cells.shape[0],
-                        self._cells.ctypes.data, float(m.depth))
+                        self._cells.ctypes.data, float(m.depth), int(self._cells.shape[1]))
             h = C.c_void_p()
             rc = lib().ora_ugeom_build(C.byref(um), C.byref(h))
             if rc:
@@ -195,7 +195,7 @@ class Oracle:
     # -- unstructured geometry (tests)
     def geometry(self):
         """(vol[nc], area[nc,K], normal[nc,K,3], nbr[nc,K], region[nc,K]) of an unstructured mesh."""
-        K = self.problem.mesh.dim + 1
+        K = int(self.problem.mesh.cells.shape[1])
         vol = np.empty(self.nc)
         area = np.empty((self.nc, K))
         nrm = np.empty((self.nc, K, 3))

@@ -20,6 +20,9 @@
  *   triangle (2-D): V = |(p1-p0) x (p2-p0)|/2 * depth, face k = edge
  *     (p_{k+1}, p_{k+2}) of length L, A = L * depth, n = the unit
  *     perpendicular of the edge pointing away from p_k;
+ *   convex m-gon (2-D, "a polygonal/polyhedral cell with m sides",
+ *     P:L176-181): V = |shoelace sum|/2 * depth, face k = edge
+ *     (p_{k+1 mod m}, p_{k+2 mod m}), n pointing away from the vertex mean;
  *   tetrahedron (3-D): V = |det(p1-p0, p2-p0, p3-p0)|/6, face k = triangle
  *     of the other three vertices (ascending local order) a, b, c,
  *     A = |(b-a) x (c-a)|/2, n = (b-a) x (c-a) / |.| pointing away from p_k.
@@ -87,8 +90,9 @@ typedef struct {
   long nverts;
   const double *verts; /* [nverts][3] */
   long ncells;
-  const long *cells;   /* [ncells][dim+1] */
+  const long *cells;   /* [ncells][nvc] */
   double depth;
+  int nvc;             /* vertices per cell: dim 2 -> 3 (triangles) or m (convex polygons), dim 3 -> 4 */
 } ora_umesh;
 
 typedef struct {
@@ -145,7 +149,9 @@ void ora_ugeom_free(ora_ugeom *g) {
 int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
   *out = NULL;
   if (m->dim != 2 && m->dim != 3) return ORA_EINVAL;
-  const int K = m->dim + 1, nfv = m->dim; /* vertices per face */
+  const int nvc = m->nvc > 0 ? m->nvc : m->dim + 1;
+  if ((m->dim == 3 && nvc != 4) || (m->dim == 2 && (nvc < 3 || nvc > 8))) return ORA_EINVAL;
+  const int K = nvc, nfv = m->dim; /* faces per cell, vertices per face */
   const long nc = m->ncells;
   ora_ugeom *g = (ora_ugeom *)calloc(1, sizeof(ora_ugeom));
   if (!g) return ORA_ENOMEM;
@@ -178,9 +184,34 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
         ora_ugeom_free(g);
         return ORA_EINVAL;
       }
-    const double *P[4];
+    const double *P[8];
     for (int k = 0; k < K; k++) P[k] = m->verts + 3 * cv[k];
-    if (m->dim == 2) {
+    if (m->dim == 2 && K > 3) {
+      double sh = 0.0, cx = 0.0, cy = 0.0;
+      for (int k = 0; k < K; k++) {
+        const double *a = P[k], *b = P[(k + 1) % K];
+        sh += a[0] * b[1] - b[0] * a[1];
+        cx += a[0];
+        cy += a[1];
+      }
+      cx /= K;
+      cy /= K;
+      g->vol[c] = fabs(sh) / 2.0 * m->depth;
+      for (int k = 0; k < K; k++) {
+        const double *a = P[(k + 1) % K], *b = P[(k + 2) % K];
+        double ex = b[0] - a[0], ey = b[1] - a[1];
+        double L = sqrt(ex * ex + ey * ey);
+        double nx = ey / L, ny = -ex / L;
+        if (nx * (cx - a[0]) + ny * (cy - a[1]) > 0.0) {
+          nx = -nx;
+          ny = -ny;
+        }
+        g->area[c * K + k] = L * m->depth;
+        g->nrm[(c * K + k) * 3 + 0] = nx;
+        g->nrm[(c * K + k) * 3 + 1] = ny;
+        g->nrm[(c * K + k) * 3 + 2] = 0.0;
+      }
+    } else if (m->dim == 2) {
       double ux = P[1][0] - P[0][0], uy = P[1][1] - P[0][1];
       double vx = P[2][0] - P[0][0], vy = P[2][1] - P[0][1];
       g->vol[c] = fabs(ux * vy - uy * vx) / 2.0 * m->depth;
@@ -238,8 +269,13 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
       face_rec *f = fr + c * K + k;
       int n = 0;
       f->key[2] = -1;
-      for (int i = 0; i < K; i++)
-        if (i != k) f->key[n++] = cv[i];
+      if (m->dim == 2) { /* edge (v_{k+1}, v_{k+2}) (for triangles: the face opposite v_k) */
+        f->key[0] = cv[(k + 1) % K];
+        f->key[1] = cv[(k + 2) % K];
+      } else {
+        for (int i = 0; i < K; i++)
+          if (i != k) f->key[n++] = cv[i];
+      }
       sort3(f->key, nfv);
       f->cell = c;
       f->k = k;
@@ -277,8 +313,12 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
         int a = r / 2;
         double wall = (r & 1) ? hi[a] : lo[a];
         int all = 1;
-        for (int i = 0; i < K; i++)
-          if (i != k && m->verts[3 * cv[i] + a] != wall) all = 0;
+        if (m->dim == 2) {
+          if (m->verts[3 * cv[(k + 1) % K] + a] != wall || m->verts[3 * cv[(k + 2) % K] + a] != wall) all = 0;
+        } else {
+          for (int i = 0; i < K; i++)
+            if (i != k && m->verts[3 * cv[i] + a] != wall) all = 0;
+        }
         if (all) reg = r;
       }
       if (reg < 0) {

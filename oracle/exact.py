@@ -128,7 +128,7 @@ def exact_usweep(problem, I, I0c, betac):
     m, dr, bd = problem.mesh, problem.dirs, problem.bands
     assert bd.mode == 0, "exact twin supports LINEAR channels only"
     nd, nb = dr.nd, bd.nb
-    K = m.dim + 1
+    K = int(m.cells.shape[1])
     P = [[Fr(float(x)) for x in row] for row in m.verts]
     cells = [[int(v) for v in row] for row in m.cells]
     nc = len(cells)
@@ -143,10 +143,15 @@ def exact_usweep(problem, I, I0c, betac):
     I0f = np.vectorize(Fr, otypes=[object])(np.asarray(I0c, dtype=np.float64))
     bf = np.vectorize(Fr, otypes=[object])(np.asarray(betac, dtype=np.float64))
     refl = {a: _reflect_map(dr.s, a) for a in range(m.dim)}
+    def face_verts(cv, k):  # 2-D: edge (v_{k+1}, v_{k+2}); 3-D: the face opposite v_k
+        if m.dim == 2:
+            return [cv[(k + 1) % K], cv[(k + 2) % K]]
+        return cv[:k] + cv[k + 1:]
+
     owner = {}
     for c, cv in enumerate(cells):
         for k in range(K):
-            owner.setdefault(frozenset(cv[:k] + cv[k + 1:]), []).append((c, k))
+            owner.setdefault(frozenset(face_verts(cv, k)), []).append((c, k))
     # wall faces in (cell, local face) order per region
     wall_index = {}
     count = [0] * 6
@@ -160,9 +165,10 @@ def exact_usweep(problem, I, I0c, betac):
     geo = []  # per cell: volume, [(An vector, neighbour or None, region)]
     for c, cv in enumerate(cells):
         X = [P[i] for i in cv]
-        if m.dim == 2:
-            u, vv = sub(X[1], X[0]), sub(X[2], X[0])
-            V = abs(u[0] * vv[1] - u[1] * vv[0]) / 2 * depth
+        if m.dim == 2:  # shoelace (for a triangle: |cross| / 2)
+            sh = sum((X[k][0] * X[(k + 1) % K][1] - X[(k + 1) % K][0] * X[k][1] for k in range(K)), Fr(0))
+            V = abs(sh) / 2 * depth
+            cen = [sum((X[k][a] for k in range(K)), Fr(0)) / K for a in range(3)]
         else:
             u, vv, ww = sub(X[1], X[0]), sub(X[2], X[0]), sub(X[3], X[0])
             det = (u[0] * (vv[1] * ww[2] - vv[2] * ww[1]) - u[1] * (vv[0] * ww[2] - vv[2] * ww[0])
@@ -170,17 +176,20 @@ def exact_usweep(problem, I, I0c, betac):
             V = abs(det) / 6
         faces = []
         for k in range(K):
-            others = [X[i] for i in range(K) if i != k]
             if m.dim == 2:
+                others = [P[v] for v in face_verts(cv, k)]
                 e = sub(others[1], others[0])
                 An = [e[1] * depth, -e[0] * depth, Fr(0)]
+                if dot(An, sub(cen, others[0])) > 0:  # outward: away from the vertex mean
+                    An = [-x for x in An]
             else:
+                others = [X[i] for i in range(K) if i != k]
                 e1, e2 = sub(others[1], others[0]), sub(others[2], others[0])
                 An = [(e1[1] * e2[2] - e1[2] * e2[1]) / 2, (e1[2] * e2[0] - e1[0] * e2[2]) / 2,
                       (e1[0] * e2[1] - e1[1] * e2[0]) / 2]
-            if dot(An, sub(X[k], others[0])) > 0:
-                An = [-x for x in An]
-            key = frozenset(cv[:k] + cv[k + 1:])
+                if dot(An, sub(X[k], others[0])) > 0:
+                    An = [-x for x in An]
+            key = frozenset(face_verts(cv, k))
             nbr = [o for o in owner[key] if o[0] != c]
             region = None
             if not nbr:

@@ -581,10 +581,11 @@ def _u_meshes():
         "tri": bi.umesh_tri(4, 3, 4e-7, 3e-7, jitter=0.2, seed=3),
         "tri_shuffled": bi.umesh_tri(3, 3, 3e-7, 3e-7, jitter=0.2, seed=4, shuffle=True),
         "tet": bi.umesh_tet(2, 2, 2, 1e-7, jitter=0.1, seed=5, shuffle=True),
+        "quad": bi.umesh_quad(4, 3, 4e-7, 3e-7, jitter=0.2, seed=6, shuffle=True),
     }
 
 
-@pytest.mark.parametrize("case", ["tri", "tri_shuffled", "tet"])
+@pytest.mark.parametrize("case", ["tri", "tri_shuffled", "tet", "quad"])
 def test_usweep_exact_rational(case):
     """The unstructured sweep against the exact-rational twin written from
     Eq. 3 with square-root-free geometry (A_f n_f / V_c rational), all wall
@@ -896,3 +897,28 @@ def test_semi_stiff_limit_isotropic():
     I1, T1, _, _ = o.run(I, T, 1)
     I0T = o.I0_vec(T1)
     assert np.max(np.abs(I1 / I0T[:, None, :] - 1)) < 1e-5
+
+
+@pytest.mark.parametrize("dirs", ["inplane", "3dquad"])
+def test_uquad_mesh_equals_structured_grid(dirs):
+    """An unjittered quadrilateral mesh in row-major order IS the structured
+    grid: the unstructured oracle (face sums over the 4 edges, Eq. 3) and the
+    structured oracle (per-axis difference form) agree to rounding over a
+    multi-step run with every wall kind -- two independently written sweeps
+    pinned against each other."""
+    h = 2.0 ** -21
+    nx, ny = 5, 4
+    d = bi.directions_inplane(12) if dirs == "inplane" else bi.directions_control_angle(2, 8)
+    b = bi.subset_bands(bi.silicon_bands(29), [1, 18, 34])
+    bcs = [bi.WallBC(bi.BC_SPECULAR), bi.WallBC(bi.BC_DIFFUSE), bi.WallBC(bi.BC_ISOTHERMAL, 300.0 + np.arange(nx)),
+           bi.WallBC(bi.BC_PARTIAL, specularity=0.3), bi.WallBC(1), bi.WallBC(1)]
+    ps = bi.Problem("grid", bi.Mesh(2, nx, ny, 1, h, h, 1.0), d, b, 1e-13, 300.0, bcs, seed=4)
+    pu = bi.Problem("quads", bi.umesh_quad(nx, ny, nx * h, ny * h, jitter=0.0), d, b, 1e-13, 300.0, bcs, seed=4)
+    os_, ou = oracle.Oracle(ps), oracle.Oracle(pu)
+    for r in range(4):
+        assert ou.n_region_faces(r) == os_.n_region_faces(r)
+    I, T = os_.random_state()
+    Is, Ts, _, _ = os_.run(I, T, 6)
+    Iu, Tu, _, _ = ou.run(I, T, 6)
+    assert np.max(np.abs(Iu / Is - 1)) < 1e-12 and np.max(np.abs(Tu - Ts)) < 1e-9
+    assert np.max(np.abs(Is / I - 1)) > 1e-4  # the run does move the state
