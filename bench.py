@@ -45,14 +45,16 @@ BYTES_PER_DOF = 16  # read I^n + write I^{n+1}, fp64
 
 
 def _problem(config: int, nranks: int):
-    if config not in (1, 2, 3, 4, 5, 6, 7, 8):
+    if config not in (1, 2, 3, 4, 5, 6, 7, 8, 9):
         raise SystemExit(f"unsupported --config {config}")
-    if config in (7, 8) and nranks > 1:
+    if config in (7, 8, 9) and nranks > 1:
         raise SystemExit("unstructured workloads (--config 7/8) run on one GPU")
     if config == 7:  # unstructured analogue of config 2: 28,800 triangles
         return bi.config_u2()
     if config == 8:  # unstructured analogue of config 3: 196,608 tetrahedra
         return bi.config_u3()
+    if config == 9:  # config 7 on jittered quadrilaterals: 14,400 cells
+        return bi.config_uq()
     if config == 2:
         p = bi.config2()
         if nranks > 1:  # weak scaling: 120 rows per GPU along the slab axis
@@ -204,7 +206,9 @@ def _oracle_sample(p, target_s: float, max_steps: int = 1000):
 
 
 def _umesh_problem(p, n):
-    return bi.config_u2(n=n) if p.mesh.dim == 2 else bi.config_u3(n=n)
+    if p.mesh.dim == 3:
+        return bi.config_u3(n=n)
+    return bi.config_uq(n=n) if p.mesh.cells.shape[1] == 4 else bi.config_u2(n=n)
 
 
 def _oracle_sample_umesh(p, target_s, max_steps, nthreads):

@@ -688,9 +688,11 @@ def config_u3(n: int = 32, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20)
 
 
 def small_umesh(dim: int = 2, n=(4, 3, 2), dirs=None, bands=None, bcs=None, dt=1e-12, shuffle=False,
-                jitter=None, seed=17) -> Problem:
+                jitter=None, seed=17, quad=False) -> Problem:
     """Small unstructured case for parity tests."""
-    if dim == 2:
+    if dim == 2 and quad:
+        mesh = umesh_quad(n[0], n[1], n[0] * 1e-6, n[1] * 1e-6, 0.2 if jitter is None else jitter, seed, shuffle)
+    elif dim == 2:
         mesh = umesh_tri(n[0], n[1], n[0] * 1e-6, n[1] * 1e-6, 0.2 if jitter is None else jitter, seed, shuffle)
     else:
         mesh = umesh_tet(n[0], n[1], n[2], 1e-6, 0.1 if jitter is None else jitter, seed, shuffle)

@@ -170,12 +170,13 @@ BTE_API bte_status bte_create(const bte_mesh *mesh, const bte_dirs *dirs, const 
 BTE_API bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                                    const bte_run *run, bte_ctx **out);
 
-/* Unstructured simplex mesh.  The finite-volume step is
+/* Unstructured mesh.  The finite-volume step is
  * Eq. 3 for m-sided cells with the upwind face value of
  * I' = I + dt*(beta (I0c - I) - v_b sum_f (A_f/V_c)(s_d.n_f) I_up).
- *   dim 2: triangles, cells[c][0..2]; verts z ignored; depth = z extent.
- *   dim 3: tetrahedra, cells[c][0..3].
- * Face k of cell c is the face opposite its local vertex k.  The domain is
+ *   dim 2: triangles (nvc 3) or convex quadrilaterals (nvc 4), verts z
+ *          ignored, depth = z extent; face k = edge (v_{k+1}, v_{k+2})
+ *          (for a triangle: the edge opposite v_k);
+ *   dim 3: tetrahedra, cells[c][0..3]; face k = the face opposite v_k.  The domain is
  * the axis-aligned bounding box of the vertices; every face without a
  * neighbour must lie on one of its walls (all face vertices at x = xmin ->
  * region 0, x = xmax -> 1, y -> 2/3, z -> 4/5, tested in that order).  Wall
@@ -187,8 +188,11 @@ typedef struct {
   int64_t nverts;
   const double *verts;   /* [nverts][3], metres */
   int64_t ncells;
-  const int64_t *cells;  /* [ncells][dim+1] vertex indices */
+  const int64_t *cells;  /* [ncells][nvc] vertex indices */
   double depth;          /* dim 2: z extent (volumes and face areas scale with it) */
+  int nvc;               /* vertices per cell: 0 -> dim + 1 (simplices); dim 2 also 4
+                            (convex quadrilaterals, vertices in boundary order:
+                            Eq. 3's "polygonal cell with m sides") */
 } bte_umesh;
 
 /* Create a single-GPU context on an unstructured mesh.  Geometry precompute

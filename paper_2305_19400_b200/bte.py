@@ -42,7 +42,7 @@ class Mesh(C.Structure):
 
 class UMeshC(C.Structure):
     _fields_ = [("dim", C.c_int), ("nverts", C.c_int64), ("verts", C.c_void_p), ("ncells", C.c_int64),
-                ("cells", C.c_void_p), ("depth", C.c_double)]
+                ("cells", C.c_void_p), ("depth", C.c_double), ("nvc", C.c_int)]
 
 
 class Dirs(C.Structure):
@@ -184,7 +184,8 @@ class Solver:
             verts = np.ascontiguousarray(mesh.verts, dtype=np.float64)
             cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
             k(verts), k(cells)
-            m = UMeshC(int(mesh.dim), verts.shape[0], _p(verts), cells.shape[0], _p(cells), float(mesh.depth))
+            m = UMeshC(int(mesh.dim), verts.shape[0], _p(verts), cells.shape[0], _p(cells), float(mesh.depth),
+                       int(cells.shape[1]))
         else:
             m = Mesh(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.dx, mesh.dy, mesh.dz)
         s, w = _f64(dirs.s), _f64(dirs.w)

@@ -315,7 +315,7 @@ struct UHost {
 // oriented away from the opposite vertex.  Faces matched by their vertex sets;
 // unmatched faces classified onto the box walls (region order -x,+x,-y,+y,-z,+z).
 static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
-  const int dim = um->dim, K = dim + 1;
+  const int dim = um->dim, K = um->nvc > 0 ? um->nvc : dim + 1;
   const int64_t nc = um->ncells, nv = um->nverts;
   h->dim = dim;
   h->K = K;
@@ -354,8 +354,13 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
     for (int k = 1; k < K; ++k)
       for (int a = 0; a < 3; ++a) cen[a] = cen[a] + X[k][a];
     for (int a = 0; a < 3; ++a) h->cen[3 * c + a] = cen[a] / K;
-    double scale = 0.0;  // 2/|cross| or 3/|det|
-    if (dim == 2) {
+    double scale = 0.0;  // 2/|cross| (2/|shoelace|) or 3/|det|
+    if (dim == 2 && K == 4) {  // convex quadrilateral: shoelace area
+      double sh = 0.0;
+      for (int k = 0; k < 4; ++k) sh += X[k][0] * X[(k + 1) & 3][1] - X[(k + 1) & 3][0] * X[k][1];
+      h->vol[c] = std::fabs(sh) * 0.5 * um->depth;
+      scale = 2.0 / std::fabs(sh);
+    } else if (dim == 2) {
       const double cr = (X[1][0] - X[0][0]) * (X[2][1] - X[0][1]) - (X[1][1] - X[0][1]) * (X[2][0] - X[0][0]);
       h->vol[c] = std::fabs(cr) * 0.5 * um->depth;
       scale = 2.0 / std::fabs(cr);
@@ -375,8 +380,15 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
     }
     for (int k = 0; k < K; ++k) {
       int q[3], n = 0;
-      for (int i = 0; i < K; ++i)
-        if (i != k) q[n++] = i;
+      if (dim == 2) {  // edge (v_{k+1}, v_{k+2})
+        q[0] = (k + 1) % K;
+        q[1] = (k + 2) % K;
+        q[2] = q[1];
+        n = 2;
+      } else {
+        for (int i = 0; i < K; ++i)
+          if (i != k) q[n++] = i;
+      }
       double An[3];
       if (dim == 2) {
         const double ex = X[q[1]][0] - X[q[0]][0], ey = X[q[1]][1] - X[q[0]][1];
@@ -393,8 +405,9 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
         An[1] = u[2] * w[0] - u[0] * w[2];
         An[2] = u[0] * w[1] - u[1] * w[0];
       }
+      // outward: away from the opposite vertex (simplices) or the vertex mean (quadrilaterals)
       double o = 0.0;
-      for (int a = 0; a < 3; ++a) o += An[a] * (X[k][a] - X[q[0]][a]);
+      for (int a = 0; a < 3; ++a) o += An[a] * ((K == 4 && dim == 2 ? h->cen[3 * c + a] : X[k][a]) - X[q[0]][a]);
       const double sg = o > 0.0 ? -scale : scale;
       for (int a = 0; a < 3; ++a) h->an[(c * K + k) * 3 + a] = sg * An[a];
       FaceKey &fk = keys[c * K + k];
@@ -435,8 +448,12 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
         const int a = r / 2;
         const double wall = (r & 1) ? hi[a] : h->lo[a];
         bool on = true;
-        for (int i = 0; i < K; ++i)
-          if (i != k && um->verts[3 * cv[i] + a] != wall) on = false;
+        if (dim == 2) {
+          on = um->verts[3 * cv[(k + 1) % K] + a] == wall && um->verts[3 * cv[(k + 2) % K] + a] == wall;
+        } else {
+          for (int i = 0; i < K; ++i)
+            if (i != k && um->verts[3 * cv[i] + a] != wall) on = false;
+        }
         if (on) reg = r;
       }
       if (reg < 0) {
@@ -465,6 +482,8 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
   if (um->ncells < 1 || um->nverts < um->dim + 1) return early("empty unstructured mesh");
   if (um->ncells > (1ll << 30)) return early("unstructured mesh too large");
   if (um->dim == 2 && !(um->depth > 0)) return early("depth must be > 0");
+  if (um->nvc != 0 && !(um->nvc == um->dim + 1 || (um->dim == 2 && um->nvc == 4)))
+    return early("vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4");
   if (run && run->nranks != 1) return early("unstructured contexts are single-rank (nranks must be 1)");
   UHost uh;
   std::string err;

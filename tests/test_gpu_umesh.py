@@ -184,3 +184,37 @@ def test_umesh_kernel_variants_bitwise(Solver, dim, monkeypatch):
         assert np.array_equal(Ix, out[1][0]) and np.array_equal(Tx, out[1][1])
     assert np.max(np.abs(out[1][0] / out[0][0] - 1)) < 1e-13
     assert np.max(np.abs(out[1][1] - out[0][1])) < 1e-10
+
+
+# ----------------------------------------------------------------- quadrilaterals (Eq. 3 "polygonal cell with m sides")
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_uquad_parity(Solver, shuffle):
+    p = bi.small_umesh(2, (6, 5, 1), shuffle=shuffle, quad=True)
+    p.bcs = _walls(p)
+    rel, dT = _run_both(Solver, p, 8)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_uquad_silicon_and_structured_equivalence(Solver):
+    """Jittered quads with the bench's 400 x 40 against the oracle; an unjittered
+    row-major quad mesh on the GPU agrees with the structured GPU path."""
+    p = bi.config_uq(n=10)
+    rel, dT = _run_both(Solver, p, 3)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    h = 2.0 ** -19
+    nx, ny = 7, 6
+    b = bi.subset_bands(bi.silicon_bands(29), [1, 18, 34, 39])
+    d = bi.directions_control_angle(4, 8)
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, 300.0 + np.arange(nx)), bi.WallBC(3, specularity=0.3),
+           bi.WallBC(1), bi.WallBC(1)]
+    ps = bi.Problem("grid", bi.Mesh(2, nx, ny, 1, h, h, 1.0), d, b, 1e-12, 300.0, bcs, seed=4)
+    pu = bi.Problem("quads", bi.umesh_quad(nx, ny, nx * h, ny * h, jitter=0.0), d, b, 1e-12, 300.0, bcs, seed=4)
+    I, T = oracle.Oracle(ps).random_state()
+    out = []
+    for p in (ps, pu):
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(6)
+            out.append((sv.intensity(), sv.temperature()))
+    assert np.max(np.abs(out[1][0] / out[0][0] - 1)) < 1e-12 and np.max(np.abs(out[1][1] - out[0][1])) < 1e-9
