@@ -201,8 +201,13 @@ typedef struct {
  * from the opposite vertex), face matching by vertex sets, wall regions.
  * State layout, set_state/get_* orders, the temperature update and the wall
  * kinds are as for bte_create (canonical cell index = position in cells).
- * run->nranks must be 1 (no slab/band decomposition of unstructured meshes);
- * octant-slot rotation is not used.  The dt check is the general positivity
+ * run->nranks > 1 partitions the mesh: rank r owns the
+ * contiguous canonical cell range [r*nc/P, (r+1)*nc/P) (bte_info.cell0 /
+ * ncells_local; state I/O covers those cells) and keeps read-only halo copies
+ * of the face neighbours owned elsewhere, refreshed after every step by NCCL
+ * send/recv (run->nccl_id) or device copies inside bte_group_step (local
+ * mode).  Every rank must pass the whole mesh.  Octant-slot rotation is not
+ * used.  The dt check is the general positivity
  * bound 1 - dt beta_b - dt v_b max_c sum_{f: s.n>0} (A_f/V_c) s.n >= 0.
  * Errors: BTE_EINVAL (degenerate cell, bad vertex index, a face shared by more
  * than two cells, a boundary face off the box walls, nranks != 1, or as
@@ -371,6 +376,7 @@ typedef struct {
   int64_t bytes_state;                               /* device bytes held by ctx    */
   int b0, b1, nb_total, band;                        /* channel band; band = 1 for bte_create_band */
   int rotate;                                        /* 1: octant-slot rotation (see bte_create)  */
+  int64_t cell0;                                     /* canonical index of the first owned cell   */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

@@ -88,7 +88,7 @@ class Info(C.Structure):
     _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
                 ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
-                ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int)]
+                ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int), ("cell0", C.c_int64)]
 
 
 _lib = None
@@ -179,8 +179,8 @@ class Solver:
 
         self.umesh = hasattr(mesh, "cells")
         if self.umesh:  # unstructured simplex mesh (bte_create_umesh)
-            if decomp != "slab" or nranks != 1:
-                raise ValueError("unstructured meshes run on one context (nranks = 1)")
+            if decomp != "slab":
+                raise ValueError("unstructured meshes partition by cells (decomp='slab')")
             verts = np.ascontiguousarray(mesh.verts, dtype=np.float64)
             cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
             k(verts), k(cells)
@@ -241,6 +241,7 @@ class Solver:
         self.b0, self.b1, self.nb_total = int(info.b0), int(info.b1), int(info.nb_total)
         self.band = bool(info.band)
         self.rotate = bool(info.rotate)
+        self.cell0 = int(info.cell0)
         if self.nb_total == 0:  # older A/B build without the band fields
             self.b0, self.b1, self.nb_total = 0, self.nb, self.nb
 

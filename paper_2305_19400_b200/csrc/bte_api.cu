@@ -38,6 +38,12 @@ const double kGL16[16][2] = {
 
 }  // namespace
 
+struct UPeer {                  // one neighbour rank of a partitioned unstructured mesh
+  int peer = 0;
+  int64_t recv_off = 0, recv_cnt = 0;  // its cells in my halo: halo positions [off, off + cnt)
+  std::vector<int64_t> send_cells;     // my cells (local indices) in its halo, in its halo order
+};
+
 struct bte_ctx {
   std::string err;
   // configuration
@@ -115,6 +121,11 @@ struct bte_ctx {
   std::vector<double> uvol;  // V_c
   std::vector<double> uKd;   // per direction: max_c sum_{f: s.an > 0} s.an (dt check)
   double *d_ucen = nullptr;  // [nc][3] centroids (random start)
+  int64_t urn_global[6] = {0, 0, 0, 0, 0, 0};  // wall faces per region (whole mesh)
+  std::vector<UPeer> upeers;                    // partition: neighbour ranks
+  int64_t unhalo = 0;
+  std::vector<int64_t *> d_usend;               // per peer: device send-cell lists
+  double *d_usendbuf = nullptr, *d_urecvbuf = nullptr;  // packed [peer][slot][k][Es]
   double ulo[3] = {0, 0, 0}, uL[3] = {0, 0, 0};
   // NCCL
   bte_slab_plan plan{};
@@ -211,7 +222,7 @@ static bte_status refresh(bte_ctx *ctx) {
 static int64_t ncl_of(const bte_ctx *ctx) { return ctx->ncells_local; }
 
 static int64_t n_faces_global(const bte_ctx *ctx, int region) {
-  if (ctx->umesh) return ctx->u.rn[region];
+  if (ctx->umesh) return ctx->urn_global[region];
   const int a = region / 2;
   const bte_mesh &m = ctx->mesh;
   if (a == 0) return m.ny * m.nz;
@@ -245,6 +256,7 @@ static bte_status sync_check(bte_ctx *ctx) {
 extern "C" {
 
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream = nullptr);
+static bte_status uhalo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream);
 
 const char *bte_version(void) { return "bte-b200 0.1 (sm_100a, fp64)"; }
 
@@ -301,14 +313,102 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
 // ---- unstructured simplex meshes: host geometry precompute (a0)
 struct UHost {
   int dim = 0, K = 0;
-  int64_t nc = 0;
-  std::vector<int64_t> nbr;   // [nc][K]
+  int64_t nc = 0;             // cells held (owned), local numbering
+  int64_t nc_global = 0, c0 = 0, nhalo = 0;
+  std::vector<int64_t> nbr;   // [nc][K]: local neighbour (owned or n_own + halo position) or wall code
   std::vector<double> an;     // [nc][K][3] A_f n_f / V_c
   std::vector<double> vol;    // [nc]
   std::vector<double> cen;    // [nc][3]
-  std::vector<int64_t> rcell[6];
+  std::vector<int64_t> rcell[6];  // owned wall faces: local cell
+  std::vector<int64_t> rface[6];  // ... and global face index
+  int64_t rn_global[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<UPeer> peers;
   double lo[3], L[3];
 };
+
+// Partition of an unstructured mesh over P ranks (SURVEY 8(f) f3 "graph
+// partitioning"): rank r owns the contiguous canonical range
+// [r*nc/P, (r+1)*nc/P) -- the generators and locality-ordered inputs make that a
+// spatially compact part -- plus read-only halo copies of the face neighbours
+// of its cells owned elsewhere, numbered after its own cells grouped by owner
+// rank (canonical order inside a group).  Every rank derives the same plan
+// from the global mesh.
+static void partition_uhost(const UHost &G, int P, int rank, UHost *L) {
+  const int K = G.K;
+  const int64_t nc = G.nc;
+  std::vector<int64_t> cut(P + 1);
+  for (int r = 0; r <= P; ++r) cut[r] = (int64_t)r * nc / P;
+  auto owner = [&](int64_t c) { return (int)(std::upper_bound(cut.begin(), cut.end(), c) - cut.begin()) - 1; };
+  const int64_t c0 = cut[rank], c1 = cut[rank + 1];
+  auto halo_of = [&](int r) {  // canonical cells outside part r adjacent to it, sorted (owner, cell)
+    std::vector<int64_t> h;
+    for (int64_t c = cut[r]; c < cut[r + 1]; ++c)
+      for (int f = 0; f < K; ++f) {
+        const int64_t e = G.nbr[c * K + f];
+        if (e >= 0 && (e < cut[r] || e >= cut[r + 1])) h.push_back(e);
+      }
+    std::sort(h.begin(), h.end());
+    h.erase(std::unique(h.begin(), h.end()), h.end());
+    std::stable_sort(h.begin(), h.end(), [&](int64_t a, int64_t b) { return owner(a) < owner(b); });
+    return h;
+  };
+  const std::vector<int64_t> halo = halo_of(rank);
+  *L = UHost();
+  L->dim = G.dim;
+  L->K = K;
+  L->nc = c1 - c0;
+  L->nc_global = nc;
+  L->c0 = c0;
+  L->nhalo = (int64_t)halo.size();
+  for (int a = 0; a < 3; ++a) {
+    L->lo[a] = G.lo[a];
+    L->L[a] = G.L[a];
+  }
+  std::vector<int64_t> hpos(halo.size());
+  auto local = [&](int64_t e) -> int64_t {
+    if (e >= c0 && e < c1) return e - c0;
+    // halo position: the halo is sorted by (owner, cell)
+    const int o = owner(e);
+    auto it = std::lower_bound(halo.begin(), halo.end(), e, [&](int64_t a, int64_t b) {
+      const int oa = owner(a), ob = owner(b);
+      return oa != ob ? oa < ob : a < b;
+    });
+    (void)o;
+    return L->nc + (int64_t)(it - halo.begin());
+  };
+  L->nbr.resize(L->nc * K);
+  L->an.assign(G.an.begin() + c0 * K * 3, G.an.begin() + c1 * K * 3);
+  L->vol.assign(G.vol.begin() + c0, G.vol.begin() + c1);
+  L->cen.assign(G.cen.begin() + c0 * 3, G.cen.begin() + c1 * 3);
+  for (int64_t c = c0; c < c1; ++c)
+    for (int f = 0; f < K; ++f) {
+      const int64_t e = G.nbr[c * K + f];
+      L->nbr[(c - c0) * K + f] = e >= 0 ? local(e) : e;  // wall codes keep the global face index
+    }
+  for (int r = 0; r < 6; ++r) {
+    L->rn_global[r] = (int64_t)G.rcell[r].size();
+    for (int64_t f = 0; f < (int64_t)G.rcell[r].size(); ++f) {
+      const int64_t c = G.rcell[r][f];
+      if (c >= c0 && c < c1) {
+        L->rcell[r].push_back(c - c0);
+        L->rface[r].push_back(f);
+      }
+    }
+  }
+  for (int q = 0; q < P; ++q) {
+    if (q == rank) continue;
+    UPeer pe;
+    pe.peer = q;
+    for (int64_t i = 0; i < (int64_t)halo.size(); ++i)
+      if (owner(halo[i]) == q) {
+        if (pe.recv_cnt == 0) pe.recv_off = i;
+        ++pe.recv_cnt;
+      }
+    for (int64_t e : halo_of(q))
+      if (e >= c0 && e < c1) pe.send_cells.push_back(e - c0);
+    if (pe.recv_cnt || !pe.send_cells.empty()) L->peers.push_back(pe);
+  }
+}
 
 // Eq. 3 geometry without square roots: triangle A_f n_f / V_c = 2 perp(edge) /
 // |cross| (depth cancels), tetrahedron = 3 cross(b - a, c - a) / |det|, each
@@ -462,8 +562,11 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
       }
       h->nbr[c * K + k] = -1 - (count[reg] * 8 + reg);
       h->rcell[reg].push_back(c);
+      h->rface[reg].push_back(count[reg]);
       ++count[reg];
     }
+  for (int r = 0; r < 6; ++r) h->rn_global[r] = count[r];
+  h->nc_global = nc;
   return true;
 }
 
@@ -484,12 +587,19 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
   if (um->dim == 2 && !(um->depth > 0)) return early("depth must be > 0");
   if (um->nvc != 0 && !(um->nvc == um->dim + 1 || (um->dim == 2 && um->nvc == 4)))
     return early("vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4");
-  if (run && run->nranks != 1) return early("unstructured contexts are single-rank (nranks must be 1)");
+  if (run && (run->nranks < 1 || run->rank < 0 || run->rank >= run->nranks || run->nranks > um->ncells))
+    return early("bad rank/nranks for the unstructured partition");
   UHost uh;
   std::string err;
   if (!build_uhost(um, &uh, &err)) return early(err.c_str());
-  // the state layout sees one plane of ncells cross cells
-  bte_mesh fm{um->dim, um->ncells, 1, 1, 1.0, 1.0, 1.0};
+  if (run && run->nranks > 1) {
+    UHost part;
+    partition_uhost(uh, run->nranks, run->rank, &part);
+    uh = std::move(part);
+  }
+  // the state layout sees one plane of the owned cells (the halo copies follow
+  // them inside each octant-slot region)
+  bte_mesh fm{um->dim, uh.nc, 1, 1, 1.0, 1.0, 1.0};
   return create_impl(&fm, dirs, bands, run, false, out, &uh);
 }
 
@@ -565,7 +675,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   ctx->nbT = bands->nb;
   ctx->nb = bands->nb;
   ctx->band = band ? 1 : 0;
-  ctx->slab_ranks = band ? 1 : run->nranks;
+  ctx->slab_ranks = (band || uh) ? 1 : run->nranks;  // unstructured parts exchange halo cells, not planes
   if (band) {
     int b1 = 0;
     if (bte_plan_band(bands->nb, run->nranks, run->rank, &ctx->b0, &b1) != BTE_OK)
@@ -663,8 +773,10 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   g.Es = g.E + (g.E & 1);
   g.plane_stride = (int64_t)g.ncross * g.Es;
   g.slot_stride = (int64_t)(g.nplanes + 2 * g.plane_off) * g.plane_stride;
+  if (uh) g.slot_stride = (uh->nc + uh->nhalo) * (int64_t)g.Es;  // owned blocks, then the halo copies
   ctx->ncells_local = (int64_t)g.nplanes * g.ncross;
-  ctx->ncells_global = mesh->nx * mesh->ny * mesh->nz;
+  ctx->ncells_global = uh ? uh->nc_global : mesh->nx * mesh->ny * mesh->nz;
+  g.cell0 = uh ? uh->c0 : g.m0 * g.ncross;  // canonical index of the first owned cell
 
   if (cudaSetDevice(ctx->device) != cudaSuccess) return bail(fail(ctx, BTE_ECUDA, "cudaSetDevice(%d) failed", ctx->device));
 
@@ -786,7 +898,12 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     }
     ctx->u.K = uh->K;
     ctx->u.ncells = uh->nc;
-    for (int r = 0; r < 6; ++r) ctx->u.rn[r] = (int64_t)uh->rcell[r].size();
+    for (int r = 0; r < 6; ++r) {
+      ctx->u.rn[r] = (int64_t)uh->rcell[r].size();
+      ctx->urn_global[r] = uh->rn_global[r];
+    }
+    ctx->upeers = uh->peers;
+    ctx->unhalo = uh->nhalo;
   }
   if (run->step_mode != 0 && run->step_mode != 1) return bail(fail(ctx, BTE_EINVAL, "step_mode must be 0 or 1"));
   if (run->step_mode == 1 && band) return bail(fail(ctx, BTE_EINVAL, "semi-implicit step: not for band contexts"));
@@ -957,9 +1074,24 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     ctx->u.an = d_an;
     ctx->u.sw = d_sw;
     for (int r = 0; r < 6; ++r) {
-      int64_t *d_rc = nullptr;
+      int64_t *d_rc = nullptr, *d_rf = nullptr;
       if ((st = upload(ctx, &d_rc, uh->rcell[r].data(), uh->rcell[r].size()))) return bail(st);
+      if ((st = upload(ctx, &d_rf, uh->rface[r].data(), uh->rface[r].size()))) return bail(st);
       ctx->u.rcell[r] = d_rc;
+      ctx->u.rface[r] = d_rf;
+    }
+    int64_t nsend = 0, nrecv = 0;
+    for (const UPeer &pe : ctx->upeers) {
+      int64_t *d_sc = nullptr;
+      if ((st = upload(ctx, &d_sc, pe.send_cells.data(), pe.send_cells.size()))) return bail(st);
+      ctx->d_usend.push_back(d_sc);
+      nsend += (int64_t)pe.send_cells.size();
+      nrecv += pe.recv_cnt;
+    }
+    if (!ctx->upeers.empty()) {
+      ctx->d_usendbuf = (double *)dev_alloc(ctx, (size_t)nsend * nslot * g.Es * sizeof(double));
+      ctx->d_urecvbuf = (double *)dev_alloc(ctx, (size_t)nrecv * nslot * g.Es * sizeof(double));
+      if (!ctx->d_usendbuf || !ctx->d_urecvbuf) return bail(fail(ctx, BTE_ENOMEM, "halo buffer allocation failed"));
     }
   }
   if (const char *e = getenv("BTE_SWEEP")) ctx->use_tma = strcmp(e, "plain") != 0;
@@ -1026,7 +1158,9 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   if ((st = refresh(ctx))) return bail(st);
   CU(launch_fill_equilibrium(g, ctx->I0s, ctx->I[0], ctx->stream));
   ctx->cur = 0;
-  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[0]))) return bail(st);
+  if (ctx->nccl_comm && !ctx->band &&
+      (st = ctx->umesh ? uhalo_exchange(ctx, ctx->I[0], nullptr) : halo_exchange(ctx, ctx->I[0])))
+    return bail(st);
   CU(cudaStreamSynchronize(ctx->stream));
   *out = ctx;
   return BTE_OK;
@@ -1142,7 +1276,9 @@ bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   } else {
     CU(launch_fill_equilibrium(ctx->g, ctx->I0s, ctx->I[ctx->cur], ctx->stream));
   }
-  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if (ctx->nccl_comm && !ctx->band &&
+      (st = ctx->umesh ? uhalo_exchange(ctx, ctx->I[ctx->cur], nullptr) : halo_exchange(ctx, ctx->I[ctx->cur])))
+    return st;
   if (I && !T) {
     // T from one reduction + Newton from T_init (beta_next = beta(T_init)):
     // Dpart = sum_j w_j (I0c - I) per octant of the given I, then the Newton kernel.
@@ -1178,7 +1314,9 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
     CU(launch_random_T(ctx->g, 0, m.dx, m.dy, m.dz, phase, T_mean, T_amp, ctx->T, ctx->stream));
   if ((st = refresh(ctx))) return st;
   CU(launch_random_I(ctx->g, ctx->d_canon_d, ctx->nd, seed, I_amp, ctx->I0s, ctx->I[ctx->cur], ctx->stream));
-  if (ctx->nccl_comm && !ctx->band && (st = halo_exchange(ctx, ctx->I[ctx->cur]))) return st;
+  if (ctx->nccl_comm && !ctx->band &&
+      (st = ctx->umesh ? uhalo_exchange(ctx, ctx->I[ctx->cur], nullptr) : halo_exchange(ctx, ctx->I[ctx->cur])))
+    return st;
   CU(cudaStreamSynchronize(ctx->stream));
   return BTE_OK;
 }
@@ -1246,7 +1384,7 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   for (int o = 0; o < 8; ++o) a.oct_slot[o] = ctx->g.oct_slot[o];
   a.W = ctx->W;
   a.ncells = ctx->ncells_local;
-  a.cell0_global = ctx->g.m0 * ctx->g.ncross;
+  a.cell0_global = ctx->g.cell0;
   a.err = ctx->d_err;
   a.step = step;
   a.col0 = 0;
@@ -1416,7 +1554,7 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   }
   // the semi-implicit step exchanges halos after its relaxation pass
-  if (split && (C > 1 || ctx->fuse_newton || ctx->rot || ctx->semi)) split = false;
+  if (split && (C > 1 || ctx->fuse_newton || ctx->rot || ctx->semi || ctx->umesh)) split = false;
   if (split) {
     int fused = 0;
     id = (size_t)-1;
@@ -1558,7 +1696,9 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
       CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
       size_t id = (size_t)-1;
       if ((st = span_begin(ctx, t, 3, ctx->comm_stream, &id))) return st;
-      if ((st = halo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream))) return st;
+      if ((st = ctx->umesh ? uhalo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream)
+                           : halo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream)))
+        return st;
       if ((st = span_end(ctx, t, ctx->comm_stream, id))) return st;
       CU(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
       CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
@@ -1689,6 +1829,97 @@ static bte_status band_exchange(bte_ctx **ctxs, int n) {
   return BTE_OK;
 }
 
+// ---- partitioned unstructured meshes: halo cells
+// Where peer q's cells sit in my halo: block position n_own + recv_off of every slot region.
+static double *uhalo_dst(bte_ctx *q, double *Ibuf, int slot, int64_t recv_off) {
+  return Ibuf + q->g.slot_off[slot] + (q->ncells_local + recv_off) * (int64_t)q->g.Es;
+}
+
+// In-process group: every rank packs the cells its peers hold as halo copies
+// (buffer `output` ? I[1-cur] : I[cur]) once its step is done, then copies each
+// peer's segment slot by slot into the peer's halo blocks; receivers wait.
+static bte_status ugroup_exchange(bte_ctx **ctxs, int n, bool output) {
+  bte_ctx *ctx = ctxs[0];
+  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
+    if (atoi(e)) return BTE_OK;
+  std::vector<cudaEvent_t> done(n), put(n);
+  for (int r = 0; r < n; ++r) {
+    CU(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&put[r], cudaEventDisableTiming));
+    CU(cudaEventRecord(done[r], ctxs[r]->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    bte_ctx *c = ctxs[r];
+    const Geometry &g = c->g;
+    const double *src = c->I[output ? 1 - c->cur : c->cur];
+    int64_t off = 0;
+    for (size_t k = 0; k < c->upeers.size(); ++k) {
+      const UPeer &pe = c->upeers[k];
+      const int64_t cnt = (int64_t)pe.send_cells.size();
+      if (cnt == 0) continue;
+      bte_ctx *q = ctxs[pe.peer];
+      double *seg = c->d_usendbuf + off * g.nslot * g.Es;
+      CU(launch_pack_cells(g, c->d_usend[k], cnt, src, seg, c->stream));
+      CU(cudaStreamWaitEvent(c->stream, done[pe.peer], 0));
+      // where q keeps my cells
+      int64_t roff = -1;
+      for (const UPeer &qe : q->upeers)
+        if (qe.peer == r) roff = qe.recv_off;
+      if (roff < 0) return fail(ctx, BTE_EINVAL, "inconsistent unstructured halo plan (rank %d -> %d)", r, pe.peer);
+      double *dstb = q->I[output ? 1 - q->cur : q->cur];
+      for (int sl = 0; sl < g.nslot; ++sl)
+        CU(cudaMemcpyAsync(uhalo_dst(q, dstb, sl, roff), seg + (int64_t)sl * cnt * g.Es,
+                           (size_t)cnt * g.Es * sizeof(double), cudaMemcpyDefault, c->stream));
+      off += cnt;
+    }
+    CU(cudaEventRecord(put[r], c->stream));
+  }
+  for (int r = 0; r < n; ++r)
+    for (const UPeer &pe : ctxs[r]->upeers)
+      if (pe.recv_cnt) CU(cudaStreamWaitEvent(ctxs[r]->stream, put[pe.peer], 0));
+  for (int r = 0; r < n; ++r) {
+    cudaEventDestroy(done[r]);
+    cudaEventDestroy(put[r]);
+  }
+  return BTE_OK;
+}
+
+// NCCL: pack, grouped send/recv of the packed segments, scatter into the halo.
+static bte_status uhalo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream) {
+  const Geometry &g = ctx->g;
+  if (!stream) stream = ctx->stream;
+  std::string emsg;
+  int64_t soff = 0;
+  for (size_t k = 0; k < ctx->upeers.size(); ++k) {
+    const int64_t cnt = (int64_t)ctx->upeers[k].send_cells.size();
+    CU(launch_pack_cells(g, ctx->d_usend[k], cnt, Ibuf, ctx->d_usendbuf + soff * g.nslot * g.Es, stream));
+    soff += cnt;
+  }
+  if (nccl_shim_group_start(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+  soff = 0;
+  int64_t roff = 0;
+  for (const UPeer &pe : ctx->upeers) {
+    const int64_t cnt = (int64_t)pe.send_cells.size();
+    if (cnt && nccl_shim_send(ctx->nccl_comm, ctx->d_usendbuf + soff * g.nslot * g.Es, (size_t)(cnt * g.nslot * g.Es),
+                              pe.peer, stream, &emsg))
+      return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+    if (pe.recv_cnt && nccl_shim_recv(ctx->nccl_comm, ctx->d_urecvbuf + roff * g.nslot * g.Es,
+                                      (size_t)(pe.recv_cnt * g.nslot * g.Es), pe.peer, stream, &emsg))
+      return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+    soff += cnt;
+    roff += pe.recv_cnt;
+  }
+  if (nccl_shim_group_end(&emsg)) return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+  roff = 0;
+  for (const UPeer &pe : ctx->upeers) {
+    for (int sl = 0; sl < g.nslot && pe.recv_cnt; ++sl)
+      CU(cudaMemcpyAsync(uhalo_dst(ctx, Ibuf, sl, pe.recv_off), ctx->d_urecvbuf + (roff * g.nslot + sl * pe.recv_cnt) * g.Es,
+                         (size_t)pe.recv_cnt * g.Es * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    roff += pe.recv_cnt;
+  }
+  return BTE_OK;
+}
+
 bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
   if (!ctxs || n < 1 || nsteps < 0) return BTE_EINVAL;
   for (int r = 0; r < n; ++r) {
@@ -1721,14 +1952,16 @@ bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
       if ((st = sync_check(ctxs[r]))) return st;
     return BTE_OK;
   }
-  if (n > 1 && (st = group_exchange(ctxs, n, false))) return st;  // prime halos from the current state
+  const bool um = ctxs[0]->umesh;
+  if (n > 1 && (st = um ? ugroup_exchange(ctxs, n, false) : group_exchange(ctxs, n, false)))
+    return st;  // prime halos from the current state
   for (int64_t s = 0; s < nsteps; ++s) {
     for (int r = 0; r < n; ++r) {
       const bool t = ctxs[r]->timing && ctxs[r]->timing_used < ctxs[r]->timing_max;
       if ((st = step_launch(ctxs[r], t, n > 1 && ctxs[r]->overlap))) return st;
       if ((st = join_newton(ctxs[r]))) return st;
     }
-    if (n > 1 && (st = group_exchange_overlap(ctxs, n))) return st;
+    if (n > 1 && (st = um ? ugroup_exchange(ctxs, n, true) : group_exchange_overlap(ctxs, n))) return st;
     for (int r = 0; r < n; ++r) {
       bte_ctx *c = ctxs[r];
       if (c->timing && c->timing_used < c->timing_max) c->timing_used++;
@@ -1907,6 +2140,7 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
   out->nb_total = ctx->nbT;
   out->band = ctx->band;
   out->rotate = ctx->rot;
+  out->cell0 = ctx->g.cell0;
   return BTE_OK;
 }
 

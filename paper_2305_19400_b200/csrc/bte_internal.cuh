@@ -55,6 +55,7 @@ struct Geometry {
   int ncross;             // cells per plane
   int nplanes;            // owned planes along the march axis
   int64_t m0;             // global index of the first owned plane
+  int64_t cell0;          // canonical index of the first owned cell (random start, errors)
   int64_t nplanes_global;
   int plane_off;          // 1 when halo planes are stored, else 0
   int64_t plane_stride;   // doubles per plane (ncross * E)
@@ -145,8 +146,9 @@ struct UMeshDev {
   const int64_t *nbr;     // [nc][4] (faces >= K unused): neighbour >= 0, or -1 - (face_in_region * 8 + region)
   const double *an;       // [nc][4][3] (faces >= K unused): (A_f / V_c) n_f
   const double *sw;       // [nslot * nj][4]: s_x, s_y, s_z, w of direction (slot, j)
-  const int64_t *rcell[6];  // wall face -> cell
-  int64_t rn[6];          // wall faces per region
+  const int64_t *rcell[6];  // owned wall faces: local cell
+  const int64_t *rface[6];  // ... and their global face index (ghost-table row)
+  int64_t rn[6];          // owned wall faces per region
 };
 
 struct USweepArgs {
@@ -187,6 +189,8 @@ cudaError_t launch_gather_cells(const Geometry &g, const int *dmap, int nd, cons
                                 const double *I, double *out, cudaStream_t s);
 cudaError_t launch_relax(const Geometry &g, double *I, const double *I0c, const double *beta, double dt,
                          cudaStream_t s);
+cudaError_t launch_pack_cells(const Geometry &g, const int64_t *cells, int64_t n, const double *I, double *out,
+                              cudaStream_t s);
 cudaError_t launch_random_I(const Geometry &g, const int *canon_d, int nd, uint64_t seed,
                             double I_amp, const double *I0c, double *I, cudaStream_t s);
 cudaError_t launch_octant_tree_g(const Geometry &g, const double *Dpart, int64_t nc, double *D,

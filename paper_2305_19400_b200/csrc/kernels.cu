@@ -1861,6 +1861,24 @@ cudaError_t launch_relax(const Geometry &g, double *I, const double *I0c, const 
   return cudaGetLastError();
 }
 
+// partitioned unstructured mesh: gather the blocks of `cells` (all octant
+// slots) into out[slot][k][Es] (the halo copies a neighbour rank receives)
+__global__ void k_pack_cells(const Geometry g, const int64_t *__restrict__ cells, int64_t n,
+                             const double *__restrict__ I, double *__restrict__ out) {
+  const int64_t k = blockIdx.x;
+  const int sl = blockIdx.y;
+  const double *src = I + g.slot_off[sl] + cells[k] * g.Es;
+  double *dst = out + ((int64_t)sl * n + k) * g.Es;
+  for (int e = threadIdx.x; e < g.Es; e += blockDim.x) dst[e] = src[e];
+}
+
+cudaError_t launch_pack_cells(const Geometry &g, const int64_t *cells, int64_t n, const double *I, double *out,
+                              cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_pack_cells<<<dim3((unsigned)n, g.nslot), 256, 0, s>>>(g, cells, n, I, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_random_T(const Geometry g, double dx, double dy, double dz, double p0, double p1,
                            double p2, double T_mean, double T_amp, double *__restrict__ T) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1913,7 +1931,7 @@ __global__ void k_random_I(const Geometry g, const int *__restrict__ canon_d, in
   const int j = e / g.nb;
   const int b = e - j * g.nb;
   const int d = canon_d[sl * g.nj + j];
-  const int64_t cg = g.m0 * g.ncross + cell;
+  const int64_t cg = g.cell0 + cell;
   const uint64_t idx = ((uint64_t)cg * nd + d) * g.nbT + g.b0 + b;
   const double u = (double)(splitmix64(seed ^ idx) >> 11) * 0x1.0p-53;
   I[g.slot_off[sl] + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] =
@@ -2465,8 +2483,8 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
 
 __global__ void k_udiffuse(const Geometry g, const UMeshDev u, const double *__restrict__ I, int region,
                            double *__restrict__ gtab) {
-  const int64_t f = blockIdx.x;
-  diffuse_face(g, I, region, f, u.rcell[region][f] * g.Es, gtab);
+  const int64_t f = blockIdx.x;  // owned wall face f: global row rface, local cell rcell
+  diffuse_face(g, I, region, u.rface[region][f], u.rcell[region][f] * g.Es, gtab);
 }
 
 cudaError_t launch_udiffuse(const Geometry &g, const UMeshDev &u, const double *I, int region, double *gtab,

@@ -157,8 +157,11 @@ def test_umesh_fixed_point_and_errors(Solver):
     with pytest.raises(BteError) as e:
         Solver.from_problem(q)
     assert e.value.status == 1
-    with pytest.raises(ValueError):
-        Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=0, nranks=2)
+    with pytest.raises(ValueError):  # unstructured meshes partition by cells, not channels
+        Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=0, nranks=2, decomp="band")
+    with pytest.raises(BteError) as e:  # more parts than cells
+        Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=0, nranks=p.mesh.ncells + 1)
+    assert e.value.status == 1
 
 
 @pytest.mark.parametrize("dim", [2, 3])
@@ -218,3 +221,87 @@ def test_uquad_silicon_and_structured_equivalence(Solver):
             sv.step(6)
             out.append((sv.intensity(), sv.temperature()))
     assert np.max(np.abs(out[1][0] / out[0][0] - 1)) < 1e-12 and np.max(np.abs(out[1][1] - out[0][1])) < 1e-9
+
+
+# ----------------------------------------------------------------- partitioned meshes (local groups)
+
+def _part_case(case):
+    if case == "tri":
+        p = bi.small_umesh(2, (7, 5, 1))
+    elif case == "quad":
+        p = bi.small_umesh(2, (6, 5, 1), quad=True, shuffle=True)
+    else:
+        p = bi.small_umesh(3, (3, 3, 3))
+    p.bcs = _walls(p)
+    return p
+
+
+def _part_group(Solver, p, P, I, T, **kw):
+    group = []
+    for r in range(P):
+        sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=P, **kw)
+        group.append(sv)
+        for reg in range(2 * p.mesh.dim):
+            sv.set_wall(reg, p.bcs[reg])
+        if I is not None:
+            sv.set_state(I[sv.cell0:sv.cell0 + sv.ncells], T[sv.cell0:sv.cell0 + sv.ncells])
+    return group
+
+
+@pytest.mark.parametrize("case,P", [("tri", 2), ("tri", 3), ("quad", 3), ("tet", 2), ("tet", 4)])
+def test_umesh_partition_group_bitexact(Solver, case, P):
+    """P contexts each owning a contiguous cell range plus halo copies of the
+    neighbours owned elsewhere (refreshed after every step) reproduce the
+    single-context run bit for bit; the random start draws the same state."""
+    p = _part_case(case)
+    I, T = oracle.Oracle(p).random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(5)
+        I1, T1 = sv.intensity(), sv.temperature()
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        sv.step(2)
+        Ir = sv.intensity()
+    group = _part_group(Solver, p, P, I, T)
+    try:
+        assert sum(s.ncells for s in group) == p.mesh.ncells
+        Solver.group_step(group, 2)
+        Solver.group_step(group, 3)
+        Ig = np.concatenate([s.intensity() for s in group])
+        Tg = np.concatenate([s.temperature() for s in group])
+        for s in group:
+            s.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        Solver.group_step(group, 2)
+        Igr = np.concatenate([s.intensity() for s in group])
+    finally:
+        for s in group:
+            s.close()
+    assert np.array_equal(Ig, I1) and np.array_equal(Tg, T1)
+    assert np.array_equal(Igr, Ir)
+
+
+def test_umesh_partition_semi_and_mutation(Solver, monkeypatch):
+    p = _semi_umesh = _part_case("tet")
+    p.dt = 8 * p.dt
+    p.semi = 1
+    I, T = oracle.Oracle(p).random_state()
+    Io, To, _, _ = oracle.Oracle(p).run(I, T, 4)
+    group = _part_group(Solver, p, 3, I, T, step_mode=1)
+    try:
+        Solver.group_step(group, 4)
+        Ig = np.concatenate([s.intensity() for s in group])
+        Tg = np.concatenate([s.temperature() for s in group])
+    finally:
+        for s in group:
+            s.close()
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")  # without the halo refresh the result must differ
+    group = _part_group(Solver, p, 3, I, T, step_mode=1)
+    try:
+        Solver.group_step(group, 4)
+        Ig2 = np.concatenate([s.intensity() for s in group])
+    finally:
+        for s in group:
+            s.close()
+    assert np.max(np.abs(Ig2 / Io - 1)) > 1e3 * REL_I
