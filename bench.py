@@ -443,13 +443,14 @@ def run_b200(args):
             "metric": "BTE DOF-updates/s (cell x dir x band / s), whole step",
             "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (band or args.config == 4) else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if (band or args.config in (4, 7, 8, 9)) else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
             "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb_total,
                        "dof_per_step": dof_global, "start": args.start, "dt": p.dt, "tau": args.tau,
                        "integrator": "semi-implicit" if args.semi > 0 else "explicit",
                        "simulated_s_per_s": p.dt * args.steps / (ms * 1e-3),
-                       "parallelism": (f"band{world}" if band else f"slab{world}") if world > 1 else "single",
+                       "parallelism": ((f"band{world}" if band else (f"cells{world}" if sv.umesh else f"slab{world}"))
+                                       if world > 1 else "single"),
                        "storage": "octant-slot rotation" if sv.rotate else "two buffers",
                        "l2": f"inputs > L2 ({state_gb:.2f} GB/buffer vs 126 MB), no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
