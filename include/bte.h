@@ -365,6 +365,26 @@ BTE_API bte_status bte_plan_slab(const bte_mesh *mesh, const bte_dirs *dirs, int
  * `nparts` owns the contiguous channels [*b0, *b1) of every cell,
  * b0 = floor(part*nb/nparts).  Host-only.  Errors: BTE_EINVAL unless
  * 1 <= nparts <= nb and 0 <= part < nparts. */
+/* Partition plan of an unstructured mesh (host only, no GPU; what
+ * bte_create_umesh builds for rank `rank` of `nranks`).  halo_cells (optional,
+ * capacity halo_cap) receives the canonical indices of the halo copies in
+ * halo order; send_cells (optional, capacity send_cap) the local indices of
+ * the owned cells each peer holds, concatenated in peer order (peer[k].send_off).
+ * Errors: BTE_EINVAL (mesh as bte_create_umesh, ranks, more than
+ * BTE_MAX_MSGS peers, capacities too small). */
+typedef struct {
+  int peer;
+  int64_t recv_off, recv_cnt; /* its cells in my halo: halo positions [off, off + cnt) */
+  int64_t send_off, send_cnt; /* my cells in its halo: send_cells[off, off + cnt)       */
+} bte_upeer;
+typedef struct {
+  int64_t cell0, n_own, n_halo;
+  int n_peers;
+  bte_upeer peer[BTE_MAX_MSGS];
+} bte_umesh_plan;
+BTE_API bte_status bte_plan_umesh(const bte_umesh *mesh, int nranks, int rank, bte_umesh_plan *out,
+                                  int64_t *halo_cells, int64_t halo_cap, int64_t *send_cells, int64_t send_cap);
+
 BTE_API bte_status bte_plan_band(int nb, int nparts, int part, int *b0, int *b1);
 
 /* Sizes of this rank's slab and the layout.  nb is the channel count this

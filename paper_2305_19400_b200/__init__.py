@@ -4,8 +4,8 @@ The product is ``libbte.so`` (C ABI in ``include/bte.h``; CUDA kernels for
 sm_100a in ``csrc/``).  ``bte.Solver`` is its thin ctypes binding.  There is
 no CPU path: without the built library or a CUDA device, ``Solver`` raises.
 """
-from .bte import (BC_DIFFUSE, BC_ISOTHERMAL, BC_SPECULAR, I0_BOSE_EINSTEIN, I0_LINEAR, LIB_PATH, BteError,
-                  Solver, load_library, nccl_unique_id, plan_band, plan_slab)
+from .bte import (BC_DIFFUSE, BC_ISOTHERMAL, BC_PARTIAL, BC_SPECULAR, I0_BOSE_EINSTEIN, I0_LINEAR, LIB_PATH,
+                  BteError, Solver, load_library, nccl_unique_id, plan_band, plan_slab, plan_umesh)
 
-__all__ = ["Solver", "BteError", "load_library", "nccl_unique_id", "plan_band", "plan_slab", "LIB_PATH", "BC_ISOTHERMAL", "BC_SPECULAR",
-           "BC_DIFFUSE", "I0_LINEAR", "I0_BOSE_EINSTEIN"]
+__all__ = ["Solver", "BteError", "load_library", "nccl_unique_id", "plan_band", "plan_slab", "plan_umesh", "LIB_PATH",
+           "BC_ISOTHERMAL", "BC_SPECULAR", "BC_DIFFUSE", "BC_PARTIAL", "I0_LINEAR", "I0_BOSE_EINSTEIN"]

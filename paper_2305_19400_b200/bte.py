@@ -23,7 +23,7 @@ STATUS = {0: "BTE_OK", 1: "BTE_EINVAL", 2: "BTE_ENOMEM", 3: "BTE_ECUDA", 4: "BTE
 BC_ISOTHERMAL, BC_SPECULAR, BC_DIFFUSE, BC_PARTIAL = 0, 1, 2, 3
 I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 
-EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
+EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_plan_umesh", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
            "bte_version")
@@ -43,6 +43,16 @@ class Mesh(C.Structure):
 class UMeshC(C.Structure):
     _fields_ = [("dim", C.c_int), ("nverts", C.c_int64), ("verts", C.c_void_p), ("ncells", C.c_int64),
                 ("cells", C.c_void_p), ("depth", C.c_double), ("nvc", C.c_int)]
+
+
+class UPeerC(C.Structure):
+    _fields_ = [("peer", C.c_int), ("recv_off", C.c_int64), ("recv_cnt", C.c_int64), ("send_off", C.c_int64),
+                ("send_cnt", C.c_int64)]
+
+
+class UPlanC(C.Structure):
+    _fields_ = [("cell0", C.c_int64), ("n_own", C.c_int64), ("n_halo", C.c_int64), ("n_peers", C.c_int),
+                ("peer", UPeerC * 32)]
 
 
 class Dirs(C.Structure):
@@ -113,6 +123,9 @@ def load_library(path: str = LIB_PATH):
         lib.bte_create_umesh.argtypes = [C.POINTER(UMeshC), C.POINTER(Dirs), C.POINTER(Bands), C.POINTER(Run),
                                          C.POINTER(C.c_void_p)]
         lib.bte_get_region_faces.argtypes = [P, C.c_int, C.POINTER(C.c_int64)]
+    if hasattr(lib, "bte_plan_umesh"):
+        lib.bte_plan_umesh.argtypes = [C.POINTER(UMeshC), C.c_int, C.c_int, C.POINTER(UPlanC), dp, C.c_int64, dp,
+                                       C.c_int64]
     if hasattr(lib, "bte_get_intensity_cells"):
         lib.bte_get_intensity_cells.argtypes = [P, dp, C.c_int64, dp]
     if hasattr(lib, "bte_set_tau_mode"):
@@ -412,3 +425,24 @@ def nccl_unique_id() -> bytes:
     if st != 0:
         raise RuntimeError(f"ncclGetUniqueId failed ({st})")
     return buf.raw
+
+
+def plan_umesh(mesh, nranks: int, rank: int) -> dict:
+    """bte_plan_umesh (host only): the cell partition libbte uses for an
+    unstructured mesh -- owned range, halo cells (canonical), per-peer lists."""
+    lib = load_library()
+    verts = np.ascontiguousarray(mesh.verts, dtype=np.float64)
+    cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
+    m = UMeshC(int(mesh.dim), verts.shape[0], _p(verts), cells.shape[0], _p(cells), float(mesh.depth),
+               int(cells.shape[1]))
+    out = UPlanC()
+    cap = int(cells.shape[0]) * int(cells.shape[1])
+    halo = np.empty(cap, dtype=np.int64)
+    send = np.empty(cap, dtype=np.int64)
+    st = lib.bte_plan_umesh(C.byref(m), int(nranks), int(rank), C.byref(out), _p(halo), cap, _p(send), cap)
+    if st != BTE_OK:
+        raise BteError(st, "bte_plan_umesh")
+    peers = [dict(peer=out.peer[k].peer, recv_off=out.peer[k].recv_off, recv_cnt=out.peer[k].recv_cnt,
+                  send=send[out.peer[k].send_off:out.peer[k].send_off + out.peer[k].send_cnt].copy())
+             for k in range(out.n_peers)]
+    return dict(cell0=out.cell0, n_own=out.n_own, n_halo=out.n_halo, halo=halo[:out.n_halo].copy(), peers=peers)

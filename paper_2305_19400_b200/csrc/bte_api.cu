@@ -323,6 +323,7 @@ struct UHost {
   std::vector<int64_t> rface[6];  // ... and global face index
   int64_t rn_global[6] = {0, 0, 0, 0, 0, 0};
   std::vector<UPeer> peers;
+  std::vector<int64_t> halo;  // canonical index of each halo copy
   double lo[3], L[3];
 };
 
@@ -360,6 +361,7 @@ static void partition_uhost(const UHost &G, int P, int rank, UHost *L) {
   L->nc_global = nc;
   L->c0 = c0;
   L->nhalo = (int64_t)halo.size();
+  L->halo = halo;
   for (int a = 0; a < 3; ++a) {
     L->lo[a] = G.lo[a];
     L->L[a] = G.L[a];
@@ -628,6 +630,38 @@ bte_status bte_set_tau_mode(bte_ctx *ctx, int mode) {
     bte_status st = refresh(ctx);
     if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return BTE_OK;
+}
+
+bte_status bte_plan_umesh(const bte_umesh *um, int nranks, int rank, bte_umesh_plan *out, int64_t *halo_cells,
+                          int64_t halo_cap, int64_t *send_cells, int64_t send_cap) {
+  if (!um || !out || !um->verts || !um->cells || nranks < 1 || rank < 0 || rank >= nranks || nranks > um->ncells)
+    return BTE_EINVAL;
+  if (um->dim != 2 && um->dim != 3) return BTE_EINVAL;
+  UHost G, L;
+  std::string err;
+  if (!build_uhost(um, &G, &err)) return BTE_EINVAL;
+  partition_uhost(G, nranks, rank, &L);
+  std::memset(out, 0, sizeof *out);
+  out->cell0 = L.c0;
+  out->n_own = L.nc;
+  out->n_halo = L.nhalo;
+  if ((int)L.peers.size() > BTE_MAX_MSGS) return BTE_EINVAL;
+  out->n_peers = (int)L.peers.size();
+  int64_t off = 0;
+  for (int k = 0; k < out->n_peers; ++k) {
+    const UPeer &pe = L.peers[k];
+    out->peer[k] = bte_upeer{pe.peer, pe.recv_off, pe.recv_cnt, off, (int64_t)pe.send_cells.size()};
+    if (send_cells) {
+      if (off + (int64_t)pe.send_cells.size() > send_cap) return BTE_EINVAL;
+      std::copy(pe.send_cells.begin(), pe.send_cells.end(), send_cells + off);
+    }
+    off += (int64_t)pe.send_cells.size();
+  }
+  if (halo_cells) {
+    if ((int64_t)L.halo.size() > halo_cap) return BTE_EINVAL;
+    std::copy(L.halo.begin(), L.halo.end(), halo_cells);
   }
   return BTE_OK;
 }
