@@ -960,3 +960,18 @@ def test_semi_groups_rotation_energy_errors(Solver, monkeypatch):
     with pytest.raises(BteError) as e:
         Solver(q.mesh, q.dirs, q.bands, q.dt, q.T_init, rank=0, nranks=2, decomp="band", step_mode=1)
     assert e.value.status == 1
+
+
+def test_sc_tau_rotation_bitexact(Solver, monkeypatch):
+    """Self-consistent tau under octant-slot rotation equals two buffers bit for bit."""
+    p = _group_case("3d")
+    p.tau_mode = 1
+    I, T = oracle.Oracle(p).random_state()
+    res = {}
+    for rot in ("0", "1"):
+        monkeypatch.setenv("BTE_ROTATE", rot)
+        with Solver.from_problem(p) as sv:
+            sv.set_state(I, T)
+            sv.step(4)
+            res[rot] = (sv.intensity(), sv.temperature())
+    assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][1], res["1"][1])
