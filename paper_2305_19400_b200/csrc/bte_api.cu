@@ -366,16 +366,13 @@ static void partition_uhost(const UHost &G, int P, int rank, UHost *L) {
     L->lo[a] = G.lo[a];
     L->L[a] = G.L[a];
   }
-  std::vector<int64_t> hpos(halo.size());
   auto local = [&](int64_t e) -> int64_t {
     if (e >= c0 && e < c1) return e - c0;
     // halo position: the halo is sorted by (owner, cell)
-    const int o = owner(e);
     auto it = std::lower_bound(halo.begin(), halo.end(), e, [&](int64_t a, int64_t b) {
       const int oa = owner(a), ob = owner(b);
       return oa != ob ? oa < ob : a < b;
     });
-    (void)o;
     return L->nc + (int64_t)(it - halo.begin());
   };
   L->nbr.resize(L->nc * K);
@@ -418,6 +415,10 @@ static void partition_uhost(const UHost &G, int P, int rank, UHost *L) {
 // unmatched faces classified onto the box walls (region order -x,+x,-y,+y,-z,+z).
 static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
   const int dim = um->dim, K = um->nvc > 0 ? um->nvc : dim + 1;
+  if (!((dim == 2 && (K == 3 || K == 4)) || (dim == 3 && K == 4))) {
+    *err = "vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4";
+    return false;
+  }
   const int64_t nc = um->ncells, nv = um->nverts;
   h->dim = dim;
   h->K = K;
@@ -444,7 +445,7 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
   std::vector<FaceKey> keys(nc * K);
   for (int64_t c = 0; c < nc; ++c) {
     const int64_t *cv = um->cells + c * K;
-    const double *X[4];
+    const double *X[4] = {nullptr, nullptr, nullptr, nullptr};
     for (int k = 0; k < K; ++k) {
       if (cv[k] < 0 || cv[k] >= nv) {
         *err = "cell " + std::to_string(c) + ": vertex index out of range";
