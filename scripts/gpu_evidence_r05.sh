@@ -13,7 +13,9 @@ timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_$
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench_${TAG}.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launches_bench_${TAG}.log 2>&1
 python scripts/ncu_summary.py launches gpurun_out/launches_bench_${TAG}.csv > gpurun_out/launches_bench_${TAG}.json
-for A in ${LINES:-"--config 3 --steps 30" "--config 4 --steps 6" "--config 6 --steps 200" "--config 7 --steps 40" "--config 8 --steps 10" "--config 9 --steps 40" "--config 2 --tau sc --steps 100" "--config 2 --semi 100 --steps 200"}; do
+LINES=("--config 3 --steps 30" "--config 4 --steps 6" "--config 6 --steps 200" "--config 7 --steps 40"
+       "--config 8 --steps 10" "--config 9 --steps 40" "--config 2 --tau sc --steps 100" "--config 2 --semi 100 --steps 200")
+for A in "${LINES[@]}"; do
   N=$(echo $A | tr -d ' -')
   timeout 600 python bench.py $A --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_$N.json 2> gpurun_out/bench_${TAG}_$N.err
 done
