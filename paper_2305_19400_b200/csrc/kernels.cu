@@ -1669,9 +1669,131 @@ __global__ void __launch_bounds__(256) k_newton_sc(const NewtonArgs a) {
   }
 }
 
+// Self-consistent tau on uniform band grids (reading R-k with the band
+// integrals of reading R-d): one warp per cell; iteration 0 uses the exact
+// F(T^n) = sum_b beta_b(T^n)/v_b D_b and F'(T^n) from the stored dI0/dT (no
+// integral, exact fixed point); later iterations evaluate every channel's
+// I0_b(T), dI0_b/dT with eval_channels.  Same bracket / step rules as
+// k_newton_sc.
+__global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const NewtonArgs a) {
+  extern __shared__ double nsh[];
+  const int nb = a.nb;
+  const int R = gl_stride(nb);
+  double *sA = nsh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ws0 = newton_scratch(a.m, nb);
+  double *scr = sA + R * kNGL + warp * (ws0 + nb);
+  double *sI0 = scr + nb + 2 * kNGL + a.m.imax + 1, *sD0 = sI0 + nb;
+  double *sDb = scr + ws0;
+  for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
+    const int b = i / kNGL, j = i - b * kNGL;
+    sA[j * R + b] = a.m.A[i];
+  }
+  __syncthreads();
+  const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
+  const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
+  for (int64_t qq = (int64_t)blockIdx.x * kNewtonWarps + warp; qq < nq; qq += nwarps) {
+    const int64_t pl = qq / ncol;
+    const int64_t c = a.col0 + (qq - pl * ncol) + pl * a.ncross;
+    const double Tn = a.T[c];
+    double F0 = 0.0, Fp0 = 0.0;
+    for (int b = lane; b < nb; b += 32) {
+      double q[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int sl = a.oct_slot[o];
+        q[o] = sl >= 0 ? __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b) : 0.0;
+      }
+      const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+      sDb[b] = D;
+      scr[b] = 0.0;  // eval_channels' weights (its weighted sums are not used here)
+      const double rv = a.m.rv[b];
+      F0 += beta_of_T(a.m.bcoef, b, Tn) * rv * D;
+      Fp0 += dbeta_of_T(a.m.bcoef, b, Tn) * rv * D + beta_of_T(a.m.bcoef, b, Tn) * rv * (a.W * a.dI0c[c * nb + b]);
+    }
+    F0 = warp_sum(F0);
+    Fp0 = warp_sum(Fp0);
+    __syncwarp();
+    double T = Tn, lo = kTlo, hi = kThi, Tf = Tn, evaluated_at = -1.0;
+    int status = ERR_NEWTON;
+    for (int it = 0; it <= kNewtonMaxIt; ++it) {
+      double F = F0, Fp = Fp0;
+      if (it > 0) {
+        double fw, fpw;
+        eval_channels(a, T, sA, scr, lane, &fw, &fpw);
+        evaluated_at = T;
+        double f = 0.0, fp = 0.0;
+        for (int b = lane; b < nb; b += 32) {
+          const double h = a.W * (sI0[b] - a.I0c[c * nb + b]) + sDb[b];
+          const double rv = a.m.rv[b];
+          const double be = beta_of_T(a.m.bcoef, b, T);
+          f += be * rv * h;
+          fp += dbeta_of_T(a.m.bcoef, b, T) * rv * h + be * rv * (a.W * sD0[b]);
+        }
+        F = warp_sum(f);
+        Fp = warp_sum(fp);
+      }
+      if (!isfinite(F) || !isfinite(Fp)) {
+        status = ERR_NONFINITE;
+        break;
+      }
+      if (F == 0.0) {
+        Tf = T;
+        status = ERR_NONE;
+        break;
+      }
+      if (it == kNewtonMaxIt) break;
+      if (F < 0.0)
+        lo = T;
+      else
+        hi = T;
+      const double stp = F / Fp;
+      double Tn1 = T - stp;
+      if (fabs(stp) <= kNewtonRtol * T) {
+        Tf = Tn1;
+        status = ERR_NONE;
+        break;
+      }
+      if (!(Tn1 > lo && Tn1 < hi) || !(Fp > 0.0)) Tn1 = 0.5 * (lo + hi);
+      T = Tn1;
+    }
+    if (status != ERR_NONE) {
+      if (lane == 0) {
+        const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+                                       (unsigned long long)(a.cell0_global + c);
+        atomicMin(a.err, key);
+      }
+      __syncwarp();
+      continue;
+    }
+    if (Tf != Tn) {
+      if (evaluated_at != Tf) {
+        double fw, fpw;
+        eval_channels(a, Tf, sA, scr, lane, &fw, &fpw);
+      }
+      if (lane == 0) a.T[c] = Tf;
+      for (int b = lane; b < nb; b += 32) {
+        a.I0c[c * nb + b] = sI0[b];
+        a.dI0c[c * nb + b] = sD0[b];
+        a.beta_next[c * nb + b] = beta_of_T(a.m.bcoef, b, Tf);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s) {
   if (a.nb > kMaxBands) return cudaErrorInvalidValue;
   if (a.ncells == 0) return cudaSuccess;
+  if (a.m.mode != 0 && a.m.uniform && !(getenv("BTE_SC_DIRECT") && atoi(getenv("BTE_SC_DIRECT")))) {
+    const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
+    const int64_t nblk = std::min<int64_t>(need, 148 * 4);
+    const size_t smem = ((size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * (newton_scratch(a.m, a.nb) + a.nb)) *
+                        sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton_scu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_newton_scu<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   const int64_t need = ((int64_t)a.ncols * a.nplanes + 7) / 8;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
   k_newton_sc<<<(unsigned)nblk, 256, 0, s>>>(a);

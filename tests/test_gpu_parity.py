@@ -975,3 +975,25 @@ def test_sc_tau_rotation_bitexact(Solver, monkeypatch):
             sv.step(4)
             res[rot] = (sv.intensity(), sv.temperature())
     assert np.array_equal(res["0"][0], res["1"][0]) and np.array_equal(res["0"][1], res["1"][1])
+
+
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_sc_tau_fixed_point_and_kernels(Solver, direct, monkeypatch):
+    """Self-consistent tau: a uniform equilibrium stays exactly fixed, and both
+    Newton kernels (uniform-grid band integrals / direct integrals) match the oracle."""
+    monkeypatch.setenv("BTE_SC_DIRECT", direct)
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 10, 20, 30, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+           bi.WallBC(1)]
+    p = bi.small_3d(8, 6, 5, bands=b, bcs=bcs)
+    p.tau_mode = 1
+    with Solver.from_problem(p) as sv:
+        I0, T0 = sv.intensity(), sv.temperature()
+        sv.step(20)
+        assert np.array_equal(sv.intensity(), I0) and np.array_equal(sv.temperature(), T0)
+    q = bi.config2(n=12)
+    q.mesh = bi.Mesh(2, 12, 12, 1, q.mesh.dx, q.mesh.dy, 1.0)
+    q.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, q.mesh.dx), 300.0)
+    q.tau_mode = 1
+    (rel, dT), _ = _run_both(Solver, q, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
