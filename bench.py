@@ -45,7 +45,7 @@ BYTES_PER_DOF = 16  # read I^n + write I^{n+1}, fp64
 
 
 def _problem(config: int, nranks: int):
-    if config not in (1, 2, 3, 4, 5, 6, 7, 8, 9):
+    if config not in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10):
         raise SystemExit(f"unsupported --config {config}")
     if config in (7, 8, 9) and nranks > 1:
         raise SystemExit("unstructured workloads (--config 7/8) run on one GPU")
@@ -55,6 +55,8 @@ def _problem(config: int, nranks: int):
         return bi.config_u3()
     if config == 9:  # config 7 on jittered quadrilaterals: 14,400 cells
         return bi.config_uq()
+    if config == 10:  # the paper's second example (Fig. 9): elongated, corner heat source
+        return bi.config_fig9()
     if config == 2:
         p = bi.config2()
         if nranks > 1:  # weak scaling: 120 rows per GPU along the slab axis

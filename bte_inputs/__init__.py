@@ -615,6 +615,26 @@ def config_demo(n: int = 120, ndirs: int = 20, n_freq: int = 40) -> Problem:
     return p
 
 
+def config_fig9(nx: int = 40, ny: int = 120, ndirs: int = 20, n_freq: int = 40) -> Problem:
+    """The paper's second example (Fig. 9): "a
+    smaller-scale, elongated material with a heat source in one corner ...
+    symmetry conditions on the left and right, and an isothermal boundary on
+    the bottom".  The figure is an image without sizes (reading R-m): 2-D,
+    nx x ny cells of 1 um (40 x 120 um), the demo's 20 in-plane directions and
+    55 channels, specular x-walls, 300 K on -y, and on +y a Gaussian source
+    centred on the left corner, T_wall(x) = 300 + 50 exp(-2 x^2 / w^2) with x
+    the face centre's distance from the corner and w = 10 um."""
+    d = 1e-6
+    mesh = Mesh(2, nx, ny, 1, d, d, 1.0)
+    x = (np.arange(nx) + 0.5) * d
+    top = 300.0 + 50.0 * np.exp(-2.0 * x * x / (10e-6 * 10e-6))
+    bcs = [WallBC(BC_SPECULAR), WallBC(BC_SPECULAR), WallBC(BC_ISOTHERMAL, None, 300.0),
+           WallBC(BC_ISOTHERMAL, top, 300.0), WallBC(BC_SPECULAR), WallBC(BC_SPECULAR)]
+    b = silicon_bands(n_freq)
+    return Problem(f"fig9_2d_si_{nx}x{ny}x{ndirs}x{b.nb}", mesh, directions_inplane(ndirs), b, dt=1e-12,
+                   T_init=300.0, bcs=bcs, nsteps=100, seed=SEED_BASE + 10)
+
+
 def config3(n: int = 64, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
     """3-D silicon box n^3, 1 um cells, z=0 isothermal 300 K, z=L 310 K, x/y specular."""
     d = 1e-6
@@ -705,4 +725,4 @@ def small_umesh(dim: int = 2, n=(4, 3, 2), dirs=None, bands=None, bcs=None, dt=1
                    bcs=bcs, nsteps=10, seed=seed)
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config_demo}
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config_demo, 10: config_fig9}

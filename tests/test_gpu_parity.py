@@ -997,3 +997,10 @@ def test_sc_tau_fixed_point_and_kernels(Solver, direct, monkeypatch):
     q.tau_mode = 1
     (rel, dT), _ = _run_both(Solver, q, 6)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_fig9_workload_full_size(Solver):
+    """The paper's second example (Fig. 9 shape, bench --config 10) at full size."""
+    p = bi.config_fig9()
+    (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, 5)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)

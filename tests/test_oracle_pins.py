@@ -922,3 +922,17 @@ def test_uquad_mesh_equals_structured_grid(dirs):
     Iu, Tu, _, _ = ou.run(I, T, 6)
     assert np.max(np.abs(Iu / Is - 1)) < 1e-12 and np.max(np.abs(Tu - Ts)) < 1e-9
     assert np.max(np.abs(Is / I - 1)) > 1e-4  # the run does move the state
+
+
+def test_fig9_corner_source_heats_its_corner():
+    """Fig. 9 shape (reading R-m, qualitative: the figure has no values): from a
+    300 K equilibrium the corner source heats the top-left corner first, the
+    far side stays colder, and nothing drops below the walls' 300 K."""
+    p = bi.config_fig9(nx=10, ny=30)
+    o = oracle.Oracle(p)
+    T0 = np.full(p.mesh.ncells, 300.0)
+    _, T, _, _ = o.run(o.equilibrium(T0), T0, 150)
+    F = T.reshape(30, 10)
+    assert np.unravel_index(np.argmax(F), F.shape) == (29, 0)
+    assert F[29, 0] > F[29, 9] > 300.0 and F[0, 0] < F[29, 0]
+    assert F.min() >= 300.0 - 1e-9
