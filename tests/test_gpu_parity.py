@@ -1004,3 +1004,25 @@ def test_fig9_workload_full_size(Solver):
     p = bi.config_fig9()
     (rel, dT), (Ig, Tg, Io, To) = _run_both(Solver, p, 5)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_demo_20000_steps_long_run(Solver):
+    """The paper's long demo run (20,000 steps = 20 ns at dt = 1 ps)
+    from the 300 K equilibrium: finite throughout, inside the walls'
+    temperature range (maximum principle of the positive explicit update),
+    mirror-symmetric about x = L/2 bit for bit after 20,000 steps, and still
+    heating (the first 100 steps are checked against the oracle in
+    test_demo_workload_full_size)."""
+    p = bi.config_demo()
+    n = p.mesh.nx
+    with Solver.from_problem(p) as sv:
+        sv.step(10000)
+        T1 = sv.temperature()
+        sv.step(10000)
+        T2 = sv.temperature()
+        E = sv.energy()
+    assert np.all(np.isfinite(T2)) and np.isfinite(E)
+    assert T2.min() >= 300.0 - 1e-9 and T2.max() <= 350.0 + 1e-9
+    F = T2.reshape(n, n)
+    assert np.array_equal(F, F[:, ::-1])
+    assert T2.mean() > T1.mean() > 300.0
