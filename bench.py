@@ -2,31 +2,35 @@
 """Benchmark of the B200 explicit phonon-BTE step (arXiv 2305.19400).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--config 2|3|5|6|1] [--start random|physical] [--decomp slab|band]
+                  [--config 4|3|5|2|6|10|1|7|8|9] [--start random|physical]
+                  [--decomp slab|band] [--repeats R]
 
-Prints ONE JSON line (rank 0).  Metric: DOF-updates/s (cell x direction x
-channel per second) of the whole step (boundary pass + fused sweep +
-reduction/Newton [+ halo]) -- BASELINE.json `metric`.
+Prints ONE JSON line (rank 0).  Metric (BASELINE.json): DOF-updates/s
+(cell x direction x channel per second) of the whole step -- boundary pass +
+fused sweep + reduction/Newton [+ halo exchange] -- and the flux sweep's
+fraction of the HBM roofline.
 
-Workload (N=1): BASELINE.json configs[1] -- 2-D non-gray silicon, 120x120
-cells, 400 directions, 40 channels, Gaussian hot spot + cold wall, specular
-sides, dt = 1e-12 s, synthetic seeded inputs (bte_inputs.config2).  Each
-intensity buffer is 1.84 GB >> 126 MB L2, so no L2 flush is needed between
-steps.  For N > 1 the mesh grows along y (120 rows per GPU, weak scaling) and
-is slab-decomposed with NCCL halo exchange; --decomp band instead keeps the
-BASELINE problem fixed and splits its channels over the N GPUs (the paper's
-band partition: one ncclAllGather of a scalar per cell per
-step, strong scaling).
+Default workload: BASELINE.json configs[3], the north_star case -- 3-D
+non-gray silicon, 100^3 = 10^6 cells, 400 directions, 40 channels, isothermal
+z walls + specular x/y walls, dt = 1e-12 s, seeded random start generated on
+the device (bte_init_random).  One GPU holds its 128 GB state only with
+octant-slot rotation (one 144 GB buffer); at N > 1 the same problem is
+slab-decomposed along z over N GPUs (strong scaling, NCCL halo exchange
+overlapped with the interior sweep).  --config 5 is the weak-scaling case
+(64^3 cells per GPU).  Each intensity buffer is >> 126 MB L2: no flush needed.
 
---impl reference times the CPU oracle (oracle/, plain fp64 C, all host cores)
-on a bounded sample of the same workload -- the paper has no runnable code,
-so the oracle is the reference arm.
+Timing: W untimed warm-up steps, then R repeats of K steps, each bracketed by
+a barrier + synchronize and timed with CUDA events on the library stream;
+max over ranks; value = global DOF x K / median repeat time.
+
+--impl reference times the CPU oracle (oracle/, plain fp64 C) on a bounded
+sample of the same workload -- the paper has no runnable code, so the oracle
+is the reference arm.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -42,39 +46,51 @@ if ROOT not in sys.path:
 import bte_inputs as bi  # noqa: E402
 
 BYTES_PER_DOF = 16  # read I^n + write I^{n+1}, fp64
+METRIC = "BTE DOF-updates/s (cell x dir x band / s), whole step"
+WEAK = (5,)  # configs whose per-GPU load is fixed as N grows
 
 
 def _problem(config: int, nranks: int):
-    if config not in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10):
-        raise SystemExit(f"unsupported --config {config}")
+    """The workload of --config at N ranks (the whole problem; the library
+    derives each rank's slab)."""
     if config in (7, 8, 9) and nranks > 1:
-        raise SystemExit("unstructured workloads (--config 7/8) run on one GPU")
-    if config == 7:  # unstructured analogue of config 2: 28,800 triangles
-        return bi.config_u2()
-    if config == 8:  # unstructured analogue of config 3: 196,608 tetrahedra
-        return bi.config_u3()
-    if config == 9:  # config 7 on jittered quadrilaterals: 14,400 cells
-        return bi.config_uq()
-    if config == 10:  # the paper's second example (Fig. 9): elongated, corner heat source
-        return bi.config_fig9()
-    if config == 2:
-        p = bi.config2()
-        if nranks > 1:  # weak scaling: 120 rows per GPU along the slab axis
-            n = p.mesh.nx
-            p.mesh = bi.Mesh(2, n, n * nranks, 1, p.mesh.dx, p.mesh.dy, 1.0)
-            p.name = f"config2_2d_si_{n}x{n * nranks}x400x40"
-        return p
-    if config == 3:
-        return bi.config3()
-    if config == 4:  # BASELINE configs[3]: 100^3 (10^6 cells), strong scaling over the slabs;
-        return bi.config4()  # one GPU holds it only with octant-slot rotation (144 GB)
-    if config == 5:
+        raise SystemExit("unstructured workloads (--config 7/8/9) are benchmarked on one GPU")
+    makers = {
+        1: bi.config1,        # BASELINE configs[0]: latency-bound, not roofline-gated
+        2: bi.config2,        # configs[1]: 2-D 120^2 (strong scaling over y slabs at N > 1)
+        3: bi.config3,        # configs[2]: 3-D 64^3
+        4: bi.config4,        # configs[3]: 10^6 cells, the north_star case (strong scaling)
+        6: bi.config_demo,    # the paper's own demo shape (SURVEY f2)
+        7: bi.config_u2,      # unstructured analogue of config 2 (SURVEY f3)
+        8: bi.config_u3,      # unstructured analogue of config 3
+        9: bi.config_uq,      # config 7 on jittered quadrilaterals
+        10: bi.config_fig9,   # the paper's second example (Fig. 9, reading R-m)
+    }
+    if config == 5:           # configs[4]: 64^3 per GPU (weak scaling)
         return bi.config5(nranks)
-    if config == 6:  # the paper's own demo shape, single GPU
-        return bi.config_demo()
-    if config == 1:  # BASELINE configs[0]: latency-bound, not roofline-gated
-        return bi.config1()
-    raise SystemExit(f"unsupported --config {config}")
+    if config not in makers:
+        raise SystemExit(f"unsupported --config {config}")
+    return makers[config]()
+
+
+def _parallelism(p, args, world):
+    if world == 1:
+        return "single"
+    if args.decomp == "band":
+        return f"band{world}"
+    return f"cells{world}" if hasattr(p.mesh, "cells") else f"slab{world}"
+
+
+def config_dict(p, args, world):
+    """The workload description both arms print (identical keys and values)."""
+    ncells = p.mesh.ncells
+    state_gb = ncells * p.dirs.nd * p.bands.nb * 8 / 1e9
+    return {"workload": p.name, "config": args.config, "cells": ncells, "directions": p.dirs.nd,
+            "channels": p.bands.nb, "dof_per_step": ncells * p.dirs.nd * p.bands.nb, "start": args.start,
+            "dt": p.dt * (args.semi if args.semi > 0 else 1.0), "tau": args.tau,
+            "integrator": "semi-implicit" if args.semi > 0 else "explicit",
+            "parallelism": _parallelism(p, args, world),
+            "l2": f"inputs > L2 ({state_gb / max(1, world):.2f} GB of I^n per GPU vs 126 MB), no flush"}
 
 
 def _peaks():
@@ -90,15 +106,47 @@ def _traffic_per_dof(workload: str):
     summary (dram__bytes_read.sum + dram__bytes_write.sum of one launch / its DOF)."""
     path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
     if not os.path.exists(path):
-        return None
+        return None, None
     try:
         d = json.load(open(path))
         e = d.get(workload)
         if e and e.get("dram_bytes_per_dof"):
-            return float(e["dram_bytes_per_dof"])
+            return float(e["dram_bytes_per_dof"]), e.get("source")
     except Exception:
-        return None
-    return None
+        return None, None
+    return None, None
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _physical_cores():
+    """Physical cores (sockets x cores per socket) from /proc/cpuinfo, else the logical count."""
+    try:
+        phys = set()
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" in line:
+                k, v = [x.strip() for x in line.split(":", 1)]
+                cur[k] = v
+            elif cur:
+                phys.add((cur.get("physical id"), cur.get("core id")))
+                cur = {}
+        if cur:
+            phys.add((cur.get("physical id"), cur.get("core id")))
+        n = len([x for x in phys if x[1] is not None])
+        if n > 0:
+            return n
+    except OSError:
+        pass
+    return os.cpu_count() or 1
 
 
 class ClockSampler:
@@ -134,8 +182,7 @@ class ClockSampler:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 except Exception:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
-                util = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
-                self.samples.append((time.time(), sm, r, util))
+                self.samples.append((time.time(), sm, r))
             except Exception:
                 pass
             time.sleep(0.005)
@@ -150,14 +197,15 @@ class ClockSampler:
             self._stop.set()
             self._t.join()
 
-    def summary(self, t0: float, t1: float):
+    def summary(self, spans):
         if not self._ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        inside = [s for s in self.samples if any(t0 <= s[0] <= t1 for t0, t1 in spans)]
         if not inside:
-            inside = sorted(self.samples, key=lambda s: abs(s[0] - 0.5 * (t0 + t1)))[:3]
+            mid = 0.5 * (spans[0][0] + spans[-1][1])
+            inside = sorted(self.samples, key=lambda s: abs(s[0] - mid))[:3]
         reasons = set()
-        for _, _, r, _ in inside:
+        for _, _, r in inside:
             for bit, name in self.REASONS.items():
                 if r & bit and name != "gpu_idle":
                     reasons.add(name)
@@ -165,81 +213,86 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(inside)}
 
 
-def _oracle_sample(p, target_s: float, max_steps: int = 1000):
-    """Time the oracle (as it stands) on a bounded y-slab sample of the workload:
-    returns (DOF-updates/s, description, threads)."""
+# ----------------------------------------------------------------- the oracle (CPU baseline / reference arm)
+
+def _slab_sample(p, nrows, nthreads):
+    """A z-slab (y-slab in 2-D) of the workload's random start: (problem, oracle, I, T)."""
     import oracle
     m = p.mesh
-    nthreads = os.cpu_count() or 1
-    rows = (m.ny if m.dim == 2 else m.nz) if not hasattr(m, "cells") else 0
-    # one-step probe on a thin slab to size the sample
-    def make(nrows):
-        if m.dim == 2:
-            box = ((0, m.nx), (m.ny - nrows, m.ny), (0, 1))
-        else:
-            box = ((0, m.nx), (0, m.ny), (m.nz - nrows, m.nz))
-        sp = bi.subproblem(p, box)
-        o = oracle.Oracle(sp, nthreads=nthreads)
-        T = bi.random_temperature(m, p.seed, p.T_init, 20.0, box=box)
-        I = o.equilibrium(T) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m, box=box)
-        return sp, o, I, T
-    if hasattr(m, "cells"):  # unstructured: a smaller mesh of the same generator
-        return _oracle_sample_umesh(p, target_s, max_steps, nthreads)
-    nr = max(1, min(rows, 4))
-    sp, o, I, T = make(nr)
-    t = time.perf_counter()
-    o.run(I, T, 1)
-    dt1 = time.perf_counter() - t
-    per_row = dt1 / nr
-    nr = int(max(1, min(rows, (target_s / 3) / max(per_row, 1e-9))))
-    sp, o, I, T = make(nr)
-    steps = 0
-    t = time.perf_counter()
-    while True:
-        I, T, _, _ = o.run(I, T, 1)[:4]
-        steps += 1
-        if time.perf_counter() - t >= target_s or steps >= max_steps:
-            break
-    el = time.perf_counter() - t
-    dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
-    desc = (f"oracle C fp64 (gcc -O2 -ffp-contract=off, OpenMP), {steps} step(s) of a "
-            f"{sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of {p.name} (random start), {el:.1f} s")
-    return dof * steps / el, desc, nthreads
+    if m.dim == 2:
+        box = ((0, m.nx), (m.ny - nrows, m.ny), (0, 1))
+    else:
+        box = ((0, m.nx), (0, m.ny), (m.nz - nrows, m.nz))
+    sp = bi.subproblem(p, box)
+    o = oracle.Oracle(sp, nthreads=nthreads)
+    T = bi.random_temperature(m, p.seed, p.T_init, 20.0, box=box)
+    I = o.equilibrium(T) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m, box=box)
+    return sp, o, I, T
 
 
-def _umesh_problem(p, n):
-    if p.mesh.dim == 3:
-        return bi.config_u3(n=n)
-    return bi.config_uq(n=n) if p.mesh.cells.shape[1] == 4 else bi.config_u2(n=n)
-
-
-def _oracle_sample_umesh(p, target_s, max_steps, nthreads):
+def _umesh_sample(p, n, nthreads):
     import oracle
-    n_full = 120 if p.mesh.dim == 2 else 32
-    sp = _umesh_problem(p, 4)
+    mk = bi.config_u3 if p.mesh.dim == 3 else (bi.config_uq if p.mesh.cells.shape[1] == 4 else bi.config_u2)
+    sp = mk(n=n)
     o = oracle.Oracle(sp, nthreads=nthreads)
     I, T = o.random_state()
+    return sp, o, I, T
+
+
+def _sized_sample(p, per_step_s, nthreads):
+    """A sample of the workload whose oracle step takes about per_step_s seconds
+    at nthreads: (problem, oracle, I, T, description of the sample)."""
+    m = p.mesh
+    if hasattr(m, "cells"):
+        n_full = 120 if m.dim == 2 else 32
+        sp, o, I, T = _umesh_sample(p, 4, nthreads)
+        t = time.perf_counter()
+        o.run(I, T, 1)
+        per_cell = (time.perf_counter() - t) / sp.mesh.ncells
+        per_unit = 2 if m.dim == 2 else 6
+        n = int(max(2, min(n_full, ((per_step_s / max(per_cell, 1e-12)) / per_unit) ** (1.0 / m.dim))))
+        sp, o, I, T = _umesh_sample(p, n, nthreads)
+        return sp, o, I, T, f"{sp.name} (the same generator at n = {n} instead of {n_full})"
+    rows = m.ny if m.dim == 2 else m.nz
+    # host memory bound: at most ~2e8 DOF (1.6 GB per state array) per sample
+    cap = max(1, int(2e8 // (m.ncells // rows * p.dirs.nd * p.bands.nb)))
+    sp, o, I, T = _slab_sample(p, 1, nthreads)
     t = time.perf_counter()
     o.run(I, T, 1)
-    per_cell = (time.perf_counter() - t) / sp.mesh.ncells
-    cells = (target_s / 3) / max(per_cell, 1e-12)
-    per_unit = 2 if p.mesh.dim == 2 else 6
-    n = int(max(2, min(n_full, (cells / per_unit) ** (1.0 / p.mesh.dim))))
-    sp = _umesh_problem(p, n)
-    o = oracle.Oracle(sp, nthreads=nthreads)
-    I, T = o.random_state()
+    per_row = time.perf_counter() - t
+    nr = int(max(1, min(rows, cap, per_step_s / max(per_row, 1e-9))))
+    if nr == 1:
+        return sp, o, I, T, f"a {sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of {p.name}"
+    sp, o, I, T = _slab_sample(p, nr, nthreads)
+    return sp, o, I, T, f"a {sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of {p.name}"
+
+
+def _oracle_rate(p, target_s, nthreads, max_steps=1000):
+    """DOF-updates/s of the oracle (as it stands) at nthreads on a bounded sample."""
+    sp, o, I, T, what = _sized_sample(p, target_s / 3, nthreads)
+    I0c, betac = o.refresh(T)
     steps = 0
     t = time.perf_counter()
     while True:
-        I, T, _, _ = o.run(I, T, 1)[:4]
+        I, T, I0c, betac = o.run(I, T, 1, I0c, betac)
         steps += 1
         if time.perf_counter() - t >= target_s or steps >= max_steps:
             break
     el = time.perf_counter() - t
     dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
-    desc = (f"oracle C fp64 (gcc -O2 -ffp-contract=off, OpenMP), {steps} step(s) of {sp.name} "
-            f"(the same generator at n = {n} instead of {n_full}, random start), {el:.1f} s")
-    return dof * steps / el, desc, nthreads
+    return dof * steps / el, f"{steps} oracle step(s) of {what}, random start, {el:.1f} s"
+
+
+def cpu_baseline(p, seconds):
+    """The oracle (plain fp64 C, gcc -O2 -ffp-contract=off, OpenMP over cells)
+    on the host cores: all logical cores and one thread."""
+    nall = os.cpu_count() or 1
+    v_all, s_all = _oracle_rate(p, seconds, nall)
+    v_one, s_one = _oracle_rate(p, seconds, 1)
+    return {"value": v_all, "unit": "DOF-updates/s", "cores": nall, "kind": "oracle",
+            "sample": s_all, "cpu_model": _cpu_model(), "physical_cores": _physical_cores(),
+            "single_thread": {"value": v_one, "cores": 1, "sample": s_one},
+            "build": "gcc -O2 -ffp-contract=off -fopenmp (no fast-math)"}
 
 
 def run_reference(args):
@@ -248,46 +301,12 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import oracle
-    p = _problem(args.config, 1)
-    m = p.mesh
+    p = _problem(args.config, world if args.config in WEAK else 1)
     nthreads = os.cpu_count() or 1
-    # each step = a bounded y-slab sample sized to ~target seconds per step so the
-    # whole --warmup W --steps K run stays within a few minutes
-    budget = 150.0
-    per_step = budget / max(1, args.steps + args.warmup)
-    rows_total = (m.ny if m.dim == 2 else m.nz) if not hasattr(m, "cells") else 0
-
-    def make(nrows):
-        if m.dim == 2:
-            box = ((0, m.nx), (m.ny - nrows, m.ny), (0, 1))
-        else:
-            box = ((0, m.nx), (0, m.ny), (m.nz - nrows, m.nz))
-        sp = bi.subproblem(p, box)
-        o = oracle.Oracle(sp, nthreads=nthreads)
-        T = bi.random_temperature(m, p.seed, p.T_init, 20.0, box=box)
-        I = o.equilibrium(T) * bi.intensity_noise_factor(p.seed, 0, p.dirs.nd, p.bands.nb, 0.05, mesh=m, box=box)
-        return sp, o, I, T
-
-    if hasattr(m, "cells"):  # unstructured: each step on a smaller mesh of the same generator
-        sp = _umesh_problem(p, 4)
-        o = oracle.Oracle(sp, nthreads=nthreads)
-        I, T = o.random_state()
-        t = time.perf_counter()
-        o.run(I, T, 1)
-        per_cell = (time.perf_counter() - t) / sp.mesh.ncells
-        per_unit = 2 if m.dim == 2 else 6
-        n = int(max(2, ((per_step / max(per_cell, 1e-12)) / per_unit) ** (1.0 / m.dim)))
-        sp = _umesh_problem(p, n)
-        o = oracle.Oracle(sp, nthreads=nthreads)
-        I, T = o.random_state()
-    else:
-        sp, o, I, T = make(1)
-        t = time.perf_counter()
-        o.run(I, T, 1)
-        per_row = time.perf_counter() - t
-        nr = int(max(1, min(rows_total, per_step / max(per_row, 1e-9))))
-        sp, o, I, T = make(nr)
+    # each step = one oracle step of a bounded sample sized so the whole
+    # --warmup W --steps K run stays within a few minutes
+    per_step = 150.0 / max(1, args.steps + args.warmup)
+    sp, o, I, T, what = _sized_sample(p, per_step, nthreads)
     I0c, betac = o.refresh(T)
     for _ in range(args.warmup):
         I, T, I0c, betac = o.run(I, T, 1, I0c, betac)
@@ -297,23 +316,21 @@ def run_reference(args):
     el = time.perf_counter() - t
     dof = sp.mesh.ncells * p.dirs.nd * p.bands.nb
     value = dof * args.steps / el
-    if hasattr(m, "cells"):
-        sample = f"each step = one oracle step of {sp.name} (same generator, smaller mesh; random start)"
-    else:
-        sample = (f"each step = one oracle step of a {sp.mesh.nx}x{sp.mesh.ny}x{sp.mesh.nz}-cell slab of "
-                  f"{p.name} (random start)")
+    sample = f"each step = one oracle step of {what} (random start)"
     line = {
-        "impl": "reference", "metric": "BTE DOF-updates/s (cell x dir x band / s), whole step",
-        "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, bte_inputs)",
-        "config": {"workload": p.name, "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.config in WEAK else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
+        "config": config_dict(p, args, world),
         "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": nthreads, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": _cpu_model(), "physical_cores": _physical_cores()},
         "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
+
+# ----------------------------------------------------------------- the B200 arm
 
 def run_b200(args):
     import torch
@@ -327,11 +344,13 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py (b200 arm) needs a CUDA device: there is no CPU path")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     band = args.decomp == "band"
-    p = _problem(args.config, 1 if band else world)
+    p = _problem(args.config, world if args.config in WEAK else 1)
     if args.semi > 0:
         p.dt = args.semi * p.dt
         p.semi = 1
@@ -348,116 +367,130 @@ def run_b200(args):
     dof_local = sv.ncells * sv.nd * sv.nb
     dof_global = sv.ncells_global * sv.nd * sv.nb_total
 
-    def init_state():
-        if args.start == "random":
-            sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
-        else:
-            sv.set_state(None, np.full(sv.ncells, p.T_init))
-
     def barrier():
         torch.cuda.synchronize(local)
         if world > 1:
             dist.barrier()
 
-    init_state()
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if args.start == "random":
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+    else:
+        sv.set_state(None, np.full(sv.ncells, p.T_init))
     sv.step(args.warmup)
+
     clocks = ClockSampler(local)
     clocks.start()
-    sv.timing_enable(True, args.steps)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    t0 = time.time()
-    ev0.record(stream)
-    sv.step(args.steps)
-    ev1.record(stream)
-    barrier()
-    t1 = time.time()
+    sv.timing_enable(True, args.steps * args.repeats)
+    reps, spans = [], []
+    for _ in range(args.repeats):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        t0 = time.time()
+        ev0.record(stream)
+        sv.step(args.steps)
+        ev1.record(stream)
+        barrier()
+        spans.append((t0, time.time()))
+        reps.append(max_over_ranks(ev0.elapsed_time(ev1)))
     clocks.stop()
-    ms = ev0.elapsed_time(ev1)
     tim = sv.timing_read()
     sv.timing_enable(False)
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = statistics.median(reps)
     value = dof_global * args.steps / (ms * 1e-3)
+    nsteps_t = max(1, tim["steps"])
 
-    # roofline of the dominant kernel (the fused sweep): algorithmic 16 B/DOF;
-    # one step launches the sweep once per column chunk
+    # roofline of the dominant kernel (the fused a1+a2 sweep): algorithmic
+    # 16 B/DOF x the DOF one launch processes / its mean CUDA-event duration
     peak, peak_src = _peaks()
-    launches_per_step = max(1, tim["sweep_launches"] // max(1, tim["steps"]))
+    launches_per_step = max(1, tim["sweep_launches"] // nsteps_t)
     sweep_ms = tim["sweep_ms"] / max(1, tim["sweep_launches"])
     dof_per_launch = dof_local / launches_per_step
     achieved = BYTES_PER_DOF * dof_per_launch / (sweep_ms * 1e-3) / 1e9
-    tpd = _traffic_per_dof(p.name)
+    tpd, tsrc = _traffic_per_dof(p.name)
+    per_step = {"sweep": tim["sweep_ms"] / nsteps_t, "newton": tim["newton_ms"] / nsteps_t,
+                "boundary": tim["boundary_ms"] / nsteps_t, "halo": tim["halo_ms"] / nsteps_t}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None if tpd is None else tpd * dof_per_launch,
-                "kernel": ("k_usweep (a1+a2 face-list upwind flux + relaxation on simplices + octant partial sums)"
-                           if sv.umesh else ("k_sweep_tma" if sv.nj * sv.nb >= 384 else "k_sweep")
-                           + " (a1+a2 fused upwind flux + relaxation + octant partial sums"
-                           + (", a3+a4 Newton fused in the tail)" if tim["newton_launches"] == 0 else ")")),
+                "traffic_source": tsrc, "kernel": sv.sweep_kernel,
                 "bytes_per_launch_algorithmic": BYTES_PER_DOF * dof_per_launch, "kernel_ms_avg": sweep_ms,
                 "launches_per_step": launches_per_step, "peak_source": peak_src,
-                "device_ms_per_step": {"sweep": tim["sweep_ms"] / args.steps, "newton": tim["newton_ms"] / args.steps,
-                                       "boundary": tim["boundary_ms"] / args.steps,
-                                       "halo": tim["halo_ms"] / args.steps},
+                "device_ms_per_step": per_step, "timing_truncated": bool(tim.get("truncated", 0)),
                 "note": ("octant-slot rotation: one sweep launch per octant, each into the spare region"
-                         if sv.rotate else "sweep and Newton serialised on one stream" if launches_per_step == 1
-                         else "Newton of chunk k on a second stream, overlapped with other chunks' sweeps")}
+                         if sv.rotate else "boundary planes first, exchange overlapped with the interior sweep"
+                         if world > 1 and not band else "sweep and Newton serialised on one stream")}
 
-    # e2e through the public API with host buffers (pinned), copies inside the
-    # timed region: the job's input state (I, T) goes host->device, K steps run,
-    # and the job's result -- the temperature field, "ultimately the quantity of
-    # interest" -- comes back device->host.
+    per_rank = None
+    if world > 1:  # per-rank breakdown: compute kernels, halo, the exposed (non-overlapped) remainder
+        mine = dict(rank=rank, step_ms=ms / args.steps, **{k + "_ms": v for k, v in per_step.items()})
+        mine["exposed_ms"] = max(0.0, mine["step_ms"] - mine["sweep_ms"] - mine["newton_ms"] - mine["boundary_ms"])
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        per_rank = gathered
+
+    # e2e through the public API with pinned host buffers, copies inside the
+    # timed region.  States up to 16 GB per GPU: the job's whole input state
+    # (I, T) goes host->device, K steps run, the temperature field -- "the
+    # quantity of interest" -- comes back.  Larger states (configs
+    # 3/4/5): the job's input is the initial temperature field (the paper's
+    # initial condition is equilibrium at T): bte_set_state(NULL,
+    # T) builds I = I0(T) on the device from the host T.
     e2e = None
     state_gb = sv.ncells * sv.nd * sv.nb * 8 / 1e9
-    if state_gb > 16:  # config 4: a 128 GB pinned host copy of the state would exhaust the host
-        e2e = {"value": None, "unit": "DOF-updates/s", "skipped": f"state {state_gb:.0f} GB per GPU > 16 GB host staging cap"}
-    elif not args.no_e2e:
-        I_h = torch.empty((sv.ncells, sv.nd, sv.nb), dtype=torch.float64, pin_memory=True).numpy()
+    if not args.no_e2e:
         T_h = torch.empty((sv.ncells,), dtype=torch.float64, pin_memory=True).numpy()
-        sv.intensity(I_h)
-        sv.temperature(T_h)
+        full = state_gb <= 16 and not band
+        if full:
+            I_h = torch.empty((sv.ncells, sv.nd, sv.nb), dtype=torch.float64, pin_memory=True).numpy()
+            sv.intensity(I_h)
+            sv.temperature(T_h)
+        else:
+            I_h = None
+            m = p.mesh
+            Tg = bi.random_temperature(m, p.seed, p.T_init, 20.0)
+            c0 = sv.cell0
+            T_h[:] = Tg[c0:c0 + sv.ncells]
         barrier()
         t = time.perf_counter()
         sv.set_state(I_h, T_h)
         sv.step(args.steps)
         sv.temperature(T_h)
         barrier()
-        el = time.perf_counter() - t
-        if world > 1:
-            tt = torch.tensor([el], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            el = float(tt.item())
+        el = max_over_ranks(time.perf_counter() - t)
         e2e = {"value": dof_global * args.steps / el, "unit": "DOF-updates/s",
-               "h2d_bytes_per_step": (I_h.nbytes + T_h.nbytes) / args.steps,
+               "h2d_bytes_per_step": ((I_h.nbytes if full else 0) + T_h.nbytes) / args.steps,
                "d2h_bytes_per_step": T_h.nbytes / args.steps,
-               "what": "bte_set_state(pinned host I, T) + bte_step(K) + bte_get_temperature (pinned host T)"}
+               "what": ("bte_set_state(pinned host I, T) + bte_step(K) + bte_get_temperature (pinned host T)"
+                        if full else
+                        "bte_set_state(NULL, pinned host T: I = I0(T) built on the device) + bte_step(K) + "
+                        "bte_get_temperature (pinned host T)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, cores = _oracle_sample(p, target_s=args.cpu_seconds)
-        cpu = {"value": v, "unit": "DOF-updates/s", "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = cpu_baseline(p, args.cpu_seconds)
 
     if rank == 0:
         line = {
-            "metric": "BTE DOF-updates/s (cell x dir x band / s), whole step",
-            "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (band or args.config in (4, 7, 8, 9)) else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.config in WEAK else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
-            "config": {"workload": p.name, "cells": sv.ncells_global, "directions": sv.nd, "channels": sv.nb_total,
-                       "dof_per_step": dof_global, "start": args.start, "dt": p.dt, "tau": args.tau,
-                       "integrator": "semi-implicit" if args.semi > 0 else "explicit",
-                       "simulated_s_per_s": p.dt * args.steps / (ms * 1e-3),
-                       "parallelism": ((f"band{world}" if band else (f"cells{world}" if sv.umesh else f"slab{world}"))
-                                       if world > 1 else "single"),
-                       "storage": "octant-slot rotation" if sv.rotate else "two buffers",
-                       "l2": f"inputs > L2 ({state_gb:.2f} GB/buffer vs 126 MB), no flush"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(tim["launches"]),
-            "clocks": clocks.summary(t0, t1),
+            "config": config_dict(p, args, world),
+            "repeats_ms_per_step": [r / args.steps for r in reps],
+            "timing": f"median of {args.repeats} repeats of {args.steps} steps, CUDA events, max over ranks",
+            "layout": "octant-slot rotation (one buffer of nslot + 1 regions)" if sv.rotate else "two buffers",
+            "simulated_s_per_s": p.dt * args.steps / (ms * 1e-3),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "per_rank": per_rank,
+            "gpu_launches": int(tim["launches"] // max(1, args.repeats)),
+            "gpu_launches_note": "library kernel launches inside one timed region of K steps",
+            "clocks": clocks.summary(spans),
         }
         print(json.dumps(line))
     sv.close()
@@ -468,14 +501,15 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--repeats", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--start", default="random", choices=["random", "physical"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--decomp", default="slab", choices=["slab", "band"])
     ap.add_argument("--semi", type=float, default=0.0,
                     help="semi-implicit step (reading R-l) at this multiple of the workload's dt (0: explicit)")
@@ -484,6 +518,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.repeats < 1 or args.steps < 1:
+        raise SystemExit("--repeats and --steps must be >= 1")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -421,6 +421,16 @@ def intensity_noise_factor(seed: int, ncells: int, nd: int, nb: int, amp: float 
     return (1.0 + amp * (2.0 * u - 1.0)).reshape(cg.size, nd, nb)
 
 
+def intensity_noise_factor_cells(seed: int, cells, nd: int, nb: int, amp: float = 0.05) -> np.ndarray:
+    """intensity_noise_factor for an explicit list of GLOBAL canonical cells
+    (e.g. a sub-mesh of an unstructured mesh), in list order."""
+    cg = np.asarray(cells, dtype=np.uint64)
+    idx = (cg[:, None] * np.uint64(nd * nb) + np.arange(nd * nb, dtype=np.uint64)[None, :]).reshape(-1)
+    z = splitmix64(np.uint64(seed & MASK64) ^ idx)
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (1.0 + amp * (2.0 * u - 1.0)).reshape(cg.size, nd, nb)
+
+
 # --------------------------------------------------------------------------
 # unstructured simplex meshes (SURVEY 8(f) f3): a lattice of squares / cubes,
 # each split into 2 triangles / 6 tetrahedra, with seeded vertex jitter.  A
@@ -508,6 +518,31 @@ def umesh_tet(nx: int, ny: int, nz: int, h: float = 1e-6, jitter: float = 0.1, s
     return UMesh(3, V, np.ascontiguousarray(C), 1.0)
 
 
+def umesh_tet_subbox(m: UMesh, n, box):
+    """The cubes [x0,x1) x [y0,y1) x [z0,z1) of a umesh_tet(n[0], n[1], n[2])
+    mesh (unshuffled, cube-major order) as a mesh of its own: returns (sub mesh,
+    global cell ids in sub order).  Vertices on a cut plane of the box are
+    moved onto the plane (their jitter along that axis dropped), so the sub
+    mesh's walls are planar; only the tetrahedra of the box's outer cube layer
+    change geometry (a sample k+1 cubes inside the cut is exact for k steps)."""
+    nx, ny, nz = n
+    (x0, x1), (y0, y1), (z0, z1) = box
+    cubes = [i + nx * (j + ny * k) for k in range(z0, z1) for j in range(y0, y1) for i in range(x0, x1)]
+    gcells = np.array([6 * c + t for c in cubes for t in range(6)], dtype=np.int64)
+    C = m.cells[gcells]
+    used, inv = np.unique(C.reshape(-1), return_inverse=True)
+    V = m.verts[used].copy()
+    vi = used % (nx + 1)
+    vj = (used // (nx + 1)) % (ny + 1)
+    vk = used // ((nx + 1) * (ny + 1))
+    h = (m.verts[:, 0].max() - m.verts[:, 0].min()) / nx
+    for a, (idx, lo, hi) in enumerate(((vi, x0, x1), (vj, y0, y1), (vk, z0, z1))):
+        on = (idx == lo) | (idx == hi)
+        V[on, a] = idx[on] * h
+    sub = UMesh(3, V, np.ascontiguousarray(inv.reshape(C.shape).astype(np.int64)), m.depth)
+    return sub, gcells
+
+
 def umesh_centroids(m: UMesh) -> np.ndarray:
     """Cell centroids: vertex coordinates summed in local vertex order, / (dim+1)."""
     X = m.verts[m.cells]  # [nc, m, 3]
@@ -517,14 +552,15 @@ def umesh_centroids(m: UMesh) -> np.ndarray:
     return acc / X.shape[1]
 
 
-def random_temperature_umesh(m: UMesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0) -> np.ndarray:
+def random_temperature_umesh(m: UMesh, seed: int, T_mean: float = 300.0, T_amp: float = 20.0,
+                             lo=None, L=None) -> np.ndarray:
     """Random start on an unstructured mesh: the structured recipe with the cell
     centre replaced by the centroid, measured from the box corner, and L the
-    box extent."""
+    box extent (a sub-mesh passes the whole mesh's corner and extent)."""
     p1, p2, p3 = random_phases(seed)
     cen = umesh_centroids(m)
-    lo = m.verts.min(axis=0)
-    L = m.verts.max(axis=0) - lo
+    lo = m.verts.min(axis=0) if lo is None else np.asarray(lo, dtype=np.float64)
+    L = (m.verts.max(axis=0) - lo) if L is None else np.asarray(L, dtype=np.float64)
     fx = np.sin(2.0 * math.pi * ((cen[:, 0] - lo[0]) / L[0] + p1))
     fy = np.sin(2.0 * math.pi * ((cen[:, 1] - lo[1]) / L[1] + p2))
     fz = np.sin(2.0 * math.pi * ((cen[:, 2] - lo[2]) / L[2] + p3)) if m.dim == 3 else np.ones(m.ncells)

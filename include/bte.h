@@ -306,9 +306,22 @@ BTE_API bte_status bte_get_intensity(bte_ctx *ctx, double *out, size_t count);
 BTE_API bte_status bte_get_intensity_cells(bte_ctx *ctx, const int64_t *cells, int64_t n, double *out);
 BTE_API bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count);
 
-/* Diagnostic total energy of this rank's slab, E = sum_c V sum_b (1/v_b)
- * sum_d w_d I_{c,d,b}.  Not on the hot path. */
+/* Diagnostic total energy E = sum_c V_c sum_b (1/v_b) sum_d w_d I_{c,d,b}
+ * (SURVEY 8(b) "allreduced").  With an NCCL communicator
+ * (nranks > 1, nccl_id given) E is the whole problem's: every rank sums its
+ * own cells (or, for band contexts, its own channels), the per-rank sums are
+ * all-gathered and added in rank order, so all ranks return the same bits.
+ * Collective: every rank must call it.  Without a communicator (one context,
+ * or an in-process local group) E covers this context only.  Not on the hot
+ * path.  Errors: BTE_EINVAL, BTE_ENOMEM, BTE_ECUDA, BTE_ENCCL. */
 BTE_API bte_status bte_get_energy(bte_ctx *ctx, double *E);
+
+/* Debug switches for the mutation tests ("skipping the exchange must
+ * break it").  BTE_DEBUG_SKIP_EXCHANGE: value 1 makes the halo / band-partial
+ * exchange of this context's group a no-op (checked on the group's first
+ * context).  Never set on a production run.  Errors: BTE_EINVAL (unknown what). */
+#define BTE_DEBUG_SKIP_EXCHANGE 1
+BTE_API bte_status bte_set_debug(bte_ctx *ctx, int what, int value);
 
 /* Sub-step access for kernel unit tests (state unchanged):
  *   which = 0: I after one boundary pass + sweep from the current state, [cell][d][b]
@@ -328,6 +341,8 @@ typedef struct {
   int64_t sweep_launches;
   int64_t newton_launches;
   int64_t boundary_launches;
+  int64_t truncated;       /* 1: the event pool (max_steps of bte_timing_enable) ran out; the
+                              *_ms sums then miss launches the *_launches counts include */
 } bte_timing;
 BTE_API bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps);
 BTE_API bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out);
@@ -397,6 +412,7 @@ typedef struct {
   int b0, b1, nb_total, band;                        /* channel band; band = 1 for bte_create_band */
   int rotate;                                        /* 1: octant-slot rotation (see bte_create)  */
   int64_t cell0;                                     /* canonical index of the first owned cell   */
+  const char *sweep_kernel;                          /* the a1+a2 kernel bte_step launches (static) */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

@@ -26,7 +26,8 @@ I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_plan_umesh", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
-           "bte_version")
+           "bte_version", "bte_set_debug")
+DEBUG_SKIP_EXCHANGE = 1
 
 
 class BteError(RuntimeError):
@@ -81,7 +82,7 @@ class Timing(C.Structure):
     _fields_ = [("steps", C.c_int64), ("launches", C.c_int64), ("sweep_ms", C.c_double),
                 ("newton_ms", C.c_double), ("boundary_ms", C.c_double), ("halo_ms", C.c_double),
                 ("sweep_launches", C.c_int64), ("newton_launches", C.c_int64),
-                ("boundary_launches", C.c_int64)]
+                ("boundary_launches", C.c_int64), ("truncated", C.c_int64)]
 
 
 class Msg(C.Structure):
@@ -98,7 +99,8 @@ class Info(C.Structure):
     _fields_ = [("ncells_local", C.c_int64), ("ncells_global", C.c_int64), ("z0", C.c_int64),
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
                 ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
-                ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int), ("cell0", C.c_int64)]
+                ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int), ("cell0", C.c_int64),
+                ("sweep_kernel", C.c_char_p)]
 
 
 _lib = None
@@ -143,6 +145,7 @@ def load_library(path: str = LIB_PATH):
     lib.bte_get_temperature.argtypes = [P, dp, C.c_size_t]
     lib.bte_get_energy.argtypes = [P, C.POINTER(C.c_double)]
     lib.bte_debug_substep.argtypes = [P, C.c_int, dp, C.c_size_t]
+    lib.bte_set_debug.argtypes = [P, C.c_int, C.c_int]
     lib.bte_timing_enable.argtypes = [P, C.c_int, C.c_int64]
     lib.bte_timing_read.argtypes = [P, C.POINTER(Timing)]
     lib.bte_get_info.argtypes = [P, C.POINTER(Info)]
@@ -255,6 +258,7 @@ class Solver:
         self.band = bool(info.band)
         self.rotate = bool(info.rotate)
         self.cell0 = int(info.cell0)
+        self.sweep_kernel = (info.sweep_kernel or b"").decode()
         if self.nb_total == 0:  # older A/B build without the band fields
             self.b0, self.b1, self.nb_total = 0, self.nb, self.nb
 
@@ -286,6 +290,8 @@ class Solver:
             self._check(self._lib.bte_set_bc_partial(self._h, int(region), float(specularity)))
             return
         Tw = _f64(T_wall)
+        if Tw is not None and Tw.size != self.region_faces(region):
+            raise ValueError(f"T_wall has {Tw.size} values, region {region} has {self.region_faces(region)} faces")
         self._check(self._lib.bte_set_bc(self._h, int(region), int(kind), _p(Tw), float(T_uniform)))
 
     def set_step_mode(self, mode: int) -> None:
@@ -341,17 +347,29 @@ class Solver:
             msgs = "; ".join(sv._err() for sv in solvers if sv._err())
             raise BteError(st, msgs)
 
-    def intensity(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+    @staticmethod
+    def _out(out: Optional[np.ndarray], shape) -> np.ndarray:
+        """Caller buffers must be C-contiguous float64 of the exact size (the
+        library writes 8*size bytes into them)."""
         if out is None:
-            out = np.empty((self.ncells, self.nd, self.nb))
+            return np.empty(shape)
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != int(np.prod(shape)):
+            raise ValueError(f"out must be a C-contiguous float64 array of {int(np.prod(shape))} elements")
+        return out
+
+    def intensity(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = self._out(out, (self.ncells, self.nd, self.nb))
         self._check(self._lib.bte_get_intensity(self._h, out.ctypes.data, out.size))
         return out
 
     def temperature(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        if out is None:
-            out = np.empty(self.ncells)
+        out = self._out(out, (self.ncells,))
         self._check(self._lib.bte_get_temperature(self._h, out.ctypes.data, out.size))
         return out
+
+    def set_debug(self, what: int, value: int) -> None:
+        """Mutation-test switches (bte_set_debug); never on a production run."""
+        self._check(self._lib.bte_set_debug(self._h, int(what), int(value)))
 
     def energy(self) -> float:
         e = C.c_double()

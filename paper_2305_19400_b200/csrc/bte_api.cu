@@ -3,6 +3,7 @@
 // precompute (a0), device state, step orchestration, error latching.
 // Every step of the hot path runs in kernels.cu; this file only launches.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -16,6 +17,12 @@
 #include "../../include/bte.h"
 #include "bte_internal.cuh"
 #include "nccl_shim.h"
+
+// NVTX phase ranges of a step (a1 boundary / a2 sweep / a3+a4 Newton / a5
+// halo), mirroring the paper's intensity / temperature / communication
+// breakdown.  No-ops unless a tool attaches.
+static inline void nvtx_push(const char *name) { nvtxRangePushA(name); }
+static inline void nvtx_pop() { nvtxRangePop(); }
 
 using namespace bte;
 
@@ -85,13 +92,15 @@ struct bte_ctx {
   double *gtab[6] = {nullptr};
   int *d_dmap = nullptr, *d_canon_d = nullptr;
   unsigned long long *d_err = nullptr;
-  int *d_done = nullptr;  // fused-Newton tickets [nseg][ncross]
   int newton_predict = 1;  // env BTE_NEWTON_PREDICT=0 disables (reading R-f)
   int newton_minb = 0;     // env BTE_NEWTON_MINB (k_newton occupancy variant)
-  int tx_override = 0;     // env BTE_TX (columns per CTA of the small-block sweep)
   unsigned long long *d_stats = nullptr;  // env BTE_NEWTON_STATS=1: Newton counters printed by bte_step
   int l2hint = 0;          // env BTE_L2HINT
-  int fuse_newton = 0;    // env BTE_FUSE=1 enables the sweep-tail Newton (measured slower)
+  int no_spare = 0;        // env BTE_SPARE=0: side jobs on compute threads (A/B)
+  int sc_direct = 0;       // env BTE_SC_DIRECT=1: direct band integrals in the self-consistent Newton (A/B)
+  int ugeneric = 0;        // env BTE_UGENERIC=1: generic unstructured sweep (A/B)
+  int dbg_skip_exchange = 0;  // bte_set_debug(BTE_DEBUG_SKIP_EXCHANGE): mutation tests only
+  double *d_energy = nullptr; // bte_get_energy scratch
   double *staging = nullptr;
   int64_t staging_cells = 0;
   int seg_len = 0;
@@ -105,11 +114,6 @@ struct bte_ctx {
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> spans;  // kind 0 sweep, 1 newton, 2 boundary, 3 halo
   bte_timing tacc{};
-  // sweep/Newton pipeline over column chunks (second stream for the Newton)
-  int nchunks = 1;
-  cudaStream_t nstream = nullptr;
-  std::vector<cudaEvent_t> ev_sw, ev_nt;
-  std::vector<char> nt_pending;
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;  // boundary planes swept / halo delivered
   int overlap = 1;  // env BTE_OVERLAP=0: exchange after the whole sweep
   // unstructured mesh (bte_create_umesh): the layout sees one plane of ncells
@@ -625,7 +629,6 @@ bte_status bte_set_tau_mode(bte_ctx *ctx, int mode) {
   if (mode == 1 && ctx->semi) return fail(ctx, BTE_EINVAL, "self-consistent tau: explicit step only");
   if (mode == 1 && ctx->band)
     return fail(ctx, BTE_EINVAL, "self-consistent tau needs every channel's reduction in the Newton (not band contexts)");
-  if (mode == 1 && ctx->fuse_newton) return fail(ctx, BTE_EINVAL, "self-consistent tau: unfused Newton only");
   ctx->tau_mode = mode;
   if (mode == 1) {  // I0c, dI0c, beta at the current T (the next sweep's beta is beta(T^n))
     bte_status st = refresh(ctx);
@@ -700,6 +703,10 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     return bail(fail(ctx, BTE_EINVAL, "bad mesh extents (dim 2 needs nz == 1)"));
   if (!(mesh->dx > 0 && mesh->dy > 0 && mesh->dz > 0)) return bail(fail(ctx, BTE_EINVAL, "cell sizes must be > 0"));
   if (mesh->nx > (1 << 30) || mesh->ny > (1 << 30)) return bail(fail(ctx, BTE_EINVAL, "mesh too large"));
+  // cells per plane are int32 in the kernels (column index = blockIdx.x)
+  if (mesh->dim == 3 && mesh->nx * mesh->ny >= (int64_t)1 << 31)
+    return bail(fail(ctx, BTE_EINVAL, "nx*ny = %lld cells per plane exceeds 2^31 - 1",
+                     (long long)(mesh->nx * mesh->ny)));
   if (dirs->nd < 1 || !dirs->s || !dirs->w) return bail(fail(ctx, BTE_EINVAL, "empty direction set"));
   if (bands->nb < 1 || bands->nb > kMaxBands || !bands->v || !bands->beta_coef)
     return bail(fail(ctx, BTE_EINVAL, "channel count must be in [1, %d]", kMaxBands));
@@ -1144,46 +1151,35 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     if (ctx->seg_override > 0) nseg = std::min(ctx->seg_override, g.nplanes);
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
   }
-  if (const char *e = getenv("BTE_FUSE")) ctx->fuse_newton = atoi(e);
+  if (const char *e = getenv("BTE_SPARE")) ctx->no_spare = atoi(e) == 0;
+  if (const char *e = getenv("BTE_SC_DIRECT")) ctx->sc_direct = atoi(e) != 0;
+  if (const char *e = getenv("BTE_UGENERIC")) ctx->ugeneric = atoi(e) != 0;
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
-  if (const char *e = getenv("BTE_TX")) ctx->tx_override = atoi(e);
   if (const char *e = getenv("BTE_L2HINT")) ctx->l2hint = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_STATS"))
     if (atoi(e)) {
       ctx->d_stats = (unsigned long long *)dev_alloc(ctx, 4 * sizeof(unsigned long long));
       if (ctx->d_stats) CU(cudaMemsetAsync(ctx->d_stats, 0, 4 * sizeof(unsigned long long), ctx->stream));
     }
-  // column chunks for the sweep/Newton two-stream pipeline: off by default
-  // (measured slower on B200); BTE_CHUNKS=n enables it.
-  ctx->nchunks = 1;
-  if (const char *e = getenv("BTE_CHUNKS")) ctx->nchunks = std::max(1, std::min(64, atoi(e)));
-  if (ctx->nchunks > 1) {
-    int lo = 0, hi = 0;
-    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&ctx->nstream, cudaStreamNonBlocking, hi));
-    ctx->ev_sw.resize(ctx->nchunks);
-    ctx->ev_nt.resize(ctx->nchunks);
-    for (auto &e : ctx->ev_sw) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto &e : ctx->ev_nt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  ctx->nt_pending.assign(ctx->nchunks, 0);
   if (const char *e = getenv("BTE_OVERLAP")) ctx->overlap = atoi(e);
   CU(cudaEventCreateWithFlags(&ctx->ev_bnd, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
   if (ctx->nranks > 1 && !ctx->comm_stream) CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
-  {
-    const int64_t nseg = (g.nplanes + ctx->seg_len - 1) / ctx->seg_len;
-    ctx->d_done = (int *)dev_alloc(ctx, nseg * g.ncross * sizeof(int));
-    if (!ctx->d_done) return bail(fail(ctx, BTE_ENOMEM, "device allocation failed"));
-    CU(cudaMemsetAsync(ctx->d_done, 0, nseg * g.ncross * sizeof(int), ctx->stream));
-  }
 
   // ---- multi-GPU communicator
   if (ctx->nranks > 1 && run->nccl_id) {
     std::string emsg;
     if (nccl_shim_init(&ctx->nccl_comm, run->nccl_id, ctx->nranks, ctx->rank, &emsg) != 0)
       return bail(fail(ctx, BTE_ENCCL, "NCCL init failed: %s", emsg.c_str()));
+    int cn = 0, cr = -1;
+    if (nccl_shim_comm_info(ctx->nccl_comm, &cn, &cr, &emsg) != 0)
+      return bail(fail(ctx, BTE_ENCCL, "NCCL comm query failed: %s", emsg.c_str()));
+    if (cn != ctx->nranks || cr != ctx->rank)
+      return bail(fail(ctx, BTE_ENCCL, "NCCL communicator is rank %d of %d, expected %d of %d", cr, cn, ctx->rank,
+                       ctx->nranks));
+    fprintf(stderr, "[bte] NCCL communicator: rank %d of %d (device %d, %s)\n", cr, cn, ctx->device,
+            ctx->band ? "band partition" : ctx->umesh ? "cell partition" : "slab partition");
     if (!ctx->comm_stream) CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
   }
 
@@ -1279,8 +1275,7 @@ static bte_status transfer_I(bte_ctx *ctx, double *host, int to_device) {
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0 = 0, int ncols = -1,
-                             cudaStream_t stream = nullptr);
+static bte_status run_newton(bte_ctx *ctx, int64_t step);
 
 bte_status bte_set_state(bte_ctx *ctx, const double *I, const double *T) {
   if (!ctx) return BTE_EINVAL;
@@ -1432,82 +1427,13 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   return a;
 }
 
-// a1+a2 (+ a3+a4 fused into the sweep tail when *fused is set on return)
-static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, bool allow_fuse, int64_t step,
-                                    int *fused, int col0 = 0, int ncols = 0, int p_lo = 0, int p_hi = 0,
-                                    int seg_len = 0) {
-  if (ctx->umesh) {
-    *fused = 0;
-    USweepArgs a{};
-    a.g = ctx->g;
-    a.u = ctx->u;
-    a.Iin = Iin;
-    a.Iout = Iout;
-    a.I0c = ctx->I0s;
-    a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
-    a.Dpart = ctx->Dpart;
-    a.v = ctx->m.v;
-    a.dt = ctx->dt;
-    a.target_threads = ctx->target_threads;
-    a.pipelined = ctx->use_tma;
-    a.stages = ctx->stages_override;
-    a.chunk = ctx->seg_override;
-    CU(launch_usweep(a, ctx->stream));
-    ctx->tacc.launches++;
-    ctx->tacc.sweep_launches++;
-    return BTE_OK;
-  }
-  if (ctx->rot) {
-    // octant-slot rotation: octant k is swept from its region into the spare
-    // region, whose old occupant's region becomes the next spare; the octants
-    // go one launch each, in slot order (each reads only its own I^n; the
-    // specular ghosts come from the boundary pass's snapshot)
-    *fused = 0;
-    for (int k = 0; k < ctx->g.nslot; ++k) {
-      SweepArgs a{};
-      a.col0 = col0;
-      a.ncols = ncols;
-      a.p_lo = p_lo;
-      a.p_hi = p_hi;
-      a.slot0 = k;
-      a.nslots = 1;
-      a.g = ctx->g;
-      for (int sl = 0; sl < kMaxSlots; ++sl) a.out_off[sl] = ctx->g.slot_off[sl];
-      a.out_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
-      a.Iin = Iin;
-      a.Iout = Iout;
-      a.I0c = ctx->I0s;
-      a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
-      a.Dpart = ctx->Dpart;
-      a.v = ctx->m.v;
-      a.dt = ctx->dt;
-      a.seg_len = seg_len > 0 ? seg_len : ctx->seg_len;
-      a.use_tma = ctx->use_tma;
-      a.stages_override = ctx->stages_override;
-      a.target_threads = ctx->target_threads;
-      a.smem_budget_kb = ctx->smem_budget_kb;
-      a.stcs = ctx->stcs;
-      a.tx_override = ctx->tx_override;
-      a.l2hint = ctx->l2hint;
-      a.nw = newton_args(ctx, step);
-      a.fuse_newton = 0;
-      a.done = ctx->d_done;
-      int f = 0;
-      CU(launch_sweep(a, ctx->stream, &f));
-      const int freed = (int)(ctx->g.slot_off[k] / ctx->g.slot_stride);
-      ctx->g.slot_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
-      ctx->spare = freed;
-      ctx->tacc.launches++;
-      ctx->tacc.sweep_launches++;
-    }
-    return BTE_OK;
-  }
+static SweepArgs sweep_args(const bte_ctx *ctx, const double *Iin, double *Iout, int p_lo, int p_hi, int seg_len) {
   SweepArgs a{};
   a.slot0 = 0;
   a.nslots = 0;
   for (int sl = 0; sl < kMaxSlots; ++sl) a.out_off[sl] = ctx->g.slot_off[sl];
-  a.col0 = col0;
-  a.ncols = ncols;
+  a.col0 = 0;
+  a.ncols = 0;
   a.p_lo = p_lo;
   a.p_hi = p_hi;
   a.g = ctx->g;
@@ -1524,27 +1450,67 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
   a.target_threads = ctx->target_threads;
   a.smem_budget_kb = ctx->smem_budget_kb;
   a.stcs = ctx->stcs;
-  a.tx_override = ctx->tx_override;
   a.l2hint = ctx->l2hint;
-  a.nw = newton_args(ctx, step);
-  a.fuse_newton = allow_fuse && ctx->fuse_newton;
-  a.done = ctx->d_done;
-  CU(launch_sweep(a, ctx->stream, fused));
+  a.no_spare = ctx->no_spare;
+  return a;
+}
+
+// a1 (inline ghosts) + a2 over planes [p_lo, p_hi) (all when p_hi <= p_lo)
+static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iout, int p_lo = 0, int p_hi = 0,
+                                    int seg_len = 0) {
+  if (ctx->umesh) {
+    USweepArgs a{};
+    a.g = ctx->g;
+    a.u = ctx->u;
+    a.Iin = Iin;
+    a.Iout = Iout;
+    a.I0c = ctx->I0s;
+    a.beta = ctx->semi ? ctx->zbeta : ctx->betas;
+    a.Dpart = ctx->Dpart;
+    a.v = ctx->m.v;
+    a.dt = ctx->dt;
+    a.target_threads = ctx->target_threads;
+    a.pipelined = ctx->use_tma;
+    a.stages = ctx->stages_override;
+    a.chunk = ctx->seg_override;
+    a.generic = ctx->ugeneric;
+    CU(launch_usweep(a, ctx->stream));
+    ctx->tacc.launches++;
+    ctx->tacc.sweep_launches++;
+    return BTE_OK;
+  }
+  if (ctx->rot) {
+    // octant-slot rotation: octant k is swept from its region into the spare
+    // region, whose old occupant's region becomes the next spare; the octants
+    // go one launch each, in slot order (each reads only its own I^n; the
+    // specular ghosts come from the boundary pass's snapshot)
+    for (int k = 0; k < ctx->g.nslot; ++k) {
+      SweepArgs a = sweep_args(ctx, Iin, Iout, p_lo, p_hi, seg_len);
+      a.slot0 = k;
+      a.nslots = 1;
+      a.out_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
+      CU(launch_sweep(a, ctx->stream));
+      const int freed = (int)(ctx->g.slot_off[k] / ctx->g.slot_stride);
+      ctx->g.slot_off[k] = (int64_t)ctx->spare * ctx->g.slot_stride;
+      ctx->spare = freed;
+      ctx->tacc.launches++;
+      ctx->tacc.sweep_launches++;
+    }
+    return BTE_OK;
+  }
+  SweepArgs a = sweep_args(ctx, Iin, Iout, p_lo, p_hi, seg_len);
+  CU(launch_sweep(a, ctx->stream));
   ctx->tacc.launches++;
   ctx->tacc.sweep_launches++;
   return BTE_OK;
 }
 
-static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0, int ncols, cudaStream_t stream) {
+static bte_status run_newton(bte_ctx *ctx, int64_t step) {
   NewtonArgs a = newton_args(ctx, step);
-  if (ncols >= 0) {
-    a.col0 = col0;
-    a.ncols = ncols;
-  }
   if (ctx->tau_mode == 1)
-    CU(launch_newton_sc(a, stream ? stream : ctx->stream));
+    CU(launch_newton_sc(a, ctx->stream));
   else
-    CU(launch_newton(a, stream ? stream : ctx->stream));
+    CU(launch_newton(a, ctx->stream));
   ctx->tacc.launches++;
   ctx->tacc.newton_launches++;
   return BTE_OK;
@@ -1553,7 +1519,10 @@ static bte_status run_newton(bte_ctx *ctx, int64_t step, int col0, int ncols, cu
 
 static bte_status span_begin(bte_ctx *ctx, bool t, int kind, cudaStream_t s, size_t *id) {
   if (!t) return BTE_OK;
-  if (ctx->ev_used + 2 > ctx->ev.size()) return BTE_OK;  // pool exhausted: stop recording
+  if (ctx->ev_used + 2 > ctx->ev.size()) {  // pool exhausted: stop recording, and say so
+    ctx->tacc.truncated = 1;
+    return BTE_OK;
+  }
   *id = ctx->ev_used;
   ctx->ev_used += 2;
   ctx->spans.push_back({kind, *id});
@@ -1566,75 +1535,53 @@ static bte_status span_end(bte_ctx *ctx, bool t, cudaStream_t s, size_t id) {
   return BTE_OK;
 }
 
-// One step = [diffuse ghosts] + for each column chunk k: sweep(k) on the
-// context stream and, on the Newton stream once sweep(k) is done, Newton(k).
-// The next step's sweep(k) waits only for Newton(k), so the FP64-bound Newton
-// of chunk k overlaps the HBM-bound sweeps of the other chunks.
-// Launch one step (a1..a4) of ctx on its streams; the caller exchanges halos.
+// Launch one step (a1..a4) of ctx on its stream; the caller exchanges halos.
 // split: sweep the two owned boundary planes first and record ctx->ev_bnd, so
 // the halo exchange (a5) can run on the comm stream while the interior planes
 // are swept (SURVEY 8(e) overlap schedule).
 static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   const bool has_bnd = n_diffuse(ctx) > 0;
-  const int C = (ctx->fuse_newton || ctx->rot || ctx->umesh || ctx->semi) ? 1 : ctx->nchunks;
-  const int ncross = ctx->g.ncross;
   const int np = ctx->g.nplanes;
   bte_status st;
   double *Iin = ctx->I[ctx->cur];
   double *Iout = ctx->I[1 - ctx->cur];
   size_t id = (size_t)-1;
+  nvtx_push("bte_step");
   if (has_bnd) {
+    nvtx_push("a1 boundary");
     if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
     if ((st = launch_boundary(ctx, Iin))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
+    nvtx_pop();
   }
   // the semi-implicit step exchanges halos after its relaxation pass
-  if (split && (C > 1 || ctx->fuse_newton || ctx->rot || ctx->semi || ctx->umesh)) split = false;
+  if (split && (ctx->rot || ctx->semi || ctx->umesh)) split = false;
+  nvtx_push("a2 sweep");
   if (split) {
-    int fused = 0;
     id = (size_t)-1;
     if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
-    if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, 0, 1, 1))) return st;
-    if (np > 1 && (st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, np - 1, np, 1)))
-      return st;
+    if ((st = launch_sweep_step(ctx, Iin, Iout, 0, 1, 1))) return st;
+    if (np > 1 && (st = launch_sweep_step(ctx, Iin, Iout, np - 1, np, 1))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
     CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
     if (np > 2) {
       id = (size_t)-1;
       if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
-      if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused, 0, 0, 1, np - 1))) return st;
+      if ((st = launch_sweep_step(ctx, Iin, Iout, 1, np - 1))) return st;
       if ((st = span_end(ctx, t, ctx->stream, id))) return st;
     }
-    id = (size_t)-1;
-    if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
-    if ((st = run_newton(ctx, ctx->steps_done, 0, -1, ctx->stream))) return st;
-    if ((st = span_end(ctx, t, ctx->stream, id))) return st;
-    return BTE_OK;
-  }
-  for (int k = 0; k < C; ++k) {
-    const int c0 = (int)((int64_t)k * ncross / C), c1 = (int)((int64_t)(k + 1) * ncross / C);
-    if (c1 <= c0) continue;
-    if (C > 1 && ctx->nt_pending[k]) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
+  } else {
     id = (size_t)-1;
     if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
-    int fused = 0;
-    if ((st = launch_sweep_step(ctx, Iin, Iout, true, ctx->steps_done, &fused, c0, c1 - c0))) return st;
+    if ((st = launch_sweep_step(ctx, Iin, Iout))) return st;
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
-    if (fused) continue;
-    cudaStream_t ns = C > 1 ? ctx->nstream : ctx->stream;
-    if (C > 1) {
-      CU(cudaEventRecord(ctx->ev_sw[k], ctx->stream));
-      CU(cudaStreamWaitEvent(ns, ctx->ev_sw[k], 0));
-    }
-    id = (size_t)-1;
-    if ((st = span_begin(ctx, t, 1, ns, &id))) return st;
-    if ((st = run_newton(ctx, ctx->steps_done, c0, c1 - c0, ns))) return st;
-    if ((st = span_end(ctx, t, ns, id))) return st;
-    if (C > 1) {
-      CU(cudaEventRecord(ctx->ev_nt[k], ns));
-      ctx->nt_pending[k] = 1;
-    }
   }
+  nvtx_pop();
+  nvtx_push("a3+a4 reduce+Newton");
+  id = (size_t)-1;
+  if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
+  if ((st = run_newton(ctx, ctx->steps_done))) return st;
+  if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   if (ctx->semi) {  // reading R-l: I^{n+1} = (J + dt beta I0(T^{n+1})) / (1 + dt beta)
     id = (size_t)-1;
     if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
@@ -1642,7 +1589,9 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
     ctx->tacc.launches++;
   }
-  CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
+  nvtx_pop();
+  if (!split) CU(cudaEventRecord(ctx->ev_bnd, ctx->stream));
+  nvtx_pop();
   return BTE_OK;
 }
 
@@ -1661,8 +1610,7 @@ static bte_status band_sweep_launch(bte_ctx *ctx, bool t) {
   }
   id = (size_t)-1;
   if ((st = span_begin(ctx, t, 0, ctx->stream, &id))) return st;
-  int fused = 0;
-  if ((st = launch_sweep_step(ctx, Iin, Iout, false, ctx->steps_done, &fused))) return st;
+  if ((st = launch_sweep_step(ctx, Iin, Iout))) return st;
   if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   id = (size_t)-1;
   if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
@@ -1679,18 +1627,10 @@ static bte_status band_newton_launch(bte_ctx *ctx, bool t) {
   bte_status st;
   size_t id = (size_t)-1;
   if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
-  if ((st = run_newton(ctx, ctx->steps_done, 0, -1, ctx->stream))) return st;
+  if ((st = run_newton(ctx, ctx->steps_done))) return st;
   return span_end(ctx, t, ctx->stream, id);
 }
 
-static bte_status join_newton(bte_ctx *ctx) {
-  for (int k = 0; k < (int)ctx->nt_pending.size(); ++k)
-    if (ctx->nt_pending[k]) {
-      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_nt[k], 0));
-      ctx->nt_pending[k] = 0;
-    }
-  return BTE_OK;
-}
 
 // One step = [diffuse ghosts] + for each column chunk k: sweep(k) on the
 // context stream and, on the Newton stream once sweep(k) is done, Newton(k)
@@ -1730,11 +1670,13 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
       // step's sweeps wait for it (the wait sits after this step's Newton)
       CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_bnd, 0));
       size_t id = (size_t)-1;
+      nvtx_push("a5 halo exchange");
       if ((st = span_begin(ctx, t, 3, ctx->comm_stream, &id))) return st;
       if ((st = ctx->umesh ? uhalo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream)
                            : halo_exchange(ctx, ctx->I[1 - ctx->cur], ctx->comm_stream)))
         return st;
       if ((st = span_end(ctx, t, ctx->comm_stream, id))) return st;
+      nvtx_pop();
       CU(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
       CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
     }
@@ -1742,7 +1684,6 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
     ctx->cur = 1 - ctx->cur;
     ctx->steps_done++;
   }
-  if ((st = join_newton(ctx))) return st;
   if (ctx->d_stats) {
     unsigned long long h[4];
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1761,8 +1702,7 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
 // step of a bte_group_step call): senders copy owned planes into halos.
 static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
   bte_ctx *ctx = ctxs[0];
-  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
-    if (atoi(e)) return BTE_OK;
+  if (ctxs[0]->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   std::vector<cudaEvent_t> done(n), put(n);
   for (int r = 0; r < n; ++r) {
     CU(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
@@ -1802,8 +1742,7 @@ static bte_status group_exchange(bte_ctx **ctxs, int n, bool output_buffers) {
 // ev_bnd), copy the planes into the receiver's halo; each receiver's compute
 // stream waits for its senders' copies after this step's Newton.
 static bte_status group_exchange_overlap(bte_ctx **ctxs, int n) {
-  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
-    if (atoi(e)) return BTE_OK;
+  if (ctxs[0]->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   bte_ctx *ctx = ctxs[0];
   for (int r = 0; r < n; ++r) {
     bte_ctx *c = ctxs[r];
@@ -1835,8 +1774,7 @@ static bte_status group_exchange_overlap(bte_ctx **ctxs, int n) {
 // read its Sall) and the sender's partial.
 static bte_status band_exchange(bte_ctx **ctxs, int n) {
   bte_ctx *ctx = ctxs[0];
-  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
-    if (atoi(e)) return BTE_OK;
+  if (ctxs[0]->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   const int64_t ncl = ctx->ncells_local;
   std::vector<cudaEvent_t> done(n), put(n);
   for (int r = 0; r < n; ++r) {
@@ -1875,8 +1813,7 @@ static double *uhalo_dst(bte_ctx *q, double *Ibuf, int slot, int64_t recv_off) {
 // peer's segment slot by slot into the peer's halo blocks; receivers wait.
 static bte_status ugroup_exchange(bte_ctx **ctxs, int n, bool output) {
   bte_ctx *ctx = ctxs[0];
-  if (const char *e = getenv("BTE_MUTATE_SKIP_HALO"))  // test-only mutation switch
-    if (atoi(e)) return BTE_OK;
+  if (ctxs[0]->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   std::vector<cudaEvent_t> done(n), put(n);
   for (int r = 0; r < n; ++r) {
     CU(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
@@ -1994,7 +1931,6 @@ bte_status bte_group_step(bte_ctx **ctxs, int n, int64_t nsteps) {
     for (int r = 0; r < n; ++r) {
       const bool t = ctxs[r]->timing && ctxs[r]->timing_used < ctxs[r]->timing_max;
       if ((st = step_launch(ctxs[r], t, n > 1 && ctxs[r]->overlap))) return st;
-      if ((st = join_newton(ctxs[r]))) return st;
     }
     if (n > 1 && (st = um ? ugroup_exchange(ctxs, n, true) : group_exchange_overlap(ctxs, n))) return st;
     for (int r = 0; r < n; ++r) {
@@ -2068,13 +2004,14 @@ bte_status bte_get_temperature(bte_ctx *ctx, double *out, size_t count) {
 bte_status bte_get_energy(bte_ctx *ctx, double *E) {
   if (!ctx || !E) return BTE_EINVAL;
   const int64_t ncl = ctx->ncells_local;
-  double *d_E = nullptr;
-  CU(cudaMalloc(&d_E, ncl * sizeof(double)));
-  CU(launch_energy(ctx->g, ctx->I[ctx->cur], ctx->m.v, d_E, ctx->stream));
+  if (!ctx->d_energy) {  // per-cell energies [ncl] + the gathered rank sums [nranks], kept for later calls
+    ctx->d_energy = (double *)dev_alloc(ctx, (size_t)(ncl + ctx->nranks) * sizeof(double));
+    if (!ctx->d_energy) return fail(ctx, BTE_ENOMEM, "energy buffer allocation failed");
+  }
+  CU(launch_energy(ctx->g, ctx->I[ctx->cur], ctx->m.v, ctx->d_energy, ctx->stream));
   std::vector<double> h(ncl);
-  CU(cudaMemcpyAsync(h.data(), d_E, ncl * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(h.data(), ctx->d_energy, ncl * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
-  CU(cudaFree(d_E));
   const bte_mesh &m = ctx->mesh;
   const double V = ctx->umesh ? 1.0 : m.dx * m.dy * m.dz;
   if (ctx->umesh)
@@ -2086,7 +2023,29 @@ bte_status bte_get_energy(bte_ctx *ctx, double *E) {
     comp = (t - s) - y;
     s = t;
   }
-  *E = V * s;
+  double e = V * s;
+  if (ctx->nccl_comm) {
+    // all ranks' partial sums (AllGather), added in rank order: the same total,
+    // bit for bit, on every rank (an AllReduce does not fix its order)
+    double *d_all = ctx->d_energy + ncl;
+    CU(cudaMemcpyAsync(d_all + ctx->rank, &e, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    std::string emsg;
+    if (nccl_shim_allgather(ctx->nccl_comm, d_all + ctx->rank, d_all, 1, ctx->stream, &emsg))
+      return fail(ctx, BTE_ENCCL, "%s", emsg.c_str());
+    std::vector<double> parts(ctx->nranks);
+    CU(cudaMemcpyAsync(parts.data(), d_all, ctx->nranks * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    e = 0.0;
+    for (double x : parts) e += x;
+  }
+  *E = e;
+  return BTE_OK;
+}
+
+bte_status bte_set_debug(bte_ctx *ctx, int what, int value) {
+  if (!ctx) return BTE_EINVAL;
+  if (what != BTE_DEBUG_SKIP_EXCHANGE) return fail(ctx, BTE_EINVAL, "unknown debug switch %d", what);
+  ctx->dbg_skip_exchange = value != 0;
   return BTE_OK;
 }
 
@@ -2106,8 +2065,7 @@ bte_status bte_debug_substep(bte_ctx *ctx, int which, double *out, size_t count)
   double *Iin = ctx->I[ctx->cur];
   double *Iout = ctx->I[1 - ctx->cur];
   if (n_diffuse(ctx) && (st = launch_boundary(ctx, Iin))) return st;
-  int fused = 0;
-  if ((st = launch_sweep_step(ctx, Iin, Iout, false, -1, &fused))) return st;
+  if ((st = launch_sweep_step(ctx, Iin, Iout))) return st;
   if (which == 0) {
     ctx->cur = 1 - ctx->cur;  // read the swept buffer, then restore
     st = transfer_I(ctx, out, 0);
@@ -2135,7 +2093,7 @@ bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps) {
   ctx->timing_used = 0;
   ctx->timing_max = enable ? max_steps : 0;
   if (enable) {
-    const int64_t per_step = 2 * (2 * (int64_t)ctx->nchunks + 2);
+    const int64_t per_step = 2 * 6;  // spans per step at most: boundary, 2 sweeps (split), Newton, relax, halo
     ctx->ev.resize((size_t)(per_step * max_steps));
     for (auto &e : ctx->ev) CU(cudaEventCreate(&e));
   }
@@ -2145,7 +2103,6 @@ bte_status bte_timing_enable(bte_ctx *ctx, int enable, int64_t max_steps) {
 bte_status bte_timing_read(bte_ctx *ctx, bte_timing *out) {
   if (!ctx || !out) return BTE_EINVAL;
   CU(cudaStreamSynchronize(ctx->stream));
-  if (ctx->nstream) CU(cudaStreamSynchronize(ctx->nstream));
   bte_timing t = ctx->tacc;
   t.steps = ctx->timing_used;
   t.sweep_ms = t.newton_ms = t.boundary_ms = t.halo_ms = 0;
@@ -2176,20 +2133,22 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
   out->band = ctx->band;
   out->rotate = ctx->rot;
   out->cell0 = ctx->g.cell0;
+  if (ctx->umesh) {
+    out->sweep_kernel = "k_usweep_tma (face-list upwind flux + relaxation on m-sided cells)";
+  } else {
+    SweepArgs a = sweep_args(ctx, ctx->I[0], ctx->I[1], 0, 0, 0);
+    out->sweep_kernel = sweep_kernel_name(a);
+  }
   return BTE_OK;
 }
 
 void bte_destroy(bte_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->nstream) cudaStreamSynchronize(ctx->nstream);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
-  for (cudaEvent_t e : ctx->ev_sw) cudaEventDestroy(e);
-  for (cudaEvent_t e : ctx->ev_nt) cudaEventDestroy(e);
   if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
   if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
-  if (ctx->nstream) cudaStreamDestroy(ctx->nstream);
   if (ctx->nccl_comm) nccl_shim_destroy(ctx->nccl_comm);
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   for (void *p : ctx->allocs) {

@@ -105,6 +105,7 @@ struct NewtonArgs {
   int minb;               // k_newton occupancy variant (0 = default)
   double semi_dt;         // > 0: semi-implicit step weights beta/(v(1 + semi_dt beta)) (reading R-l)
   unsigned long long *stats;  // debug counters: [evaluations, final re-evaluations, cells solved] or null
+  int sc_direct;          // self-consistent tau: direct band integrals even on uniform grids (A/B)
 };
 
 struct SweepArgs {
@@ -118,8 +119,6 @@ struct SweepArgs {
   int seg_len;            // cells per CTA along the march axis
   int jpt;                // directions per thread (set by launch_sweep)
   int jg;                 // thread groups (set by launch_sweep)
-  int tx;                 // columns per CTA (k_sweep_tmx; set by launch_sweep)
-  int tx_override;        // 0 auto, 1 force single-column kernel, > 1 force k_sweep_tmx width
   int use_tma;            // cp.async.bulk pipeline (k_sweep_tma) when the layout allows
   int stages;             // pipeline depth (set by launch_sweep)
   int stages_override;    // 0 = automatic
@@ -132,9 +131,7 @@ struct SweepArgs {
   int slot0, nslots;      // octant slots of this launch (nslots = 0: all)
   int64_t out_off[kMaxSlots];  // where slot s of I^{n+1} goes in Iout
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
-  NewtonArgs nw;          // fused a3+a4 (k_sweep_tma tail)
-  int fuse_newton;
-  int *done;              // [nseg][ncross] tickets, zero between launches
+  int no_spare;           // 1: side jobs on compute threads (A/B switch read at create)
 };
 
 // Unstructured simplex mesh, device view.  The state layout
@@ -164,10 +161,12 @@ struct USweepArgs {
   int target_threads;
   int pipelined;          // k_usweep_tma (default) vs the one-CTA-per-cell k_usweep
   int stages, chunk;      // pipeline depth and cells per CTA (0 = automatic)
+  int generic;            // 1: skip the 40-channel x 50-direction specialisation (A/B)
 };
 
 // kernels / launchers (kernels.cu)
-cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused);
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s);
+const char *sweep_kernel_name(const SweepArgs &a);
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "bte_internal.cuh"
 
@@ -298,171 +300,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-// Small-block sweep with per-thread cp.async prefetch (the demo's 5 x 55
-// blocks): as k_sweep, but the values cell i+1 needs (own, cross-upwind, I0c,
-// beta) are copied into a per-thread shared-memory slot pair while cell i
-// computes, so a DRAM latency is paid once per column segment instead of once
-// per cell, without the registers a register prefetch costs (occupancy).
-// Identical arithmetic to k_sweep (bitwise equal results).
-template <int DIM, int JMAX>
-__global__ void __launch_bounds__(1024) k_sweep_ca(const SweepArgs A) {
-  extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb] | pf[2][W][blockDim]
-  const Geometry &g = A.g;
-  const int nb = g.nb, nj = g.nj, Es = g.Es;
-  const int tid = threadIdx.x;
-  const int nt = blockDim.x;
-  const int grp = tid / nb;
-  const int b = tid - grp * nb;
-  const int JG = blockDim.x / nb;
-  const int j0 = grp * A.jpt;
-  const int nloc = max(0, min(A.jpt, nj - j0));
-  constexpr int W = (DIM == 3 ? 3 : 2) * JMAX + 2;  // own | xu | (yu) | I0 | beta
-  double *coef = sm;
-  double *red = sm + 4 * nj;
-  double *pf = red + 2 * JG * nb;
-
-  const int slot = A.slot0 + blockIdx.y;
-  const int oct = g.slot_oct[slot];
-  const int col = A.col0 + blockIdx.x;
-  const int x = (DIM == 3) ? col % g.nx : col;
-  const int y = (DIM == 3) ? col / g.nx : 0;
-  const bool xneg = oct & 4;
-  const bool yneg = oct & 2;
-  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
-  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
-  const int xregion = xneg ? 1 : 0;
-  const int64_t xoff = xneg ? (int64_t)Es : -(int64_t)Es;
-  bool yghost = false;
-  int yregion = 2;
-  int64_t yoff = 0;
-  if (DIM == 3) {
-    yghost = yneg ? (y == g.ny - 1) : (y == 0);
-    yregion = yneg ? 3 : 2;
-    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
-  }
-  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
-  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
-
-  const int pb = A.p_lo + blockIdx.z * A.seg_len;
-  const int pe = min(A.p_hi, pb + A.seg_len);
-  const int np = pe - pb;
-  const int step = mneg ? -1 : 1;
-  const int pfirst = mneg ? pe - 1 : pb;
-  const double *__restrict__ Iin = A.Iin;
-  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
-  double *__restrict__ Os = A.Iout + A.out_off[slot];
-  const int64_t colE = (int64_t)col * Es;
-  const double dt = A.dt;
-  const double v = A.v[b < nb ? b : 0];
-  const bool active = grp < JG && tid < JG * nb;
-
-  auto cp8 = [&](double *dst, const double *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-  };
-  // values of the i-th cell of the segment into slot pair buf
-  auto prefetch = [&](int i, int buf) {
-    if (active && i < np) {
-      const int p = pfirst + i * step;
-      const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
-      const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
-      double *q = pf + ((size_t)buf * W) * nt + tid;
-#pragma unroll
-      for (int k = 0; k < JMAX; ++k)
-        if (k < nloc) {
-          const int e = (j0 + k) * nb + b;
-          cp8(q + (size_t)k * nt, Is + base + e);
-          if (!xghost) cp8(q + (size_t)(JMAX + k) * nt, Is + base + xoff + e);
-          if (DIM == 3 && !yghost) cp8(q + (size_t)(2 * JMAX + k) * nt, Is + base + yoff + e);
-        }
-      cp8(q + (size_t)(W - 2) * nt, A.I0c + cell * nb + b);
-      cp8(q + (size_t)(W - 1) * nt, A.beta + cell * nb + b);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  double prev[JMAX];
-  {
-    const int p = pfirst;
-    const int pm = p - step;
-    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
-    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
-    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
-#pragma unroll
-    for (int k = 0; k < JMAX; ++k) {
-      prev[k] = 0.0;
-      if (active && k < nloc) {
-        const int e = (j0 + k) * nb + b;
-        if (stored)
-          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colE + e);
-        else
-          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
-      }
-    }
-  }
-  prefetch(0, 0);
-  __syncthreads();
-
-  int buf = 0;
-  int p = pfirst;
-  for (int i = 0; i < np; ++i, p += step) {
-    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
-    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
-    const int64_t mg = g.m0 + p;
-    prefetch(i + 1, buf ^ 1);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    double acc = 0.0;
-    if (active) {
-      const double *q = pf + ((size_t)buf * W) * nt + tid;
-      const double I0 = q[(size_t)(W - 2) * nt];
-      const double dtb = dt * q[(size_t)(W - 1) * nt];
-#pragma unroll
-      for (int k = 0; k < JMAX; ++k) {
-        if (k < nloc) {
-          const int j = j0 + k;
-          const int e = j * nb + b;
-          const double Ic = q[(size_t)k * nt];
-          double xu, yu = 0.0;
-          if (!xghost) {
-            xu = q[(size_t)(JMAX + k) * nt];
-          } else {
-            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
-            xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
-          }
-          if (DIM == 3) {
-            if (!yghost) {
-              yu = q[(size_t)(2 * JMAX + k) * nt];
-            } else {
-              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
-              yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
-            }
-          }
-          const double *cf = coef + 4 * j;
-          const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cf, v, I0, dtb);
-          Os[base + e] = In;
-          acc = fma(cf[3], I0 - In, acc);
-          prev[k] = Ic;
-        }
-      }
-    }
-    double *rb = red + (i & 1) * JG * nb;
-    if (active) rb[tid] = acc;
-    __syncthreads();
-    if (tid < nb) {
-      double s = 0.0;
-      for (int qq = 0; qq < JG; ++qq) s += rb[qq * nb + tid];
-      A.Dpart[(cell * g.nslot + slot) * nb + tid] = s;
-    }
-    buf ^= 1;
-  }
-}
-
 // Same decomposition as k_sweep, but the (cell, octant) blocks of the cell and
 // of its cross-axis upwind neighbours (16 KB each at 50 x 40), plus the cell's
 // I0c/beta rows, stream into an S-stage shared-memory ring with cp.async.bulk
 // + mbarrier, issued S cells ahead by one thread.  Keeps S x (2 or 3) x 16 KB
 // of HBM/L2 reads in flight per CTA.  NBT > 0 fixes the channel count at
 // compile time (immediate smem/global offsets); NBT = 0 is the generic path.
-template <int DIM, int JMAX, int NBT, bool FUSE>
+template <int DIM, int JMAX, int NBT>
 __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -654,236 +498,6 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     }
     buf ^= 1;
   }
-  if (FUSE) {
-    // a3 + a4 fused: the last of the nslot CTAs of this (column, segment) runs
-    // the Newton for its cells (threadfence + ticket), overlapping the
-    // FP64-bound solve with other CTAs' HBM streaming.
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      int *ctr = A.done + (int64_t)blockIdx.z * g.ncross + col;
-      const int old = atomicAdd(ctr, 1);
-      s_last = (old == g.nslot - 1);
-      if (s_last) *ctr = 0;  // ready for the next step
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      const NewtonArgs &na = A.nw;
-      const int R = gl_stride(nb);
-      double *sA = stage0;  // stage ring is free: every stage was consumed
-      double *sX = sA + R * kNGL;
-      const int nwarp = blockDim.x >> 5;
-      const int wsd = newton_scratch(na.m, nb);
-      double *cs = sX + R * kNGL + (tid >> 5) * wsd;
-      int *sI = reinterpret_cast<int *>(sX + R * kNGL + nwarp * wsd);
-      if (na.m.mode != 0) {
-        for (int q = tid; q < nb * kNGL; q += blockDim.x) {
-          const int bq = q / kNGL, jq = q - bq * kNGL;
-          sA[jq * R + bq] = na.m.A[q];
-          sX[jq * R + bq] = na.m.X[q];
-        }
-        for (int q = tid; q < 4 * (na.m.imax + 1); q += blockDim.x) sI[q] = na.m.ichan[q];
-      }
-      __syncthreads();
-      for (int pp = pb + (tid >> 5); pp < pe; pp += nwarp)
-        newton_cell(na, (int64_t)col + (int64_t)pp * g.ncross, sA, sX, sI, cs, tid & 31);
-    }
-  }
-}
-
-// Multi-column variant for small (cell, octant) blocks (e.g. the paper's demo:
-// 5 directions x 55 channels = 2.2 KB): one CTA = TX adjacent columns of one
-// x-row (fixed y in 3-D) x one octant slot x one segment.  Per plane one bulk
-// copy brings the TX own blocks plus the upwind halo column (contiguous in
-// memory), so the x-upwind value of every interior column comes from the same
-// stage; 3-D adds one copy of the TX y-upwind blocks.  Thread (t, grp, b)
-// owns column t, channel b and directions [grp*jpt, grp*jpt + jpt).
-template <int DIM, int JMAX>
-__global__ void __launch_bounds__(1024) k_sweep_tmx(const SweepArgs A) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  const Geometry &g = A.g;
-  const int nb = g.nb, nj = g.nj, Es = g.Es;
-  const int S = A.stages, TX = A.tx, JG = A.jg;
-  const int tpc = JG * nb;  // threads per column
-  const int tid = threadIdx.x;
-  const int t = tid / tpc;
-  const int rr0 = tid - t * tpc;
-  const int grp = rr0 / nb;
-  const int b = rr0 - grp * nb;
-  const int j0 = grp * A.jpt;
-  const int nloc = max(0, min(A.jpt, nj - j0));
-
-  const int slot = A.slot0 + blockIdx.y;
-  const int oct = g.slot_oct[slot];
-  const int ngx = (g.nx + TX - 1) / TX;
-  const int gx = blockIdx.x % ngx;
-  const int y = (DIM == 3) ? blockIdx.x / ngx : 0;
-  const int x0 = gx * TX, x1 = min(g.nx, x0 + TX), tw = x1 - x0;
-  const bool active = t < tw;
-  const int x = x0 + t;
-  const bool xneg = oct & 4;
-  const bool yneg = oct & 2;
-  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
-  const bool halo = xneg ? (x1 < g.nx) : (x0 > 0);
-  const int xa = (xneg || !halo) ? x0 : x0 - 1;
-  const int nxb = tw + (halo ? 1 : 0);
-  const int own_idx = x - xa;
-  const int up_idx = xneg ? own_idx + 1 : own_idx - 1;
-  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
-  const int xregion = xneg ? 1 : 0;
-  bool yghost = false;
-  int yregion = 2;
-  int ycol = 0;
-  if (DIM == 3) {
-    yghost = yneg ? (y == g.ny - 1) : (y == 0);
-    yregion = yneg ? 3 : 2;
-    ycol = yneg ? g.nx : -g.nx;
-  }
-  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
-  const int64_t rowcol0 = (DIM == 3) ? (int64_t)y * g.nx : 0;  // cross index of x = 0 in this row
-  const int64_t colx = rowcol0 + x;
-
-  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
-  double *coef = reinterpret_cast<double *>(smraw + 128);
-  double *red = coef + 4 * nj;                // [2][TX*tpc]
-  double *stage0 = red + 2 * TX * tpc;
-  const int64_t sd = A.stage_doubles;
-  const int oY = (TX + 1) * Es;
-  const int oI0 = oY + (DIM == 3 ? TX * Es : 0);
-  const int oBe = oI0 + TX * nb;
-  const bool rows_tma = (nb % 2) == 0;
-
-  const int pb = A.p_lo + blockIdx.z * A.seg_len;
-  const int pe = min(A.p_hi, pb + A.seg_len);
-  const int np = pe - pb;
-  const int step = mneg ? -1 : 1;
-  const int pfirst = mneg ? pe - 1 : pb;
-
-  const double *__restrict__ Iin = A.Iin;
-  const double *__restrict__ Is = A.Iin + g.slot_off[slot];
-  double *__restrict__ Os = A.Iout + A.out_off[slot];
-  const double dt = A.dt;
-
-  auto issue = [&](int i, int st) {
-    const int pp = pfirst + i * step;
-    const int64_t pbase = (int64_t)(pp + g.plane_off) * g.plane_stride;
-    const int64_t cell0 = rowcol0 + x0 + (int64_t)pp * g.ncross;
-    double *sp = stage0 + st * sd;
-    const uint32_t bx = (uint32_t)nxb * Es * 8u;
-    const uint32_t by = (DIM == 3 && !yghost) ? (uint32_t)tw * Es * 8u : 0u;
-    const uint32_t br = rows_tma ? (uint32_t)tw * nb * 8u : 0u;
-    mbar_expect_tx(&full[st], bx + by + 2u * br);
-    bulk_g2s(sp, Is + pbase + (rowcol0 + xa) * Es, bx, &full[st]);
-    if (by) bulk_g2s(sp + oY, Is + pbase + (rowcol0 + x0 + ycol) * Es, by, &full[st]);
-    if (br) {
-      bulk_g2s(sp + oI0, A.I0c + cell0 * nb, br, &full[st]);
-      bulk_g2s(sp + oBe, A.beta + cell0 * nb, br, &full[st]);
-    }
-  };
-
-  if (tid == 0) {
-    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
-  __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < min(S, np); ++i) issue(i, i);
-
-  const double v = A.v[b];
-  const int e0 = j0 * nb + b;
-  const double *cq = coef + 4 * j0;
-  double prev[JMAX];
-  {
-    const int p = pfirst;
-    const int pm = p - step;
-    const bool stored = (pm >= 0 && pm < g.nplanes) || (pm < 0 ? !g.has_lo_wall : !g.has_hi_wall);
-    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colx * Es;
-    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
-#pragma unroll
-    for (int k = 0; k < JMAX; ++k) {
-      prev[k] = 0.0;
-      if (active && grp < JG && k < nloc) {
-        if (stored)
-          prev[k] = ldg(Is + (int64_t)(pm + g.plane_off) * g.plane_stride + colx * Es + e0 + k * nb);
-        else
-          prev[k] = ghost_value(g, Iin, mregion, face, base, slot, j0 + k, b);
-      }
-    }
-  }
-
-  int buf = 0;
-  int p = pfirst;
-  for (int i = 0; i < np; ++i, p += step) {
-    const int st = i % S;
-    const int64_t cell = colx + (int64_t)p * g.ncross;
-    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colx * Es;
-    const double *sp = stage0 + st * sd;
-    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
-    double acc = 0.0;
-    if (active && grp < JG) {
-      const double I0 = rows_tma ? sp[oI0 + t * nb + b] : ldg(A.I0c + cell * nb + b);
-      const double dtb = dt * (rows_tma ? sp[oBe + t * nb + b] : ldg(A.beta + cell * nb + b));
-      const double *so = sp + own_idx * Es + e0;
-      const double *sxu = sp + up_idx * Es + e0;
-      const double *syu = sp + oY + t * Es + e0;
-      double *op = Os + base + e0;
-      if (!xghost && !yghost && nloc == JMAX) {
-#pragma unroll
-        for (int k = 0; k < JMAX; ++k) {
-          const double Ic = so[k * nb];
-          const double In = bte_update<DIM>(Ic, sxu[k * nb], DIM == 3 ? syu[k * nb] : 0.0, prev[k], cq + 4 * k, v,
-                                            I0, dtb);
-          __stcs(op + k * nb, In);
-          acc = fma(cq[4 * k + 3], I0 - In, acc);
-          prev[k] = Ic;
-        }
-      } else {
-        const int64_t mg = g.m0 + p;
-#pragma unroll
-        for (int k = 0; k < JMAX; ++k) {
-          if (k < nloc) {
-            const int j = j0 + k;
-            const double Ic = so[k * nb];
-            double xu, yu = 0.0;
-            if (!xghost) {
-              xu = sxu[k * nb];
-            } else {
-              const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
-              xu = ghost_value(g, Iin, xregion, face, base, slot, j, b);
-            }
-            if (DIM == 3) {
-              if (!yghost) {
-                yu = syu[k * nb];
-              } else {
-                const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
-                yu = ghost_value(g, Iin, yregion, face, base, slot, j, b);
-              }
-            }
-            const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cq + 4 * k, v, I0, dtb);
-            __stcs(op + k * nb, In);
-            acc = fma(cq[4 * k + 3], I0 - In, acc);
-            prev[k] = Ic;
-          }
-        }
-      }
-    }
-    double *rb = red + buf * TX * tpc;
-    if (tid < TX * tpc) rb[tid] = acc;
-    __syncthreads();
-    if (tid == 0 && i + S < np) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(i + S, st);
-    }
-    if (active && grp == 0) {
-      double s = 0.0;
-      for (int q = 0; q < JG; ++q) s += rb[t * tpc + q * nb + b];
-      A.Dpart[(cell * g.nslot + slot) * nb + b] = s;
-    }
-    buf ^= 1;
-  }
 }
 
 // thread shape: JG groups of nb threads, jpt directions per thread
@@ -898,10 +512,22 @@ static void sweep_shape(int nb, int nj, int target, int *jpt, int *JG) {
   *JG = jg;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
+// the launchers run on every step, the attribute only has to grow
+static cudaError_t smem_attr(const void *fn, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void *, size_t> done;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &cur = done[fn];
+  if (smem <= cur || smem <= 48 * 1024) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
 template <int DIM>
-static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fused) {
+static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
   SweepArgs a = a0;
-  *fused = 0;
   const Geometry &g = a.g;
   int jpt, JG;
   sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 448, &jpt, &JG);
@@ -916,48 +542,6 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   dim3 grid(a.ncols > 0 ? a.ncols : g.ncross, a.nslots > 0 ? a.nslots : g.nslot, nseg);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   const bool tma = a.use_tma && (g.Es % 2 == 0);
-  // small blocks: several columns per CTA (k_sweep_tmx)
-  const bool full_cols = (a.ncols <= 0 || a.ncols == g.ncross) && a.col0 == 0;
-  if (tma && full_cols && !a.fuse_newton && a.tx_override > 1 && g.nj <= 16) {
-    int jp = g.nj, jgm = 1;                     // all directions of the octant in one thread
-    const int tpc = jgm * g.nb;
-    int TX = std::max(1, std::min(g.nx, 448 / std::max(1, tpc)));
-    if (a.tx_override > 1) TX = std::min(g.nx, a.tx_override);
-    const int thr = ((TX * tpc) + 31) / 32 * 32;
-    if (thr <= 1024) {
-      a.jpt = jp;
-      a.jg = jgm;
-      a.tx = TX;
-      const int64_t sdx = ((int64_t)(TX + 1) * g.Es + (DIM == 3 ? (int64_t)TX * g.Es : 0) + 2 * (int64_t)TX * g.nb + 15) /
-                          16 * 16;
-      const size_t fixedx = 128 + (4 * (size_t)g.nj + 2 * (size_t)TX * tpc) * sizeof(double);
-      const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;
-      int S = (int)((budget > fixedx ? budget - fixedx : 0) / (sdx * sizeof(double)));
-      S = std::max(2, std::min(4, S));
-      if (a.stages_override > 0) S = std::min(16, a.stages_override);
-      a.stages = S;
-      a.stage_doubles = sdx;
-      const size_t smem = fixedx + (size_t)S * sdx * sizeof(double);
-      const int ngx = (g.nx + TX - 1) / TX;
-      dim3 gridx(ngx * (DIM == 3 ? g.ny : 1), a.nslots > 0 ? a.nslots : g.nslot, nseg);
-      const int jc = jp <= 1 ? 1 : jp <= 2 ? 2 : jp <= 4 ? 4 : jp <= 5 ? 5 : jp <= 8 ? 8 : 16;
-      switch (jc) {
-#define BTE_TMX(N)                                                                                  \
-  case N:                                                                                           \
-    cudaFuncSetAttribute(k_sweep_tmx<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_sweep_tmx<DIM, N><<<gridx, thr, smem, s>>>(a);                                                \
-    break;
-        BTE_TMX(1)
-        BTE_TMX(2)
-        BTE_TMX(4)
-        BTE_TMX(5)
-        BTE_TMX(8)
-        BTE_TMX(16)
-#undef BTE_TMX
-      }
-      return cudaGetLastError();
-    }
-  }
   // blocks under 384 doubles: the direct-load kernel keeps more cells in
   // flight than a per-cell TMA ring (measured: demo 0.089 vs 0.110 ms)
   if (tma && g.E >= 384) {
@@ -971,30 +555,16 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
     a.stages = S;
     a.stage_doubles = stage_d;
     a.jg = JG;
-    size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
-    const int tthreads0 = (threads + 31) / 32 * 32;
-    if (a.fuse_newton) {  // the Newton tail reuses the stage ring for its tables
-      const size_t need = fixed + (2 * (size_t)gl_stride(g.nb) * kNGL + (size_t)(tthreads0 / 32) * newton_scratch(a.nw.m, g.nb)) * sizeof(double) +
-                          4 * (size_t)(a.nw.m.imax + 1) * sizeof(int);
-      smem = std::max(smem, need);
-      *fused = 1;
-    }
+    const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    // spare threads for the side jobs (reducers + issuer) unless BTE_SPARE=0
-    const bool spare = !(getenv("BTE_SPARE") && atoi(getenv("BTE_SPARE")) == 0) && !a.fuse_newton;
-    const int tthreads = ((spare ? threads + g.nb + 1 : threads) + 31) / 32 * 32;
-#define BTE_LAUNCH(N, NB)                                                                        \
-  {                                                                                              \
-    if (a.fuse_newton) {                                                                         \
-      cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB, true>,                                        \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
-      k_sweep_tma<DIM, N, NB, true><<<grid, tthreads, smem, s>>>(a);                             \
-    } else {                                                                                     \
-      cudaFuncSetAttribute(k_sweep_tma<DIM, N, NB, false>,                                       \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
-      k_sweep_tma<DIM, N, NB, false><<<grid, tthreads, smem, s>>>(a);                            \
-    }                                                                                            \
-    break;                                                                                       \
+    // spare threads for the side jobs (reducers + issuer) unless disabled at create
+    const int tthreads = ((a.no_spare ? threads : threads + g.nb + 1) + 31) / 32 * 32;
+    cudaError_t e;
+#define BTE_LAUNCH(N, NB)                                                       \
+  {                                                                             \
+    if ((e = smem_attr((const void *)k_sweep_tma<DIM, N, NB>, smem))) return e; \
+    k_sweep_tma<DIM, N, NB><<<grid, tthreads, smem, s>>>(a);                    \
+    break;                                                                      \
   }
     if (g.nb == 40 && jcase == 5) {
       switch (0) { default: BTE_LAUNCH(5, 40) }
@@ -1016,42 +586,13 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
 #undef BTE_LAUNCH
     return cudaGetLastError();
   }
-  a.fuse_newton = 0;
-  // k_sweep_ca (cp.async prefetch of cell i+1) only on request (BTE_CA=1):
-  // measured slower on the demo shape (0.118 vs 0.095 ms), DESIGN.md section 7
-  if (getenv("BTE_CA") && atoi(getenv("BTE_CA")) == 1) {
-    const int W = (DIM == 3 ? 3 : 2) * jcase + 2;
-    const size_t smemc = (4 * (size_t)g.nj + 2 * (size_t)threads + 2 * (size_t)W * threads) * sizeof(double);
-    if (smemc <= 227 * 1024) {
-      switch (jcase) {
-#define BTE_CCASE(N)                                                                      \
-  case N:                                                                                 \
-    if (smemc > 48 * 1024)                                                                \
-      cudaFuncSetAttribute(k_sweep_ca<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smemc);                                                   \
-    k_sweep_ca<DIM, N><<<grid, threads, smemc, s>>>(a);                                   \
-    return cudaGetLastError();
-        BTE_CCASE(1)
-        BTE_CCASE(2)
-        BTE_CCASE(4)
-        BTE_CCASE(5)
-        BTE_CCASE(8)
-        BTE_CCASE(10)
-        BTE_CCASE(16)
-#undef BTE_CCASE
-        default:
-          break;
-      }
-    }
-  }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
+  cudaError_t e;
   switch (jcase) {
-#define BTE_CASE(N)                                                                       \
-  case N:                                                                                 \
-    if (smem > 48 * 1024)                                                                 \
-      cudaFuncSetAttribute(k_sweep<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                           (int)smem);                                                    \
-    k_sweep<DIM, N><<<grid, threads, smem, s>>>(a);                                       \
+#define BTE_CASE(N)                                                       \
+  case N:                                                                 \
+    if ((e = smem_attr((const void *)k_sweep<DIM, N>, smem))) return e;   \
+    k_sweep<DIM, N><<<grid, threads, smem, s>>>(a);                       \
     break;
     BTE_CASE(1)
     BTE_CASE(2)
@@ -1067,8 +608,15 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s, int *fu
   return cudaGetLastError();
 }
 
-cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s, int *fused) {
-  return a.g.dim == 3 ? launch_sweep_dim<3>(a, s, fused) : launch_sweep_dim<2>(a, s, fused);
+const char *sweep_kernel_name(const SweepArgs &a) {
+  const Geometry &g = a.g;
+  const bool tma = a.use_tma && (g.Es % 2 == 0) && g.E >= 384;
+  if (g.dim == 3) return tma ? "k_sweep_tma<3>" : "k_sweep<3>";
+  return tma ? "k_sweep_tma<2>" : "k_sweep<2>";
+}
+
+cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s) {
+  return a.g.dim == 3 ? launch_sweep_dim<3>(a, s) : launch_sweep_dim<2>(a, s);
 }
 
 // ---------------------------------------------------------------- diffuse ghosts
@@ -1785,12 +1333,12 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const Newto
 cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s) {
   if (a.nb > kMaxBands) return cudaErrorInvalidValue;
   if (a.ncells == 0) return cudaSuccess;
-  if (a.m.mode != 0 && a.m.uniform && !(getenv("BTE_SC_DIRECT") && atoi(getenv("BTE_SC_DIRECT")))) {
+  if (a.m.mode != 0 && a.m.uniform && !a.sc_direct) {
     const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
     const int64_t nblk = std::min<int64_t>(need, 148 * 4);
     const size_t smem = ((size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * (newton_scratch(a.m, a.nb) + a.nb)) *
                         sizeof(double);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton_scu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = smem_attr((const void *)k_newton_scu, smem)) return e;
     k_newton_scu<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
     return cudaGetLastError();
   }
@@ -1809,14 +1357,13 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
                       4 * (size_t)(a.m.imax + 1) * sizeof(int);
   const int minb = a.minb > 0 ? a.minb : BTE_NEWTON_MINB;
   if (a.Sall) {  // band partition (bte_create_band)
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_newton<BTE_NEWTON_MINB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaError_t e = smem_attr((const void *)k_newton<BTE_NEWTON_MINB, true>, smem)) return e;
     k_newton<BTE_NEWTON_MINB, true><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
     return cudaGetLastError();
   }
 #define BTE_NL(M)                                                                                   \
   case M:                                                                                           \
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_newton<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (cudaError_t e = smem_attr((const void *)k_newton<M, false>, smem)) return e;              \
     k_newton<M, false><<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);                          \
     break;
   switch (minb) {
@@ -2547,13 +2094,13 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
         dim3 grid((unsigned)((a.u.ncells + a.chunk - 1) / a.chunk), g.nslot);
 #define BTE_UTMA_(N, KK, B, J)                                                                          \
   {                                                                                                     \
-    cudaFuncSetAttribute(k_usweep_tma<N, KK, B, J>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (cudaError_t e = smem_attr((const void *)k_usweep_tma<N, KK, B, J>, smem)) return e;              \
     k_usweep_tma<N, KK, B, J><<<grid, threads, smem, s>>>(a);                                           \
     return cudaGetLastError();                                                                          \
   }
 #define BTE_UTMA(N, KK) \
   if (jpt == N && a.u.K == KK) BTE_UTMA_(N, KK, 0, 0)
-        if (g.nb == 40 && g.nj == 50 && !getenv("BTE_UGENERIC")) {
+        if (g.nb == 40 && g.nj == 50 && !a.generic) {
           if (jpt == 1 && JG == 50 && threads == 1000) {
             if (a.u.K == 3) BTE_UTMA_(1, 3, 40, 50)
             if (a.u.K == 4) BTE_UTMA_(1, 4, 40, 50)
@@ -2584,9 +2131,7 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   switch (jcase) {
 #define BTE_UCASE(N)                                                                    \
   case N:                                                                               \
-    if (smem > 48 * 1024)                                                               \
-      cudaFuncSetAttribute(k_usweep<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                           (int)smem);                                                  \
+    if (cudaError_t e = smem_attr((const void *)k_usweep<N>, smem)) return e;          \
     k_usweep<N><<<grid, threads, smem, s>>>(a);                                         \
     break;
     BTE_UCASE(1)

@@ -18,6 +18,8 @@ struct Nccl {
   decltype(&ncclGroupEnd) gend = nullptr;
   decltype(&ncclCommDestroy) destroy = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
+  decltype(&ncclCommCount) count = nullptr;
+  decltype(&ncclCommUserRank) userrank = nullptr;
 };
 
 Nccl &lib(std::string *err) {
@@ -41,7 +43,10 @@ Nccl &lib(std::string *err) {
   n.gend = (decltype(n.gend))dlsym(n.h, "ncclGroupEnd");
   n.destroy = (decltype(n.destroy))dlsym(n.h, "ncclCommDestroy");
   n.errstr = (decltype(n.errstr))dlsym(n.h, "ncclGetErrorString");
-  if (!n.init || !n.send || !n.recv || !n.allgather || !n.gstart || !n.gend || !n.destroy || !n.errstr) {
+  n.count = (decltype(n.count))dlsym(n.h, "ncclCommCount");
+  n.userrank = (decltype(n.userrank))dlsym(n.h, "ncclCommUserRank");
+  if (!n.init || !n.send || !n.recv || !n.allgather || !n.gstart || !n.gend || !n.destroy || !n.errstr || !n.count ||
+      !n.userrank) {
     if (err) *err = "libnccl is missing symbols (send/recv/allgather/group)";
     dlclose(n.h);
     n.h = nullptr;
@@ -78,6 +83,13 @@ int nccl_shim_recv(void *comm, double *buf, size_t count, int peer, cudaStream_t
 int nccl_shim_allgather(void *comm, const double *send, double *recv, size_t count, cudaStream_t s,
                         std::string *err) {
   return check(lib(err).allgather(send, recv, count, ncclFloat64, (ncclComm_t)comm, s), err);
+}
+
+int nccl_shim_comm_info(void *comm, int *nranks, int *rank, std::string *err) {
+  Nccl &n = lib(err);
+  if (!n.h) return 1;
+  if (check(n.count((ncclComm_t)comm, nranks), err)) return 1;
+  return check(n.userrank((ncclComm_t)comm, rank), err);
 }
 
 int nccl_shim_group_start(std::string *err) { return check(lib(err).gstart(), err); }

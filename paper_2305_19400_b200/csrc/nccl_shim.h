@@ -14,6 +14,8 @@ int nccl_shim_recv(void *comm, double *buf, size_t count, int peer, cudaStream_t
 // in-place when send == recv + rank*count (band-partition partials)
 int nccl_shim_allgather(void *comm, const double *send, double *recv, size_t count, cudaStream_t s,
                         std::string *err);
+// the communicator's own view: ncclCommCount / ncclCommUserRank
+int nccl_shim_comm_info(void *comm, int *nranks, int *rank, std::string *err);
 int nccl_shim_group_start(std::string *err);
 int nccl_shim_group_end(std::string *err);
 void nccl_shim_destroy(void *comm);

@@ -15,6 +15,7 @@ import pytest
 
 import bte_inputs as bi
 import oracle
+from paper_2305_19400_b200.bte import DEBUG_SKIP_EXCHANGE
 
 pytestmark = pytest.mark.gpu
 
@@ -36,6 +37,14 @@ def _cmp(Ig, Tg, Io, To):
     rel = float(np.max(np.abs(Ig - Io) / np.abs(Io)))
     dT = float(np.max(np.abs(Tg - To)))
     return rel, dT
+
+
+def _assert_oracle(p, I, T, nsteps, Ig, Tg):
+    """A multi-rank (gathered) result against the oracle's single-domain run
+    of the same problem and start (north_star tolerance)."""
+    Io, To, _, _ = oracle.Oracle(p).run(I, T, nsteps)
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
 
 
 def _run_both(Solver, p, nsteps, start="random", solve_T=False):
@@ -207,6 +216,26 @@ def test_full_size_config3_sampled(Solver):
     n = p.mesh.nx
     samples = [(0, 0, 0), (n - 1, n - 1, n - 1), (31, 17, 0), (5, n - 1, 40), (32, 32, 32), (n - 1, 0, n - 2)]
     rel, dT = _sampled_full_size(Solver, p, 2, samples)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_full_size_config3_sampled_5_steps(Solver):
+    """BASELINE configs[2] at full size, 5 steps, 36 sampled cells (I and T):
+    every wall and edge, and the planes on both sides of each z-segment
+    boundary of the sweep (segments restart their march-axis upwind value)."""
+    p = bi.config3()
+    n = p.mesh.nx
+    rng = np.random.Generator(np.random.PCG64(2305194003))
+    zs = [0, 1, 15, 16, 17, 31, 32, 33, 47, 48, 62, 63]
+    samples = []
+    for i, z in enumerate(zs):
+        samples.append((int(rng.integers(0, n)), int(rng.integers(0, n)), z))
+        edge = [(0, int(rng.integers(0, n))), (n - 1, int(rng.integers(0, n))), (int(rng.integers(0, n)), 0),
+                (int(rng.integers(0, n)), n - 1)][i % 4]
+        samples.append((edge[0], edge[1], z))
+        samples.append(((0, n - 1)[i % 2], (n - 1, 0)[(i // 2) % 2], z))  # x/y corners (two walls)
+    assert len(samples) >= 32
+    rel, dT = _sampled_full_size(Solver, p, 5, samples)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
 
 
@@ -445,6 +474,7 @@ def test_local_slab_group_matches_single_domain(Solver, case, P, overlap, monkey
     o = oracle.Oracle(p)
     I, T = o.random_state()
     nsteps = 7
+    Io, To, _, _ = o.run(I, T, nsteps)
     with Solver.from_problem(p) as sv:
         sv.set_state(I, T)
         sv.step(nsteps)
@@ -467,6 +497,8 @@ def test_local_slab_group_matches_single_domain(Solver, case, P, overlap, monkey
     finally:
         for sv in group:
             sv.close()
+    rel, dT = _cmp(Ig, Tg, Io, To)  # the multi-rank result against the oracle (north_star tolerance)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
     assert np.array_equal(Ig, I1) and np.array_equal(Tg, T1)
 
 
@@ -479,11 +511,11 @@ def test_local_slab_group_mutation_skip_halo(Solver, monkeypatch):
         sv.set_state(I, T)
         sv.step(4)
         I1 = sv.intensity()
-    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")
     group = []
     try:
         for r in range(2):
             sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=2)
+            sv.set_debug(DEBUG_SKIP_EXCHANGE, 1)
             for reg in range(6):
                 bc = p.bcs[reg]
                 sv.set_wall(reg, bc)
@@ -523,14 +555,14 @@ def test_parity_nonuniform_band_grid(Solver):
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
 
 
-@pytest.mark.parametrize("variant", ["BTE_FUSE", "BTE_CHUNKS", "BTE_SWEEP_PLAIN", "BTE_TX", "BTE_CA"])
+@pytest.mark.parametrize("variant", ["BTE_SWEEP_PLAIN", "BTE_SPARE"])
 def test_parity_kernel_variants(Solver, variant, monkeypatch):
-    """The A/B kernel variants (sweep-tail Newton, chunked two-stream pipeline,
-    direct-load sweep, multi-column TMA sweep) reach the same results."""
+    """The A/B kernel variants (direct-load sweep for large blocks, side jobs
+    on the compute threads) reach the same results."""
     if variant == "BTE_SWEEP_PLAIN":
         monkeypatch.setenv("BTE_SWEEP", "plain")
     else:
-        monkeypatch.setenv(variant, {"BTE_CHUNKS": "3", "BTE_TX": "4", "BTE_CA": "1"}.get(variant, "1"))
+        monkeypatch.setenv("BTE_SPARE", "0")
     for p, n in ((bi.config2(n=16), 8), (bi.config3(n=8), 4)):
         if p.mesh.dim == 3:
             p.mesh = bi.Mesh(3, 9, 7, 6, 1e-6, 1e-6, 1e-6)
@@ -600,8 +632,8 @@ def test_band_group_mutation_skip_exchange(Solver, monkeypatch):
     o = oracle.Oracle(p)
     I, T = o.random_state()
     Io, To, _, _ = o.run(I, T, 3)
-    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")
     group = _band_group(Solver, p, 2, I, T)
+    group[0].set_debug(DEBUG_SKIP_EXCHANGE, 1)
     try:
         Solver.group_step(group, 3)
         Tg = group[0].temperature()
@@ -705,6 +737,8 @@ def test_slot_rotation_groups(Solver, monkeypatch):
         out[rot] = slab + band
     for x, y in zip(out["0"], out["1"]):
         assert np.array_equal(x, y)
+    _assert_oracle(p, I, T, 5, out["1"][0], out["1"][1])  # rotated slab group
+    _assert_oracle(p, I, T, 5, out["1"][2], out["1"][3])  # rotated band group
 
 
 # ----------------------------------------------------------------- partially specular walls (reading R-i)
@@ -791,6 +825,7 @@ def test_partial_wall_rotation_and_groups(Solver, monkeypatch):
     finally:
         for sv in group:
             sv.close()
+    _assert_oracle(p, I, T, 5, Ig, Tg)
     assert np.array_equal(Ig, res["0"][0]) and np.array_equal(Tg, res["0"][1])
     bgroup = _band_group(Solver, p, 2, I, T)
     try:
@@ -800,6 +835,7 @@ def test_partial_wall_rotation_and_groups(Solver, monkeypatch):
     finally:
         for sv in bgroup:
             sv.close()
+    _assert_oracle(p, I, T, 5, Ib, Tb)
     assert np.max(np.abs(Tb - res["0"][1])) <= 1e-10 and np.max(np.abs(Ib / res["0"][0] - 1)) <= 1e-12
 
 
@@ -869,6 +905,7 @@ def test_sc_tau_slab_group_and_errors(Solver):
     finally:
         for sv in group:
             sv.close()
+    _assert_oracle(p, I, T, 5, Ig, Tg)
     assert np.array_equal(Ig, I1) and np.array_equal(Tg, T1)
     bg = _band_group(Solver, p, 2, I, T)
     try:
@@ -937,6 +974,7 @@ def test_semi_groups_rotation_energy_errors(Solver, monkeypatch):
     finally:
         for sv in group:
             sv.close()
+    _assert_oracle(p, I, T, 5, Ig, Tg)
     assert np.array_equal(Ig, res["0"][0]) and np.array_equal(Tg, res["0"][1])
     # closed box at 40x the explicit bound: conservative and positive
     b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])

@@ -8,6 +8,7 @@ import pytest
 
 import bte_inputs as bi
 import oracle
+from paper_2305_19400_b200.bte import DEBUG_SKIP_EXCHANGE
 
 pytestmark = pytest.mark.gpu
 
@@ -296,8 +297,8 @@ def test_umesh_partition_semi_and_mutation(Solver, monkeypatch):
             s.close()
     rel, dT = _cmp(Ig, Tg, Io, To)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
-    monkeypatch.setenv("BTE_MUTATE_SKIP_HALO", "1")  # without the halo refresh the result must differ
     group = _part_group(Solver, p, 3, I, T, step_mode=1)
+    group[0].set_debug(DEBUG_SKIP_EXCHANGE, 1)  # without the halo refresh the result must differ
     try:
         Solver.group_step(group, 4)
         Ig2 = np.concatenate([s.intensity() for s in group])
@@ -305,3 +306,43 @@ def test_umesh_partition_semi_and_mutation(Solver, monkeypatch):
         for s in group:
             s.close()
     assert np.max(np.abs(Ig2 / Io - 1)) > 1e3 * REL_I
+
+
+def test_umesh_full_size_u3_sampled(Solver):
+    """u3 at full size (196,608 tetrahedra x 400 x 40, the bench workload),
+    device random start, 3 steps, against the oracle at sampled cells: each
+    sample's 3-step domain of dependence (cubes within 3, plus one layer) is
+    cut out as a mesh of its own and run by the oracle with the same global
+    random start (centroids from the whole box, noise from global indices)."""
+    p = bi.config_u3()
+    n = (32, 32, 32)
+    k = 3
+    samples = [(0, 0, 0, 0), (31, 31, 31, 5), (16, 9, 0, 3), (4, 31, 20, 1), (15, 16, 17, 2), (31, 0, 30, 4),
+               (7, 22, 11, 5), (0, 15, 31, 0)]
+    gids = [6 * (x + 32 * (y + 32 * z)) + t for (x, y, z, t) in samples]
+    with Solver.from_problem(p) as sv:
+        sv.init_random(p.seed, bi.random_phases(p.seed), p.T_init, 20.0, 0.05)
+        sv.step(k)
+        Tg = sv.temperature()
+        Is = sv.intensity_cells(gids)
+    m = p.mesh
+    lo = m.verts.min(axis=0)
+    L = m.verts.max(axis=0) - lo
+    worst_rel, worst_T = 0.0, 0.0
+    for si, (x, y, z, t) in enumerate(samples):
+        box = [(max(0, c - k - 1), min(32, c + k + 2)) for c in (x, y, z)]
+        sub, gcells = bi.umesh_tet_subbox(m, n, box)
+        bcs = []
+        for r in range(6):
+            a = r // 2
+            on_wall = box[a][0] == 0 if r % 2 == 0 else box[a][1] == n[a]
+            bcs.append(p.bcs[r] if on_wall else bi.WallBC(bi.BC_SPECULAR))
+        sp = bi.Problem(p.name + f"_sub{si}", sub, p.dirs, p.bands, p.dt, p.T_init, bcs, p.nsteps, p.seed)
+        o = oracle.Oracle(sp)
+        T0 = bi.random_temperature_umesh(sub, p.seed, p.T_init, 20.0, lo=lo, L=L)
+        I0 = o.equilibrium(T0) * bi.intensity_noise_factor_cells(p.seed, gcells, p.dirs.nd, p.bands.nb, 0.05)
+        Io, To, _, _ = o.run(I0, T0, k)
+        lc = int(np.nonzero(gcells == gids[si])[0][0])
+        worst_T = max(worst_T, abs(Tg[gids[si]] - To[lc]))
+        worst_rel = max(worst_rel, float(np.max(np.abs(Is[si] - Io[lc]) / np.abs(Io[lc]))))
+    assert worst_rel <= REL_I and worst_T <= ABS_T, (worst_rel, worst_T)
