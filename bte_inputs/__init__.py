@@ -154,6 +154,9 @@ class Problem:
     seed: int = 0
     tau_mode: int = 0  # 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k)
     semi: int = 0  # 1: semi-implicit step (explicit advection, implicit relaxation; reading R-l)
+    implicit: int = 0  # 1: implicit step by source iteration (reading R-n)
+    imp_max_iter: int = 0  # R-n: iterations per step (exactly this many when imp_tol == 0)
+    imp_tol: float = 0.0  # R-n: stop early when max_c |T^{k+1} - T^k| / T^k <= imp_tol
 
     @property
     def dof(self) -> int:
@@ -598,7 +601,8 @@ def subproblem(problem: "Problem", box, open_kind: int = BC_SPECULAR) -> "Proble
             Tw = np.ascontiguousarray(Tw)
         bcs.append(WallBC(bc.kind, Tw, bc.T_uniform))
     return Problem(problem.name + f"_sub{box}", sub, problem.dirs, problem.bands, problem.dt,
-                   problem.T_init, bcs, problem.nsteps, problem.seed, problem.tau_mode, problem.semi)
+                   problem.T_init, bcs, problem.nsteps, problem.seed, problem.tau_mode, problem.semi,
+                   problem.implicit, problem.imp_max_iter, problem.imp_tol)
 
 
 # --------------------------------------------------------------------------

@@ -60,6 +60,9 @@ class _Problem(C.Structure):
         ("specularity", C.c_double * 6),
         ("tau_mode", C.c_int),
         ("semi", C.c_int),
+        ("implicit", C.c_int),
+        ("imp_max_iter", C.c_int),
+        ("imp_tol", C.c_double),
     ]
 
 
@@ -93,6 +96,8 @@ def lib():
                                                 C.POINTER(C.c_long), C.POINTER(C.c_int)]
         _lib.ora_run.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long,
                                  C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int)]
+        _lib.ora_run_implicit.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long,
+                                          C.c_void_p, C.POINTER(C.c_long), C.POINTER(C.c_long)]
         _lib.ora_solve_T.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.ora_n_faces.restype = C.c_long
         _lib.ora_n_faces.argtypes = [P, C.c_int]
@@ -172,6 +177,9 @@ class Oracle:
         st.nthreads = nthreads if nthreads else (os.cpu_count() or 1)
         st.tau_mode = int(getattr(problem, "tau_mode", 0))
         st.semi = int(getattr(problem, "semi", 0))
+        st.implicit = int(getattr(problem, "implicit", 0))
+        st.imp_max_iter = int(getattr(problem, "imp_max_iter", 0))
+        st.imp_tol = float(getattr(problem, "imp_tol", 0.0))
         self._st = st
         self.nc, self.nd, self.nb = m.ncells, d.nd, b.nb
         lib()
@@ -334,6 +342,16 @@ class Oracle:
             I0c, betac = _f64(I0c).copy(), _f64(betac).copy()
         es, ec = C.c_long(), C.c_long()
         it = C.c_int()
+        if self._st.implicit:  # reading R-n: implicit step by source iteration
+            if self.umesh:
+                raise OracleError(1, "implicit step: structured grids only")
+            iters = np.zeros(max(1, nsteps), dtype=np.int64)
+            st = lib().ora_run_implicit(C.byref(self._st), _ptr(I), _ptr(T), _ptr(I0c), _ptr(betac), nsteps,
+                                        iters.ctypes.data, C.byref(es), C.byref(ec))
+            if st:
+                raise OracleError(st, f"step {es.value} cell {ec.value}")
+            self.last_iters = iters[:nsteps].copy()
+            return I, T, I0c, betac
         if self.umesh:
             st = lib().ora_urun(C.byref(self._st), self._ug, _ptr(I), _ptr(T), _ptr(I0c), _ptr(betac), nsteps,
                                 C.byref(es), C.byref(ec), C.byref(it))

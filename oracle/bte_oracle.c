@@ -80,6 +80,9 @@ typedef struct {
   double specularity[6]; /* BC_PART: fraction p of specular reflection */
   int tau_mode;          /* 0: lagged tau (reading #15); 1: self-consistent tau(T^{n+1}) (reading R-k) */
   int semi;              /* 1: semi-implicit step, implicit relaxation (reading R-l) */
+  int implicit;          /* 1: implicit step solved by source iteration (reading R-n) */
+  int imp_max_iter;      /* R-n: iterations per step (the count when imp_tol == 0) */
+  double imp_tol;        /* R-n: stop when max_c |T^{k+1} - T^k| <= imp_tol * T^k (0: fixed count) */
 } ora_problem;
 
 /* ---------------------------------------------------------------- quadrature */
@@ -686,6 +689,236 @@ int ora_run(const ora_problem *p, double *I, double *T, double *I0c, double *bet
   free(J);
   free(D);
   free(Z);
+  bc_free(&bd);
+  return st;
+}
+
+/* ---------------------------------------------------------- implicit step (R-n)
+ *
+ * "solvers take 10-20 iterations (depending on the time
+ * step size) to attain 3-4 orders of convergence within each time step".
+ * Reading R-n: the backward-Euler step of Eq. 4 in the finite-volume form of
+ * Eq. 5, every term at the new time level,
+ *   I' - I^n = dt [ beta_{c,b} (I0_b(T') - I') - v_b sum_a (|s_a|/D_a)(I' - I'_up,a) ],
+ * beta = beta(T^n) (lagged as #15), ghosts of I' (Eq. 6), and T' from the
+ * scattering balance (#2) of I'.  Solved by source iteration, k = 0, 1, ...
+ * from I^0 = I^n, T^0 = T^n:
+ *   (a) wall ghosts from I^k (diffuse tables, specular partners);
+ *   (b) for every direction, a transport sweep in upwind order -- each cell
+ *       after its upwind neighbours, so I'_up is this sweep's own value
+ *       (exact inversion of the upwind operator for the source I0(T^k)):
+ *         I^{k+1} = I^n + [dt beta (I0c^k - I^n) + sum_a kk_a (I^{k+1}_up,a - I^n)]
+ *                         / (1 + dt beta + sum_a kk_a),     kk_a = dt v_b |s_a| / D_a,
+ *       axis terms in x, y, z order (the deviation form keeps a uniform
+ *       equilibrium exact, like #19);
+ *   (c) D = sum_d w_d (I0c^k - I^{k+1}) (step-3 order), Newton for T^{k+1}
+ *       from T^k with weights beta/v_b (the step's beta), I0c^{k+1} = I0(T^{k+1});
+ * until k = imp_max_iter, or earlier when imp_tol > 0 and both inputs of the
+ * last sweep had settled: max_c |T^{k+1} - T^k| <= imp_tol T^k and the wall
+ * data of (a) changed by at most imp_tol relative from the previous
+ * iteration's (the outgoing intensities of specular/partial wall cells, the
+ * diffuse ghost tables; at k = 0 there is no previous, so no early stop while
+ * such walls exist).  The step ends with I^{n+1} = I^K, T^{n+1} = T^K,
+ * I0c = I0(T^K), betac = beta(T^n). */
+
+/* largest relative change of the wall data (a) between iterates Ik and Ikm1:
+ * outgoing intensities of the cells on specular / partial walls, and the
+ * diffuse tables gd vs gdm1 (diffuse / partial walls) */
+static double wall_change(const ora_problem *p, const ora_bcdata *bd, const double *Ik, const double *Ikm1,
+                          double *const *gdm1) {
+  int nreg = p->dim == 3 ? 6 : 4;
+  int nd = p->nd, nb = p->nb;
+  double m = 0.0;
+  for (int r = 0; r < nreg; r++) {
+    int k = p->bc_kind[r];
+    int a = r / 2;
+    double sg = (r & 1) ? 1.0 : -1.0;
+    long nf = ora_n_faces(p, r);
+    if (k == BC_SPEC || k == BC_PART) {
+      for (long f = 0; f < nf; f++) {
+        long x, y, z;
+        if (a == 0) {
+          y = f % p->ny; z = f / p->ny; x = (r & 1) ? p->nx - 1 : 0;
+        } else if (a == 1) {
+          x = f % p->nx; z = f / p->nx; y = (r & 1) ? p->ny - 1 : 0;
+        } else {
+          x = f % p->nx; y = f / p->nx; z = (r & 1) ? p->nz - 1 : 0;
+        }
+        long c = x + p->nx * (y + p->ny * z);
+        for (int d = 0; d < nd; d++) {
+          if (!(sg * p->s[3 * d + a] > 0.0)) continue; /* outgoing through this wall */
+          for (int b = 0; b < nb; b++) {
+            long e = (c * nd + d) * nb + b;
+            double rel = fabs(Ik[e] - Ikm1[e]) / fabs(Ikm1[e]);
+            if (rel > m) m = rel;
+          }
+        }
+      }
+    }
+    if (k == BC_DIFF || k == BC_PART) {
+      for (long e = 0; e < nf * nb; e++) {
+        double rel = fabs(bd->gdiff[r][e] - gdm1[r][e]) / fabs(gdm1[r][e]);
+        if (rel > m) m = rel;
+      }
+    }
+  }
+  return m;
+}
+
+/* one upwind-ordered transport sweep (b) for all directions */
+static void implicit_sweep(const ora_problem *p, const ora_bcdata *bd, const double *In, const double *Ik,
+                           const double *I0c, const double *beta, double *Inew) {
+  long nx = p->nx, ny = p->ny, nz = p->nz;
+  int nd = p->nd, nb = p->nb;
+  int na = p->dim == 3 ? 3 : 2;
+  long n[3] = {nx, ny, nz};
+  long stride[3] = {1, nx, nx * ny};
+#pragma omp parallel for schedule(dynamic, 1) num_threads(p->nthreads > 0 ? p->nthreads : 1)
+  for (int d = 0; d < nd; d++) {
+    const double *sd = p->s + 3 * d;
+    /* per axis: march from the upwind side (any order where s_a == 0) */
+    long lo[3], st[3];
+    for (int a = 0; a < 3; a++) {
+      int neg = a < na && sd[a] < 0.0;
+      lo[a] = neg ? n[a] - 1 : 0;
+      st[a] = neg ? -1 : 1;
+    }
+    for (long kz = 0; kz < nz; kz++)
+      for (long ky = 0; ky < ny; ky++)
+        for (long kx = 0; kx < nx; kx++) {
+          long ix[3] = {lo[0] + st[0] * kx, lo[1] + st[1] * ky, lo[2] + st[2] * kz};
+          long c = ix[0] + nx * (ix[1] + ny * ix[2]);
+          for (int b = 0; b < nb; b++) {
+            double Ic = In[(c * nd + d) * nb + b];
+            double db = p->dt * beta[c * nb + b];
+            double num = db * (I0c[c * nb + b] - Ic);
+            double den = 1.0 + db;
+            for (int a = 0; a < na; a++) {
+              double sa = sd[a];
+              if (sa == 0.0) continue;
+              double up;
+              if (sa > 0.0) {
+                if (ix[a] > 0)
+                  up = Inew[((c - stride[a]) * nd + d) * nb + b];
+                else
+                  up = ghost(p, bd, 2 * a, face_index(p, a, ix[0], ix[1], ix[2]), c, d, b, Ik);
+              } else {
+                if (ix[a] < n[a] - 1)
+                  up = Inew[((c + stride[a]) * nd + d) * nb + b];
+                else
+                  up = ghost(p, bd, 2 * a + 1, face_index(p, a, ix[0], ix[1], ix[2]), c, d, b, Ik);
+              }
+              double kk = p->dt * p->v[b] * (fabs(sa) / d_axis(p, a));
+              num += kk * (up - Ic);
+              den += kk;
+            }
+            Inew[(c * nd + d) * nb + b] = Ic + num / den;
+          }
+        }
+  }
+}
+
+/* nsteps implicit steps (R-n) in place; iters[s] = iterations of step s (optional) */
+int ora_run_implicit(const ora_problem *p, double *I, double *T, double *I0c, double *betac, long nsteps,
+                     long *iters, long *err_step, long *err_cell) {
+  long nc = p->nx * p->ny * p->nz;
+  int nb = p->nb;
+  size_t n = (size_t)nc * p->nd * nb;
+  if (p->imp_max_iter < 1 || p->tau_mode != 0 || p->semi) return ORA_EINVAL;
+  ora_bcdata bd;
+  int st = bc_prepare(p, &bd);
+  if (st) {
+    bc_free(&bd);
+    return st;
+  }
+  int nreg = p->dim == 3 ? 6 : 4;
+  double *In = (double *)malloc(sizeof(double) * n);
+  double *J = (double *)malloc(sizeof(double) * n);
+  double *Ip = (double *)malloc(sizeof(double) * n); /* I^{k-1}: the wall-data change */
+  double *D = (double *)malloc(sizeof(double) * nc * nb);
+  double *beta = (double *)malloc(sizeof(double) * nc * nb);
+  double *gdm1[6] = {NULL, NULL, NULL, NULL, NULL, NULL};
+  int ok = In && J && Ip && D && beta;
+  int walls = 0; /* walls whose data (a) come from the iterate */
+  for (int r = 0; r < nreg && ok; r++) {
+    if (p->bc_kind[r] != BC_ISO) walls = 1;
+    if (p->bc_kind[r] == BC_DIFF || p->bc_kind[r] == BC_PART) {
+      gdm1[r] = (double *)malloc(sizeof(double) * ora_n_faces(p, r) * nb);
+      ok = gdm1[r] != NULL;
+    }
+  }
+  if (!ok) {
+    free(In);
+    free(J);
+    free(Ip);
+    free(D);
+    free(beta);
+    for (int r = 0; r < 6; r++) free(gdm1[r]);
+    bc_free(&bd);
+    return ORA_ENOMEM;
+  }
+  if (err_step) *err_step = -1;
+  if (err_cell) *err_cell = -1;
+  for (long s = 0; s < nsteps && st == ORA_OK; s++) {
+    memcpy(In, I, sizeof(double) * n);
+    for (long c = 0; c < nc; c++)
+      for (int b = 0; b < nb; b++) beta[c * nb + b] = ora_beta(p, b, T[c]); /* beta(T^n) for the whole step */
+    long k = 0;
+    for (; k < p->imp_max_iter; k++) {
+      for (int r = 0; r < nreg; r++) /* (a) ghosts of I^k */
+        if (p->bc_kind[r] == BC_DIFF || p->bc_kind[r] == BC_PART) {
+          if (k > 0) memcpy(gdm1[r], bd.gdiff[r], sizeof(double) * ora_n_faces(p, r) * nb);
+          diffuse_table(p, r, I, bd.den[r], bd.gdiff[r]);
+        }
+      double gch = walls ? (k > 0 ? wall_change(p, &bd, I, Ip, gdm1) : INFINITY) : 0.0;
+      implicit_sweep(p, &bd, In, I, I0c, beta, J); /* (b) */
+      ora_reduce(p, J, I0c, D);                    /* (c) */
+      double dmax = 0.0;
+      long first_bad = -1;
+      int cst = ORA_OK;
+#pragma omp parallel for schedule(static) num_threads(p->nthreads > 0 ? p->nthreads : 1) reduction(max : dmax)
+      for (long c = 0; c < nc; c++) {
+        double Tnew;
+        int it;
+        int r = ora_newton(p, T[c], D + c * nb, I0c + c * nb, beta + c * nb, &Tnew, &it);
+        if (r != ORA_OK) {
+#pragma omp critical
+          {
+            if (first_bad < 0 || c < first_bad) {
+              first_bad = c;
+              cst = r;
+            }
+          }
+          continue;
+        }
+        double rel = fabs(Tnew - T[c]) / T[c];
+        if (rel > dmax) dmax = rel;
+        T[c] = Tnew;
+        for (int b = 0; b < nb; b++) I0c[c * nb + b] = ora_I0(p, b, Tnew, NULL);
+      }
+      memcpy(Ip, I, sizeof(double) * n);
+      memcpy(I, J, sizeof(double) * n);
+      if (cst != ORA_OK) {
+        st = cst;
+        if (err_step) *err_step = s;
+        if (err_cell) *err_cell = first_bad;
+        k++;
+        break;
+      }
+      if (p->imp_tol > 0.0 && dmax <= p->imp_tol && gch <= p->imp_tol) {
+        k++;
+        break;
+      }
+    }
+    if (iters) iters[s] = k;
+    memcpy(betac, beta, sizeof(double) * nc * nb);
+  }
+  free(In);
+  free(J);
+  free(Ip);
+  free(D);
+  free(beta);
+  for (int r = 0; r < 6; r++) free(gdm1[r]);
   bc_free(&bd);
   return st;
 }

@@ -936,3 +936,221 @@ def test_fig9_corner_source_heats_its_corner():
     assert np.unravel_index(np.argmax(F), F.shape) == (29, 0)
     assert F[29, 0] > F[29, 9] > 300.0 and F[0, 0] < F[29, 0]
     assert F.min() >= 300.0 - 1e-9
+
+
+# ----------------------------------------------------------------- implicit step by source iteration (reading R-n)
+
+def _imp(p, iters, tol=0.0):
+    p.implicit = 1
+    p.imp_max_iter = iters
+    p.imp_tol = tol
+    return p
+
+
+def _dense_implicit_step(p, I, T):
+    """The backward-Euler step of reading R-n for LINEAR tables, assembled face by
+    face from the definition (Eq. 5 face sum, upwind P:L150-157, ghosts Eq. 6 /
+    #11 evaluated at the new level) with the scattering balance #2 as the
+    temperature equation, and solved as ONE dense linear system in (I', T')
+    -- no iteration, no sweep order.  beta = beta(T^n) (constant-tau tables)."""
+    m, d, b = p.mesh, p.dirs, p.bands
+    nc, nd, nb = m.ncells, d.nd, b.nb
+    dims = [m.nx, m.ny, m.nz]
+    dx = [m.dx, m.dy, m.dz]
+    na = 3 if m.dim == 3 else 2
+    beta = b.beta_coef[:, 0]
+    W = d.w.sum()
+    nI = nc * nd * nb
+    A = np.zeros((nI + nc, nI + nc))
+    rhs = np.zeros(nI + nc)
+    idx = lambda c, dd, bb: (c * nd + dd) * nb + bb  # noqa: E731
+
+    def refl(a, dd):
+        t = d.s[dd].copy()
+        t[a] = -t[a]
+        hits = [k for k in range(nd) if np.array_equal(d.s[k], t)]
+        assert len(hits) == 1
+        return hits[0]
+
+    for c in range(nc):
+        ix = [c % m.nx, (c // m.nx) % m.ny, c // (m.nx * m.ny)]
+        for dd in range(nd):
+            for bb in range(nb):
+                r = idx(c, dd, bb)
+                v = b.v[bb]
+                A[r, r] += 1.0 / p.dt + beta[bb]
+                A[r, nI + c] -= beta[bb] * b.slope[bb]
+                rhs[r] = I[c, dd, bb] / p.dt + beta[bb] * (b.I_ref[bb] - b.slope[bb] * b.T_ref)
+                for a in range(na):
+                    sa = d.s[dd, a]
+                    if sa == 0.0:
+                        continue
+                    k = v * abs(sa) / dx[a]
+                    A[r, r] += k  # outflow face: s.n > 0, the cell's own value
+                    side = 0 if sa > 0 else 1  # inflow across the low (s_a > 0) or high face
+                    nb_ix = list(ix)
+                    nb_ix[a] += -1 if sa > 0 else 1
+                    if 0 <= nb_ix[a] < dims[a]:
+                        cn = nb_ix[0] + m.nx * (nb_ix[1] + m.ny * nb_ix[2])
+                        A[r, idx(cn, dd, bb)] -= k
+                        continue
+                    region = 2 * a + side
+                    bc = p.bcs[region]
+                    if bc.kind == bi.BC_ISOTHERMAL:
+                        assert bc.T_wall is None
+                        rhs[r] += k * (b.I_ref[bb] + b.slope[bb] * (bc.T_uniform - b.T_ref))
+                    elif bc.kind == bi.BC_SPECULAR:
+                        A[r, idx(c, refl(a, dd), bb)] -= k
+                    else:  # diffuse-adiabatic: outgoing through this wall / incoming normaliser
+                        out = [q for q in range(nd) if (d.s[q, a] < 0) == (side == 0) and d.s[q, a] != 0]
+                        inn = [q for q in range(nd) if (d.s[q, a] > 0) == (side == 0) and d.s[q, a] != 0]
+                        den = sum(d.w[q] * abs(d.s[q, a]) for q in inn)
+                        for q in out:
+                            A[r, idx(c, q, bb)] -= k * d.w[q] * abs(d.s[q, a]) / den
+        row = nI + c
+        for bb in range(nb):
+            cw = beta[bb] / b.v[bb]
+            A[row, nI + c] += cw * W * b.slope[bb]
+            rhs[row] -= cw * W * (b.I_ref[bb] - b.slope[bb] * b.T_ref)
+            for dd in range(nd):
+                A[row, idx(c, dd, bb)] -= cw * d.w[dd]
+    x = np.linalg.solve(A, rhs)
+    return x[:nI].reshape(nc, nd, nb), x[nI:]
+
+
+@pytest.mark.parametrize("dt_factor", [1.0, 6.0])
+def test_implicit_step_equals_dense_solve(dt_factor):
+    """Source iteration converges to the implicit step's unique solution: the
+    dense linear solve of the same backward-Euler equations (every wall kind)."""
+    mesh = bi.Mesh(3, 3, 3, 2, 1e-7, 1.3e-7, 0.9e-7)
+    dirs = bi.directions_control_angle(2, 4)
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 303.0), bi.WallBC(1), bi.WallBC(2),
+           bi.WallBC(0, None, 298.0)]
+    p = _lin_problem(mesh, dirs, bcs, nb=2)
+    p.dt *= dt_factor
+    rng = np.random.default_rng(5)
+    o0 = oracle.Oracle(p)
+    T = rng.uniform(295, 305, mesh.ncells)
+    I0c, betac = o0.refresh(T)
+    I = I0c[:, None, :] * rng.uniform(0.95, 1.05, (mesh.ncells, dirs.nd, 2))
+    Ie, Te = _dense_implicit_step(p, I, T)
+    o = oracle.Oracle(_imp(p, 400))
+    I1, T1, I0n, bn = o.run(I, T, 1, I0c, betac)
+    assert np.max(np.abs(I1 / Ie - 1)) < 1e-11
+    assert np.max(np.abs(T1 - Te)) < 1e-9
+    assert np.array_equal(bn, betac)  # beta(T^n) (constant-tau table)
+
+
+def test_implicit_uniform_fixed_point_bitexact():
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 10, 20, 30, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+           bi.WallBC(1)]
+    p = _imp(bi.small_3d(bands=b, bcs=bcs), 5)
+    p.dt *= 20
+    o = oracle.Oracle(p)
+    T = np.full(p.mesh.ncells, 300.0)
+    I = o.equilibrium(T)
+    I2, T2, _, _ = o.run(I, T, 10)
+    assert np.array_equal(I2, I) and np.array_equal(T2, T)
+
+
+@pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE])
+def test_implicit_closed_box_conservation(kind):
+    """Converged steps conserve energy in a closed box far beyond the explicit dt bound."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    p = bi.small_3d(6, 5, 4, bands=b, bcs=bi.uniform_bcs(kind), dirs=bi.directions_control_angle(4, 8))
+    p.dt *= 10.0
+    o = oracle.Oracle(_imp(p, 200, 1e-15))
+    I, T0 = o.random_state()
+    T, I0c, betac = o.solve_T(I, T0)
+    E0 = o.energy(I)
+    I2, T2, _, _ = o.run(I, T, 3, I0c, betac)
+    assert abs(o.energy(I2) / E0 - 1) < 1e-12
+    assert I2.min() > 0 and np.all(o.last_iters < 200)
+
+
+def test_implicit_second_order_local_consistency():
+    """One implicit step and one explicit step from the same balanced state
+    differ by O(dt^2) (both are first-order consistent with Eq. 4): the
+    difference drops towards 4x per halving of dt.  Constant-tau LINEAR table,
+    so the start's temperature balances with the step's own weights."""
+    mesh = bi.Mesh(3, 4, 3, 3, 1e-7, 1.2e-7, 0.9e-7)
+    dirs = bi.directions_control_angle(2, 4)
+    bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 303.0), bi.WallBC(1), bi.WallBC(2),
+           bi.WallBC(0, None, 298.0)]
+    base = _lin_problem(mesh, dirs, bcs, nb=2, seed=3)
+    err = []
+    for k in (2, 4, 8, 16):
+        runs = []
+        for imp in (0, 1):
+            q = _lin_problem(mesh, dirs, bcs, nb=2, seed=3)
+            q.dt = base.dt / k
+            if imp:
+                _imp(q, 300, 1e-15)
+            o = oracle.Oracle(q)
+            T0 = np.full(mesh.ncells, 300.0)
+            I0c, _ = o.refresh(T0)
+            I = I0c[:, None, :] * (1 + 0.05 * np.sin(np.arange(I0c.size * dirs.nd))).reshape(mesh.ncells, dirs.nd, 2)
+            T, I0c, betac = o.solve_T(I, T0)
+            runs.append(o.run(I, T, 1, I0c, betac)[0])
+        err.append(np.max(np.abs(runs[1] - runs[0]) / runs[0]))
+    r = [err[i] / err[i + 1] for i in range(3)]
+    assert r[0] < r[1] < r[2] and 3.4 < r[1] and 3.6 < r[2] < 4.4, (err, r)
+
+
+def test_implicit_ballistic_slab_steady_state_one_step():
+    """A single implicit step with dt far beyond every time scale is the steady
+    BTE: the ballistic slab's closed-form flux (I0(T_h) - I0(T_c)) sum_{s_x>0} w s_x."""
+    p, a = _slab(8, 0, beta_scale=0.0)
+    p.dt = 1e3  # s: steady state
+    # the specular y-wall ghosts are lagged by one iteration: the grazing
+    # directions converge at ~0.8 per iteration
+    o = oracle.Oracle(_imp(p, 600, 1e-15), nthreads=1)
+    T = np.full(8, 300.0)
+    I, _, _, _ = o.run(o.equilibrium(T), T, 1)
+    q = _flux_x(p, I)
+    d = p.dirs
+    expect = (a * 305.0 - a * 295.0) * (d.w * d.s[:, 0])[d.s[:, 0] > 0].sum()
+    assert np.max(np.abs(q / expect - 1)) < 1e-12
+
+
+def test_implicit_mirror_symmetry_2d_hotspot_bitexact():
+    p = bi.config2(n=12)
+    p.mesh = bi.Mesh(2, 12, 8, 1, p.mesh.dx, p.mesh.dy, 1.0)
+    p.dirs = bi.directions_control_angle(4, 8)
+    p.bands = bi.subset_bands(bi.silicon_bands(29), [3, 22, 30])
+    p.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, p.mesh.dx, width=4 * p.mesh.dx), 300.0)
+    p.dt *= 5
+    o = oracle.Oracle(_imp(p, 6))
+    T = np.full(p.mesh.ncells, 300.0)
+    I, T2, _, _ = o.run(o.equilibrium(T), T, 4)
+    nx = p.mesh.nx
+    r = o.reflection(0)
+    Ig = I.reshape(p.mesh.ny, nx, p.dirs.nd, -1)
+    assert np.array_equal(Ig, Ig[:, ::-1][:, :, r])
+    Tg = T2.reshape(p.mesh.ny, nx)
+    assert np.array_equal(Tg, Tg[:, ::-1]) and Tg.max() > 300.0
+
+
+def test_implicit_iteration_converges_geometrically():
+    """Source iteration: the per-iteration temperature change shrinks; a
+    tolerance stops it early; fixed counts do exactly that many."""
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    p = bi.small_3d(6, 5, 4, bands=b, dirs=bi.directions_control_angle(4, 8))
+    p.dt *= 4.0
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    res = {}
+    for it in (2, 4, 8, 16, 32):
+        q = _imp(bi.small_3d(6, 5, 4, bands=b, dirs=bi.directions_control_angle(4, 8)), it)
+        q.dt = p.dt
+        oq = oracle.Oracle(q)
+        res[it] = oq.run(I, T, 1)[1]
+        assert list(oq.last_iters) == [it]
+    d = [np.max(np.abs(res[k] - res[32])) for k in (2, 4, 8, 16)]
+    assert d[0] > d[1] > d[2] > d[3] and d[3] < 1e-5 * d[0], d
+    q = _imp(bi.small_3d(6, 5, 4, bands=b, dirs=bi.directions_control_angle(4, 8)), 100, 1e-9)
+    q.dt = p.dt
+    oq = oracle.Oracle(q)
+    oq.run(I, T, 1)
+    assert 2 < oq.last_iters[0] < 32
