@@ -135,7 +135,8 @@ typedef struct {
   void (*dealloc)(void *ptr, void *alloc_ctx);
   void *alloc_ctx;
   int step_mode;  /* 0: explicit step (Eq. 5 + forward Euler); 1: semi-implicit (reading
-                     R-l: explicit advection, implicit relaxation, bte_set_step_mode) */
+                     R-l: explicit advection, implicit relaxation); 2: implicit step by
+                     source iteration (reading R-n); see bte_set_step_mode */
 } bte_run;
 
 /* Create a context: validates tables (positive sizes/speeds, equal octant
@@ -226,7 +227,7 @@ BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs,
  * Errors: BTE_EINVAL (mode, band contexts, the fused-Newton variant). */
 BTE_API bte_status bte_set_tau_mode(bte_ctx *ctx, int mode);
 
-/* Time integrator (SURVEY 8(f) f4 "implicit per-step solvers", reading R-l).
+/* Time integrator (SURVEY 8(f) f4 "implicit per-step solvers").
  *   mode 0 (default): explicit forward-Euler step of Eq. 5;
  *   mode 1: semi-implicit step -- J = I^n - dt v_b sum_f (A_f/V)(s.n) I_up
  *           (explicit upwind advection), T^{n+1} from the energy balance with
@@ -234,11 +235,41 @@ BTE_API bte_status bte_set_tau_mode(bte_ctx *ctx, int mode);
  *           I^{n+1} = (J + dt beta_b I0_b(T^{n+1})) / (1 + dt beta_b).
  *           The dt bound keeps only the advection term (1 - dt v_b
  *           sum_a |s_a|/D_a >= 0), so stiff scattering no longer limits dt.
+ *   mode 2: implicit step (reading R-n; "solvers take 10-20 iterations
+ *           ... within each time step"): backward Euler for every term of
+ *           Eq. 4/5, I' - I^n = dt[beta (I0(T') - I') - v_b sum_f (A_f/V)(s.n) I'_up],
+ *           beta = beta(T^n), wall ghosts of I', T' from the scattering
+ *           balance of I'; solved by source iteration -- per iteration k:
+ *           wall data from I^k; a wavefront transport sweep per octant
+ *           (every cell after its upwind neighbours, exact inversion of the
+ *           upwind operator):
+ *             I^{k+1} = I^n + [dt beta (I0c^k - I^n) + sum_a kk_a (I^{k+1}_up - I^n)]
+ *                             / (1 + dt beta + sum_a kk_a),  kk_a = dt v_b |s_a|/D_a;
+ *           then the lagged Newton (#18) for T^{k+1} with weights beta(T^n)/v_b
+ *           and I0c^{k+1} = I0(T^{k+1}).  bte_set_implicit sets the iteration
+ *           count and tolerance.  No dt bound (positive for every dt).  One
+ *           structured context only (no band / unstructured / multi-rank /
+ *           octant-slot rotation: every iteration re-reads I^n).
  * Also settable at creation through bte_run.step_mode (needed when dt
  * exceeds the explicit bound).  Errors: BTE_EINVAL (mode, band contexts,
- * self-consistent tau, fused Newton), BTE_EUNSTABLE (switching to the explicit
- * step at a dt beyond its bound). */
+ * self-consistent tau, the context kinds above), BTE_EUNSTABLE (switching to
+ * the explicit step at a dt beyond its bound). */
 BTE_API bte_status bte_set_step_mode(bte_ctx *ctx, int mode);
+
+/* Source iterations of the implicit step (step mode 2): at most max_iter per
+ * step (default 20); with tol > 0 (default 1e-10) a step stops early once both
+ * inputs of its last sweep had settled -- max_c |T^{k+1} - T^k| / T^k <= tol
+ * and the wall data (outgoing intensities of specular / partial wall cells,
+ * diffuse ghost tables) changed by at most tol relative since the previous
+ * iterate (the first iteration never stops while such walls exist).  tol = 0:
+ * exactly max_iter iterations, no host synchronisation inside the step.
+ * Errors: BTE_EINVAL (max_iter outside [1, 100000], tol < 0 or not finite). */
+BTE_API bte_status bte_set_implicit(bte_ctx *ctx, int max_iter, double tol);
+
+/* Iterations taken by each step of the last bte_step call in implicit mode:
+ * *count = number of steps recorded, out[0 .. min(n, count)) their iteration
+ * counts.  Errors: BTE_EINVAL. */
+BTE_API bte_status bte_get_iterations(const bte_ctx *ctx, int64_t *out, int64_t n, int64_t *count);
 
 /* Number of boundary faces of wall region 0..5 (the T_wall length of
  * bte_set_bc) for structured and unstructured contexts.  Errors: BTE_EINVAL. */
@@ -413,6 +444,7 @@ typedef struct {
   int rotate;                                        /* 1: octant-slot rotation (see bte_create)  */
   int64_t cell0;                                     /* canonical index of the first owned cell   */
   const char *sweep_kernel;                          /* the a1+a2 kernel bte_step launches (static) */
+  int step_mode;                                     /* 0 explicit, 1 semi-implicit, 2 implicit     */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

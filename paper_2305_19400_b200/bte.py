@@ -26,7 +26,7 @@ I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_plan_umesh", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
-           "bte_version", "bte_set_debug")
+           "bte_version", "bte_set_debug", "bte_set_implicit", "bte_get_iterations")
 DEBUG_SKIP_EXCHANGE = 1
 
 
@@ -100,7 +100,7 @@ class Info(C.Structure):
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
                 ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
                 ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int), ("cell0", C.c_int64),
-                ("sweep_kernel", C.c_char_p)]
+                ("sweep_kernel", C.c_char_p), ("step_mode", C.c_int)]
 
 
 _lib = None
@@ -146,6 +146,8 @@ def load_library(path: str = LIB_PATH):
     lib.bte_get_energy.argtypes = [P, C.POINTER(C.c_double)]
     lib.bte_debug_substep.argtypes = [P, C.c_int, dp, C.c_size_t]
     lib.bte_set_debug.argtypes = [P, C.c_int, C.c_int]
+    lib.bte_set_implicit.argtypes = [P, C.c_int, C.c_double]
+    lib.bte_get_iterations.argtypes = [P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
     lib.bte_timing_enable.argtypes = [P, C.c_int, C.c_int64]
     lib.bte_timing_read.argtypes = [P, C.POINTER(Timing)]
     lib.bte_get_info.argtypes = [P, C.POINTER(Info)]
@@ -266,8 +268,10 @@ class Solver:
     @classmethod
     def from_problem(cls, problem, **kw) -> "Solver":
         """Build from a problem description (mesh/dirs/bands/dt/T_init/bcs)."""
-        kw.setdefault("step_mode", int(getattr(problem, "semi", 0)))
+        kw.setdefault("step_mode", 2 if getattr(problem, "implicit", 0) else int(getattr(problem, "semi", 0)))
         sv = cls(problem.mesh, problem.dirs, problem.bands, problem.dt, problem.T_init, **kw)
+        if getattr(problem, "implicit", 0):
+            sv.set_implicit(int(problem.imp_max_iter), float(problem.imp_tol))
         nreg = 6 if problem.mesh.dim == 3 else 4
         for r in range(nreg):
             sv.set_wall(r, problem.bcs[r])
@@ -297,6 +301,19 @@ class Solver:
     def set_step_mode(self, mode: int) -> None:
         """0: explicit step; 1: semi-implicit (explicit advection, implicit relaxation; reading R-l)."""
         self._check(self._lib.bte_set_step_mode(self._h, int(mode)))
+
+    def set_implicit(self, max_iter: int, tol: float) -> None:
+        """Source iterations per implicit step (reading R-n): at most max_iter, early stop at tol (0: exactly max_iter)."""
+        self._check(self._lib.bte_set_implicit(self._h, int(max_iter), float(tol)))
+
+    def iterations(self) -> np.ndarray:
+        """Iterations of each step of the last step() call in implicit mode."""
+        n = C.c_int64()
+        self._check(self._lib.bte_get_iterations(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int64)
+        if n.value:
+            self._check(self._lib.bte_get_iterations(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out
 
     def set_tau_mode(self, mode: int) -> None:
         """0: lagged tau (default); 1: self-consistent tau(T^{n+1}) (reading R-k)."""

@@ -106,6 +106,8 @@ struct NewtonArgs {
   double semi_dt;         // > 0: semi-implicit step weights beta/(v(1 + semi_dt beta)) (reading R-l)
   unsigned long long *stats;  // debug counters: [evaluations, final re-evaluations, cells solved] or null
   int sc_direct;          // self-consistent tau: direct band integrals even on uniform grids (A/B)
+  int beta_fixed;         // implicit step (R-n): weights from the stored beta_next, not beta(T)
+  unsigned long long *dTmax;  // implicit step: max_c |T^{k+1} - T^k| / T^k (double bits), or null
 };
 
 struct SweepArgs {
@@ -132,6 +134,8 @@ struct SweepArgs {
   int64_t out_off[kMaxSlots];  // where slot s of I^{n+1} goes in Iout
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
   int no_spare;           // 1: side jobs on compute threads (A/B switch read at create)
+  int raster;             // 3-D column order: strips of `raster` columns along x (0: row-major)
+  int l2pf;               // L2 prefetch distance (cells beyond the TMA ring) of the own block, 0: off
 };
 
 // Unstructured simplex mesh, device view.  The state layout
@@ -170,8 +174,11 @@ const char *sweep_kernel_name(const SweepArgs &a);
 cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
-                           cudaStream_t s);
-cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s);
+                           cudaStream_t s, unsigned long long *chg = nullptr);
+cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s,
+                                 unsigned long long *chg = nullptr);
+cudaError_t launch_sweep_imp(const SweepArgs &a, const int2 *tasks, int ntasks, int *prog, unsigned *ticket,
+                             cudaStream_t s);
 cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,
                              cudaStream_t s);
 cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, double *I0c,

@@ -104,6 +104,23 @@ __device__ __forceinline__ double bte_update(double Ic, double xu, double yu, do
   return fma(dtb, I0 - Ic, Ic) - v * fl;
 }
 
+// Column of this CTA.  raster = W > 0 (3-D): the columns go in strips of W
+// along x, y fastest inside a strip, so the y-upwind neighbour is W launches
+// back instead of nx -- its block is still in L2 when this CTA re-reads it,
+// which lets the segments grow (fewer march-axis restarts).  The x-upwind
+// column of a strip's first column is one strip back (a re-read from DRAM
+// on 1/W of the columns).
+__device__ __forceinline__ int sweep_column(const SweepArgs &A, int id) {
+  const Geometry &g = A.g;
+  if (g.dim != 3 || A.raster <= 0 || A.ncols > 0) return A.col0 + id;
+  const int W = A.raster, ny = g.ny;
+  const int strip = id / (W * ny);
+  const int r = id - strip * W * ny;
+  const int w = min(W, g.nx - strip * W);
+  const int y = r / w;
+  return strip * W + (r - y * w) + g.nx * y;
+}
+
 // One CTA = one (cross cell, octant slot, segment of the march axis).  The CTA
 // walks its column in the upwind-to-downwind order of that octant, so the
 // march-axis upwind value is the previous iteration's I^n kept in registers.
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
 
   const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
-  const int col = A.col0 + blockIdx.x;
+  const int col = sweep_column(A, blockIdx.x);
   const int x = (DIM == 3) ? col % g.nx : col;
   const int y = (DIM == 3) ? col / g.nx : 0;
   const bool xneg = oct & 4;
@@ -291,6 +308,10 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// bulk prefetch of global memory into L2 (no shared-memory destination)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -306,13 +327,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // + mbarrier, issued S cells ahead by one thread.  Keeps S x (2 or 3) x 16 KB
 // of HBM/L2 reads in flight per CTA.  NBT > 0 fixes the channel count at
 // compile time (immediate smem/global offsets); NBT = 0 is the generic path.
-template <int DIM, int JMAX, int NBT>
-__global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
+// SS > 0 fixes the ring depth at compile time (stage index and phase kept as
+// running counters, no division per cell); the 40-channel specialisation is
+// bounded to 448 threads x 2 CTAs/SM, so ptxas may use 72 registers and keeps
+// the loop-invariant addresses in registers instead of re-deriving them from
+// the kernel parameters every cell.
+template <int DIM, int JMAX, int NBT, int SS>
+__global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_sweep_tma(const SweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
   const int nb = NBT > 0 ? NBT : g.nb;
   const int nj = g.nj, Es = g.Es;
-  const int S = A.stages;
+  const int S = SS > 0 ? SS : A.stages;
   const int tid = threadIdx.x;
   const int grp = tid / nb;
   const int b = tid - grp * nb;
@@ -326,11 +352,12 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   const int spare0 = JG * nb;
   const bool spare = (int)blockDim.x >= spare0 + nb + 1;
   const int rtid = spare ? tid - spare0 : tid;  // reducer index (channel) when in [0, nb)
+  const bool reducer = rtid >= 0 && rtid < nb;
   const int tis = spare ? spare0 + nb : 0;
 
   const int slot = A.slot0 + blockIdx.y;
   const int oct = g.slot_oct[slot];
-  const int col = A.col0 + blockIdx.x;
+  const int col = sweep_column(A, blockIdx.x);
   const int x = (DIM == 3) ? col % g.nx : col;
   const int y = (DIM == 3) ? col / g.nx : 0;
   const bool xneg = oct & 4;
@@ -403,8 +430,19 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
   }
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
   __syncthreads();
-  if (tid == tis)
+  // L2 prefetch of the own block PF cells beyond the ring (A.l2pf = PF > 0):
+  // the DRAM latency is paid ahead of the ring, whose copies then hit L2
+  const int PF = A.l2pf;
+  auto prefetch = [&](int i) {
+    if (PF > 0 && i < np) {
+      const int pp = pfirst + i * step;
+      bulk_prefetch_l2(Is + (int64_t)(pp + g.plane_off) * g.plane_stride + colE, (uint32_t)Es * 8u);
+    }
+  };
+  if (tid == tis) {
     for (int i = 0; i < min(S, np); ++i) issue(i, i);
+    for (int i = S; i < S + PF; ++i) prefetch(i);
+  }
 
   const double v = A.v[active ? b : 0];
   const int e0 = j0 * nb + b;  // this thread's first element; element k is e0 + k*nb
@@ -428,20 +466,24 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
     }
   }
 
-  int buf = 0;
+  // running addresses along the march: this thread's output row and the
+  // reducer's octant-partial entry
+  const int64_t pstep = (int64_t)step * g.plane_stride;
+  double *op = Os + (int64_t)(pfirst + g.plane_off) * g.plane_stride + colE + e0;
+  const int64_t dstep = (int64_t)step * g.ncross * g.nslot * nb;
+  double *dp = A.Dpart + (((int64_t)col + (int64_t)pfirst * g.ncross) * g.nslot + slot) * nb + (reducer ? rtid : 0);
+  const double *rb0 = red, *rb1 = red + JG * nb;
+  int st = 0;
+  uint32_t ph = 0;
   int p = pfirst;
   for (int i = 0; i < np; ++i, p += step) {
-    const int st = i % S;
-    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
-    const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
     const double *sp = stage0 + st * sd;
-    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    mbar_wait(&full[st], ph);
     double acc = 0.0;
     if (active) {
-      const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + cell * nb + b);
-      const double dtb = dt * (rows_tma ? sp[o_be + b] : ldg(A.beta + cell * nb + b));
+      const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + ((int64_t)col + (int64_t)p * g.ncross) * nb + b);
+      const double dtb = dt * (rows_tma ? sp[o_be + b] : ldg(A.beta + ((int64_t)col + (int64_t)p * g.ncross) * nb + b));
       const double *so = sp + e0;
-      double *op = Os + base + e0;
       if (interior && nloc == JMAX) {
         const double *sx = so + o_x;
         const double *sy = so + o_y;
@@ -455,6 +497,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
           prev[k] = Ic;
         }
       } else {
+        const int64_t base = (int64_t)(p + g.plane_off) * g.plane_stride + colE;
         const int64_t mg = g.m0 + p;
 #pragma unroll
         for (int k = 0; k < JMAX; ++k) {
@@ -484,19 +527,25 @@ __global__ void __launch_bounds__(1024) k_sweep_tma(const SweepArgs A) {
         }
       }
     }
-    double *rb = red + buf * JG * nb;
+    double *rb = const_cast<double *>((i & 1) ? rb1 : rb0);
     if (active) rb[tid] = acc;
     __syncthreads();  // stage st fully consumed, rb complete
     if (tid == tis && i + S < np) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S, st);
+      prefetch(i + S + PF);
     }
-    if (rtid >= 0 && rtid < nb) {
+    if (reducer) {
       double s = 0.0;
       for (int q = 0; q < JG; ++q) s += rb[q * nb + rtid];
-      A.Dpart[(cell * g.nslot + slot) * nb + rtid] = s;
+      *dp = s;
     }
-    buf ^= 1;
+    op += pstep;
+    dp += dstep;
+    if (++st == S) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
 }
 
@@ -560,16 +609,25 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
     // spare threads for the side jobs (reducers + issuer) unless disabled at create
     const int tthreads = ((a.no_spare ? threads : threads + g.nb + 1) + 31) / 32 * 32;
     cudaError_t e;
-#define BTE_LAUNCH(N, NB)                                                       \
-  {                                                                             \
-    if ((e = smem_attr((const void *)k_sweep_tma<DIM, N, NB>, smem))) return e; \
-    k_sweep_tma<DIM, N, NB><<<grid, tthreads, smem, s>>>(a);                    \
-    break;                                                                      \
+#define BTE_LAUNCH_S(N, NB, SV)                                                      \
+  {                                                                                  \
+    if ((e = smem_attr((const void *)k_sweep_tma<DIM, N, NB, SV>, smem))) return e;  \
+    k_sweep_tma<DIM, N, NB, SV><<<grid, tthreads, smem, s>>>(a);                     \
+    break;                                                                           \
   }
-    if (g.nb == 40 && jcase == 5) {
-      switch (0) { default: BTE_LAUNCH(5, 40) }
-    } else if (g.nb == 55 && jcase == 8) {
-      switch (0) { default: BTE_LAUNCH(8, 55) }
+#define BTE_LAUNCH(N, NB) BTE_LAUNCH_S(N, NB, 0)
+    if (g.nb == 40 && jcase == 5 && tthreads <= 448 && S >= 2 && S <= 4) {
+      switch (S) {
+        case 2: BTE_LAUNCH_S(5, 40, 2)
+        case 3: BTE_LAUNCH_S(5, 40, 3)
+        default: BTE_LAUNCH_S(5, 40, 4)
+      }
+    } else if (g.nb == 55 && jcase == 8 && S >= 2 && S <= 4) {
+      switch (S) {
+        case 2: BTE_LAUNCH_S(8, 55, 2)
+        case 3: BTE_LAUNCH_S(8, 55, 3)
+        default: BTE_LAUNCH_S(8, 55, 4)
+      }
     } else {
       switch (jcase) {
         case 1: BTE_LAUNCH(1, 0)
@@ -584,6 +642,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
       }
     }
 #undef BTE_LAUNCH
+#undef BTE_LAUNCH_S
     return cudaGetLastError();
   }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
@@ -617,6 +676,274 @@ const char *sweep_kernel_name(const SweepArgs &a) {
 
 cudaError_t launch_sweep(const SweepArgs &a, cudaStream_t s) {
   return a.g.dim == 3 ? launch_sweep_dim<3>(a, s) : launch_sweep_dim<2>(a, s);
+}
+
+// ---------------------------------------------------------------- implicit transport sweep (R-n)
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One source iteration's transport sweep of the implicit step (reading R-n):
+//   I^{k+1} = I^n + [dt beta (I0c - I^n) + sum_a kk_a (I^{k+1}_up,a - I^n)] / (1 + dt beta + sum_a kk_a),
+// kk_a = v_b dt |s_a| / D_a, axis terms in x, y, z order.  I'_up is THIS sweep's
+// value of the upwind cell (a wavefront: exact inversion of the upwind operator
+// for the scattering source I0c = I0(T^k)), or the wall ghost of I^k (snapshot
+// / tables, the g.rot path of ghost_value).
+//
+// One CTA per (octant slot, column) task.  Tasks are taken by ticket in a
+// topological order of the upwind dependence (host table: the column's
+// distance from its octant's upwind corner), so every column a CTA waits for
+// belongs to a CTA that took its ticket earlier and is running or done -- no
+// deadlock whatever the block scheduler does.  The CTA marches its column
+// from the upwind wall along the march axis (upwind value in registers, the
+// CTA's own previous result); before each plane it waits until the x- (and
+// y-) upwind columns have published that plane (release/acquire counter per
+// (slot, column)), reads their I^{k+1} values from L2 and publishes its own
+// plane after writing it.  The own I^n block and the I0c / beta rows do not
+// depend on the wavefront and stream through an S-stage TMA ring.
+template <int DIM, int JMAX>
+__global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int2 *__restrict__ tasks,
+                                                    int *__restrict__ prog, unsigned *__restrict__ ticket) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ int s_task;
+  const Geometry &g = A.g;
+  const int nb = g.nb;
+  const int nj = g.nj, Es = g.Es;
+  const int S = A.stages;
+  const int tid = threadIdx.x;
+  const int grp = tid / nb;
+  const int b = tid - grp * nb;
+  const int JG = A.jg;
+  const int j0 = grp * A.jpt;
+  const int nloc = max(0, min(A.jpt, nj - j0));
+  const bool active = grp < JG;
+  const int spare0 = JG * nb;
+  const bool spare = (int)blockDim.x >= spare0 + nb + 1;
+  const int rtid = spare ? tid - spare0 : tid;
+  const int tis = spare ? spare0 + nb : 0;
+
+  if (tid == 0) s_task = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int2 task = tasks[s_task];
+  const int slot = task.x, col = task.y;
+  const int oct = g.slot_oct[slot];
+  const int x = (DIM == 3) ? col % g.nx : col;
+  const int y = (DIM == 3) ? col / g.nx : 0;
+  const bool xneg = oct & 4;
+  const bool yneg = oct & 2;
+  const bool mneg = (DIM == 3) ? (oct & 1) : (oct & 2);
+  const bool xghost = xneg ? (x == g.nx - 1) : (x == 0);
+  const int xregion = xneg ? 1 : 0;
+  const int64_t xoff = xneg ? (int64_t)Es : -(int64_t)Es;
+  const int xcol = xneg ? col + 1 : col - 1;
+  bool yghost = true;
+  int yregion = 2;
+  int64_t yoff = 0;
+  int ycol = 0;
+  if (DIM == 3) {
+    yghost = yneg ? (y == g.ny - 1) : (y == 0);
+    yregion = yneg ? 3 : 2;
+    yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
+    ycol = yneg ? col + g.nx : col - g.nx;
+  }
+  const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
+  int *pr = prog + (int64_t)slot * g.ncross;
+
+  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  double *coef = reinterpret_cast<double *>(smraw + 128);
+  double *red = coef + 4 * nj;
+  double *stage0 = red + 2 * JG * nb;
+  const int64_t sd = A.stage_doubles;  // own I^n | I0 | beta
+  const int o_i0 = Es, o_be = Es + nb;
+  const bool rows_tma = (nb % 2) == 0;
+  const int np = g.nplanes;
+  const int step = mneg ? -1 : 1;
+  const int pfirst = mneg ? np - 1 : 0;
+
+  const double *__restrict__ In = A.Iin + g.slot_off[slot];
+  double *__restrict__ Os = A.Iout + A.out_off[slot];
+  const int64_t colE = (int64_t)col * Es;
+  const double dt = A.dt;
+
+  auto issue = [&](int i, int st) {
+    const int pp = pfirst + i * step;
+    const int64_t base = (int64_t)pp * g.plane_stride + colE;
+    const int64_t cell = (int64_t)col + (int64_t)pp * g.ncross;
+    double *sp = stage0 + st * sd;
+    const uint32_t blk = (uint32_t)Es * 8u;
+    const uint32_t row = (uint32_t)nb * 8u;
+    mbar_expect_tx(&full[st], blk + (rows_tma ? 2u * row : 0u));
+    bulk_g2s(sp, In + base, blk, &full[st]);
+    if (rows_tma) {
+      bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
+      bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
+    }
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
+  __syncthreads();
+  if (tid == tis)
+    for (int i = 0; i < min(S, np); ++i) issue(i, i);
+
+  const double v = A.v[active ? b : 0];
+  const int e0 = j0 * nb + b;
+  const double *cq = coef + 4 * j0;
+  double prev[JMAX];  // march-axis upwind I^{k+1}: the wall ghost, then this CTA's own results
+  {
+    const int64_t base = (int64_t)pfirst * g.plane_stride + colE;
+    const int64_t face = (DIM == 3) ? (int64_t)x + (int64_t)g.nx * y : x;
+#pragma unroll
+    for (int k = 0; k < JMAX; ++k) {
+      prev[k] = 0.0;
+      if (active && k < nloc) prev[k] = ghost_value(g, A.Iin, mregion, face, base, slot, j0 + k, b);
+    }
+  }
+
+  int buf = 0;
+  int p = pfirst;
+  for (int i = 0; i < np; ++i, p += step) {
+    const int st = i % S;
+    const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
+    const int64_t base = (int64_t)p * g.plane_stride + colE;
+    const double *sp = stage0 + st * sd;
+    // wavefront: the upwind columns' plane p of I^{k+1} must be published
+    if (tid == 0) {
+      if (!xghost)
+        while (ld_acquire_gpu(pr + xcol) <= i) __nanosleep(32);
+      if (DIM == 3 && !yghost)
+        while (ld_acquire_gpu(pr + ycol) <= i) __nanosleep(32);
+    }
+    __syncthreads();
+    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    double acc = 0.0;
+    if (active) {
+      const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + cell * nb + b);
+      const double dtb = dt * (rows_tma ? sp[o_be + b] : ldg(A.beta + cell * nb + b));
+      const int64_t mg = g.m0 + p;
+#pragma unroll
+      for (int k = 0; k < JMAX; ++k) {
+        if (k < nloc) {
+          const int j = j0 + k;
+          const int e = e0 + k * nb;
+          const double Inn = sp[e];
+          double xu, yu = 0.0;
+          if (!xghost) {
+            xu = __ldcg(Os + base + xoff + e);
+          } else {
+            const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
+            xu = ghost_value(g, A.Iin, xregion, face, base, slot, j, b);
+          }
+          if (DIM == 3) {
+            if (!yghost) {
+              yu = __ldcg(Os + base + yoff + e);
+            } else {
+              const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
+              yu = ghost_value(g, A.Iin, yregion, face, base, slot, j, b);
+            }
+          }
+          const double *cf = cq + 4 * k;
+          double num = dtb * (I0 - Inn), den = 1.0 + dtb;
+          if (cf[0] != 0.0) {
+            const double kk = v * cf[0];
+            num = fma(kk, xu - Inn, num);
+            den += kk;
+          }
+          if (DIM == 3 && cf[1] != 0.0) {
+            const double kk = v * cf[1];
+            num = fma(kk, yu - Inn, num);
+            den += kk;
+          }
+          if (cf[DIM - 1] != 0.0) {
+            const double kk = v * cf[DIM - 1];
+            num = fma(kk, prev[k] - Inn, num);
+            den += kk;
+          }
+          const double Inew = Inn + num / den;
+          __stcg(Os + base + e, Inew);
+          acc = fma(cf[3], I0 - Inew, acc);
+          prev[k] = Inew;
+        }
+      }
+    }
+    double *rb = red + buf * JG * nb;
+    if (active) rb[tid] = acc;
+    __syncthreads();  // stage st consumed, rb complete, this plane's stores issued
+    if (tid == 0) {
+      __threadfence();  // cumulative over the CTA's stores ordered by the barrier
+      st_release_gpu(pr + col, i + 1);
+    }
+    if (tid == tis && i + S < np) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + S, st);
+    }
+    if (rtid >= 0 && rtid < nb) {
+      double s = 0.0;
+      for (int q = 0; q < JG; ++q) s += rb[q * nb + rtid];
+      A.Dpart[(cell * g.nslot + slot) * nb + rtid] = s;
+    }
+    buf ^= 1;
+  }
+}
+
+template <int DIM>
+static cudaError_t launch_sweep_imp_dim(const SweepArgs &a0, const int2 *tasks, int ntasks, int *prog,
+                                        unsigned *ticket, cudaStream_t s) {
+  SweepArgs a = a0;
+  const Geometry &g = a.g;
+  int jpt, JG;
+  sweep_shape(g.nb, g.nj, a.target_threads > 0 ? a.target_threads : 448, &jpt, &JG);
+  a.jpt = jpt;
+  a.jg = JG;
+  const int threads = JG * g.nb;
+  if (threads > 1024 || (g.Es & 1)) return cudaErrorInvalidConfiguration;
+  const int64_t stage_d = ((int64_t)g.Es + 2 * g.nb + 15) / 16 * 16;
+  const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
+  const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;
+  int S = (int)((budget > fixed ? budget - fixed : 0) / (stage_d * sizeof(double)));
+  S = std::max(2, std::min(4, S));
+  if (a.stages_override > 0) S = std::min(16, a.stages_override);
+  a.stages = S;
+  a.stage_doubles = stage_d;
+  const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  const int tthreads = ((a.no_spare ? threads : threads + g.nb + 1) + 31) / 32 * 32;
+  if (tthreads > 1024) return cudaErrorInvalidConfiguration;
+  const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
+  cudaError_t e;
+  switch (jcase) {
+#define BTE_IMP(N)                                                                    \
+  case N:                                                                             \
+    if ((e = smem_attr((const void *)k_sweep_imp<DIM, N>, smem))) return e;           \
+    k_sweep_imp<DIM, N><<<ntasks, tthreads, smem, s>>>(a, tasks, prog, ticket);       \
+    break;
+    BTE_IMP(1)
+    BTE_IMP(2)
+    BTE_IMP(4)
+    BTE_IMP(5)
+    BTE_IMP(8)
+    BTE_IMP(10)
+    BTE_IMP(16)
+#undef BTE_IMP
+    default:
+      return cudaErrorInvalidConfiguration;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_imp(const SweepArgs &a, const int2 *tasks, int ntasks, int *prog, unsigned *ticket,
+                             cudaStream_t s) {
+  return a.g.dim == 3 ? launch_sweep_imp_dim<3>(a, tasks, ntasks, prog, ticket, s)
+                      : launch_sweep_imp_dim<2>(a, tasks, ntasks, prog, ticket, s);
 }
 
 // ---------------------------------------------------------------- diffuse ghosts
@@ -670,7 +997,8 @@ static int64_t wall_faces_local(const Geometry &g, int region) {
 }
 
 __device__ __forceinline__ void diffuse_face(const Geometry &g, const double *__restrict__ I, int region,
-                                             int64_t face, int64_t cell_base, double *__restrict__ gtab) {
+                                             int64_t face, int64_t cell_base, double *__restrict__ gtab,
+                                             double *chg = nullptr) {
   const int axis = region >> 1;
   const bool hi = region & 1;
   // outgoing octants: s_a < 0 on the low wall (bit set), s_a >= 0 on the high wall
@@ -690,24 +1018,36 @@ __device__ __forceinline__ void diffuse_face(const Geometry &g, const double *__
       q[o] = acc;
     }
     const double num = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-    gtab[face * g.nb + b] = num / g.diff_den[region];
+    const double gv = num / g.diff_den[region];
+    if (chg) {  // relative change against the table's previous content (R-n convergence)
+      const double old = gtab[face * g.nb + b];
+      *chg = fmax(*chg, fabs(gv - old) / fabs(old));
+    }
+    gtab[face * g.nb + b] = gv;
   }
 }
 
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long *w, double x) {
+  // non-negative doubles order like their bit patterns
+  if (x > 0.0) atomicMax(w, (unsigned long long)__double_as_longlong(x));
+}
+
 __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
-                          double *__restrict__ gtab) {
+                          double *__restrict__ gtab, unsigned long long *chg) {
   int64_t face, cell_base;
   wall_face(g, region, blockIdx.x, &face, &cell_base);
-  diffuse_face(g, I, region, face, cell_base, gtab);
+  double m = 0.0;
+  diffuse_face(g, I, region, face, cell_base, gtab, chg ? &m : nullptr);
+  if (chg) atomic_max_nonneg(chg, m);
 }
 
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
-                           cudaStream_t s) {
+                           cudaStream_t s, unsigned long long *chg) {
   const int64_t nf = wall_faces_local(g, region);
   if (nf == 0) return cudaSuccess;
   int threads = ((g.nb + 31) / 32) * 32;
   if (threads > 256) threads = 256;
-  k_diffuse<<<(unsigned)nf, threads, 0, s>>>(g, I, region, gtab);
+  k_diffuse<<<(unsigned)nf, threads, 0, s>>>(g, I, region, gtab, chg);
   return cudaGetLastError();
 }
 
@@ -718,7 +1058,8 @@ constexpr int kMaxSnapJ = 1024;  // directions per octant handled by k_spec_snap
 // octant is swept, so the boundary pass snapshots them from I^n first:
 // out[face][slot][j][b] = I^n of the boundary cell at the reflection of (slot, j).
 __global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, int region,
-                                double *__restrict__ out, const int4 ins_lo, const int4 ins_hi) {
+                                double *__restrict__ out, const int4 ins_lo, const int4 ins_hi,
+                                unsigned long long *chg) {
   const int axis = region >> 1;
   int64_t face, cell_base;
   wall_face(g, region, blockIdx.x, &face, &cell_base);
@@ -738,21 +1079,32 @@ __global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, 
     srow[j] = I + g.slot_off[sr] + (off - sr * g.slot_stride) + cell_base;
   }
   __syncthreads();
+  double m = 0.0;  // relative change against the previous snapshot (R-n convergence)
   if ((g.nb & 1) == 0) {  // 16-B rows: double2 copies
     const int hp = g.nb >> 1;
     for (int e = threadIdx.x; e < g.nj * hp; e += blockDim.x) {
       const int j = e / hp, q = e - j * hp;
-      reinterpret_cast<double2 *>(o + (int64_t)j * g.nb)[q] = __ldg(reinterpret_cast<const double2 *>(srow[j]) + q);
+      double2 *dst = reinterpret_cast<double2 *>(o + (int64_t)j * g.nb) + q;
+      const double2 val = __ldg(reinterpret_cast<const double2 *>(srow[j]) + q);
+      if (chg) {
+        const double2 old = *dst;
+        m = fmax(m, fmax(fabs(val.x - old.x) / fabs(old.x), fabs(val.y - old.y) / fabs(old.y)));
+      }
+      *dst = val;
     }
   } else {
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       const int j = e / g.nb, b = e - j * g.nb;
-      o[e] = srow[j][b];
+      const double val = srow[j][b];
+      if (chg) m = fmax(m, fabs(val - o[e]) / fabs(o[e]));
+      o[e] = val;
     }
   }
+  if (chg) atomic_max_nonneg(chg, m);
 }
 
-cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s) {
+cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s,
+                                 unsigned long long *chg) {
   const int64_t nf = wall_faces_local(g, region);
   if (nf == 0) return cudaSuccess;
   if (g.nj > kMaxSnapJ) return cudaErrorInvalidValue;
@@ -766,7 +1118,7 @@ cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region,
   if (nin == 0) return cudaSuccess;
   const int thr = std::min(256, (g.E + 31) / 32 * 32);
   k_spec_snapshot<<<dim3((unsigned)nf, (unsigned)nin), thr, 0, s>>>(
-      g, I, region, out, make_int4(ins[0], ins[1], ins[2], ins[3]), make_int4(ins[4], ins[5], ins[6], ins[7]));
+      g, I, region, out, make_int4(ins[0], ins[1], ins[2], ins[3]), make_int4(ins[4], ins[5], ins[6], ins[7]), chg);
   return cudaGetLastError();
 }
 
@@ -910,11 +1262,12 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
       q[o] = sl >= 0 ? __ldcg(a.Dpart + (c * a.nslot + sl) * nb + b) : 0.0;
     }
     const double D = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-    const double bn = beta_of_T(a.m.bcoef, b, Tn);
+    // implicit step (R-n): the step's beta(T^n), stored at its start, weights every iteration
+    const double bn = a.beta_fixed ? a.beta_next[c * nb + b] : beta_of_T(a.m.bcoef, b, Tn);
     // semi-implicit step (reading R-l): weights beta / (v (1 + dt beta))
     const double cb = a.semi_dt > 0.0 ? bn * a.m.rv[b] / (1.0 + a.semi_dt * bn) : bn * a.m.rv[b];
     cs[b] = cb;
-    a.beta_next[c * nb + b] = bn;
+    if (!a.beta_fixed) a.beta_next[c * nb + b] = bn;
     F0 += cb * D;
     K0 += cb * (D - a.W * a.I0c[c * nb + b]);
     Fp0 += cb * (a.W * a.dI0c[c * nb + b]);
@@ -1034,6 +1387,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   if (Tf != Tn) {
     // refresh I0c = I0(T^{n+1}) and its derivative
     if (lane == 0) a.T[c] = Tf;
+    if (a.dTmax && lane == 0) atomic_max_nonneg(a.dTmax, fabs(Tf - Tn) / Tn);
     if (be && a.m.uniform) {
       // refresh from the per-channel values of the last evaluation (at Tf itself
       // after a final pass, else the second-order Taylor step of reading R-g)
@@ -1405,9 +1759,11 @@ __global__ void k_refresh(const Material m, const double *__restrict__ T, int64_
   const int64_t c = i / m.nb;
   const int b = (int)(i - c * m.nb);
   const double t = T[c];
-  double d;
-  I0c[i] = I0_of_T(m, b, t, &d);
-  dI0c[i] = d;
+  if (I0c) {  // (null: beta only -- the implicit step's beta(T^n))
+    double d;
+    I0c[i] = I0_of_T(m, b, t, &d);
+    dI0c[i] = d;
+  }
   beta[i] = beta_of_T(m.bcoef, b, t);
 }
 

@@ -1064,3 +1064,100 @@ def test_demo_20000_steps_long_run(Solver):
     F = T2.reshape(n, n)
     assert np.array_equal(F, F[:, ::-1])
     assert T2.mean() > T1.mean() > 300.0
+
+
+# ----------------------------------------------------------------- implicit step by source iteration (reading R-n)
+
+def _implicit(p, iters, tol=0.0, dt_factor=1.0):
+    p.dt = dt_factor * p.dt
+    p.implicit = 1
+    p.imp_max_iter = iters
+    p.imp_tol = tol
+    return p
+
+
+def _imp_cases():
+    c2 = bi.config2(n=12)
+    c2.mesh = bi.Mesh(2, 12, 10, 1, c2.mesh.dx, c2.mesh.dy, 1.0)
+    c2.bcs[3] = bi.WallBC(0, bi.hotspot_profile(12, c2.mesh.dx), 300.0)
+    c3 = bi.config3()
+    c3.mesh = bi.Mesh(3, 7, 6, 5, c3.mesh.dx, c3.mesh.dy, c3.mesh.dz)  # the 400 x 40 tables: TMA-ring blocks
+    return {"small3d": bi.small_3d(7, 5, 4), "config2_reduced": c2, "config3_tables": c3,
+            "inplane_55": bi.Problem("demo_small", bi.Mesh(2, 9, 7, 1, 4.375e-6, 4.375e-6, 1.0),
+                                     bi.directions_inplane(20), bi.silicon_bands(40), 1e-12, 300.0,
+                                     [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+                                      bi.WallBC(0, bi.hotspot_profile(9, 4.375e-6), 300.0), bi.WallBC(1),
+                                      bi.WallBC(1)], seed=3),
+            "all_kinds_3d": bi.small_3d(6, 5, 4, bcs=[bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0),
+                                                      bi.WallBC(3, specularity=0.4), bi.WallBC(2),
+                                                      bi.WallBC(0, None, 298.0)])}
+
+
+@pytest.mark.parametrize("case", ["small3d", "config2_reduced", "config3_tables", "inplane_55", "all_kinds_3d"])
+def test_implicit_parity_fixed_iterations(Solver, case):
+    """Implicit step (wavefront transport sweeps + lagged Newton per source
+    iteration) against the oracle: 3 steps x 5 iterations at 8x the explicit dt."""
+    p = _implicit(_imp_cases()[case], 5, 0.0, 8.0)
+    (rel, dT), _ = _run_both(Solver, p, 3)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_implicit_parity_tolerance_and_iteration_counts(Solver):
+    """Early stop at a tolerance: the GPU takes the oracle's iteration counts."""
+    p = _implicit(_imp_cases()["all_kinds_3d"], 60, 1e-9, 4.0)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    Io, To, _, _ = o.run(I, T, 3)
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(3)
+        Ig, Tg = sv.intensity(), sv.temperature()
+        its = sv.iterations()
+    assert list(its) == list(o.last_iters) and its.max() < 60, (its, o.last_iters)
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_implicit_fixed_point_and_closed_box(Solver):
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 10, 20, 30, 39])
+    bcs = [bi.WallBC(1), bi.WallBC(1), bi.WallBC(0, None, 300.0), bi.WallBC(1), bi.WallBC(0, None, 300.0),
+           bi.WallBC(1)]
+    p = _implicit(bi.small_3d(6, 5, 4, bands=b, bcs=bcs), 4, 0.0, 20.0)
+    with Solver.from_problem(p) as sv:
+        T0, I0 = sv.temperature(), sv.intensity()
+        sv.step(5)
+        assert np.array_equal(sv.intensity(), I0) and np.array_equal(sv.temperature(), T0)
+    b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
+    q = _implicit(bi.small_3d(6, 5, 4, bands=b, bcs=bi.uniform_bcs(bi.BC_DIFFUSE)), 200, 1e-14, 10.0)
+    I, _ = oracle.Oracle(q).random_state()
+    with Solver.from_problem(q) as sv:
+        sv.set_state(I, None)
+        E0 = sv.energy()
+        sv.step(3)
+        E1 = sv.energy()
+        assert sv.intensity().min() > 0 and sv.iterations().max() < 200
+    assert abs(E1 / E0 - 1) < 1e-12
+
+
+def test_implicit_errors(Solver, monkeypatch):
+    from paper_2305_19400_b200 import BteError
+    p = _group_case("3d")
+    with Solver.from_problem(p) as sv:
+        with pytest.raises(BteError):
+            sv.set_implicit(0, 1e-9)
+        with pytest.raises(BteError):
+            sv.set_implicit(5, -1.0)
+        sv.set_step_mode(2)
+        with pytest.raises(BteError):
+            sv.set_tau_mode(1)
+        assert sv._lib.bte_set_step_mode(sv._h, 3) == 1
+    sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=0, nranks=2)
+    try:
+        with pytest.raises(BteError):
+            sv.set_step_mode(2)  # multi-rank: no wavefront across slabs
+    finally:
+        sv.close()
+    monkeypatch.setenv("BTE_ROTATE", "1")
+    with Solver.from_problem(p) as sv:
+        with pytest.raises(BteError):
+            sv.set_step_mode(2)  # every iteration re-reads I^n: two buffers needed
