@@ -87,8 +87,10 @@ def config_dict(p, args, world):
     state_gb = ncells * p.dirs.nd * p.bands.nb * 8 / 1e9
     return {"workload": p.name, "config": args.config, "cells": ncells, "directions": p.dirs.nd,
             "channels": p.bands.nb, "dof_per_step": ncells * p.dirs.nd * p.bands.nb, "start": args.start,
-            "dt": p.dt * (args.semi if args.semi > 0 else 1.0), "tau": args.tau,
-            "integrator": "semi-implicit" if args.semi > 0 else "explicit",
+            "dt": p.dt * (args.semi if args.semi > 0 else args.dt_factor if args.implicit > 0 else 1.0),
+            "tau": args.tau,
+            "integrator": ("semi-implicit" if args.semi > 0 else
+                           f"implicit ({args.implicit} source iterations/step)" if args.implicit > 0 else "explicit"),
             "parallelism": _parallelism(p, args, world),
             "l2": f"inputs > L2 ({state_gb / max(1, world):.2f} GB of I^n per GPU vs 126 MB), no flush"}
 
@@ -354,6 +356,9 @@ def run_b200(args):
     if args.semi > 0:
         p.dt = args.semi * p.dt
         p.semi = 1
+    if args.implicit > 0:  # reading R-n: fixed iteration count, no host sync inside a step
+        p.dt = args.dt_factor * p.dt
+        p.implicit, p.imp_max_iter, p.imp_tol = 1, args.implicit, 0.0
     nccl_id = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
@@ -387,22 +392,30 @@ def run_b200(args):
 
     clocks = ClockSampler(local)
     clocks.start()
-    sv.timing_enable(True, args.steps * args.repeats)
-    reps, spans = [], []
-    for _ in range(args.repeats):
+
+    def timed(k):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         barrier()
         t0 = time.time()
         ev0.record(stream)
-        sv.step(args.steps)
+        sv.step(k)
         ev1.record(stream)
         barrier()
         spans.append((t0, time.time()))
-        reps.append(max_over_ranks(ev0.elapsed_time(ev1)))
-    clocks.stop()
+        return max_over_ranks(ev0.elapsed_time(ev1))
+
+    # the timed repeats run the production path (CUDA-graph replay where the
+    # library uses it); one more repeat with per-kernel CUDA events gives the
+    # kernel breakdown and the roofline's launch time
+    reps, spans = [], []
+    for _ in range(args.repeats):
+        reps.append(timed(args.steps))
+    sv.timing_enable(True, args.steps)
+    ms_events = timed(args.steps)
     tim = sv.timing_read()
     sv.timing_enable(False)
+    clocks.stop()
     ms = statistics.median(reps)
     value = dof_global * args.steps / (ms * 1e-3)
     nsteps_t = max(1, tim["steps"])
@@ -412,7 +425,9 @@ def run_b200(args):
     peak, peak_src = _peaks()
     launches_per_step = max(1, tim["sweep_launches"] // nsteps_t)
     sweep_ms = tim["sweep_ms"] / max(1, tim["sweep_launches"])
-    dof_per_launch = dof_local / launches_per_step
+    # rotation splits a step's DOF over its 8 octant launches; the implicit
+    # step's launches are whole sweeps (one per source iteration)
+    dof_per_launch = dof_local if args.implicit > 0 else dof_local / launches_per_step
     achieved = BYTES_PER_DOF * dof_per_launch / (sweep_ms * 1e-3) / 1e9
     tpd, tsrc = _traffic_per_dof(p.name)
     per_step = {"sweep": tim["sweep_ms"] / nsteps_t, "newton": tim["newton_ms"] / nsteps_t,
@@ -429,7 +444,7 @@ def run_b200(args):
 
     per_rank = None
     if world > 1:  # per-rank breakdown: compute kernels, halo, the exposed (non-overlapped) remainder
-        mine = dict(rank=rank, step_ms=ms / args.steps, **{k + "_ms": v for k, v in per_step.items()})
+        mine = dict(rank=rank, step_ms=ms_events / args.steps, **{k + "_ms": v for k, v in per_step.items()})
         mine["exposed_ms"] = max(0.0, mine["step_ms"] - mine["sweep_ms"] - mine["newton_ms"] - mine["boundary_ms"])
         gathered = [None] * world
         dist.all_gather_object(gathered, mine)
@@ -484,11 +499,12 @@ def run_b200(args):
             "data": "synthetic (seeded bte_inputs; silicon tables are paper-silent data)",
             "config": config_dict(p, args, world),
             "repeats_ms_per_step": [r / args.steps for r in reps],
-            "timing": f"median of {args.repeats} repeats of {args.steps} steps, CUDA events, max over ranks",
+            "timing": f"median of {args.repeats} repeats of {args.steps} steps, CUDA events, max over ranks; "
+                      f"a further repeat with per-kernel events for the breakdown: {ms_events / args.steps:.4f} ms/step",
             "layout": "octant-slot rotation (one buffer of nslot + 1 regions)" if sv.rotate else "two buffers",
             "simulated_s_per_s": p.dt * args.steps / (ms * 1e-3),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "per_rank": per_rank,
-            "gpu_launches": int(tim["launches"] // max(1, args.repeats)),
+            "gpu_launches": int(tim["launches"]),
             "gpu_launches_note": "library kernel launches inside one timed region of K steps",
             "clocks": clocks.summary(spans),
         }
@@ -513,6 +529,9 @@ def main():
     ap.add_argument("--decomp", default="slab", choices=["slab", "band"])
     ap.add_argument("--semi", type=float, default=0.0,
                     help="semi-implicit step (reading R-l) at this multiple of the workload's dt (0: explicit)")
+    ap.add_argument("--implicit", type=int, default=0,
+                    help="implicit step (reading R-n) with this many source iterations per step (0: explicit)")
+    ap.add_argument("--dt-factor", type=float, default=8.0, help="--implicit: dt as a multiple of the workload's")
     ap.add_argument("--tau", default="lagged", choices=["lagged", "sc"],
                     help="temperature update: lagged tau (reading #15) or self-consistent tau (R-k)")
     args = ap.parse_args()

@@ -521,6 +521,27 @@ def umesh_tet(nx: int, ny: int, nz: int, h: float = 1e-6, jitter: float = 0.1, s
     return UMesh(3, V, np.ascontiguousarray(C), 1.0)
 
 
+def umesh_hex(nx: int, ny: int, nz: int, h: float = 1e-6, jitter: float = 0.1, seed: int = 23,
+              shuffle: bool = False) -> UMesh:
+    """3-D hexahedral mesh: the nx x ny x nz lattice of cubes of side h with
+    jittered interior vertices (faces become bilinear, non-planar), vertices in
+    the Gmsh order (bottom 0-1-2-3 counter-clockwise, top 4-5-6-7 above them);
+    cube-major cell order unless shuffled.  jitter = 0 gives the structured grid
+    in its canonical cell order."""
+    V = _lattice_verts((nx, ny, nz), (h, h, h), jitter, seed)
+    vid = lambda i, j, k: i + (nx + 1) * (j + (ny + 1) * k)  # noqa: E731
+    cells = []
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                cells.append((vid(i, j, k), vid(i + 1, j, k), vid(i + 1, j + 1, k), vid(i, j + 1, k),
+                              vid(i, j, k + 1), vid(i + 1, j, k + 1), vid(i + 1, j + 1, k + 1), vid(i, j + 1, k + 1)))
+    C = np.array(cells, dtype=np.int64)
+    if shuffle:
+        C = C[np.random.Generator(np.random.PCG64(seed + 2)).permutation(len(C))]
+    return UMesh(3, V, np.ascontiguousarray(C), 1.0)
+
+
 def umesh_tet_subbox(m: UMesh, n, box):
     """The cubes [x0,x1) x [y0,y1) x [z0,z1) of a umesh_tet(n[0], n[1], n[2])
     mesh (unshuffled, cube-major order) as a mesh of its own: returns (sub mesh,
@@ -748,13 +769,15 @@ def config_u3(n: int = 32, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20)
 
 
 def small_umesh(dim: int = 2, n=(4, 3, 2), dirs=None, bands=None, bcs=None, dt=1e-12, shuffle=False,
-                jitter=None, seed=17, quad=False) -> Problem:
-    """Small unstructured case for parity tests."""
-    if dim == 2 and quad:
+                jitter=None, seed=17, quad=False, hexa=False) -> Problem:
+    """Small unstructured case for parity tests (hexa: hexahedra in 3-D)."""
+    if dim == 3 and hexa:
+        mesh = umesh_hex(n[0], n[1], n[2], 1e-6, 0.1 if jitter is None else jitter, seed, shuffle)
+    elif dim == 2 and quad:
         mesh = umesh_quad(n[0], n[1], n[0] * 1e-6, n[1] * 1e-6, 0.2 if jitter is None else jitter, seed, shuffle)
     elif dim == 2:
         mesh = umesh_tri(n[0], n[1], n[0] * 1e-6, n[1] * 1e-6, 0.2 if jitter is None else jitter, seed, shuffle)
-    else:
+    elif dim == 3:
         mesh = umesh_tet(n[0], n[1], n[2], 1e-6, 0.1 if jitter is None else jitter, seed, shuffle)
     dirs = dirs if dirs is not None else directions_control_angle(4, 8)
     bands = bands if bands is not None else subset_bands(silicon_bands(29), [0, 5, 17, 28, 30, 39])

@@ -216,6 +216,44 @@ typedef struct {
 BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs, const bte_bands *bands,
                                     const bte_run *run, bte_ctx **out);
 
+/* Mesh import ("A mesh must either be imported
+ * from a Gmsh or MEDIT formatted mesh file, or generated internally").
+ * Host only, no GPU.  Reads an ASCII Gmsh file (format 2.2 or 4.1: $Nodes,
+ * $Elements; element types 2 triangle, 3 quadrangle, 4 tetrahedron; points
+ * and lines are boundary tags and skipped; other sections ignored) or a MEDIT
+ * .mesh file (Dimension, Vertices, Triangles / Quadrilaterals / Tetrahedra,
+ * 1-based, with references; Edges / Corners skipped).  The cells are the
+ * tetrahedra when present (triangles are then boundary faces), else the
+ * triangles or the quadrilaterals (not both).  Node order of the file is kept
+ * (Gmsh node tags are mapped to their position).  *out is allocated by the
+ * library: verts [nverts][3] (z = 0 for 2-D files), cells [ncells][nvc]
+ * 0-based; free it with bte_mesh_free.  The arrays plug into bte_umesh
+ * (depth is the caller's).  Errors: BTE_EINVAL (unreadable file, malformed
+ * record, binary Gmsh, hexahedra / prisms / pyramids, mixed 2-D cell kinds,
+ * index out of range) with the reason in bte_mesh_error(). */
+typedef struct {
+  int dim, nvc;
+  int64_t nverts, ncells;
+  double *verts;
+  int64_t *cells;
+} bte_mesh_data;
+BTE_API bte_status bte_mesh_read(const char *path, bte_mesh_data **out);
+BTE_API void bte_mesh_free(bte_mesh_data *mesh);
+BTE_API const char *bte_mesh_error(void); /* thread-local text of the last mesh-call failure */
+
+/* Recursive coordinate bisection of an unstructured mesh into nparts
+ * (host only): perm[0..ncells) receives a cell order in which part r is the
+ * range [r ncells/nparts, (r+1) ncells/nparts) -- exactly the ranges
+ * bte_create_umesh gives rank r of nparts -- and each part is a compact box
+ * of cell centroids (the centroid set is split at the median of its longest
+ * extent, recursively, parts sized as those ranges; ties by cell index; the
+ * input order is kept inside a part).  Apply it as cells' = cells[perm] (and
+ * state rows likewise) before bte_create_umesh.  The paper partitions with
+ * Metis; any partition works with the halo exchange, this one
+ * keeps halos small for meshes given in arbitrary order.  Errors: BTE_EINVAL
+ * (nparts outside [1, ncells], bad mesh) with the reason in bte_mesh_error(). */
+BTE_API bte_status bte_partition_rcb(const bte_umesh *mesh, int nparts, int64_t *perm);
+
 /* Temperature-update rule for tau(T).
  *   mode 0 (default, reading #15): lagged, beta_next = beta_b(T^n) weights the
  *          Newton for T^{n+1} and the next sweep;

@@ -203,7 +203,8 @@ class Oracle:
     # -- unstructured geometry (tests)
     def geometry(self):
         """(vol[nc], area[nc,K], normal[nc,K,3], nbr[nc,K], region[nc,K]) of an unstructured mesh."""
-        K = int(self.problem.mesh.cells.shape[1])
+        m = self.problem.mesh
+        K = 6 if (m.dim == 3 and m.cells.shape[1] == 8) else int(m.cells.shape[1])  # faces per cell
         vol = np.empty(self.nc)
         area = np.empty((self.nc, K))
         nrm = np.empty((self.nc, K, 3))

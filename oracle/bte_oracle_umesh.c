@@ -25,7 +25,15 @@
  *     (p_{k+1 mod m}, p_{k+2 mod m}), n pointing away from the vertex mean;
  *   tetrahedron (3-D): V = |det(p1-p0, p2-p0, p3-p0)|/6, face k = triangle
  *     of the other three vertices (ascending local order) a, b, c,
- *     A = |(b-a) x (c-a)|/2, n = (b-a) x (c-a) / |.| pointing away from p_k.
+ *     A = |(b-a) x (c-a)|/2, n = (b-a) x (c-a) / |.| pointing away from p_k;
+ *   hexahedron (3-D, "polyhedral cell with m sides"; Gmsh vertex
+ *     order, bottom 0-1-2-3, top 4-5-6-7): faces 0 (0,1,2,3), 1 (4,5,6,7),
+ *     2 (0,1,5,4), 3 (1,2,6,5), 4 (2,3,7,6), 5 (3,0,4,7), each the bilinear
+ *     patch through its four corners (planar when the corners are coplanar):
+ *     area vector S = (q2-q0) x (q3-q1) / 2 (the integral of the normal over
+ *     the patch), A = |S|, n = S/|S| pointing away from the cell's vertex
+ *     mean; V = (1/3) sum_f qbar_f . S_f (divergence theorem with the face
+ *     vertex mean qbar_f, exact for bilinear faces).
  * Boundary faces (no neighbour) must lie on a wall of the vertices' bounding
  * box: all vertices at x = xmin -> region 0, x = xmax -> 1, y -> 2/3, z -> 4/5
  * (tested in that order).  A wall face's normal is the outward axis vector,
@@ -92,7 +100,7 @@ typedef struct {
   long ncells;
   const long *cells;   /* [ncells][nvc] */
   double depth;
-  int nvc;             /* vertices per cell: dim 2 -> 3 (triangles) or m (convex polygons), dim 3 -> 4 */
+  int nvc;             /* vertices per cell: dim 2 -> 3 (triangles) or m (convex polygons), dim 3 -> 4 or 8 */
 } ora_umesh;
 
 typedef struct {
@@ -109,14 +117,17 @@ typedef struct {
 } ora_ugeom;
 
 typedef struct {
-  long key[3];
+  long key[4];
   long cell;
   int k;
 } face_rec;
 
+/* hexahedron faces as cycles of local vertices (Gmsh order) */
+static const int HEXF[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+
 static int face_cmp(const void *a, const void *b) {
   const face_rec *x = (const face_rec *)a, *y = (const face_rec *)b;
-  for (int i = 0; i < 3; i++)
+  for (int i = 0; i < 4; i++)
     if (x->key[i] != y->key[i]) return x->key[i] < y->key[i] ? -1 : 1;
   if (x->cell != y->cell) return x->cell < y->cell ? -1 : 1;
   return x->k - y->k;
@@ -150,8 +161,9 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
   *out = NULL;
   if (m->dim != 2 && m->dim != 3) return ORA_EINVAL;
   const int nvc = m->nvc > 0 ? m->nvc : m->dim + 1;
-  if ((m->dim == 3 && nvc != 4) || (m->dim == 2 && (nvc < 3 || nvc > 8))) return ORA_EINVAL;
-  const int K = nvc, nfv = m->dim; /* faces per cell, vertices per face */
+  if ((m->dim == 3 && nvc != 4 && nvc != 8) || (m->dim == 2 && (nvc < 3 || nvc > 8))) return ORA_EINVAL;
+  const int hexa = m->dim == 3 && nvc == 8;
+  const int K = hexa ? 6 : nvc, nfv = hexa ? 4 : m->dim; /* faces per cell, vertices per face */
   const long nc = m->ncells;
   ora_ugeom *g = (ora_ugeom *)calloc(1, sizeof(ora_ugeom));
   if (!g) return ORA_ENOMEM;
@@ -177,16 +189,41 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
       if (x > hi[a]) hi[a] = x;
     }
   for (long c = 0; c < nc; c++) {
-    const long *cv = m->cells + c * K;
-    for (int k = 0; k < K; k++)
+    const long *cv = m->cells + c * nvc;
+    for (int k = 0; k < nvc; k++)
       if (cv[k] < 0 || cv[k] >= m->nverts) {
         free(fr);
         ora_ugeom_free(g);
         return ORA_EINVAL;
       }
     const double *P[8];
-    for (int k = 0; k < K; k++) P[k] = m->verts + 3 * cv[k];
-    if (m->dim == 2 && K > 3) {
+    for (int k = 0; k < nvc; k++) P[k] = m->verts + 3 * cv[k];
+    if (hexa) {
+      double cm[3] = {0.0, 0.0, 0.0};
+      for (int k = 0; k < 8; k++)
+        for (int t = 0; t < 3; t++) cm[t] += P[k][t];
+      for (int t = 0; t < 3; t++) cm[t] /= 8.0;
+      double vol = 0.0;
+      for (int k = 0; k < 6; k++) {
+        const double *q0 = P[HEXF[k][0]], *q1 = P[HEXF[k][1]], *q2 = P[HEXF[k][2]], *q3 = P[HEXF[k][3]];
+        double d1[3], d2[3], S[3], qb[3];
+        for (int t = 0; t < 3; t++) {
+          d1[t] = q2[t] - q0[t];
+          d2[t] = q3[t] - q1[t];
+          qb[t] = (q0[t] + q1[t] + q2[t] + q3[t]) / 4.0;
+        }
+        S[0] = (d1[1] * d2[2] - d1[2] * d2[1]) / 2.0;
+        S[1] = (d1[2] * d2[0] - d1[0] * d2[2]) / 2.0;
+        S[2] = (d1[0] * d2[1] - d1[1] * d2[0]) / 2.0;
+        if (S[0] * (qb[0] - cm[0]) + S[1] * (qb[1] - cm[1]) + S[2] * (qb[2] - cm[2]) < 0.0)
+          for (int t = 0; t < 3; t++) S[t] = -S[t];
+        double A = sqrt(S[0] * S[0] + S[1] * S[1] + S[2] * S[2]);
+        g->area[c * K + k] = A;
+        for (int t = 0; t < 3; t++) g->nrm[(c * K + k) * 3 + t] = S[t] / A;
+        vol += qb[0] * S[0] + qb[1] * S[1] + qb[2] * S[2];
+      }
+      g->vol[c] = vol / 3.0;
+    } else if (m->dim == 2 && K > 3) {
       double sh = 0.0, cx = 0.0, cy = 0.0;
       for (int k = 0; k < K; k++) {
         const double *a = P[k], *b = P[(k + 1) % K];
@@ -269,7 +306,10 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
       face_rec *f = fr + c * K + k;
       int n = 0;
       f->key[2] = -1;
-      if (m->dim == 2) { /* edge (v_{k+1}, v_{k+2}) (for triangles: the face opposite v_k) */
+      f->key[3] = -1;
+      if (hexa) {
+        for (int i = 0; i < 4; i++) f->key[i] = cv[HEXF[k][i]];
+      } else if (m->dim == 2) { /* edge (v_{k+1}, v_{k+2}) (for triangles: the face opposite v_k) */
         f->key[0] = cv[(k + 1) % K];
         f->key[1] = cv[(k + 2) % K];
       } else {
@@ -289,7 +329,8 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
   long nf = nc * K;
   for (long i = 0; i < nf;) {
     long j = i + 1;
-    while (j < nf && fr[j].key[0] == fr[i].key[0] && fr[j].key[1] == fr[i].key[1] && fr[j].key[2] == fr[i].key[2])
+    while (j < nf && fr[j].key[0] == fr[i].key[0] && fr[j].key[1] == fr[i].key[1] &&
+           fr[j].key[2] == fr[i].key[2] && fr[j].key[3] == fr[i].key[3])
       j++;
     if (j - i > 2) {
       free(fr);
@@ -307,13 +348,16 @@ int ora_ugeom_build(const ora_umesh *m, ora_ugeom **out) {
   for (long c = 0; c < nc; c++)
     for (int k = 0; k < K; k++) {
       if (g->nbr[c * K + k] >= 0) continue;
-      const long *cv = m->cells + c * K;
+      const long *cv = m->cells + c * nvc;
       int reg = -1;
       for (int r = 0; r < 2 * m->dim && reg < 0; r++) {
         int a = r / 2;
         double wall = (r & 1) ? hi[a] : lo[a];
         int all = 1;
-        if (m->dim == 2) {
+        if (hexa) {
+          for (int i = 0; i < 4; i++)
+            if (m->verts[3 * cv[HEXF[k][i]] + a] != wall) all = 0;
+        } else if (m->dim == 2) {
           if (m->verts[3 * cv[(k + 1) % K] + a] != wall || m->verts[3 * cv[(k + 2) % K] + a] != wall) all = 0;
         } else {
           for (int i = 0; i < K; i++)

@@ -122,13 +122,20 @@ def exact_usweep(problem, I, I0c, betac):
     for a face f of cell c, A_f n_f / V_c is computed without square roots --
       triangle: A_f n_f = depth * perp(edge), V = depth * |cross| / 2,
       tetrahedron: A_f n_f = cross(b - a, c - a) / 2, V = |det| / 6,
-    oriented away from the opposite vertex.  Faces are matched by their vertex
+    oriented away from the opposite vertex;
+      hexahedron (8 vertices, Gmsh order): face = bilinear patch through its
+      4 corners q0..q3, A_f n_f = cross(q2 - q0, q3 - q1) / 2 (the integral of
+      the normal over the patch), oriented away from the vertex mean;
+      V = sum_f qbar_f . A_f n_f / 3 (divergence theorem, exact for such
+      faces; qbar_f the mean of the face's corners).  Faces are matched by their vertex
     sets; a boundary face's wall is the box plane all its vertices lie on.
     Returns Fractions [nc, nd, nb].  LINEAR channel tables only."""
     m, dr, bd = problem.mesh, problem.dirs, problem.bands
     assert bd.mode == 0, "exact twin supports LINEAR channels only"
     nd, nb = dr.nd, bd.nb
-    K = int(m.cells.shape[1])
+    hexa = m.dim == 3 and int(m.cells.shape[1]) == 8
+    HEXF = ((0, 1, 2, 3), (4, 5, 6, 7), (0, 1, 5, 4), (1, 2, 6, 5), (2, 3, 7, 6), (3, 0, 4, 7))
+    K = 6 if hexa else int(m.cells.shape[1])
     P = [[Fr(float(x)) for x in row] for row in m.verts]
     cells = [[int(v) for v in row] for row in m.cells]
     nc = len(cells)
@@ -143,7 +150,9 @@ def exact_usweep(problem, I, I0c, betac):
     I0f = np.vectorize(Fr, otypes=[object])(np.asarray(I0c, dtype=np.float64))
     bf = np.vectorize(Fr, otypes=[object])(np.asarray(betac, dtype=np.float64))
     refl = {a: _reflect_map(dr.s, a) for a in range(m.dim)}
-    def face_verts(cv, k):  # 2-D: edge (v_{k+1}, v_{k+2}); 3-D: the face opposite v_k
+    def face_verts(cv, k):  # 2-D: edge (v_{k+1}, v_{k+2}); 3-D: the face opposite v_k; hexahedron: HEXF[k]
+        if hexa:
+            return [cv[i] for i in HEXF[k]]
         if m.dim == 2:
             return [cv[(k + 1) % K], cv[(k + 2) % K]]
         return cv[:k] + cv[k + 1:]
@@ -165,7 +174,21 @@ def exact_usweep(problem, I, I0c, betac):
     geo = []  # per cell: volume, [(An vector, neighbour or None, region)]
     for c, cv in enumerate(cells):
         X = [P[i] for i in cv]
-        if m.dim == 2:  # shoelace (for a triangle: |cross| / 2)
+        if hexa:
+            cm = [sum((X[k][a] for k in range(8)), Fr(0)) / 8 for a in range(3)]
+            V = Fr(0)
+            hexS = []
+            for k in range(6):
+                q = [X[i] for i in HEXF[k]]
+                d1, d2 = sub(q[2], q[0]), sub(q[3], q[1])
+                S = [(d1[1] * d2[2] - d1[2] * d2[1]) / 2, (d1[2] * d2[0] - d1[0] * d2[2]) / 2,
+                     (d1[0] * d2[1] - d1[1] * d2[0]) / 2]
+                qb = [(q[0][a] + q[1][a] + q[2][a] + q[3][a]) / 4 for a in range(3)]
+                if dot(S, sub(qb, cm)) < 0:
+                    S = [-x for x in S]
+                V += dot(qb, S) / 3
+                hexS.append(S)
+        elif m.dim == 2:  # shoelace (for a triangle: |cross| / 2)
             sh = sum((X[k][0] * X[(k + 1) % K][1] - X[(k + 1) % K][0] * X[k][1] for k in range(K)), Fr(0))
             V = abs(sh) / 2 * depth
             cen = [sum((X[k][a] for k in range(K)), Fr(0)) / K for a in range(3)]
@@ -176,7 +199,10 @@ def exact_usweep(problem, I, I0c, betac):
             V = abs(det) / 6
         faces = []
         for k in range(K):
-            if m.dim == 2:
+            if hexa:
+                others = [P[v] for v in face_verts(cv, k)]
+                An = hexS[k]
+            elif m.dim == 2:
                 others = [P[v] for v in face_verts(cv, k)]
                 e = sub(others[1], others[0])
                 An = [e[1] * depth, -e[0] * depth, Fr(0)]

@@ -26,7 +26,8 @@ I0_LINEAR, I0_BOSE_EINSTEIN = 0, 1
 EXPORTS = ("bte_group_step", "bte_plan_slab", "bte_plan_band", "bte_create", "bte_create_band", "bte_create_umesh", "bte_get_region_faces", "bte_plan_umesh", "bte_set_tau_mode", "bte_set_step_mode", "bte_set_bc", "bte_set_bc_partial", "bte_set_state", "bte_init_random", "bte_step",
            "bte_get_intensity", "bte_get_intensity_cells", "bte_get_temperature", "bte_get_energy", "bte_debug_substep",
            "bte_timing_enable", "bte_timing_read", "bte_get_info", "bte_last_error", "bte_destroy",
-           "bte_version", "bte_set_debug", "bte_set_implicit", "bte_get_iterations")
+           "bte_version", "bte_set_debug", "bte_set_implicit", "bte_get_iterations", "bte_mesh_read",
+           "bte_mesh_free", "bte_mesh_error", "bte_partition_rcb")
 DEBUG_SKIP_EXCHANGE = 1
 
 
@@ -54,6 +55,11 @@ class UPeerC(C.Structure):
 class UPlanC(C.Structure):
     _fields_ = [("cell0", C.c_int64), ("n_own", C.c_int64), ("n_halo", C.c_int64), ("n_peers", C.c_int),
                 ("peer", UPeerC * 32)]
+
+
+class MeshDataC(C.Structure):
+    _fields_ = [("dim", C.c_int), ("nvc", C.c_int), ("nverts", C.c_int64), ("ncells", C.c_int64),
+                ("verts", C.POINTER(C.c_double)), ("cells", C.POINTER(C.c_int64))]
 
 
 class Dirs(C.Structure):
@@ -147,6 +153,11 @@ def load_library(path: str = LIB_PATH):
     lib.bte_debug_substep.argtypes = [P, C.c_int, dp, C.c_size_t]
     lib.bte_set_debug.argtypes = [P, C.c_int, C.c_int]
     lib.bte_set_implicit.argtypes = [P, C.c_int, C.c_double]
+    lib.bte_mesh_read.argtypes = [C.c_char_p, C.POINTER(C.POINTER(MeshDataC))]
+    lib.bte_mesh_free.argtypes = [C.POINTER(MeshDataC)]
+    lib.bte_mesh_free.restype = None
+    lib.bte_mesh_error.restype = C.c_char_p
+    lib.bte_partition_rcb.argtypes = [C.POINTER(UMeshC), C.c_int, C.c_void_p]
     lib.bte_get_iterations.argtypes = [P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
     lib.bte_timing_enable.argtypes = [P, C.c_int, C.c_int64]
     lib.bte_timing_read.argtypes = [P, C.POINTER(Timing)]
@@ -158,7 +169,8 @@ def load_library(path: str = LIB_PATH):
     lib.bte_destroy.restype = None
     lib.bte_version.restype = C.c_char_p
     for name in EXPORTS:
-        if name not in ("bte_last_error", "bte_destroy", "bte_version") and hasattr(lib, name):
+        if name not in ("bte_last_error", "bte_destroy", "bte_version", "bte_mesh_free", "bte_mesh_error") and \
+                hasattr(lib, name):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -481,3 +493,36 @@ def plan_umesh(mesh, nranks: int, rank: int) -> dict:
                   send=send[out.peer[k].send_off:out.peer[k].send_off + out.peer[k].send_cnt].copy())
              for k in range(out.n_peers)]
     return dict(cell0=out.cell0, n_own=out.n_own, n_halo=out.n_halo, halo=halo[:out.n_halo].copy(), peers=peers)
+
+
+def read_mesh(path: str, depth: float = 1.0):
+    """bte_mesh_read (host only): a Gmsh (ASCII 2.2 / 4.1) or MEDIT .mesh file as
+    a bte_inputs.UMesh (vertex coordinates [n, 3], cells [nc, m] 0-based)."""
+    import bte_inputs as bi
+    lib = load_library()
+    out = C.POINTER(MeshDataC)()
+    st = lib.bte_mesh_read(os.fsencode(path), C.byref(out))
+    if st != BTE_OK:
+        raise BteError(st, lib.bte_mesh_error().decode(errors="replace"))
+    try:
+        m = out.contents
+        verts = np.ctypeslib.as_array(m.verts, shape=(m.nverts, 3)).copy()
+        cells = np.ctypeslib.as_array(m.cells, shape=(m.ncells, m.nvc)).copy()
+        return bi.UMesh(int(m.dim), verts, cells, float(depth))
+    finally:
+        lib.bte_mesh_free(out)
+
+
+def partition_rcb(mesh, nparts: int) -> np.ndarray:
+    """bte_partition_rcb (host only): a cell permutation whose ranges
+    [r N/P, (r+1) N/P) are compact parts (recursive coordinate bisection)."""
+    lib = load_library()
+    verts = np.ascontiguousarray(mesh.verts, dtype=np.float64)
+    cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
+    m = UMeshC(int(mesh.dim), verts.shape[0], _p(verts), cells.shape[0], _p(cells), float(mesh.depth),
+               int(cells.shape[1]))
+    perm = np.empty(cells.shape[0], dtype=np.int64)
+    st = lib.bte_partition_rcb(C.byref(m), int(nparts), _p(perm))
+    if st != BTE_OK:
+        raise BteError(st, lib.bte_mesh_error().decode(errors="replace"))
+    return perm

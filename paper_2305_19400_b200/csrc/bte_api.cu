@@ -98,11 +98,19 @@ struct bte_ctx {
   int l2hint = 0;          // env BTE_L2HINT
   int no_spare = 0;        // env BTE_SPARE=0: side jobs on compute threads (A/B)
   int raster = 0;          // 3-D sweep column order (SweepArgs.raster); env BTE_RASTER
-  int l2pf = 0;            // L2 prefetch distance of the sweep's own blocks (SweepArgs.l2pf); env BTE_L2PF
   int sc_direct = 0;       // env BTE_SC_DIRECT=1: direct band integrals in the self-consistent Newton (A/B)
   int ugeneric = 0;        // env BTE_UGENERIC=1: generic unstructured sweep (A/B)
   int dbg_skip_exchange = 0;  // bte_set_debug(BTE_DEBUG_SKIP_EXCHANGE): mutation tests only
   double *d_energy = nullptr; // bte_get_energy scratch
+  // CUDA-graph replay of explicit steps (SURVEY 8(b) "graph replay"): one
+  // captured step per buffer parity, rebuilt when a setter changes the step
+  int use_graph = 1;           // env BTE_GRAPH=0 disables (A/B)
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t graph_launches = 0;  // kernels in one captured step
+  bool graph_capture = false;  // step_launch is being captured (Newton reads the device step index)
+  cudaStream_t cap_stream = nullptr;  // private stream the step graphs are captured on
+  unsigned long long *d_stepctr = nullptr;
+  unsigned long long h_stepctr = 0;
   double *staging = nullptr;
   int64_t staging_cells = 0;
   int seg_len = 0;
@@ -271,6 +279,8 @@ static bte_status sync_check(bte_ctx *ctx) {
 }
 
 extern "C" {
+
+static void graph_invalidate(bte_ctx *ctx);
 
 static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream = nullptr);
 static bte_status uhalo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream);
@@ -625,6 +635,7 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
 
 bte_status bte_set_step_mode(bte_ctx *ctx, int mode) {
   if (!ctx) return BTE_EINVAL;
+  graph_invalidate(ctx);
   if (mode < 0 || mode > 2)
     return fail(ctx, BTE_EINVAL, "step mode must be 0 (explicit), 1 (semi-implicit) or 2 (implicit)");
   if (mode == 1 && ctx->band) return fail(ctx, BTE_EINVAL, "semi-implicit step: not for band contexts");
@@ -663,6 +674,7 @@ bte_status bte_get_iterations(const bte_ctx *ctx, int64_t *out, int64_t n, int64
 
 bte_status bte_set_tau_mode(bte_ctx *ctx, int mode) {
   if (!ctx) return BTE_EINVAL;
+  graph_invalidate(ctx);
   if (mode != 0 && mode != 1) return fail(ctx, BTE_EINVAL, "tau mode must be 0 (lagged) or 1 (self-consistent)");
   if (mode == 1 && (ctx->semi || ctx->implicit)) return fail(ctx, BTE_EINVAL, "self-consistent tau: explicit step only");
   if (mode == 1 && ctx->band)
@@ -1199,7 +1211,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   // config 4: DRAM 20.3 -> 17.6 B/DOF per sweep launch)
   ctx->raster = g.dim == 3 ? 16 : 0;
   if (const char *e = getenv("BTE_RASTER")) ctx->raster = std::max(0, atoi(e));
-  if (const char *e = getenv("BTE_L2PF")) ctx->l2pf = std::max(0, std::min(64, atoi(e)));
+  if (const char *e = getenv("BTE_GRAPH")) ctx->use_graph = atoi(e) != 0;
   if (const char *e = getenv("BTE_SC_DIRECT")) ctx->sc_direct = atoi(e) != 0;
   if (const char *e = getenv("BTE_UGENERIC")) ctx->ugeneric = atoi(e) != 0;
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
@@ -1247,6 +1259,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
 
 bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, double T_uniform) {
   if (!ctx) return BTE_EINVAL;
+  graph_invalidate(ctx);
   const int nreg = ctx->mesh.dim == 3 ? 6 : 4;
   if (region < 0 || region >= nreg) return fail(ctx, BTE_EINVAL, "region %d out of range", region);
   if (kind == BTE_BC_SPECULAR) {
@@ -1289,6 +1302,7 @@ bte_status bte_set_bc(bte_ctx *ctx, int region, int kind, const double *T_wall, 
 
 bte_status bte_set_bc_partial(bte_ctx *ctx, int region, double specularity) {
   if (!ctx) return BTE_EINVAL;
+  graph_invalidate(ctx);
   const int nreg = ctx->mesh.dim == 3 ? 6 : 4;
   if (region < 0 || region >= nreg) return fail(ctx, BTE_EINVAL, "region %d out of range", region);
   if (!(specularity >= 0.0 && specularity <= 1.0))
@@ -1444,6 +1458,7 @@ static int n_diffuse(const bte_ctx *ctx) {
 static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   NewtonArgs a{};
   a.sc_direct = ctx->sc_direct;
+  a.step_ctr = ctx->graph_capture ? ctx->d_stepctr : nullptr;
   a.m = ctx->mF;
   a.Dpart = ctx->Dpart;
   a.T = ctx->T;
@@ -1502,7 +1517,6 @@ static SweepArgs sweep_args(const bte_ctx *ctx, const double *Iin, double *Iout,
   a.l2hint = ctx->l2hint;
   a.no_spare = ctx->no_spare;
   a.raster = ctx->raster;
-  a.l2pf = ctx->l2pf;
   return a;
 }
 
@@ -1771,6 +1785,61 @@ static bte_status implicit_step(bte_ctx *ctx, bool t) {
   return BTE_OK;
 }
 
+static void graph_invalidate(bte_ctx *ctx) {
+  for (auto &e : ctx->gexec)
+    if (e) {
+      cudaGraphExecDestroy(e);
+      e = nullptr;
+    }
+}
+
+// One explicit step by replaying its captured graph (one context, two
+// buffers, no timing): the launches of step_launch for this buffer parity,
+// plus k_step_tick for the device step index the Newton's error key reads.
+static bte_status graph_step(bte_ctx *ctx) {
+  const int par = ctx->cur;
+  if (!ctx->gexec[par]) {
+    if (!ctx->d_stepctr) {
+      ctx->d_stepctr = (unsigned long long *)dev_alloc(ctx, sizeof(unsigned long long));
+      if (!ctx->d_stepctr) return fail(ctx, BTE_ENOMEM, "graph step counter");
+    }
+    const int64_t l0 = ctx->tacc.launches;
+    cudaGraph_t graph = nullptr;
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on ctx->stream
+    if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    cudaError_t e0 = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed);
+    if (e0 != cudaSuccess) {
+      ctx->stream = user;
+      CU(e0);
+    }
+    ctx->graph_capture = true;
+    bte_status st = step_launch(ctx, false);
+    cudaError_t e = st ? cudaSuccess : launch_step_tick(ctx->d_stepctr, ctx->stream);
+    ctx->graph_capture = false;
+    cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &graph);
+    ctx->stream = user;
+    if (st) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    CU(e);
+    CU(e2);
+    e = cudaGraphInstantiate(&ctx->gexec[par], graph, 0);
+    cudaGraphDestroy(graph);
+    CU(e);
+    ctx->graph_launches = ctx->tacc.launches - l0 + 1;
+    ctx->tacc.launches = l0;
+  }
+  ctx->h_stepctr = (unsigned long long)ctx->steps_done;
+  CU(cudaMemcpyAsync(ctx->d_stepctr, &ctx->h_stepctr, sizeof ctx->h_stepctr, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaGraphLaunch(ctx->gexec[par], ctx->stream));
+  ctx->tacc.launches += ctx->graph_launches;
+  return BTE_OK;
+}
+
 // Band partition, first half of a step: boundary + sweep of this part's
 // channels, then its partial S_r = sum_{b in part} c_b D_b into row `rank`
 // of Sall (the bands couple only through this reduction).
@@ -1851,6 +1920,15 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
   }
   for (int64_t s = 0; s < nsteps; ++s) {
     const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
+    // graph replay for repeated steps of a single two-buffer context (the
+    // rotated layout changes its slot map every step; groups exchange halos)
+    const bool graph = ctx->use_graph && nsteps > 1 && !t && ctx->nranks == 1 && !ctx->rot && !ctx->band;
+    if (graph) {
+      if ((st = graph_step(ctx))) return st;
+      ctx->cur = 1 - ctx->cur;
+      ctx->steps_done++;
+      continue;
+    }
     if ((st = step_launch(ctx, t, ctx->nranks > 1 && ctx->overlap))) return st;
     if (ctx->nranks > 1) {
       // a5 on the comm stream once the boundary planes are swept; the next
@@ -2335,6 +2413,8 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
 void bte_destroy(bte_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
+  graph_invalidate(ctx);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);

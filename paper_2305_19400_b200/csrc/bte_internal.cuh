@@ -108,6 +108,7 @@ struct NewtonArgs {
   int sc_direct;          // self-consistent tau: direct band integrals even on uniform grids (A/B)
   int beta_fixed;         // implicit step (R-n): weights from the stored beta_next, not beta(T)
   unsigned long long *dTmax;  // implicit step: max_c |T^{k+1} - T^k| / T^k (double bits), or null
+  const unsigned long long *step_ctr;  // graph replay: device step index for the error key (else `step`)
 };
 
 struct SweepArgs {
@@ -135,7 +136,6 @@ struct SweepArgs {
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
   int no_spare;           // 1: side jobs on compute threads (A/B switch read at create)
   int raster;             // 3-D column order: strips of `raster` columns along x (0: row-major)
-  int l2pf;               // L2 prefetch distance (cells beyond the TMA ring) of the own block, 0: off
 };
 
 // Unstructured simplex mesh, device view.  The state layout
@@ -177,6 +177,7 @@ cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, doubl
                            cudaStream_t s, unsigned long long *chg = nullptr);
 cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s,
                                  unsigned long long *chg = nullptr);
+cudaError_t launch_step_tick(unsigned long long *ctr, cudaStream_t s);
 cudaError_t launch_sweep_imp(const SweepArgs &a, const int2 *tasks, int ntasks, int *prog, unsigned *ticket,
                              cudaStream_t s);
 cudaError_t launch_iso_table(const Material &m, const double *Tw, int64_t nf, double *gtab,

@@ -308,10 +308,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-// bulk prefetch of global memory into L2 (no shared-memory destination)
-__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -383,8 +379,9 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
   double *red = coef + 4 * nj;                                   // [2][JG*nb]
   double *stage0 = red + 2 * JG * nb;                            // [S][stage_doubles]
   const int64_t sd = A.stage_doubles;                            // own | xup | (yup) | I0 | beta
-  const int nblk = 1 + (xghost ? 0 : 1) + ((DIM == 3 && !yghost) ? 1 : 0);
-  const int o_x = Es, o_y = 2 * Es, o_i0 = (DIM == 3 ? 3 : 2) * Es, o_be = o_i0 + nb;
+  constexpr bool ystage = DIM == 3;  // y-upwind block in the stage
+  const int nblk = 1 + (xghost ? 0 : 1) + ((ystage && !yghost) ? 1 : 0);
+  const int o_x = Es, o_y = 2 * Es, o_i0 = (ystage ? 3 : 2) * Es, o_be = o_i0 + nb;
   const bool rows_tma = (nb % 2) == 0;  // 16-B bulk-copy granularity; else direct loads
 
   const int pb = A.p_lo + blockIdx.z * A.seg_len;
@@ -412,11 +409,11 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
       const uint64_t keep = l2_policy(A.l2hint == 2 ? 2 : 0), last = l2_policy(1);
       bulk_g2s_hint(sp, Is + base, blk, &full[st], keep);
       if (!xghost) bulk_g2s_hint(sp + o_x, Is + base + xoff, blk, &full[st], DIM == 3 ? keep : last);
-      if (DIM == 3 && !yghost) bulk_g2s_hint(sp + o_y, Is + base + yoff, blk, &full[st], last);
+      if (ystage && !yghost) bulk_g2s_hint(sp + o_y, Is + base + yoff, blk, &full[st], last);
     } else {
       bulk_g2s(sp, Is + base, blk, &full[st]);
       if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
-      if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
+      if (ystage && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
     }
     if (rows_tma) {
       bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
@@ -430,19 +427,8 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
   }
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
   __syncthreads();
-  // L2 prefetch of the own block PF cells beyond the ring (A.l2pf = PF > 0):
-  // the DRAM latency is paid ahead of the ring, whose copies then hit L2
-  const int PF = A.l2pf;
-  auto prefetch = [&](int i) {
-    if (PF > 0 && i < np) {
-      const int pp = pfirst + i * step;
-      bulk_prefetch_l2(Is + (int64_t)(pp + g.plane_off) * g.plane_stride + colE, (uint32_t)Es * 8u);
-    }
-  };
-  if (tid == tis) {
+  if (tid == tis)
     for (int i = 0; i < min(S, np); ++i) issue(i, i);
-    for (int i = S; i < S + PF; ++i) prefetch(i);
-  }
 
   const double v = A.v[active ? b : 0];
   const int e0 = j0 * nb + b;  // this thread's first element; element k is e0 + k*nb
@@ -490,8 +476,8 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
 #pragma unroll
         for (int k = 0; k < JMAX; ++k) {
           const double Ic = so[k * nb];
-          const double In = bte_update<DIM>(Ic, sx[k * nb], DIM == 3 ? sy[k * nb] : 0.0, prev[k], cq + 4 * k, v,
-                                            I0, dtb);
+          const double In = bte_update<DIM>(Ic, sx[k * nb], DIM == 3 ? sy[k * nb] : 0.0, prev[k],
+                                            cq + 4 * k, v, I0, dtb);
           __stcs(op + k * nb, In);  // evict-first: I^{n+1} is not re-read this step
           acc = fma(cq[4 * k + 3], I0 - In, acc);
           prev[k] = Ic;
@@ -533,7 +519,6 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
     if (tid == tis && i + S < np) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S, st);
-      prefetch(i + S + PF);
     }
     if (reducer) {
       double s = 0.0;
@@ -594,7 +579,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
   // blocks under 384 doubles: the direct-load kernel keeps more cells in
   // flight than a per-cell TMA ring (measured: demo 0.089 vs 0.110 ms)
   if (tma && g.E >= 384) {
-    // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B
+    // stage: own | xup | (yup) | I0 row | beta row, rounded to 128 B (y-direct: no yup)
     const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.Es + 2 * g.nb + 15) / 16 * 16;
     const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
     const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;  // two CTAs/SM
@@ -616,6 +601,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
     break;                                                                           \
   }
 #define BTE_LAUNCH(N, NB) BTE_LAUNCH_S(N, NB, 0)
+
     if (g.nb == 40 && jcase == 5 && tthreads <= 448 && S >= 2 && S <= 4) {
       switch (S) {
         case 2: BTE_LAUNCH_S(5, 40, 2)
@@ -643,6 +629,7 @@ static cudaError_t launch_sweep_dim(const SweepArgs &a0, cudaStream_t s) {
     }
 #undef BTE_LAUNCH
 #undef BTE_LAUNCH_S
+
     return cudaGetLastError();
   }
   const size_t smem = (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
@@ -944,6 +931,14 @@ cudaError_t launch_sweep_imp(const SweepArgs &a, const int2 *tasks, int ntasks, 
                              cudaStream_t s) {
   return a.g.dim == 3 ? launch_sweep_imp_dim<3>(a, tasks, ntasks, prog, ticket, s)
                       : launch_sweep_imp_dim<2>(a, tasks, ntasks, prog, ticket, s);
+}
+
+// CUDA-graph replay of steps: the step index of the error key lives on the device
+__global__ void k_step_tick(unsigned long long *ctr) { ++*ctr; }
+
+cudaError_t launch_step_tick(unsigned long long *ctr, cudaStream_t s) {
+  k_step_tick<<<1, 1, 0, s>>>(ctr);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- diffuse ghosts
@@ -1377,7 +1372,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
   }
   if (status != ERR_NONE) {
     if (lane == 0) {
-      const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+      const unsigned long long key = ((unsigned long long)(a.step_ctr ? *a.step_ctr : (unsigned long long)a.step) << 40) | ((unsigned long long)status << 36) |
                                      (unsigned long long)(a.cell0_global + c);
       atomicMin(a.err, key);
     }
@@ -1550,7 +1545,7 @@ __global__ void __launch_bounds__(256) k_newton_sc(const NewtonArgs a) {
     }
     if (status != ERR_NONE) {
       if (lane == 0) {
-        const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+        const unsigned long long key = ((unsigned long long)(a.step_ctr ? *a.step_ctr : (unsigned long long)a.step) << 40) | ((unsigned long long)status << 36) |
                                        (unsigned long long)(a.cell0_global + c);
         atomicMin(a.err, key);
       }
@@ -1661,7 +1656,7 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const Newto
     }
     if (status != ERR_NONE) {
       if (lane == 0) {
-        const unsigned long long key = ((unsigned long long)a.step << 40) | ((unsigned long long)status << 36) |
+        const unsigned long long key = ((unsigned long long)(a.step_ctr ? *a.step_ctr : (unsigned long long)a.step) << 40) | ((unsigned long long)status << 36) |
                                        (unsigned long long)(a.cell0_global + c);
         atomicMin(a.err, key);
       }

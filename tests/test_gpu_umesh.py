@@ -346,3 +346,56 @@ def test_umesh_full_size_u3_sampled(Solver):
         worst_T = max(worst_T, abs(Tg[gids[si]] - To[lc]))
         worst_rel = max(worst_rel, float(np.max(np.abs(Is[si] - Io[lc]) / np.abs(Io[lc]))))
     assert worst_rel <= REL_I and worst_T <= ABS_T, (worst_rel, worst_T)
+
+
+# ----------------------------------------------------------------- mesh import and RCB partition
+
+@pytest.mark.parametrize("kind", ["tet", "quad"])
+def test_imported_mesh_parity(Solver, tmp_path, kind):
+    """A mesh read from a Gmsh file (bte_mesh_read) runs on the GPU
+    and matches the oracle run on the generator's arrays."""
+    import test_mesh_io as tio
+    from paper_2305_19400_b200 import read_mesh
+    if kind == "tet":
+        p = bi.small_umesh(3, (3, 3, 2), shuffle=True)
+    else:
+        p = bi.small_umesh(2, (5, 4, 1), quad=True)
+    path = str(tmp_path / "m.msh")
+    tio._gmsh41(path, p.mesh)
+    m = read_mesh(path, depth=p.mesh.depth)
+    q = bi.Problem(p.name + "_imported", m, p.dirs, p.bands, p.dt, p.T_init, p.bcs, p.nsteps, p.seed)
+    o = oracle.Oracle(p)  # the generator's mesh
+    I, T = o.random_state()
+    Io, To, _, _ = o.run(I, T, 4)
+    with Solver.from_problem(q) as sv:
+        sv.set_state(I, T)
+        sv.step(4)
+        rel, dT = _cmp(sv.intensity(), sv.temperature(), Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+@pytest.mark.parametrize("kind,P", [("tri", 3), ("tet", 4)])
+def test_rcb_partitioned_group_parity(Solver, kind, P):
+    """A randomly ordered mesh reordered by bte_partition_rcb, then split over
+    P contexts (the cell-range partition now follows the RCB parts): the
+    gathered result matches the oracle on the reordered mesh."""
+    from paper_2305_19400_b200 import partition_rcb
+    if kind == "tri":
+        p = bi.small_umesh(2, (9, 7, 1), shuffle=True)
+    else:
+        p = bi.small_umesh(3, (4, 4, 3), shuffle=True)
+    perm = partition_rcb(p.mesh, P)
+    p.mesh = bi.UMesh(p.mesh.dim, p.mesh.verts, np.ascontiguousarray(p.mesh.cells[perm]), p.mesh.depth)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    Io, To, _, _ = o.run(I, T, 4)
+    group = _part_group(Solver, p, P, I, T)
+    try:
+        Solver.group_step(group, 4)
+        Ig = np.concatenate([s.intensity() for s in group])
+        Tg = np.concatenate([s.temperature() for s in group])
+    finally:
+        for s in group:
+            s.close()
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)

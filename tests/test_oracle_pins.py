@@ -582,10 +582,11 @@ def _u_meshes():
         "tri_shuffled": bi.umesh_tri(3, 3, 3e-7, 3e-7, jitter=0.2, seed=4, shuffle=True),
         "tet": bi.umesh_tet(2, 2, 2, 1e-7, jitter=0.1, seed=5, shuffle=True),
         "quad": bi.umesh_quad(4, 3, 4e-7, 3e-7, jitter=0.2, seed=6, shuffle=True),
+        "hex": bi.umesh_hex(2, 2, 2, 1e-7, jitter=0.1, seed=7, shuffle=True),
     }
 
 
-@pytest.mark.parametrize("case", ["tri", "tri_shuffled", "tet", "quad"])
+@pytest.mark.parametrize("case", ["tri", "tri_shuffled", "tet", "quad", "hex"])
 def test_usweep_exact_rational(case):
     """The unstructured sweep against the exact-rational twin written from
     Eq. 3 with square-root-free geometry (A_f n_f / V_c rational), all wall
@@ -625,7 +626,7 @@ def test_ugeometry_closure_and_volume():
         box = L[0] * L[1] * (L[2] if mesh.dim == 3 else mesh.depth)
         assert abs(vol.sum() / box - 1) < 1e-13
         for c in range(mesh.ncells):
-            for k in range(mesh.dim + 1):
+            for k in range(nbr.shape[1]):  # faces per cell: dim + 1, 4 (quadrilateral), 6 (hexahedron)
                 e = nbr[c, k]
                 if e < 0:
                     assert reg[c, k] >= 0
@@ -641,13 +642,14 @@ def test_ugeometry_closure_and_volume():
 
 
 @pytest.mark.parametrize("kind", [bi.BC_SPECULAR, bi.BC_DIFFUSE, bi.BC_PARTIAL])
-@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dim", [2, 3, "hex"])
 def test_ustep_closed_box_conservation(kind, dim):
     """Closed box of adiabatic walls: interior face fluxes cancel pairwise and
     the walls carry no net flux, so the energy is conserved."""
     b = bi.subset_bands(bi.silicon_bands(29), [2, 19, 33])
     bcs = [bi.WallBC(kind, specularity=0.6) for _ in range(6)]
-    p = bi.small_umesh(dim, (4, 3, 2), bands=b, bcs=bcs, dirs=bi.directions_control_angle(2, 8))
+    p = bi.small_umesh(3 if dim == "hex" else dim, (4, 3, 2), bands=b, bcs=bcs,
+                       dirs=bi.directions_control_angle(2, 8), hexa=dim == "hex")
     o = oracle.Oracle(p)
     I, T0 = o.random_state()
     T, I0c, betac = o.solve_T(I, T0)
@@ -657,14 +659,14 @@ def test_ustep_closed_box_conservation(kind, dim):
     assert I2.min() > 0 and np.max(np.abs(I2 / I - 1)) > 1e-4
 
 
-@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dim", [2, 3, "hex"])
 def test_ustep_uniform_fixed_point(dim):
     """Uniform equilibrium with specular/diffuse walls and isothermal walls at
     the same temperature stays fixed (Eq. 3 with sum_f A_f n_f = 0)."""
     b = bi.subset_bands(bi.silicon_bands(29), [0, 20, 39])
     bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 300.0), bi.WallBC(3, specularity=0.5),
            bi.WallBC(1), bi.WallBC(0, None, 300.0)]
-    p = bi.small_umesh(dim, (4, 3, 2), bands=b, bcs=bcs)
+    p = bi.small_umesh(3 if dim == "hex" else dim, (4, 3, 2), bands=b, bcs=bcs, hexa=dim == "hex")
     o = oracle.Oracle(p)
     T = np.full(p.mesh.ncells, 300.0)
     I = o.equilibrium(T)
@@ -922,6 +924,29 @@ def test_uquad_mesh_equals_structured_grid(dirs):
     Iu, Tu, _, _ = ou.run(I, T, 6)
     assert np.max(np.abs(Iu / Is - 1)) < 1e-12 and np.max(np.abs(Tu - Ts)) < 1e-9
     assert np.max(np.abs(Is / I - 1)) > 1e-4  # the run does move the state
+
+
+def test_uhex_mesh_equals_structured_grid():
+    """An unjittered hexahedral mesh in cube-major order IS the 3-D structured
+    grid: the unstructured oracle (face sums over the 6 faces, Eq. 3 for
+    m-sided polyhedra) and the structured oracle agree to
+    rounding over a multi-step run with every wall kind."""
+    h = 2.0 ** -20
+    nx, ny, nz = 4, 3, 3
+    d = bi.directions_control_angle(4, 8)
+    b = bi.subset_bands(bi.silicon_bands(29), [0, 12, 30])
+    bcs = [bi.WallBC(bi.BC_SPECULAR), bi.WallBC(bi.BC_DIFFUSE), bi.WallBC(0, None, 305.0),
+           bi.WallBC(bi.BC_PARTIAL, specularity=0.4), bi.WallBC(0, 298.0 + np.arange(nx * ny)), bi.WallBC(1)]
+    ps = bi.Problem("grid", bi.Mesh(3, nx, ny, nz, h, h, h), d, b, 1e-13, 300.0, bcs, seed=4)
+    pu = bi.Problem("hex", bi.umesh_hex(nx, ny, nz, h, jitter=0.0), d, b, 1e-13, 300.0, bcs, seed=4)
+    os_, ou = oracle.Oracle(ps), oracle.Oracle(pu)
+    for r in range(6):
+        assert ou.n_region_faces(r) == os_.n_region_faces(r)
+    I, T = os_.random_state()
+    Is, Ts, _, _ = os_.run(I, T, 6)
+    Iu, Tu, _, _ = ou.run(I, T, 6)
+    assert np.max(np.abs(Iu / Is - 1)) < 1e-12 and np.max(np.abs(Tu - Ts)) < 1e-9
+    assert np.max(np.abs(Is / I - 1)) > 1e-4
 
 
 def test_fig9_corner_source_heats_its_corner():
