@@ -177,7 +177,12 @@ BTE_API bte_status bte_create_band(const bte_mesh *mesh, const bte_dirs *dirs, c
  *   dim 2: triangles (nvc 3) or convex quadrilaterals (nvc 4), verts z
  *          ignored, depth = z extent; face k = edge (v_{k+1}, v_{k+2})
  *          (for a triangle: the edge opposite v_k);
- *   dim 3: tetrahedra, cells[c][0..3]; face k = the face opposite v_k.  The domain is
+ *   dim 3: tetrahedra, cells[c][0..3]; face k = the face opposite v_k;
+ *          or hexahedra (nvc 8, Gmsh order: bottom 0-1-2-3, top 4-5-6-7),
+ *          faces (0,1,2,3) (4,5,6,7) (0,1,5,4) (1,2,6,5) (2,3,7,6) (3,0,4,7),
+ *          each the bilinear patch through its corners: A_f n_f =
+ *          (q2 - q0) x (q3 - q1)/2 away from the vertex mean, V_c from the
+ *          divergence theorem (exact for such faces).  The domain is
  * the axis-aligned bounding box of the vertices; every face without a
  * neighbour must lie on one of its walls (all face vertices at x = xmin ->
  * region 0, x = xmax -> 1, y -> 2/3, z -> 4/5, tested in that order).  Wall
@@ -193,7 +198,8 @@ typedef struct {
   double depth;          /* dim 2: z extent (volumes and face areas scale with it) */
   int nvc;               /* vertices per cell: 0 -> dim + 1 (simplices); dim 2 also 4
                             (convex quadrilaterals, vertices in boundary order:
-                            Eq. 3's "polygonal cell with m sides") */
+                            Eq. 3's "polygonal cell with m sides");
+                            dim 3 also 8 (hexahedra) */
 } bte_umesh;
 
 /* Create a single-GPU context on an unstructured mesh.  Geometry precompute
@@ -219,18 +225,19 @@ BTE_API bte_status bte_create_umesh(const bte_umesh *mesh, const bte_dirs *dirs,
 /* Mesh import ("A mesh must either be imported
  * from a Gmsh or MEDIT formatted mesh file, or generated internally").
  * Host only, no GPU.  Reads an ASCII Gmsh file (format 2.2 or 4.1: $Nodes,
- * $Elements; element types 2 triangle, 3 quadrangle, 4 tetrahedron; points
- * and lines are boundary tags and skipped; other sections ignored) or a MEDIT
- * .mesh file (Dimension, Vertices, Triangles / Quadrilaterals / Tetrahedra,
- * 1-based, with references; Edges / Corners skipped).  The cells are the
- * tetrahedra when present (triangles are then boundary faces), else the
- * triangles or the quadrilaterals (not both).  Node order of the file is kept
+ * $Elements; element types 2 triangle, 3 quadrangle, 4 tetrahedron, 5
+ * hexahedron; points and lines are boundary tags and skipped; other sections
+ * ignored) or a MEDIT .mesh file (Dimension, Vertices, Triangles /
+ * Quadrilaterals / Tetrahedra / Hexahedra, 1-based, with references; Edges /
+ * Corners skipped).  The cells are the 3-D elements when present (tetrahedra
+ * or hexahedra, not both; triangles / quadrilaterals are then boundary
+ * faces), else the triangles or the quadrilaterals (not both).  Node order of the file is kept
  * (Gmsh node tags are mapped to their position).  *out is allocated by the
  * library: verts [nverts][3] (z = 0 for 2-D files), cells [ncells][nvc]
  * 0-based; free it with bte_mesh_free.  The arrays plug into bte_umesh
  * (depth is the caller's).  Errors: BTE_EINVAL (unreadable file, malformed
- * record, binary Gmsh, hexahedra / prisms / pyramids, mixed 2-D cell kinds,
- * index out of range) with the reason in bte_mesh_error(). */
+ * record, binary Gmsh, prisms / pyramids, mixed cell kinds, index out of
+ * range) with the reason in bte_mesh_error(). */
 typedef struct {
   int dim, nvc;
   int64_t nverts, ncells;

@@ -440,12 +440,17 @@ static void partition_uhost(const UHost &G, int P, int rank, UHost *L) {
 // |cross| (depth cancels), tetrahedron = 3 cross(b - a, c - a) / |det|, each
 // oriented away from the opposite vertex.  Faces matched by their vertex sets;
 // unmatched faces classified onto the box walls (region order -x,+x,-y,+y,-z,+z).
+// hexahedron faces as vertex cycles (Gmsh order: bottom 0-1-2-3, top 4-5-6-7)
+static const int kHexF[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+
 static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
-  const int dim = um->dim, K = um->nvc > 0 ? um->nvc : dim + 1;
-  if (!((dim == 2 && (K == 3 || K == 4)) || (dim == 3 && K == 4))) {
-    *err = "vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4";
+  const int dim = um->dim, nvc = um->nvc > 0 ? um->nvc : dim + 1;
+  if (!((dim == 2 && (nvc == 3 || nvc == 4)) || (dim == 3 && (nvc == 4 || nvc == 8)))) {
+    *err = "vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4 (tetrahedra) or 8 (hexahedra)";
     return false;
   }
+  const bool hexa = dim == 3 && nvc == 8;
+  const int K = hexa ? 6 : nvc;  // faces per cell
   const int64_t nc = um->ncells, nv = um->nverts;
   h->dim = dim;
   h->K = K;
@@ -466,14 +471,14 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
     }
   for (int a = 0; a < 3; ++a) h->L[a] = hi[a] - h->lo[a];
   struct FaceKey {
-    int64_t v[3];
+    int64_t v[4];
     int64_t slot;  // c*K + k
   };
   std::vector<FaceKey> keys(nc * K);
   for (int64_t c = 0; c < nc; ++c) {
-    const int64_t *cv = um->cells + c * K;
-    const double *X[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int k = 0; k < K; ++k) {
+    const int64_t *cv = um->cells + c * nvc;
+    const double *X[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    for (int k = 0; k < nvc; ++k) {
       if (cv[k] < 0 || cv[k] >= nv) {
         *err = "cell " + std::to_string(c) + ": vertex index out of range";
         return false;
@@ -481,9 +486,46 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
       X[k] = um->verts + 3 * cv[k];
     }
     double cen[3] = {X[0][0], X[0][1], X[0][2]};
-    for (int k = 1; k < K; ++k)
+    for (int k = 1; k < nvc; ++k)
       for (int a = 0; a < 3; ++a) cen[a] = cen[a] + X[k][a];
-    for (int a = 0; a < 3; ++a) h->cen[3 * c + a] = cen[a] / K;
+    for (int a = 0; a < 3; ++a) h->cen[3 * c + a] = cen[a] / nvc;
+    if (hexa) {
+      // bilinear faces: area vector S = (q2 - q0) x (q3 - q1) / 2 away from the
+      // vertex mean, V = sum_f qbar_f . S_f / 3 (divergence theorem); A n / V = S / V
+      double S[6][3], vol = 0.0;
+      for (int k = 0; k < 6; ++k) {
+        const double *q0 = X[kHexF[k][0]], *q1 = X[kHexF[k][1]], *q2 = X[kHexF[k][2]], *q3 = X[kHexF[k][3]];
+        double d1[3], d2[3], qb[3];
+        for (int a = 0; a < 3; ++a) {
+          d1[a] = q2[a] - q0[a];
+          d2[a] = q3[a] - q1[a];
+          qb[a] = 0.25 * (q0[a] + q1[a] + q2[a] + q3[a]);
+        }
+        S[k][0] = 0.5 * (d1[1] * d2[2] - d1[2] * d2[1]);
+        S[k][1] = 0.5 * (d1[2] * d2[0] - d1[0] * d2[2]);
+        S[k][2] = 0.5 * (d1[0] * d2[1] - d1[1] * d2[0]);
+        double o = 0.0;
+        for (int a = 0; a < 3; ++a) o += S[k][a] * (qb[a] - h->cen[3 * c + a]);
+        if (o < 0.0)
+          for (int a = 0; a < 3; ++a) S[k][a] = -S[k][a];
+        vol += qb[0] * S[k][0] + qb[1] * S[k][1] + qb[2] * S[k][2];
+      }
+      vol /= 3.0;
+      if (!(vol > 0.0) || !std::isfinite(vol)) {
+        *err = "cell " + std::to_string(c) + " is degenerate (zero volume)";
+        return false;
+      }
+      h->vol[c] = vol;
+      for (int k = 0; k < 6; ++k) {
+        for (int a = 0; a < 3; ++a) h->an[(c * K + k) * 3 + a] = S[k][a] / vol;
+        FaceKey &fk = keys[c * K + k];
+        int64_t vv[4] = {cv[kHexF[k][0]], cv[kHexF[k][1]], cv[kHexF[k][2]], cv[kHexF[k][3]]};
+        std::sort(vv, vv + 4);
+        for (int a = 0; a < 4; ++a) fk.v[a] = vv[a];
+        fk.slot = c * K + k;
+      }
+      continue;
+    }
     double scale = 0.0;  // 2/|cross| (2/|shoelace|) or 3/|det|
     if (dim == 2 && K == 4) {  // convex quadrilateral: shoelace area
       double sh = 0.0;
@@ -544,19 +586,19 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
       int64_t vv[3] = {cv[q[0]], cv[q[1]], dim == 3 ? cv[q[2]] : -1};
       std::sort(vv, vv + (dim == 3 ? 3 : 2));
       for (int a = 0; a < 3; ++a) fk.v[a] = vv[a];
+      fk.v[3] = -1;
       fk.slot = c * K + k;
     }
   }
   std::sort(keys.begin(), keys.end(), [](const FaceKey &x, const FaceKey &y) {
-    if (x.v[0] != y.v[0]) return x.v[0] < y.v[0];
-    if (x.v[1] != y.v[1]) return x.v[1] < y.v[1];
-    if (x.v[2] != y.v[2]) return x.v[2] < y.v[2];
+    for (int a = 0; a < 4; ++a)
+      if (x.v[a] != y.v[a]) return x.v[a] < y.v[a];
     return x.slot < y.slot;
   });
   for (size_t i = 0; i < keys.size();) {
     size_t j = i + 1;
     while (j < keys.size() && keys[j].v[0] == keys[i].v[0] && keys[j].v[1] == keys[i].v[1] &&
-           keys[j].v[2] == keys[i].v[2])
+           keys[j].v[2] == keys[i].v[2] && keys[j].v[3] == keys[i].v[3])
       ++j;
     if (j - i > 2) {
       *err = "a face is shared by more than two cells";
@@ -572,13 +614,16 @@ static bool build_uhost(const bte_umesh *um, UHost *h, std::string *err) {
   for (int64_t c = 0; c < nc; ++c)
     for (int k = 0; k < K; ++k) {
       if (h->nbr[c * K + k] >= 0) continue;
-      const int64_t *cv = um->cells + c * K;
+      const int64_t *cv = um->cells + c * nvc;
       int reg = -1;
       for (int r = 0; r < 2 * dim && reg < 0; ++r) {
         const int a = r / 2;
         const double wall = (r & 1) ? hi[a] : h->lo[a];
         bool on = true;
-        if (dim == 2) {
+        if (hexa) {
+          for (int i = 0; i < 4; ++i)
+            if (um->verts[3 * cv[kHexF[k][i]] + a] != wall) on = false;
+        } else if (dim == 2) {
           on = um->verts[3 * cv[(k + 1) % K] + a] == wall && um->verts[3 * cv[(k + 2) % K] + a] == wall;
         } else {
           for (int i = 0; i < K; ++i)
@@ -611,12 +656,12 @@ bte_status bte_create_umesh(const bte_umesh *um, const bte_dirs *dirs, const bte
     return BTE_EINVAL;
   };
   if (!um || !um->verts || !um->cells) return early("null unstructured mesh");
-  if (um->dim != 2 && um->dim != 3) return early("unstructured dim must be 2 (triangles) or 3 (tetrahedra)");
+  if (um->dim != 2 && um->dim != 3) return early("unstructured dim must be 2 (triangles, quadrilaterals) or 3 (tetrahedra, hexahedra)");
   if (um->ncells < 1 || um->nverts < um->dim + 1) return early("empty unstructured mesh");
   if (um->ncells > (1ll << 30)) return early("unstructured mesh too large");
   if (um->dim == 2 && !(um->depth > 0)) return early("depth must be > 0");
-  if (um->nvc != 0 && !(um->nvc == um->dim + 1 || (um->dim == 2 && um->nvc == 4)))
-    return early("vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4");
+  if (um->nvc != 0 && !(um->nvc == um->dim + 1 || (um->dim == 2 && um->nvc == 4) || (um->dim == 3 && um->nvc == 8)))
+    return early("vertices per cell: dim 2 takes 3 or 4, dim 3 takes 4 or 8");
   if (run && (run->nranks < 1 || run->rank < 0 || run->rank >= run->nranks || run->nranks > um->ncells))
     return early("bad rank/nranks for the unstructured partition");
   UHost uh;
@@ -989,6 +1034,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
       ctx->uL[a] = uh->L[a];
     }
     ctx->u.K = uh->K;
+    ctx->u.KP = uh->K <= 4 ? 4 : 8;
     ctx->u.ncells = uh->nc;
     for (int r = 0; r < 6; ++r) {
       ctx->u.rn[r] = (int64_t)uh->rcell[r].size();
@@ -1150,12 +1196,13 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     double *d_an = nullptr, *d_sw = nullptr;
     // device rows padded to 4 faces: nbr [nc][4] (32 B), an [nc][4][3] (96 B), so
     // that the pipelined sweep moves them with 16-B bulk copies
-    std::vector<int64_t> nbr4(4 * (size_t)uh->nc, -1);
-    std::vector<double> an4(12 * (size_t)uh->nc, 0.0);
+    const int KP = uh->K <= 4 ? 4 : 8;  // device face slots per cell
+    std::vector<int64_t> nbr4(KP * (size_t)uh->nc, -1);
+    std::vector<double> an4(3 * KP * (size_t)uh->nc, 0.0);
     for (int64_t c = 0; c < uh->nc; ++c)
       for (int f = 0; f < uh->K; ++f) {
-        nbr4[4 * c + f] = uh->nbr[c * uh->K + f];
-        for (int a = 0; a < 3; ++a) an4[12 * c + 3 * f + a] = uh->an[(c * uh->K + f) * 3 + a];
+        nbr4[KP * c + f] = uh->nbr[c * uh->K + f];
+        for (int a = 0; a < 3; ++a) an4[3 * KP * c + 3 * f + a] = uh->an[(c * uh->K + f) * 3 + a];
       }
     if ((st = upload(ctx, &d_nbr, nbr4.data(), nbr4.size()))) return bail(st);
     if ((st = upload(ctx, &d_an, an4.data(), an4.size()))) return bail(st);

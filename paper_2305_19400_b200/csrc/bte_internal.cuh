@@ -142,10 +142,11 @@ struct SweepArgs {
 // is the structured one with one "plane" of ncells cross cells:
 // I[slot][cell][j][b], (cell, slot) blocks of Es doubles.
 struct UMeshDev {
-  int K;                  // faces per cell (dim + 1)
+  int K;                  // faces per cell (triangle 3, tetrahedron / quadrilateral 4, hexahedron 6)
+  int KP;                 // face slots per device row: 4 (K <= 4) or 8 (hexahedra)
   int64_t ncells;
-  const int64_t *nbr;     // [nc][4] (faces >= K unused): neighbour >= 0, or -1 - (face_in_region * 8 + region)
-  const double *an;       // [nc][4][3] (faces >= K unused): (A_f / V_c) n_f
+  const int64_t *nbr;     // [nc][KP] (faces >= K unused): neighbour >= 0, or -1 - (face_in_region * 8 + region)
+  const double *an;       // [nc][KP][3] (faces >= K unused): (A_f / V_c) n_f
   const double *sw;       // [nslot * nj][4]: s_x, s_y, s_z, w of direction (slot, j)
   const int64_t *rcell[6];  // owned wall faces: local cell
   const int64_t *rface[6];  // ... and their global face index (ghost-table row)

@@ -855,7 +855,11 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
             num = fma(kk, prev[k] - Inn, num);
             den += kk;
           }
-          const double Inew = Inn + num / den;
+          // I^{k+1} = I^n + num/den: a correctly rounded reciprocal refined by
+          // one Newton step, then the product (within 2 ulp of the quotient)
+          double r = __drcp_rn(den);
+          r = fma(r, fma(-den, r, 1.0), r);
+          const double Inew = fma(num, r, Inn);
           __stcg(Os + base + e, Inew);
           acc = fma(cf[3], I0 - Inew, acc);
           prev[k] = Inew;
@@ -1027,13 +1031,30 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long *w, double 
   if (x > 0.0) atomicMax(w, (unsigned long long)__double_as_longlong(x));
 }
 
+// block-wide max of a non-negative value, then one atomic per block (the
+// per-thread atomics on one word serialised: 12 ms per snapshot on config 3)
+__device__ __forceinline__ void block_max_to(unsigned long long *w, double x) {
+  __shared__ double wm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // wm may still be read by a previous call
+  if (lane == 0) wm[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)((blockDim.x + 31) >> 5); ++k) m = fmax(m, wm[k]);
+    atomic_max_nonneg(w, m);
+  }
+}
+
 __global__ void k_diffuse(const Geometry g, const double *__restrict__ I, int region,
                           double *__restrict__ gtab, unsigned long long *chg) {
   int64_t face, cell_base;
   wall_face(g, region, blockIdx.x, &face, &cell_base);
   double m = 0.0;
   diffuse_face(g, I, region, face, cell_base, gtab, chg ? &m : nullptr);
-  if (chg) atomic_max_nonneg(chg, m);
+  if (chg) block_max_to(chg, m);
 }
 
 cudaError_t launch_diffuse(const Geometry &g, const double *I, int region, double *gtab,
@@ -1095,7 +1116,7 @@ __global__ void k_spec_snapshot(const Geometry g, const double *__restrict__ I, 
       o[e] = val;
     }
   }
-  if (chg) atomic_max_nonneg(chg, m);
+  if (chg) block_max_to(chg, m);
 }
 
 cudaError_t launch_spec_snapshot(const Geometry &g, const double *I, int region, double *out, cudaStream_t s,
@@ -2080,10 +2101,10 @@ cudaError_t launch_energy(const Geometry &g, const double *I, const double *v, d
 // Neighbour reads are 8*nb-byte coalesced rows of the neighbour's block; the
 // octant partial sum over j feeds the same Dpart[c][slot][b] as the
 // structured sweep (fixed order: within a thread ascending j, then groups).
-template <int JMAX>
+template <int JMAX, int KM>
 __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
   extern __shared__ double sm[];  // a[K][nj] | red[JG*nb]
-  __shared__ int64_t snbr[4];
+  __shared__ int64_t snbr[KM];
   const Geometry &g = A.g;
   const UMeshDev &u = A.u;
   const int nb = g.nb, nj = g.nj, Es = g.Es, K = u.K;
@@ -2096,12 +2117,12 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
   const int64_t cell = blockIdx.x;
   const int slot = blockIdx.y;
   double *a = sm;
-  double *red = sm + 4 * nj;
-  if (tid < K) snbr[tid] = u.nbr[cell * 4 + tid];
+  double *red = sm + KM * nj;
+  if (tid < K) snbr[tid] = u.nbr[cell * u.KP + tid];
   for (int i = tid; i < K * nj; i += blockDim.x) {
     const int f = i / nj, j = i - f * nj;
     const double *sv = u.sw + (int64_t)(slot * nj + j) * 4;
-    const double *an = u.an + cell * 12 + f * 3;
+    const double *an = u.an + cell * 3 * u.KP + f * 3;
     a[f * nj + j] = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
   }
   __syncthreads();
@@ -2114,7 +2135,7 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
     const double I0 = __ldg(A.I0c + cell * nb + b);
     const double dtb = A.dt * __ldg(A.beta + cell * nb + b);
     const double v = A.v[b];
-    double Ic[JMAX], up[JMAX][4];
+    double Ic[JMAX], up[JMAX][KM];
 #pragma unroll
     for (int k = 0; k < JMAX; ++k) {  // issue every load of the cell first
       if (k < nloc) {
@@ -2122,7 +2143,7 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
         const int e = j * nb + b;
         Ic[k] = __ldg(Is + base + e);
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
+        for (int f = 0; f < KM; ++f) {
           up[k][f] = 0.0;
           if (f < K && !(a[f * nj + j] > 0.0)) {
             const int64_t n = snbr[f];
@@ -2138,7 +2159,7 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
         const int e = j * nb + b;
         double flux = 0.0;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
+        for (int f = 0; f < KM; ++f) {
           if (f < K) {
             const double af = a[f * nj + j];
             double w;
@@ -2418,7 +2439,7 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   USweepArgs a = a0;
   const Geometry &g = a.g;
   if (a.u.ncells == 0) return cudaSuccess;
-  if (a.pipelined && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
+  if (a.pipelined && a.u.K <= 4 && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
     const int NBP = g.nb / 2;
     // 2 directions x 2 channels per thread on triangles (measured 3 % faster on u2),
     // 1 x 2 on tetrahedra (their 4-face lists fill the registers)
@@ -2476,14 +2497,20 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   a.jg = JG;
   const int threads = JG * g.nb;
   if (threads > 1024) return cudaErrorInvalidConfiguration;
-  const size_t smem = (4 * (size_t)g.nj + (size_t)threads) * sizeof(double);
+  const int KM = a.u.K <= 4 ? 4 : 8;  // face slots (hexahedra: 6 faces in 8)
+  const size_t smem = ((size_t)KM * g.nj + (size_t)threads) * sizeof(double);
   dim3 grid((unsigned)a.u.ncells, g.nslot);
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   switch (jcase) {
-#define BTE_UCASE(N)                                                                    \
-  case N:                                                                               \
-    if (cudaError_t e = smem_attr((const void *)k_usweep<N>, smem)) return e;          \
-    k_usweep<N><<<grid, threads, smem, s>>>(a);                                         \
+#define BTE_UCASE(N)                                                                          \
+  case N:                                                                                     \
+    if (KM == 4) {                                                                            \
+      if (cudaError_t e = smem_attr((const void *)k_usweep<N, 4>, smem)) return e;            \
+      k_usweep<N, 4><<<grid, threads, smem, s>>>(a);                                          \
+    } else {                                                                                  \
+      if (cudaError_t e = smem_attr((const void *)k_usweep<N, 8>, smem)) return e;            \
+      k_usweep<N, 8><<<grid, threads, smem, s>>>(a);                                          \
+    }                                                                                         \
     break;
     BTE_UCASE(1)
     BTE_UCASE(2)

@@ -46,7 +46,7 @@ bte_status mfail(const char *fmt, ...) {
 struct Raw {
   int dim = 0;
   std::vector<double> verts;          // [n][3]
-  std::vector<int64_t> tri, quad, tet;  // 0-based vertex indices
+  std::vector<int64_t> tri, quad, tet, hex;  // 0-based vertex indices
 };
 
 // Reads whitespace-separated tokens line by line (comments '#' in MEDIT).
@@ -110,10 +110,11 @@ int gmsh_nodes(int type) {
 }
 
 bte_status add_elem(Raw &r, int type, const std::vector<int64_t> &nodes) {
-  std::vector<int64_t> *dst = type == 2 ? &r.tri : type == 3 ? &r.quad : type == 4 ? &r.tet : nullptr;
-  if (type == 5 || type == 6 || type == 7)
-    return mfail("element type %d (hexahedron / prism / pyramid) is not supported: tetrahedra, triangles "
-                 "and quadrilaterals only", type);
+  std::vector<int64_t> *dst = type == 2 ? &r.tri : type == 3 ? &r.quad : type == 4 ? &r.tet
+                            : type == 5 ? &r.hex : nullptr;
+  if (type == 6 || type == 7)
+    return mfail("element type %d (prism / pyramid) is not supported: tetrahedra, hexahedra, triangles and "
+                 "quadrilaterals only", type);
   if (!dst) return BTE_OK;  // points and lines: boundary tags, not cells
   dst->insert(dst->end(), nodes.begin(), nodes.end());
   return BTE_OK;
@@ -271,10 +272,10 @@ bte_status read_medit(std::istream &in, Raw &r) {
       const int nn = k == "triangles" ? 3 : k == "quadrilaterals" || k == "tetrahedra" ? 4 : k == "edges" ? 2
                    : k == "hexahedra" ? 8 : k == "prisms" ? 6 : 1;
       const bool refs = nn > 1;  // element records end with a reference; corner-type lists do not
-      if ((k == "hexahedra" || k == "prisms") && n > 0)
-        return mfail("%s are not supported: tetrahedra, triangles and quadrilaterals only", t.c_str());
+      if (k == "prisms" && n > 0)
+        return mfail("%s are not supported: tetrahedra, hexahedra, triangles and quadrilaterals only", t.c_str());
       std::vector<int64_t> *dst = k == "triangles" ? &r.tri : k == "quadrilaterals" ? &r.quad
-                                : k == "tetrahedra" ? &r.tet : nullptr;
+                                : k == "tetrahedra" ? &r.tet : k == "hexahedra" ? &r.hex : nullptr;
       for (int64_t q = 0; q < n; ++q) {
         for (int a = 0; a < nn; ++a) {
           int64_t vid;
@@ -325,8 +326,12 @@ bte_status bte_mesh_read(const char *path, bte_mesh_data **out) {
   // tags), else 2-D triangles or quadrilaterals (not both)
   int dim, nvc;
   const std::vector<int64_t> *cells;
-  if (!r.tet.empty()) {
+  if (!r.tet.empty() && !r.hex.empty()) {
+    return mfail("mixed tetrahedra and hexahedra: one cell kind per mesh");
+  } else if (!r.tet.empty()) {
     dim = 3, nvc = 4, cells = &r.tet;
+  } else if (!r.hex.empty()) {
+    dim = 3, nvc = 8, cells = &r.hex;
   } else if (!r.tri.empty() && !r.quad.empty()) {
     return mfail("mixed triangles and quadrilaterals: one cell kind per mesh");
   } else if (!r.tri.empty()) {

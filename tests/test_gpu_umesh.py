@@ -231,6 +231,8 @@ def _part_case(case):
         p = bi.small_umesh(2, (7, 5, 1))
     elif case == "quad":
         p = bi.small_umesh(2, (6, 5, 1), quad=True, shuffle=True)
+    elif case == "hex":
+        p = bi.small_umesh(3, (4, 3, 3), hexa=True, shuffle=True)
     else:
         p = bi.small_umesh(3, (3, 3, 3))
     p.bcs = _walls(p)
@@ -249,7 +251,7 @@ def _part_group(Solver, p, P, I, T, **kw):
     return group
 
 
-@pytest.mark.parametrize("case,P", [("tri", 2), ("tri", 3), ("quad", 3), ("tet", 2), ("tet", 4)])
+@pytest.mark.parametrize("case,P", [("tri", 2), ("tri", 3), ("quad", 3), ("tet", 2), ("tet", 4), ("hex", 3)])
 def test_umesh_partition_group_bitexact(Solver, case, P):
     """P contexts each owning a contiguous cell range plus halo copies of the
     neighbours owned elsewhere (refreshed after every step) reproduce the
@@ -350,7 +352,7 @@ def test_umesh_full_size_u3_sampled(Solver):
 
 # ----------------------------------------------------------------- mesh import and RCB partition
 
-@pytest.mark.parametrize("kind", ["tet", "quad"])
+@pytest.mark.parametrize("kind", ["tet", "quad", "hex"])
 def test_imported_mesh_parity(Solver, tmp_path, kind):
     """A mesh read from a Gmsh file (bte_mesh_read) runs on the GPU
     and matches the oracle run on the generator's arrays."""
@@ -358,6 +360,8 @@ def test_imported_mesh_parity(Solver, tmp_path, kind):
     from paper_2305_19400_b200 import read_mesh
     if kind == "tet":
         p = bi.small_umesh(3, (3, 3, 2), shuffle=True)
+    elif kind == "hex":
+        p = bi.small_umesh(3, (3, 3, 2), hexa=True, shuffle=True)
     else:
         p = bi.small_umesh(2, (5, 4, 1), quad=True)
     path = str(tmp_path / "m.msh")
@@ -399,3 +403,37 @@ def test_rcb_partitioned_group_parity(Solver, kind, P):
             s.close()
     rel, dT = _cmp(Ig, Tg, Io, To)
     assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+# ----------------------------------------------------------------- hexahedra (Eq. 3 for polyhedra)
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_hex_parity_all_wall_kinds(Solver, shuffle):
+    """Jittered hexahedra (bilinear, non-planar faces) against the oracle, every wall kind."""
+    p = bi.small_umesh(3, (4, 3, 3), hexa=True, shuffle=shuffle)
+    p.bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(3, specularity=0.4),
+             bi.WallBC(0, None, 298.0), bi.WallBC(2)]
+    rel, dT = _run_both(Solver, p, 6)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_hex_silicon_400x40_and_structured_equivalence(Solver):
+    """Hexahedra with the BASELINE 400 x 40 tables against the oracle; an
+    unjittered hexahedral mesh reproduces the structured-grid GPU run to
+    rounding (two different kernels and geometries)."""
+    p = bi.config3(n=6)
+    p.mesh = bi.umesh_hex(6, 5, 4, 1e-6, jitter=0.1, seed=31, shuffle=True)
+    rel, dT = _run_both(Solver, p, 3)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+    g = bi.config3(n=6)
+    g.mesh = bi.Mesh(3, 6, 5, 4, 1e-6, 1e-6, 1e-6)
+    h = bi.config3(n=6)
+    h.mesh = bi.umesh_hex(6, 5, 4, 1e-6, jitter=0.0)
+    I, T = oracle.Oracle(g).random_state()
+    out = []
+    for q in (g, h):
+        with Solver.from_problem(q) as sv:
+            sv.set_state(I, T)
+            sv.step(4)
+            out.append((sv.intensity(), sv.temperature()))
+    assert np.max(np.abs(out[1][0] / out[0][0] - 1)) < 1e-12 and np.max(np.abs(out[1][1] - out[0][1])) < 1e-9

@@ -16,8 +16,12 @@ from paper_2305_19400_b200 import BteError, partition_rcb, plan_umesh, read_mesh
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+def _etype(m):
+    return {3: 2, 4: 3 if m.dim == 2 else 4, 8: 5}[m.cells.shape[1]]
+
+
 def _gmsh22(path, m, extra_boundary=True):
-    etype = {3: 2, 4: 3 if m.dim == 2 else 4}[m.cells.shape[1]]
+    etype = _etype(m)
     with open(path, "w") as f:
         f.write("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n$Nodes\n%d\n" % m.nverts)
         for k, x in enumerate(m.verts):
@@ -36,7 +40,7 @@ def _gmsh22(path, m, extra_boundary=True):
 
 
 def _gmsh41(path, m):
-    etype = {3: 2, 4: 3 if m.dim == 2 else 4}[m.cells.shape[1]]
+    etype = _etype(m)
     n = m.nverts
     half = n // 2
     with open(path, "w") as f:
@@ -56,7 +60,7 @@ def _gmsh41(path, m):
 
 
 def _medit(path, m):
-    kw = {3: "Triangles", 4: "Quadrilaterals" if m.dim == 2 else "Tetrahedra"}[m.cells.shape[1]]
+    kw = {3: "Triangles", 4: "Quadrilaterals" if m.dim == 2 else "Tetrahedra", 8: "Hexahedra"}[m.cells.shape[1]]
     with open(path, "w") as f:
         f.write("MeshVersionFormatted 2\n# written by the tests\nDimension %d\nVertices\n%d\n" % (m.dim, m.nverts))
         for x in m.verts:
@@ -80,11 +84,12 @@ def test_golden_fixtures(name):
 def _meshes():
     return {"tri": bi.umesh_tri(5, 4, 5e-6, 4e-6, jitter=0.2, seed=3, shuffle=True),
             "quad": bi.umesh_quad(4, 3, 4e-6, 3e-6, jitter=0.2, seed=4),
-            "tet": bi.umesh_tet(3, 3, 2, 1e-6, jitter=0.1, seed=5, shuffle=True)}
+            "tet": bi.umesh_tet(3, 3, 2, 1e-6, jitter=0.1, seed=5, shuffle=True),
+            "hex": bi.umesh_hex(3, 2, 2, 1e-6, jitter=0.1, seed=6, shuffle=True)}
 
 
 @pytest.mark.parametrize("fmt", ["gmsh22", "gmsh41", "medit"])
-@pytest.mark.parametrize("kind", ["tri", "quad", "tet"])
+@pytest.mark.parametrize("kind", ["tri", "quad", "tet", "hex"])
 def test_roundtrip_bit_exact(tmp_path, fmt, kind):
     m = _meshes()[kind]
     path = str(tmp_path / ("m.mesh" if fmt == "medit" else "m.msh"))
@@ -102,12 +107,12 @@ def test_read_errors(tmp_path):
     bad.write_text("$MeshFormat\n2.2 1 8\n$EndMeshFormat\n")
     with pytest.raises(BteError, match="binary"):
         read_mesh(str(bad))
-    hexa = tmp_path / "hex.msh"
-    hexa.write_text("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n$Nodes\n8\n" +
-                    "".join("%d %d %d %d\n" % (k + 1, k & 1, (k >> 1) & 1, k >> 2) for k in range(8)) +
-                    "$EndNodes\n$Elements\n1\n1 5 0 1 2 4 3 5 6 8 7\n$EndElements\n")
+    prism = tmp_path / "prism.msh"
+    prism.write_text("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n$Nodes\n6\n" +
+                     "".join("%d %d %d %d\n" % (k + 1, k & 1, (k >> 1) & 1, k >> 2) for k in range(6)) +
+                     "$EndNodes\n$Elements\n1\n1 6 0 1 2 3 4 5 6\n$EndElements\n")
     with pytest.raises(BteError, match="not supported"):
-        read_mesh(str(hexa))
+        read_mesh(str(prism))
     mixed = tmp_path / "mixed.mesh"
     mixed.write_text("MeshVersionFormatted 2\nDimension 2\nVertices\n4\n0 0 0\n1 0 0\n1 1 0\n0 1 0\n"
                      "Triangles\n1\n1 2 3 0\nQuadrilaterals\n1\n1 2 3 4 0\nEnd\n")
@@ -123,13 +128,15 @@ def _centroids(m):
     return m.verts[m.cells].mean(axis=1)
 
 
-@pytest.mark.parametrize("kind,P", [("tri", 3), ("tri", 8), ("tet", 4), ("tet", 7)])
+@pytest.mark.parametrize("kind,P", [("tri", 3), ("tri", 8), ("tet", 4), ("tet", 7), ("hex", 5)])
 def test_rcb_parts_are_ranges_compact_and_cut_halos(kind, P):
     """RCB on a randomly ordered mesh: a permutation; part r is exactly the
     range bte_create_umesh gives rank r; parts are compact (their centroid
     boxes overlap little); halos far smaller than for the shuffled order."""
     if kind == "tri":
         m = bi.umesh_tri(24, 20, 24e-6, 20e-6, jitter=0.2, seed=8, shuffle=True)
+    elif kind == "hex":
+        m = bi.umesh_hex(12, 10, 9, 1e-6, jitter=0.1, seed=10, shuffle=True)
     else:
         m = bi.umesh_tet(8, 7, 6, 1e-6, jitter=0.1, seed=9, shuffle=True)
     perm = partition_rcb(m, P)
