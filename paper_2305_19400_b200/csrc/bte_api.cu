@@ -1734,7 +1734,7 @@ static bte_status implicit_setup(bte_ctx *ctx) {
   for (size_t k = 0; k < key.size(); ++k) tasks[k] = key[k].second;
   bte_status st;
   if ((st = upload(ctx, &ctx->d_tasks, tasks.data(), tasks.size()))) return st;
-  ctx->d_prog = (int *)dev_alloc(ctx, tasks.size() * sizeof(int));
+  ctx->d_prog = (int *)dev_alloc(ctx, tasks.size() * 32 * sizeof(int));  // one 128-B line per counter
   ctx->d_ticket = (unsigned *)dev_alloc(ctx, 16);
   ctx->d_conv = (unsigned long long *)dev_alloc(ctx, 2 * sizeof(unsigned long long));
   if (!ctx->d_prog || !ctx->d_ticket || !ctx->d_conv) return fail(ctx, BTE_ENOMEM, "implicit-step tables");
@@ -1791,7 +1791,7 @@ static bte_status implicit_step(bte_ctx *ctx, bool t) {
     if ((st = implicit_boundary(ctx, k == 0 ? In : Iout, t))) return st;
     nvtx_pop();
     nvtx_push("a2 implicit sweep");
-    CU(cudaMemsetAsync(ctx->d_prog, 0, (size_t)g.nslot * g.ncross * sizeof(int), ctx->stream));
+    CU(cudaMemsetAsync(ctx->d_prog, 0, (size_t)g.nslot * g.ncross * 32 * sizeof(int), ctx->stream));
     CU(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned), ctx->stream));
     SweepArgs a = sweep_args(ctx, In, Iout, 0, 0, 0);
     a.g.rot = 1;  // wall ghosts from the snapshot of I^k (the sweep overwrites I^k)

@@ -689,13 +689,16 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v) {
 // belongs to a CTA that took its ticket earlier and is running or done -- no
 // deadlock whatever the block scheduler does.  The CTA marches its column
 // from the upwind wall along the march axis (upwind value in registers, the
-// CTA's own previous result); before each plane it waits until the x- (and
-// y-) upwind columns have published that plane (release/acquire counter per
-// (slot, column)), reads their I^{k+1} values from L2 and publishes its own
-// plane after writing it.  The own I^n block and the I0c / beta rows do not
-// depend on the wavefront and stream through an S-stage TMA ring.
-template <int DIM, int JMAX>
-__global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int2 *__restrict__ tasks,
+// CTA's own previous result) and publishes each plane it has written
+// (release counter per (slot, column), one 128-B line each).  Its stage ring
+// holds per plane the own I^n block + I0c / beta rows (barrier A, issued S
+// planes ahead: independent of the wavefront) and the x- / y-upwind columns'
+// I^{k+1} blocks (barrier B): a dedicated issuer warp copies a neighbour plane
+// as soon as both counters have passed it -- often planes ahead of the
+// compute, since the upwind columns started earlier -- so the compute warps
+// never poll and the L2 latency of the neighbour data overlaps other work.
+template <int DIM, int JMAX, int MT, int MB>
+__global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const int2 *__restrict__ tasks,
                                                     int *__restrict__ prog, unsigned *__restrict__ ticket) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ int s_task;
@@ -710,10 +713,8 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
   const int j0 = grp * A.jpt;
   const int nloc = max(0, min(A.jpt, nj - j0));
   const bool active = grp < JG;
-  const int spare0 = JG * nb;
-  const bool spare = (int)blockDim.x >= spare0 + nb + 1;
-  const int rtid = spare ? tid - spare0 : tid;
-  const int tis = spare ? spare0 + nb : 0;
+  const int rtid = tid - JG * nb;            // reducers: [0, nb)
+  const int tis = (int)blockDim.x - 32;      // issuer: first thread of the last warp (launcher adds it)
 
   if (tid == 0) s_task = (int)atomicAdd(ticket, 1u);
   __syncthreads();
@@ -739,15 +740,18 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
     yoff = (yneg ? 1 : -1) * (int64_t)g.nx * Es;
     ycol = yneg ? col + g.nx : col - g.nx;
   }
+  const bool hasB = !xghost || (DIM == 3 && !yghost);
   const int mregion = (DIM == 3) ? (mneg ? 5 : 4) : (mneg ? 3 : 2);
-  int *pr = prog + (int64_t)slot * g.ncross;
+  constexpr int kProgStride = 32;  // counters one 128-B line apart
+  int *pr = prog + (int64_t)slot * g.ncross * kProgStride;
 
-  uint64_t *full = reinterpret_cast<uint64_t *>(smraw);
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(smraw);  // [S] own + rows
+  uint64_t *fullB = fullA + 8;                            // [S] upwind neighbours (S <= 8)
   double *coef = reinterpret_cast<double *>(smraw + 128);
   double *red = coef + 4 * nj;
   double *stage0 = red + 2 * JG * nb;
-  const int64_t sd = A.stage_doubles;  // own I^n | I0 | beta
-  const int o_i0 = Es, o_be = Es + nb;
+  const int64_t sd = A.stage_doubles;  // own I^n | x-up | y-up | I0 | beta
+  const int o_x = Es, o_y = 2 * Es, o_i0 = (DIM == 3 ? 3 : 2) * Es, o_be = o_i0 + nb;
   const bool rows_tma = (nb % 2) == 0;
   const int np = g.nplanes;
   const int step = mneg ? -1 : 1;
@@ -757,30 +761,49 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
   double *__restrict__ Os = A.Iout + A.out_off[slot];
   const int64_t colE = (int64_t)col * Es;
   const double dt = A.dt;
+  const uint32_t blk = (uint32_t)Es * 8u;
 
-  auto issue = [&](int i, int st) {
+  auto issueA = [&](int i, int st) {
     const int pp = pfirst + i * step;
     const int64_t base = (int64_t)pp * g.plane_stride + colE;
     const int64_t cell = (int64_t)col + (int64_t)pp * g.ncross;
     double *sp = stage0 + st * sd;
-    const uint32_t blk = (uint32_t)Es * 8u;
     const uint32_t row = (uint32_t)nb * 8u;
-    mbar_expect_tx(&full[st], blk + (rows_tma ? 2u * row : 0u));
-    bulk_g2s(sp, In + base, blk, &full[st]);
+    mbar_expect_tx(&fullA[st], blk + (rows_tma ? 2u * row : 0u));
+    bulk_g2s(sp, In + base, blk, &fullA[st]);
     if (rows_tma) {
-      bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
-      bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
+      bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &fullA[st]);
+      bulk_g2s(sp + o_be, A.beta + cell * nb, row, &fullA[st]);
     }
+  };
+  // plane i of the upwind columns, once published (their stores are generic-
+  // proxy writes of other SMs: acquire, then order the bulk reads after it)
+  auto nb_ready = [&](int i) {
+    if (!xghost && ld_acquire_gpu(pr + (int64_t)xcol * kProgStride) <= i) return false;
+    if (DIM == 3 && !yghost && ld_acquire_gpu(pr + (int64_t)ycol * kProgStride) <= i) return false;
+    return true;
+  };
+  auto issueB = [&](int i, int st) {
+    const int pp = pfirst + i * step;
+    const int64_t base = (int64_t)pp * g.plane_stride + colE;
+    double *sp = stage0 + st * sd;
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(&fullB[st], blk * ((xghost ? 0u : 1u) + ((DIM == 3 && !yghost) ? 1u : 0u)));
+    if (!xghost) bulk_g2s(sp + o_x, Os + base + xoff, blk, &fullB[st]);
+    if (DIM == 3 && !yghost) bulk_g2s(sp + o_y, Os + base + yoff, blk, &fullB[st]);
   };
 
   if (tid == 0) {
-    for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&fullA[st], 1);
+      mbar_init(&fullB[st], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < 4 * nj; i += blockDim.x) coef[i] = g.coef[(int64_t)slot * nj * 4 + i];
   __syncthreads();
   if (tid == tis)
-    for (int i = 0; i < min(S, np); ++i) issue(i, i);
+    for (int i = 0; i < min(S, np); ++i) issueA(i, i);
 
   const double v = A.v[active ? b : 0];
   const int e0 = j0 * nb + b;
@@ -796,22 +819,29 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
     }
   }
 
-  int buf = 0;
+  int nbq = 0;  // issuer: next plane whose neighbour blocks are to be copied
+  int st = 0;
+  uint32_t ph = 0;
   int p = pfirst;
   for (int i = 0; i < np; ++i, p += step) {
-    const int st = i % S;
     const int64_t cell = (int64_t)col + (int64_t)p * g.ncross;
     const int64_t base = (int64_t)p * g.plane_stride + colE;
     const double *sp = stage0 + st * sd;
-    // wavefront: the upwind columns' plane p of I^{k+1} must be published
-    if (tid == 0) {
-      if (!xghost)
-        while (ld_acquire_gpu(pr + xcol) <= i) __nanosleep(32);
-      if (DIM == 3 && !yghost)
-        while (ld_acquire_gpu(pr + ycol) <= i) __nanosleep(32);
+    if (tid == tis && hasB) {
+      // copy every published neighbour plane whose stage is free (planes < i + S);
+      // plane i itself is needed now: wait for it
+      while (nbq < np && nbq < i + S) {
+        if (!nb_ready(nbq)) {
+          if (nbq > i) break;
+          __nanosleep(64);
+          continue;
+        }
+        issueB(nbq, nbq % S);
+        ++nbq;
+      }
     }
-    __syncthreads();
-    mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+    mbar_wait(&fullA[st], ph);
+    if (hasB) mbar_wait(&fullB[st], ph);
     double acc = 0.0;
     if (active) {
       const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + cell * nb + b);
@@ -825,14 +855,14 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
           const double Inn = sp[e];
           double xu, yu = 0.0;
           if (!xghost) {
-            xu = __ldcg(Os + base + xoff + e);
+            xu = sp[o_x + e];
           } else {
             const int64_t face = (DIM == 3) ? (int64_t)y + (int64_t)g.ny * mg : mg;
             xu = ghost_value(g, A.Iin, xregion, face, base, slot, j, b);
           }
           if (DIM == 3) {
             if (!yghost) {
-              yu = __ldcg(Os + base + yoff + e);
+              yu = sp[o_y + e];
             } else {
               const int64_t face = (int64_t)x + (int64_t)g.nx * mg;
               yu = ghost_value(g, A.Iin, yregion, face, base, slot, j, b);
@@ -866,23 +896,26 @@ __global__ void __launch_bounds__(1024) k_sweep_imp(const SweepArgs A, const int
         }
       }
     }
-    double *rb = red + buf * JG * nb;
+    double *rb = red + (i & 1) * JG * nb;
     if (active) rb[tid] = acc;
     __syncthreads();  // stage st consumed, rb complete, this plane's stores issued
     if (tid == 0) {
       __threadfence();  // cumulative over the CTA's stores ordered by the barrier
-      st_release_gpu(pr + col, i + 1);
+      st_release_gpu(pr + (int64_t)col * kProgStride, i + 1);
     }
     if (tid == tis && i + S < np) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(i + S, st);
+      issueA(i + S, st);
     }
     if (rtid >= 0 && rtid < nb) {
       double s = 0.0;
       for (int q = 0; q < JG; ++q) s += rb[q * nb + rtid];
       A.Dpart[(cell * g.nslot + slot) * nb + rtid] = s;
     }
-    buf ^= 1;
+    if (++st == S) {
+      st = 0;
+      ph ^= 1u;
+    }
   }
 }
 
@@ -897,25 +930,32 @@ static cudaError_t launch_sweep_imp_dim(const SweepArgs &a0, const int2 *tasks, 
   a.jg = JG;
   const int threads = JG * g.nb;
   if (threads > 1024 || (g.Es & 1)) return cudaErrorInvalidConfiguration;
-  const int64_t stage_d = ((int64_t)g.Es + 2 * g.nb + 15) / 16 * 16;
+  // stage: own | x-up | (y-up) | I0 | beta
+  const int64_t stage_d = ((int64_t)(DIM == 3 ? 3 : 2) * g.Es + 2 * g.nb + 15) / 16 * 16;
   const size_t fixed = 128 + (4 * (size_t)g.nj + 2 * (size_t)threads) * sizeof(double);
-  const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : 113) * 1024;
+  const int tthreads = ((threads + g.nb + 31) / 32) * 32 + 32;  // compute + reducers, then the issuer warp
+  if (tthreads > 1024) return cudaErrorInvalidConfiguration;
+  const bool small = tthreads <= 288;
+  const size_t budget = (size_t)(a.smem_budget_kb > 0 ? a.smem_budget_kb : (small ? 75 : 113)) * 1024;
   int S = (int)((budget > fixed ? budget - fixed : 0) / (stage_d * sizeof(double)));
   S = std::max(2, std::min(4, S));
-  if (a.stages_override > 0) S = std::min(16, a.stages_override);
+  if (a.stages_override > 0) S = std::min(8, a.stages_override);
   a.stages = S;
   a.stage_doubles = stage_d;
   const size_t smem = fixed + (size_t)S * stage_d * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  const int tthreads = ((a.no_spare ? threads : threads + g.nb + 1) + 31) / 32 * 32;
-  if (tthreads > 1024) return cudaErrorInvalidConfiguration;
   const int jcase = jpt <= 1 ? 1 : jpt <= 2 ? 2 : jpt <= 4 ? 4 : jpt <= 5 ? 5 : jpt <= 8 ? 8 : jpt <= 10 ? 10 : jpt <= 16 ? 16 : 0;
   cudaError_t e;
   switch (jcase) {
-#define BTE_IMP(N)                                                                    \
-  case N:                                                                             \
-    if ((e = smem_attr((const void *)k_sweep_imp<DIM, N>, smem))) return e;           \
-    k_sweep_imp<DIM, N><<<ntasks, tthreads, smem, s>>>(a, tasks, prog, ticket);       \
+#define BTE_IMP(N)                                                                          \
+  case N:                                                                                   \
+    if (tthreads <= 288) {                                                                  \
+      if ((e = smem_attr((const void *)k_sweep_imp<DIM, N, 288, 3>, smem))) return e;       \
+      k_sweep_imp<DIM, N, 288, 3><<<ntasks, tthreads, smem, s>>>(a, tasks, prog, ticket);   \
+    } else {                                                                                \
+      if ((e = smem_attr((const void *)k_sweep_imp<DIM, N, 1024, 1>, smem))) return e;      \
+      k_sweep_imp<DIM, N, 1024, 1><<<ntasks, tthreads, smem, s>>>(a, tasks, prog, ticket);  \
+    }                                                                                       \
     break;
     BTE_IMP(1)
     BTE_IMP(2)
