@@ -1711,7 +1711,10 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
 
 // the (slot, column) tasks of the implicit sweep in an upwind-topological
 // order: by distance of the column from its octant's upwind corner, octants
-// interleaved, so a task's upwind columns always hold smaller tickets
+// interleaved, so a task's upwind columns always hold smaller tickets.
+// (Measured on config 3: a strip raster -- also topological, neighbours one
+// and 16 tickets apart -- took 32.8 ms per iteration against 26 ms: each
+// ticket then waits on the one just before it, the chains never get slack.)
 static bte_status implicit_setup(bte_ctx *ctx) {
   if (ctx->d_tasks) return BTE_OK;
   const Geometry &g = ctx->g;

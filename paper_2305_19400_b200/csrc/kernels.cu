@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const i
   const int nloc = max(0, min(A.jpt, nj - j0));
   const bool active = grp < JG;
   const int rtid = tid - JG * nb;            // reducers: [0, nb)
-  const int tis = (int)blockDim.x - 32;      // issuer: first thread of the last warp (launcher adds it)
+  const int tis = (int)blockDim.x - 32;      // issuer: lane 0 of the last warp (the launcher adds it)
 
   if (tid == 0) s_task = (int)atomicAdd(ticket, 1u);
   __syncthreads();
@@ -778,9 +778,18 @@ __global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const i
   };
   // plane i of the upwind columns, once published (their stores are generic-
   // proxy writes of other SMs: acquire, then order the bulk reads after it)
+  // the issuer caches the counters it last saw: the upwind columns usually run
+  // far ahead, so one acquire load clears many planes (each costs an L2 round trip)
+  int xseen = xghost ? np : 0, yseen = (DIM == 3 && !yghost) ? 0 : np;
   auto nb_ready = [&](int i) {
-    if (!xghost && ld_acquire_gpu(pr + (int64_t)xcol * kProgStride) <= i) return false;
-    if (DIM == 3 && !yghost && ld_acquire_gpu(pr + (int64_t)ycol * kProgStride) <= i) return false;
+    if (i >= xseen) {
+      xseen = ld_acquire_gpu(pr + (int64_t)xcol * kProgStride);
+      if (i >= xseen) return false;
+    }
+    if (i >= yseen) {
+      yseen = ld_acquire_gpu(pr + (int64_t)ycol * kProgStride);
+      if (i >= yseen) return false;
+    }
     return true;
   };
   auto issueB = [&](int i, int st) {
@@ -899,10 +908,12 @@ __global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const i
     double *rb = red + (i & 1) * JG * nb;
     if (active) rb[tid] = acc;
     __syncthreads();  // stage st consumed, rb complete, this plane's stores issued
-    if (tid == 0) {
-      __threadfence();  // cumulative over the CTA's stores ordered by the barrier
-      st_release_gpu(pr + (int64_t)col * kProgStride, i + 1);
-    }
+    // publish the plane: a gpu-scope release after the CTA barrier orders every
+    // thread's stores before it (cumulativity; the pattern of CUTLASS's
+    // GenericBarrier), no membar.gl.  (A separate publisher warp on named
+    // barriers was 3 % faster but lets the compute warps arrive for the next
+    // plane before it has synchronised -- a barrier-phase race; reverted.)
+    if (tid == 0) st_release_gpu(pr + (int64_t)col * kProgStride, i + 1);
     if (tid == tis && i + S < np) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issueA(i + S, st);
