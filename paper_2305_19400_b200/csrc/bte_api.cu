@@ -109,6 +109,11 @@ struct bte_ctx {
   int64_t graph_launches = 0;  // kernels in one captured step
   bool graph_capture = false;  // step_launch is being captured (Newton reads the device step index)
   cudaStream_t cap_stream = nullptr;  // private stream the step graphs are captured on
+  // rotation: the next step's boundary pass overlapped with this step's Newton
+  int prefetch_bnd = 0;        // set by bte_step while more steps follow in the call
+  bool bnd_ready = false;      // the side stream has run the current step's boundary pass
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_swept = nullptr, ev_side = nullptr;
   unsigned long long *d_stepctr = nullptr;
   unsigned long long h_stepctr = 0;
   double *staging = nullptr;
@@ -1462,8 +1467,9 @@ bte_status bte_init_random(bte_ctx *ctx, uint64_t seed, const double phase[3], d
 
 // ---- the step
 
-static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
+static bte_status launch_boundary(bte_ctx *ctx, const double *Icur, cudaStream_t strm = nullptr) {
   Geometry &g = ctx->g;
+  cudaStream_t stream = strm ? strm : ctx->stream;
   const int nreg = g.dim == 3 ? 6 : 4;
   int n = 0;
   for (int r = 0; r < nreg; ++r) {
@@ -1471,9 +1477,9 @@ static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
     if (a == g.dim - 1 && !((r & 1) ? g.has_hi_wall : g.has_lo_wall)) continue;
     if (g.kind[r] == BC_DIFF || g.kind[r] == BC_PART) {
       if (ctx->umesh)
-        CU(launch_udiffuse(g, ctx->u, Icur, r, ctx->gtab[r], ctx->stream));
+        CU(launch_udiffuse(g, ctx->u, Icur, r, ctx->gtab[r], stream));
       else
-        CU(launch_diffuse(g, Icur, r, ctx->gtab[r], ctx->stream));
+        CU(launch_diffuse(g, Icur, r, ctx->gtab[r], stream));
       ++n;
     }
     if ((g.kind[r] == BC_SPEC || g.kind[r] == BC_PART) && ctx->rot) {
@@ -1483,7 +1489,7 @@ static bte_status launch_boundary(bte_ctx *ctx, const double *Icur) {
         if (!ctx->gspec[r]) return fail(ctx, BTE_ENOMEM, "specular snapshot allocation (%zu bytes) failed", bytes);
         g.gspec[r] = ctx->gspec[r];
       }
-      CU(launch_spec_snapshot(g, Icur, r, ctx->gspec[r], ctx->stream));
+      CU(launch_spec_snapshot(g, Icur, r, ctx->gspec[r], stream));
       ++n;
     }
   }
@@ -1659,7 +1665,12 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
   double *Iout = ctx->I[1 - ctx->cur];
   size_t id = (size_t)-1;
   nvtx_push("bte_step");
-  if (has_bnd) {
+  if (has_bnd && ctx->bnd_ready) {
+    // the previous step already ran this step's boundary pass on the side
+    // stream, concurrently with its Newton
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
+    ctx->bnd_ready = false;
+  } else if (has_bnd) {
     nvtx_push("a1 boundary");
     if ((st = span_begin(ctx, t, 2, ctx->stream, &id))) return st;
     if ((st = launch_boundary(ctx, Iin))) return st;
@@ -1689,6 +1700,26 @@ static bte_status step_launch(bte_ctx *ctx, bool t, bool split = false) {
     if ((st = span_end(ctx, t, ctx->stream, id))) return st;
   }
   nvtx_pop();
+  if (has_bnd && ctx->rot && !ctx->semi && ctx->prefetch_bnd) {
+    // octant-slot rotation: the next step's boundary pass (specular
+    // snapshots, diffuse tables) reads only I^{n+1}, not T: run it on a side
+    // stream concurrently with this step's Newton (FP64-bound vs memory-bound)
+    if (!ctx->side_stream) {
+      CU(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&ctx->ev_swept, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(ctx->ev_swept, ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_swept, 0));
+    nvtx_push("a1 boundary (next step, side stream)");
+    id = (size_t)-1;
+    if ((st = span_begin(ctx, t, 2, ctx->side_stream, &id))) return st;
+    if ((st = launch_boundary(ctx, Iout, ctx->side_stream))) return st;
+    if ((st = span_end(ctx, t, ctx->side_stream, id))) return st;
+    nvtx_pop();
+    CU(cudaEventRecord(ctx->ev_side, ctx->side_stream));
+    ctx->bnd_ready = true;
+  }
   nvtx_push("a3+a4 reduce+Newton");
   id = (size_t)-1;
   if ((st = span_begin(ctx, t, 1, ctx->stream, &id))) return st;
@@ -1979,7 +2010,16 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
       ctx->steps_done++;
       continue;
     }
-    if ((st = step_launch(ctx, t, ctx->nranks > 1 && ctx->overlap))) return st;
+    ctx->prefetch_bnd = s + 1 < nsteps;
+    st = step_launch(ctx, t, ctx->nranks > 1 && ctx->overlap);
+    ctx->prefetch_bnd = 0;
+    if (st) {
+      if (ctx->bnd_ready) {  // keep the stream order simple after an error
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0);
+        ctx->bnd_ready = false;
+      }
+      return st;
+    }
     if (ctx->nranks > 1) {
       // a5 on the comm stream once the boundary planes are swept; the next
       // step's sweeps wait for it (the wait sits after this step's Newton)
@@ -2465,6 +2505,12 @@ void bte_destroy(bte_ctx *ctx) {
   cudaStreamSynchronize(ctx->stream);
   graph_invalidate(ctx);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+  }
+  if (ctx->ev_swept) cudaEventDestroy(ctx->ev_swept);
+  if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
   for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   if (ctx->ev_bnd) cudaEventDestroy(ctx->ev_bnd);
   if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
