@@ -53,8 +53,8 @@ WEAK = (5,)  # configs whose per-GPU load is fixed as N grows
 def _problem(config: int, nranks: int):
     """The workload of --config at N ranks (the whole problem; the library
     derives each rank's slab)."""
-    if config in (7, 8, 9) and nranks > 1:
-        raise SystemExit("unstructured workloads (--config 7/8/9) are benchmarked on one GPU")
+    if config in (7, 8, 9, 11) and nranks > 1:
+        raise SystemExit("unstructured workloads (--config 7/8/9/11) are benchmarked on one GPU")
     makers = {
         1: bi.config1,        # BASELINE configs[0]: latency-bound, not roofline-gated
         2: bi.config2,        # configs[1]: 2-D 120^2 (strong scaling over y slabs at N > 1)
@@ -65,6 +65,7 @@ def _problem(config: int, nranks: int):
         8: bi.config_u3,      # unstructured analogue of config 3
         9: bi.config_uq,      # config 7 on jittered quadrilaterals
         10: bi.config_fig9,   # the paper's second example (Fig. 9, reading R-m)
+        11: bi.config_u3h,    # config 3 on jittered hexahedra (reading R-o)
     }
     if config == 5:           # configs[4]: 64^3 per GPU (weak scaling)
         return bi.config5(nranks)
@@ -234,7 +235,10 @@ def _slab_sample(p, nrows, nthreads):
 
 def _umesh_sample(p, n, nthreads):
     import oracle
-    mk = bi.config_u3 if p.mesh.dim == 3 else (bi.config_uq if p.mesh.cells.shape[1] == 4 else bi.config_u2)
+    if p.mesh.dim == 3:
+        mk = bi.config_u3h if p.mesh.cells.shape[1] == 8 else bi.config_u3
+    else:
+        mk = bi.config_uq if p.mesh.cells.shape[1] == 4 else bi.config_u2
     sp = mk(n=n)
     o = oracle.Oracle(sp, nthreads=nthreads)
     I, T = o.random_state()
@@ -246,12 +250,12 @@ def _sized_sample(p, per_step_s, nthreads):
     at nthreads: (problem, oracle, I, T, description of the sample)."""
     m = p.mesh
     if hasattr(m, "cells"):
-        n_full = 120 if m.dim == 2 else 32
+        n_full = 120 if m.dim == 2 else (64 if m.cells.shape[1] == 8 else 32)
         sp, o, I, T = _umesh_sample(p, 4, nthreads)
         t = time.perf_counter()
         o.run(I, T, 1)
         per_cell = (time.perf_counter() - t) / sp.mesh.ncells
-        per_unit = 2 if m.dim == 2 else 6
+        per_unit = 2 if m.dim == 2 else (1 if m.cells.shape[1] == 8 else 6)
         n = int(max(2, min(n_full, ((per_step_s / max(per_cell, 1e-12)) / per_unit) ** (1.0 / m.dim))))
         sp, o, I, T = _umesh_sample(p, n, nthreads)
         return sp, o, I, T, f"{sp.name} (the same generator at n = {n} instead of {n_full})"

@@ -768,6 +768,16 @@ def config_u3(n: int = 32, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20)
     return p
 
 
+def config_u3h(n: int = 64, n_freq: int = 29, n_theta: int = 20, n_phi: int = 20) -> Problem:
+    """config 3 on jittered hexahedra (R-o): n^3 cells of 1 um with bilinear
+    faces, 400 directions, 40 channels, z walls 300/310 K, x/y specular."""
+    p = config3(n=n, n_freq=n_freq, n_theta=n_theta, n_phi=n_phi)
+    p.mesh = umesh_hex(n, n, n, 1e-6, jitter=0.1, seed=SEED_BASE + 11)
+    p.name = f"u3h_hex_{n**3}x{n_theta*n_phi}x{p.bands.nb}"
+    p.seed = SEED_BASE + 11
+    return p
+
+
 def small_umesh(dim: int = 2, n=(4, 3, 2), dirs=None, bands=None, bcs=None, dt=1e-12, shuffle=False,
                 jitter=None, seed=17, quad=False, hexa=False) -> Problem:
     """Small unstructured case for parity tests (hexa: hexahedra in 3-D)."""

@@ -2274,6 +2274,11 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   const int nb = FIX ? NBT : g.nb, nj = FIX ? NJT : g.nj;
   const int E = FIX ? NBT * NJT : g.E, Es = FIX ? (NBT * NJT + ((NBT * NJT) & 1)) : g.Es;
   const int NBP = nb >> 1;
+  // face-list words per direction (aout, nin, ain[], src[]); staged inflow
+  // slots (hexahedra: 3 -- a direction crossing more inflow faces takes the
+  // generic path); device face-row width
+  constexpr int KUW = KF > 4 ? 2 + 2 * KF : kUW, SRC = KF > 4 ? 2 + KF : 6;
+  constexpr int NIN = KF > 4 ? 3 : KF - 1, KP = KF > 4 ? 8 : 4;
   const int S = A.stages, Q = A.chunk;  // S is a power of two
   const int Sm = S - 1, Sl = __ffs(S) - 1;
   const int tid = threadIdx.x;
@@ -2283,17 +2288,17 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   const int JG = FIX ? NJT / JPT : A.jg;
   const bool active = jg < JG;
   // stage layout (doubles): own[Es] | I0[nb] | beta[nb] | an[12] | nbr[4] (int64)
-  const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 12;
-  const int sd = o_nb + 4;
+  const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 3 * KP;
+  const int sd = o_nb + KP;
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);        // [S]
   int *slow = reinterpret_cast<int *>(smraw + 64);            // [4] cell needs the generic path
   double *stg = reinterpret_cast<double *>(smraw + 128);      // [S][sd]
   double *red = stg + (size_t)S * sd;                         // [2][JG][nb]
   double *red2 = red + 2 * JG * nb;                           // [2][8][nb]
   double *sws = red2 + 2 * 8 * nb;                            // [nj][4]
-  double *fl = sws + 4 * nj;                                  // [4][nj][kUW]
+  double *fl = sws + 4 * nj;                                  // [4][nj][KUW]
   // inflow neighbour values: [2 cells][KF-1 slots][JPT][nt] (16 B each)
-  double2 *nbuf = reinterpret_cast<double2 *>(fl + ((4 * nj * kUW + 1) & ~1));
+  double2 *nbuf = reinterpret_cast<double2 *>(fl + ((4 * nj * KUW + 1) & ~1));
   const int slot = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * Q;
   const int n = (int)min((int64_t)Q, u.ncells - c0);
@@ -2304,12 +2309,12 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     const int st = i & Sm;
     const int64_t cell = c0 + i;
     double *sp = stg + (size_t)st * sd;
-    mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + 16) * 8u);
+    mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + 4 * KP) * 8u);
     bulk_g2s(sp, Is + cell * Es, (uint32_t)E * 8u, &full[st]);
     bulk_g2s(sp + o_i0, A.I0c + cell * nb, (uint32_t)nb * 8u, &full[st]);
     bulk_g2s(sp + o_be, A.beta + cell * nb, (uint32_t)nb * 8u, &full[st]);
-    bulk_g2s(sp + o_an, u.an + cell * 12, 96u, &full[st]);
-    bulk_g2s(sp + o_nb, u.nbr + cell * 4, 32u, &full[st]);
+    bulk_g2s(sp + o_an, u.an + cell * 3 * KP, 24u * KP, &full[st]);
+    bulk_g2s(sp + o_nb, u.nbr + cell * KP, 8u * KP, &full[st]);
   };
   // face lists of cell i (the last nj threads: the reducers and the issuing
   // thread sit in other warps, so no warp carries two extra jobs), from its stage
@@ -2322,7 +2327,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     const double *sp = stg + (size_t)st * sd;
     const int64_t *rn = reinterpret_cast<const int64_t *>(sp + o_nb);
     const double *sv = sws + 4 * pj;
-    double *w = fl + ((size_t)(i & 3) * nj + pj) * kUW;
+    double *w = fl + ((size_t)(i & 3) * nj + pj) * KUW;
     int64_t *wi = reinterpret_cast<int64_t *>(w);
     double aout = 0.0;
     int nin = 0;
@@ -2336,14 +2341,14 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
         aout += a;
       } else {
         w[2 + nin] = a;
-        wi[6 + nin] = rn[f] >= 0 ? rn[f] * Es : rn[f];  // source block offset, or the wall code (< 0)
+        wi[SRC + nin] = rn[f] >= 0 ? rn[f] * Es : rn[f];  // source block offset, or the wall code (< 0)
         ++nin;
       }
     }
-    if (nin == KF) generic = true;
+    if (nin > NIN) generic = true;
     for (int f = nin; f < KF; ++f) {
       w[2 + f] = 0.0;
-      wi[6 + f] = -1;
+      wi[SRC + f] = -1;
     }
     w[0] = aout;
     wi[1] = nin;
@@ -2351,7 +2356,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   };
 
   for (int t = tid; t < 4 * nj; t += nt) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
-  for (int t = tid; t < 2 * (KF - 1) * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
+  for (int t = tid; t < 2 * NIN * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
   if (tid < 4) slow[tid] = 0;
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
@@ -2369,16 +2374,16 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   // stage the inflow values of cell i (slot f of direction r at nbuf[((i&1)(KF-1) + f) JPT + r][tid])
   auto prefetch = [&](int i) {
     if (active && i < n) {
-      const double *w = fl + ((size_t)(i & 3) * nj + jg) * kUW;
+      const double *w = fl + ((size_t)(i & 3) * nj + jg) * KUW;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         if (jg + r * JG < nj) {
-          const int64_t *wi = reinterpret_cast<const int64_t *>(w + (size_t)r * JG * kUW);
+          const int64_t *wi = reinterpret_cast<const int64_t *>(w + (size_t)r * JG * KUW);
 #pragma unroll
-          for (int f = 0; f < KF - 1; ++f) {
-            const int64_t src = wi[6 + f];
+          for (int f = 0; f < NIN; ++f) {
+            const int64_t src = wi[SRC + f];
             if (src >= 0) {
-              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * (KF - 1) + f) * JPT + r)) * nt + tid);
+              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * NIN + f) * JPT + r)) * nt + tid);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                            "l"(Is + src + e0 + r * JG * nb)
                            : "memory");
@@ -2405,18 +2410,18 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
       const bool generic = slow[i & 3] != 0;  // CTA-uniform
-      const double2 *nb2 = nbuf + (size_t)((i & 1) * (KF - 1) * JPT) * nt + tid;
+      const double2 *nb2 = nbuf + (size_t)((i & 1) * NIN * JPT) * nt + tid;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
         if (j < nj) {
-          const double *w = fl + ((size_t)(i & 3) * nj + j) * kUW;
+          const double *w = fl + ((size_t)(i & 3) * nj + j) * KUW;
           const int e = e0 + r * JG * nb;
           const double2 Ic = *reinterpret_cast<const double2 *>(sp + e);
           double f0 = w[0] * Ic.x, f1 = w[0] * Ic.y;
           if (!generic) {
 #pragma unroll
-            for (int f = 0; f < KF - 1; ++f) {  // unused slots: a = 0 times a finite stale value
+            for (int f = 0; f < NIN; ++f) {  // unused slots: a = 0 times a finite stale value
               const double a = w[2 + f];
               const double2 up = nb2[(size_t)(f * JPT + r) * nt];
               f0 = fma(a, up.x, f0);
@@ -2427,9 +2432,9 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
             const int nin = (int)wi[1];
             for (int f = 0; f < nin; ++f) {
               const double a = w[2 + f];
-              const int64_t src = wi[6 + f];
+              const int64_t src = wi[SRC + f];
               double2 up;
-              if (src >= 0 && f < KF - 1) {
+              if (src >= 0 && f < NIN) {
                 up = nb2[(size_t)(f * JPT + r) * nt];
               } else if (src >= 0) {
                 up = __ldg(reinterpret_cast<const double2 *>(Is + src + e));
@@ -2490,7 +2495,7 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
   USweepArgs a = a0;
   const Geometry &g = a.g;
   if (a.u.ncells == 0) return cudaSuccess;
-  if (a.pipelined && a.u.K <= 4 && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
+  if (a.pipelined && (a.u.K <= 4 || a.u.K == 6) && g.nb % 2 == 0 && 8 * g.nb <= 1024) {
     const int NBP = g.nb / 2;
     // 2 directions x 2 channels per thread on triangles (measured 3 % faster on u2),
     // 1 x 2 on tetrahedra (their 4-face lists fill the registers)
@@ -2504,10 +2509,11 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.jg = JG;
       a.chunk = a.chunk > 0 ? a.chunk : 64;
       // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
+      const int K = a.u.K, KUW = K > 4 ? 2 + 2 * K : kUW, NIN = K > 4 ? 3 : K - 1, KP = K > 4 ? 8 : 4;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
-                                  4 * (size_t)g.nj * kUW + 2) * sizeof(double) +
-                           2 * (size_t)(a.u.K - 1) * jpt * threads * 16;
-      const size_t sd = (size_t)g.Es + 2 * g.nb + 16;
+                                  4 * (size_t)g.nj * KUW + 2) * sizeof(double) +
+                           2 * (size_t)NIN * jpt * threads * 16;
+      const size_t sd = (size_t)g.Es + 2 * g.nb + 4 * KP;
       int S = a.stages > 0 ? a.stages : (int)(((size_t)226 * 1024 - fixed) / (sd * 8));
       S = std::max(4, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
@@ -2527,6 +2533,7 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
           if (jpt == 1 && JG == 50 && threads == 1000) {
             if (a.u.K == 3) BTE_UTMA_(1, 3, 40, 50)
             if (a.u.K == 4) BTE_UTMA_(1, 4, 40, 50)
+            if (a.u.K == 6) BTE_UTMA_(1, 6, 40, 50)
           }
           if (jpt == 2 && JG == 25 && threads == 500) {
             if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
@@ -2537,6 +2544,8 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
         BTE_UTMA(2, 3)
         BTE_UTMA(1, 4)
         BTE_UTMA(2, 4)
+        BTE_UTMA(1, 6)
+        BTE_UTMA(2, 6)
 #undef BTE_UTMA
 #undef BTE_UTMA_
       }

@@ -16,7 +16,7 @@ ap.add_argument("--start", default="random")
 ap.add_argument("--tau", type=int, default=0)
 a = ap.parse_args()
 p = {2: bi.config2, 3: bi.config3, 4: bi.config4, 1: bi.config1, 5: bi.config5, 6: bi.config_demo, 7: bi.config_u2,
-     8: bi.config_u3, 9: bi.config_uq, 10: bi.config_fig9}[a.config]()
+     8: bi.config_u3, 9: bi.config_uq, 10: bi.config_fig9, 11: bi.config_u3h}[a.config]()
 with Solver.from_problem(p) as sv:
     if a.tau:
         sv.set_tau_mode(a.tau)
