@@ -1161,3 +1161,74 @@ def test_implicit_errors(Solver, monkeypatch):
     with Solver.from_problem(p) as sv:
         with pytest.raises(BteError):
             sv.set_step_mode(2)  # every iteration re-reads I^n: two buffers needed
+
+
+# ----------------------------------------------------------------- degenerate sizes and edge cases
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 1, 5), (7, 1, 1), (1, 6, 1), (2, 2, 1)])
+def test_degenerate_3d_boxes_400x40(Solver, shape):
+    """The BASELINE 400 x 40 tables (the TMA sweep) on boxes whose every column
+    is a wall column in x and/or y, single-plane columns and a single cell;
+    every wall kind."""
+    p = bi.config3()
+    p.mesh = bi.Mesh(3, *shape, p.mesh.dx, p.mesh.dy, p.mesh.dz)
+    p.bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(3, specularity=0.3),
+             bi.WallBC(0, None, 298.0), bi.WallBC(1)]
+    (rel, dT), _ = _run_both(Solver, p, 4)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (9, 1), (1, 9)])
+def test_degenerate_2d_strips(Solver, shape):
+    p = bi.config2(n=4)
+    p.mesh = bi.Mesh(2, shape[0], shape[1], 1, p.mesh.dx, p.mesh.dy, 1.0)
+    p.bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 300.0), bi.WallBC(0, None, 310.0),
+             bi.WallBC(1), bi.WallBC(1)]
+    (rel, dT), _ = _run_both(Solver, p, 5)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
+
+
+def test_zero_steps_and_repeated_calls(Solver):
+    """step(0) changes nothing; many step(1) calls equal one step(n) call (the
+    graph-replayed path) bit for bit; the step counter in error messages follows."""
+    p = bi.small_3d(6, 5, 4)
+    I, T = oracle.Oracle(p).random_state()
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(0)
+        assert np.array_equal(sv.intensity(), I) and np.array_equal(sv.temperature(), T)
+        for _ in range(6):
+            sv.step(1)
+        a = (sv.intensity(), sv.temperature())
+    with Solver.from_problem(p) as sv:
+        sv.set_state(I, T)
+        sv.step(6)
+        b = (sv.intensity(), sv.temperature())
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_slab_group_one_plane_slabs(Solver):
+    """As many slabs as planes (every rank owns one plane: both halo planes are
+    live, walls only on the end ranks) against the oracle."""
+    p = _group_case("3d")
+    p.mesh = bi.Mesh(3, 4, 3, 5, p.mesh.dx, p.mesh.dy, p.mesh.dz)
+    o = oracle.Oracle(p)
+    I, T = o.random_state()
+    group = []
+    try:
+        for r in range(5):
+            sv = Solver(p.mesh, p.dirs, p.bands, p.dt, p.T_init, rank=r, nranks=5)
+            group.append(sv)
+            for reg in range(6):
+                sv.set_wall(reg, p.bcs[reg])
+            ncross = sv.ncells // sv.nz_local
+            c0, c1 = sv.z0 * ncross, (sv.z0 + sv.nz_local) * ncross
+            sv.set_state(I[c0:c1], T[c0:c1])
+        assert all(sv.nz_local == 1 for sv in group)
+        Solver.group_step(group, 4)
+        Ig = np.concatenate([sv.intensity() for sv in group])
+        Tg = np.concatenate([sv.temperature() for sv in group])
+    finally:
+        for sv in group:
+            sv.close()
+    _assert_oracle(p, I, T, 4, Ig, Tg)
