@@ -1256,7 +1256,10 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   // small problems: enough segments for ~8 CTAs per SM (config 1, 20 x 20
   // cells x 4 quadrants: 1 -> 15 segments, sweep 0.019 -> 0.0085 ms)
   {
-    int nseg = std::max(1, (int)((g.nplanes + 8) / 16));
+    // 3-D: ~32-plane segments (ncu, round 2: config 4 17.63 -> 17.50 B/DOF, sweep
+    // 6.15 -> 6.06 ms; config 3 17.66 -> 17.53 B/DOF; full columns raise the
+    // y-upwind L2 misses to 18.4-20.2 B/DOF; profiles/round2_ab_seg.jsonl)
+    int nseg = g.dim == 3 ? std::max(1, (int)((g.nplanes + 16) / 32)) : std::max(1, (int)((g.nplanes + 8) / 16));
     const int64_t tasks = (int64_t)g.ncross * g.nslot;
     const int64_t want = 8 * 148;
     if (tasks * nseg < want) nseg = (int)std::min<int64_t>(g.nplanes, (want + tasks - 1) / tasks);

@@ -130,7 +130,7 @@ __device__ __forceinline__ int sweep_column(const SweepArgs &A, int id) {
 // thread, and the octant partial sum over j accumulates in a register before
 // a JG-way fixed-order smem combine.
 template <int DIM, int JMAX>
-__global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
+__global__ void __launch_bounds__(JMAX == 1 ? 448 : 1024, JMAX == 1 ? 4 : 1) k_sweep(const SweepArgs A) {
   extern __shared__ double sm[];  // coef[nj][4] | red[2][JG][nb]
   const Geometry &g = A.g;
   const int nb = g.nb, nj = g.nj, Es = g.Es;
@@ -201,6 +201,55 @@ __global__ void __launch_bounds__(1024) k_sweep(const SweepArgs A) {
     }
   }
   __syncthreads();
+
+  if (!xghost && (DIM == 2 || !yghost)) {
+    // interior column (every column but the wall ones): running pointers along
+    // the march, no per-cell 64-bit index products, no ghost branches
+    const int e0 = j0 * nb + b;
+    const int64_t pstep = (int64_t)step * g.plane_stride;
+    const int64_t cstep = (int64_t)step * g.ncross * nb;
+    const int64_t dstep = cstep * g.nslot;
+    const int64_t c0 = (int64_t)col + (int64_t)p * g.ncross;
+    const double *ip = Is + (int64_t)(p + g.plane_off) * g.plane_stride + colE + e0;
+    double *op = Os + (int64_t)(p + g.plane_off) * g.plane_stride + colE + e0;
+    const double *i0p = A.I0c + c0 * nb + b;
+    const double *bp = A.beta + c0 * nb + b;
+    double *dp = A.Dpart + (c0 * g.nslot + slot) * nb + (tid < nb ? tid : 0);
+    const double *cq = coef + 4 * j0;
+    for (int i = 0; i < np; ++i) {
+      double acc = 0.0;
+      if (active) {
+        const double I0 = ldg(i0p);
+        const double dtb = dt * ldg(bp);
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+          if (k < nloc) {
+            const double Ic = ldg(ip + k * nb);
+            const double xu = ldg(ip + xoff + k * nb);
+            const double yu = DIM == 3 ? ldg(ip + yoff + k * nb) : 0.0;
+            const double In = bte_update<DIM>(Ic, xu, yu, prev[k], cq + 4 * k, v, I0, dtb);
+            op[k * nb] = In;
+            acc = fma(cq[4 * k + 3], I0 - In, acc);
+            prev[k] = Ic;
+          }
+        }
+      }
+      double *rb = red + (i & 1) * JG * nb;
+      if (active) rb[tid] = acc;
+      __syncthreads();
+      if (tid < nb) {
+        double s = 0.0;
+        for (int q = 0; q < JG; ++q) s += rb[q * nb + tid];
+        *dp = s;
+      }
+      ip += pstep;
+      op += pstep;
+      i0p += cstep;
+      bp += cstep;
+      dp += dstep;
+    }
+    return;
+  }
 
   int buf = 0;
   for (int i = 0; i < np; ++i, p += step) {
