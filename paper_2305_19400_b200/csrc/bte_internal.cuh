@@ -127,14 +127,13 @@ struct SweepArgs {
   int stages_override;    // 0 = automatic
   int target_threads;     // CTA size target (0 = 448)
   int smem_budget_kb;     // per-CTA shared memory budget for the stage ring (0 = 113 KB)
-  int stcs;               // streaming (evict-first) stores of I^{n+1}
-  int l2hint;             // bulk-copy L2 policies: 0 none, 1 last-use evict-first, 2 + own evict-last
   int64_t stage_doubles;  // doubles per stage (set by launch_sweep)
   int col0, ncols;        // column range of this launch (ncols = 0: all)
   int slot0, nslots;      // octant slots of this launch (nslots = 0: all)
   int64_t out_off[kMaxSlots];  // where slot s of I^{n+1} goes in Iout
   int p_lo, p_hi;         // owned-plane range of this launch (p_hi <= p_lo: all)
   int no_spare;           // 1: side jobs on compute threads (A/B switch read at create)
+  int pf;                 // k_sweep: L2 prefetch distance in cells (0: off)
   int raster;             // 3-D column order: strips of `raster` columns along x (0: row-major)
 };
 

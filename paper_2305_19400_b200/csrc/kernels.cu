@@ -216,8 +216,19 @@ __global__ void __launch_bounds__(JMAX == 1 ? 448 : 1024, JMAX == 1 ? 4 : 1) k_s
     const double *bp = A.beta + c0 * nb + b;
     double *dp = A.Dpart + (c0 * g.nslot + slot) * nb + (tid < nb ? tid : 0);
     const double *cq = coef + 4 * j0;
+    const int pf = A.pf;
     for (int i = 0; i < np; ++i) {
       double acc = 0.0;
+      if (active && pf > 0 && i + pf < np) {
+        // L2 prefetch of this thread's elements pf cells ahead (no registers held)
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k)
+          if (k < nloc) asm volatile("prefetch.global.L2 [%0];" ::"l"(ip + pf * pstep + k * nb));
+        if (grp == 0) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(i0p + pf * cstep));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(bp + pf * cstep));
+        }
+      }
       if (active) {
         const double I0 = ldg(i0p);
         const double dtb = dt * ldg(bp);
@@ -338,25 +349,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// L2 eviction-priority policies for bulk copies
-__device__ __forceinline__ uint64_t l2_policy(int kind) {
-  uint64_t pol;
-  if (kind == 1)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  else if (kind == 2)
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                              uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
 // TMA bulk copy global -> shared (UBLKCP), completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -453,17 +445,9 @@ __global__ void __launch_bounds__(NBT == 40 ? 448 : 1024, NBT == 40 ? 2 : 1) k_s
     const uint32_t blk = (uint32_t)Es * 8u;
     const uint32_t row = (uint32_t)nb * 8u;
     mbar_expect_tx(&full[st], blk * nblk + (rows_tma ? 2u * row : 0u));
-    if (A.l2hint) {
-      // own/x-upwind: keep (read again by the next columns); y-upwind: last use this step
-      const uint64_t keep = l2_policy(A.l2hint == 2 ? 2 : 0), last = l2_policy(1);
-      bulk_g2s_hint(sp, Is + base, blk, &full[st], keep);
-      if (!xghost) bulk_g2s_hint(sp + o_x, Is + base + xoff, blk, &full[st], DIM == 3 ? keep : last);
-      if (ystage && !yghost) bulk_g2s_hint(sp + o_y, Is + base + yoff, blk, &full[st], last);
-    } else {
-      bulk_g2s(sp, Is + base, blk, &full[st]);
-      if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
-      if (ystage && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
-    }
+    bulk_g2s(sp, Is + base, blk, &full[st]);
+    if (!xghost) bulk_g2s(sp + o_x, Is + base + xoff, blk, &full[st]);
+    if (ystage && !yghost) bulk_g2s(sp + o_y, Is + base + yoff, blk, &full[st]);
     if (rows_tma) {
       bulk_g2s(sp + o_i0, A.I0c + cell * nb, row, &full[st]);
       bulk_g2s(sp + o_be, A.beta + cell * nb, row, &full[st]);
@@ -1580,9 +1564,10 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const Newton
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
   // cells of the column range [col0, col0 + ncols) over all planes
   const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
+  const int lane = threadIdx.x & 31;
   for (int64_t q = (int64_t)blockIdx.x * kNewtonWarps + warp; q < nq; q += nwarps) {
     const int64_t p = q / ncol;
-    newton_cell<BAND>(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, threadIdx.x & 31);
+    newton_cell<BAND>(a, a.col0 + (q - p * ncol) + p * a.ncross, sA, sX, sI, cs, lane);
   }
 }
 
