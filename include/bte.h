@@ -123,7 +123,13 @@ typedef struct {
  * pointer / (ptr, alloc_ctx); NULL -> cudaMalloc/cudaFree.
  * rank/nranks/nccl_id: multi-GPU slab decomposition along the slowest axis
  * (z for dim 3, y for dim 2); nccl_id = 128-byte ncclUniqueId broadcast by the
- * caller (e.g. through torch.distributed), ignored when nranks == 1. */
+ * caller (e.g. through torch.distributed), ignored when nranks == 1.
+ * An nccl_id whose first 7 bytes are "BTELOOP" selects the in-process loopback
+ * transport instead of NCCL (test infrastructure): the ranks are threads of one
+ * process sharing that id, every send/recv/AllGather is matched across them at
+ * group end and executed as stream-ordered device copies, so the multi-rank
+ * code path runs on one GPU; a rank that never reaches an exchange makes its
+ * peers fail with BTE_ENCCL after 120 s. */
 typedef struct {
   double dt;
   double T_init;

@@ -5,9 +5,9 @@ sm_100a in ``csrc/``).  ``bte.Solver`` is its thin ctypes binding.  There is
 no CPU path: without the built library or a CUDA device, ``Solver`` raises.
 """
 from .bte import (BC_DIFFUSE, BC_ISOTHERMAL, BC_PARTIAL, BC_SPECULAR, I0_BOSE_EINSTEIN, I0_LINEAR, LIB_PATH,
-                  BteError, Solver, load_library, nccl_unique_id, partition_rcb, plan_band, plan_slab, plan_umesh,
+                  BteError, Solver, load_library, loopback_unique_id, nccl_unique_id, partition_rcb, plan_band, plan_slab, plan_umesh,
                   read_mesh)
 
-__all__ = ["Solver", "BteError", "load_library", "nccl_unique_id", "plan_band", "plan_slab", "plan_umesh", "LIB_PATH",
+__all__ = ["Solver", "BteError", "load_library", "loopback_unique_id", "nccl_unique_id", "plan_band", "plan_slab", "plan_umesh", "LIB_PATH",
            "read_mesh", "partition_rcb",
            "BC_ISOTHERMAL", "BC_SPECULAR", "BC_DIFFUSE", "BC_PARTIAL", "I0_LINEAR", "I0_BOSE_EINSTEIN"]

@@ -474,6 +474,13 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def loopback_unique_id() -> bytes:
+    """A fresh id for the in-process loopback transport (include/bte.h, bte_run):
+    ranks as threads of one process, exchanges as device copies -- the
+    multi-rank code path on one GPU (test infrastructure)."""
+    return b"BTELOOP\0" + os.urandom(16) + bytes(104)
+
+
 def plan_umesh(mesh, nranks: int, rank: int) -> dict:
     """bte_plan_umesh (host only): the cell partition libbte uses for an
     unstructured mesh -- owned range, halo cells (canonical), per-peer lists."""

@@ -100,6 +100,7 @@ struct bte_ctx {
   int raster = 0;          // 3-D sweep column order (SweepArgs.raster); env BTE_RASTER
   int sc_direct = 0;       // env BTE_SC_DIRECT=1: direct band integrals in the self-consistent Newton (A/B)
   int ugeneric = 0;        // env BTE_UGENERIC=1: generic unstructured sweep (A/B)
+  int usingle = 0;         // env BTE_USINGLE=1: one neighbour buffer, 2 CTAs/SM on triangles (A/B)
   int dbg_skip_exchange = 0;  // bte_set_debug(BTE_DEBUG_SKIP_EXCHANGE): mutation tests only
   double *d_energy = nullptr; // bte_get_energy scratch
   // CUDA-graph replay of explicit steps (SURVEY 8(b) "graph replay"): one
@@ -1274,6 +1275,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   if (const char *e = getenv("BTE_GRAPH")) ctx->use_graph = atoi(e) != 0;
   if (const char *e = getenv("BTE_SC_DIRECT")) ctx->sc_direct = atoi(e) != 0;
   if (const char *e = getenv("BTE_UGENERIC")) ctx->ugeneric = atoi(e) != 0;
+  if (const char *e = getenv("BTE_USINGLE")) ctx->usingle = atoi(e) != 0;
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_STATS"))
@@ -1598,6 +1600,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
     a.stages = ctx->stages_override;
     a.chunk = ctx->seg_override;
     a.generic = ctx->ugeneric;
+    a.single_buf = ctx->usingle;
     CU(launch_usweep(a, ctx->stream));
     ctx->tacc.launches++;
     ctx->tacc.sweep_launches++;
@@ -1978,7 +1981,7 @@ bte_status bte_step(bte_ctx *ctx, int64_t nsteps) {
     for (int64_t s = 0; s < nsteps; ++s) {
       const bool t = ctx->timing && ctx->timing_used < ctx->timing_max;
       if ((st = band_sweep_launch(ctx, t))) return st;
-      if (ctx->nranks > 1) {  // AllGather of the per-cell partials, in place
+      if (ctx->nranks > 1 && !ctx->dbg_skip_exchange) {  // AllGather of the per-cell partials, in place
         size_t id = (size_t)-1;
         if ((st = span_begin(ctx, t, 3, ctx->stream, &id))) return st;
         std::string emsg;
@@ -2219,6 +2222,7 @@ static bte_status ugroup_exchange(bte_ctx **ctxs, int n, bool output) {
 
 // NCCL: pack, grouped send/recv of the packed segments, scatter into the halo.
 static bte_status uhalo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream) {
+  if (ctx->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   const Geometry &g = ctx->g;
   if (!stream) stream = ctx->stream;
   std::string emsg;
@@ -2310,6 +2314,7 @@ static bte_status halo_exchange(bte_ctx *ctx, double *Ibuf, cudaStream_t stream)
   // a5: execute this rank's halo plan (bte_plan_slab) as one NCCL group on
   // `stream` (default: the context stream); plane p (global) lives at local
   // index p - m0 + plane_off.
+  if (ctx->dbg_skip_exchange) return BTE_OK;  // mutation tests (bte_set_debug)
   const Geometry &g = ctx->g;
   if (!stream) stream = ctx->stream;
   std::string emsg;

@@ -1266,8 +1266,8 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // W*sum c_b dI0_b/dT in *F (without K0) and *Fp (identical in every lane).
 // Node term g = A/(e^x - 1), x = X/T, r = 1/(e^x - 1):
 //   dg/dT = g (x/T)(1 + r),   d2g/dT2 = g (1 + r)(x/T^2)(x(1 + 2r) - 2).
-__device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, const double *sA, double *scr,
-                                           int lane, double *F, double *Fp) {
+__device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, const double *sA, const int *sIB,
+                                           double *scr, int lane, double *F, double *Fp) {
   const int nb = a.nb;
   const double *cs = scr;
   double *sE = scr + nb, *sM = sE + kNGL, *sR = sM + kNGL;
@@ -1293,7 +1293,7 @@ __device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, con
     const int b = rd * 8 + (lane & 7);
     double f = 0.0, fp = 0.0, f2 = 0.0;
     if (b < nb) {
-      const int ib = a.m.ib[b];
+      const int ib = sIB[b];  // band index of channel b (shared-memory copy of a.m.ib)
       const double Rb = sR[ib];
       const double bi = (double)ib;
 #pragma unroll
@@ -1394,7 +1394,7 @@ __device__ void newton_cell(const NewtonArgs &a, int64_t c, const double *sA, co
       if (it > 0) {
         if (uni) {
           double fw, fpw;
-          eval_channels(a, T, sA, cs, lane, &fw, &fpw);
+          eval_channels(a, T, sA, sI + 4 * (a.m.imax + 1), cs, lane, &fw, &fpw);
           F = fw + K0;
           Fp = fpw;
           evaluated_at = T;
@@ -1559,6 +1559,8 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, MINB) k_newton(const Newton
       sX[j * R + b] = a.m.X[i];
     }
     for (int i = threadIdx.x; i < 4 * (a.m.imax + 1); i += blockDim.x) sI[i] = a.m.ichan[i];
+    if (a.m.uniform)  // band index per channel, after ichan (read every eval_channels round)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) sI[4 * (a.m.imax + 1) + i] = a.m.ib[i];
   }
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
@@ -1688,10 +1690,12 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const Newto
   double *scr = sA + R * kNGL + warp * (ws0 + nb);
   double *sI0 = scr + nb + 2 * kNGL + a.m.imax + 1, *sD0 = sI0 + nb;
   double *sDb = scr + ws0;
+  int *sIB = reinterpret_cast<int *>(sA + R * kNGL + kNewtonWarps * (ws0 + nb));  // [nb] band index per channel
   for (int i = threadIdx.x; i < nb * kNGL; i += blockDim.x) {
     const int b = i / kNGL, j = i - b * kNGL;
     sA[j * R + b] = a.m.A[i];
   }
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sIB[i] = a.m.ib[i];
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * kNewtonWarps;
   const int64_t ncol = a.ncols, nq = ncol * a.nplanes;
@@ -1723,7 +1727,7 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const Newto
       double F = F0, Fp = Fp0;
       if (it > 0) {
         double fw, fpw;
-        eval_channels(a, T, sA, scr, lane, &fw, &fpw);
+        eval_channels(a, T, sA, sIB, scr, lane, &fw, &fpw);
         evaluated_at = T;
         double f = 0.0, fp = 0.0;
         for (int b = lane; b < nb; b += 32) {
@@ -1772,7 +1776,7 @@ __global__ void __launch_bounds__(32 * kNewtonWarps, 4) k_newton_scu(const Newto
     if (Tf != Tn) {
       if (evaluated_at != Tf) {
         double fw, fpw;
-        eval_channels(a, Tf, sA, scr, lane, &fw, &fpw);
+        eval_channels(a, Tf, sA, sIB, scr, lane, &fw, &fpw);
       }
       if (lane == 0) a.T[c] = Tf;
       for (int b = lane; b < nb; b += 32) {
@@ -1792,7 +1796,7 @@ cudaError_t launch_newton_sc(const NewtonArgs &a, cudaStream_t s) {
     const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
     const int64_t nblk = std::min<int64_t>(need, 148 * 4);
     const size_t smem = ((size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * (newton_scratch(a.m, a.nb) + a.nb)) *
-                        sizeof(double);
+                            sizeof(double) + (size_t)a.nb * sizeof(int);
     if (cudaError_t e = smem_attr((const void *)k_newton_scu, smem)) return e;
     k_newton_scu<<<(unsigned)nblk, 32 * kNewtonWarps, smem, s>>>(a);
     return cudaGetLastError();
@@ -1809,7 +1813,7 @@ cudaError_t launch_newton(const NewtonArgs &a, cudaStream_t s) {
   const int64_t need = ((int64_t)a.ncols * a.nplanes + kNewtonWarps - 1) / kNewtonWarps;
   const int64_t nblk = std::min<int64_t>(need, 148 * 8);
   const size_t smem = (2 * (size_t)gl_stride(a.nb) * kNGL + (size_t)kNewtonWarps * newton_scratch(a.m, a.nb)) * sizeof(double) +
-                      4 * (size_t)(a.m.imax + 1) * sizeof(int);
+                      (4 * (size_t)(a.m.imax + 1) + (size_t)a.nb) * sizeof(int);
   const int minb = a.minb > 0 ? a.minb : BTE_NEWTON_MINB;
   if (a.Sall) {  // band partition (bte_create_band)
     if (cudaError_t e = smem_attr((const void *)k_newton<BTE_NEWTON_MINB, true>, smem)) return e;
@@ -2299,7 +2303,9 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
 
 // NBT/NJT > 0 fix the channel and direction counts at compile time (with JPT = 1).
-template <int JPT, int KF, int NBT, int NJT>
+// DB = 1: one neighbour-value buffer (cell i+1's gather is issued after cell i's
+// barrier; half the shared memory, so two CTAs fit an SM -- A/B variant).
+template <int JPT, int KF, int NBT, int NJT, int DB = 2>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -2417,7 +2423,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
           for (int f = 0; f < NIN; ++f) {
             const int64_t src = wi[SRC + f];
             if (src >= 0) {
-              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * NIN + f) * JPT + r)) * nt + tid);
+              const uint32_t dst = smem_u32(nbuf + ((size_t)((((DB == 2 ? i : 0) & 1) * NIN + f) * JPT + r)) * nt + tid);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                            "l"(Is + src + e0 + r * JG * nb)
                            : "memory");
@@ -2433,9 +2439,12 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
     const int st = i & Sm;
-    prefetch(i + 1);
+    if (DB == 2) prefetch(i + 1);
     double2 acc = make_double2(0.0, 0.0);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
+    if (DB == 2)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
@@ -2444,7 +2453,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
       const bool generic = slow[i & 3] != 0;  // CTA-uniform
-      const double2 *nb2 = nbuf + (size_t)((i & 1) * NIN * JPT) * nt + tid;
+      const double2 *nb2 = nbuf + (size_t)(((DB == 2 ? i : 0) & 1) * NIN * JPT) * nt + tid;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
@@ -2497,6 +2506,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     if (tid == 0) slow[(i + 3) & 3] = 0;
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
+    if (DB == 1) prefetch(i + 1);  // the single neighbour buffer is free now
     if (tid == tis && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
@@ -2543,13 +2553,15 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.jg = JG;
       a.chunk = a.chunk > 0 ? a.chunk : 64;
       // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
+      // (one buffer instead of two on triangles when a.single_buf: 2 CTAs per SM)
+      const int DBN = (a.single_buf && a.u.K == 3 && jpt == 2 && g.nb == 40 && g.nj == 50 && !a.generic) ? 1 : 2;
       const int K = a.u.K, KUW = K > 4 ? 2 + 2 * K : kUW, NIN = K > 4 ? 3 : K - 1, KP = K > 4 ? 8 : 4;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
                                   4 * (size_t)g.nj * KUW + 2) * sizeof(double) +
-                           2 * (size_t)NIN * jpt * threads * 16;
+                           (size_t)DBN * NIN * jpt * threads * 16;
       const size_t sd = (size_t)g.Es + 2 * g.nb + 4 * KP;
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)226 * 1024 - fixed) / (sd * 8));
-      S = std::max(4, std::min(8, S));
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)(DBN == 2 ? 226 : 113) * 1024 - fixed) / (sd * 8));
+      S = std::max(DBN == 2 ? 4 : 2, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;
       const size_t smem = fixed + (size_t)S * sd * 8;
@@ -2570,6 +2582,11 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
             if (a.u.K == 6) BTE_UTMA_(1, 6, 40, 50)
           }
           if (jpt == 2 && JG == 25 && threads == 500) {
+            if (a.u.K == 3 && DBN == 1) {
+              if (cudaError_t e = smem_attr((const void *)k_usweep_tma<2, 3, 40, 50, 1>, smem)) return e;
+              k_usweep_tma<2, 3, 40, 50, 1><<<grid, threads, smem, s>>>(a);
+              return cudaGetLastError();
+            }
             if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
             if (a.u.K == 4) BTE_UTMA_(2, 4, 40, 50)
           }

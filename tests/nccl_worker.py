@@ -22,6 +22,58 @@ def _case(kind):
     return bi.small_3d(6, 5, 9, bands=b, bcs=bcs)
 
 
+def rank_job(p, I, T, rank, world, kind, skip, nccl_id, device, stream=None, nsteps=5):
+    """One rank: its part of the problem through libbte's multi-rank path."""
+    from paper_2305_19400_b200 import Solver
+    from paper_2305_19400_b200.bte import DEBUG_SKIP_EXCHANGE
+    decomp = "band" if kind == "band" else "slab"
+    sv = Solver.from_problem(p, device=device, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id, decomp=decomp)
+    try:
+        if skip:
+            sv.set_debug(DEBUG_SKIP_EXCHANGE, 1)
+        if kind == "band":
+            sv.set_state(np.ascontiguousarray(I[:, :, sv.b0:sv.b1]), T)
+        else:
+            c0 = sv.cell0 if kind == "umesh" else sv.z0 * (sv.ncells // max(1, sv.nz_local))
+            sv.set_state(I[c0:c0 + sv.ncells], T[c0:c0 + sv.ncells])
+        E0 = sv.energy()
+        sv.step(nsteps)
+        E1 = sv.energy()
+        return {"rank": rank, "I": sv.intensity(), "T": sv.temperature(), "E0": E0, "E1": E1,
+                "b0": sv.b0, "b1": sv.b1}
+    finally:
+        sv.close()
+
+
+def verdict(p, o, I, T, allr, kind, nsteps=5) -> dict:
+    """The gathered parts against one context (bit-exact) and the oracle (north_star tolerance)."""
+    from paper_2305_19400_b200 import Solver
+    allr = sorted(allr, key=lambda d: d["rank"])
+    if kind == "band":
+        Ig = np.concatenate([d["I"] for d in allr], axis=2)
+        Tg = allr[0]["T"]
+        same_T = all(np.array_equal(d["T"], Tg) for d in allr)
+    else:
+        Ig = np.concatenate([d["I"] for d in allr])
+        Tg = np.concatenate([d["T"] for d in allr])
+        same_T = True
+    with Solver.from_problem(p, device=0) as s1:
+        s1.set_state(I, T)
+        s1.step(nsteps)
+        I1, T1 = s1.intensity(), s1.temperature()
+    Io, To, _, _ = o.run(I, T, nsteps)
+    if kind == "band":  # reading R-h: the parts' sums associate differently -> rounding-level agreement
+        same = bool(np.max(np.abs(Tg - T1)) <= 1e-10 and np.max(np.abs(Ig / I1 - 1)) <= 1e-12)
+    else:
+        same = bool(np.array_equal(Ig, I1) and np.array_equal(Tg, T1))
+    return {"bit_exact": same,
+            "rel_I_oracle": float(np.max(np.abs(Ig - Io) / np.abs(Io))),
+            "dT_oracle": float(np.max(np.abs(Tg - To))),
+            "T_same_on_parts": bool(same_T),
+            "energy_same_on_ranks": len({(d["E0"], d["E1"]) for d in allr}) == 1,
+            "energy_rel_vs_oracle": abs(allr[0]["E0"] / o.energy(I) - 1)}
+
+
 def run(rank, world, port, kind, skip, out):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ["MASTER_PORT"] = str(port)
@@ -29,60 +81,20 @@ def run(rank, world, port, kind, skip, out):
     import torch.distributed as dist
 
     import oracle
-    from paper_2305_19400_b200 import Solver, nccl_unique_id
-    from paper_2305_19400_b200.bte import DEBUG_SKIP_EXCHANGE
+    from paper_2305_19400_b200 import nccl_unique_id
 
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     p = _case(kind)
     o = oracle.Oracle(p)
     I, T = o.random_state()
-    nsteps = 5
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    decomp = "band" if kind == "band" else "slab"
     if kind == "overlap0":
         os.environ["BTE_OVERLAP"] = "0"
-    sv = Solver.from_problem(p, device=rank, rank=rank, nranks=world, nccl_id=obj[0], decomp=decomp)
-    if skip:
-        sv.set_debug(DEBUG_SKIP_EXCHANGE, 1)
-    if kind == "band":
-        sv.set_state(np.ascontiguousarray(I[:, :, sv.b0:sv.b1]), T)
-    else:
-        c0 = sv.cell0 if kind == "umesh" else sv.z0 * (sv.ncells // max(1, sv.nz_local))
-        sv.set_state(I[c0:c0 + sv.ncells], T[c0:c0 + sv.ncells])
-    E0 = sv.energy()
-    sv.step(nsteps)
-    E1 = sv.energy()
-    mine = {"rank": rank, "I": sv.intensity(), "T": sv.temperature(), "E0": E0, "E1": E1,
-            "b0": sv.b0, "b1": sv.b1}
-    sv.close()
+    mine = rank_job(p, I, T, rank, world, kind, skip, obj[0], rank)
     allr = [None] * world
     dist.all_gather_object(allr, mine)
     if rank == 0:
-        allr.sort(key=lambda d: d["rank"])
-        if kind == "band":
-            Ig = np.concatenate([d["I"] for d in allr], axis=2)
-            Tg = allr[0]["T"]
-            same_T = all(np.array_equal(d["T"], Tg) for d in allr)
-        else:
-            Ig = np.concatenate([d["I"] for d in allr])
-            Tg = np.concatenate([d["T"] for d in allr])
-            same_T = True
-        with Solver.from_problem(p, device=0) as s1:
-            s1.set_state(I, T)
-            s1.step(nsteps)
-            I1, T1 = s1.intensity(), s1.temperature()
-        Io, To, _, _ = o.run(I, T, nsteps)
-        if kind == "band":  # reading R-h: the parts' sums associate differently -> rounding-level agreement
-            same = bool(np.max(np.abs(Tg - T1)) <= 1e-10 and np.max(np.abs(Ig / I1 - 1)) <= 1e-12)
-        else:
-            same = bool(np.array_equal(Ig, I1) and np.array_equal(Tg, T1))
-        res = {"bit_exact": same,
-               "rel_I_oracle": float(np.max(np.abs(Ig - Io) / np.abs(Io))),
-               "dT_oracle": float(np.max(np.abs(Tg - To))),
-               "T_same_on_parts": bool(same_T),
-               "energy_same_on_ranks": len({(d["E0"], d["E1"]) for d in allr}) == 1,
-               "energy_rel_vs_oracle": abs(allr[0]["E0"] / o.energy(I) - 1)}
-        json.dump(res, open(out, "w"))
+        json.dump(verdict(p, o, I, T, allr, kind), open(out, "w"))
     dist.destroy_process_group()
