@@ -2303,9 +2303,7 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
 
 // NBT/NJT > 0 fix the channel and direction counts at compile time (with JPT = 1).
-// DB = 1: one neighbour-value buffer (cell i+1's gather is issued after cell i's
-// barrier; half the shared memory, so two CTAs fit an SM -- A/B variant).
-template <int JPT, int KF, int NBT, int NJT, int DB = 2>
+template <int JPT, int KF, int NBT, int NJT>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -2423,7 +2421,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
           for (int f = 0; f < NIN; ++f) {
             const int64_t src = wi[SRC + f];
             if (src >= 0) {
-              const uint32_t dst = smem_u32(nbuf + ((size_t)((((DB == 2 ? i : 0) & 1) * NIN + f) * JPT + r)) * nt + tid);
+              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * NIN + f) * JPT + r)) * nt + tid);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                            "l"(Is + src + e0 + r * JG * nb)
                            : "memory");
@@ -2439,12 +2437,9 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
     const int st = i & Sm;
-    if (DB == 2) prefetch(i + 1);
+    prefetch(i + 1);
     double2 acc = make_double2(0.0, 0.0);
-    if (DB == 2)
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
-    else
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
@@ -2453,7 +2448,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
       const bool generic = slow[i & 3] != 0;  // CTA-uniform
-      const double2 *nb2 = nbuf + (size_t)(((DB == 2 ? i : 0) & 1) * NIN * JPT) * nt + tid;
+      const double2 *nb2 = nbuf + (size_t)((i & 1) * NIN * JPT) * nt + tid;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
@@ -2506,7 +2501,6 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     if (tid == 0) slow[(i + 3) & 3] = 0;
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
-    if (DB == 1) prefetch(i + 1);  // the single neighbour buffer is free now
     if (tid == tis && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
@@ -2553,15 +2547,15 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.jg = JG;
       a.chunk = a.chunk > 0 ? a.chunk : 64;
       // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
-      // (one buffer instead of two on triangles when a.single_buf: 2 CTAs per SM)
-      const int DBN = (a.single_buf && a.u.K == 3 && jpt == 2 && g.nb == 40 && g.nj == 50 && !a.generic) ? 1 : 2;
       const int K = a.u.K, KUW = K > 4 ? 2 + 2 * K : kUW, NIN = K > 4 ? 3 : K - 1, KP = K > 4 ? 8 : 4;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
                                   4 * (size_t)g.nj * KUW + 2) * sizeof(double) +
-                           (size_t)DBN * NIN * jpt * threads * 16;
+                           2 * (size_t)NIN * jpt * threads * 16;
       const size_t sd = (size_t)g.Es + 2 * g.nb + 4 * KP;
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)(DBN == 2 ? 226 : 113) * 1024 - fixed) / (sd * 8));
-      S = std::max(DBN == 2 ? 4 : 2, std::min(8, S));
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)226 * 1024 - fixed) / (sd * 8));
+      // S >= 4: the face lists of cell i+2 are prepared (waiting on its stage)
+      // before the barrier after which cell i+S is issued
+      S = std::max(4, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;
       const size_t smem = fixed + (size_t)S * sd * 8;
@@ -2582,11 +2576,6 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
             if (a.u.K == 6) BTE_UTMA_(1, 6, 40, 50)
           }
           if (jpt == 2 && JG == 25 && threads == 500) {
-            if (a.u.K == 3 && DBN == 1) {
-              if (cudaError_t e = smem_attr((const void *)k_usweep_tma<2, 3, 40, 50, 1>, smem)) return e;
-              k_usweep_tma<2, 3, 40, 50, 1><<<grid, threads, smem, s>>>(a);
-              return cudaGetLastError();
-            }
             if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
             if (a.u.K == 4) BTE_UTMA_(2, 4, 40, 50)
           }
