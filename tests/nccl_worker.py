@@ -19,7 +19,15 @@ def _case(kind):
     b = bi.subset_bands(bi.silicon_bands(29), [0, 17, 33, 39])
     bcs = [bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(1), bi.WallBC(2),
            bi.WallBC(0, None, 302.0)]
-    return bi.small_3d(6, 5, 9, bands=b, bcs=bcs)
+    p = bi.small_3d(6, 5, 9, bands=b, bcs=bcs)
+    if kind == "semi":  # semi-implicit step (reading R-l) beyond the explicit dt bound
+        p.dt, p.semi = 20.0 * p.dt, 1
+    elif kind == "sctau":  # self-consistent tau (reading R-k)
+        p.tau_mode = 1
+    elif kind == "partial":  # partially specular walls (reading R-i)
+        p.bcs = [bi.WallBC(3, None, 300.0, 0.6), bi.WallBC(2), bi.WallBC(0, None, 305.0), bi.WallBC(3, None, 300.0, 0.25),
+                 bi.WallBC(1), bi.WallBC(0, None, 302.0)]
+    return p
 
 
 def rank_job(p, I, T, rank, world, kind, skip, nccl_id, device, stream=None, nsteps=5):

@@ -75,6 +75,16 @@ def test_loopback_ranks(kind, world):
     assert res["energy_rel_vs_oracle"] < 1e-12, res
 
 
+@pytest.mark.parametrize("kind", ["semi", "sctau", "partial"])
+def test_loopback_step_variants(kind):
+    """The NCCL-path slab exchange under the other integrators / wall kinds:
+    semi-implicit step (R-l), self-consistent tau (R-k), partially specular walls (R-i)."""
+    res = _run_threads(2, kind, skip=False)
+    assert res["bit_exact"], res
+    assert res["rel_I_oracle"] <= 1e-10 and res["dT_oracle"] <= 1e-8, res
+    assert res["energy_same_on_ranks"], res
+
+
 @pytest.mark.parametrize("kind", ["slab", "band", "umesh"])
 def test_loopback_skip_exchange_mutation(kind):
     """Mutation: without the exchange the parts must disagree with one context."""
