@@ -496,6 +496,7 @@ typedef struct {
   int64_t cell0;                                     /* canonical index of the first owned cell   */
   const char *sweep_kernel;                          /* the a1+a2 kernel bte_step launches (static) */
   int step_mode;                                     /* 0 explicit, 1 semi-implicit, 2 implicit     */
+  const char *newton_kernel;                         /* the a3+a4 kernel of an explicit step (static) */
 } bte_info;
 BTE_API bte_status bte_get_info(const bte_ctx *ctx, bte_info *out);
 

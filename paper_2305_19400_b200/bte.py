@@ -106,7 +106,8 @@ class Info(C.Structure):
                 ("nz_local", C.c_int64), ("nd", C.c_int), ("nb", C.c_int), ("n_octants", C.c_int),
                 ("nj", C.c_int), ("bytes_state", C.c_int64), ("b0", C.c_int), ("b1", C.c_int),
                 ("nb_total", C.c_int), ("band", C.c_int), ("rotate", C.c_int), ("cell0", C.c_int64),
-                ("sweep_kernel", C.c_char_p), ("step_mode", C.c_int)]
+                ("sweep_kernel", C.c_char_p), ("step_mode", C.c_int),
+                ("newton_kernel", C.c_char_p)]
 
 
 _lib = None
@@ -273,6 +274,7 @@ class Solver:
         self.rotate = bool(info.rotate)
         self.cell0 = int(info.cell0)
         self.sweep_kernel = (info.sweep_kernel or b"").decode()
+        self.newton_kernel = (info.newton_kernel or b"").decode()
         if self.nb_total == 0:  # older A/B build without the band fields
             self.b0, self.b1, self.nb_total = 0, self.nb, self.nb
 

@@ -2499,6 +2499,10 @@ bte_status bte_get_info(const bte_ctx *ctx, bte_info *out) {
   out->rotate = ctx->rot;
   out->cell0 = ctx->g.cell0;
   out->step_mode = ctx->implicit ? 2 : ctx->semi ? 1 : 0;
+  out->newton_kernel = ctx->band ? "k_newton (warp per cell, band partials)"
+                       : ctx->tau_mode == 1 ? (ctx->mF.uniform && !ctx->sc_direct ? "k_newton_scu (self-consistent tau)"
+                                                                                  : "k_newton_sc (self-consistent tau)")
+                                            : "k_newton (warp per cell)";
   if (ctx->umesh) {
     out->sweep_kernel = "k_usweep_tma (face-list upwind flux + relaxation on m-sided cells)";
   } else {
