@@ -1881,22 +1881,43 @@ cudaError_t launch_refresh(const Material &m, const double *T, int64_t nc, doubl
 }
 
 // I[slot][plane][cross][j][b] = I0c[cell][b] over owned planes
-__global__ void k_fill_eq(const Geometry g, const double *__restrict__ I0c, double *__restrict__ I) {
-  const int64_t n_per_slot = (int64_t)g.nplanes * g.ncross * g.E;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_per_slot * g.nslot) return;
-  const int sl = (int)(i / n_per_slot);
-  const int64_t r = i - sl * n_per_slot;
-  const int64_t cell = r / g.E;
-  const int e = (int)(r - cell * g.E);
-  const int b = e % g.nb;
-  I[g.slot_off[sl] + (int64_t)g.plane_off * g.plane_stride + cell * g.Es + e] = I0c[cell * g.nb + b];
+// I = I0c(cell) for every direction: one (slot, cell) block per block-iteration
+// (persistent grid), the cell's I0c row staged in shared memory, channel index
+// carried incrementally -- a streaming write of the whole state (the previous
+// one-thread-per-element version spent three 64-bit divisions per element and
+// ran at ~1.2 TB/s: 107 ms for config 4's 128 GB).
+__global__ void __launch_bounds__(256) k_fill_eq(const Geometry g, const double *__restrict__ I0c,
+                                                 double *__restrict__ I) {
+  __shared__ double row[kMaxBands];
+  const int64_t ncell = (int64_t)g.nplanes * g.ncross;
+  const int64_t items = ncell * g.nslot;
+  const int nb = g.nb, E = g.E;
+  const int b0 = (int)threadIdx.x % nb, db = (int)blockDim.x % nb;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int sl = (int)(it / ncell);
+    const int64_t cell = it - (int64_t)sl * ncell;
+    __syncthreads();  // previous item's row fully read
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) row[t] = I0c[cell * nb + t];
+    __syncthreads();
+    double *dst = I + g.slot_off[sl] + (int64_t)g.plane_off * g.plane_stride + cell * g.Es;
+    int b = b0;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      dst[e] = row[b];
+      b += db;
+      if (b >= nb) b -= nb;
+    }
+  }
 }
 
 cudaError_t launch_fill_equilibrium(const Geometry &g, const double *I0c, double *I, cudaStream_t s) {
-  const int64_t n = (int64_t)g.nplanes * g.ncross * g.E * g.nslot;
-  if (n == 0) return cudaSuccess;
-  k_fill_eq<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, I0c, I);
+  const int64_t items = (int64_t)g.nplanes * g.ncross * g.nslot;
+  if (items == 0 || g.E == 0) return cudaSuccess;
+  if (g.nb > kMaxBands) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nblk = std::min<int64_t>(items, (int64_t)sms * 8);
+  k_fill_eq<<<(unsigned)nblk, 256, 0, s>>>(g, I0c, I);
   return cudaGetLastError();
 }
 

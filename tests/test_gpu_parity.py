@@ -1232,3 +1232,34 @@ def test_slab_group_one_plane_slabs(Solver):
         for sv in group:
             sv.close()
     _assert_oracle(p, I, T, 4, Ig, Tg)
+
+
+@pytest.mark.parametrize("case", ["config3_tables", "rotated", "inplane55"])
+def test_set_state_temperature_only(Solver, monkeypatch, case):
+    """bte_set_state(NULL, T) -- the e2e job's input path: I = I0(T) built on the
+    device (k_fill_eq) must equal the oracle's equilibrium of that T field, and
+    the steps that follow must match the oracle from (I0(T), T).  Covers the
+    40-channel 3-D tables, the octant-slot rotated layout and an in-plane set
+    with 55 channels (E not a multiple of the 256-thread block)."""
+    if case == "rotated":
+        monkeypatch.setenv("BTE_ROTATE", "1")
+    if case == "inplane55":
+        p = bi.small_3d(6, 5, 3, dirs=bi.directions_inplane(20), bands=bi.silicon_bands(40),
+                        bcs=[bi.WallBC(1), bi.WallBC(2), bi.WallBC(0, None, 303.0), bi.WallBC(1),
+                             bi.WallBC(1), bi.WallBC(1)])
+    else:
+        p = bi.config3(n=8)
+        p.mesh = bi.Mesh(3, 7, 6, 5, 1e-6, 1e-6, 1e-6)
+    o = oracle.Oracle(p)
+    _, T = o.random_state()
+    I = o.equilibrium(T)
+    with Solver.from_problem(p) as sv:
+        sv.set_state(None, T)
+        Ig0 = sv.intensity()
+        assert np.array_equal(sv.temperature(), T)
+        assert np.max(np.abs(Ig0 - I) / np.abs(I)) <= REL_I
+        sv.step(3)
+        Ig, Tg = sv.intensity(), sv.temperature()
+    Io, To, _, _ = o.run(I, T, 3)
+    rel, dT = _cmp(Ig, Tg, Io, To)
+    assert rel <= REL_I and dT <= ABS_T, (rel, dT)
