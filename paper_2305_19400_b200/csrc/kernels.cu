@@ -889,6 +889,36 @@ __global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const i
       const double I0 = rows_tma ? sp[o_i0 + b] : ldg(A.I0c + cell * nb + b);
       const double dtb = dt * (rows_tma ? sp[o_be + b] : ldg(A.beta + cell * nb + b));
       const int64_t mg = g.m0 + p;
+      if (!xghost && (DIM == 2 || !yghost) && nloc == JMAX) {
+        // interior column: no ghost branches; the flux terms without the
+        // s_a == 0 tests (a zero coefficient adds exactly 0 to num and den)
+#pragma unroll
+        for (int k = 0; k < JMAX; ++k) {
+          const int e = e0 + k * nb;
+          const double Inn = sp[e];
+          const double *cf = cq + 4 * k;
+          const double kx = v * cf[0], km = v * cf[DIM - 1];
+          double num = dtb * (I0 - Inn), den = 1.0 + dtb;
+          num = fma(kx, sp[o_x + e] - Inn, num);
+          den += kx;
+          if (DIM == 3) {
+            const double ky = v * cf[1];
+            num = fma(ky, sp[o_y + e] - Inn, num);
+            den += ky;
+          }
+          num = fma(km, prev[k] - Inn, num);
+          den += km;
+          // 1/den (den >= 1): MUFU seed + two Newton-Raphson steps (~1 ulp)
+          double r;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+          r = fma(r, fma(-den, r, 1.0), r);
+          r = fma(r, fma(-den, r, 1.0), r);
+          const double Inew = fma(num, r, Inn);
+          __stcg(Os + base + e, Inew);
+          acc = fma(cf[3], I0 - Inew, acc);
+          prev[k] = Inew;
+        }
+      } else {
 #pragma unroll
       for (int k = 0; k < JMAX; ++k) {
         if (k < nloc) {
@@ -936,6 +966,7 @@ __global__ void __launch_bounds__(MT, MB) k_sweep_imp(const SweepArgs A, const i
           acc = fma(cf[3], I0 - Inew, acc);
           prev[k] = Inew;
         }
+      }
       }
     }
     double *rb = red + (i & 1) * JG * nb;
