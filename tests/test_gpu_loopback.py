@@ -90,3 +90,55 @@ def test_loopback_skip_exchange_mutation(kind):
     """Mutation: without the exchange the parts must disagree with one context."""
     res = _run_threads(2, kind, skip=True)
     assert not res["bit_exact"], res
+
+
+@pytest.mark.parametrize("kind", ["slab", "overlap0", "band", "umesh"])
+def test_loopback_per_rank_timers(kind):
+    """The per-rank phase timers bench.py reports at N > 1 (sweep, Newton,
+    boundary, halo), observed on the multi-rank path: every rank records its
+    halo / AllGather spans (> 0 ms) next to its sweep and Newton, one sweep
+    launch set and one Newton per step, nothing truncated."""
+    import torch
+
+    from nccl_worker import _case
+    from paper_2305_19400_b200 import Solver, loopback_unique_id
+
+    p = _case(kind)
+    uid = loopback_unique_id()
+    world, nsteps = 2, 6
+    res, errs = [None] * world, []
+
+    def job(r):
+        try:
+            torch.cuda.set_device(0)
+            decomp = "band" if kind == "band" else "slab"
+            with Solver.from_problem(p, device=0, stream=torch.cuda.Stream(device=0), rank=r, nranks=world,
+                                     nccl_id=uid, decomp=decomp) as sv:
+                sv.step(2)
+                sv.timing_enable(True, 64)
+                sv.step(nsteps)
+                res[r] = sv.timing_read()
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"rank {r}: {e!r}")
+
+    old = os.environ.get("BTE_OVERLAP")
+    if kind == "overlap0":
+        os.environ["BTE_OVERLAP"] = "0"
+    try:
+        th = [threading.Thread(target=job, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+    finally:
+        if kind == "overlap0":
+            if old is None:
+                os.environ.pop("BTE_OVERLAP", None)
+            else:
+                os.environ["BTE_OVERLAP"] = old
+    assert not errs, errs
+    for t in res:
+        assert t is not None and t["steps"] == nsteps, t
+        assert t["truncated"] == 0, t
+        assert t["halo_ms"] > 0.0 and t["sweep_ms"] > 0.0 and t["newton_ms"] > 0.0, t
+        assert t["newton_launches"] >= nsteps and t["sweep_launches"] >= nsteps, t  # band: partial + Newton
