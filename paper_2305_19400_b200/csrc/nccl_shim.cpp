@@ -333,7 +333,13 @@ int nccl_shim_group_end(std::string *err) {
     std::vector<loopback::Pending> pend;
     pend.swap(loopback::t_pending);
     std::vector<loopback::Op> ops;
-    for (auto &p : pend) ops.push_back(p.op);
+    for (auto &p : pend) {
+      if (p.c != pend[0].c) {  // one communicator per group (the library's usage)
+        if (err) *err = "loopback: a group mixes communicators";
+        return 1;
+      }
+      ops.push_back(p.op);
+    }
     if (loopback::run_group(pend[0].c, std::move(ops), err)) rc = 1;
   }
   return rc;
