@@ -1260,7 +1260,10 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
     // y-upwind L2 misses to 18.4-20.2 B/DOF; profiles/round2_ab_seg.jsonl)
     int nseg = g.dim == 3 ? std::max(1, (int)((g.nplanes + 16) / 32)) : std::max(1, (int)((g.nplanes + 8) / 16));
     const int64_t tasks = (int64_t)g.ncross * g.nslot;
-    const int64_t want = 8 * 148;
+    // (>= 12 CTAs per SM: Fig. 9's 160 column tasks x 8 segments = 1.2 waves
+    // of the small-block sweep -> 12 segments, 0.0405 -> 0.0371 ms; knob table
+    // profiles/round2_ab_knobs.jsonl)
+    const int64_t want = 12 * 148;
     if (tasks * nseg < want) nseg = (int)std::min<int64_t>(g.nplanes, (want + tasks - 1) / tasks);
     if (ctx->seg_override > 0) nseg = std::min(ctx->seg_override, g.nplanes);
     ctx->seg_len = (g.nplanes + nseg - 1) / nseg;
