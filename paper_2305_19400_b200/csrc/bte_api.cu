@@ -96,6 +96,7 @@ struct bte_ctx {
   int newton_minb = 0;     // env BTE_NEWTON_MINB (k_newton occupancy variant)
   unsigned long long *d_stats = nullptr;  // env BTE_NEWTON_STATS=1: Newton counters printed by bte_step
   int no_spare = 0;        // env BTE_SPARE=0: side jobs on compute threads (A/B)
+  int newton_lpc = -1;      // env BTE_NEWTON_LPC=0/1 forces the band-integral lane mapping (-1: by channel count)
   int pf = 1;              // env BTE_PF: k_sweep L2 prefetch distance in cells (demo sweep 0.093 -> 0.086 ms)
   int raster = 0;          // 3-D sweep column order (SweepArgs.raster); env BTE_RASTER
   int sc_direct = 0;       // env BTE_SC_DIRECT=1: direct band integrals in the self-consistent Newton (A/B)
@@ -1270,6 +1271,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   }
   if (const char *e = getenv("BTE_SPARE")) ctx->no_spare = atoi(e) == 0;
   if (const char *e = getenv("BTE_PF")) ctx->pf = atoi(e);
+  if (const char *e = getenv("BTE_NEWTON_LPC")) ctx->newton_lpc = atoi(e);
   // 3-D sweep column order: strips of 16 columns along x (measured on B200,
   // config 4: DRAM 20.3 -> 17.6 B/DOF per sweep launch)
   ctx->raster = g.dim == 3 ? 16 : 0;
@@ -1551,6 +1553,14 @@ static NewtonArgs newton_args(bte_ctx *ctx, int64_t step) {
   a.predict = ctx->newton_predict;
   a.minb = ctx->newton_minb;
   a.stats = ctx->d_stats;
+  // band integrals lane per channel when its 16*ceil(nb/32) node terms per lane
+  // are within 1.2x of the (node group, channel) mapping's 4*ceil(nb/8) -- it
+  // saves the cross-lane sums (measured: 55 channels -7 % Newton, 40 channels +3.5 %)
+  {
+    const int nb = ctx->nbT;
+    const bool lpc_auto = 16 * ((nb + 31) / 32) * 5 <= 6 * 4 * ((nb + 7) / 8);
+    a.lpc = ctx->newton_lpc >= 0 ? ctx->newton_lpc : (lpc_auto ? 1 : 0);
+  }
   return a;
 }
 

@@ -109,6 +109,7 @@ struct NewtonArgs {
   int beta_fixed;         // implicit step (R-n): weights from the stored beta_next, not beta(T)
   unsigned long long *dTmax;  // implicit step: max_c |T^{k+1} - T^k| / T^k (double bits), or null
   const unsigned long long *step_ctr;  // graph replay: device step index for the error key (else `step`)
+  int lpc;                // eval_channels: lane per channel (A/B)
 };
 
 struct SweepArgs {

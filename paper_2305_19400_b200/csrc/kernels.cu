@@ -1314,8 +1314,39 @@ __device__ __forceinline__ void eval_channels(const NewtonArgs &a, double T, con
   for (int i = lane; i <= a.m.imax; i += 32) sR[i] = exp(aa * (double)i);
   __syncwarp();
   double facc = 0.0, fpacc = 0.0;
-  const int q = lane >> 3;            // node group: nodes 4q .. 4q+3
   const int R = gl_stride(nb);
+  if (a.lpc) {
+    // lane per channel: all 16 nodes of channel b in one lane, no cross-lane
+    // sums; ceil(nb/32) rounds instead of ceil(nb/8) (chosen by channel count)
+    for (int b = lane; b < nb; b += 32) {
+      const int ib = sIB[b];
+      const double Rb = sR[ib];
+      const double bi = (double)ib;
+      double f = 0.0, fp = 0.0, f2 = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < kNGL; ++j) {
+        const double em1 = (ib == 0) ? sM[j] : fma(sE[j], Rb, -1.0);
+        const double rr = rcp_nr(em1);
+        const double t = sA[j * R + b] * rr;
+        const double x = aa * (bi + __ldg(a.m.U + j));
+        const double tq = t * (1.0 + rr);
+        f += t;
+        fp = fma(tq, x, fp);
+        f2 = fma(tq * x, fma(x, fma(2.0, rr, 1.0), -2.0), f2);
+      }
+      const double d = fp * rT;
+      sI0[b] = f;
+      sD0[b] = d;
+      sD2[b] = f2 * rT * rT;
+      facc += cs[b] * f;
+      fpacc += cs[b] * d;
+    }
+    *F = a.W * warp_sum(facc);
+    *Fp = a.W * warp_sum(fpacc);
+    __syncwarp();
+    return;
+  }
+  const int q = lane >> 3;            // node group: nodes 4q .. 4q+3
   double u[4];
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) u[jj] = a.m.U[4 * q + jj];
