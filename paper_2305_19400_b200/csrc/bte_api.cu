@@ -101,6 +101,7 @@ struct bte_ctx {
   int raster = 0;          // 3-D sweep column order (SweepArgs.raster); env BTE_RASTER
   int sc_direct = 0;       // env BTE_SC_DIRECT=1: direct band integrals in the self-consistent Newton (A/B)
   int ugeneric = 0;        // env BTE_UGENERIC=1: generic unstructured sweep (A/B)
+  int usingle = 1;         // env BTE_USINGLE=0: two neighbour buffers, 1 CTA/SM on triangles too (A/B)
   int dbg_skip_exchange = 0;  // bte_set_debug(BTE_DEBUG_SKIP_EXCHANGE): mutation tests only
   double *d_energy = nullptr; // bte_get_energy scratch
   // CUDA-graph replay of explicit steps (SURVEY 8(b) "graph replay"): one
@@ -1279,6 +1280,7 @@ static bte_status create_impl(const bte_mesh *mesh, const bte_dirs *dirs, const 
   if (const char *e = getenv("BTE_GRAPH")) ctx->use_graph = atoi(e) != 0;
   if (const char *e = getenv("BTE_SC_DIRECT")) ctx->sc_direct = atoi(e) != 0;
   if (const char *e = getenv("BTE_UGENERIC")) ctx->ugeneric = atoi(e) != 0;
+  if (const char *e = getenv("BTE_USINGLE")) ctx->usingle = atoi(e) != 0;
   if (const char *e = getenv("BTE_NEWTON_PREDICT")) ctx->newton_predict = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_MINB")) ctx->newton_minb = atoi(e);
   if (const char *e = getenv("BTE_NEWTON_STATS"))
@@ -1611,6 +1613,7 @@ static bte_status launch_sweep_step(bte_ctx *ctx, const double *Iin, double *Iou
     a.stages = ctx->stages_override;
     a.chunk = ctx->seg_override;
     a.generic = ctx->ugeneric;
+    a.single_buf = ctx->usingle;
     CU(launch_usweep(a, ctx->stream));
     ctx->tacc.launches++;
     ctx->tacc.sweep_launches++;

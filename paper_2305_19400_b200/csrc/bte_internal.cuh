@@ -167,6 +167,7 @@ struct USweepArgs {
   int pipelined;          // k_usweep_tma (default) vs the one-CTA-per-cell k_usweep
   int stages, chunk;      // pipeline depth and cells per CTA (0 = automatic)
   int generic;            // 1: skip the 40-channel x 50-direction specialisation (A/B)
+  int single_buf;         // 1: one neighbour buffer, 2-deep ring, 2 CTAs/SM on triangles (A/B)
 };
 
 // kernels / launchers (kernels.cu)

@@ -2386,7 +2386,13 @@ __global__ void __launch_bounds__(1024) k_usweep(const USweepArgs A) {
 constexpr int kUW = 10;  // face-list words per direction: aout, nin, ain[4], src[4]
 
 // NBT/NJT > 0 fix the channel and direction counts at compile time (with JPT = 1).
-template <int JPT, int KF, int NBT, int NJT>
+// DB = 1 (default on triangles): one neighbour-value buffer (cell i+1's
+// gather is issued after cell i's barrier) and the face lists prepared from
+// the global geometry rows instead of the stage, so a 2-deep ring suffices and
+// two CTAs (~105 KB each) fit an SM -- each hides the other's per-cell barrier
+// (u2: 2.53 -> 2.11 ms, 0.45 -> 0.53 of HBM).  Tetrahedra / quadrilaterals
+// (three inflow slots) do not fit twice and keep DB = 2.
+template <int JPT, int KF, int NBT, int NJT, int DB = 2>
 __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const Geometry &g = A.g;
@@ -2444,9 +2450,9 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   auto prep = [&](int i) {
     if (i >= n || pj < 0) return;
     const int st = i & Sm;
-    mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     const double *sp = stg + (size_t)st * sd;
-    const int64_t *rn = reinterpret_cast<const int64_t *>(sp + o_nb);
+    if (DB == 2) mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
+    const int64_t *rn = DB == 2 ? reinterpret_cast<const int64_t *>(sp + o_nb) : u.nbr + (c0 + i) * KP;
     const double *sv = sws + 4 * pj;
     double *w = fl + ((size_t)(i & 3) * nj + pj) * KUW;
     int64_t *wi = reinterpret_cast<int64_t *>(w);
@@ -2455,7 +2461,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     bool generic = false;
 #pragma unroll
     for (int f = 0; f < KF; ++f) {
-      const double *an = sp + o_an + 3 * f;
+      const double *an = DB == 2 ? sp + o_an + 3 * f : u.an + (c0 + i) * 3 * KP + 3 * f;
       const double a = A.dt * fma(sv[2], an[2], fma(sv[1], an[1], sv[0] * an[0]));
       if (rn[f] < 0) generic = true;
       if (a > 0.0) {
@@ -2477,7 +2483,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   };
 
   for (int t = tid; t < 4 * nj; t += nt) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
-  for (int t = tid; t < 2 * NIN * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
+  for (int t = tid; t < DB * NIN * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
   if (tid < 4) slow[tid] = 0;
   if (tid == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
@@ -2504,7 +2510,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
           for (int f = 0; f < NIN; ++f) {
             const int64_t src = wi[SRC + f];
             if (src >= 0) {
-              const uint32_t dst = smem_u32(nbuf + ((size_t)(((i & 1) * NIN + f) * JPT + r)) * nt + tid);
+              const uint32_t dst = smem_u32(nbuf + ((size_t)((((DB == 2 ? i : 0) & 1) * NIN + f) * JPT + r)) * nt + tid);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                            "l"(Is + src + e0 + r * JG * nb)
                            : "memory");
@@ -2520,9 +2526,12 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   for (int i = 0; i < n; ++i) {
     const int64_t cell = c0 + i;
     const int st = i & Sm;
-    prefetch(i + 1);
+    if (DB == 2) prefetch(i + 1);
     double2 acc = make_double2(0.0, 0.0);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
+    if (DB == 2)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // cell i's values (cell i+1's may pend)
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     if (active) {
       const double *sp = stg + (size_t)st * sd;
@@ -2531,7 +2540,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       const double dtb0 = A.dt * be.x, dtb1 = A.dt * be.y;
       const int64_t base = cell * Es;
       const bool generic = slow[i & 3] != 0;  // CTA-uniform
-      const double2 *nb2 = nbuf + (size_t)((i & 1) * NIN * JPT) * nt + tid;
+      const double2 *nb2 = nbuf + (size_t)(((DB == 2 ? i : 0) & 1) * NIN * JPT) * nt + tid;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
@@ -2584,6 +2593,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     if (tid == 0) slow[(i + 3) & 3] = 0;
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
+    if (DB == 1) prefetch(i + 1);  // the single neighbour buffer is free now
     if (tid == tis && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
@@ -2631,14 +2641,16 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       a.chunk = a.chunk > 0 ? a.chunk : 64;
       // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
       const int K = a.u.K, KUW = K > 4 ? 2 + 2 * K : kUW, NIN = K > 4 ? 3 : K - 1, KP = K > 4 ? 8 : 4;
+      // triangles: one neighbour buffer, face lists from global, 2-deep ring, 2 CTAs/SM
+      const int DBN = (a.single_buf && K == 3 && jpt == 2 && g.nb == 40 && g.nj == 50 && !a.generic) ? 1 : 2;
       const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
                                   4 * (size_t)g.nj * KUW + 2) * sizeof(double) +
-                           2 * (size_t)NIN * jpt * threads * 16;
+                           (size_t)DBN * NIN * jpt * threads * 16;
       const size_t sd = (size_t)g.Es + 2 * g.nb + 4 * KP;
-      int S = a.stages > 0 ? a.stages : (int)(((size_t)226 * 1024 - fixed) / (sd * 8));
+      int S = a.stages > 0 ? a.stages : (int)(((size_t)(DBN == 2 ? 226 : 113) * 1024 - fixed) / (sd * 8));
       // S >= 4: the face lists of cell i+2 are prepared (waiting on its stage)
-      // before the barrier after which cell i+S is issued
-      S = std::max(4, std::min(8, S));
+      // before the barrier after which cell i+S is issued (DB = 1 reads them from global)
+      S = std::max(DBN == 2 ? 4 : 2, std::min(8, S));
       while (S & (S - 1)) --S;  // power of two (stage index and phase by mask/shift)
       a.stages = S;
       const size_t smem = fixed + (size_t)S * sd * 8;
@@ -2659,6 +2671,11 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
             if (a.u.K == 6) BTE_UTMA_(1, 6, 40, 50)
           }
           if (jpt == 2 && JG == 25 && threads == 500) {
+            if (a.u.K == 3 && DBN == 1) {
+              if (cudaError_t e = smem_attr((const void *)k_usweep_tma<2, 3, 40, 50, 1>, smem)) return e;
+              k_usweep_tma<2, 3, 40, 50, 1><<<grid, threads, smem, s>>>(a);
+              return cudaGetLastError();
+            }
             if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
             if (a.u.K == 4) BTE_UTMA_(2, 4, 40, 50)
           }

@@ -3,7 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 TAG=${TAG:-usingle}
-BTE_USINGLE=1 timeout 600 python -m pytest tests/test_gpu_umesh.py -m gpu -x -q 2>&1 | tail -1
+BTE_USINGLE=1 timeout 600 python -m pytest tests/test_gpu_umesh.py -m gpu -x -q -rf 2>&1 | tail -3
 : > gpurun_out/ab_${TAG}.jsonl
 for R in 1 2; do
 for V in 0 1; do
