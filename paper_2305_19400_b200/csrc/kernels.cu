@@ -2416,16 +2416,18 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   const bool active = jg < JG;
   // stage layout (doubles): own[Es] | I0[nb] | beta[nb] | an[12] | nbr[4] (int64)
   const int o_i0 = Es, o_be = Es + nb, o_an = Es + 2 * nb, o_nb = o_an + 3 * KP;
-  const int sd = o_nb + KP;
+  const int sd = DB == 2 ? o_nb + KP : o_an;  // DB = 1: the face rows are read from global
   uint64_t *full = reinterpret_cast<uint64_t *>(smraw);        // [S]
   int *slow = reinterpret_cast<int *>(smraw + 64);            // [4] cell needs the generic path
   double *stg = reinterpret_cast<double *>(smraw + 128);      // [S][sd]
   double *red = stg + (size_t)S * sd;                         // [2][JG][nb]
   double *red2 = red + 2 * JG * nb;                           // [2][8][nb]
-  double *sws = red2 + 2 * 8 * nb;                            // [nj][4]
-  double *fl = sws + 4 * nj;                                  // [4][nj][KUW]
+  // [nj][4] s_x, s_y, s_z, w per direction (DB = 1: straight from global, L1)
+  const double *sws = DB == 2 ? red2 + 2 * 8 * nb : u.sw + (int64_t)blockIdx.y * nj * 4;
+  double *fl = red2 + 2 * 8 * nb + (DB == 2 ? 4 * nj : 0);  // [FLR][nj][KUW]
+  constexpr int FLR = DB == 2 ? 4 : 3;  // face-list ring: cells i (compute), i+1 (gather), i+2 (prep)
   // inflow neighbour values: [2 cells][KF-1 slots][JPT][nt] (16 B each)
-  double2 *nbuf = reinterpret_cast<double2 *>(fl + ((4 * nj * KUW + 1) & ~1));
+  double2 *nbuf = reinterpret_cast<double2 *>(fl + ((FLR * nj * KUW + 1) & ~1));
   const int slot = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.x * Q;
   const int n = (int)min((int64_t)Q, u.ncells - c0);
@@ -2436,12 +2438,14 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     const int st = i & Sm;
     const int64_t cell = c0 + i;
     double *sp = stg + (size_t)st * sd;
-    mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + 4 * KP) * 8u);
+    mbar_expect_tx(&full[st], (uint32_t)(E + 2 * nb + (DB == 2 ? 4 * KP : 0)) * 8u);
     bulk_g2s(sp, Is + cell * Es, (uint32_t)E * 8u, &full[st]);
     bulk_g2s(sp + o_i0, A.I0c + cell * nb, (uint32_t)nb * 8u, &full[st]);
     bulk_g2s(sp + o_be, A.beta + cell * nb, (uint32_t)nb * 8u, &full[st]);
-    bulk_g2s(sp + o_an, u.an + cell * 3 * KP, 24u * KP, &full[st]);
-    bulk_g2s(sp + o_nb, u.nbr + cell * KP, 8u * KP, &full[st]);
+    if (DB == 2) {
+      bulk_g2s(sp + o_an, u.an + cell * 3 * KP, 24u * KP, &full[st]);
+      bulk_g2s(sp + o_nb, u.nbr + cell * KP, 8u * KP, &full[st]);
+    }
   };
   // face lists of cell i (the last nj threads: the reducers and the issuing
   // thread sit in other warps, so no warp carries two extra jobs), from its stage
@@ -2454,7 +2458,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     if (DB == 2) mbar_wait(&full[st], (uint32_t)((i >> Sl) & 1));
     const int64_t *rn = DB == 2 ? reinterpret_cast<const int64_t *>(sp + o_nb) : u.nbr + (c0 + i) * KP;
     const double *sv = sws + 4 * pj;
-    double *w = fl + ((size_t)(i & 3) * nj + pj) * KUW;
+    double *w = fl + ((size_t)(i % FLR) * nj + pj) * KUW;
     int64_t *wi = reinterpret_cast<int64_t *>(w);
     double aout = 0.0;
     int nin = 0;
@@ -2482,7 +2486,8 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     if (generic) slow[i & 3] = 1;  // every writer stores the same value
   };
 
-  for (int t = tid; t < 4 * nj; t += nt) sws[t] = u.sw[(int64_t)slot * nj * 4 + t];
+  if (DB == 2)
+    for (int t = tid; t < 4 * nj; t += nt) const_cast<double *>(sws)[t] = u.sw[(int64_t)slot * nj * 4 + t];
   for (int t = tid; t < DB * NIN * JPT * nt; t += nt) nbuf[t] = make_double2(0.0, 0.0);
   if (tid < 4) slow[tid] = 0;
   if (tid == 0) {
@@ -2501,7 +2506,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
   // stage the inflow values of cell i (slot f of direction r at nbuf[((i&1)(KF-1) + f) JPT + r][tid])
   auto prefetch = [&](int i) {
     if (active && i < n) {
-      const double *w = fl + ((size_t)(i & 3) * nj + jg) * KUW;
+      const double *w = fl + ((size_t)(i % FLR) * nj + jg) * KUW;
 #pragma unroll
       for (int r = 0; r < JPT; ++r) {
         if (jg + r * JG < nj) {
@@ -2545,7 +2550,7 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
       for (int r = 0; r < JPT; ++r) {
         const int j = jg + r * JG;
         if (j < nj) {
-          const double *w = fl + ((size_t)(i & 3) * nj + j) * KUW;
+          const double *w = fl + ((size_t)(i % FLR) * nj + j) * KUW;
           const int e = e0 + r * JG * nb;
           const double2 Ic = *reinterpret_cast<const double2 *>(sp + e);
           double f0 = w[0] * Ic.x, f1 = w[0] * Ic.y;
@@ -2630,7 +2635,9 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
     const int NBP = g.nb / 2;
     // 2 directions x 2 channels per thread on triangles (measured 3 % faster on u2),
     // 1 x 2 on tetrahedra (their 4-face lists fill the registers)
-    const int tgt = a.target_threads > 0 ? a.target_threads : (a.u.K == 3 ? 500 : 1024);
+    // (tetrahedra / quadrilaterals also at 500 threads when the single-buffer two-CTA shape applies)
+    const int tgt = a.target_threads > 0 ? a.target_threads
+                                         : (a.u.K == 3 || (a.u.K == 4 && a.single_buf && g.nb == 40 && g.nj == 50 && !a.generic) ? 500 : 1024);
     int JG = std::max(1, std::min(g.nj, tgt / NBP));
     const int jpt = (g.nj + JG - 1) / JG;
     JG = (g.nj + jpt - 1) / jpt;
@@ -2642,11 +2649,11 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
       // red, red2, sws, face lists (+ alignment), then the cp.async neighbour buffers
       const int K = a.u.K, KUW = K > 4 ? 2 + 2 * K : kUW, NIN = K > 4 ? 3 : K - 1, KP = K > 4 ? 8 : 4;
       // triangles: one neighbour buffer, face lists from global, 2-deep ring, 2 CTAs/SM
-      const int DBN = (a.single_buf && K == 3 && jpt == 2 && g.nb == 40 && g.nj == 50 && !a.generic) ? 1 : 2;
-      const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + 4 * (size_t)g.nj +
-                                  4 * (size_t)g.nj * KUW + 2) * sizeof(double) +
+      const int DBN = (a.single_buf && (K == 3 || K == 4) && jpt == 2 && g.nb == 40 && g.nj == 50 && !a.generic) ? 1 : 2;
+      const size_t fixed = 128 + (2 * (size_t)JG * g.nb + 16 * (size_t)g.nb + (DBN == 2 ? 4 * (size_t)g.nj : 0) +
+                                  (DBN == 2 ? 4 : 3) * (size_t)g.nj * KUW + 2) * sizeof(double) +
                            (size_t)DBN * NIN * jpt * threads * 16;
-      const size_t sd = (size_t)g.Es + 2 * g.nb + 4 * KP;
+      const size_t sd = (size_t)g.Es + 2 * g.nb + (DBN == 2 ? 4 * KP : 0);
       int S = a.stages > 0 ? a.stages : (int)(((size_t)(DBN == 2 ? 226 : 113) * 1024 - fixed) / (sd * 8));
       // S >= 4: the face lists of cell i+2 are prepared (waiting on its stage)
       // before the barrier after which cell i+S is issued (DB = 1 reads them from global)
@@ -2677,6 +2684,11 @@ cudaError_t launch_usweep(const USweepArgs &a0, cudaStream_t s) {
               return cudaGetLastError();
             }
             if (a.u.K == 3) BTE_UTMA_(2, 3, 40, 50)
+            if (a.u.K == 4 && DBN == 1) {
+              if (cudaError_t e = smem_attr((const void *)k_usweep_tma<2, 4, 40, 50, 1>, smem)) return e;
+              k_usweep_tma<2, 4, 40, 50, 1><<<grid, threads, smem, s>>>(a);
+              return cudaGetLastError();
+            }
             if (a.u.K == 4) BTE_UTMA_(2, 4, 40, 50)
           }
         }
