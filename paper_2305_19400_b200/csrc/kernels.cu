@@ -2595,10 +2595,13 @@ __global__ void __launch_bounds__(1024, 1) k_usweep_tma(const USweepArgs A) {
     }
     // flag of ring entry (i+3)&3: last read at iteration i-1, next written by
     // prep(i+3) in iteration i+1 (after this iteration's barrier)
+    // DB = 1: each thread's neighbour-buffer slots are its own (written and read
+    // only by it), so cell i+1's gather goes out as soon as this thread's
+    // compute of cell i has consumed them -- before the barrier
+    if (DB == 1) prefetch(i + 1);
     if (tid == 0) slow[(i + 3) & 3] = 0;
     prep(i + 2);
     __syncthreads();  // stage st consumed, red[i&1] complete, face lists of i+2 written
-    if (DB == 1) prefetch(i + 1);  // the single neighbour buffer is free now
     if (tid == tis && i + S < n) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(i + S);
