@@ -30,7 +30,14 @@ struct Nccl {
 
 Nccl &lib(std::string *err) {
   static Nccl n;
+  static bool failed = false;  // a missing libnccl is looked up once (loopback-only runs)
+  static std::mutex mu;        // loopback ranks are threads: one resolver at a time
+  std::lock_guard<std::mutex> lk(mu);
   if (n.h) return n;
+  if (failed) {
+    if (err) *err = "cannot dlopen libnccl.so.2 (import torch first or set BTE_NCCL_LIB)";
+    return n;
+  }
   const char *cands[] = {getenv("BTE_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
   for (const char *c : cands) {
     if (!c) continue;
@@ -38,6 +45,7 @@ Nccl &lib(std::string *err) {
     if (n.h) break;
   }
   if (!n.h) {
+    failed = true;
     if (err) *err = "cannot dlopen libnccl.so.2 (import torch first or set BTE_NCCL_LIB)";
     return n;
   }
