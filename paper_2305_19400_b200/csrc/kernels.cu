@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(JMAX == 1 ? 448 : 1024, JMAX == 1 ? 4 : 1) k_s
     double *dp = A.Dpart + (c0 * g.nslot + slot) * nb + (tid < nb ? tid : 0);
     const double *cq = coef + 4 * j0;
     const int pf = A.pf;
+    double *rbw = red + tid, *rbw_alt = red + JG * nb + tid;  // this thread's partial slot
+    const double *rbr = red + (tid < nb ? tid : 0), *rbr_alt = rbr + JG * nb;  // reducer's column
     for (int i = 0; i < np; ++i) {
       double acc = 0.0;
       if (active && pf > 0 && i + pf < np) {
@@ -245,13 +247,22 @@ __global__ void __launch_bounds__(JMAX == 1 ? 448 : 1024, JMAX == 1 ? 4 : 1) k_s
           }
         }
       }
-      double *rb = red + (i & 1) * JG * nb;
-      if (active) rb[tid] = acc;
+      // reduction buffer of this cell: two halves, pointer swapped per cell
+      // (no per-cell address rebuild)
+      if (active) *rbw = acc;
       __syncthreads();
       if (tid < nb) {
         double s = 0.0;
-        for (int q = 0; q < JG; ++q) s += rb[q * nb + tid];
+        for (int q = 0; q < JG; ++q) s += rbr[q * nb];
         *dp = s;
+      }
+      {
+        double *t = rbw;
+        rbw = rbw_alt;
+        rbw_alt = t;
+        const double *u = rbr;
+        rbr = rbr_alt;
+        rbr_alt = u;
       }
       ip += pstep;
       op += pstep;
